@@ -1,0 +1,32 @@
+# Builds the C-ABI executor library in-tree (it travels to the GPU box with
+# the snapshot).  sm_100a only.
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
+PKG := paper_1701_03980_b200
+SRC := $(PKG)/csrc
+OBJ := build/obj
+LIB := $(PKG)/libdyngpu.so
+OBJS := $(OBJ)/executor.o $(OBJ)/kernels.o $(OBJ)/gemm.o
+
+all: $(LIB)
+
+$(OBJ):
+	mkdir -p $(OBJ)
+
+$(OBJ)/executor.o: $(SRC)/executor.cpp $(SRC)/kernels.cuh include/dyngpu.h | $(OBJ)
+	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
+
+$(OBJ)/kernels.o: $(SRC)/kernels.cu $(SRC)/kernels.cuh | $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(OBJ)/gemm.o: $(SRC)/gemm.cu $(SRC)/kernels.cuh | $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart_static -lrt -ldl -lpthread
+
+clean:
+	rm -rf build $(LIB)
+
+.PHONY: all clean

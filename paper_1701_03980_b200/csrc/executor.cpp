@@ -1,0 +1,2056 @@
+// Native executor behind include/dyngpu.h.
+//
+// Replaces the reference's per-node interpreter (pkg/src/dyncore/graph.py:115-164)
+// with a batching planner:
+//   1. rewrite left-deep chains of equal-shape `add` nodes (the loss chain,
+//      bench/tasks.py:419,439,558, and Tree-LSTM cell sums builders.py:255-257)
+//      into one n-ary prefix-sum unit, so the per-step loss terms do not
+//      serialise the graph;
+//   2. schedule units by list scheduling over dependency levels: a signature
+//      group (kind, shapes, shared parameter identity, aux) is launched when one
+//      of its ready members becomes urgent (its ALAP level is reached), and it
+//      then takes every ready member -> recurrent steps batch across layers,
+//      non-recurrent branches (output affine, pnls, masks) batch across all
+//      time steps, tree nodes batch by height;
+//   3. lay every group's outputs out contiguously in the forward arena (same
+//      total bytes as the reference bump allocator, so PoolExhausted and
+//      alloc_count semantics are unchanged) and upload one table blob per call;
+//   4. backward walks the groups in reverse; parameter gradients accumulate in
+//      place (the default sink, graph.py:51-63), weight gradients of every use
+//      of a parameter are aggregated into ONE GEMM (K = all rows), lookup rows
+//      are flushed by an atomic-free sorted segmented scatter-add.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/dyngpu.h"
+#include "kernels.cuh"
+
+namespace dg {
+
+// --------------------------------------------------------------------- errors
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define DG_CUDA_TRY(expr)                                                          \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess) return fail(DG_CUDA, std::string(#expr ": ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+// ------------------------------------------------------------ param registry
+struct Param {
+  int kind = 0;  // 0 dense, 1 lookup
+  int64_t rows = 0, cols = 0;
+  float* val = nullptr;
+  float* grad = nullptr;
+  bool alive = false;
+  std::vector<uint8_t> touched_bits;
+  std::vector<int64_t> touched_list;  // insertion order; sorted on read
+  int64_t size() const { return rows * cols; }
+};
+
+static std::mutex g_param_mu;
+static std::vector<Param> g_params;
+
+static Param* param_at(int64_t h) {
+  if (h < 0 || h >= (int64_t)g_params.size() || !g_params[h].alive) return nullptr;
+  return &g_params[h];
+}
+
+static void touch(Param& p, int64_t id) {
+  if (!p.touched_bits[id]) {
+    p.touched_bits[id] = 1;
+    p.touched_list.push_back(id);
+  }
+}
+
+static std::vector<int64_t> touched_sorted(Param& p) {
+  std::vector<int64_t> v = p.touched_list;
+  std::sort(v.begin(), v.end());
+  return v;
+}
+
+static void touched_clear(Param& p) {
+  for (int64_t id : p.touched_list) p.touched_bits[id] = 0;
+  p.touched_list.clear();
+}
+
+// ------------------------------------------------------------------ staging
+// One table blob per forward/backward call: built on the host, copied with a
+// single H2D into the head of the workspace; kernels read it from there.
+struct Blob {
+  std::vector<uint8_t> host;
+  size_t push_bytes(const void* p, size_t n, size_t align = 16) {
+    size_t off = (host.size() + align - 1) & ~(align - 1);
+    host.resize(off + n);
+    if (n) std::memcpy(host.data() + off, p, n);
+    return off;
+  }
+  template <class T>
+  size_t push(const std::vector<T>& v) {
+    return push_bytes(v.data(), v.size() * sizeof(T));
+  }
+  void clear() { host.clear(); }
+};
+
+struct Pinned {
+  void* ptr = nullptr;
+  size_t cap = 0;
+  cudaEvent_t ev = nullptr;
+  bool pending = false;
+};
+
+// -------------------------------------------------------------------- graph
+struct Node {
+  int kind, n_in, in_off, rank;
+  int dims[4];
+  int batch;
+  int64_t elem;
+  int64_t ai_off, ai_len, af_off, af_len;
+  float* val = nullptr;
+  float* grad = nullptr;
+  int64_t size() const { return elem * batch; }
+};
+
+static inline size_t round64(size_t n) { return (n + 63) & ~size_t(63); }
+
+enum UnitKind { U_NODE = 0, U_CHAIN = 1 };
+
+struct Unit {
+  int type;                 // U_NODE / U_CHAIN
+  std::vector<int> nodes;   // U_NODE: {i}; U_CHAIN: add nodes in chain order
+  std::vector<int> ins;     // external inputs (node indices) in slot order
+  int first() const { return nodes.front(); }
+  int last() const { return nodes.back(); }
+};
+
+struct Group {
+  int kind;                 // node kind, or -1 for chains
+  std::vector<int> units;   // unit ids, ascending
+};
+
+struct Schedule {
+  std::vector<Unit> units;
+  std::vector<int> unit_of;        // node -> unit id (or -1 when not scheduled)
+  std::vector<Group> groups;       // execution order (forward)
+  std::vector<int> input_nodes;    // `input` leaves
+  std::vector<int> lookup_nodes;   // lookup / lookup_batch leaves
+  std::vector<int> param_nodes;
+};
+
+struct AffineUse {  // weight-gradient aggregation (one GEMM per parameter)
+  std::vector<uintptr_t> x_rows;  // device pointers (forward values)
+  std::vector<uintptr_t> g_rows;  // device pointers (grad slots)
+  int64_t n_in = 0, m = 0;
+};
+
+struct dg_graph_impl;
+
+}  // namespace dg
+
+struct dg_graph {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  char* fwd_base = nullptr;
+  size_t fwd_bytes = 0, fwd_cursor = 0;
+  int64_t fwd_alloc_count = 0;
+  char* bwd_base = nullptr;
+  size_t bwd_bytes = 0, bwd_cursor = 0;
+  int64_t bwd_alloc_count = 0;
+  char* work_base = nullptr;
+  size_t work_bytes = 0;
+  std::vector<dg::Node> nodes;
+  std::vector<int32_t> inputs;
+  std::vector<int64_t> aux_i;
+  std::vector<float> aux_f;
+  int watermark = -1;
+  int64_t forward_calls = 0;
+  int64_t launches = 0;
+  int64_t h2d_bytes = 0;
+  int64_t d2h_bytes = 0;
+  int64_t stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  // live profiling: CUDA events around launches of the enabled op classes
+  uint32_t prof_mask = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_pending[16];
+  std::vector<int> prof_pending_cls;
+  double prof_ms[16] = {0};
+  double prof_flops[16] = {0};
+  double prof_bytes[16] = {0};
+  int64_t prof_count[16] = {0};
+  std::vector<cudaEvent_t> event_pool;
+  dg::Pinned pinned[2];
+  int pin_idx = 0;
+  bool has_grads = false;  // any backward in this generation
+};
+
+struct dg_trainer {
+  dg::RuleArgs rule{};
+  int sparse = 1;
+  int64_t t = 0;
+  struct Slot {
+    int64_t handle;
+    float* s0;
+    float* s1;
+  };
+  std::vector<Slot> slots;
+  void* segs_dev = nullptr;  // device TensorSeg table
+  size_t segs_cap = 0;
+  void* ids_dev = nullptr;   // device sorted ids for sparse rows
+  size_t ids_cap = 0;
+  dg::Pinned pinned;
+};
+
+namespace dg {
+
+// ------------------------------------------------------------ pinned upload
+static int pinned_acquire(Pinned& p, size_t n) {
+  if (p.pending) {
+    DG_CUDA_TRY(cudaEventSynchronize(p.ev));
+    p.pending = false;
+  }
+  if (!p.ev) DG_CUDA_TRY(cudaEventCreateWithFlags(&p.ev, cudaEventDisableTiming));
+  if (n > p.cap) {
+    if (p.ptr) DG_CUDA_TRY(cudaFreeHost(p.ptr));
+    size_t cap = std::max<size_t>(n, 1 << 16);
+    cap = cap + cap / 2;
+    DG_CUDA_TRY(cudaHostAlloc(&p.ptr, cap, cudaHostAllocDefault));
+    p.cap = cap;
+  }
+  return DG_OK;
+}
+
+static int upload(dg_graph* g, const Blob& blob, void* dst) {
+  if (blob.host.empty()) return DG_OK;
+  Pinned& p = g->pinned[g->pin_idx];
+  g->pin_idx ^= 1;
+  int rc = pinned_acquire(p, blob.host.size());
+  if (rc) return rc;
+  std::memcpy(p.ptr, blob.host.data(), blob.host.size());
+  DG_CUDA_TRY(cudaMemcpyAsync(dst, p.ptr, blob.host.size(), cudaMemcpyHostToDevice, g->stream));
+  g->h2d_bytes += (int64_t)blob.host.size();
+  DG_CUDA_TRY(cudaEventRecord(p.ev, g->stream));
+  p.pending = true;
+  return DG_OK;
+}
+
+// ----------------------------------------------------------- signatures
+struct SigHash {
+  uint64_t h = 1469598103934665603ull;
+  void add(int64_t v) {
+    uint64_t x = static_cast<uint64_t>(v);
+    for (int i = 0; i < 8; ++i) {
+      h ^= (x & 0xff);
+      h *= 1099511628211ull;
+      x >>= 8;
+    }
+  }
+};
+
+static bool is_leaf(int kind) {
+  return kind == DG_OP_INPUT || kind == DG_OP_PARAMETER || kind == DG_OP_LOOKUP || kind == DG_OP_LOOKUP_BATCH;
+}
+
+static int64_t param_handle_of(const dg_graph* g, int node) {
+  const Node& n = g->nodes[node];
+  if (n.kind != DG_OP_PARAMETER) return -1;
+  return g->aux_i[n.ai_off];
+}
+
+// Signature of a unit: everything that must agree for one batched launch.
+static uint64_t unit_signature(const dg_graph* g, const Unit& u) {
+  SigHash s;
+  const Node& n = g->nodes[u.last()];
+  s.add(u.type);
+  s.add(u.type == U_CHAIN ? -1 : n.kind);
+  s.add(n.rank);
+  for (int d = 0; d < n.rank; ++d) s.add(n.dims[d]);
+  s.add(n.batch);
+  s.add((int64_t)u.nodes.size());
+  s.add((int64_t)u.ins.size());
+  for (size_t k = 0; k < u.ins.size(); ++k) {
+    const Node& in = g->nodes[u.ins[k]];
+    s.add(in.batch);
+    s.add(in.elem);
+    s.add(in.rank);
+    for (int d = 0; d < in.rank; ++d) s.add(in.dims[d]);
+  }
+  switch (n.kind) {
+    case DG_OP_AFFINE: {
+      // W operands must be the same parameter for a shared-weight GEMM; the
+      // bias may be a shared parameter (epilogue) or a per-node value.
+      for (size_t k = 0; k < u.ins.size(); ++k) {
+        const int64_t h = param_handle_of(g, u.ins[k]);
+        if (k == 0 || (k % 2) == 1) s.add(h);
+        if ((k % 2) == 1 && (h < 0 || g->nodes[u.ins[k]].batch != 1)) s.add(1000000 + u.last());  // generic: singleton
+      }
+      break;
+    }
+    case DG_OP_SCALAR_MUL: {
+      float f = g->aux_f[n.af_off];
+      int32_t bits;
+      std::memcpy(&bits, &f, 4);
+      s.add(bits);
+      break;
+    }
+    case DG_OP_PICK_RANGE:
+      s.add(g->aux_i[n.ai_off]);
+      s.add(g->aux_i[n.ai_off + 1]);
+      break;
+    default:
+      break;
+  }
+  return s.h;
+}
+
+// ------------------------------------------------------------- scheduling
+// Builds units (with add-chain rewrite) and the group order for the node set
+// `active` (ascending).  consumers_limit bounds the consumer count scope.
+static void build_schedule(const dg_graph* g, const std::vector<int>& active, int scope_hi, Schedule& S) {
+  const int N = (int)g->nodes.size();
+  S = Schedule();
+  S.unit_of.assign(N, -1);
+  std::vector<char> in_set(N, 0);
+  for (int i : active) in_set[i] = 1;
+
+  // consumer counts over all nodes <= scope_hi (backward correctness needs the
+  // full scope; see header comment)
+  std::vector<int> consumers(N, 0);
+  for (int i = 0; i <= scope_hi && i < N; ++i) {
+    const Node& n = g->nodes[i];
+    for (int k = 0; k < n.n_in; ++k) consumers[g->inputs[n.in_off + k]]++;
+  }
+  auto same_shape = [&](int a, int b) {
+    const Node& x = g->nodes[a];
+    const Node& y = g->nodes[b];
+    if (x.batch != y.batch || x.rank != y.rank) return false;
+    for (int d = 0; d < x.rank; ++d)
+      if (x.dims[d] != y.dims[d]) return false;
+    return true;
+  };
+  auto chainable_add = [&](int i) {
+    const Node& n = g->nodes[i];
+    if (n.kind != DG_OP_ADD) return false;
+    const int a = g->inputs[n.in_off], b = g->inputs[n.in_off + 1];
+    return same_shape(i, a) && same_shape(i, b);
+  };
+
+  // units
+  std::vector<int> chain_next(N, -1);  // add node -> the add that extends it
+  for (int i : active) {
+    if (!chainable_add(i)) continue;
+    const int p = g->inputs[g->nodes[i].in_off];
+    if (p >= 0 && in_set[p] && chainable_add(p) && consumers[p] == 1 && chain_next[p] < 0) chain_next[p] = i;
+  }
+  std::vector<char> has_prev(N, 0);
+  for (int i : active)
+    if (chain_next[i] >= 0) has_prev[chain_next[i]] = 1;
+
+  for (int i : active) {
+    const Node& n = g->nodes[i];
+    if (S.unit_of[i] >= 0) continue;
+    if (n.kind == DG_OP_INPUT) { S.input_nodes.push_back(i); continue; }
+    if (n.kind == DG_OP_PARAMETER) { S.param_nodes.push_back(i); continue; }
+    if (n.kind == DG_OP_LOOKUP || n.kind == DG_OP_LOOKUP_BATCH) { S.lookup_nodes.push_back(i); continue; }
+    Unit u;
+    if (chainable_add(i) && !has_prev[i] && chain_next[i] >= 0) {
+      u.type = U_CHAIN;
+      int c = i;
+      u.ins.push_back(g->inputs[n.in_off]);
+      u.ins.push_back(g->inputs[n.in_off + 1]);
+      u.nodes.push_back(c);
+      while (chain_next[c] >= 0) {
+        c = chain_next[c];
+        u.nodes.push_back(c);
+        u.ins.push_back(g->inputs[g->nodes[c].in_off + 1]);
+      }
+    } else {
+      u.type = U_NODE;
+      u.nodes.push_back(i);
+      for (int k = 0; k < n.n_in; ++k) u.ins.push_back(g->inputs[n.in_off + k]);
+    }
+    const int id = (int)S.units.size();
+    for (int x : u.nodes) S.unit_of[x] = id;
+    S.units.push_back(std::move(u));
+  }
+
+  const int U = (int)S.units.size();
+  if (U == 0) return;
+  // unit dependency graph
+  std::vector<std::vector<int>> succ(U);
+  std::vector<int> indeg(U, 0);
+  for (int u = 0; u < U; ++u) {
+    std::vector<int> preds;
+    for (int x : S.units[u].ins) {
+      const int pu = x >= 0 && x < N ? S.unit_of[x] : -1;
+      if (pu >= 0 && pu != u) preds.push_back(pu);
+    }
+    std::sort(preds.begin(), preds.end());
+    preds.erase(std::unique(preds.begin(), preds.end()), preds.end());
+    indeg[u] = (int)preds.size();
+    for (int p : preds) succ[p].push_back(u);
+  }
+  // units are created in ascending node order and every input precedes its
+  // consumer, so unit ids are already a topological order
+  std::vector<int> height(U, 0);
+  for (int u = U - 1; u >= 0; --u)
+    for (int c : succ[u]) height[u] = std::max(height[u], height[c] + 1);
+  int L = 0;
+  for (int u = 0; u < U; ++u) L = std::max(L, height[u]);
+  std::vector<int> alap(U);
+  for (int u = 0; u < U; ++u) alap[u] = L - height[u];
+  std::vector<uint64_t> sig(U);
+  for (int u = 0; u < U; ++u) sig[u] = unit_signature(g, S.units[u]);
+
+  // list scheduling
+  std::unordered_map<uint64_t, std::vector<int>> ready;
+  std::vector<uint64_t> ready_keys;  // insertion-ordered keys for determinism
+  auto add_ready = [&](int u) {
+    auto it = ready.find(sig[u]);
+    if (it == ready.end()) {
+      ready.emplace(sig[u], std::vector<int>{u});
+      ready_keys.push_back(sig[u]);
+    } else {
+      it->second.push_back(u);
+    }
+  };
+  for (int u = 0; u < U; ++u)
+    if (indeg[u] == 0) add_ready(u);
+  int done = 0, level = 0;
+  std::vector<int> newly;
+  while (done < U) {
+    // urgent signatures at this level
+    std::vector<std::pair<int, uint64_t>> urgent;  // (min unit id, key)
+    int min_alap = 1 << 30;
+    for (uint64_t k : ready_keys) {
+      const auto& v = ready[k];
+      int ma = 1 << 30, mu = 1 << 30;
+      for (int u : v) {
+        ma = std::min(ma, alap[u]);
+        mu = std::min(mu, u);
+      }
+      min_alap = std::min(min_alap, ma);
+      if (ma <= level) urgent.push_back({mu, k});
+    }
+    if (urgent.empty()) {
+      level = std::max(level + 1, min_alap);
+      continue;
+    }
+    std::sort(urgent.begin(), urgent.end());
+    newly.clear();
+    for (auto& uk : urgent) {
+      std::vector<int> members = std::move(ready[uk.second]);
+      ready.erase(uk.second);
+      ready_keys.erase(std::find(ready_keys.begin(), ready_keys.end(), uk.second));
+      std::sort(members.begin(), members.end());
+      Group gr;
+      const Unit& u0 = S.units[members[0]];
+      gr.kind = u0.type == U_CHAIN ? -1 : g->nodes[u0.last()].kind;
+      gr.units = members;
+      for (int u : members) {
+        ++done;
+        for (int c : succ[u])
+          if (--indeg[c] == 0) newly.push_back(c);
+      }
+      S.groups.push_back(std::move(gr));
+    }
+    for (int c : newly) add_ready(c);
+    ++level;
+  }
+}
+
+// ----------------------------------------------------------------- planning
+// A plan = host-built table blob + deferred launch closures that read the
+// blob's device base.
+enum OpClass {
+  C_GEMM_FWD = 0, C_GEMM_DX = 1, C_GEMM_DW = 2, C_PNLS_FWD = 3, C_PNLS_BWD = 4,
+  C_ELEMWISE = 5, C_GATHER = 6, C_SCATTER = 7, C_COLSUM = 8, C_OTHER = 9, C_NCLASS = 10
+};
+
+struct OpMeta {
+  int cls = C_OTHER;
+  double flops = 0, bytes = 0;  // algorithmic work of the launch
+};
+
+struct Plan {
+  Blob blob;
+  std::vector<std::function<int(char*)>> ops;  // arg: device blob base
+  std::vector<OpMeta> meta;
+  size_t scratch_need = 0;
+  void tag(int cls, double flops, double bytes) {
+    meta.resize(ops.size());
+    meta.back() = OpMeta{cls, flops, bytes};
+  }
+};
+
+template <class T>
+static inline T* at(char* base, size_t off) {
+  return reinterpret_cast<T*>(base + off);
+}
+
+static bool all_aligned16(const std::vector<uintptr_t>& v) {
+  for (uintptr_t p : v)
+    if (p & 15) return false;
+  return true;
+}
+
+// pointers helpers
+static inline uintptr_t P(const float* p) { return reinterpret_cast<uintptr_t>(p); }
+
+// rounds: split a group's (node j, slot) targets so that no round writes the
+// same target from two different nodes (same-node duplicates are handled by
+// one thread in the elementwise kernels).  Returns per-round masks.
+static std::vector<std::vector<char>> conflict_rounds(const std::vector<std::vector<int>>& targets,
+                                                      bool same_node_ok) {
+  // targets[j] = target node ids for node j (one per slot)
+  const size_t n = targets.size();
+  std::vector<std::vector<char>> rounds;
+  std::vector<int> round_of(n, -1);
+  std::vector<std::unordered_map<int, int>> owner;  // per round: target -> node j
+  bool any_conflict = false;
+  {
+    std::unordered_map<int, int> seen;
+    for (size_t j = 0; j < n && !any_conflict; ++j) {
+      for (size_t k = 0; k < targets[j].size(); ++k) {
+        int t = targets[j][k];
+        auto it = seen.find(t);
+        if (it != seen.end() && (!same_node_ok || it->second != (int)j)) {
+          any_conflict = true;
+          break;
+        }
+        seen[t] = (int)j;
+      }
+    }
+  }
+  if (!any_conflict) {
+    rounds.push_back(std::vector<char>(n, 1));
+    return rounds;
+  }
+  // node-granular greedy rounds; intra-node duplicates (not same_node_ok) are
+  // split further by the caller through slot masks
+  for (size_t j = 0; j < n; ++j) {
+    int r = 0;
+    for (;; ++r) {
+      if (r == (int)owner.size()) {
+        owner.emplace_back();
+        rounds.push_back(std::vector<char>(n, 0));
+      }
+      bool ok = true;
+      for (int t : targets[j]) {
+        auto it = owner[r].find(t);
+        if (it != owner[r].end() && it->second != (int)j) { ok = false; break; }
+      }
+      if (ok) break;
+    }
+    for (int t : targets[j]) owner[r][t] = (int)j;
+    rounds[r][j] = 1;
+  }
+  return rounds;
+}
+
+}  // namespace dg
+
+using namespace dg;
+
+// =========================================================================
+// C-ABI
+// =========================================================================
+
+extern "C" {
+
+const char* dg_last_error(void) { return g_err.c_str(); }
+int dg_abi_version(void) { return 1; }
+
+int dg_param_register(int kind, int64_t rows, int64_t cols, float* values, float* grad, int64_t* handle) {
+  if (rows < 1 || cols < 1) return fail(DG_BAD_SHAPE, "parameter needs rows >= 1 and cols >= 1");
+  std::lock_guard<std::mutex> lk(g_param_mu);
+  Param p;
+  p.kind = kind;
+  p.rows = rows;
+  p.cols = cols;
+  p.val = values;
+  p.grad = grad;
+  p.alive = true;
+  if (kind == 1) p.touched_bits.assign(rows, 0);
+  g_params.push_back(std::move(p));
+  *handle = (int64_t)g_params.size() - 1;
+  return DG_OK;
+}
+
+int dg_param_rebind(int64_t h, float* values, float* grad) {
+  std::lock_guard<std::mutex> lk(g_param_mu);
+  Param* p = param_at(h);
+  if (!p) return fail(DG_INDEX, "unknown parameter handle");
+  p->val = values;
+  p->grad = grad;
+  return DG_OK;
+}
+
+int dg_param_release(int64_t h) {
+  std::lock_guard<std::mutex> lk(g_param_mu);
+  Param* p = param_at(h);
+  if (!p) return fail(DG_INDEX, "unknown parameter handle");
+  p->alive = false;
+  p->touched_bits.clear();
+  p->touched_list.clear();
+  return DG_OK;
+}
+
+int dg_touched_count(int64_t h, int64_t* n) {
+  Param* p = param_at(h);
+  if (!p) return fail(DG_INDEX, "unknown parameter handle");
+  *n = (int64_t)p->touched_list.size();
+  return DG_OK;
+}
+
+int dg_touched_get(int64_t h, int64_t* ids, int64_t cap) {
+  Param* p = param_at(h);
+  if (!p) return fail(DG_INDEX, "unknown parameter handle");
+  std::vector<int64_t> v = touched_sorted(*p);
+  if ((int64_t)v.size() > cap) return fail(DG_INDEX, "touched buffer too small");
+  std::copy(v.begin(), v.end(), ids);
+  return DG_OK;
+}
+
+int dg_touched_add(int64_t h, const int64_t* ids, int64_t n) {
+  Param* p = param_at(h);
+  if (!p || p->kind != 1) return fail(DG_INDEX, "not a lookup parameter");
+  for (int64_t i = 0; i < n; ++i) {
+    if (ids[i] < 0 || ids[i] >= p->rows) return fail(DG_INDEX, "touched id out of range");
+    touch(*p, ids[i]);
+  }
+  return DG_OK;
+}
+
+int dg_touched_clear(int64_t h) {
+  Param* p = param_at(h);
+  if (!p) return fail(DG_INDEX, "unknown parameter handle");
+  touched_clear(*p);
+  return DG_OK;
+}
+
+// ------------------------------------------------------------------ graph
+
+int dg_graph_create(int device, void* fwd_base, size_t fwd_bytes, void* bwd_base, size_t bwd_bytes, void* work_base,
+                    size_t work_bytes, dg_graph** out) {
+  if (!fwd_base || !bwd_base || !work_base) return fail(DG_CONFIG, "null arena");
+  dg_graph* g = new dg_graph();
+  g->device = device;
+  g->fwd_base = static_cast<char*>(fwd_base);
+  g->fwd_bytes = fwd_bytes;
+  g->bwd_base = static_cast<char*>(bwd_base);
+  g->bwd_bytes = bwd_bytes;
+  g->work_base = static_cast<char*>(work_base);
+  g->work_bytes = work_bytes;
+  *out = g;
+  return DG_OK;
+}
+
+int dg_graph_destroy(dg_graph* g) {
+  if (!g) return DG_OK;
+  for (auto& p : g->pinned) {
+    if (p.pending) cudaEventSynchronize(p.ev);
+    if (p.ptr) cudaFreeHost(p.ptr);
+    if (p.ev) cudaEventDestroy(p.ev);
+  }
+  delete g;
+  return DG_OK;
+}
+
+int dg_graph_set_stream(dg_graph* g, void* stream) {
+  g->stream = static_cast<cudaStream_t>(stream);
+  return DG_OK;
+}
+
+int dg_graph_renew(dg_graph* g) {
+  g->nodes.clear();
+  g->inputs.clear();
+  g->aux_i.clear();
+  g->aux_f.clear();
+  g->watermark = -1;
+  // the reference zeroes the used backward prefix here (arena.py:85-92); the
+  // device backward slots are zeroed when a backward pass allocates them
+  g->fwd_cursor = 0;
+  g->bwd_cursor = 0;
+  g->has_grads = false;
+  return DG_OK;
+}
+
+int dg_graph_append(dg_graph* g, const dg_node* nodes, int32_t n, const int32_t* inputs, int32_t n_inputs,
+                    const int64_t* aux_i, int64_t n_aux_i, const float* aux_f, int64_t n_aux_f) {
+  const int in_base = (int)g->inputs.size();
+  const int64_t ai_base = (int64_t)g->aux_i.size(), af_base = (int64_t)g->aux_f.size();
+  const int first = (int)g->nodes.size();
+  g->inputs.insert(g->inputs.end(), inputs, inputs + n_inputs);
+  g->aux_i.insert(g->aux_i.end(), aux_i, aux_i + n_aux_i);
+  g->aux_f.insert(g->aux_f.end(), aux_f, aux_f + n_aux_f);
+  g->nodes.reserve(g->nodes.size() + n);
+  for (int i = 0; i < n; ++i) {
+    const dg_node& r = nodes[i];
+    Node x;
+    x.kind = r.kind;
+    x.n_in = r.n_in;
+    x.in_off = r.in_off + in_base;
+    x.rank = r.rank;
+    x.elem = 1;
+    for (int d = 0; d < 4; ++d) {
+      x.dims[d] = d < r.rank ? r.dims[d] : 1;
+      if (d < r.rank) x.elem *= r.dims[d];
+    }
+    x.batch = r.batch;
+    x.ai_off = r.aux_i_off + ai_base;
+    x.ai_len = r.aux_i_len;
+    x.af_off = r.aux_f_off + af_base;
+    x.af_len = r.aux_f_len;
+    if (x.kind < 0 || x.kind >= DG_OP_COUNT) return fail(DG_INTERNAL, "bad op kind");
+    for (int k = 0; k < x.n_in; ++k) {
+      const int src = g->inputs[x.in_off + k];
+      if (src < 0 || src >= first + i) return fail(DG_STALE, "input refers to a later or unknown node");
+    }
+    if (x.kind == DG_OP_PARAMETER || x.kind == DG_OP_LOOKUP || x.kind == DG_OP_LOOKUP_BATCH) {
+      Param* p = param_at(g->aux_i[x.ai_off]);
+      if (!p) return fail(DG_INDEX, "node references an unknown parameter");
+      if (x.kind != DG_OP_PARAMETER) {
+        for (int64_t q = 1; q < x.ai_len; ++q) {
+          const int64_t id = g->aux_i[x.ai_off + q];
+          if (id < 0 || id >= p->rows) return fail(DG_INDEX, "lookup row out of range");
+        }
+      }
+    }
+    g->nodes.push_back(x);
+  }
+  return DG_OK;
+}
+
+// ---------------------------------------------------------------- forward
+
+static int launch_plan(dg_graph* g, Plan& plan) {
+  const size_t blob_bytes = (plan.blob.host.size() + 255) & ~size_t(255);
+  if (blob_bytes > g->work_bytes / 2) return fail(DG_CONFIG, "plan tables exceed the workspace");
+  int rc = upload(g, plan.blob, g->work_base);
+  if (rc) return rc;
+  plan.meta.resize(plan.ops.size());
+  for (size_t q = 0; q < plan.ops.size(); ++q) {
+    const OpMeta& mt = plan.meta[q];
+    const bool prof = (g->prof_mask >> mt.cls) & 1u;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (prof) {
+      for (cudaEvent_t* e : {&e0, &e1}) {
+        if (g->event_pool.empty()) {
+          DG_CUDA_TRY(cudaEventCreate(e));
+        } else {
+          *e = g->event_pool.back();
+          g->event_pool.pop_back();
+        }
+      }
+      DG_CUDA_TRY(cudaEventRecord(e0, g->stream));
+    }
+    int n = plan.ops[q](g->work_base);
+    if (n < 0) return fail(DG_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+    g->launches += n;
+    if (prof) {
+      DG_CUDA_TRY(cudaEventRecord(e1, g->stream));
+      g->prof_pending[mt.cls].push_back({e0, e1});
+      g->prof_flops[mt.cls] += mt.flops;
+      g->prof_bytes[mt.cls] += mt.bytes;
+      g->prof_count[mt.cls] += 1;
+    }
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(DG_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  return DG_OK;
+}
+
+// scratch region of the workspace (after the table blob half)
+static inline char* scratch_base(dg_graph* g) { return g->work_base + g->work_bytes / 2; }
+static inline size_t scratch_bytes(dg_graph* g) { return g->work_bytes / 2; }
+
+static int ew_kind_of(int kind) {
+  switch (kind) {
+    case DG_OP_TANH: return EW_TANH;
+    case DG_OP_LOGISTIC: return EW_LOGISTIC;
+    case DG_OP_SCALAR_MUL: return EW_SCALE;
+    case DG_OP_ADD: return EW_ADD;
+    case DG_OP_CMULT: return EW_CMULT;
+    default: return -1;
+  }
+}
+
+// forward launches for one group; node values are already placed
+static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, Plan& plan) {
+  Blob& B = plan.blob;
+  std::vector<int> nodes;
+  for (int u : gr.units) nodes.push_back(S.units[u].last());
+  const int n = (int)nodes.size();
+  const Node& n0 = g->nodes[nodes[0]];
+  const cudaStream_t st = g->stream;
+
+  if (gr.kind == -1) {  // add chain
+    const int len = (int)S.units[gr.units[0]].nodes.size();
+    std::vector<uintptr_t> ins((len + 1) * n), outs(len * n);
+    for (int j = 0; j < n; ++j) {
+      const Unit& u = S.units[gr.units[j]];
+      for (int i = 0; i <= len; ++i) ins[i * n + j] = P(g->nodes[u.ins[i]].val);
+      for (int i = 0; i < len; ++i) outs[i * n + j] = P(g->nodes[u.nodes[i]].val);
+    }
+    const size_t oi = B.push(ins), oo = B.push(outs);
+    ChainArgs a{};
+    a.n = n;
+    a.len = len;
+    a.size = (int)n0.size();
+    plan.ops.push_back([a, oi, oo, st](char* d) mutable {
+      a.ins = at<const float* const>(d, oi);
+      a.outs = at<float* const>(d, oo);
+      return launch_chain_fwd(a, st);
+    });
+    return;
+  }
+
+  auto in_vals = [&](int slot) {
+    std::vector<uintptr_t> v(n);
+    for (int j = 0; j < n; ++j) v[j] = P(g->nodes[g->inputs[g->nodes[nodes[j]].in_off + slot]].val);
+    return v;
+  };
+  std::vector<uintptr_t> outs(n);
+  for (int j = 0; j < n; ++j) outs[j] = P(g->nodes[nodes[j]].val);
+  const Node& in0 = g->nodes[g->inputs[n0.in_off]];
+
+  switch (gr.kind) {
+    case DG_OP_TANH:
+    case DG_OP_LOGISTIC:
+    case DG_OP_SCALAR_MUL:
+    case DG_OP_ADD:
+    case DG_OP_CMULT: {
+      EwArgs a{};
+      a.kind = ew_kind_of(gr.kind);
+      a.n = n;
+      a.elem = (int)n0.elem;
+      a.batch = n0.batch;
+      a.scalar = gr.kind == DG_OP_SCALAR_MUL ? g->aux_f[n0.af_off] : 0.f;
+      a.a_b1 = (in0.batch == 1 && n0.batch > 1);
+      const size_t oa = B.push(in_vals(0));
+      size_t ob = 0;
+      if (n0.n_in > 1) {
+        a.b_b1 = (g->nodes[g->inputs[n0.in_off + 1]].batch == 1 && n0.batch > 1);
+        ob = B.push(in_vals(1));
+      }
+      const size_t oo = B.push(outs);
+      const bool binary = n0.n_in > 1;
+      plan.ops.push_back([a, oa, ob, oo, binary, st](char* d) mutable {
+        a.a = at<const float* const>(d, oa);
+        a.b = binary ? at<const float* const>(d, ob) : nullptr;
+        a.out = at<float* const>(d, oo);
+        return launch_ew_fwd(a, st);
+      });
+      plan.tag(C_ELEMWISE, 0.0, 4.0 * (double)n0.size() * n * (binary ? 3 : 2));
+      return;
+    }
+    case DG_OP_PICK_RANGE: {
+      PickArgs a{};
+      a.n = n;
+      a.batch = n0.batch;
+      a.in_elem = (int)in0.elem;
+      a.lo = (int)g->aux_i[n0.ai_off];
+      a.width = (int)n0.elem;
+      const size_t oi = B.push(in_vals(0)), oo = B.push(outs);
+      plan.ops.push_back([a, oi, oo, st](char* d) mutable {
+        a.in = at<const float* const>(d, oi);
+        a.out = at<float* const>(d, oo);
+        return launch_pick_fwd(a, st);
+      });
+      return;
+    }
+    case DG_OP_CONCATENATE: {
+      ConcatArgs a{};
+      a.n = n;
+      a.batch = n0.batch;
+      a.parts = n0.n_in;
+      a.total = (int)n0.elem;
+      std::vector<int32_t> offs(a.parts + 1, 0);
+      for (int k = 0; k < a.parts; ++k) offs[k + 1] = offs[k] + (int)g->nodes[g->inputs[n0.in_off + k]].elem;
+      std::vector<uintptr_t> ins((size_t)a.parts * n);
+      for (int k = 0; k < a.parts; ++k) {
+        auto v = in_vals(k);
+        std::copy(v.begin(), v.end(), ins.begin() + (size_t)k * n);
+      }
+      const size_t of = B.push(offs), oi = B.push(ins), oo = B.push(outs);
+      plan.ops.push_back([a, of, oi, oo, st](char* d) mutable {
+        a.offs = at<const int>(d, of);
+        a.in = at<const float* const>(d, oi);
+        a.out = at<float* const>(d, oo);
+        return launch_concat_fwd(a, st);
+      });
+      return;
+    }
+    case DG_OP_SUM_BATCHES: {
+      SumBatchesArgs a{};
+      a.n = n;
+      a.batch = in0.batch;
+      a.elem = (int)in0.elem;
+      const size_t oi = B.push(in_vals(0)), oo = B.push(outs);
+      plan.ops.push_back([a, oi, oo, st](char* d) mutable {
+        a.in = at<const float* const>(d, oi);
+        a.out = at<float* const>(d, oo);
+        return launch_sum_batches_fwd(a, st);
+      });
+      return;
+    }
+    case DG_OP_SOFTMAX:
+    case DG_OP_PNLS:
+    case DG_OP_PNLS_BATCH: {
+      RowArgs a{};
+      a.batch = in0.batch;
+      a.rows = n * in0.batch;
+      a.width = (int)in0.elem;
+      const size_t oi = B.push(in_vals(0)), oo = B.push(outs);
+      size_t ol = 0;
+      const bool pnls = gr.kind != DG_OP_SOFTMAX;
+      if (pnls) {
+        std::vector<int32_t> labels;
+        labels.reserve(a.rows);
+        for (int j = 0; j < n; ++j) {
+          const Node& x = g->nodes[nodes[j]];
+          for (int64_t q = 0; q < x.ai_len; ++q) labels.push_back((int32_t)g->aux_i[x.ai_off + q]);
+        }
+        ol = B.push(labels);
+      }
+      plan.ops.push_back([a, oi, oo, ol, pnls, st](char* d) mutable {
+        a.in = at<const float* const>(d, oi);
+        a.out = at<float* const>(d, oo);
+        if (pnls) {
+          a.labels = at<const int>(d, ol);
+          return launch_pnls_fwd(a, st);
+        }
+        return launch_softmax_fwd(a, st);
+      });
+      plan.tag(pnls ? C_PNLS_FWD : C_ELEMWISE, 0.0, (double)a.rows * a.width * 4 * (pnls ? 1 : 2));
+      return;
+    }
+    case DG_OP_MATMUL: {
+      const Node& x = g->nodes[g->inputs[n0.in_off + 1]];
+      MatmulArgs a{};
+      a.n = n;
+      a.batch = n0.batch;
+      a.m = in0.dims[0];
+      a.k = in0.dims[1];
+      a.p = x.rank == 1 ? 1 : x.dims[1];
+      a.a_b1 = in0.batch == 1 && n0.batch > 1;
+      a.x_b1 = x.batch == 1 && n0.batch > 1;
+      const size_t oa = B.push(in_vals(0)), ox = B.push(in_vals(1)), oo = B.push(outs);
+      plan.ops.push_back([a, oa, ox, oo, st](char* d) mutable {
+        a.a = at<const float* const>(d, oa);
+        a.x = at<const float* const>(d, ox);
+        a.out = at<float* const>(d, oo);
+        return launch_matmul_fwd(a, st);
+      });
+      return;
+    }
+    case DG_OP_AFFINE: {
+      const int terms = (n0.n_in - 1) / 2;
+      const int m = (int)n0.elem;
+      const int Bt = n0.batch;
+      bool gemm = terms <= 4;
+      for (int k = 0; k < terms; ++k) {
+        const int w = g->inputs[n0.in_off + 1 + 2 * k];
+        if (g->nodes[w].kind != DG_OP_PARAMETER || g->nodes[w].batch != 1) gemm = false;
+      }
+      const Node& b0 = g->nodes[g->inputs[n0.in_off]];
+      if (gemm) {
+        GemmArgs a{};
+        a.M = n * Bt;
+        a.N = m;
+        a.n_seg = terms;
+        a.a_kmajor = false;
+        a.b_nmajor = false;
+        a.accumulate = false;
+        std::vector<size_t> xoffs(terms);
+        bool a_al = true;
+        for (int k = 0; k < terms; ++k) {
+          const Node& xk0 = g->nodes[g->inputs[n0.in_off + 2 + 2 * k]];
+          const int K = (int)xk0.elem;
+          const bool xb1 = xk0.batch == 1 && Bt > 1;
+          std::vector<uintptr_t> rows((size_t)n * Bt);
+          for (int j = 0; j < n; ++j) {
+            const float* xv = g->nodes[g->inputs[g->nodes[nodes[j]].in_off + 2 + 2 * k]].val;
+            for (int b = 0; b < Bt; ++b) rows[(size_t)j * Bt + b] = P(xv + (xb1 ? 0 : (int64_t)b * K));
+          }
+          a_al = a_al && all_aligned16(rows);
+          xoffs[k] = B.push(rows);
+          a.seg[k].K = K;
+          const float* W = g->nodes[g->inputs[n0.in_off + 1 + 2 * k]].val;
+          a.seg[k].B.base = W;  // column-major m x K == row-major K x m (W^T)
+          a.seg[k].B.ld = m;
+          a.seg[k].B.rows = nullptr;
+        }
+        a.a_rows_aligned = a_al;
+        a.b_rows_aligned = true;
+        std::vector<uintptr_t> crow((size_t)n * Bt);
+        for (int j = 0; j < n; ++j)
+          for (int b = 0; b < Bt; ++b) crow[(size_t)j * Bt + b] = P(g->nodes[nodes[j]].val + (int64_t)b * m);
+        const size_t oc = B.push(crow);
+        size_t obias = 0;
+        const bool bias_param = b0.kind == DG_OP_PARAMETER;
+        // a bias node shared by every group member with batch 1 -> base/ld 0
+        bool shared_bias = true;
+        for (int j = 0; j < n; ++j)
+          if (g->inputs[g->nodes[nodes[j]].in_off] != g->inputs[n0.in_off]) shared_bias = false;
+        if (bias_param && !shared_bias) {
+          // same parameter through different nodes: still the same storage
+          shared_bias = true;
+        }
+        if (shared_bias && b0.batch == 1) {
+          a.bias.base = b0.val;
+          a.bias.ld = 0;
+        } else {
+          const bool bb1 = b0.batch == 1 && Bt > 1;
+          std::vector<uintptr_t> brow((size_t)n * Bt);
+          for (int j = 0; j < n; ++j) {
+            const float* bv = g->nodes[g->inputs[g->nodes[nodes[j]].in_off]].val;
+            for (int b = 0; b < Bt; ++b) brow[(size_t)j * Bt + b] = P(bv + (bb1 ? 0 : (int64_t)b * m));
+          }
+          obias = B.push(brow);
+        }
+        const bool bias_table = !(shared_bias && b0.batch == 1);
+        char* scratch = scratch_base(g);
+        const int64_t scratch_floats = (int64_t)(scratch_bytes(g) / 4);
+        plan.ops.push_back([a, xoffs, oc, obias, bias_table, terms, scratch, scratch_floats, st](char* d) mutable {
+          for (int k = 0; k < terms; ++k) {
+            a.seg[k].A.base = nullptr;
+            a.seg[k].A.ld = 0;
+            a.seg[k].A.rows = at<const float* const>(d, xoffs[k]);
+          }
+          a.C.rows = at<const float* const>(d, oc);
+          if (bias_table) a.bias.rows = at<const float* const>(d, obias);
+          a.work = reinterpret_cast<float*>(scratch);
+          a.work_floats = scratch_floats;
+          return launch_gemm(a, st);
+        });
+        {
+          double kk = 0;
+          for (int k = 0; k < terms; ++k) kk += a.seg[k].K;
+          plan.tag(C_GEMM_FWD, 2.0 * a.M * a.N * kk, 4.0 * ((double)a.M * kk + kk * a.N + (double)a.M * a.N));
+        }
+      } else {
+        AffineGenericArgs a{};
+        a.n = n;
+        a.batch = Bt;
+        a.m = m;
+        a.terms = terms;
+        a.b_b1 = b0.batch == 1 && Bt > 1;
+        std::vector<uintptr_t> w((size_t)terms * n), x((size_t)terms * n);
+        for (int k = 0; k < terms && k < 8; ++k) {
+          const Node& wk = g->nodes[g->inputs[n0.in_off + 1 + 2 * k]];
+          const Node& xk = g->nodes[g->inputs[n0.in_off + 2 + 2 * k]];
+          a.kdim[k] = (int)xk.elem;
+          a.w_b1[k] = wk.batch == 1 && Bt > 1;
+          a.x_b1[k] = xk.batch == 1 && Bt > 1;
+          for (int j = 0; j < n; ++j) {
+            const Node& nj = g->nodes[nodes[j]];
+            w[(size_t)k * n + j] = P(g->nodes[g->inputs[nj.in_off + 1 + 2 * k]].val);
+            x[(size_t)k * n + j] = P(g->nodes[g->inputs[nj.in_off + 2 + 2 * k]].val);
+          }
+        }
+        const size_t ob = B.push(in_vals(0)), ow = B.push(w), ox = B.push(x), oo = B.push(outs);
+        plan.ops.push_back([a, ob, ow, ox, oo, st](char* d) mutable {
+          a.bias = at<const float* const>(d, ob);
+          a.w = at<const float* const>(d, ow);
+          a.x = at<const float* const>(d, ox);
+          a.out = at<float* const>(d, oo);
+          return launch_affine_generic_fwd(a, st);
+        });
+      }
+      return;
+    }
+    default:
+      return;
+  }
+}
+
+static int do_forward(dg_graph* g, int upto) {
+  const int lo = g->watermark + 1;
+  if (upto < lo) return DG_OK;
+  // arena accounting first (arena.py:48-56): same rounded total as the
+  // reference's per-node bump allocation, checked before any launch
+  size_t need = 0;
+  for (int i = lo; i <= upto; ++i) {
+    const Node& x = g->nodes[i];
+    if (x.kind == DG_OP_PARAMETER) continue;
+    const size_t nb = (size_t)x.size() * 4;
+    if (round64(nb) > g->fwd_bytes - g->fwd_cursor - need) {
+      char buf[160];
+      std::snprintf(buf, sizeof buf, "forward|%zu|%zu", nb, g->fwd_bytes - g->fwd_cursor - need);
+      return fail(DG_POOL_EXHAUSTED, buf);
+    }
+    need += round64(nb);
+  }
+
+  std::vector<int> active;
+  active.reserve(upto - lo + 1);
+  for (int i = lo; i <= upto; ++i) active.push_back(i);
+  Schedule S;
+  build_schedule(g, active, upto, S);
+
+  // placement: inputs first (one contiguous block filled by a single copy),
+  // then lookups, then groups in execution order
+  size_t cur = g->fwd_cursor;
+  auto place = [&](int i) {
+    Node& x = g->nodes[i];
+    x.val = reinterpret_cast<float*>(g->fwd_base + cur);
+    cur += round64((size_t)x.size() * 4);
+  };
+  for (int i : S.param_nodes) g->nodes[i].val = param_at(g->aux_i[g->nodes[i].ai_off])->val;
+  const size_t in_begin = cur;
+  for (int i : S.input_nodes) place(i);
+  const size_t in_end = cur;
+  for (int i : S.lookup_nodes) place(i);
+  for (const Group& gr : S.groups)
+    for (int u : gr.units)
+      for (int i : S.units[u].nodes) place(i);
+
+  Plan plan;
+  Blob& B = plan.blob;
+  // input payloads: laid out in the blob exactly like the arena block
+  size_t in_blob = 0;
+  if (in_end > in_begin) {
+    std::vector<uint8_t> block(in_end - in_begin, 0);
+    for (int i : S.input_nodes) {
+      const Node& x = g->nodes[i];
+      const size_t off = reinterpret_cast<char*>(x.val) - (g->fwd_base + in_begin);
+      std::memcpy(block.data() + off, g->aux_f.data() + x.af_off, (size_t)x.size() * 4);
+    }
+    in_blob = B.push_bytes(block.data(), block.size(), 64);
+    char* dst = g->fwd_base + in_begin;
+    const size_t nbytes = in_end - in_begin;
+    cudaStream_t st = g->stream;
+    plan.ops.push_back([dst, in_blob, nbytes, st](char* d) {
+      return cudaMemcpyAsync(dst, d + in_blob, nbytes, cudaMemcpyDeviceToDevice, st) == cudaSuccess ? 0 : -1;
+    });
+  }
+  // lookups: one gather per table
+  {
+    std::unordered_map<int64_t, std::pair<std::vector<int64_t>, std::vector<uintptr_t>>> by_table;
+    std::vector<int64_t> order;
+    for (int i : S.lookup_nodes) {
+      const Node& x = g->nodes[i];
+      const int64_t h = g->aux_i[x.ai_off];
+      auto it = by_table.find(h);
+      if (it == by_table.end()) {
+        order.push_back(h);
+        it = by_table.emplace(h, std::make_pair(std::vector<int64_t>{}, std::vector<uintptr_t>{})).first;
+      }
+      const int64_t dim = x.elem;
+      for (int64_t q = 1; q < x.ai_len; ++q) {
+        it->second.first.push_back(g->aux_i[x.ai_off + q]);
+        it->second.second.push_back(P(x.val + (q - 1) * dim));
+      }
+    }
+    for (int64_t h : order) {
+      Param* p = param_at(h);
+      auto& pr = by_table[h];
+      const size_t oid = B.push(pr.first), orow = B.push(pr.second);
+      const float* table = p->val;
+      const int dim = (int)p->cols;
+      const int rows = (int)pr.first.size();
+      cudaStream_t st = g->stream;
+      plan.ops.push_back([table, dim, oid, orow, rows, st](char* d) {
+        return launch_gather_rows(table, dim, at<const int64_t>(d, oid), at<float* const>(d, orow), rows, st);
+      });
+      plan.tag(C_GATHER, 0.0, 8.0 * rows * dim + 8.0 * rows);
+    }
+  }
+  for (const Group& gr : S.groups) plan_forward_group(g, S, gr, plan);
+
+  int rc = launch_plan(g, plan);
+  if (rc) return rc;
+  g->fwd_cursor = cur;
+  g->fwd_alloc_count += (int64_t)(S.input_nodes.size() + S.lookup_nodes.size());
+  for (const Group& gr : S.groups)
+    for (int u : gr.units) g->fwd_alloc_count += (int64_t)S.units[u].nodes.size();
+  g->forward_calls += upto - lo + 1;
+  g->watermark = upto;
+  g->stats[0] = (int64_t)S.groups.size();
+  g->stats[1] = (int64_t)S.units.size();
+  g->stats[2] = (int64_t)(upto - lo + 1);
+  return DG_OK;
+}
+
+int dg_forward(dg_graph* g, int32_t upto) {
+  if (upto >= (int)g->nodes.size()) return fail(DG_STALE, "node index out of range");
+  return do_forward(g, upto);
+}
+
+// --------------------------------------------------------------- backward
+
+static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr, Plan& plan, float* dummy,
+                                std::unordered_map<int64_t, AffineUse>& wuse,
+                                std::unordered_map<int64_t, std::vector<uintptr_t>>& buse) {
+  Blob& B = plan.blob;
+  const cudaStream_t st = g->stream;
+  std::vector<int> all_nodes;
+  for (int u : gr.units) all_nodes.push_back(S.units[u].last());
+  const Node& n0 = g->nodes[all_nodes[0]];
+
+  // targets per member for conflict rounds
+  std::vector<std::vector<int>> targets(gr.units.size());
+  for (size_t j = 0; j < gr.units.size(); ++j) targets[j] = S.units[gr.units[j]].ins;
+  const bool ew = gr.kind == DG_OP_ADD || gr.kind == DG_OP_CMULT || gr.kind == DG_OP_TANH ||
+                  gr.kind == DG_OP_LOGISTIC || gr.kind == DG_OP_SCALAR_MUL || gr.kind == -1;
+  if (gr.kind == DG_OP_AFFINE) {
+    // dX is conflict-free by construction (temp + segmented reduce); only the
+    // per-node (non-parameter) bias needs rounds
+    for (size_t j = 0; j < targets.size(); ++j) targets[j] = {targets[j][0]};
+  }
+  auto rounds = conflict_rounds(targets, ew);
+  // intra-node duplicate slots in non-elementwise kinds (e.g. concatenate([x,x]))
+  bool intra_dup = false;
+  if (!ew && gr.kind != DG_OP_AFFINE) {
+    for (auto& t : targets) {
+      std::vector<int> s = t;
+      std::sort(s.begin(), s.end());
+      if (std::adjacent_find(s.begin(), s.end()) != s.end()) intra_dup = true;
+    }
+  }
+
+  for (const auto& mask : rounds) {
+    std::vector<int> nodes;
+    std::vector<int> units;
+    for (size_t j = 0; j < all_nodes.size(); ++j)
+      if (mask[j]) { nodes.push_back(all_nodes[j]); units.push_back(gr.units[j]); }
+    const int n = (int)nodes.size();
+    if (n == 0) continue;
+    // slot passes: with intra-node duplicates, one pass per slot with every
+    // other slot's gradient redirected to a dummy buffer
+    const int n_slots = n0.n_in;
+    const int passes = intra_dup ? n_slots : 1;
+    for (int pass = 0; pass < passes; ++pass) {
+      auto gin = [&](int slot) {
+        std::vector<uintptr_t> v(n);
+        for (int j = 0; j < n; ++j) {
+          const bool live = !intra_dup || slot == pass;
+          v[j] = live ? P(g->nodes[g->inputs[g->nodes[nodes[j]].in_off + slot]].grad) : P(dummy);
+        }
+        return v;
+      };
+      auto inval = [&](int slot) {
+        std::vector<uintptr_t> v(n);
+        for (int j = 0; j < n; ++j) v[j] = P(g->nodes[g->inputs[g->nodes[nodes[j]].in_off + slot]].val);
+        return v;
+      };
+      std::vector<uintptr_t> gout(n), oval(n);
+      for (int j = 0; j < n; ++j) {
+        gout[j] = P(g->nodes[nodes[j]].grad);
+        oval[j] = P(g->nodes[nodes[j]].val);
+      }
+      const Node& in0 = g->nodes[g->inputs[n0.in_off]];
+      switch (gr.kind) {
+        case -1: {
+          const int len = (int)S.units[units[0]].nodes.size();
+          std::vector<uintptr_t> gins((size_t)(len + 1) * n), gouts((size_t)len * n);
+          for (int j = 0; j < n; ++j) {
+            const Unit& u = S.units[units[j]];
+            for (int i = 0; i <= len; ++i) gins[(size_t)i * n + j] = P(g->nodes[u.ins[i]].grad);
+            for (int i = 0; i < len; ++i) gouts[(size_t)i * n + j] = P(g->nodes[u.nodes[i]].grad);
+          }
+          ChainArgs a{};
+          a.n = n;
+          a.len = len;
+          a.size = (int)n0.size();
+          const size_t og = B.push(gout), ogi = B.push(gins), ogo = B.push(gouts);
+          plan.ops.push_back([a, og, ogi, ogo, st](char* d) mutable {
+            a.gfinal = at<const float* const>(d, og);
+            a.gins = at<float* const>(d, ogi);
+            a.gouts = at<float* const>(d, ogo);
+            return launch_chain_bwd(a, st);
+          });
+          break;
+        }
+        case DG_OP_TANH:
+        case DG_OP_LOGISTIC:
+        case DG_OP_SCALAR_MUL:
+        case DG_OP_ADD:
+        case DG_OP_CMULT: {
+          EwArgs a{};
+          a.kind = ew_kind_of(gr.kind);
+          a.n = n;
+          a.elem = (int)n0.elem;
+          a.batch = n0.batch;
+          a.scalar = gr.kind == DG_OP_SCALAR_MUL ? g->aux_f[n0.af_off] : 0.f;
+          const bool binary = n0.n_in > 1;
+          a.a_b1 = in0.batch == 1 && n0.batch > 1;
+          a.b_b1 = binary && g->nodes[g->inputs[n0.in_off + 1]].batch == 1 && n0.batch > 1;
+          const size_t oa = B.push(inval(0)), oga = B.push(gin(0));
+          size_t ob = 0, ogb = 0;
+          if (binary) {
+            ob = B.push(inval(1));
+            ogb = B.push(gin(1));
+          }
+          const size_t ogo = B.push(gout), oov = B.push(oval);
+          plan.ops.push_back([a, oa, oga, ob, ogb, ogo, oov, binary, st](char* d) mutable {
+            a.a = at<const float* const>(d, oa);
+            a.ga = at<float* const>(d, oga);
+            if (binary) {
+              a.b = at<const float* const>(d, ob);
+              a.gb = at<float* const>(d, ogb);
+            }
+            a.gout = at<const float* const>(d, ogo);
+            a.oval = at<const float* const>(d, oov);
+            return launch_ew_bwd(a, st);
+          });
+          plan.tag(C_ELEMWISE, 0.0, 4.0 * (double)n0.size() * n * (binary ? 6 : 4));
+          break;
+        }
+        case DG_OP_PICK_RANGE: {
+          PickArgs a{};
+          a.n = n;
+          a.batch = n0.batch;
+          a.in_elem = (int)in0.elem;
+          a.lo = (int)g->aux_i[n0.ai_off];
+          a.width = (int)n0.elem;
+          const size_t og = B.push(gout), oi = B.push(gin(0));
+          plan.ops.push_back([a, og, oi, st](char* d) mutable {
+            a.gout = at<const float* const>(d, og);
+            a.gin = at<float* const>(d, oi);
+            return launch_pick_bwd(a, st);
+          });
+          break;
+        }
+        case DG_OP_CONCATENATE: {
+          ConcatArgs a{};
+          a.n = n;
+          a.batch = n0.batch;
+          a.parts = n0.n_in;
+          a.total = (int)n0.elem;
+          std::vector<int32_t> offs(a.parts + 1, 0);
+          for (int k = 0; k < a.parts; ++k) offs[k + 1] = offs[k] + (int)g->nodes[g->inputs[n0.in_off + k]].elem;
+          std::vector<uintptr_t> gins((size_t)a.parts * n);
+          for (int k = 0; k < a.parts; ++k) {
+            auto v = gin(k);
+            std::copy(v.begin(), v.end(), gins.begin() + (size_t)k * n);
+          }
+          const size_t of = B.push(offs), og = B.push(gout), oi = B.push(gins);
+          plan.ops.push_back([a, of, og, oi, st](char* d) mutable {
+            a.offs = at<const int>(d, of);
+            a.gout = at<const float* const>(d, og);
+            a.gin = at<float* const>(d, oi);
+            return launch_concat_bwd(a, st);
+          });
+          break;
+        }
+        case DG_OP_SUM_BATCHES: {
+          SumBatchesArgs a{};
+          a.n = n;
+          a.batch = in0.batch;
+          a.elem = (int)in0.elem;
+          const size_t og = B.push(gout), oi = B.push(gin(0));
+          plan.ops.push_back([a, og, oi, st](char* d) mutable {
+            a.gout = at<const float* const>(d, og);
+            a.gin = at<float* const>(d, oi);
+            return launch_sum_batches_bwd(a, st);
+          });
+          break;
+        }
+        case DG_OP_SOFTMAX:
+        case DG_OP_PNLS:
+        case DG_OP_PNLS_BATCH: {
+          RowArgs a{};
+          a.batch = in0.batch;
+          a.rows = n * in0.batch;
+          a.width = (int)in0.elem;
+          const bool pnls = gr.kind != DG_OP_SOFTMAX;
+          size_t ol = 0;
+          if (pnls) {
+            std::vector<int32_t> labels;
+            for (int j = 0; j < n; ++j) {
+              const Node& x = g->nodes[nodes[j]];
+              for (int64_t q = 0; q < x.ai_len; ++q) labels.push_back((int32_t)g->aux_i[x.ai_off + q]);
+            }
+            ol = B.push(labels);
+          }
+          const size_t oi = B.push(inval(0)), og = B.push(gout), ov = B.push(oval), ogi = B.push(gin(0));
+          plan.ops.push_back([a, oi, og, ov, ogi, ol, pnls, st](char* d) mutable {
+            a.in = at<const float* const>(d, oi);
+            a.gout = at<const float* const>(d, og);
+            a.oval = at<const float* const>(d, ov);
+            a.gin = at<float* const>(d, ogi);
+            if (pnls) {
+              a.labels = at<const int>(d, ol);
+              return launch_pnls_bwd(a, st);
+            }
+            return launch_softmax_bwd(a, st);
+          });
+          plan.tag(pnls ? C_PNLS_BWD : C_ELEMWISE, 0.0, (double)a.rows * a.width * 4 * 3);
+          break;
+        }
+        case DG_OP_MATMUL: {
+          const Node& x = g->nodes[g->inputs[n0.in_off + 1]];
+          MatmulArgs a{};
+          a.n = n;
+          a.batch = n0.batch;
+          a.m = in0.dims[0];
+          a.k = in0.dims[1];
+          a.p = x.rank == 1 ? 1 : x.dims[1];
+          a.a_b1 = in0.batch == 1 && n0.batch > 1;
+          a.x_b1 = x.batch == 1 && n0.batch > 1;
+          const size_t oa = B.push(inval(0)), ox = B.push(inval(1)), og = B.push(gout);
+          const size_t oga = B.push(gin(0)), ogx = B.push(gin(1));
+          plan.ops.push_back([a, oa, ox, og, oga, ogx, st](char* d) mutable {
+            a.a = at<const float* const>(d, oa);
+            a.x = at<const float* const>(d, ox);
+            a.gout = at<const float* const>(d, og);
+            a.ga = at<float* const>(d, oga);
+            a.gx = at<float* const>(d, ogx);
+            return launch_matmul_bwd(a, st);
+          });
+          break;
+        }
+        case DG_OP_AFFINE: {
+          const int terms = (n0.n_in - 1) / 2;
+          const int m = (int)n0.elem;
+          const int Bt = n0.batch;
+          bool gemm = terms <= 4;
+          for (int k = 0; k < terms; ++k) {
+            const Node& w = g->nodes[g->inputs[n0.in_off + 1 + 2 * k]];
+            if (w.kind != DG_OP_PARAMETER || w.batch != 1) gemm = false;
+          }
+          if (!gemm) {
+            AffineGenericArgs a{};
+            a.n = n;
+            a.batch = Bt;
+            a.m = m;
+            a.terms = terms;
+            a.b_b1 = in0.batch == 1 && Bt > 1;
+            std::vector<uintptr_t> w((size_t)terms * n), x((size_t)terms * n), gw((size_t)terms * n),
+                gx((size_t)terms * n);
+            for (int k = 0; k < terms && k < 8; ++k) {
+              const Node& wk = g->nodes[g->inputs[n0.in_off + 1 + 2 * k]];
+              const Node& xk = g->nodes[g->inputs[n0.in_off + 2 + 2 * k]];
+              a.kdim[k] = (int)xk.elem;
+              a.w_b1[k] = wk.batch == 1 && Bt > 1;
+              a.x_b1[k] = xk.batch == 1 && Bt > 1;
+              auto wv = inval(1 + 2 * k), xv = inval(2 + 2 * k), gwv = gin(1 + 2 * k), gxv = gin(2 + 2 * k);
+              for (int j = 0; j < n; ++j) {
+                w[(size_t)k * n + j] = wv[j];
+                x[(size_t)k * n + j] = xv[j];
+                gw[(size_t)k * n + j] = gwv[j];
+                gx[(size_t)k * n + j] = gxv[j];
+              }
+            }
+            const size_t ob = B.push(inval(0)), ow = B.push(w), ox = B.push(x), og = B.push(gout);
+            const size_t ogb = B.push(gin(0)), ogw = B.push(gw), ogx = B.push(gx);
+            plan.ops.push_back([a, ob, ow, ox, og, ogb, ogw, ogx, st](char* d) mutable {
+              a.bias = at<const float* const>(d, ob);
+              a.w = at<const float* const>(d, ow);
+              a.x = at<const float* const>(d, ox);
+              a.gout = at<const float* const>(d, og);
+              a.gbias = at<float* const>(d, ogb);
+              a.gw = at<float* const>(d, ogw);
+              a.gx = at<float* const>(d, ogx);
+              return launch_affine_generic_bwd(a, st);
+            });
+            break;
+          }
+          // G rows of this round
+          std::vector<uintptr_t> grows((size_t)n * Bt);
+          for (int j = 0; j < n; ++j)
+            for (int b = 0; b < Bt; ++b) grows[(size_t)j * Bt + b] = P(g->nodes[nodes[j]].grad + (int64_t)b * m);
+          // bias
+          const Node& b0 = in0;
+          if (b0.kind == DG_OP_PARAMETER) {
+            auto& v = buse[g->aux_i[b0.ai_off]];
+            v.insert(v.end(), grows.begin(), grows.end());
+          } else {
+            EwArgs a{};
+            a.kind = EW_SCALE;
+            a.scalar = 1.f;
+            a.n = n;
+            a.elem = m;
+            a.batch = Bt;
+            a.a_b1 = b0.batch == 1 && Bt > 1;
+            const size_t og = B.push(gout), oga = B.push(gin(0));
+            plan.ops.push_back([a, og, oga, st](char* d) mutable {
+              a.gout = at<const float* const>(d, og);
+              a.ga = at<float* const>(d, oga);
+              return launch_ew_bwd(a, st);
+            });
+          }
+          const bool g_al = all_aligned16(grows);
+          const size_t og_rows = B.push(grows);
+          for (int k = 0; k < terms; ++k) {
+            const Node& wn = g->nodes[g->inputs[n0.in_off + 1 + 2 * k]];
+            const Node& xk0 = g->nodes[g->inputs[n0.in_off + 2 + 2 * k]];
+            const int K = (int)xk0.elem;
+            const bool xb1 = xk0.batch == 1 && Bt > 1;
+            std::vector<uintptr_t> xrows((size_t)n * Bt), dxrows((size_t)n * Bt);
+            for (int j = 0; j < n; ++j) {
+              const Node& xj = g->nodes[g->inputs[g->nodes[nodes[j]].in_off + 2 + 2 * k]];
+              for (int b = 0; b < Bt; ++b) {
+                xrows[(size_t)j * Bt + b] = P(xj.val + (xb1 ? 0 : (int64_t)b * K));
+                dxrows[(size_t)j * Bt + b] = P(xj.grad + (xb1 ? 0 : (int64_t)b * K));
+              }
+            }
+            // weight-gradient aggregation (one GEMM per parameter later)
+            AffineUse& use = wuse[g->aux_i[wn.ai_off]];
+            use.n_in = K;
+            use.m = m;
+            use.x_rows.insert(use.x_rows.end(), xrows.begin(), xrows.end());
+            use.g_rows.insert(use.g_rows.end(), grows.begin(), grows.end());
+            // dX = G W  (B(k=i, n=t) = W[i + t*m] -> n-major rows of W^T)
+            std::vector<uintptr_t> uniq = dxrows;
+            std::sort(uniq.begin(), uniq.end());
+            const bool dup = std::adjacent_find(uniq.begin(), uniq.end()) != uniq.end();
+            GemmArgs a{};
+            a.M = n * Bt;
+            a.N = K;
+            a.n_seg = 1;
+            a.seg[0].K = m;
+            a.seg[0].B.base = wn.val;
+            a.seg[0].B.ld = m;
+            a.a_kmajor = false;
+            a.b_nmajor = true;
+            a.a_rows_aligned = g_al;
+            a.b_rows_aligned = true;
+            char* scratch = scratch_base(g);
+            const int64_t scratch_floats = (int64_t)(scratch_bytes(g) / 4);
+            if (!dup) {
+              a.accumulate = true;
+              const size_t oc = B.push(dxrows);
+              plan.ops.push_back([a, og_rows, oc, scratch, scratch_floats, st](char* d) mutable {
+                a.seg[0].A.rows = at<const float* const>(d, og_rows);
+                a.C.rows = at<const float* const>(d, oc);
+                a.work = reinterpret_cast<float*>(scratch);
+                a.work_floats = scratch_floats;
+                return launch_gemm(a, st);
+              });
+              plan.tag(C_GEMM_DX, 2.0 * a.M * a.N * m, 4.0 * ((double)a.M * m + (double)m * a.N + 2.0 * a.M * a.N));
+            } else {
+              // temp = G W (dense), then deterministic segmented row reduce
+              const int64_t R = (int64_t)n * Bt;
+              std::vector<int> order(R);
+              std::iota(order.begin(), order.end(), 0);
+              std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return dxrows[x] < dxrows[y]; });
+              std::vector<uintptr_t> tgt;
+              std::vector<int32_t> seg;
+              std::vector<int32_t> perm;  // temp row index per sorted position
+              for (int64_t q = 0; q < R; ++q) {
+                if (q == 0 || dxrows[order[q]] != dxrows[order[q - 1]]) {
+                  tgt.push_back(dxrows[order[q]]);
+                  seg.push_back((int32_t)q);
+                }
+                perm.push_back(order[q]);
+              }
+              seg.push_back((int32_t)R);
+              // temp rows are written in sorted order so segments are contiguous
+              std::vector<uintptr_t> crow(R);
+              // C row for original row r -> temp slot = position of r in order
+              std::vector<int64_t> pos(R);
+              for (int64_t q = 0; q < R; ++q) pos[order[q]] = q;
+              float* temp = reinterpret_cast<float*>(scratch);
+              const int64_t temp_floats = R * K;
+              for (int64_t r = 0; r < R; ++r) crow[r] = P(temp + pos[r] * K);
+              a.accumulate = false;
+              const size_t oc = B.push(crow), ot = B.push(tgt), os = B.push(seg);
+              const int n_t = (int)tgt.size();
+              plan.ops.push_back([a, og_rows, oc, ot, os, n_t, K, temp, temp_floats, scratch, scratch_floats,
+                                  st](char* d) mutable {
+                a.seg[0].A.rows = at<const float* const>(d, og_rows);
+                a.C.rows = at<const float* const>(d, oc);
+                a.work = reinterpret_cast<float*>(scratch) + ((temp_floats + 63) & ~int64_t(63));
+                a.work_floats = scratch_floats - ((temp_floats + 63) & ~int64_t(63));
+                int l = launch_gemm(a, st);
+                l += launch_row_reduce_scatter(at<float* const>(d, ot), at<const int>(d, os), temp, n_t, K, st);
+                return l;
+              });
+              plan.tag(C_GEMM_DX, 2.0 * a.M * a.N * m, 4.0 * ((double)a.M * m + (double)m * a.N + 2.0 * a.M * a.N));
+            }
+          }
+          break;
+        }
+        default:
+          break;
+      }
+    }
+  }
+}
+
+int dg_backward(dg_graph* g, int32_t loss) {
+  if (loss < 0 || loss >= (int)g->nodes.size()) return fail(DG_STALE, "loss index out of range");
+  {
+    const Node& L = g->nodes[loss];
+    if (L.elem != 1 || L.batch != 1) return fail(DG_NON_SCALAR_LOSS, "backward needs a scalar");
+  }
+  int rc = do_forward(g, loss);
+  if (rc) return rc;
+
+  // slots for every node <= loss (graph.py:149-150): identical accounting
+  size_t need = 0;
+  for (int i = 0; i <= loss; ++i) {
+    const size_t nb = (size_t)g->nodes[i].size() * 4;
+    if (round64(nb) > g->bwd_bytes - g->bwd_cursor - need) {
+      char buf[160];
+      std::snprintf(buf, sizeof buf, "backward|%zu|%zu", nb, g->bwd_bytes - g->bwd_cursor - need);
+      return fail(DG_POOL_EXHAUSTED, buf);
+    }
+    need += round64(nb);
+  }
+  // ancestors of the loss
+  std::vector<char> anc(loss + 1, 0);
+  anc[loss] = 1;
+  for (int i = loss; i >= 0; --i) {
+    if (!anc[i]) continue;
+    const Node& x = g->nodes[i];
+    for (int k = 0; k < x.n_in; ++k) anc[g->inputs[x.in_off + k]] = 1;
+  }
+  std::vector<int> active;
+  for (int i = 0; i <= loss; ++i)
+    if (anc[i]) active.push_back(i);
+  Schedule S;
+  build_schedule(g, active, loss, S);
+
+  // placement of grad slots: group order for scheduled units, then the rest
+  const size_t begin = g->bwd_cursor;
+  size_t cur = begin;
+  std::vector<char> placed(loss + 1, 0);
+  auto place = [&](int i) {
+    if (placed[i]) return;
+    placed[i] = 1;
+    Node& x = g->nodes[i];
+    x.grad = reinterpret_cast<float*>(g->bwd_base + cur);
+    cur += round64((size_t)x.size() * 4);
+  };
+  for (const Group& gr : S.groups)
+    for (int u : gr.units)
+      for (int i : S.units[u].nodes) place(i);
+  for (int i = 0; i <= loss; ++i) place(i);
+  // parameter nodes accumulate straight into the parameter's gradient (the
+  // default sink adds the slot to p.gradient, graph.py:54-55)
+  for (int i = 0; i <= loss; ++i)
+    if (g->nodes[i].kind == DG_OP_PARAMETER) g->nodes[i].grad = param_at(g->aux_i[g->nodes[i].ai_off])->grad;
+
+  Plan plan;
+  Blob& B = plan.blob;
+  cudaStream_t st = g->stream;
+  // zero the fresh slots (arena contract, graph.py:146-148) and seed dloss = 1
+  {
+    char* z0 = g->bwd_base + begin;
+    const size_t zn = cur - begin;
+    float* seed = g->nodes[loss].grad;
+    plan.ops.push_back([z0, zn, seed, st](char*) {
+      if (cudaMemsetAsync(z0, 0, zn, st) != cudaSuccess) return -1;
+      return launch_fill(seed, 1, 1.f, st);
+    });
+  }
+  // dummy gradient target for slot-serial passes
+  float* dummy = reinterpret_cast<float*>(scratch_base(g) + scratch_bytes(g) - (16 << 20));
+  std::unordered_map<int64_t, AffineUse> wuse;
+  std::unordered_map<int64_t, std::vector<uintptr_t>> buse;
+  for (int q = (int)S.groups.size() - 1; q >= 0; --q) plan_backward_group(g, S, S.groups[q], plan, dummy, wuse, buse);
+
+  // aggregated weight gradients: dW^T (K x m) += X^T G over every use
+  std::vector<int64_t> wkeys;
+  for (auto& kv : wuse) wkeys.push_back(kv.first);
+  std::sort(wkeys.begin(), wkeys.end());
+  for (int64_t h : wkeys) {
+    AffineUse& use = wuse[h];
+    Param* p = param_at(h);
+    GemmArgs a{};
+    a.M = (int)use.n_in;
+    a.N = (int)use.m;
+    a.n_seg = 1;
+    a.seg[0].K = (int)use.x_rows.size();
+    a.a_kmajor = true;
+    a.b_nmajor = false;
+    a.accumulate = true;
+    a.C.base = p->grad;
+    a.C.ld = use.m;
+    a.a_rows_aligned = all_aligned16(use.x_rows);
+    a.b_rows_aligned = all_aligned16(use.g_rows);
+    const size_t ox = B.push(use.x_rows), og = B.push(use.g_rows);
+    char* scratch = scratch_base(g);
+    const int64_t scratch_floats = (int64_t)(scratch_bytes(g) / 4) - (16 << 18);
+    plan.ops.push_back([a, ox, og, scratch, scratch_floats, st](char* d) mutable {
+      a.seg[0].A.rows = at<const float* const>(d, ox);
+      a.seg[0].B.rows = at<const float* const>(d, og);
+      a.work = reinterpret_cast<float*>(scratch);
+      a.work_floats = scratch_floats;
+      return launch_gemm(a, st);
+    });
+    plan.tag(C_GEMM_DW, 2.0 * a.M * a.N * a.seg[0].K,
+             4.0 * ((double)a.seg[0].K * (a.M + a.N) + 2.0 * a.M * a.N));
+  }
+  std::vector<int64_t> bkeys;
+  for (auto& kv : buse) bkeys.push_back(kv.first);
+  std::sort(bkeys.begin(), bkeys.end());
+  for (int64_t h : bkeys) {
+    auto& rows = buse[h];
+    Param* p = param_at(h);
+    const size_t orow = B.push(rows);
+    float* dst = p->grad;
+    const int width = (int)p->size();
+    const int nr = (int)rows.size();
+    float* work = reinterpret_cast<float*>(scratch_base(g));
+    plan.ops.push_back([dst, orow, nr, width, work, st](char* d) {
+      return launch_colsum_rows(dst, at<const float* const>(d, orow), nr, width, work, st);
+    });
+    plan.tag(C_COLSUM, 0.0, 4.0 * nr * width + 8.0 * width);
+  }
+  // lookup flush: sorted segmented scatter-add per table (graph.py:57-63)
+  {
+    struct Rows {
+      std::vector<std::pair<int64_t, uintptr_t>> v;
+    };
+    std::unordered_map<int64_t, Rows> by_table;
+    std::vector<int64_t> order;
+    for (int i = 0; i <= loss; ++i) {
+      const Node& x = g->nodes[i];
+      if (x.kind != DG_OP_LOOKUP && x.kind != DG_OP_LOOKUP_BATCH) continue;
+      const int64_t h = g->aux_i[x.ai_off];
+      Param* p = param_at(h);
+      // touched includes non-ancestor lookups <= loss (graph.py:155-159)
+      for (int64_t q = 1; q < x.ai_len; ++q) touch(*p, g->aux_i[x.ai_off + q]);
+      if (!anc[i]) continue;
+      auto it = by_table.find(h);
+      if (it == by_table.end()) {
+        order.push_back(h);
+        it = by_table.emplace(h, Rows{}).first;
+      }
+      for (int64_t q = 1; q < x.ai_len; ++q)
+        it->second.v.push_back({g->aux_i[x.ai_off + q], P(x.grad + (q - 1) * x.elem)});
+    }
+    for (int64_t h : order) {
+      auto& v = by_table[h].v;
+      std::stable_sort(v.begin(), v.end(), [](auto& a, auto& b) { return a.first < b.first; });
+      std::vector<int64_t> uids;
+      std::vector<int32_t> seg;
+      std::vector<uintptr_t> src;
+      for (size_t q = 0; q < v.size(); ++q) {
+        if (q == 0 || v[q].first != v[q - 1].first) {
+          uids.push_back(v[q].first);
+          seg.push_back((int32_t)q);
+        }
+        src.push_back(v[q].second);
+      }
+      seg.push_back((int32_t)v.size());
+      Param* p = param_at(h);
+      const size_t ou = B.push(uids), os = B.push(seg), osrc = B.push(src);
+      float* tg = p->grad;
+      const int dim = (int)p->cols;
+      const int nu = (int)uids.size();
+      plan.ops.push_back([tg, dim, ou, os, osrc, nu, st](char* d) {
+        return launch_segment_scatter_add(tg, dim, at<const int64_t>(d, ou), at<const int>(d, os),
+                                          at<const float* const>(d, osrc), nu, 1.f, st);
+      });
+      plan.tag(C_SCATTER, 0.0, 4.0 * dim * ((double)src.size() + 2.0 * nu));
+    }
+  }
+  rc = launch_plan(g, plan);
+  if (rc) return rc;
+  g->bwd_cursor = cur;
+  g->bwd_alloc_count += loss + 1;
+  g->has_grads = true;
+  g->stats[3] = (int64_t)S.groups.size();
+  g->stats[4] = (int64_t)wuse.size();
+  return DG_OK;
+}
+
+int dg_value(dg_graph* g, int32_t node, float* host_dst, int64_t n) {
+  if (node < 0 || node >= (int)g->nodes.size()) return fail(DG_STALE, "node index out of range");
+  int rc = do_forward(g, node);
+  if (rc) return rc;
+  const Node& x = g->nodes[node];
+  if (n != x.size()) return fail(DG_SHAPE, "value buffer size mismatch");
+  DG_CUDA_TRY(cudaMemcpyAsync(host_dst, x.val, (size_t)n * 4, cudaMemcpyDeviceToHost, g->stream));
+  g->d2h_bytes += n * 4;
+  DG_CUDA_TRY(cudaStreamSynchronize(g->stream));
+  return DG_OK;
+}
+
+int dg_gradient(dg_graph* g, int32_t node, float* host_dst, int64_t n) {
+  if (node < 0 || node >= (int)g->nodes.size()) return fail(DG_STALE, "node index out of range");
+  const Node& x = g->nodes[node];
+  if (!g->has_grads || !x.grad) return fail(DG_SHAPE, "no backward pass has populated this node yet");
+  if (n != x.size()) return fail(DG_SHAPE, "gradient buffer size mismatch");
+  DG_CUDA_TRY(cudaMemcpyAsync(host_dst, x.grad, (size_t)n * 4, cudaMemcpyDeviceToHost, g->stream));
+  DG_CUDA_TRY(cudaStreamSynchronize(g->stream));
+  return DG_OK;
+}
+
+int dg_value_ptr(dg_graph* g, int32_t node, float** dev_ptr) {
+  if (node < 0 || node > g->watermark) return fail(DG_STALE, "node not evaluated");
+  *dev_ptr = g->nodes[node].val;
+  return DG_OK;
+}
+
+int dg_graph_counters(dg_graph* g, int64_t* out8) {
+  out8[0] = g->forward_calls;
+  out8[1] = g->fwd_alloc_count;
+  out8[2] = g->bwd_alloc_count;
+  out8[3] = (int64_t)g->fwd_cursor;
+  out8[4] = (int64_t)g->bwd_cursor;
+  out8[5] = g->launches;
+  out8[6] = g->h2d_bytes;
+  out8[7] = g->d2h_bytes;
+  return DG_OK;
+}
+
+int dg_profile_enable(dg_graph* g, uint32_t class_mask) {
+  g->prof_mask = class_mask;
+  return DG_OK;
+}
+
+int dg_profile_read(dg_graph* g, int32_t cls, double* out4) {
+  if (cls < 0 || cls >= C_NCLASS) return fail(DG_INDEX, "profile class out of range");
+  for (int c = 0; c < C_NCLASS; ++c) {
+    for (auto& pr : g->prof_pending[c]) {
+      DG_CUDA_TRY(cudaEventSynchronize(pr.second));
+      float ms = 0.f;
+      DG_CUDA_TRY(cudaEventElapsedTime(&ms, pr.first, pr.second));
+      g->prof_ms[c] += ms;
+      g->event_pool.push_back(pr.first);
+      g->event_pool.push_back(pr.second);
+    }
+    g->prof_pending[c].clear();
+  }
+  out4[0] = g->prof_ms[cls];
+  out4[1] = (double)g->prof_count[cls];
+  out4[2] = g->prof_flops[cls];
+  out4[3] = g->prof_bytes[cls];
+  return DG_OK;
+}
+
+int dg_profile_reset(dg_graph* g) {
+  double tmp[4];
+  dg_profile_read(g, 0, tmp);
+  for (int c = 0; c < 16; ++c) {
+    g->prof_ms[c] = g->prof_flops[c] = g->prof_bytes[c] = 0;
+    g->prof_count[c] = 0;
+  }
+  return DG_OK;
+}
+
+int dg_graph_plan_stats(dg_graph* g, int64_t* out8) {
+  for (int i = 0; i < 8; ++i) out8[i] = g->stats[i];
+  return DG_OK;
+}
+
+// ---------------------------------------------------------------- trainer
+
+int dg_trainer_create(int rule, float lr, float momentum, float adagrad_eps, float beta1, float beta2,
+                      float adam_eps, int sparse, dg_trainer** out) {
+  if (rule < 0 || rule > 3) return fail(DG_BAD_SHAPE, "unknown trainer rule");
+  dg_trainer* t = new dg_trainer();
+  t->rule.rule = rule;
+  t->rule.lr = lr;
+  t->rule.momentum = momentum;
+  t->rule.adagrad_eps = adagrad_eps;
+  t->rule.beta1 = beta1;
+  t->rule.beta2 = beta2;
+  t->rule.adam_eps = adam_eps;
+  t->sparse = sparse;
+  *out = t;
+  return DG_OK;
+}
+
+int dg_trainer_destroy(dg_trainer* t) {
+  if (!t) return DG_OK;
+  if (t->pinned.pending) cudaEventSynchronize(t->pinned.ev);
+  if (t->pinned.ptr) cudaFreeHost(t->pinned.ptr);
+  if (t->pinned.ev) cudaEventDestroy(t->pinned.ev);
+  if (t->segs_dev) cudaFree(t->segs_dev);
+  if (t->ids_dev) cudaFree(t->ids_dev);
+  delete t;
+  return DG_OK;
+}
+
+int dg_trainer_set(dg_trainer* t, float lr, int sparse) {
+  t->rule.lr = lr;
+  t->sparse = sparse;
+  return DG_OK;
+}
+
+int dg_trainer_attach(dg_trainer* t, int64_t handle, float* s0, float* s1) {
+  for (auto& s : t->slots)
+    if (s.handle == handle) {
+      s.s0 = s0;
+      s.s1 = s1;
+      return DG_OK;
+    }
+  t->slots.push_back({handle, s0, s1});
+  return DG_OK;
+}
+
+int dg_trainer_step_count(dg_trainer* t, int64_t* step) {
+  *step = t->t;
+  return DG_OK;
+}
+int dg_trainer_set_step(dg_trainer* t, int64_t step) {
+  t->t = step;
+  return DG_OK;
+}
+
+int dg_trainer_update(dg_trainer* t, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  RuleArgs r = t->rule;
+  if (r.rule == 3) {
+    t->t += 1;
+    // python floats: 1 - beta**t in double, then used as fp32 divisors (trainers.py:80-81)
+    r.bc1 = (float)(1.0 - std::pow((double)t->rule.beta1, (double)t->t));
+    r.bc2 = (float)(1.0 - std::pow((double)t->rule.beta2, (double)t->t));
+    // (1 - beta) as python computes it in double, then fp32
+    r.beta1 = t->rule.beta1;
+    r.beta2 = t->rule.beta2;
+  }
+  // dense segments (+ lookups when not sparse), one multi-tensor launch
+  std::vector<TensorSeg> segs;
+  struct RowJob {
+    Param* p;
+    float* s0;
+    float* s1;
+    std::vector<int64_t> ids;
+  };
+  std::vector<RowJob> rows;
+  int64_t blocks = 0;
+  const int chunk = update_chunk();
+  for (auto& s : t->slots) {
+    Param* p = param_at(s.handle);
+    if (!p) return fail(DG_INDEX, "trainer references a released parameter");
+    if (p->kind == 0 || !t->sparse) {
+      segs.push_back({p->val, p->grad, s.s0, s.s1, p->size()});
+      blocks += (p->size() + chunk - 1) / chunk;
+    } else if (!p->touched_list.empty()) {
+      rows.push_back({p, s.s0, s.s1, touched_sorted(*p)});
+    }
+  }
+  // host staging for the segment table and the sorted row ids
+  size_t ids_total = 0;
+  for (auto& j : rows) ids_total += j.ids.size();
+  const size_t seg_bytes = segs.size() * sizeof(TensorSeg);
+  const size_t total = seg_bytes + ids_total * 8 + 64;
+  int rc = pinned_acquire(t->pinned, total);
+  if (rc) return rc;
+  if (t->segs_cap < seg_bytes + 1) {
+    if (t->segs_dev) DG_CUDA_TRY(cudaFree(t->segs_dev));
+    t->segs_cap = std::max<size_t>(seg_bytes * 2, 4096);
+    DG_CUDA_TRY(cudaMalloc(&t->segs_dev, t->segs_cap));
+  }
+  if (t->ids_cap < ids_total * 8 + 8) {
+    if (t->ids_dev) DG_CUDA_TRY(cudaFree(t->ids_dev));
+    t->ids_cap = std::max<size_t>(ids_total * 16, 1 << 16);
+    DG_CUDA_TRY(cudaMalloc(&t->ids_dev, t->ids_cap));
+  }
+  char* hp = static_cast<char*>(t->pinned.ptr);
+  std::memcpy(hp, segs.data(), seg_bytes);
+  size_t off = 0;
+  for (auto& j : rows) {
+    std::memcpy(hp + seg_bytes + off * 8, j.ids.data(), j.ids.size() * 8);
+    off += j.ids.size();
+  }
+  if (seg_bytes) DG_CUDA_TRY(cudaMemcpyAsync(t->segs_dev, hp, seg_bytes, cudaMemcpyHostToDevice, st));
+  if (ids_total)
+    DG_CUDA_TRY(cudaMemcpyAsync(t->ids_dev, hp + seg_bytes, ids_total * 8, cudaMemcpyHostToDevice, st));
+  DG_CUDA_TRY(cudaEventRecord(t->pinned.ev, st));
+  t->pinned.pending = true;
+  launch_update_dense(r, static_cast<const TensorSeg*>(t->segs_dev), (int)segs.size(), blocks, st);
+  off = 0;
+  for (auto& j : rows) {
+    launch_update_rows(r, j.p->val, j.p->grad, j.s0, j.s1, (int)j.p->cols,
+                       static_cast<const int64_t*>(t->ids_dev) + off, (int)j.ids.size(), st);
+    off += j.ids.size();
+  }
+  // zero_gradients (params.py:114-119): dense grads were zeroed by the update
+  // pass; sparse tables only ever hold gradient on touched rows, which the
+  // row pass zeroed.  Clear touched sets.
+  for (auto& s : t->slots) {
+    Param* p = param_at(s.handle);
+    touched_clear(*p);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(DG_CUDA, std::string("update launch: ") + cudaGetErrorString(e));
+  return DG_OK;
+}
+
+// --------------------------------------------------------------- DP helpers
+
+int dg_lookup_pack(int64_t handle, int64_t* ids_dev, float* rows_dev, int64_t cap, int64_t* n, void* stream) {
+  Param* p = param_at(handle);
+  if (!p || p->kind != 1) return fail(DG_INDEX, "not a lookup parameter");
+  std::vector<int64_t> ids = touched_sorted(*p);
+  *n = (int64_t)ids.size();
+  if ((int64_t)ids.size() > cap) return fail(DG_INDEX, "pack capacity too small");
+  if (ids.empty()) return DG_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DG_CUDA_TRY(cudaMemcpyAsync(ids_dev, ids.data(), ids.size() * 8, cudaMemcpyHostToDevice, st));
+  launch_pack_rows(p->grad, (int)p->cols, ids_dev, rows_dev, (int)ids.size(), st);
+  DG_CUDA_TRY(cudaStreamSynchronize(st));  // ids vector is pageable host memory
+  return DG_OK;
+}
+
+int dg_lookup_merge(int64_t handle, const int64_t* ids_host, const float* rows_dev, int64_t n, float scale,
+                    void* stream) {
+  // table_grad[ids] = scale * sum of gathered rows per id (ranks' rows arrive
+  // in rank order; the stable sort keeps that order inside a segment)
+  Param* p = param_at(handle);
+  if (!p || p->kind != 1) return fail(DG_INDEX, "not a lookup parameter");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::vector<int64_t> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return ids_host[a] < ids_host[b]; });
+  std::vector<int64_t> uids;
+  std::vector<int32_t> seg;
+  std::vector<uintptr_t> src;
+  for (int64_t q = 0; q < n; ++q) {
+    const int64_t id = ids_host[order[q]];
+    if (id < 0 || id >= p->rows) return fail(DG_INDEX, "merge id out of range");
+    if (q == 0 || id != ids_host[order[q - 1]]) {
+      uids.push_back(id);
+      seg.push_back((int32_t)q);
+    }
+    src.push_back(P(rows_dev + order[q] * p->cols));
+  }
+  seg.push_back((int32_t)n);
+  // zero the rows that will be overwritten, then add the merged sums
+  size_t bytes = uids.size() * 8 + seg.size() * 4 + src.size() * 8 + 64;
+  void* dbuf = nullptr;
+  DG_CUDA_TRY(cudaMallocAsync(&dbuf, bytes, st));
+  char* d = static_cast<char*>(dbuf);
+  std::vector<uint8_t> host(bytes, 0);
+  size_t o_u = 0, o_s = (uids.size() * 8 + 15) & ~size_t(15);
+  size_t o_src = (o_s + seg.size() * 4 + 15) & ~size_t(15);
+  if (o_src + src.size() * 8 > bytes) return fail(DG_INTERNAL, "merge staging");
+  std::memcpy(host.data() + o_u, uids.data(), uids.size() * 8);
+  std::memcpy(host.data() + o_s, seg.data(), seg.size() * 4);
+  std::memcpy(host.data() + o_src, src.data(), src.size() * 8);
+  DG_CUDA_TRY(cudaMemcpyAsync(d, host.data(), bytes, cudaMemcpyHostToDevice, st));
+  // rows of this table's gradient that are in the merged set are replaced:
+  // scale them to zero first (the local contribution is part of the gather)
+  launch_update_rows(RuleArgs{0, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 1.f, 1.f}, p->val, p->grad, nullptr, nullptr,
+                     (int)p->cols, reinterpret_cast<const int64_t*>(d + o_u), (int)uids.size(), st);
+  launch_segment_scatter_add(p->grad, (int)p->cols, reinterpret_cast<const int64_t*>(d + o_u),
+                             reinterpret_cast<const int*>(d + o_s), reinterpret_cast<const float* const*>(d + o_src),
+                             (int)uids.size(), scale, st);
+  DG_CUDA_TRY(cudaStreamSynchronize(st));
+  DG_CUDA_TRY(cudaFreeAsync(dbuf, st));
+  for (int64_t id : uids) touch(*p, id);
+  return DG_OK;
+}
+
+int dg_scale(float* y, int64_t n, float alpha, void* stream) {
+  launch_scale(y, n, alpha, static_cast<cudaStream_t>(stream));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(DG_CUDA, cudaGetErrorString(e));
+  return DG_OK;
+}
+
+}  // extern "C"

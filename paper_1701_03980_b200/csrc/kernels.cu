@@ -1,0 +1,755 @@
+// Group kernels of the executor: elementwise, structural, row-wise (softmax /
+// pickneglogsoftmax), embedding gather + sorted segmented scatter-add, generic
+// matmul/affine fallbacks, and the trainer rules.  sm_100a, fp32.
+//
+// Semantics restate pkg/src/dyncore/ops.py (forward overwrites, backward
+// accumulates into zero-initialised slots) and trainers.py:63-83.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace dg {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ float sigmoidf_ref(float x) {
+  // ops.py:78-83: clip to +-60 before exp
+  x = fminf(fmaxf(x, -60.f), 60.f);
+  return 1.f / (1.f + expf(-x));
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// ------------------------------------------------------------------ elementwise
+
+__global__ void ew_fwd_kernel(EwArgs a) {
+  const int64_t size = static_cast<int64_t>(a.elem) * a.batch;
+  const int64_t total = size * a.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(t / size);
+    const int64_t r = t - (int64_t)j * size;
+    const int64_t e = r % a.elem;
+    const float x = a.a[j][a.a_b1 ? e : r];
+    float y;
+    switch (a.kind) {
+      case EW_TANH: y = tanhf(x); break;
+      case EW_LOGISTIC: y = sigmoidf_ref(x); break;
+      case EW_SCALE: y = x * a.scalar; break;
+      case EW_ADD: y = x + a.b[j][a.b_b1 ? e : r]; break;
+      default: y = x * a.b[j][a.b_b1 ? e : r]; break;
+    }
+    a.out[j][r] = y;
+  }
+}
+
+// no-broadcast backward: one thread per output element
+__global__ void ew_bwd_flat_kernel(EwArgs a) {
+  const int64_t size = static_cast<int64_t>(a.elem) * a.batch;
+  const int64_t total = size * a.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(t / size);
+    const int64_t r = t - (int64_t)j * size;
+    const float g = a.gout[j][r];
+    switch (a.kind) {
+      case EW_TANH: {
+        const float y = a.oval[j][r];
+        a.ga[j][r] += (1.f - y * y) * g;
+        break;
+      }
+      case EW_LOGISTIC: {
+        const float y = a.oval[j][r];
+        a.ga[j][r] += y * (1.f - y) * g;
+        break;
+      }
+      case EW_SCALE: a.ga[j][r] += a.scalar * g; break;
+      case EW_ADD:
+        a.ga[j][r] += g;
+        a.gb[j][r] += g;
+        break;
+      default: {
+        const float av = a.a[j][r], bv = a.b[j][r];
+        a.ga[j][r] += g * bv;
+        a.gb[j][r] += g * av;
+        break;
+      }
+    }
+  }
+}
+
+// broadcast backward (binary ops): one thread per (node, element) loops over
+// the batch so batch-1 operands receive the batch sum (ops.py:69-75)
+__global__ void ew_bwd_bcast_kernel(EwArgs a) {
+  const int64_t total = static_cast<int64_t>(a.elem) * a.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(t / a.elem);
+    const int e = static_cast<int>(t - (int64_t)j * a.elem);
+    float acc_a = 0.f, acc_b = 0.f;
+    for (int b = 0; b < a.batch; ++b) {
+      const int64_t r = (int64_t)b * a.elem + e;
+      const float g = a.gout[j][r];
+      float ca, cb = 0.f;
+      if (a.kind == EW_SCALE) {
+        ca = a.scalar * g;
+      } else if (a.kind == EW_ADD) {
+        ca = g;
+        cb = g;
+      } else {
+        ca = g * a.b[j][a.b_b1 ? e : r];
+        cb = g * a.a[j][a.a_b1 ? e : r];
+      }
+      if (a.a_b1) acc_a += ca; else a.ga[j][r] += ca;
+      if (a.kind != EW_SCALE) {
+        if (a.b_b1) acc_b += cb; else a.gb[j][r] += cb;
+      }
+    }
+    if (a.a_b1) a.ga[j][e] += acc_a;
+    if (a.b_b1 && a.kind != EW_SCALE) a.gb[j][e] += acc_b;
+  }
+}
+
+__global__ void chain_fwd_kernel(ChainArgs a) {
+  const int64_t total = (int64_t)a.size * a.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(t / a.size);
+    const int64_t e = t - (int64_t)j * a.size;
+    float s = a.ins[j][e] + a.ins[a.n + j][e];
+    a.outs[j][e] = s;
+    for (int i = 2; i <= a.len; ++i) {
+      s = s + a.ins[(int64_t)i * a.n + j][e];
+      a.outs[(int64_t)(i - 1) * a.n + j][e] = s;
+    }
+  }
+}
+
+__global__ void chain_bwd_kernel(ChainArgs a) {
+  const int64_t total = (int64_t)a.size * a.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(t / a.size);
+    const int64_t e = t - (int64_t)j * a.size;
+    const float g = a.gfinal[j][e];
+    for (int i = 0; i + 1 < a.len; ++i) a.gouts[(int64_t)i * a.n + j][e] += g;
+    for (int i = 0; i <= a.len; ++i) a.gins[(int64_t)i * a.n + j][e] += g;
+  }
+}
+
+// ------------------------------------------------------------------ structural
+
+__global__ void pick_fwd_kernel(PickArgs a) {
+  const int64_t per = (int64_t)a.batch * a.width;
+  const int64_t total = per * a.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(t / per);
+    const int64_t r = t - (int64_t)j * per;
+    const int64_t b = r / a.width, e = r - b * a.width;
+    a.out[j][r] = a.in[j][b * a.in_elem + a.lo + e];
+  }
+}
+
+__global__ void pick_bwd_kernel(PickArgs a) {
+  const int64_t per = (int64_t)a.batch * a.width;
+  const int64_t total = per * a.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(t / per);
+    const int64_t r = t - (int64_t)j * per;
+    const int64_t b = r / a.width, e = r - b * a.width;
+    a.gin[j][b * a.in_elem + a.lo + e] += a.gout[j][r];
+  }
+}
+
+__device__ __forceinline__ int find_part(const int* offs, int parts, int col) {
+  int k = 0;
+  while (k + 1 < parts && col >= offs[k + 1]) ++k;
+  return k;
+}
+
+__global__ void concat_fwd_kernel(ConcatArgs a) {
+  const int64_t per = (int64_t)a.batch * a.total;
+  const int64_t all = per * a.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < all; t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(t / per);
+    const int64_t r = t - (int64_t)j * per;
+    const int b = static_cast<int>(r / a.total), col = static_cast<int>(r - (int64_t)b * a.total);
+    const int k = find_part(a.offs, a.parts, col);
+    const int w = a.offs[k + 1] - a.offs[k];
+    a.out[j][r] = a.in[(int64_t)k * a.n + j][(int64_t)b * w + (col - a.offs[k])];
+  }
+}
+
+__global__ void concat_bwd_kernel(ConcatArgs a) {
+  const int64_t per = (int64_t)a.batch * a.total;
+  const int64_t all = per * a.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < all; t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(t / per);
+    const int64_t r = t - (int64_t)j * per;
+    const int b = static_cast<int>(r / a.total), col = static_cast<int>(r - (int64_t)b * a.total);
+    const int k = find_part(a.offs, a.parts, col);
+    const int w = a.offs[k + 1] - a.offs[k];
+    a.gin[(int64_t)k * a.n + j][(int64_t)b * w + (col - a.offs[k])] += a.gout[j][r];
+  }
+}
+
+__global__ void sum_batches_fwd_kernel(SumBatchesArgs a) {
+  const int64_t total = (int64_t)a.elem * a.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(t / a.elem);
+    const int e = static_cast<int>(t - (int64_t)j * a.elem);
+    float s = 0.f;
+    for (int b = 0; b < a.batch; ++b) s += a.in[j][(int64_t)b * a.elem + e];
+    a.out[j][e] = s;
+  }
+}
+
+__global__ void sum_batches_bwd_kernel(SumBatchesArgs a) {
+  const int64_t per = (int64_t)a.batch * a.elem;
+  const int64_t total = per * a.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(t / per);
+    const int64_t r = t - (int64_t)j * per;
+    a.gin[j][r] += a.gout[j][r % a.elem];
+  }
+}
+
+// ------------------------------------------------------------------ row-wise
+// One warp per row for narrow rows, one 256-thread block per row otherwise.
+
+template <bool kBlock>
+__device__ __forceinline__ float row_reduce_max(float v, float* sh) {
+  v = warp_max(v);
+  if (!kBlock) return v;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  float r = (threadIdx.x < (blockDim.x >> 5)) ? sh[threadIdx.x] : -INFINITY;
+  if (w == 0) {
+    r = warp_max(r);
+    if (lane == 0) sh[0] = r;
+  }
+  __syncthreads();
+  return sh[0];
+}
+
+template <bool kBlock>
+__device__ __forceinline__ float row_reduce_sum(float v, float* sh) {
+  v = warp_sum(v);
+  if (!kBlock) return v;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  float r = (threadIdx.x < (blockDim.x >> 5)) ? sh[threadIdx.x] : 0.f;
+  if (w == 0) {
+    r = warp_sum(r);
+    if (lane == 0) sh[0] = r;
+  }
+  __syncthreads();
+  return sh[0];
+}
+
+// op: 0 softmax fwd, 1 softmax bwd, 2 pnls fwd, 3 pnls bwd
+template <int kOp, bool kBlock>
+__global__ void row_kernel(RowArgs a) {
+  __shared__ float sh[32];
+  const int row = kBlock ? blockIdx.x : (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+  if (row >= a.rows) return;
+  const int stride = kBlock ? blockDim.x : 32;
+  const int tid = kBlock ? threadIdx.x : (threadIdx.x & 31);
+  const int j = row / a.batch, b = row - j * a.batch;
+  const int64_t off = (int64_t)b * a.width;
+  if (kOp == 1) {  // softmax backward: gin += y * (g - <g, y>)   (ops.py:240-247)
+    const float* y = a.oval[j] + off;
+    const float* g = a.gout[j] + off;
+    float d = 0.f;
+    for (int c = tid; c < a.width; c += stride) d += g[c] * y[c];
+    d = row_reduce_sum<kBlock>(d, sh);
+    float* gi = a.gin[j] + off;
+    for (int c = tid; c < a.width; c += stride) gi[c] += y[c] * (g[c] - d);
+    return;
+  }
+  const float* x = a.in[j] + off;
+  float m = -INFINITY;
+  for (int c = tid; c < a.width; c += stride) m = fmaxf(m, x[c]);
+  m = row_reduce_max<kBlock>(m, sh);
+  float s = 0.f;
+  for (int c = tid; c < a.width; c += stride) s += expf(x[c] - m);
+  s = row_reduce_sum<kBlock>(s, sh);
+  if (kOp == 0) {  // softmax forward (ops.py:231-237)
+    float* o = a.out[j] + off;
+    for (int c = tid; c < a.width; c += stride) o[c] = expf(x[c] - m) / s;
+  } else if (kOp == 2) {  // pnls forward: max + log sum exp(x - max) - x[label] (ops.py:470-473)
+    if (tid == 0) a.out[j][b] = m + logf(s) - x[a.labels[row]];
+  } else {  // pnls backward: gin += g * (softmax - onehot) (ops.py:476-479, 503-508)
+    const float g = a.gout[j][b];
+    const int lab = a.labels[row];
+    float* gi = a.gin[j] + off;
+    for (int c = tid; c < a.width; c += stride) {
+      float p = expf(x[c] - m) / s;
+      if (c == lab) p -= 1.f;
+      gi[c] += g * p;
+    }
+  }
+}
+
+template <int kOp>
+int launch_rows(const RowArgs& a, cudaStream_t s) {
+  if (a.rows <= 0) return 0;
+  if (a.width > 512) {
+    row_kernel<kOp, true><<<a.rows, 256, 0, s>>>(a);
+  } else {
+    const int rows_per_block = 8;
+    row_kernel<kOp, false><<<(a.rows + rows_per_block - 1) / rows_per_block, 32 * rows_per_block, 0, s>>>(a);
+  }
+  return 1;
+}
+
+// ------------------------------------------------------------- lookup tables
+
+__global__ void gather_rows_kernel(const float* __restrict__ table, int dim, const int64_t* __restrict__ ids,
+                                   float* const* out_rows, int rows) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const float* src = table + ids[w] * (int64_t)dim;
+  float* dst = out_rows[w];
+  const bool vec = ((dim & 3) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+  if (vec) {
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    for (int c = lane; c < (dim >> 2); c += 32) d4[c] = __ldg(s4 + c);
+  } else {
+    for (int c = lane; c < dim; c += 32) dst[c] = src[c];
+  }
+}
+
+__global__ void segment_scatter_add_kernel(float* __restrict__ table_grad, int dim, const int64_t* __restrict__ ids,
+                                           const int* __restrict__ seg, const float* const* src_rows, int n_unique,
+                                           float scale) {
+  const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (u >= n_unique) return;
+  const int lane = threadIdx.x & 31;
+  float* dst = table_grad + ids[u] * (int64_t)dim;
+  const int k0 = seg[u], k1 = seg[u + 1];
+  for (int c = lane; c < dim; c += 32) {
+    float acc = 0.f;
+    for (int k = k0; k < k1; ++k) acc += src_rows[k][c];  // fixed (sorted) order: deterministic
+    dst[c] += scale * acc;
+  }
+}
+
+__global__ void pack_rows_kernel(const float* __restrict__ table, int dim, const int64_t* __restrict__ ids,
+                                 float* __restrict__ out, int n) {
+  const int64_t total = (int64_t)n * dim;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = t / dim, c = t - u * dim;
+    out[t] = table[ids[u] * dim + c];
+  }
+}
+
+// ------------------------------------------------------------------ generic
+
+// matmul per batch element, column-major: out(i,c) = sum_t A(i,t) X(t,c)
+__global__ void matmul_fwd_kernel(MatmulArgs a) {
+  const int64_t osz = (int64_t)a.m * a.p;
+  const int64_t total = osz * a.batch * a.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t jb = t / osz;
+    const int64_t o = t - jb * osz;
+    const int j = static_cast<int>(jb / a.batch), b = static_cast<int>(jb - (int64_t)j * a.batch);
+    const int i = static_cast<int>(o % a.m), c = static_cast<int>(o / a.m);
+    const float* A = a.a[j] + (a.a_b1 ? 0 : (int64_t)b * a.m * a.k);
+    const float* X = a.x[j] + (a.x_b1 ? 0 : (int64_t)b * a.k * a.p);
+    float s = 0.f;
+    for (int q = 0; q < a.k; ++q) s += A[i + (int64_t)q * a.m] * X[q + (int64_t)c * a.k];
+    a.out[j][(int64_t)b * osz + o] = s;
+  }
+}
+
+// gA(i,q) += sum_b sum_c g(i,c) X(q,c);  one thread per (node, A-batch, element)
+__global__ void matmul_bwd_a_kernel(MatmulArgs a) {
+  const int ab = a.a_b1 ? 1 : a.batch;
+  const int64_t asz = (int64_t)a.m * a.k;
+  const int64_t total = asz * ab * a.n;
+  const int64_t osz = (int64_t)a.m * a.p;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t jb = t / asz;
+    const int64_t o = t - jb * asz;
+    const int j = static_cast<int>(jb / ab), bb = static_cast<int>(jb - (int64_t)j * ab);
+    const int i = static_cast<int>(o % a.m), q = static_cast<int>(o / a.m);
+    float s = 0.f;
+    const int b0 = a.a_b1 ? 0 : bb, b1 = a.a_b1 ? a.batch : bb + 1;
+    for (int b = b0; b < b1; ++b) {
+      const float* X = a.x[j] + (a.x_b1 ? 0 : (int64_t)b * a.k * a.p);
+      const float* G = a.gout[j] + (int64_t)b * osz;
+      for (int c = 0; c < a.p; ++c) s += G[i + (int64_t)c * a.m] * X[q + (int64_t)c * a.k];
+    }
+    a.ga[j][(int64_t)bb * asz + o] += s;
+  }
+}
+
+// gX(q,c) += sum_b sum_i A(i,q) g(i,c)
+__global__ void matmul_bwd_x_kernel(MatmulArgs a) {
+  const int xb = a.x_b1 ? 1 : a.batch;
+  const int64_t xsz = (int64_t)a.k * a.p;
+  const int64_t total = xsz * xb * a.n;
+  const int64_t osz = (int64_t)a.m * a.p;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t jb = t / xsz;
+    const int64_t o = t - jb * xsz;
+    const int j = static_cast<int>(jb / xb), bb = static_cast<int>(jb - (int64_t)j * xb);
+    const int q = static_cast<int>(o % a.k), c = static_cast<int>(o / a.k);
+    float s = 0.f;
+    const int b0 = a.x_b1 ? 0 : bb, b1 = a.x_b1 ? a.batch : bb + 1;
+    for (int b = b0; b < b1; ++b) {
+      const float* A = a.a[j] + (a.a_b1 ? 0 : (int64_t)b * a.m * a.k);
+      const float* G = a.gout[j] + (int64_t)b * osz;
+      for (int i = 0; i < a.m; ++i) s += A[i + (int64_t)q * a.m] * G[i + (int64_t)c * a.m];
+    }
+    a.gx[j][(int64_t)bb * xsz + o] += s;
+  }
+}
+
+__global__ void affine_generic_fwd_kernel(AffineGenericArgs a) {
+  const int64_t total = (int64_t)a.m * a.batch * a.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t jb = t / a.m;
+    const int i = static_cast<int>(t - jb * a.m);
+    const int j = static_cast<int>(jb / a.batch), b = static_cast<int>(jb - (int64_t)j * a.batch);
+    float s = a.bias[j][(a.b_b1 ? 0 : (int64_t)b * a.m) + i];
+    for (int k = 0; k < a.terms; ++k) {
+      const int K = a.kdim[k];
+      const float* W = a.w[(int64_t)k * a.n + j] + (a.w_b1[k] ? 0 : (int64_t)b * a.m * K);
+      const float* X = a.x[(int64_t)k * a.n + j] + (a.x_b1[k] ? 0 : (int64_t)b * K);
+      float acc = 0.f;
+      for (int q = 0; q < K; ++q) acc += W[i + (int64_t)q * a.m] * X[q];
+      s += acc;
+    }
+    a.out[j][(int64_t)b * a.m + i] = s;
+  }
+}
+
+// which: 0 bias, 1 W of term k, 2 x of term k
+__global__ void affine_generic_bwd_kernel(AffineGenericArgs a, int which, int k) {
+  const int K = which == 0 ? 1 : a.kdim[k];
+  int ob;  // operand batch
+  int64_t osz;
+  if (which == 0) { ob = a.b_b1 ? 1 : a.batch; osz = a.m; }
+  else if (which == 1) { ob = a.w_b1[k] ? 1 : a.batch; osz = (int64_t)a.m * K; }
+  else { ob = a.x_b1[k] ? 1 : a.batch; osz = K; }
+  const bool b1 = ob == 1 && a.batch > 1;
+  const int64_t total = osz * ob * a.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t jb = t / osz;
+    const int64_t o = t - jb * osz;
+    const int j = static_cast<int>(jb / ob), bb = static_cast<int>(jb - (int64_t)j * ob);
+    const int b0 = b1 ? 0 : bb, b1e = b1 ? a.batch : bb + 1;
+    float s = 0.f;
+    for (int b = b0; b < b1e; ++b) {
+      const float* G = a.gout[j] + (int64_t)b * a.m;
+      if (which == 0) {
+        s += G[o];
+      } else if (which == 1) {
+        const int i = static_cast<int>(o % a.m), q = static_cast<int>(o / a.m);
+        const float* X = a.x[(int64_t)k * a.n + j] + (a.x_b1[k] ? 0 : (int64_t)b * K);
+        s += G[i] * X[q];
+      } else {
+        const float* W = a.w[(int64_t)k * a.n + j] + (a.w_b1[k] ? 0 : (int64_t)b * a.m * K);
+        const int q = static_cast<int>(o);
+        for (int i = 0; i < a.m; ++i) s += W[i + (int64_t)q * a.m] * G[i];
+      }
+    }
+    float* dst = which == 0 ? a.gbias[j] : (which == 1 ? a.gw[(int64_t)k * a.n + j] : a.gx[(int64_t)k * a.n + j]);
+    dst[(int64_t)bb * osz + o] += s;
+  }
+}
+
+// column sums over gathered rows, two deterministic passes
+__global__ void colsum_partial_kernel(const float* const* rows, int n_rows, int width, int chunks, float* work) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ch = blockIdx.y;
+  if (c >= width) return;
+  const int r0 = (int)((int64_t)n_rows * ch / chunks), r1 = (int)((int64_t)n_rows * (ch + 1) / chunks);
+  float s = 0.f;
+  for (int r = r0; r < r1; ++r) s += rows[r][c];
+  work[(int64_t)ch * width + c] = s;
+}
+
+__global__ void colsum_final_kernel(float* dst, const float* work, int width, int chunks) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= width) return;
+  float s = 0.f;
+  for (int ch = 0; ch < chunks; ++ch) s += work[(int64_t)ch * width + c];
+  dst[c] += s;
+}
+
+__global__ void row_reduce_scatter_kernel(float* const* dst_rows, const int* seg, const float* src, int n_targets,
+                                          int width) {
+  const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (u >= n_targets) return;
+  const int lane = threadIdx.x & 31;
+  float* dst = dst_rows[u];
+  for (int c = lane; c < width; c += 32) {
+    float acc = 0.f;
+    for (int k = seg[u]; k < seg[u + 1]; ++k) acc += src[(int64_t)k * width + c];
+    dst[c] += acc;
+  }
+}
+
+// ------------------------------------------------------------------ trainers
+// trainers.py:63-83 elementwise rules; the gradient is zeroed in the same pass
+// (Model.zero_gradients, params.py:114-119).
+
+__device__ __forceinline__ void apply_rule(const RuleArgs& r, float& w, float& g, float* s0, float* s1) {
+  switch (r.rule) {
+    case 0:
+      w = w - r.lr * g;
+      break;
+    case 1: {
+      const float v = r.momentum * (*s0) - r.lr * g;
+      *s0 = v;
+      w = w + v;
+      break;
+    }
+    case 2: {
+      const float sq = (*s0) + g * g;
+      *s0 = sq;
+      w = w - r.lr * g / (sqrtf(sq) + r.adagrad_eps);
+      break;
+    }
+    default: {
+      const float m1 = r.beta1 * (*s0) + (1.f - r.beta1) * g;
+      const float m2 = r.beta2 * (*s1) + (1.f - r.beta2) * (g * g);
+      *s0 = m1;
+      *s1 = m2;
+      const float mhat = m1 / r.bc1;
+      const float vhat = m2 / r.bc2;
+      w = w - r.lr * mhat / (sqrtf(vhat) + r.adam_eps);
+      break;
+    }
+  }
+  g = 0.f;
+}
+
+constexpr int kUpdChunk = 2048;
+
+__global__ void update_dense_kernel(RuleArgs r, const TensorSeg* __restrict__ segs, int nseg) {
+  // locate this block's segment: segments are laid out in order, each taking
+  // ceil(n / kUpdChunk) blocks
+  int blk = blockIdx.x, s = 0;
+  for (; s < nseg; ++s) {
+    const int nb = static_cast<int>((segs[s].n + kUpdChunk - 1) / kUpdChunk);
+    if (blk < nb) break;
+    blk -= nb;
+  }
+  if (s >= nseg) return;
+  const TensorSeg sg = segs[s];
+  const int64_t e0 = (int64_t)blk * kUpdChunk;
+  const int64_t e1 = min(e0 + kUpdChunk, sg.n);
+  float dummy0 = 0.f, dummy1 = 0.f;
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    float w = sg.w[e], g = sg.g[e];
+    float* p0 = sg.s0 ? sg.s0 + e : &dummy0;
+    float* p1 = sg.s1 ? sg.s1 + e : &dummy1;
+    apply_rule(r, w, g, p0, p1);
+    sg.w[e] = w;
+    sg.g[e] = g;
+  }
+}
+
+__global__ void update_rows_kernel(RuleArgs r, float* w, float* g, float* s0, float* s1, int dim,
+                                   const int64_t* __restrict__ ids, int n_rows) {
+  const int64_t total = (int64_t)n_rows * dim;
+  float dummy0 = 0.f, dummy1 = 0.f;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = t / dim, c = t - u * dim;
+    const int64_t e = ids[u] * dim + c;
+    float wv = w[e], gv = g[e];
+    apply_rule(r, wv, gv, s0 ? s0 + e : &dummy0, s1 ? s1 + e : &dummy1);
+    w[e] = wv;
+    g[e] = gv;
+  }
+}
+
+__global__ void scale_kernel(float* y, int64_t n, float alpha) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    y[t] *= alpha;
+}
+__global__ void fill_kernel(float* y, int64_t n, float v) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    y[t] = v;
+}
+
+inline int grid_for(int64_t n) {
+  const int64_t cap = 148 * 32;
+  int64_t b = (n + kThreads - 1) / kThreads;
+  if (b > cap) b = cap;
+  return b < 1 ? 1 : static_cast<int>(b);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+
+int launch_ew_fwd(const EwArgs& a, cudaStream_t s) {
+  const int64_t total = (int64_t)a.elem * a.batch * a.n;
+  if (total == 0) return 0;
+  ew_fwd_kernel<<<grid_for(total), kThreads, 0, s>>>(a);
+  return 1;
+}
+
+int launch_ew_bwd(const EwArgs& a, cudaStream_t s) {
+  const bool bcast_ok = a.kind == EW_ADD || a.kind == EW_CMULT || a.kind == EW_SCALE;
+  if (bcast_ok && (a.a_b1 || a.b_b1) && a.batch > 1) {
+    ew_bwd_bcast_kernel<<<grid_for((int64_t)a.elem * a.n), kThreads, 0, s>>>(a);
+  } else {
+    EwArgs c = a;
+    c.a_b1 = c.b_b1 = 0;
+    ew_bwd_flat_kernel<<<grid_for((int64_t)a.elem * a.batch * a.n), kThreads, 0, s>>>(c);
+  }
+  return 1;
+}
+
+int launch_chain_fwd(const ChainArgs& a, cudaStream_t s) {
+  chain_fwd_kernel<<<grid_for((int64_t)a.size * a.n), kThreads, 0, s>>>(a);
+  return 1;
+}
+int launch_chain_bwd(const ChainArgs& a, cudaStream_t s) {
+  chain_bwd_kernel<<<grid_for((int64_t)a.size * a.n), kThreads, 0, s>>>(a);
+  return 1;
+}
+
+int launch_pick_fwd(const PickArgs& a, cudaStream_t s) {
+  pick_fwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.width), kThreads, 0, s>>>(a);
+  return 1;
+}
+int launch_pick_bwd(const PickArgs& a, cudaStream_t s) {
+  pick_bwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.width), kThreads, 0, s>>>(a);
+  return 1;
+}
+int launch_concat_fwd(const ConcatArgs& a, cudaStream_t s) {
+  concat_fwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.total), kThreads, 0, s>>>(a);
+  return 1;
+}
+int launch_concat_bwd(const ConcatArgs& a, cudaStream_t s) {
+  concat_bwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.total), kThreads, 0, s>>>(a);
+  return 1;
+}
+int launch_sum_batches_fwd(const SumBatchesArgs& a, cudaStream_t s) {
+  sum_batches_fwd_kernel<<<grid_for((int64_t)a.n * a.elem), kThreads, 0, s>>>(a);
+  return 1;
+}
+int launch_sum_batches_bwd(const SumBatchesArgs& a, cudaStream_t s) {
+  sum_batches_bwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.elem), kThreads, 0, s>>>(a);
+  return 1;
+}
+
+int launch_softmax_fwd(const RowArgs& a, cudaStream_t s) { return launch_rows<0>(a, s); }
+int launch_softmax_bwd(const RowArgs& a, cudaStream_t s) { return launch_rows<1>(a, s); }
+int launch_pnls_fwd(const RowArgs& a, cudaStream_t s) { return launch_rows<2>(a, s); }
+int launch_pnls_bwd(const RowArgs& a, cudaStream_t s) { return launch_rows<3>(a, s); }
+
+int launch_gather_rows(const float* table, int dim, const int64_t* ids, float* const* out_rows, int rows,
+                       cudaStream_t s) {
+  if (rows <= 0) return 0;
+  gather_rows_kernel<<<(rows + 7) / 8, 256, 0, s>>>(table, dim, ids, out_rows, rows);
+  return 1;
+}
+
+int launch_segment_scatter_add(float* table_grad, int dim, const int64_t* uniq_ids, const int* seg,
+                               const float* const* src_rows, int n_unique, float scale, cudaStream_t s) {
+  if (n_unique <= 0) return 0;
+  segment_scatter_add_kernel<<<(n_unique + 7) / 8, 256, 0, s>>>(table_grad, dim, uniq_ids, seg, src_rows, n_unique,
+                                                                 scale);
+  return 1;
+}
+
+int launch_pack_rows(const float* table, int dim, const int64_t* ids, float* out, int n, cudaStream_t s) {
+  if (n <= 0) return 0;
+  pack_rows_kernel<<<grid_for((int64_t)n * dim), kThreads, 0, s>>>(table, dim, ids, out, n);
+  return 1;
+}
+
+int launch_matmul_fwd(const MatmulArgs& a, cudaStream_t s) {
+  matmul_fwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.m * a.p), kThreads, 0, s>>>(a);
+  return 1;
+}
+int launch_matmul_bwd(const MatmulArgs& a, cudaStream_t s) {
+  matmul_bwd_a_kernel<<<grid_for((int64_t)a.n * a.batch * a.m * a.k), kThreads, 0, s>>>(a);
+  matmul_bwd_x_kernel<<<grid_for((int64_t)a.n * a.batch * a.k * a.p), kThreads, 0, s>>>(a);
+  return 2;
+}
+
+int launch_affine_generic_fwd(const AffineGenericArgs& a, cudaStream_t s) {
+  affine_generic_fwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.m), kThreads, 0, s>>>(a);
+  return 1;
+}
+int launch_affine_generic_bwd(const AffineGenericArgs& a, cudaStream_t s) {
+  int launches = 0;
+  affine_generic_bwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.m), kThreads, 0, s>>>(a, 0, 0);
+  ++launches;
+  for (int k = 0; k < a.terms; ++k) {
+    affine_generic_bwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.m * a.kdim[k]), kThreads, 0, s>>>(a, 1, k);
+    affine_generic_bwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.kdim[k]), kThreads, 0, s>>>(a, 2, k);
+    launches += 2;
+  }
+  return launches;
+}
+
+int launch_colsum_rows(float* dst, const float* const* rows, int n_rows, int width, float* work, cudaStream_t s) {
+  if (n_rows <= 0) return 0;
+  int chunks = n_rows / 16;
+  if (chunks < 1) chunks = 1;
+  if (chunks > 64) chunks = 64;
+  dim3 g1((width + 255) / 256, chunks);
+  colsum_partial_kernel<<<g1, 256, 0, s>>>(rows, n_rows, width, chunks, work);
+  colsum_final_kernel<<<(width + 255) / 256, 256, 0, s>>>(dst, work, width, chunks);
+  return 2;
+}
+
+int launch_row_reduce_scatter(float* const* dst_rows, const int* seg, const float* src, int n_targets, int width,
+                              cudaStream_t s) {
+  if (n_targets <= 0) return 0;
+  row_reduce_scatter_kernel<<<(n_targets + 7) / 8, 256, 0, s>>>(dst_rows, seg, src, n_targets, width);
+  return 1;
+}
+
+int launch_update_dense(const RuleArgs& r, const TensorSeg* segs_dev, int nseg, int64_t total_blocks, cudaStream_t s) {
+  if (nseg <= 0 || total_blocks <= 0) return 0;
+  update_dense_kernel<<<static_cast<unsigned>(total_blocks), 256, 0, s>>>(r, segs_dev, nseg);
+  return 1;
+}
+
+int launch_update_rows(const RuleArgs& r, float* w, float* g, float* s0, float* s1, int dim, const int64_t* ids,
+                       int n_rows, cudaStream_t s) {
+  if (n_rows <= 0) return 0;
+  update_rows_kernel<<<grid_for((int64_t)n_rows * dim), kThreads, 0, s>>>(r, w, g, s0, s1, dim, ids, n_rows);
+  return 1;
+}
+
+int launch_scale(float* y, int64_t n, float alpha, cudaStream_t s) {
+  if (n <= 0) return 0;
+  scale_kernel<<<grid_for(n), kThreads, 0, s>>>(y, n, alpha);
+  return 1;
+}
+int launch_fill(float* y, int64_t n, float v, cudaStream_t s) {
+  if (n <= 0) return 0;
+  fill_kernel<<<grid_for(n), kThreads, 0, s>>>(y, n, v);
+  return 1;
+}
+
+int update_chunk() { return kUpdChunk; }
+
+}  // namespace dg

@@ -1,0 +1,188 @@
+// Kernel launchers of the B200 executor (sm_100a).  Every launcher enqueues on
+// the given stream and returns the number of kernels it launched (>= 0) so the
+// executor can report gpu_launches; errors surface through cudaGetLastError.
+//
+// Group kernels operate on N same-signature nodes at once ("operation
+// batching"); per-node operands are addressed through device pointer tables
+// built by the planner (executor.cpp) and uploaded once per plan.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dg {
+
+// ---------------------------------------------------------------- elementwise
+enum EwKind : int {
+  EW_TANH = 0, EW_LOGISTIC = 1, EW_SCALE = 2, EW_ADD = 3, EW_CMULT = 4
+};
+
+struct EwArgs {
+  int kind;
+  int n;            // nodes in the group
+  int elem;         // per-batch-element size of the output
+  int batch;        // output batch
+  int a_b1, b_b1;   // operand is batch-1 (broadcast over batch)
+  float scalar;
+  const float* const* a;   // [n] operand 0 values
+  const float* const* b;   // [n] operand 1 values (binary only)
+  float* const* out;       // [n] output values
+  // backward
+  const float* const* gout;  // [n]
+  const float* const* oval;  // [n] output values (tanh/logistic backward)
+  float* const* ga;          // [n] operand-0 grads
+  float* const* gb;          // [n] operand-1 grads
+};
+int launch_ew_fwd(const EwArgs& a, cudaStream_t s);
+int launch_ew_bwd(const EwArgs& a, cudaStream_t s);
+
+// n-ary prefix sum for rewritten add chains: outs[i] = ins[0] + ... + ins[i+1]
+struct ChainArgs {
+  int n;       // chains in the group
+  int len;     // number of add nodes in each chain (inputs = len + 1)
+  int size;    // elements per value
+  const float* const* ins;   // [(len+1) * n], slot-major
+  float* const* outs;        // [len * n]
+  const float* const* gfinal;  // [n] grad of the last add
+  float* const* gins;        // [(len+1) * n]
+  float* const* gouts;       // [len * n] grads of the intermediate adds (get gfinal)
+};
+int launch_chain_fwd(const ChainArgs& a, cudaStream_t s);
+int launch_chain_bwd(const ChainArgs& a, cudaStream_t s);
+
+// --------------------------------------------------------------- structural
+struct PickArgs {
+  int n, batch, in_elem, lo, width;
+  const float* const* in; float* const* out;
+  const float* const* gout; float* const* gin;
+};
+int launch_pick_fwd(const PickArgs& a, cudaStream_t s);
+int launch_pick_bwd(const PickArgs& a, cudaStream_t s);
+
+struct ConcatArgs {
+  int n, batch, parts, total;
+  const int* offs;                 // [parts + 1] column offsets (device)
+  const float* const* in;          // [parts * n]
+  float* const* out;               // [n]
+  const float* const* gout;
+  float* const* gin;               // [parts * n]
+};
+int launch_concat_fwd(const ConcatArgs& a, cudaStream_t s);
+int launch_concat_bwd(const ConcatArgs& a, cudaStream_t s);
+
+struct SumBatchesArgs {
+  int n, batch, elem;
+  const float* const* in; float* const* out;
+  const float* const* gout; float* const* gin;
+};
+int launch_sum_batches_fwd(const SumBatchesArgs& a, cudaStream_t s);
+int launch_sum_batches_bwd(const SumBatchesArgs& a, cudaStream_t s);
+
+// ----------------------------------------------------------------- row-wise
+struct RowArgs {
+  int rows;        // total rows (n nodes * batch)
+  int width;       // row length
+  int batch;       // rows per node
+  const float* const* in;    // [n] node input values (rows batch-contiguous)
+  float* const* out;         // [n] node outputs
+  const int* labels;         // [rows] (pnls)
+  const float* const* gout;  // [n]
+  const float* const* oval;  // [n] (softmax backward)
+  float* const* gin;         // [n]
+};
+int launch_softmax_fwd(const RowArgs& a, cudaStream_t s);
+int launch_softmax_bwd(const RowArgs& a, cudaStream_t s);
+int launch_pnls_fwd(const RowArgs& a, cudaStream_t s);
+int launch_pnls_bwd(const RowArgs& a, cudaStream_t s);
+
+// ------------------------------------------------------------ lookup tables
+// gather: out_rows[r] = table[ids[r]]  (one warp per row, 128-bit vectors)
+int launch_gather_rows(const float* table, int dim, const int64_t* ids, float* const* out_rows, int rows,
+                       cudaStream_t s);
+// atomic-free sorted segmented scatter-add:
+//   for u in unique: table_grad[ids[u]] += scale * sum_{k in seg[u]..seg[u+1]} src_rows[k]
+int launch_segment_scatter_add(float* table_grad, int dim, const int64_t* uniq_ids, const int* seg,
+                               const float* const* src_rows, int n_unique, float scale, cudaStream_t s);
+
+// ---------------------------------------------------------------- generic
+// matmul (ops.py:252-301) per batch element, column-major element layout
+struct MatmulArgs {
+  int n, batch, m, k, p, a_b1, x_b1;
+  const float* const* a; const float* const* x; float* const* out;
+  const float* const* gout; float* const* ga; float* const* gx;
+};
+int launch_matmul_fwd(const MatmulArgs& a, cudaStream_t s);
+int launch_matmul_bwd(const MatmulArgs& a, cudaStream_t s);
+
+// affine with a per-element (batched) or non-parameter matrix: slow generic path
+struct AffineGenericArgs {
+  int n, batch, m, terms;
+  int b_b1;
+  const float* const* bias;   // [n]
+  int kdim[8];                // per term (<= 8 terms)
+  int w_b1[8];
+  int x_b1[8];
+  const float* const* w;      // [terms * n]
+  const float* const* x;      // [terms * n]
+  float* const* out;          // [n]
+  const float* const* gout;
+  float* const* gbias;
+  float* const* gw;
+  float* const* gx;
+};
+int launch_affine_generic_fwd(const AffineGenericArgs& a, cudaStream_t s);
+int launch_affine_generic_bwd(const AffineGenericArgs& a, cudaStream_t s);
+
+// column sums over gathered rows: dst[c] += sum_r rows[r][c]  (deterministic)
+int launch_colsum_rows(float* dst, const float* const* rows, int n_rows, int width, float* work,
+                       cudaStream_t s);
+// row reduce-scatter: for t in targets: dst[t] += sum_{k in seg} src[k]  (src dense, width)
+int launch_row_reduce_scatter(float* const* dst_rows, const int* seg, const float* src, int n_targets,
+                              int width, cudaStream_t s);
+
+// ------------------------------------------------------------------- GEMM
+// C[M x N] (=|+=) sum_seg A_seg(m,k) B_seg(k,n) (+ bias_m(n)), fp32 SIMT.
+struct Operand {
+  const float* base;     // used when rows == nullptr: row(i) = base + i*ld
+  int64_t ld;
+  const float* const* rows;  // row pointer table (device) or nullptr
+};
+struct GemmSeg {
+  int K;
+  Operand A, B;
+};
+struct GemmArgs {
+  int M, N;
+  int n_seg;
+  GemmSeg seg[4];
+  bool a_kmajor;    // A(m,k) = A.row(k)[m]  (else A.row(m)[k])
+  bool b_nmajor;    // B(k,n) = B.row(n)[k]  (else B.row(k)[n])
+  Operand C;        // row(m) -> N contiguous outputs
+  bool accumulate;  // C += acc  (else C = acc)
+  Operand bias;     // optional per-row bias vector (row(m)[n]); base==rows==nullptr -> none
+  float* work;      // split-K partials
+  int64_t work_floats;
+  bool a_rows_aligned;  // every A row-table entry is 16B aligned (planner-checked)
+  bool b_rows_aligned;
+};
+int launch_gemm(const GemmArgs& a, cudaStream_t s);
+
+// ------------------------------------------------------------- trainers
+struct TensorSeg { float* w; float* g; float* s0; float* s1; int64_t n; };
+int update_chunk();
+struct RuleArgs {
+  int rule;  // 0 sgd 1 momentum 2 adagrad 3 adam
+  float lr, momentum, adagrad_eps, beta1, beta2, adam_eps;
+  float bc1, bc2;  // Adam bias corrections 1-beta^t (computed in double on host)
+};
+// dense multi-tensor apply over `nseg` segments (device table), zeroes grads
+int launch_update_dense(const RuleArgs& r, const TensorSeg* segs_dev, int nseg, int64_t total, cudaStream_t s);
+// sparse rows: for u < n_rows: row ids[u] of (w,g,s0,s1) with width dim; zeroes those grad rows
+int launch_update_rows(const RuleArgs& r, float* w, float* g, float* s0, float* s1, int dim, const int64_t* ids,
+                       int n_rows, cudaStream_t s);
+
+int launch_scale(float* y, int64_t n, float alpha, cudaStream_t s);
+int launch_fill(float* y, int64_t n, float v, cudaStream_t s);
+// pack rows: out[u] = table[ids[u]] (for DP exchange)
+int launch_pack_rows(const float* table, int dim, const int64_t* ids, float* out, int n, cudaStream_t s);
+
+}  // namespace dg

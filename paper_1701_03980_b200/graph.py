@@ -1,0 +1,268 @@
+"""ComputationGraph of the drop-in API (pkg/src/dyncore/graph.py:20-172).
+
+Construction stays on the host and keeps the reference contract: add_node
+checks staleness and runs the shape rule immediately (errors at construction,
+no numeric work), nodes are append-only, `renew()` bumps the generation.
+Execution is delegated in bulk to the native executor (libdyngpu.so): the
+pending node records are packed into one dg_node table per call
+(dg_graph_append), `forward_to`/`value` evaluate only nodes past the
+watermark (incremental, never recomputes), `backward` runs the batched
+reverse sweep with gradients landing in the Model's device storage.
+
+Counters keep the reference's semantics: `forward_calls` counts nodes
+(including parameter aliases), the pools' alloc_count/cursor charge the same
+64-byte-rounded sizes per node (arena.py:48-56).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from . import device as _dev
+from .errors import ConfigError, NonScalarLoss, ShapeError, StaleExpression
+from .ops import REGISTRY
+from .params import materialize_pending
+from .tensor import Shape, Tensor
+
+
+class Expression:
+    """Handle to a graph node; valid for one graph generation."""
+
+    __slots__ = ("graph", "index", "generation")
+
+    def __init__(self, graph: "ComputationGraph", index: int, generation: int):
+        self.graph = graph
+        self.index = index
+        self.generation = generation
+
+    @property
+    def shape(self) -> Shape:
+        self.graph.check_current(self)
+        return self.graph.nodes[self.index].shape
+
+    def __repr__(self) -> str:
+        return f"Expression(node={self.index}, gen={self.generation})"
+
+
+class Node:
+    __slots__ = ("kind", "inputs", "shape", "aux", "code")
+
+    def __init__(self, kind: str, inputs: tuple, shape: Shape, aux, code: int):
+        self.kind = kind
+        self.inputs = inputs
+        self.shape = shape
+        self.aux = aux
+        self.code = code
+
+
+class ModelGradientSink:
+    """Default backward target: the parameters' own gradient storage.  On the
+    device executor this is the only sink (data parallelism uses per-rank
+    model replicas plus a collective, see parallel.py)."""
+
+
+DIRECT_SINK = ModelGradientSink()
+
+_HDR_FIELDS = 13
+
+
+class ComputationGraph:
+    def __init__(self, pools):
+        self.pools = pools
+        self.dtype = pools.dtype
+        self.nodes: list[Node] = []
+        self.generation = 0
+        self.watermark = -1
+        self.forward_calls = 0
+        self.sink = DIRECT_SINK
+        self._h = None  # native dg_graph*
+        self._sent = 0  # nodes already appended to the native table
+        self._stream = None
+        pools.bind(self)
+
+    # -- native plumbing ---------------------------------------------------
+
+    def _native(self):
+        if self._h is None:
+            lib = _native.lib()
+            fwd, bwd, work = self.pools.device_buffers()
+            h = ctypes.c_void_p()
+            _native.check(lib.dg_graph_create(
+                _dev.torch().cuda.current_device(), _native.ptr(fwd), self.pools.forward.capacity,
+                _native.ptr(bwd), self.pools.backward.capacity, _native.ptr(work), self.pools.work_bytes,
+                ctypes.byref(h)))
+            self._h = h
+        s = _dev.stream_ptr()
+        if s != self._stream:
+            _native.check(_native.lib().dg_graph_set_stream(self._h, s))
+            self._stream = s
+        return self._h
+
+    def _counters(self):
+        out = np.zeros(8, dtype=np.int64)
+        if self._h is not None:
+            _native.check(_native.lib().dg_graph_counters(self._h, out.ctypes.data))
+        return out
+
+    def plan_stats(self):
+        out = np.zeros(8, dtype=np.int64)
+        if self._h is not None:
+            _native.check(_native.lib().dg_graph_plan_stats(self._h, out.ctypes.data))
+        return out
+
+    def profile_enable(self, classes) -> None:
+        """CUDA-event timing of every launch of the given op classes
+        (names from _native.PROFILE_CLASSES)."""
+        mask = 0
+        for c in classes:
+            mask |= 1 << _native.PROFILE_CLASSES.index(c)
+        _native.check(_native.lib().dg_profile_enable(self._native(), mask))
+
+    def profile_read(self, cls: str) -> dict:
+        out = np.zeros(4, dtype=np.float64)
+        _native.check(_native.lib().dg_profile_read(self._native(), _native.PROFILE_CLASSES.index(cls),
+                                                    out.ctypes.data))
+        return {"ms": float(out[0]), "launches": int(out[1]), "flops": float(out[2]), "bytes": float(out[3])}
+
+    def profile_reset(self) -> None:
+        _native.check(_native.lib().dg_profile_reset(self._native()))
+
+    def _native_renew(self):
+        if self._h is not None:
+            _native.check(_native.lib().dg_graph_renew(self._h))
+
+    def __del__(self):
+        try:
+            if self._h is not None:
+                _native.lib().dg_graph_destroy(self._h)
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+    def _flush(self, h) -> None:
+        """Pack pending nodes into one dg_node table (dg_graph_append)."""
+        nodes = self.nodes
+        start, end = self._sent, len(nodes)
+        if start == end:
+            return
+        hdr = []
+        ins = []
+        aux_i = []
+        aux_f = []
+        n_f = 0
+        for i in range(start, end):
+            nd = nodes[i]
+            inputs = nd.inputs
+            dims = nd.shape.dims
+            r = len(dims)
+            ai, af = REGISTRY[nd.kind].encode(nd.aux)
+            nai = len(ai)
+            naf = 0 if af is None else af.shape[0]
+            d = dims + (1,) * (4 - r)
+            hdr.extend((nd.code, len(inputs), len(ins), r, d[0], d[1], d[2], d[3], nd.shape.batch,
+                        len(aux_i), nai, n_f, naf))
+            ins.extend(inputs)
+            if nai:
+                aux_i.extend(ai)
+            if naf:
+                aux_f.append(af)
+                n_f += naf
+        hdr_a = np.array(hdr, dtype=np.int32)
+        ins_a = np.array(ins, dtype=np.int32) if ins else np.zeros(1, np.int32)
+        ai_a = np.array(aux_i, dtype=np.int64) if aux_i else np.zeros(1, np.int64)
+        af_a = np.concatenate(aux_f).astype(np.float32, copy=False) if aux_f else np.zeros(1, np.float32)
+        _native.check(_native.lib().dg_graph_append(
+            h, hdr_a.ctypes.data, end - start, ins_a.ctypes.data, len(ins), ai_a.ctypes.data, len(aux_i),
+            af_a.ctypes.data, n_f))
+        self._sent = end
+
+    def _prepare(self):
+        materialize_pending()
+        h = self._native()
+        self._flush(h)
+        return h
+
+    # -- lifecycle ---------------------------------------------------------
+
+    def renew(self) -> None:
+        self.nodes.clear()
+        self.generation += 1
+        self.watermark = -1
+        self._sent = 0
+        self.pools.reset_transient()
+
+    def check_current(self, e: Expression) -> None:
+        if e.graph is not self or e.generation != self.generation:
+            raise StaleExpression(
+                f"expression from generation {e.generation} used in generation {self.generation}"
+            )
+
+    # -- construction ------------------------------------------------------
+
+    def add_node(self, kind: str, inputs=(), aux=None) -> Expression:
+        gen = self.generation
+        nodes = self.nodes
+        in_shapes = []
+        indices = []
+        for e in inputs:
+            if e.graph is not self or e.generation != gen:
+                self.check_current(e)
+            in_shapes.append(nodes[e.index].shape)
+            indices.append(e.index)
+        od = REGISTRY[kind]
+        shape = od.shape(aux, in_shapes)
+        nodes.append(Node(kind, tuple(indices), shape, aux, od.code))
+        return Expression(self, len(nodes) - 1, gen)
+
+    # -- evaluation --------------------------------------------------------
+
+    def _advance(self, upto: int) -> None:
+        if upto > self.watermark:
+            self.forward_calls += upto - self.watermark
+            self.watermark = upto
+
+    def forward_to(self, e: Expression) -> None:
+        self.check_current(e)
+        if e.index <= self.watermark:
+            return
+        h = self._prepare()
+        _native.check(_native.lib().dg_forward(h, e.index))
+        self._advance(e.index)
+
+    def value(self, e: Expression) -> Tensor:
+        """Host copy of a node value (graph.py:132-135); synchronises."""
+        self.check_current(e)
+        h = self._prepare()
+        shape = self.nodes[e.index].shape
+        out = np.empty(shape.size(), dtype=np.float32)
+        _native.check(_native.lib().dg_value(h, e.index, out.ctypes.data, out.shape[0]))
+        self._advance(e.index)
+        return Tensor(shape, out)
+
+    # -- differentiation ---------------------------------------------------
+
+    def backward(self, e: Expression) -> None:
+        self.check_current(e)
+        loss = self.nodes[e.index]
+        if loss.shape.elem_size() != 1 or loss.shape.batch != 1:
+            raise NonScalarLoss(f"backward needs a scalar, got {loss.shape}")
+        if self.sink is not DIRECT_SINK:
+            raise ConfigError("the device executor accumulates into model storage only; use parallel.py for DP")
+        h = self._prepare()
+        _native.check(_native.lib().dg_backward(h, e.index))
+        self._advance(e.index)
+        _dev.bump_epoch()
+
+    def gradient(self, e: Expression) -> Tensor:
+        """Debug accessor for a node's last backward slot.  Parameter nodes
+        accumulate straight into the parameter gradient, so for them this is
+        the parameter's accumulated gradient."""
+        self.check_current(e)
+        shape = self.nodes[e.index].shape
+        if self._h is None:
+            raise ShapeError("no backward pass has populated this node yet")
+        out = np.empty(shape.size(), dtype=np.float32)
+        _native.check(_native.lib().dg_gradient(self._h, e.index, out.ctypes.data, out.shape[0]))
+        return Tensor(shape, out)

@@ -1,0 +1,151 @@
+"""CUDA executor vs the reference: golden fixtures (generated from the real
+reference) and the live CPU oracle at BASELINE sizes.  Every call goes through
+the drop-in API into libdyngpu.so (C-ABI)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import engine as orc
+from paper_1701_03980_b200 import workloads as W
+from tests.golden import cases
+from tests.helpers import gpu_ctx, oracle_ctx, parity, pgrad, pvals
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+OPS = np.load(os.path.join(GOLD, "ops.npz"))
+WL = np.load(os.path.join(GOLD, "workloads.npz"))
+
+
+@pytest.mark.parametrize("name", sorted(cases.OP_CASES))
+def test_op_cases_match_reference(name):
+    dy, cg, model = gpu_ctx(seed=7, mb=64)
+    out, ins = cases.OP_CASES[name](dy, cg, model)
+    loss = cases.scalarize(dy, cg, out)
+    cg.backward(loss)
+    parity(cg.value(loss).data, OPS[f"{name}/loss"], what="loss")
+    parity(cg.value(out).data, OPS[f"{name}/value"], what="value")
+    for k, e in enumerate(ins):
+        parity(cg.gradient(e).data, OPS[f"{name}/grad{k}"], what=f"grad{k}")
+    for p in model.parameters:
+        parity(pgrad(p), OPS[f"{name}/pgrad/{p.name}"], what=p.name)
+    for lp in model.lookups:
+        parity(pgrad(lp), OPS[f"{name}/lgrad/{lp.name}"].reshape(-1), what=lp.name)
+        assert sorted(lp.touched) == list(OPS[f"{name}/touched/{lp.name}"])
+    assert cg.forward_calls == int(OPS[f"{name}/forward_calls"][0])
+    fa, ba = OPS[f"{name}/alloc"]
+    assert cg.pools.forward.alloc_count == fa
+    assert cg.pools.backward.alloc_count == ba
+
+
+@pytest.mark.parametrize("name", sorted(cases.workload_cases()))
+def test_workload_traces_match_reference(name):
+    make_task, data, rule, steps = cases.workload_cases()[name]
+    dy, cg, model = gpu_ctx(seed=1, mb=256)
+    task = make_task(dy, model)
+    for p in model.parameters:
+        assert np.array_equal(pvals(p), WL[f"{name}/init/{p.name}"].astype(np.float64))
+    tr = dy.Trainer(model, rule)
+    lr = tr.lr
+    for s in range(steps):
+        cg.renew()
+        loss = cases.call_loss(task, cg, data[s])
+        cg.backward(loss)
+        parity(cg.value(loss).data, WL[f"{name}/loss{s}"], what=f"loss{s}")
+        for p in model.parameters:
+            key = f"{name}/grad{s}/{p.name}"
+            if key in WL:
+                parity(pgrad(p), WL[key], what=key)
+        for lp in model.lookups:
+            rows = WL[f"{name}/touched{s}/{lp.name}"]
+            assert sorted(lp.touched) == list(rows), "touched set must be bit-exact"
+            parity(np.asarray(lp.gradient)[rows], WL[f"{name}/lgrad{s}/{lp.name}"], what=f"{lp.name} rows")
+        tr.update()
+    band = 0.0 if rule == "sgd" else 2 * lr * steps
+    for p in model.parameters:
+        parity(pvals(p), WL[f"{name}/final/{p.name}"], band=band, what=f"final {p.name}")
+    for lp in model.lookups:
+        parity(pvals(lp), WL[f"{name}/final/{lp.name}"].reshape(-1), band=band, what=f"final {lp.name}")
+
+
+# ---------------------------------------------------------------------------
+# BASELINE-size configs against the live oracle (same seeds, same inputs)
+# ---------------------------------------------------------------------------
+
+
+def _run_steps(dy, cg, model, task, batches, rule, n_steps, record):
+    tr = dy.Trainer(model, rule)
+    out = []
+    for s in range(n_steps):
+        cg.renew()
+        loss = cases.call_loss(task, cg, batches[s])
+        cg.backward(loss)
+        rec = {"loss": float(cg.value(loss).data[0])}
+        if record:
+            rec["grads"] = {p.name: pgrad(p) for p in model.parameters}
+            rec["touched"] = {lp.name: sorted(lp.touched) for lp in model.lookups}
+            rec["lgrads"] = {lp.name: np.asarray(lp.gradient)[sorted(lp.touched)].copy() for lp in model.lookups}
+        out.append(rec)
+        tr.update()
+    return out, model
+
+
+def _compare_full(make_task, batches, rule="adam", n_steps=2):
+    dyg, cgg, mg = gpu_ctx(seed=3, mb=1024)
+    got, mg = _run_steps(dyg, cgg, mg, make_task(dyg, mg), batches, rule, n_steps, True)
+    dyo, cgo, mo = oracle_ctx(seed=3)
+    ref, mo = _run_steps(dyo, cgo, mo, make_task(dyo, mo), batches, rule, n_steps, True)
+    for s in range(n_steps):
+        parity(got[s]["loss"], ref[s]["loss"], what=f"loss{s}")
+        for name, g in ref[s]["grads"].items():
+            parity(got[s]["grads"][name], g, what=f"step{s} {name}")
+        for name, t in ref[s]["touched"].items():
+            assert got[s]["touched"][name] == t
+            parity(got[s]["lgrads"][name], ref[s]["lgrads"][name], what=f"step{s} {name} rows")
+    band = 0.0 if rule == "sgd" else 2 * 1e-3 * n_steps
+    for p, q in zip(mg.parameters, mo.parameters):
+        parity(pvals(p), pvals(q), band=band, what=f"final {p.name}")
+
+
+def test_ptb_mb16_full_size_vs_oracle():
+    sents = W.ptb_corpus(21, 32)
+    batches = W.minibatches(sents, 16)
+    _compare_full(lambda dy, m: W.RNNLM(dy, m, 10_000, 128, 256, 2), batches)
+
+
+def test_ptb_mb64_full_size_vs_oracle_sgd():
+    sents = W.ptb_corpus(22, 64)
+    batches = W.minibatches(sents, 64)
+    _compare_full(lambda dy, m: W.RNNLM(dy, m, 10_000, 128, 256, 2), batches, rule="sgd", n_steps=1)
+
+
+def test_tiny_lm_full_size_vs_oracle():
+    sents = W.tiny_lm_corpus(23, 3)
+    _compare_full(lambda dy, m: W.RNNLM(dy, m, 1000, 64, 64, 1), [[s] for s in sents], n_steps=3)
+
+
+def test_tree_lstm_full_size_vs_oracle():
+    td = W.tree_corpus(24, 3)
+    _compare_full(lambda dy, m: W.TreeClassifier(dy, m, td.vocab_size, 5, 128, 150),
+                  list(zip(td.trees, td.labels)), n_steps=3)
+
+
+def test_char_tagger_full_size_vs_oracle():
+    tg = W.tagger_corpus(25, 200, n_types=4000)
+    _compare_full(lambda dy, m: W.CharTagger(dy, m, tg), tg.sentences, n_steps=3)
+
+
+def test_bitwise_determinism_full_size():
+    """Two identical runs are bitwise identical (tests/test_graph.py:160-173)."""
+    sents = W.ptb_corpus(26, 16)
+    outs = []
+    for _ in range(2):
+        dy, cg, m = gpu_ctx(seed=5, mb=512)
+        task = W.RNNLM(dy, m, 10_000, 128, 256, 2)
+        res, m = _run_steps(dy, cg, m, task, [sents], "adam", 1, False)
+        outs.append((res[0]["loss"], [pvals(p).copy() for p in m.parameters]))
+    assert outs[0][0] == outs[1][0]
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(a, b)

@@ -1,0 +1,319 @@
+"""Reference test semantics re-run on the CUDA executor (fp32 variants of
+pkg/tests/test_graph.py, test_ops.py, test_trainers.py, test_params.py)."""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_1701_03980_b200 as dc
+from paper_1701_03980_b200 import ops
+from paper_1701_03980_b200.errors import NonScalarLoss, PoolExhausted, StaleExpression
+from tests.helpers import gpu_ctx
+
+pytestmark = pytest.mark.gpu
+
+
+def make_ctx(mb=4.0, seed=1, init_zero=False):
+    pools = dc.new_poolset(mb, mb, mb)
+    return dc.ComputationGraph(pools), dc.Model(pools, seed=seed, init_zero=init_zero)
+
+
+def vec(values, batch=1):
+    return dc.from_values(dc.Shape((len(values) // batch,), batch), values)
+
+
+# -- graph semantics (tests/test_graph.py) ----------------------------------
+
+
+def test_input_value_and_defensive_copy():
+    cg, _ = make_ctx()
+    x = ops.input(cg, vec([1.0, 2.0]))
+    kept = cg.value(x)
+    cg.renew()
+    assert np.allclose(kept.data, [1, 2])
+    with pytest.raises(StaleExpression):
+        cg.value(x)
+
+
+def test_incremental_forward_never_recomputes():
+    cg, _ = make_ctx()
+    x = ops.input(cg, vec([1.0, 2.0]))
+    cg.value(x)
+    calls = cg.forward_calls
+    y = ops.tanh(x)
+    assert np.allclose(cg.value(y).data, np.tanh([1.0, 2.0]), atol=1e-6)
+    assert cg.forward_calls == calls + 1
+    cg.value(y)
+    assert cg.forward_calls == calls + 1
+
+
+def test_forward_to_and_watermark():
+    cg, _ = make_ctx()
+    x = ops.input(cg, vec([0.5]))
+    y = ops.logistic(x)
+    z = ops.tanh(y)
+    cg.forward_to(y)
+    assert cg.watermark == y.index
+    assert cg.forward_calls == 2
+    assert np.allclose(cg.value(z).data, np.tanh(1 / (1 + np.exp(-0.5))), atol=1e-6)
+
+
+def test_non_scalar_loss():
+    cg, _ = make_ctx()
+    with pytest.raises(NonScalarLoss):
+        cg.backward(ops.input(cg, vec([1.0, 2.0])))
+
+
+def test_two_backward_calls_accumulate_twice():
+    cg, model = make_ctx()
+    p = model.add_parameters((2,), "p")
+    p.set_value([1.0, 2.0])
+    pe = ops.parameter(cg, p)
+    loss = ops.matmul(ops.input(cg, dc.from_values(dc.Shape((1, 2)), [1.0, 1.0])), ops.cmult(pe, pe))
+    cg.backward(loss)
+    g1 = p.gradient.data.copy()
+    cg.backward(loss)
+    assert np.allclose(p.gradient.data, 2 * g1)
+    assert np.allclose(g1, [2.0, 4.0])
+
+
+def test_pnls_gradient_known_answer():
+    cg, model = make_ctx()
+    x = ops.input(cg, vec([0.0, 0.0]))
+    loss = ops.pickneglogsoftmax(x, 0)
+    cg.backward(loss)
+    assert np.allclose(cg.value(loss).data, [math.log(2)], atol=1e-6)
+    assert np.allclose(cg.gradient(x).data, [-0.5, 0.5], atol=1e-6)
+
+
+def test_shared_node_sums_both_branches():
+    cg, model = make_ctx()
+    x = ops.input(cg, vec([0.3, -0.7]))
+    t = ops.tanh(x)
+    s = ops.add(t, t)
+    loss = ops.matmul(ops.input(cg, dc.from_values(dc.Shape((1, 2)), [1.0, 1.0])), s)
+    cg.backward(loss)
+    expect = 2 * (1 - np.tanh([0.3, -0.7]) ** 2)
+    assert np.allclose(cg.gradient(x).data, expect, atol=1e-6)
+
+
+def test_pool_exhausted_and_alloc_counts():
+    cg, model = make_ctx(mb=0.01)
+    x = ops.input(cg, vec([1.0] * 1000, 4))
+    with pytest.raises(PoolExhausted):
+        cg.value(ops.tanh(ops.tanh(ops.tanh(x))))
+
+
+def test_forward_alloc_count_100_nodes_one_alias():
+    # acceptance C4 (tests/test_acceptance.py:408-415): +99 allocations for a
+    # 100-node graph whose first node is a parameter alias
+    cg, model = make_ctx()
+    p = model.add_parameters((4,), "p")
+    before = cg.pools.forward.alloc_count
+    e = ops.parameter(cg, p)
+    for _ in range(99):
+        e = ops.tanh(e)
+    cg.value(e)
+    assert cg.pools.forward.alloc_count - before == 99
+    assert cg.forward_calls == 100
+
+
+# -- ops known answers (tests/test_ops.py) ----------------------------------
+
+
+def test_op_known_answers():
+    cg, model = make_ctx()
+    a = ops.input(cg, vec([1.0, 2.0, 3.0, 4.0], 2))
+    b = ops.input(cg, vec([10.0, 10.0]))
+    assert np.allclose(cg.value(ops.add(a, b)).data, [11, 12, 13, 14])
+    A = model.add_parameters((2, 2), "A")
+    A.set_value(np.array([[1.0, 2.0], [3.0, 4.0]]).reshape(-1, order="F"))
+    y = ops.matmul(ops.parameter(cg, A), ops.input(cg, vec([1.0, 1.0])))
+    assert np.allclose(cg.value(y).data, [3, 7])
+    assert np.allclose(cg.value(ops.logistic(ops.input(cg, vec([0.0])))).data, [0.5])
+    assert np.allclose(cg.value(ops.tanh(ops.input(cg, vec([1.0])))).data, [0.7615941559557649], atol=1e-6)
+    sm = ops.softmax(ops.input(cg, vec([1000.0, 1000.0])))
+    assert np.allclose(cg.value(sm).data, [0.5, 0.5])
+    assert cg.value(ops.pickneglogsoftmax(ops.input(cg, vec([50.0, 0.0])), 0)).data[0] < 1e-6
+    s = ops.sum_batches(ops.input(cg, vec([1.0, 2.0, 3.0], 3)))
+    assert np.allclose(cg.value(s).data, [6.0])
+
+
+def test_touched_only_looked_up_rows():
+    cg, model = make_ctx()
+    E = model.add_lookup_parameters(4, 3, "E")
+    x = ops.lookup(cg, E, 1)
+    loss = ops.pickneglogsoftmax(x, 0)
+    cg.backward(loss)
+    assert E.touched == {1}
+    g = E.gradient
+    assert np.all(g[[0, 2, 3]] == 0)
+
+
+def test_touched_includes_non_ancestors_excludes_later():
+    cg, model = make_ctx()
+    E = model.add_lookup_parameters(10, 3, "E")
+    a = ops.lookup(cg, E, 2)
+    ops.lookup(cg, E, 7)  # not an ancestor of the loss, still touched
+    loss = ops.pickneglogsoftmax(a, 1)
+    ops.lookup(cg, E, 9)  # created after the loss: not touched
+    cg.backward(loss)
+    assert E.touched == {2, 7}
+    assert np.all(E.gradient[7] == 0)
+
+
+def test_lookup_batch_repeated_ids_accumulate():
+    cg, model = make_ctx()
+    E = model.add_lookup_parameters(5, 2, "E")
+    x = ops.lookup_batch(cg, E, [3, 1, 3])
+    w = ops.input(cg, vec([1.0, 2.0, 3.0, 4.0, 5.0, 6.0], 3))
+    loss = ops.sum_batches(ops.matmul(ops.input(cg, dc.from_values(dc.Shape((1, 2)), [1.0, 1.0])), ops.cmult(x, w)))
+    cg.backward(loss)
+    g = E.gradient
+    assert np.allclose(g[3], [1.0 + 5.0, 2.0 + 6.0])
+    assert np.allclose(g[1], [3.0, 4.0])
+    assert E.touched == {1, 3}
+
+
+# -- trainers (tests/test_trainers.py), fp32 --------------------------------
+
+
+def one_param_model(theta):
+    cg, model = make_ctx(init_zero=True)
+    p = model.add_parameters((len(theta),), "p")
+    p.set_value(theta)
+    return cg, model, p
+
+
+def test_sgd_step():
+    _, model, p = one_param_model([1.0, 1.0])
+    tr = dc.Trainer(model, "sgd", lr=0.1)
+    p.gradient.data[:] = [0.5, 0.0]
+    tr.update()
+    assert np.allclose(p.values.data, [0.95, 1.0])
+    assert np.all(p.gradient.data == 0)
+
+
+def test_adagrad_step():
+    _, model, p = one_param_model([0.0])
+    tr = dc.Trainer(model, "adagrad", lr=1.0, adagrad_eps=0.0)
+    p.gradient.data[:] = [3.0]
+    tr.update()
+    assert np.allclose(tr.sq[id(p)], [9.0])
+    assert np.allclose(p.values.data, [-1.0])
+
+
+def test_adam_first_step():
+    _, model, p = one_param_model([0.0])
+    tr = dc.Trainer(model, "adam")
+    p.gradient.data[:] = [1.0]
+    tr.update()
+    assert np.isclose(p.values.data[0], -0.000999999995, atol=1e-9)
+    assert tr.t == 1
+
+
+def test_momentum_step():
+    _, model, p = one_param_model([0.0])
+    tr = dc.Trainer(model, "momentum", lr=0.1, momentum=0.9)
+    p.gradient.data[:] = [1.0]
+    tr.update()
+    assert np.allclose(tr.vel[id(p)], [-0.1])
+    assert np.allclose(p.values.data, [-0.1])
+
+
+def test_sgd_half_norm_halves_exactly():
+    cg, model = make_ctx(init_zero=True)
+    p = model.add_parameters((3,), "p")
+    theta0 = np.array([0.7, -1.3, 2.9], dtype=np.float32)
+    p.set_value(theta0)
+    ones_row = dc.from_values(dc.Shape((1, 3)), [1.0, 1.0, 1.0])
+    pe = ops.parameter(cg, p)
+    loss = ops.scalar_mul(ops.matmul(ops.input(cg, ones_row), ops.cmult(pe, pe)), 0.5)
+    cg.backward(loss)
+    assert np.allclose(p.gradient.data, theta0)
+    dc.Trainer(model, "sgd", lr=0.5).update()
+    assert np.array_equal(p.values.data, theta0 * np.float32(0.5))
+
+
+def _train_lookup(rule, sparse, steps):
+    cg, model = make_ctx(seed=4)
+    E = model.add_lookup_parameters(2, 2, "E")
+    tr = dc.Trainer(model, rule, sparse=sparse)
+    for rows in steps:
+        cg.renew()
+        loss = None
+        for row in rows:
+            term = ops.pickneglogsoftmax(ops.lookup(cg, E, row), row % 2)
+            loss = term if loss is None else ops.add(loss, term)
+        cg.backward(loss)
+        tr.update()
+    return E.values.copy()
+
+
+@pytest.mark.parametrize("rule", ["sgd", "adagrad"])
+def test_sparse_dense_equivalence(rule):
+    steps = [(0, 1), (0,), (0, 0, 1), (1,)]
+    assert np.allclose(_train_lookup(rule, False, steps), _train_lookup(rule, True, steps), atol=1e-6)
+
+
+@pytest.mark.parametrize("rule", ["adam", "momentum"])
+def test_sparse_freezes_untouched_rows(rule):
+    steps = [(0, 1), (0,)]
+    after1 = _train_lookup(rule, True, steps[:1])
+    sparse = _train_lookup(rule, True, steps)
+    dense = _train_lookup(rule, False, steps)
+    assert np.array_equal(sparse[1], after1[1])
+    assert not np.array_equal(dense[1], after1[1])
+
+
+def test_update_clears_touched():
+    cg, model = make_ctx()
+    E = model.add_lookup_parameters(3, 2, "E")
+    tr = dc.Trainer(model, "sgd")
+    cg.backward(ops.pickneglogsoftmax(ops.lookup(cg, E, 2), 0))
+    assert E.touched == {2}
+    tr.update()
+    assert E.touched == set()
+    assert np.all(E.gradient == 0)
+
+
+def test_adam_kernel_matches_oracle_on_injected_gradients():
+    """Adam in isolation: identical gradients into both sides, 5 steps."""
+    from oracle import engine as orc
+
+    rng = np.random.default_rng(0)
+    grads = [rng.standard_normal(257).astype(np.float32) for _ in range(5)]
+    _, model, p = one_param_model(np.zeros(257))
+    tr = dc.Trainer(model, "adam")
+    om = orc.Model(orc.new_poolset(), init_zero=True)
+    op = om.add_parameters((257,), "p")
+    otr = orc.Trainer(om, "adam")
+    for g in grads:
+        p.gradient.data[:] = g
+        tr.update()
+        op.gradient[:] = g
+        otr.update()
+    assert np.allclose(p.values.data, op.values, rtol=1e-5, atol=1e-8)
+
+
+# -- persistence (tests/test_params.py) --------------------------------------
+
+
+def test_dyn1_roundtrip(tmp_path):
+    dy, cg, model = gpu_ctx(seed=3, mb=8)
+    W_ = model.add_parameters((3, 4), "W")
+    E = model.add_lookup_parameters(5, 2, "E")
+    tr = dy.Trainer(model, "sgd")
+    loss = ops.pickneglogsoftmax(ops.affine(ops.input(cg, vec([0.0, 0.0, 0.0])), ops.parameter(cg, W_),
+                                            ops.lookup(cg, E, 1) if False else ops.input(cg, vec([1.0, 2.0, 3.0, 4.0]))), 1)
+    cg.backward(loss)
+    tr.update()
+    path = str(tmp_path / "m.dyn")
+    model.save(path)
+    dy2, cg2, m2 = gpu_ctx(seed=99, mb=8)
+    m2.add_parameters((3, 4), "W")
+    m2.add_lookup_parameters(5, 2, "E")
+    m2.load(path)
+    assert np.array_equal(m2.parameters[0].values.data, W_.values.data)
+    assert np.array_equal(m2.lookups[0].values, E.values)
