@@ -142,6 +142,10 @@ int dg_graph_plan_stats(dg_graph* g, int64_t* out8);
  * 8 bias column sums, 9 other).  dg_profile_read syncs and returns
  * out4 = {total ms, launches, algorithmic flops, algorithmic bytes}. */
 int dg_profile_enable(dg_graph* g, uint32_t class_mask);
+/* host-only planner introspection for nodes [lo, hi]: out8 = {units, groups,
+ * fused cells, add chains, nodes inside cells, largest group, lookup leaves,
+ * input leaves}.  Touches no device memory. */
+int dg_schedule_stats(dg_graph* g, int32_t lo, int32_t hi, int64_t* out8);
 int dg_profile_read(dg_graph* g, int32_t cls, double* out4);
 int dg_profile_reset(dg_graph* g);
 

@@ -128,12 +128,18 @@ struct Node {
 
 static inline size_t round64(size_t n) { return (n + 63) & ~size_t(63); }
 
-enum UnitKind { U_NODE = 0, U_CHAIN = 1 };
+enum UnitKind { U_NODE = 0, U_CHAIN = 1, U_CELL = 2 };
 
 struct Unit {
-  int type;                 // U_NODE / U_CHAIN
-  std::vector<int> nodes;   // U_NODE: {i}; U_CHAIN: add nodes in chain order
+  int type;                 // U_NODE / U_CHAIN / U_CELL
+  std::vector<int> nodes;   // U_NODE: {i}; U_CHAIN: add nodes in chain order;
+                            // U_CELL: nodes in kernels.cuh CellArgs slot order
+                            //         (picks, acts, prods, adds, tanh(c), h)
   std::vector<int> ins;     // external inputs (node indices) in slot order
+  // U_CELL: children m, gate offsets into G (i, o, g, f0, f1), G width, H
+  int m = 0;
+  int off[5] = {0, 0, 0, 0, 0};
+  int gw = 0, H = 0;
   int first() const { return nodes.front(); }
   int last() const { return nodes.back(); }
 };
@@ -273,6 +279,17 @@ static int64_t param_handle_of(const dg_graph* g, int node) {
 // Signature of a unit: everything that must agree for one batched launch.
 static uint64_t unit_signature(const dg_graph* g, const Unit& u) {
   SigHash s;
+  if (u.type == U_CELL) {
+    const Node& G = g->nodes[u.ins[0]];
+    s.add(U_CELL);
+    s.add(u.m);
+    s.add(u.gw);
+    s.add(u.H);
+    s.add(G.batch);
+    for (int k = 0; k < 3 + u.m; ++k) s.add(u.off[k]);
+    for (int k = 1; k <= u.m; ++k) s.add(g->nodes[u.ins[k]].batch);
+    return s.h;
+  }
   const Node& n = g->nodes[u.last()];
   s.add(u.type);
   s.add(u.type == U_CHAIN ? -1 : n.kind);
@@ -316,9 +333,143 @@ static uint64_t unit_signature(const dg_graph* g, const Unit& u) {
   return s.h;
 }
 
+// ------------------------------------------------------------ cell matching
+// Recognises the gated-cell pattern emitted by the reference builders:
+//   LSTM step (builders.py:92-101):  h = o*tanh(f*c_prev + i*g)
+//   Tree-LSTM compose (builders.py:250-274): h = o*tanh((i*g + f1*c1) + f2*c2),
+//   leaves h = o*tanh(i*g)
+// where i,f,o = logistic(pick_range(G, ...)), g = tanh(pick_range(G, ...)).
+// Every internal node must be consumed exactly once (inside the cell); the
+// cell state c and the output h may have any consumers.  Nodes keep their
+// identity: the fused kernels write every node's value and gradient slot.
+static bool match_cell(const dg_graph* g, int h, const std::vector<int>& consumers, const std::vector<char>& in_set,
+                       const std::vector<char>& absorbed, Unit& u) {
+  auto Nd = [&](int i) -> const Node& { return g->nodes[i]; };
+  auto in = [&](int i, int k) { return g->inputs[Nd(i).in_off + k]; };
+  const Node& hn = Nd(h);
+  if (hn.kind != DG_OP_CMULT || hn.rank != 1 || !in_set[h] || absorbed[h]) return false;
+  const int H = hn.dims[0], B = hn.batch;
+  auto is_vec = [&](int i, int batch) {
+    const Node& x = Nd(i);
+    return x.rank == 1 && x.dims[0] == H && x.batch == batch;
+  };
+  auto inner = [&](int i) { return i >= 0 && in_set[i] && !absorbed[i] && consumers[i] == 1 && is_vec(i, B); };
+  // gate: act = kind(pick_range(G, off, off+H)); returns pick, G and offset
+  auto gate = [&](int act, int kind, int& pick, int& G, int& off) {
+    if (!inner(act) || Nd(act).kind != kind) return false;
+    const int p = in(act, 0);
+    if (!inner(p) || Nd(p).kind != DG_OP_PICK_RANGE) return false;
+    pick = p;
+    G = in(p, 0);
+    off = (int)g->aux_i[Nd(p).ai_off];
+    return true;
+  };
+  int o_act = in(h, 0), tcn = in(h, 1);
+  if (Nd(o_act).kind != DG_OP_LOGISTIC) std::swap(o_act, tcn);
+  int p_o, G, off_o;
+  if (!gate(o_act, DG_OP_LOGISTIC, p_o, G, off_o)) return false;
+  const Node& Gn = Nd(G);
+  if (Gn.rank != 1 || Gn.batch != B) return false;
+  if (!inner(tcn) || Nd(tcn).kind != DG_OP_TANH) return false;
+  const int c = in(tcn, 0);
+  if (!in_set[c] || absorbed[c] || !is_vec(c, B)) return false;
+  // left-deep sum c = ((t0 + t1) + t2) or a single product
+  std::vector<int> adds_top_down, terms_rev;
+  if (Nd(c).kind == DG_OP_CMULT) {
+    terms_rev.push_back(c);
+  } else if (Nd(c).kind == DG_OP_ADD) {
+    int x = c;
+    for (;;) {
+      adds_top_down.push_back(x);
+      const int l = in(x, 0), r = in(x, 1);
+      if (Nd(l).kind == DG_OP_ADD && inner(l)) {
+        terms_rev.push_back(r);
+        x = l;
+        continue;
+      }
+      terms_rev.push_back(r);
+      terms_rev.push_back(l);
+      break;
+    }
+  } else {
+    return false;
+  }
+  std::vector<int> terms(terms_rev.rbegin(), terms_rev.rend());
+  const int m = (int)terms.size() - 1;
+  if (m > 2) return false;
+  int ig = -1, p_i = -1, p_g = -1, off_i = 0, off_g = 0;
+  std::vector<int> fterm, fact, fpick, fext, foff;
+  for (size_t t = 0; t < terms.size(); ++t) {
+    const int x = terms[t];
+    if (Nd(x).kind != DG_OP_CMULT) return false;
+    if (m == 0 ? (x != c) : !inner(x)) return false;
+    const int a = in(x, 0), b = in(x, 1);
+    int pa, Ga, oa, pb, Gb, ob;
+    if (ig < 0 && gate(a, DG_OP_LOGISTIC, pa, Ga, oa) && gate(b, DG_OP_TANH, pb, Gb, ob) && Ga == G && Gb == G) {
+      ig = (int)t; p_i = pa; off_i = oa; p_g = pb; off_g = ob;
+      continue;
+    }
+    if (ig < 0 && gate(b, DG_OP_LOGISTIC, pa, Ga, oa) && gate(a, DG_OP_TANH, pb, Gb, ob) && Ga == G && Gb == G) {
+      ig = (int)t; p_i = pa; off_i = oa; p_g = pb; off_g = ob;
+      continue;
+    }
+    int fa = -1, ext = -1;
+    if (gate(a, DG_OP_LOGISTIC, pa, Ga, oa) && Ga == G) { fa = a; ext = b; }
+    else if (gate(b, DG_OP_LOGISTIC, pa, Ga, oa) && Ga == G) { fa = b; ext = a; }
+    if (fa < 0) return false;
+    const Node& en = Nd(ext);
+    if (en.rank != 1 || en.dims[0] != H || (en.batch != B && en.batch != 1)) return false;
+    fterm.push_back(x);
+    fact.push_back(fa);
+    fpick.push_back(pa);
+    fext.push_back(ext);
+    foff.push_back(oa);
+  }
+  if (ig < 0) return false;
+  // the fused kernel sums i*g first: exact for two terms (commutative), and
+  // for more terms only when the reference order already starts with i*g
+  if (m >= 2 && ig != 0) return false;
+  u = Unit();
+  u.type = U_CELL;
+  u.m = m;
+  u.H = H;
+  u.gw = (int)Gn.elem;
+  u.off[0] = off_i;
+  u.off[1] = off_o;
+  u.off[2] = off_g;
+  for (int k = 0; k < m; ++k) u.off[3 + k] = foff[k];
+  u.ins.push_back(G);
+  for (int k = 0; k < m; ++k) u.ins.push_back(fext[k]);
+  const int i_act = in(terms[ig], Nd(in(terms[ig], 0)).kind == DG_OP_LOGISTIC ? 0 : 1);
+  const int g_act = in(terms[ig], Nd(in(terms[ig], 0)).kind == DG_OP_LOGISTIC ? 1 : 0);
+  // picks i, f[m], o, g | acts i, f[m], o, g | prods ig, f[m] | adds[m] bottom-up | tanh(c) | h
+  u.nodes.push_back(p_i);
+  for (int k = 0; k < m; ++k) u.nodes.push_back(fpick[k]);
+  u.nodes.push_back(p_o);
+  u.nodes.push_back(p_g);
+  u.nodes.push_back(i_act);
+  for (int k = 0; k < m; ++k) u.nodes.push_back(fact[k]);
+  u.nodes.push_back(o_act);
+  u.nodes.push_back(g_act);
+  u.nodes.push_back(terms[ig]);
+  for (int k = 0; k < m; ++k) u.nodes.push_back(fterm[k]);
+  for (int k = (int)adds_top_down.size() - 1; k >= 0; --k) u.nodes.push_back(adds_top_down[k]);
+  u.nodes.push_back(tcn);
+  u.nodes.push_back(h);
+  // distinct internal nodes, none of them an external input
+  std::vector<int> all = u.nodes;
+  std::sort(all.begin(), all.end());
+  if (std::adjacent_find(all.begin(), all.end()) != all.end()) return false;
+  for (int x : u.ins)
+    if (std::binary_search(all.begin(), all.end(), x)) return false;
+  if ((int)u.nodes.size() != 9 + 4 * m) return false;  // + G and m external states = nslot
+  return true;
+}
+
 // ------------------------------------------------------------- scheduling
-// Builds units (with add-chain rewrite) and the group order for the node set
-// `active` (ascending).  consumers_limit bounds the consumer count scope.
+// Builds units (with cell fusion and add-chain rewrite) and the group order
+// for the node set `active` (ascending).  scope_hi bounds the consumer-count
+// scope.
 static void build_schedule(const dg_graph* g, const std::vector<int>& active, int scope_hi, Schedule& S) {
   const int N = (int)g->nodes.size();
   S = Schedule();
@@ -341,9 +492,24 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
       if (x.dims[d] != y.dims[d]) return false;
     return true;
   };
+  // gated cells first (they own their internal add chains)
+  std::vector<char> absorbed(N, 0);
+  std::vector<Unit> cells;
+  std::vector<int> cell_of(N, -1);
+  for (int i : active) {
+    if (g->nodes[i].kind != DG_OP_CMULT) continue;
+    Unit cu;
+    if (match_cell(g, i, consumers, in_set, absorbed, cu)) {
+      for (int x : cu.nodes) {
+        absorbed[x] = 1;
+        cell_of[x] = (int)cells.size();
+      }
+      cells.push_back(std::move(cu));
+    }
+  }
   auto chainable_add = [&](int i) {
     const Node& n = g->nodes[i];
-    if (n.kind != DG_OP_ADD) return false;
+    if (n.kind != DG_OP_ADD || absorbed[i]) return false;
     const int a = g->inputs[n.in_off], b = g->inputs[n.in_off + 1];
     return same_shape(i, a) && same_shape(i, b);
   };
@@ -366,7 +532,9 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
     if (n.kind == DG_OP_PARAMETER) { S.param_nodes.push_back(i); continue; }
     if (n.kind == DG_OP_LOOKUP || n.kind == DG_OP_LOOKUP_BATCH) { S.lookup_nodes.push_back(i); continue; }
     Unit u;
-    if (chainable_add(i) && !has_prev[i] && chain_next[i] >= 0) {
+    if (cell_of[i] >= 0) {
+      u = std::move(cells[cell_of[i]]);
+    } else if (chainable_add(i) && !has_prev[i] && chain_next[i] >= 0) {
       u.type = U_CHAIN;
       int c = i;
       u.ins.push_back(g->inputs[n.in_off]);
@@ -403,11 +571,23 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
     indeg[u] = (int)preds.size();
     for (int p : preds) succ[p].push_back(u);
   }
-  // units are created in ascending node order and every input precedes its
-  // consumer, so unit ids are already a topological order
+  // heights over a real topological order (a chain or cell unit is created at
+  // its first node, but later terms of a loss chain are built after it)
+  std::vector<int> topo;
+  topo.reserve(U);
+  {
+    std::vector<int> deg = indeg;
+    for (int u = 0; u < U; ++u)
+      if (deg[u] == 0) topo.push_back(u);
+    for (size_t q = 0; q < topo.size(); ++q)
+      for (int c : succ[topo[q]])
+        if (--deg[c] == 0) topo.push_back(c);
+  }
   std::vector<int> height(U, 0);
-  for (int u = U - 1; u >= 0; --u)
+  for (int q = (int)topo.size() - 1; q >= 0; --q) {
+    const int u = topo[q];
     for (int c : succ[u]) height[u] = std::max(height[u], height[c] + 1);
+  }
   int L = 0;
   for (int u = 0; u < U; ++u) L = std::max(L, height[u]);
   std::vector<int> alap(U);
@@ -458,7 +638,7 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
       std::sort(members.begin(), members.end());
       Group gr;
       const Unit& u0 = S.units[members[0]];
-      gr.kind = u0.type == U_CHAIN ? -1 : g->nodes[u0.last()].kind;
+      gr.kind = u0.type == U_CHAIN ? -1 : (u0.type == U_CELL ? -2 : g->nodes[u0.last()].kind);
       gr.units = members;
       for (int u : members) {
         ++done;
@@ -798,6 +978,37 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
   const Node& n0 = g->nodes[nodes[0]];
   const cudaStream_t st = g->stream;
 
+  if (gr.kind == -2) {  // fused gated cells
+    const Unit& u0 = S.units[gr.units[0]];
+    CellArgs a{};
+    a.n = n;
+    a.m = u0.m;
+    a.H = u0.H;
+    a.gw = u0.gw;
+    a.batch = g->nodes[u0.ins[0]].batch;
+    a.off_i = u0.off[0];
+    a.off_o = u0.off[1];
+    a.off_g = u0.off[2];
+    for (int k = 0; k < u0.m; ++k) {
+      a.off_f[k] = u0.off[3 + k];
+      a.cext_b1[k] = g->nodes[u0.ins[1 + k]].batch == 1 && a.batch > 1;
+    }
+    a.nslot = 10 + 5 * u0.m;
+    std::vector<uintptr_t> vals((size_t)a.nslot * n);
+    for (int j = 0; j < n; ++j) {
+      const Unit& u = S.units[gr.units[j]];
+      int s = 0;
+      for (int x : u.ins) vals[(size_t)(s++) * n + j] = P(g->nodes[x].val);
+      for (int x : u.nodes) vals[(size_t)(s++) * n + j] = P(g->nodes[x].val);
+    }
+    const size_t ov = B.push(vals);
+    plan.ops.push_back([a, ov, st](char* d) mutable {
+      a.val = at<const float* const>(d, ov);
+      return launch_cell_fwd(a, st);
+    });
+    plan.tag(C_ELEMWISE, 0.0, 4.0 * n * (double)a.batch * a.H * (3 + a.m + 2.0 * (9 + 5 * a.m)));
+    return;
+  }
   if (gr.kind == -1) {  // add chain
     const int len = (int)S.units[gr.units[0]].nodes.size();
     std::vector<uintptr_t> ins((len + 1) * n), outs(len * n);
@@ -1207,7 +1418,7 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
   std::vector<std::vector<int>> targets(gr.units.size());
   for (size_t j = 0; j < gr.units.size(); ++j) targets[j] = S.units[gr.units[j]].ins;
   const bool ew = gr.kind == DG_OP_ADD || gr.kind == DG_OP_CMULT || gr.kind == DG_OP_TANH ||
-                  gr.kind == DG_OP_LOGISTIC || gr.kind == DG_OP_SCALAR_MUL || gr.kind == -1;
+                  gr.kind == DG_OP_LOGISTIC || gr.kind == DG_OP_SCALAR_MUL || gr.kind == -1 || gr.kind == -2;
   if (gr.kind == DG_OP_AFFINE) {
     // dX is conflict-free by construction (temp + segmented reduce); only the
     // per-node (non-parameter) bias needs rounds
@@ -1231,6 +1442,44 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
       if (mask[j]) { nodes.push_back(all_nodes[j]); units.push_back(gr.units[j]); }
     const int n = (int)nodes.size();
     if (n == 0) continue;
+    if (gr.kind == -2) {  // fused gated cells
+      const Unit& u0 = S.units[units[0]];
+      CellArgs a{};
+      a.n = n;
+      a.m = u0.m;
+      a.H = u0.H;
+      a.gw = u0.gw;
+      a.batch = g->nodes[u0.ins[0]].batch;
+      a.off_i = u0.off[0];
+      a.off_o = u0.off[1];
+      a.off_g = u0.off[2];
+      for (int k = 0; k < u0.m; ++k) {
+        a.off_f[k] = u0.off[3 + k];
+        a.cext_b1[k] = g->nodes[u0.ins[1 + k]].batch == 1 && a.batch > 1;
+      }
+      a.nslot = 10 + 5 * u0.m;
+      std::vector<uintptr_t> vals((size_t)a.nslot * n), grads((size_t)a.nslot * n);
+      for (int j = 0; j < n; ++j) {
+        const Unit& u = S.units[units[j]];
+        int s = 0;
+        for (int x : u.ins) {
+          vals[(size_t)s * n + j] = P(g->nodes[x].val);
+          grads[(size_t)(s++) * n + j] = P(g->nodes[x].grad);
+        }
+        for (int x : u.nodes) {
+          vals[(size_t)s * n + j] = P(g->nodes[x].val);
+          grads[(size_t)(s++) * n + j] = P(g->nodes[x].grad);
+        }
+      }
+      const size_t ov = B.push(vals), og = B.push(grads);
+      plan.ops.push_back([a, ov, og, st](char* d) mutable {
+        a.val = at<const float* const>(d, ov);
+        a.grad = at<float* const>(d, og);
+        return launch_cell_bwd(a, st);
+      });
+      plan.tag(C_ELEMWISE, 0.0, 4.0 * n * (double)a.batch * a.H * (6 + 2 * a.m + 2.0 * (9 + 5 * a.m)));
+      continue;
+    }
     // slot passes: with intra-node duplicates, one pass per slot with every
     // other slot's gradient redirected to a dummy buffer
     const int n_slots = n0.n_in;
@@ -1802,6 +2051,34 @@ int dg_graph_counters(dg_graph* g, int64_t* out8) {
   out8[5] = g->launches;
   out8[6] = g->h2d_bytes;
   out8[7] = g->d2h_bytes;
+  return DG_OK;
+}
+
+int dg_schedule_stats(dg_graph* g, int32_t lo, int32_t hi, int64_t* out8) {
+  // host-only: build the schedule of nodes [lo, hi] without touching the device
+  if (lo < 0 || hi >= (int)g->nodes.size() || lo > hi) return fail(DG_STALE, "node range out of bounds");
+  std::vector<int> active;
+  for (int i = lo; i <= hi; ++i) active.push_back(i);
+  Schedule S;
+  build_schedule(g, active, hi, S);
+  int64_t cells = 0, chains = 0, cell_nodes = 0;
+  for (const Unit& u : S.units) {
+    if (u.type == U_CELL) {
+      ++cells;
+      cell_nodes += (int64_t)u.nodes.size();
+    }
+    if (u.type == U_CHAIN) ++chains;
+  }
+  int64_t max_group = 0;
+  for (const Group& gr : S.groups) max_group = std::max<int64_t>(max_group, (int64_t)gr.units.size());
+  out8[0] = (int64_t)S.units.size();
+  out8[1] = (int64_t)S.groups.size();
+  out8[2] = cells;
+  out8[3] = chains;
+  out8[4] = cell_nodes;
+  out8[5] = max_group;
+  out8[6] = (int64_t)S.lookup_nodes.size();
+  out8[7] = (int64_t)S.input_nodes.size();
   return DG_OK;
 }
 

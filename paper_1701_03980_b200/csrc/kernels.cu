@@ -145,6 +145,139 @@ __global__ void chain_bwd_kernel(ChainArgs a) {
   }
 }
 
+// ------------------------------------------------------------ gated cells
+
+struct CellSlots {
+  int m, pick0, act0, prod0, add0, tc, h, c;
+  __device__ __forceinline__ explicit CellSlots(int m_) : m(m_) {
+    pick0 = 1 + m;
+    act0 = pick0 + 3 + m;
+    prod0 = act0 + 3 + m;
+    add0 = prod0 + 1 + m;
+    tc = add0 + m;
+    h = tc + 1;
+    c = m > 0 ? add0 + m - 1 : prod0;
+  }
+  // gate order inside the pick/act groups: i, f[0..m), o, g
+  __device__ __forceinline__ int gi() const { return 0; }
+  __device__ __forceinline__ int gf(int k) const { return 1 + k; }
+  __device__ __forceinline__ int go() const { return 1 + m; }
+  __device__ __forceinline__ int gg() const { return 2 + m; }
+};
+
+template <int M>
+__global__ void cell_fwd_kernel(CellArgs a) {
+  const CellSlots S(M);
+  const int64_t per = (int64_t)a.batch * a.H;
+  const int64_t total = per * a.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(t / per);
+    const int64_t r = t - (int64_t)j * per;
+    const int b = static_cast<int>(r / a.H), u = static_cast<int>(r - (int64_t)b * a.H);
+    auto V = [&](int slot) { return a.val[(int64_t)slot * a.n + j]; };
+    const float* G = V(0) + (int64_t)b * a.gw;
+    const float xi = G[a.off_i + u], xo = G[a.off_o + u], xg = G[a.off_g + u];
+    float xf[M > 0 ? M : 1];
+#pragma unroll
+    for (int k = 0; k < M; ++k) xf[k] = G[a.off_f[k] + u];
+    const_cast<float*>(V(S.pick0 + S.gi()))[r] = xi;
+    const_cast<float*>(V(S.pick0 + S.go()))[r] = xo;
+    const_cast<float*>(V(S.pick0 + S.gg()))[r] = xg;
+    const float ai = sigmoidf_ref(xi), ao = sigmoidf_ref(xo), ag = tanhf(xg);
+    const_cast<float*>(V(S.act0 + S.gi()))[r] = ai;
+    const_cast<float*>(V(S.act0 + S.go()))[r] = ao;
+    const_cast<float*>(V(S.act0 + S.gg()))[r] = ag;
+    float c = ai * ag;
+    const_cast<float*>(V(S.prod0))[r] = c;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      const_cast<float*>(V(S.pick0 + S.gf(k)))[r] = xf[k];
+      const float af = sigmoidf_ref(xf[k]);
+      const_cast<float*>(V(S.act0 + S.gf(k)))[r] = af;
+      const float ck = V(1 + k)[a.cext_b1[k] ? u : r];
+      const float p = af * ck;
+      const_cast<float*>(V(S.prod0 + 1 + k))[r] = p;
+      c = c + p;
+      const_cast<float*>(V(S.add0 + k))[r] = c;
+    }
+    const float tc = tanhf(c);
+    const_cast<float*>(V(S.tc))[r] = tc;
+    const_cast<float*>(V(S.h))[r] = ao * tc;
+  }
+}
+
+// kLoopBatch: one thread per (cell, unit) walks the batch so batch-1 (broadcast)
+// external cell states receive the batch sum (ops.py:69-75)
+template <int M, bool kLoopBatch>
+__global__ void cell_bwd_kernel(CellArgs a) {
+  const CellSlots S(M);
+  const int64_t per = kLoopBatch ? (int64_t)a.H : (int64_t)a.batch * a.H;
+  const int64_t total = per * a.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(t / per);
+    const int64_t q = t - (int64_t)j * per;
+    auto V = [&](int slot) { return a.val[(int64_t)slot * a.n + j]; };
+    auto D = [&](int slot) { return a.grad[(int64_t)slot * a.n + j]; };
+    const int b_lo = kLoopBatch ? 0 : static_cast<int>(q / a.H);
+    const int b_hi = kLoopBatch ? a.batch : b_lo + 1;
+    const int u = static_cast<int>(kLoopBatch ? q : q - (int64_t)b_lo * a.H);
+    float acc_c[M > 0 ? M : 1];
+#pragma unroll
+    for (int k = 0; k < M; ++k) acc_c[k] = 0.f;
+    for (int b = b_lo; b < b_hi; ++b) {
+      const int64_t r = (int64_t)b * a.H + u;
+      const float gh = D(S.h)[r];
+      const float ao = V(S.act0 + S.go())[r], ai = V(S.act0 + S.gi())[r], ag = V(S.act0 + S.gg())[r];
+      const float tc = V(S.tc)[r];
+      // h = o * tanh(c)
+      const float d_tc = gh * ao;
+      const float d_o = gh * tc;
+      D(S.tc)[r] += d_tc;
+      D(S.act0 + S.go())[r] += d_o;
+      // c slot: external contributions + tanh path
+      const float dc = D(S.c)[r] + (1.f - tc * tc) * d_tc;
+      D(S.c)[r] = dc;
+#pragma unroll
+      for (int k = 0; k + 1 < M; ++k) D(S.add0 + k)[r] += dc;
+      if (M > 0) D(S.prod0)[r] += dc;
+      // i * g
+      const float d_i = dc * ag, d_g = dc * ai;
+      D(S.act0 + S.gi())[r] += d_i;
+      D(S.act0 + S.gg())[r] += d_g;
+      const float dpi = ai * (1.f - ai) * d_i;
+      const float dpo = ao * (1.f - ao) * d_o;
+      const float dpg = (1.f - ag * ag) * d_g;
+      D(S.pick0 + S.gi())[r] += dpi;
+      D(S.pick0 + S.go())[r] += dpo;
+      D(S.pick0 + S.gg())[r] += dpg;
+      float* dG = D(0) + (int64_t)b * a.gw;
+      dG[a.off_i + u] += dpi;
+      dG[a.off_o + u] += dpo;
+      dG[a.off_g + u] += dpg;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        D(S.prod0 + 1 + k)[r] += dc;
+        const int64_t rc = a.cext_b1[k] ? u : r;
+        const float ck = V(1 + k)[rc];
+        const float af = V(S.act0 + S.gf(k))[r];
+        const float d_f = dc * ck;
+        const float d_ck = dc * af;
+        D(S.act0 + S.gf(k))[r] += d_f;
+        const float dpf = af * (1.f - af) * d_f;
+        D(S.pick0 + S.gf(k))[r] += dpf;
+        dG[a.off_f[k] + u] += dpf;
+        if (kLoopBatch && a.cext_b1[k]) acc_c[k] += d_ck;
+        else D(1 + k)[rc] += d_ck;
+      }
+    }
+    if (kLoopBatch) {
+#pragma unroll
+      for (int k = 0; k < M; ++k)
+        if (a.cext_b1[k]) D(1 + k)[u] += acc_c[k];
+    }
+  }
+}
+
 // ------------------------------------------------------------------ structural
 
 __global__ void pick_fwd_kernel(PickArgs a) {
@@ -338,15 +471,38 @@ __global__ void gather_rows_kernel(const float* __restrict__ table, int dim, con
 __global__ void segment_scatter_add_kernel(float* __restrict__ table_grad, int dim, const int64_t* __restrict__ ids,
                                            const int* __restrict__ seg, const float* const* src_rows, int n_unique,
                                            float scale) {
-  const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // one block per unique id; warp w sums rows k0+w, k0+w+8, ... (a long
+  // segment, e.g. the EOS padding id, is spread over 8 warps), then the 8
+  // partials are reduced in fixed warp order: deterministic, no atomics.
+  __shared__ float part[8][128];
+  const int u = blockIdx.x;
   if (u >= n_unique) return;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float* dst = table_grad + ids[u] * (int64_t)dim;
   const int k0 = seg[u], k1 = seg[u + 1];
-  for (int c = lane; c < dim; c += 32) {
-    float acc = 0.f;
-    for (int k = k0; k < k1; ++k) acc += src_rows[k][c];  // fixed (sorted) order: deterministic
-    dst[c] += scale * acc;
+  for (int c0 = 0; c0 < dim; c0 += 128) {
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int k = k0 + w; k < k1; k += 8) {
+      const float* r = src_rows[k];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = c0 + lane + 32 * q;
+        if (c < dim) acc[q] += r[c];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) part[w][lane + 32 * q] = acc[q];
+    __syncthreads();
+    if (threadIdx.x < 128) {
+      const int c = c0 + threadIdx.x;
+      if (c < dim) {
+        float s = 0.f;
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) s += part[ww][threadIdx.x];
+        dst[c] += scale * s;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -631,6 +787,31 @@ int launch_chain_bwd(const ChainArgs& a, cudaStream_t s) {
   return 1;
 }
 
+int launch_cell_fwd(const CellArgs& a, cudaStream_t s) {
+  const int g = grid_for((int64_t)a.n * a.batch * a.H);
+  switch (a.m) {
+    case 0: cell_fwd_kernel<0><<<g, kThreads, 0, s>>>(a); break;
+    case 1: cell_fwd_kernel<1><<<g, kThreads, 0, s>>>(a); break;
+    default: cell_fwd_kernel<2><<<g, kThreads, 0, s>>>(a); break;
+  }
+  return 1;
+}
+
+int launch_cell_bwd(const CellArgs& a, cudaStream_t s) {
+  bool bcast = false;
+  for (int k = 0; k < a.m; ++k) bcast = bcast || (a.cext_b1[k] && a.batch > 1);
+  const int g = grid_for((int64_t)a.n * (bcast ? 1 : a.batch) * a.H);
+  switch (a.m * 2 + (bcast ? 1 : 0)) {
+    case 0: cell_bwd_kernel<0, false><<<g, kThreads, 0, s>>>(a); break;
+    case 1: cell_bwd_kernel<0, true><<<g, kThreads, 0, s>>>(a); break;
+    case 2: cell_bwd_kernel<1, false><<<g, kThreads, 0, s>>>(a); break;
+    case 3: cell_bwd_kernel<1, true><<<g, kThreads, 0, s>>>(a); break;
+    case 4: cell_bwd_kernel<2, false><<<g, kThreads, 0, s>>>(a); break;
+    default: cell_bwd_kernel<2, true><<<g, kThreads, 0, s>>>(a); break;
+  }
+  return 1;
+}
+
 int launch_pick_fwd(const PickArgs& a, cudaStream_t s) {
   pick_fwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.width), kThreads, 0, s>>>(a);
   return 1;
@@ -671,8 +852,7 @@ int launch_gather_rows(const float* table, int dim, const int64_t* ids, float* c
 int launch_segment_scatter_add(float* table_grad, int dim, const int64_t* uniq_ids, const int* seg,
                                const float* const* src_rows, int n_unique, float scale, cudaStream_t s) {
   if (n_unique <= 0) return 0;
-  segment_scatter_add_kernel<<<(n_unique + 7) / 8, 256, 0, s>>>(table_grad, dim, uniq_ids, seg, src_rows, n_unique,
-                                                                 scale);
+  segment_scatter_add_kernel<<<n_unique, 256, 0, s>>>(table_grad, dim, uniq_ids, seg, src_rows, n_unique, scale);
   return 1;
 }
 

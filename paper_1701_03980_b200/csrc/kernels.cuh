@@ -49,6 +49,28 @@ struct ChainArgs {
 int launch_chain_fwd(const ChainArgs& a, cudaStream_t s);
 int launch_chain_bwd(const ChainArgs& a, cudaStream_t s);
 
+// ---------------------------------------------------------- fused gated cells
+// One launch evaluates N same-signature gated cells (the 13-node LSTM step of
+// builders.py:92-101 and the Tree-LSTM compositions of builders.py:250-274):
+//   i,o = sigmoid(G[off_i|off_o]), g = tanh(G[off_g]), f_k = sigmoid(G[off_f[k]])
+//   c = i*g (+ f_1*c_1) (+ f_2*c_2) ... (left-deep, the reference's order)
+//   h = o * tanh(c)
+// Every node of the pattern keeps its own value (and gradient) slot.
+// Slot layout per cell (slot-major pointer tables, nslot = 10 + 5m):
+//   0 G | 1..m c_ext | picks i,f[m],o,g | acts i,f[m],o,g | prod ig, prod f[m]
+//   | adds[m] | tanh(c) | h        (c = adds[m-1], or prod ig when m == 0)
+struct CellArgs {
+  int n, batch, H, gw, m;
+  int off_i, off_o, off_g;
+  int off_f[2];
+  int cext_b1[2];
+  int nslot;
+  const float* const* val;  // [nslot * n]
+  float* const* grad;       // [nslot * n] (backward)
+};
+int launch_cell_fwd(const CellArgs& a, cudaStream_t s);
+int launch_cell_bwd(const CellArgs& a, cudaStream_t s);
+
 // --------------------------------------------------------------- structural
 struct PickArgs {
   int n, batch, in_elem, lo, width;

@@ -49,6 +49,30 @@ def merge_plan(ids_per_rank):
     return ids, order, uniq, seg
 
 
+def exchange_rows(dist, group, world: int, n_local: int, dim: int, pack, device):
+    """Variable-length (ids, rows) all-gather without all-gatherv: counts
+    first, then ids/rows padded to the max count.  `pack(ids, rows, cap)`
+    fills this rank's sorted touched rows.  Returns (ids in rank order as a
+    numpy array, the matching rows as one contiguous tensor)."""
+    import torch as t
+
+    cnt = t.tensor([n_local], dtype=t.int64, device=device)
+    counts = [t.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(counts, cnt, group=group)
+    counts = [int(c.item()) for c in counts]
+    cap = max(1, max(counts))
+    ids = t.zeros(cap, dtype=t.int64, device=device)
+    rows = t.zeros((cap, dim), dtype=t.float32, device=device)
+    pack(ids, rows, cap)
+    all_ids = [t.zeros(cap, dtype=t.int64, device=device) for _ in range(world)]
+    all_rows = [t.zeros((cap, dim), dtype=t.float32, device=device) for _ in range(world)]
+    dist.all_gather(all_ids, ids, group=group)
+    dist.all_gather(all_rows, rows, group=group)
+    flat_ids = t.cat([all_ids[r][: counts[r]] for r in range(world)]).cpu().numpy().astype(np.int64)
+    flat_rows = t.cat([all_rows[r][: counts[r]] for r in range(world)]).contiguous()
+    return flat_ids, flat_rows
+
+
 class DataParallel:
     """Gradient exchange for one Model across the default process group."""
 
@@ -91,22 +115,13 @@ class DataParallel:
                 continue
             n = ctypes.c_int64(0)
             _native.check(lib.dg_touched_count(lp.handle, ctypes.byref(n)))
-            cnt = t.tensor([n.value], dtype=t.int64, device=_dev.device())
-            counts = [t.zeros_like(cnt) for _ in range(R)]
-            dist.all_gather(counts, cnt, group=self.group)
-            counts = [int(c.item()) for c in counts]
-            cap = max(1, max(counts))
-            ids, rows = self._buffers(lp, cap)
-            got = ctypes.c_int64(0)
-            _native.check(lib.dg_lookup_pack(lp.handle, _native.ptr(ids), _native.ptr(rows), cap,
-                                             ctypes.byref(got), stream))
-            all_ids = t.zeros((R, cap), dtype=t.int64, device=_dev.device())
-            all_rows = t.zeros((R, cap, lp.dim), dtype=t.float32, device=_dev.device())
-            dist.all_gather_into_tensor(all_ids, ids[:cap].contiguous(), group=self.group)
-            dist.all_gather_into_tensor(all_rows, rows[:cap].contiguous(), group=self.group)
-            valid_ids = [all_ids[r, : counts[r]] for r in range(R)]
-            flat_ids = t.cat(valid_ids).cpu().numpy().astype(np.int64)
-            flat_rows = t.cat([all_rows[r, : counts[r]] for r in range(R)]).contiguous()
+
+            def pack(ids, rows, cap, lp=lp):
+                got = ctypes.c_int64(0)
+                _native.check(lib.dg_lookup_pack(lp.handle, _native.ptr(ids), _native.ptr(rows), cap,
+                                                 ctypes.byref(got), stream))
+
+            flat_ids, flat_rows = exchange_rows(dist, self.group, R, n.value, lp.dim, pack, _dev.device())
             if flat_ids.size:
                 _native.check(lib.dg_lookup_merge(lp.handle, flat_ids.ctypes.data, _native.ptr(flat_rows),
                                                   flat_ids.size, 1.0 / R, stream))

@@ -27,8 +27,12 @@ def test_op_cases_match_reference(name):
     cg.backward(loss)
     parity(cg.value(loss).data, OPS[f"{name}/loss"], what="loss")
     parity(cg.value(out).data, OPS[f"{name}/value"], what="value")
+    # softmax backward is y * (g - <g, y>): with a dominant class g_c ~ <g, y>
+    # cancels, so 1-ulp differences of expf vs numpy exp show up at ~1e-5 of
+    # the gradient scale; that case gets a 1e-5 atol floor
+    floor = 1e-5 if name == "softmax" else 1e-6
     for k, e in enumerate(ins):
-        parity(cg.gradient(e).data, OPS[f"{name}/grad{k}"], what=f"grad{k}")
+        parity(cg.gradient(e).data, OPS[f"{name}/grad{k}"], atol_frac=floor, what=f"grad{k}")
     for p in model.parameters:
         parity(pgrad(p), OPS[f"{name}/pgrad/{p.name}"], what=p.name)
     for lp in model.lookups:
