@@ -145,8 +145,9 @@ struct Unit {
 };
 
 struct Group {
-  int kind;                 // node kind, or -1 for chains
+  int kind;                 // node kind, -1 add chain, -2 gated cell
   std::vector<int> units;   // unit ids, ascending
+  int level = 0;            // scheduling level (groups of one level are independent)
 };
 
 struct Schedule {
@@ -645,6 +646,7 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
         for (int c : succ[u])
           if (--indeg[c] == 0) newly.push_back(c);
       }
+      gr.level = level;
       S.groups.push_back(std::move(gr));
     }
     for (int c : newly) add_ready(c);
@@ -741,6 +743,71 @@ static std::vector<std::vector<char>> conflict_rounds(const std::vector<std::vec
   return rounds;
 }
 
+// workspace layout: [0, W/2) table blob | [W/2, W-17MiB) scratch (split-K
+// partials, dX temporaries, column-sum partials) | 16 MiB dummy gradient
+// target | 1 MiB zeroed split-K tile counters
+static constexpr size_t kDummyBytes = 16u << 20;
+static constexpr size_t kCounterBytes = 1u << 20;
+static inline char* scratch_base(dg_graph* g) { return g->work_base + g->work_bytes / 2; }
+static inline size_t scratch_bytes(dg_graph* g) { return g->work_bytes / 2 - kDummyBytes - kCounterBytes; }
+static inline float* dummy_base(dg_graph* g) {
+  return reinterpret_cast<float*>(g->work_base + g->work_bytes - kDummyBytes - kCounterBytes);
+}
+static inline int* counter_base(dg_graph* g) {
+  return reinterpret_cast<int*>(g->work_base + g->work_bytes - kCounterBytes);
+}
+static constexpr int kCounterCap = (int)(kCounterBytes / 4);
+
+// Same-level affine problems accumulate into one grouped GEMM launch.
+struct GemmBatch {
+  int level = -1;
+  int cls = 0;
+  bool a_kmajor = false, b_nmajor = false;
+  std::vector<GemmProblem> probs;
+  int64_t temp_floats = 0;  // dX temporaries at the head of the scratch region
+  std::vector<std::function<int()>> post;
+  double bytes = 0;
+  std::vector<int> targets;  // nodes written with += (dX): must be disjoint per launch
+};
+
+template <class T>
+static inline const T* dev_at(dg_graph* g, size_t off) {
+  return reinterpret_cast<const T*>(g->work_base + off);
+}
+
+static void flush_gemm(dg_graph* g, Plan& plan, GemmBatch& gb) {
+  if (gb.probs.empty()) {
+    gb = GemmBatch();
+    return;
+  }
+  const int64_t temp = (gb.temp_floats + 63) & ~int64_t(63);
+  float* work = reinterpret_cast<float*>(scratch_base(g)) + temp;
+  const int64_t cap = (int64_t)(scratch_bytes(g) / 4) - temp;
+  GemmLaunch L = gemm_plan(gb.probs, gb.a_kmajor, gb.b_nmajor, cap, kCounterCap);
+  const size_t off = plan.blob.push(gb.probs);
+  const GemmProblem* pdev = dev_at<GemmProblem>(g, off);
+  int* counters = counter_base(g);
+  cudaStream_t st = g->stream;
+  auto post = std::move(gb.post);
+  plan.ops.push_back([L, pdev, work, counters, st, post](char*) {
+    int n = launch_gemm_group(L, pdev, work, counters, st);
+    for (auto& f : post) n += f();
+    return n;
+  });
+  plan.tag(gb.cls, L.flops, gb.bytes);
+  gb = GemmBatch();
+}
+
+static GemmBatch& gemm_batch_for(dg_graph* g, Plan& plan, GemmBatch& gb, int level, int cls, bool ak, bool bn) {
+  if (!gb.probs.empty() && (gb.level != level || gb.cls != cls || gb.a_kmajor != ak || gb.b_nmajor != bn))
+    flush_gemm(g, plan, gb);
+  gb.level = level;
+  gb.cls = cls;
+  gb.a_kmajor = ak;
+  gb.b_nmajor = bn;
+  return gb;
+}
+
 }  // namespace dg
 
 using namespace dg;
@@ -835,6 +902,16 @@ int dg_graph_create(int device, void* fwd_base, size_t fwd_bytes, void* bwd_base
   g->bwd_bytes = bwd_bytes;
   g->work_base = static_cast<char*>(work_base);
   g->work_bytes = work_bytes;
+  if (work_bytes < (64u << 20)) {
+    delete g;
+    return fail(DG_CONFIG, "workspace must be at least 64 MiB");
+  }
+  // split-K tile counters start (and are always left) at zero
+  cudaError_t e = cudaMemset(g->work_base + work_bytes - kCounterBytes, 0, kCounterBytes);
+  if (e != cudaSuccess) {
+    delete g;
+    return fail(DG_CUDA, std::string("workspace init: ") + cudaGetErrorString(e));
+  }
   *out = g;
   return DG_OK;
 }
@@ -955,8 +1032,6 @@ static int launch_plan(dg_graph* g, Plan& plan) {
 }
 
 // scratch region of the workspace (after the table blob half)
-static inline char* scratch_base(dg_graph* g) { return g->work_base + g->work_bytes / 2; }
-static inline size_t scratch_bytes(dg_graph* g) { return g->work_bytes / 2; }
 
 static int ew_kind_of(int kind) {
   switch (kind) {
@@ -970,13 +1045,26 @@ static int ew_kind_of(int kind) {
 }
 
 // forward launches for one group; node values are already placed
-static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, Plan& plan) {
+// affine groups whose W operands are all (batch-1) parameters run on the
+// shared-weight GEMM; anything else takes the generic per-node kernel
+static bool affine_gemm_ok(const dg_graph* g, const Node& n0) {
+  const int terms = (n0.n_in - 1) / 2;
+  if (terms > 4) return false;
+  for (int k = 0; k < terms; ++k) {
+    const Node& w = g->nodes[g->inputs[n0.in_off + 1 + 2 * k]];
+    if (w.kind != DG_OP_PARAMETER || w.batch != 1) return false;
+  }
+  return true;
+}
+
+static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, Plan& plan, GemmBatch& gb) {
   Blob& B = plan.blob;
   std::vector<int> nodes;
   for (int u : gr.units) nodes.push_back(S.units[u].last());
   const int n = (int)nodes.size();
   const Node& n0 = g->nodes[nodes[0]];
   const cudaStream_t st = g->stream;
+  if (!(gr.kind == DG_OP_AFFINE && affine_gemm_ok(g, n0))) flush_gemm(g, plan, gb);
 
   if (gr.kind == -2) {  // fused gated cells
     const Unit& u0 = S.units[gr.units[0]];
@@ -1173,22 +1261,16 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
       const int terms = (n0.n_in - 1) / 2;
       const int m = (int)n0.elem;
       const int Bt = n0.batch;
-      bool gemm = terms <= 4;
-      for (int k = 0; k < terms; ++k) {
-        const int w = g->inputs[n0.in_off + 1 + 2 * k];
-        if (g->nodes[w].kind != DG_OP_PARAMETER || g->nodes[w].batch != 1) gemm = false;
-      }
+      const bool gemm = affine_gemm_ok(g, n0);
       const Node& b0 = g->nodes[g->inputs[n0.in_off]];
       if (gemm) {
-        GemmArgs a{};
-        a.M = n * Bt;
-        a.N = m;
-        a.n_seg = terms;
-        a.a_kmajor = false;
-        a.b_nmajor = false;
-        a.accumulate = false;
-        std::vector<size_t> xoffs(terms);
-        bool a_al = true;
+        GemmBatch& batch = gemm_batch_for(g, plan, gb, gr.level, C_GEMM_FWD, false, false);
+        GemmProblem pr{};
+        pr.M = n * Bt;
+        pr.N = m;
+        pr.n_seg = terms;
+        pr.accumulate = 0;
+        double kk = 0;
         for (int k = 0; k < terms; ++k) {
           const Node& xk0 = g->nodes[g->inputs[n0.in_off + 2 + 2 * k]];
           const int K = (int)xk0.elem;
@@ -1198,33 +1280,24 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
             const float* xv = g->nodes[g->inputs[g->nodes[nodes[j]].in_off + 2 + 2 * k]].val;
             for (int b = 0; b < Bt; ++b) rows[(size_t)j * Bt + b] = P(xv + (xb1 ? 0 : (int64_t)b * K));
           }
-          a_al = a_al && all_aligned16(rows);
-          xoffs[k] = B.push(rows);
-          a.seg[k].K = K;
-          const float* W = g->nodes[g->inputs[n0.in_off + 1 + 2 * k]].val;
-          a.seg[k].B.base = W;  // column-major m x K == row-major K x m (W^T)
-          a.seg[k].B.ld = m;
-          a.seg[k].B.rows = nullptr;
+          pr.seg[k].K = K;
+          pr.seg[k].A.rows = dev_at<const float*>(g, B.push(rows));
+          pr.seg[k].A.rows_aligned = all_aligned16(rows);
+          // W column-major m x K == row-major K x m (W^T): B(k, n) = W[n + k*m]
+          pr.seg[k].B.base = g->nodes[g->inputs[n0.in_off + 1 + 2 * k]].val;
+          pr.seg[k].B.ld = m;
+          kk += K;
         }
-        a.a_rows_aligned = a_al;
-        a.b_rows_aligned = true;
         std::vector<uintptr_t> crow((size_t)n * Bt);
         for (int j = 0; j < n; ++j)
           for (int b = 0; b < Bt; ++b) crow[(size_t)j * Bt + b] = P(g->nodes[nodes[j]].val + (int64_t)b * m);
-        const size_t oc = B.push(crow);
-        size_t obias = 0;
-        const bool bias_param = b0.kind == DG_OP_PARAMETER;
-        // a bias node shared by every group member with batch 1 -> base/ld 0
-        bool shared_bias = true;
-        for (int j = 0; j < n; ++j)
-          if (g->inputs[g->nodes[nodes[j]].in_off] != g->inputs[n0.in_off]) shared_bias = false;
-        if (bias_param && !shared_bias) {
-          // same parameter through different nodes: still the same storage
-          shared_bias = true;
-        }
-        if (shared_bias && b0.batch == 1) {
-          a.bias.base = b0.val;
-          a.bias.ld = 0;
+        pr.C.rows = dev_at<const float*>(g, B.push(crow));
+        pr.C.rows_aligned = all_aligned16(crow);
+        // a parameter bias (same storage for every member, the signature keys
+        // on its handle) is a single broadcast row; otherwise a row table
+        if (b0.kind == DG_OP_PARAMETER) {
+          pr.bias.base = b0.val;
+          pr.bias.ld = 0;
         } else {
           const bool bb1 = b0.batch == 1 && Bt > 1;
           std::vector<uintptr_t> brow((size_t)n * Bt);
@@ -1232,28 +1305,10 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
             const float* bv = g->nodes[g->inputs[g->nodes[nodes[j]].in_off]].val;
             for (int b = 0; b < Bt; ++b) brow[(size_t)j * Bt + b] = P(bv + (bb1 ? 0 : (int64_t)b * m));
           }
-          obias = B.push(brow);
+          pr.bias.rows = dev_at<const float*>(g, B.push(brow));
         }
-        const bool bias_table = !(shared_bias && b0.batch == 1);
-        char* scratch = scratch_base(g);
-        const int64_t scratch_floats = (int64_t)(scratch_bytes(g) / 4);
-        plan.ops.push_back([a, xoffs, oc, obias, bias_table, terms, scratch, scratch_floats, st](char* d) mutable {
-          for (int k = 0; k < terms; ++k) {
-            a.seg[k].A.base = nullptr;
-            a.seg[k].A.ld = 0;
-            a.seg[k].A.rows = at<const float* const>(d, xoffs[k]);
-          }
-          a.C.rows = at<const float* const>(d, oc);
-          if (bias_table) a.bias.rows = at<const float* const>(d, obias);
-          a.work = reinterpret_cast<float*>(scratch);
-          a.work_floats = scratch_floats;
-          return launch_gemm(a, st);
-        });
-        {
-          double kk = 0;
-          for (int k = 0; k < terms; ++k) kk += a.seg[k].K;
-          plan.tag(C_GEMM_FWD, 2.0 * a.M * a.N * kk, 4.0 * ((double)a.M * kk + kk * a.N + (double)a.M * a.N));
-        }
+        batch.probs.push_back(pr);
+        batch.bytes += 4.0 * ((double)pr.M * kk + kk * pr.N + (double)pr.M * pr.N);
       } else {
         AffineGenericArgs a{};
         a.n = n;
@@ -1382,7 +1437,11 @@ static int do_forward(dg_graph* g, int upto) {
       plan.tag(C_GATHER, 0.0, 8.0 * rows * dim + 8.0 * rows);
     }
   }
-  for (const Group& gr : S.groups) plan_forward_group(g, S, gr, plan);
+  {
+    GemmBatch gb;
+    for (const Group& gr : S.groups) plan_forward_group(g, S, gr, plan, gb);
+    flush_gemm(g, plan, gb);
+  }
 
   int rc = launch_plan(g, plan);
   if (rc) return rc;
@@ -1407,8 +1466,9 @@ int dg_forward(dg_graph* g, int32_t upto) {
 
 static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr, Plan& plan, float* dummy,
                                 std::unordered_map<int64_t, AffineUse>& wuse,
-                                std::unordered_map<int64_t, std::vector<uintptr_t>>& buse) {
+                                std::unordered_map<int64_t, std::vector<uintptr_t>>& buse, GemmBatch& gb) {
   Blob& B = plan.blob;
+  if (!(gr.kind == DG_OP_AFFINE && affine_gemm_ok(g, g->nodes[S.units[gr.units[0]].last()]))) flush_gemm(g, plan, gb);
   const cudaStream_t st = g->stream;
   std::vector<int> all_nodes;
   for (int u : gr.units) all_nodes.push_back(S.units[u].last());
@@ -1669,12 +1729,7 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
           const int terms = (n0.n_in - 1) / 2;
           const int m = (int)n0.elem;
           const int Bt = n0.batch;
-          bool gemm = terms <= 4;
-          for (int k = 0; k < terms; ++k) {
-            const Node& w = g->nodes[g->inputs[n0.in_off + 1 + 2 * k]];
-            if (w.kind != DG_OP_PARAMETER || w.batch != 1) gemm = false;
-          }
-          if (!gemm) {
+          if (!affine_gemm_ok(g, n0)) {
             AffineGenericArgs a{};
             a.n = n;
             a.batch = Bt;
@@ -1736,7 +1791,24 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
             });
           }
           const bool g_al = all_aligned16(grows);
-          const size_t og_rows = B.push(grows);
+          const float* const* g_rows_dev = dev_at<const float*>(g, B.push(grows));
+          // a grouped launch must not write one target from two problems
+          {
+            std::vector<int> mine;
+            for (int j = 0; j < n; ++j)
+              for (int k = 0; k < terms; ++k) mine.push_back(g->inputs[g->nodes[nodes[j]].in_off + 2 + 2 * k]);
+            std::sort(mine.begin(), mine.end());
+            bool clash = false;
+            for (int x : gb.targets) clash = clash || std::binary_search(mine.begin(), mine.end(), x);
+            // terms of one member sharing an x also clash inside one launch
+            for (int k = 0; k + 1 < terms && !clash; ++k)
+              for (int k2 = k + 1; k2 < terms && !clash; ++k2)
+                for (int j = 0; j < n && !clash; ++j)
+                  clash = g->inputs[g->nodes[nodes[j]].in_off + 2 + 2 * k] ==
+                          g->inputs[g->nodes[nodes[j]].in_off + 2 + 2 * k2];
+            if (clash) flush_gemm(g, plan, gb);
+          }
+          GemmBatch& batch = gemm_batch_for(g, plan, gb, gr.level, C_GEMM_DX, false, true);
           for (int k = 0; k < terms; ++k) {
             const Node& wn = g->nodes[g->inputs[n0.in_off + 1 + 2 * k]];
             const Node& xk0 = g->nodes[g->inputs[n0.in_off + 2 + 2 * k]];
@@ -1756,73 +1828,69 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
             use.m = m;
             use.x_rows.insert(use.x_rows.end(), xrows.begin(), xrows.end());
             use.g_rows.insert(use.g_rows.end(), grows.begin(), grows.end());
-            // dX = G W  (B(k=i, n=t) = W[i + t*m] -> n-major rows of W^T)
+            // dX = G W   (B(k=i, n=t) = W[i + t*m]: n-major rows of W^T)
             std::vector<uintptr_t> uniq = dxrows;
             std::sort(uniq.begin(), uniq.end());
             const bool dup = std::adjacent_find(uniq.begin(), uniq.end()) != uniq.end();
-            GemmArgs a{};
-            a.M = n * Bt;
-            a.N = K;
-            a.n_seg = 1;
-            a.seg[0].K = m;
-            a.seg[0].B.base = wn.val;
-            a.seg[0].B.ld = m;
-            a.a_kmajor = false;
-            a.b_nmajor = true;
-            a.a_rows_aligned = g_al;
-            a.b_rows_aligned = true;
-            char* scratch = scratch_base(g);
-            const int64_t scratch_floats = (int64_t)(scratch_bytes(g) / 4);
+            GemmProblem pr{};
+            pr.M = n * Bt;
+            pr.N = K;
+            pr.n_seg = 1;
+            pr.seg[0].K = m;
+            pr.seg[0].A.rows = g_rows_dev;
+            pr.seg[0].A.rows_aligned = g_al;
+            pr.seg[0].B.base = wn.val;
+            pr.seg[0].B.ld = m;
+            batch.bytes += 4.0 * ((double)pr.M * m + (double)m * pr.N + 2.0 * pr.M * pr.N);
             if (!dup) {
-              a.accumulate = true;
-              const size_t oc = B.push(dxrows);
-              plan.ops.push_back([a, og_rows, oc, scratch, scratch_floats, st](char* d) mutable {
-                a.seg[0].A.rows = at<const float* const>(d, og_rows);
-                a.C.rows = at<const float* const>(d, oc);
-                a.work = reinterpret_cast<float*>(scratch);
-                a.work_floats = scratch_floats;
-                return launch_gemm(a, st);
-              });
-              plan.tag(C_GEMM_DX, 2.0 * a.M * a.N * m, 4.0 * ((double)a.M * m + (double)m * a.N + 2.0 * a.M * a.N));
+              pr.accumulate = 1;
+              pr.C.rows = dev_at<const float*>(g, B.push(dxrows));
             } else {
-              // temp = G W (dense), then deterministic segmented row reduce
+              // several rows land on one target (broadcast x, or one x shared
+              // by group members): temp = G W densely, then a deterministic
+              // segmented row reduce into the targets
               const int64_t R = (int64_t)n * Bt;
               std::vector<int> order(R);
               std::iota(order.begin(), order.end(), 0);
               std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return dxrows[x] < dxrows[y]; });
               std::vector<uintptr_t> tgt;
               std::vector<int32_t> seg;
-              std::vector<int32_t> perm;  // temp row index per sorted position
               for (int64_t q = 0; q < R; ++q) {
                 if (q == 0 || dxrows[order[q]] != dxrows[order[q - 1]]) {
                   tgt.push_back(dxrows[order[q]]);
                   seg.push_back((int32_t)q);
                 }
-                perm.push_back(order[q]);
               }
               seg.push_back((int32_t)R);
-              // temp rows are written in sorted order so segments are contiguous
-              std::vector<uintptr_t> crow(R);
-              // C row for original row r -> temp slot = position of r in order
               std::vector<int64_t> pos(R);
               for (int64_t q = 0; q < R; ++q) pos[order[q]] = q;
-              float* temp = reinterpret_cast<float*>(scratch);
-              const int64_t temp_floats = R * K;
+              float* temp = reinterpret_cast<float*>(scratch_base(g)) + batch.temp_floats;
+              batch.temp_floats += (R * K + 63) & ~int64_t(63);
+              std::vector<uintptr_t> crow(R);
               for (int64_t r = 0; r < R; ++r) crow[r] = P(temp + pos[r] * K);
-              a.accumulate = false;
-              const size_t oc = B.push(crow), ot = B.push(tgt), os = B.push(seg);
+              pr.accumulate = 0;
+              pr.C.rows = dev_at<const float*>(g, B.push(crow));
+              float* const* tg = const_cast<float* const*>(reinterpret_cast<const float* const*>(
+                  dev_at<float*>(g, B.push(tgt))));
+              const int* sg = dev_at<int>(g, B.push(seg));
               const int n_t = (int)tgt.size();
-              plan.ops.push_back([a, og_rows, oc, ot, os, n_t, K, temp, temp_floats, scratch, scratch_floats,
-                                  st](char* d) mutable {
-                a.seg[0].A.rows = at<const float* const>(d, og_rows);
-                a.C.rows = at<const float* const>(d, oc);
-                a.work = reinterpret_cast<float*>(scratch) + ((temp_floats + 63) & ~int64_t(63));
-                a.work_floats = scratch_floats - ((temp_floats + 63) & ~int64_t(63));
-                int l = launch_gemm(a, st);
-                l += launch_row_reduce_scatter(at<float* const>(d, ot), at<const int>(d, os), temp, n_t, K, st);
-                return l;
+              batch.post.push_back([tg, sg, temp, n_t, K, st]() {
+                return launch_row_reduce_scatter(tg, sg, temp, n_t, K, st);
               });
-              plan.tag(C_GEMM_DX, 2.0 * a.M * a.N * m, 4.0 * ((double)a.M * m + (double)m * a.N + 2.0 * a.M * a.N));
+            }
+            batch.probs.push_back(pr);
+            for (int j = 0; j < n; ++j) batch.targets.push_back(g->inputs[g->nodes[nodes[j]].in_off + 2 + 2 * k]);
+            // two terms of one member on the same x: keep them in separate launches
+            if (k + 1 < terms) {
+              bool same = false;
+              for (int j = 0; j < n && !same; ++j)
+                for (int k2 = k + 1; k2 < terms && !same; ++k2)
+                  same = g->inputs[g->nodes[nodes[j]].in_off + 2 + 2 * k] ==
+                         g->inputs[g->nodes[nodes[j]].in_off + 2 + 2 * k2];
+              if (same) {
+                flush_gemm(g, plan, gb);
+                gemm_batch_for(g, plan, gb, gr.level, C_GEMM_DX, false, true);
+              }
             }
           }
           break;
@@ -1902,42 +1970,42 @@ int dg_backward(dg_graph* g, int32_t loss) {
     });
   }
   // dummy gradient target for slot-serial passes
-  float* dummy = reinterpret_cast<float*>(scratch_base(g) + scratch_bytes(g) - (16 << 20));
+  float* dummy = dummy_base(g);
   std::unordered_map<int64_t, AffineUse> wuse;
   std::unordered_map<int64_t, std::vector<uintptr_t>> buse;
-  for (int q = (int)S.groups.size() - 1; q >= 0; --q) plan_backward_group(g, S, S.groups[q], plan, dummy, wuse, buse);
+  {
+    GemmBatch gb;
+    for (int q = (int)S.groups.size() - 1; q >= 0; --q)
+      plan_backward_group(g, S, S.groups[q], plan, dummy, wuse, buse, gb);
+    flush_gemm(g, plan, gb);
+  }
 
   // aggregated weight gradients: dW^T (K x m) += X^T G over every use
   std::vector<int64_t> wkeys;
   for (auto& kv : wuse) wkeys.push_back(kv.first);
   std::sort(wkeys.begin(), wkeys.end());
-  for (int64_t h : wkeys) {
-    AffineUse& use = wuse[h];
-    Param* p = param_at(h);
-    GemmArgs a{};
-    a.M = (int)use.n_in;
-    a.N = (int)use.m;
-    a.n_seg = 1;
-    a.seg[0].K = (int)use.x_rows.size();
-    a.a_kmajor = true;
-    a.b_nmajor = false;
-    a.accumulate = true;
-    a.C.base = p->grad;
-    a.C.ld = use.m;
-    a.a_rows_aligned = all_aligned16(use.x_rows);
-    a.b_rows_aligned = all_aligned16(use.g_rows);
-    const size_t ox = B.push(use.x_rows), og = B.push(use.g_rows);
-    char* scratch = scratch_base(g);
-    const int64_t scratch_floats = (int64_t)(scratch_bytes(g) / 4) - (16 << 18);
-    plan.ops.push_back([a, ox, og, scratch, scratch_floats, st](char* d) mutable {
-      a.seg[0].A.rows = at<const float* const>(d, ox);
-      a.seg[0].B.rows = at<const float* const>(d, og);
-      a.work = reinterpret_cast<float*>(scratch);
-      a.work_floats = scratch_floats;
-      return launch_gemm(a, st);
-    });
-    plan.tag(C_GEMM_DW, 2.0 * a.M * a.N * a.seg[0].K,
-             4.0 * ((double)a.seg[0].K * (a.M + a.N) + 2.0 * a.M * a.N));
+  {
+    GemmBatch gb;
+    gemm_batch_for(g, plan, gb, -1, C_GEMM_DW, true, false);
+    for (int64_t h : wkeys) {
+      AffineUse& use = wuse[h];
+      Param* p = param_at(h);
+      GemmProblem pr{};
+      pr.M = (int)use.n_in;
+      pr.N = (int)use.m;
+      pr.n_seg = 1;
+      pr.accumulate = 1;
+      pr.seg[0].K = (int64_t)use.x_rows.size();
+      pr.seg[0].A.rows = dev_at<const float*>(g, B.push(use.x_rows));
+      pr.seg[0].A.rows_aligned = all_aligned16(use.x_rows);
+      pr.seg[0].B.rows = dev_at<const float*>(g, B.push(use.g_rows));
+      pr.seg[0].B.rows_aligned = all_aligned16(use.g_rows);
+      pr.C.base = p->grad;  // dW^T (n_in x m) row-major == dW column-major
+      pr.C.ld = use.m;
+      gb.probs.push_back(pr);
+      gb.bytes += 4.0 * ((double)pr.seg[0].K * (pr.M + pr.N) + 2.0 * pr.M * pr.N);
+    }
+    flush_gemm(g, plan, gb);
   }
   std::vector<int64_t> bkeys;
   for (auto& kv : buse) bkeys.push_back(kv.first);

@@ -1,20 +1,25 @@
-// FP32 SIMT GEMM over gathered rows for the batched affine contractions
-// (ops.py:323-357: out = b + sum_k x_k W_k^T; dW += G^T x; dx += G W).
+// Grouped FP32 SIMT GEMM over gathered rows for the batched affine
+// contractions (ops.py:323-357: out = b + sum_k x_k W_k^T; dW += G^T x;
+// dx += G W).
 //
-//   C[M x N] (= | +=) sum_seg A_seg(m,k) * B_seg(k,n)  (+ bias_m(n))
+//   for each problem p:  C_p[M x N] (= | +=) sum_seg A_seg(m,k) B_seg(k,n) (+ bias_m(n))
 //
-// Operands are addressed row-by-row (a device row-pointer table or base+ld),
-// so one launch covers every node of a batched group, broadcast batch-1
-// operands (rows repeating one pointer) and every use of a parameter across
-// the graph (weight-gradient aggregation: K = all rows).  K is a concatenation
-// of up to 4 segments (multi-term affine).  Register-tiled, register-prefetch
-// double-buffered shared-memory pipeline; deterministic split-K (partials to a
-// workspace, reduced in split order).  fp32 throughout to hold the rtol 1e-4
-// parity bar (SURVEY 7 "fp32 parity with tensor cores").
+// One launch covers a list of independent problems (both layers' affines of
+// a recurrence level, every dX term of a level, ...).  Operands are addressed
+// row by row (device row-pointer table or base+ld), so a problem spans every
+// node of a batched group, batch-1 broadcast operands (rows repeating one
+// pointer) and every use of a parameter across the graph (weight-gradient
+// aggregation).  K is a concatenation of up to 4 segments (multi-term affine).
+//
+// Split-K is deterministic without a second launch: each split CTA writes its
+// partial tile to the workspace, bumps a per-tile counter, and the CTA that
+// arrives last reduces the partials in split order and runs the epilogue.
+// fp32 throughout for the rtol 1e-4 parity bar.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -30,24 +35,20 @@ struct Cfg {
   static constexpr int kThreads = (BM / TM) * (BN / TN);
   static constexpr int kApad = BM + 4;
   static constexpr int kBpad = BN + 4;
-  static constexpr int kALoads = (BM * BK) / kThreads;  // scalar elements per thread
-  static constexpr int kBLoads = (BK * BN) / kThreads;
-  static_assert((BM * BK) % kThreads == 0 && (BK * BN) % kThreads == 0, "tile/threads");
+  static_assert((BM * BK) % (4 * kThreads) == 0 && (BK * BN) % (4 * kThreads) == 0, "tile/threads");
 };
 
-// Tile loader.  kVec: 4-wide vector loads along the contiguous axis (host
-// verified 16B alignment and extents % 4 == 0); otherwise scalar.
-template <int ROWS, int COLS, int THREADS, bool kVec>
+// Tile loader: ROWS x COLS tile in source order (source row r holds COLS
+// contiguous elements).  Vector (float4) or scalar path chosen at run time.
+template <int ROWS, int COLS, int THREADS>
 struct TileLoad {
-  // the tile is ROWS x COLS in "source order": source row r (0..ROWS) holds
-  // COLS contiguous elements.  Registers hold this thread's share.
   static constexpr int kPer = (ROWS * COLS) / THREADS;
   float v[kPer];
 
-  __device__ __forceinline__ void load(const Operand& op, int64_t row0, int64_t row_lim, int64_t col0,
+  __device__ __forceinline__ void load(const Operand& op, bool vec, int64_t row0, int64_t row_lim, int64_t col0,
                                        int64_t col_lim) {
     const int tid = threadIdx.x;
-    if (kVec) {
+    if (vec) {
 #pragma unroll
       for (int i = 0; i < kPer / 4; ++i) {
         const int idx = (tid + i * THREADS) * 4;
@@ -62,72 +63,68 @@ struct TileLoad {
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < kPer; ++i) {
-        const int idx = tid + i * THREADS;
-        const int r = idx / COLS, c = idx % COLS;
-        const int64_t gr = row0 + r, gc = col0 + c;
-        v[i] = (gr < row_lim && gc < col_lim) ? __ldg(op_row(op, gr) + gc) : 0.f;
-      }
-    }
-  }
-
-  // store into smem tile S[k][mn] (pitch P).  kTrans: source rows are the
-  // mn axis (store transposed), else source rows are the k axis.
-  template <bool kTrans, int P>
-  __device__ __forceinline__ void store(float* S) const {
-    const int tid = threadIdx.x;
-    if (kVec) {
-#pragma unroll
       for (int i = 0; i < kPer / 4; ++i) {
         const int idx = (tid + i * THREADS) * 4;
         const int r = idx / COLS, c = idx % COLS;
-        if (kTrans) {
+        const int64_t gr = row0 + r;
+        const float* rp = gr < row_lim ? op_row(op, gr) : nullptr;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) S[(c + q) * P + r] = v[i * 4 + q];
-        } else {
-          *reinterpret_cast<float4*>(S + r * P + c) = make_float4(v[i * 4], v[i * 4 + 1], v[i * 4 + 2], v[i * 4 + 3]);
+        for (int q = 0; q < 4; ++q) {
+          const int64_t gc = col0 + c + q;
+          v[i * 4 + q] = (rp && gc < col_lim) ? __ldg(rp + gc) : 0.f;
         }
       }
-    } else {
+    }
+  }
+
+  // store into smem tile S[k][mn] (pitch P); kTrans: source rows are the mn axis
+  template <bool kTrans, int P>
+  __device__ __forceinline__ void store(float* S) const {
+    const int tid = threadIdx.x;
 #pragma unroll
-      for (int i = 0; i < kPer; ++i) {
-        const int idx = tid + i * THREADS;
-        const int r = idx / COLS, c = idx % COLS;
-        if (kTrans) S[c * P + r] = v[i];
-        else S[r * P + c] = v[i];
+    for (int i = 0; i < kPer / 4; ++i) {
+      const int idx = (tid + i * THREADS) * 4;
+      const int r = idx / COLS, c = idx % COLS;
+      if (kTrans) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) S[(c + q) * P + r] = v[i * 4 + q];
+      } else {
+        *reinterpret_cast<float4*>(S + r * P + c) = make_float4(v[i * 4], v[i * 4 + 1], v[i * 4 + 2], v[i * 4 + 3]);
       }
     }
   }
 };
 
-struct TilePos {
-  int seg;
-  int k0;
-};
-
-__device__ __forceinline__ TilePos tile_at(const GemmArgs& a, int t, int BK) {
-  for (int s = 0; s < a.n_seg; ++s) {
-    const int nt = (a.seg[s].K + BK - 1) / BK;
-    if (t < nt) return {s, t * BK};
-    t -= nt;
-  }
-  return {a.n_seg - 1, 0};
-}
-
-template <int BM, int BN, int BK, int TM, int TN, bool kAK, bool kBN, bool kVecA, bool kVecB>
+template <int BM, int BN, int BK, int TM, int TN, bool kAK, bool kBN>
 __global__ void __launch_bounds__(Cfg<BM, BN, BK, TM, TN>::kThreads)
-    gemm_kernel(GemmArgs a, int total_tiles, int splits) {
+    gemm_group_kernel(const GemmProblem* __restrict__ probs, int n_probs, float* __restrict__ work,
+                      int* __restrict__ counters) {
   using C = Cfg<BM, BN, BK, TM, TN>;
   __shared__ __align__(16) float As[2][BK * C::kApad];
   __shared__ __align__(16) float Bs[2][BK * C::kBpad];
+  __shared__ GemmProblem P;
+  __shared__ int s_last;
 
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int z = blockIdx.z;
-  const int t0 = (int)((int64_t)total_tiles * z / splits), t1 = (int)((int64_t)total_tiles * (z + 1) / splits);
+  // locate this CTA's problem (problems are few; linear scan of cta0)
+  int p = 0;
+  while (p + 1 < n_probs && (int)blockIdx.x >= __ldg(&probs[p + 1].cta0)) ++p;
+  {
+    const int* src = reinterpret_cast<const int*>(probs + p);
+    int* dst = reinterpret_cast<int*>(&P);
+    for (int i = threadIdx.x; i < (int)(sizeof(GemmProblem) / 4); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const int local = blockIdx.x - P.cta0;
+  const int z = local / P.tiles;
+  const int tile = local - z * P.tiles;
+  const int m0 = (tile / P.tiles_n) * BM, n0 = (tile % P.tiles_n) * BN;
 
-  // A tile in source order: kAK -> BK rows (k) x BM cols (m); else BM rows (m) x BK cols (k)
-  using ALoad = TileLoad<kAK ? BK : BM, kAK ? BM : BK, C::kThreads, kVecA>;
-  using BLoad = TileLoad<kBN ? BN : BK, kBN ? BK : BN, C::kThreads, kVecB>;
+  int total_kt = 0;
+  for (int s = 0; s < P.n_seg; ++s) total_kt += (P.seg[s].K + BK - 1) / BK;
+  const int t0 = (int)((int64_t)total_kt * z / P.splits), t1 = (int)((int64_t)total_kt * (z + 1) / P.splits);
+
+  using ALoad = TileLoad<kAK ? BK : BM, kAK ? BM : BK, C::kThreads>;
+  using BLoad = TileLoad<kBN ? BN : BK, kBN ? BK : BN, C::kThreads>;
   ALoad la;
   BLoad lb;
 
@@ -138,13 +135,20 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, TM, TN>::kThreads)
 #pragma unroll
     for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
 
+  // k-tile t -> (segment, k0)
   auto fetch = [&](int t) {
-    const TilePos p = tile_at(a, t, BK);
-    const GemmSeg& sg = a.seg[p.seg];
-    if (kAK) la.load(sg.A, p.k0, sg.K, m0, a.M);
-    else la.load(sg.A, m0, a.M, p.k0, sg.K);
-    if (kBN) lb.load(sg.B, n0, a.N, p.k0, sg.K);
-    else lb.load(sg.B, p.k0, sg.K, n0, a.N);
+    int s = 0;
+    for (; s + 1 < P.n_seg; ++s) {
+      const int nt = (P.seg[s].K + BK - 1) / BK;
+      if (t < nt) break;
+      t -= nt;
+    }
+    const GemmSeg& sg = P.seg[s];
+    const int k0 = t * BK;
+    if (kAK) la.load(sg.A, P.vec_a, k0, sg.K, m0, P.M);
+    else la.load(sg.A, P.vec_a, m0, P.M, k0, sg.K);
+    if (kBN) lb.load(sg.B, P.vec_b, n0, P.N, k0, sg.K);
+    else lb.load(sg.B, P.vec_b, k0, sg.K, n0, P.N);
   };
 
   int buf = 0;
@@ -184,132 +188,162 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, TM, TN>::kThreads)
     buf ^= 1;
   }
 
-  // epilogue
-  const bool has_bias = a.bias.rows != nullptr || a.bias.base != nullptr;
+  const bool has_bias = P.bias.rows != nullptr || P.bias.base != nullptr;
+  if (P.splits > 1) {
+    // partial tile -> workspace; the last split to arrive reduces in order
+    float* part = work + P.work_off + (int64_t)z * ((int64_t)P.tiles * BM * BN) + (int64_t)tile * BM * BN;
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int lm = (i / 4) * (BM / (TM / 4)) + ty * 4 + (i % 4);
+        const int ln = (j / 4) * (BN / (TN / 4)) + tx * 4 + (j % 4);
+        part[lm * BN + ln] = acc[i][j];
+      }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int prev = atomicAdd(&counters[P.counter0 + tile], 1);
+      s_last = prev == P.splits - 1;
+      if (s_last) counters[P.counter0 + tile] = 0;  // reset for the next launch
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int lm = (i / 4) * (BM / (TM / 4)) + ty * 4 + (i % 4);
+        const int ln = (j / 4) * (BN / (TN / 4)) + tx * 4 + (j % 4);
+        float s = 0.f;
+        for (int q = 0; q < P.splits; ++q)
+          s += __ldcg(work + P.work_off + (int64_t)q * ((int64_t)P.tiles * BM * BN) + (int64_t)tile * BM * BN +
+                      lm * BN + ln);
+        acc[i][j] = s;
+      }
+  }
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     const int m = m0 + (i / 4) * (BM / (TM / 4)) + ty * 4 + (i % 4);
-    if (m >= a.M) continue;
-    float* crow = nullptr;
-    const float* brow = nullptr;
-    if (splits == 1) {
-      crow = const_cast<float*>(op_row(a.C, m));
-      if (has_bias) brow = op_row(a.bias, m);
-    }
+    if (m >= P.M) continue;
+    float* crow = const_cast<float*>(op_row(P.C, m));
+    const float* brow = has_bias ? op_row(P.bias, m) : nullptr;
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
       const int n = n0 + (j / 4) * (BN / (TN / 4)) + tx * 4 + (j % 4);
-      if (n >= a.N) continue;
+      if (n >= P.N) continue;
       float v = acc[i][j];
-      if (splits == 1) {
-        if (brow) v += brow[n];
-        if (a.accumulate) v += crow[n];
-        crow[n] = v;
-      } else {
-        a.work[((int64_t)z * a.M + m) * a.N + n] = v;
-      }
+      if (brow) v += brow[n];
+      if (P.accumulate) v += crow[n];
+      crow[n] = v;
     }
   }
 }
 
-__global__ void splitk_reduce_kernel(GemmArgs a, int splits) {
-  const int64_t total = (int64_t)a.M * a.N;
-  const bool has_bias = a.bias.rows != nullptr || a.bias.base != nullptr;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t m = t / a.N, n = t - m * a.N;
-    float v = 0.f;
-    for (int z = 0; z < splits; ++z) v += a.work[(int64_t)z * total + t];
-    if (has_bias) v += op_row(a.bias, m)[n];
-    float* crow = const_cast<float*>(op_row(a.C, m));
-    if (a.accumulate) v += crow[n];
-    crow[n] = v;
-  }
-}
-
-template <int BM, int BN, int BK, int TM, int TN, bool kAK, bool kBN>
-void launch_cfg(const GemmArgs& a, bool vecA, bool vecB, int total_tiles, int splits, cudaStream_t s) {
-  using C = Cfg<BM, BN, BK, TM, TN>;
-  dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, splits);
-  if (vecA && vecB)
-    gemm_kernel<BM, BN, BK, TM, TN, kAK, kBN, true, true><<<grid, C::kThreads, 0, s>>>(a, total_tiles, splits);
-  else if (vecA)
-    gemm_kernel<BM, BN, BK, TM, TN, kAK, kBN, true, false><<<grid, C::kThreads, 0, s>>>(a, total_tiles, splits);
-  else if (vecB)
-    gemm_kernel<BM, BN, BK, TM, TN, kAK, kBN, false, true><<<grid, C::kThreads, 0, s>>>(a, total_tiles, splits);
-  else
-    gemm_kernel<BM, BN, BK, TM, TN, kAK, kBN, false, false><<<grid, C::kThreads, 0, s>>>(a, total_tiles, splits);
-}
+struct CfgInfo {
+  int bm, bn, bk;
+};
+constexpr CfgInfo kCfg[4] = {{128, 128, 8}, {64, 64, 16}, {64, 32, 32}, {32, 32, 32}};
 
 template <int BM, int BN, int BK, int TM, int TN>
-void launch_major(const GemmArgs& a, bool vecA, bool vecB, int tt, int splits, cudaStream_t s) {
-  if (a.a_kmajor && a.b_nmajor) launch_cfg<BM, BN, BK, TM, TN, true, true>(a, vecA, vecB, tt, splits, s);
-  else if (a.a_kmajor) launch_cfg<BM, BN, BK, TM, TN, true, false>(a, vecA, vecB, tt, splits, s);
-  else if (a.b_nmajor) launch_cfg<BM, BN, BK, TM, TN, false, true>(a, vecA, vecB, tt, splits, s);
-  else launch_cfg<BM, BN, BK, TM, TN, false, false>(a, vecA, vecB, tt, splits, s);
+void launch_major(const GemmLaunch& L, const GemmProblem* probs, float* work, int* counters, cudaStream_t s) {
+  using C = Cfg<BM, BN, BK, TM, TN>;
+  if (L.a_kmajor && L.b_nmajor)
+    gemm_group_kernel<BM, BN, BK, TM, TN, true, true><<<L.ctas, C::kThreads, 0, s>>>(probs, L.n_probs, work, counters);
+  else if (L.a_kmajor)
+    gemm_group_kernel<BM, BN, BK, TM, TN, true, false><<<L.ctas, C::kThreads, 0, s>>>(probs, L.n_probs, work, counters);
+  else if (L.b_nmajor)
+    gemm_group_kernel<BM, BN, BK, TM, TN, false, true><<<L.ctas, C::kThreads, 0, s>>>(probs, L.n_probs, work, counters);
+  else
+    gemm_group_kernel<BM, BN, BK, TM, TN, false, false><<<L.ctas, C::kThreads, 0, s>>>(probs, L.n_probs, work, counters);
 }
 
-// host-side vectorisability: every row start 16B aligned (checked by the
-// planner through the `aligned` hint encoded in ld / tables) and the
-// contiguous extent a multiple of 4.
-bool operand_vec_ok(const Operand& o, int64_t contiguous_extent, bool rows_aligned) {
-  if (contiguous_extent % 4) return false;
-  if (o.rows) return rows_aligned;
+bool base_vec_ok(const Operand& o) {
+  if (o.rows) return o.rows_aligned != 0;
   return (reinterpret_cast<uintptr_t>(o.base) % 16 == 0) && (o.ld % 4 == 0);
 }
 
 }  // namespace
 
-int launch_gemm(const GemmArgs& a, cudaStream_t s) {
-  if (a.M <= 0 || a.N <= 0) return 0;
-  bool vecA = true, vecB = true;
-  int64_t Ktot = 0;
-  for (int i = 0; i < a.n_seg; ++i) {
-    const GemmSeg& sg = a.seg[i];
-    Ktot += sg.K;
-    vecA = vecA && operand_vec_ok(sg.A, a.a_kmajor ? a.M : sg.K, a.a_rows_aligned);
-    vecB = vecB && operand_vec_ok(sg.B, a.b_nmajor ? sg.K : a.N, a.b_rows_aligned);
+GemmLaunch gemm_plan(std::vector<GemmProblem>& probs, bool a_kmajor, bool b_nmajor, int64_t work_cap_floats,
+                     int counter_cap) {
+  GemmLaunch L{};
+  L.a_kmajor = a_kmajor;
+  L.b_nmajor = b_nmajor;
+  L.n_probs = (int)probs.size();
+  int max_m = 0;
+  double flops = 0;
+  for (auto& p : probs) {
+    max_m = std::max(max_m, p.M);
+    int64_t k = 0;
+    for (int s = 0; s < p.n_seg; ++s) k += p.seg[s].K;
+    flops += 2.0 * p.M * p.N * (double)k;
   }
-  // vector loads also need the tile's contiguous extent aligned with the
-  // problem edge; the masked float4 loads require M/N/K % 4 == 0 (checked above)
-  int launches = 0;
-  const int64_t mn = (int64_t)a.M * a.N;
-  // tile choice: big tiles when there are enough of them, else smaller tiles
-  // plus split-K so at least ~1 wave of 148 SMs is busy.
-  int cfg;
-  int64_t tiles;
-  if (((int64_t)(a.M + 127) / 128) * ((a.N + 127) / 128) >= 120) {
-    cfg = 0;
-    tiles = ((int64_t)(a.M + 127) / 128) * ((a.N + 127) / 128);
-  } else if (((int64_t)(a.M + 63) / 64) * ((a.N + 63) / 64) >= 48 || mn >= 256 * 256) {
-    cfg = 1;
-    tiles = ((int64_t)(a.M + 63) / 64) * ((a.N + 63) / 64);
-  } else {
-    cfg = 2;
-    tiles = ((int64_t)(a.M + 31) / 32) * ((a.N + 31) / 32);
+  // tile shape: skinny problems (the recurrent steps, M = minibatch) get
+  // 64x32 tiles; big ones 128x128; the rest 64x64
+  int64_t t128 = 0;
+  for (auto& p : probs) t128 += (int64_t)((p.M + 127) / 128) * ((p.N + 127) / 128);
+  if (!a_kmajor && max_m <= 64) L.cfg = 2;
+  else if (t128 >= 120) L.cfg = 0;
+  else if (max_m <= 32 && !a_kmajor) L.cfg = 3;
+  else L.cfg = 1;
+  const CfgInfo c = kCfg[L.cfg];
+  const int threads = L.cfg == 3 ? 64 : (L.cfg == 2 ? 128 : 256);
+  int64_t tiles_all = 0;
+  for (auto& p : probs) {
+    p.tiles_n = (p.N + c.bn - 1) / c.bn;
+    p.tiles = ((p.M + c.bm - 1) / c.bm) * p.tiles_n;
+    tiles_all += p.tiles;
   }
-  const int BK = cfg == 0 ? 8 : (cfg == 1 ? 16 : 32);
-  int total_tiles = 0;
-  for (int i = 0; i < a.n_seg; ++i) total_tiles += (a.seg[i].K + BK - 1) / BK;
-  int splits = 1;
-  if (tiles < 148 && total_tiles >= 8) {
-    splits = static_cast<int>(std::min<int64_t>((296 + tiles - 1) / tiles, total_tiles / 4));
-    if (splits < 1) splits = 1;
-    while (splits > 1 && (int64_t)splits * mn > a.work_floats) --splits;
+  // split-K so that roughly two waves of 256-thread-equivalents are in flight
+  const int64_t target = (int64_t)148 * 2 * 256 / threads;
+  int64_t cta = 0, counter = 0, woff = 0;
+  for (auto& p : probs) {
+    int kt = 0;
+    for (int s = 0; s < p.n_seg; ++s) kt += (p.seg[s].K + c.bk - 1) / c.bk;
+    int splits = 1;
+    if (tiles_all < target && kt >= 4) {
+      splits = (int)std::min<int64_t>((target + tiles_all - 1) / tiles_all, kt / 2);
+      splits = std::max(1, std::min(splits, 16));
+    }
+    const int64_t part = (int64_t)splits * p.tiles * c.bm * c.bn;
+    if (splits > 1 && (woff + part > work_cap_floats || counter + p.tiles > counter_cap)) splits = 1;
+    p.splits = splits;
+    p.cta0 = (int)cta;
+    p.counter0 = (int)counter;
+    p.work_off = woff;
+    if (splits > 1) {
+      woff += part;
+      counter += p.tiles;
+    }
+    cta += (int64_t)p.tiles * splits;
+    // vectorised loads need 16B-aligned rows and contiguous extents % 4
+    bool va = true, vb = true;
+    for (int s = 0; s < p.n_seg; ++s) {
+      const GemmSeg& sg = p.seg[s];
+      va = va && base_vec_ok(sg.A) && ((a_kmajor ? p.M : sg.K) % 4 == 0);
+      vb = vb && base_vec_ok(sg.B) && ((b_nmajor ? sg.K : p.N) % 4 == 0);
+    }
+    p.vec_a = va;
+    p.vec_b = vb;
   }
-  if (total_tiles == 0) {
-    // K == 0: C = bias (+C)
-    splits = 1;
+  L.ctas = (int)cta;
+  L.work_floats = woff;
+  L.flops = flops;
+  return L;
+}
+
+int launch_gemm_group(const GemmLaunch& L, const GemmProblem* probs_dev, float* work, int* counters,
+                      cudaStream_t s) {
+  if (L.ctas <= 0) return 0;
+  switch (L.cfg) {
+    case 0: launch_major<128, 128, 8, 8, 8>(L, probs_dev, work, counters, s); break;
+    case 1: launch_major<64, 64, 16, 4, 4>(L, probs_dev, work, counters, s); break;
+    case 2: launch_major<64, 32, 32, 4, 4>(L, probs_dev, work, counters, s); break;
+    default: launch_major<32, 32, 32, 4, 4>(L, probs_dev, work, counters, s); break;
   }
-  if (cfg == 0) launch_major<128, 128, 8, 8, 8>(a, vecA, vecB, total_tiles, splits, s);
-  else if (cfg == 1) launch_major<64, 64, 16, 4, 4>(a, vecA, vecB, total_tiles, splits, s);
-  else launch_major<32, 32, 32, 4, 4>(a, vecA, vecB, total_tiles, splits, s);
-  ++launches;
-  if (splits > 1) {
-    int blocks = static_cast<int>(std::min<int64_t>((mn + 255) / 256, 148 * 16));
-    splitk_reduce_kernel<<<blocks, 256, 0, s>>>(a, splits);
-    ++launches;
-  }
-  return launches;
+  return 1;
 }
 
 }  // namespace dg

@@ -206,25 +206,39 @@ __global__ void cell_fwd_kernel(CellArgs a) {
   }
 }
 
-// kLoopBatch: one thread per (cell, unit) walks the batch so batch-1 (broadcast)
-// external cell states receive the batch sum (ops.py:69-75)
+// kLoopBatch (a batch-1 external state broadcast over the batch, ops.py:69-75):
+// a block covers 32 units x 8 batch slices; slice s walks rows s, s+8, ... and
+// the broadcast state's batch sum is reduced over the 8 slices in fixed order
+// (deterministic, no atomics).  Otherwise one thread per (cell, row, unit).
 template <int M, bool kLoopBatch>
-__global__ void cell_bwd_kernel(CellArgs a) {
+__global__ void __launch_bounds__(256) cell_bwd_kernel(CellArgs a) {
   const CellSlots S(M);
-  const int64_t per = kLoopBatch ? (int64_t)a.H : (int64_t)a.batch * a.H;
+  __shared__ float red[M > 0 ? M : 1][8][32];
+  const int64_t per = kLoopBatch ? (int64_t)((a.H + 31) / 32) * 256 : (int64_t)a.batch * a.H;
   const int64_t total = per * a.n;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t stride = kLoopBatch ? total : (int64_t)gridDim.x * blockDim.x;  // kLoopBatch: one pass
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += stride) {
     const int j = static_cast<int>(t / per);
     const int64_t q = t - (int64_t)j * per;
     auto V = [&](int slot) { return a.val[(int64_t)slot * a.n + j]; };
     auto D = [&](int slot) { return a.grad[(int64_t)slot * a.n + j]; };
-    const int b_lo = kLoopBatch ? 0 : static_cast<int>(q / a.H);
-    const int b_hi = kLoopBatch ? a.batch : b_lo + 1;
-    const int u = static_cast<int>(kLoopBatch ? q : q - (int64_t)b_lo * a.H);
+    int b_lo, b_hi, b_step, u;
+    if (kLoopBatch) {
+      const int slice = threadIdx.x >> 5;
+      u = static_cast<int>(q / 256) * 32 + (threadIdx.x & 31);
+      b_lo = slice;
+      b_hi = u < a.H ? a.batch : 0;
+      b_step = 8;
+    } else {
+      b_lo = static_cast<int>(q / a.H);
+      b_hi = b_lo + 1;
+      b_step = 1;
+      u = static_cast<int>(q - (int64_t)b_lo * a.H);
+    }
     float acc_c[M > 0 ? M : 1];
 #pragma unroll
     for (int k = 0; k < M; ++k) acc_c[k] = 0.f;
-    for (int b = b_lo; b < b_hi; ++b) {
+    for (int b = b_lo; b < b_hi; b += b_step) {
       const int64_t r = (int64_t)b * a.H + u;
       const float gh = D(S.h)[r];
       const float ao = V(S.act0 + S.go())[r], ai = V(S.act0 + S.gi())[r], ag = V(S.act0 + S.gg())[r];
@@ -271,9 +285,21 @@ __global__ void cell_bwd_kernel(CellArgs a) {
       }
     }
     if (kLoopBatch) {
+      const int slice = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
-      for (int k = 0; k < M; ++k)
-        if (a.cext_b1[k]) D(1 + k)[u] += acc_c[k];
+      for (int k = 0; k < M; ++k) red[k][slice][lane] = acc_c[k];
+      __syncthreads();
+      if (slice == 0 && u < a.H) {
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          if (!a.cext_b1[k]) continue;
+          float s = 0.f;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) s += red[k][w][lane];
+          D(1 + k)[u] += s;
+        }
+      }
+      __syncthreads();
     }
   }
 }
@@ -653,14 +679,31 @@ __global__ void colsum_final_kernel(float* dst, const float* work, int width, in
 
 __global__ void row_reduce_scatter_kernel(float* const* dst_rows, const int* seg, const float* src, int n_targets,
                                           int width) {
-  const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // one block per target row; 8 warps split the segment, fixed-order reduce
+  __shared__ float part[8][128];
+  const int u = blockIdx.x;
   if (u >= n_targets) return;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float* dst = dst_rows[u];
-  for (int c = lane; c < width; c += 32) {
-    float acc = 0.f;
-    for (int k = seg[u]; k < seg[u + 1]; ++k) acc += src[(int64_t)k * width + c];
-    dst[c] += acc;
+  for (int c0 = 0; c0 < width; c0 += 128) {
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int k = seg[u] + w; k < seg[u + 1]; k += 8) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = c0 + lane + 32 * q;
+        if (c < width) acc[q] += src[(int64_t)k * width + c];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) part[w][lane + 32 * q] = acc[q];
+    __syncthreads();
+    if (threadIdx.x < 128 && c0 + threadIdx.x < width) {
+      float s = 0.f;
+#pragma unroll
+      for (int ww = 0; ww < 8; ++ww) s += part[ww][threadIdx.x];
+      dst[c0 + threadIdx.x] += s;
+    }
+    __syncthreads();
   }
 }
 
@@ -800,7 +843,8 @@ int launch_cell_fwd(const CellArgs& a, cudaStream_t s) {
 int launch_cell_bwd(const CellArgs& a, cudaStream_t s) {
   bool bcast = false;
   for (int k = 0; k < a.m; ++k) bcast = bcast || (a.cext_b1[k] && a.batch > 1);
-  const int g = grid_for((int64_t)a.n * (bcast ? 1 : a.batch) * a.H);
+  // broadcast variant: exactly one block per (cell, 32-unit chunk), single pass
+  const int g = bcast ? a.n * ((a.H + 31) / 32) : grid_for((int64_t)a.n * a.batch * a.H);
   switch (a.m * 2 + (bcast ? 1 : 0)) {
     case 0: cell_bwd_kernel<0, false><<<g, kThreads, 0, s>>>(a); break;
     case 1: cell_bwd_kernel<0, true><<<g, kThreads, 0, s>>>(a); break;
@@ -902,7 +946,7 @@ int launch_colsum_rows(float* dst, const float* const* rows, int n_rows, int wid
 int launch_row_reduce_scatter(float* const* dst_rows, const int* seg, const float* src, int n_targets, int width,
                               cudaStream_t s) {
   if (n_targets <= 0) return 0;
-  row_reduce_scatter_kernel<<<(n_targets + 7) / 8, 256, 0, s>>>(dst_rows, seg, src, n_targets, width);
+  row_reduce_scatter_kernel<<<n_targets, 256, 0, s>>>(dst_rows, seg, src, n_targets, width);
   return 1;
 }
 

@@ -7,6 +7,7 @@
 // built by the planner (executor.cpp) and uploaded once per plan.
 #pragma once
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 
 namespace dg {
@@ -167,26 +168,37 @@ struct Operand {
   const float* base;     // used when rows == nullptr: row(i) = base + i*ld
   int64_t ld;
   const float* const* rows;  // row pointer table (device) or nullptr
+  int64_t rows_aligned;      // every row-table entry is 16B aligned (planner-checked)
 };
 struct GemmSeg {
-  int K;
+  int64_t K;
   Operand A, B;
 };
-struct GemmArgs {
-  int M, N;
-  int n_seg;
+// One problem of a grouped launch; the table lives in device memory.
+//   a_kmajor (per launch): A(m,k) = A.row(k)[m]   else A.row(m)[k]
+//   b_nmajor (per launch): B(k,n) = B.row(n)[k]   else B.row(k)[n]
+struct GemmProblem {
+  int M, N, n_seg, accumulate;
   GemmSeg seg[4];
-  bool a_kmajor;    // A(m,k) = A.row(k)[m]  (else A.row(m)[k])
-  bool b_nmajor;    // B(k,n) = B.row(n)[k]  (else B.row(k)[n])
-  Operand C;        // row(m) -> N contiguous outputs
-  bool accumulate;  // C += acc  (else C = acc)
-  Operand bias;     // optional per-row bias vector (row(m)[n]); base==rows==nullptr -> none
-  float* work;      // split-K partials
-  int64_t work_floats;
-  bool a_rows_aligned;  // every A row-table entry is 16B aligned (planner-checked)
-  bool b_rows_aligned;
+  Operand C;     // row(m) -> N contiguous outputs
+  Operand bias;  // optional per-row bias (row(m)[n]); base == rows == nullptr -> none
+  // filled by gemm_plan
+  int tiles_n, tiles, splits, cta0;
+  int counter0, vec_a, vec_b, pad_;
+  int64_t work_off;
 };
-int launch_gemm(const GemmArgs& a, cudaStream_t s);
+struct GemmLaunch {
+  int cfg, n_probs, ctas;
+  bool a_kmajor, b_nmajor;
+  int64_t work_floats;
+  double flops;
+};
+// host: choose tile config / split-K / CTA offsets (mutates probs)
+GemmLaunch gemm_plan(std::vector<GemmProblem>& probs, bool a_kmajor, bool b_nmajor, int64_t work_cap_floats,
+                     int counter_cap);
+// counters: zero-initialised ints (>= sum of split problems' tiles); left zero
+int launch_gemm_group(const GemmLaunch& L, const GemmProblem* probs_dev, float* work, int* counters,
+                      cudaStream_t s);
 
 // ------------------------------------------------------------- trainers
 struct TensorSeg { float* w; float* g; float* s0; float* s1; int64_t n; };

@@ -103,10 +103,16 @@ def _compare_full(make_task, batches, rule="adam", n_steps=2):
     ref, mo = _run_steps(dyo, cgo, mo, make_task(dyo, mo), batches, rule, n_steps, True)
     for s in range(n_steps):
         parity(got[s]["loss"], ref[s]["loss"], what=f"loss{s}")
+        for name, t in ref[s]["touched"].items():
+            assert got[s]["touched"][name] == t  # bit-exact at every step
+        # gradients: strict at every step under SGD; under Adam only before the
+        # first update -- after it the two runs evaluate the graph at parameters
+        # that already differ inside the Adam band ("Adam amplifies")
+        if rule != "sgd" and s > 0:
+            continue
         for name, g in ref[s]["grads"].items():
             parity(got[s]["grads"][name], g, what=f"step{s} {name}")
-        for name, t in ref[s]["touched"].items():
-            assert got[s]["touched"][name] == t
+        for name in ref[s]["touched"]:
             parity(got[s]["lgrads"][name], ref[s]["lgrads"][name], what=f"step{s} {name} rows")
     band = 0.0 if rule == "sgd" else 2 * 1e-3 * n_steps
     for p, q in zip(mg.parameters, mo.parameters):
@@ -117,6 +123,12 @@ def test_ptb_mb16_full_size_vs_oracle():
     sents = W.ptb_corpus(21, 32)
     batches = W.minibatches(sents, 16)
     _compare_full(lambda dy, m: W.RNNLM(dy, m, 10_000, 128, 256, 2), batches)
+
+
+def test_ptb_mb16_full_size_vs_oracle_sgd_multistep():
+    sents = W.ptb_corpus(27, 48)
+    batches = W.minibatches(sents, 16)
+    _compare_full(lambda dy, m: W.RNNLM(dy, m, 10_000, 128, 256, 2), batches, rule="sgd", n_steps=3)
 
 
 def test_ptb_mb64_full_size_vs_oracle_sgd():
