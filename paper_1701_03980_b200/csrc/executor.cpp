@@ -202,6 +202,7 @@ struct dg_graph {
   dg::Pinned pinned[2];
   int pin_idx = 0;
   bool has_grads = false;  // any backward in this generation
+  bool counters_ready = false;  // split-K tile counters zeroed (first launch)
 };
 
 struct dg_trainer {
@@ -906,12 +907,6 @@ int dg_graph_create(int device, void* fwd_base, size_t fwd_bytes, void* bwd_base
     delete g;
     return fail(DG_CONFIG, "workspace must be at least 64 MiB");
   }
-  // split-K tile counters start (and are always left) at zero
-  cudaError_t e = cudaMemset(g->work_base + work_bytes - kCounterBytes, 0, kCounterBytes);
-  if (e != cudaSuccess) {
-    delete g;
-    return fail(DG_CUDA, std::string("workspace init: ") + cudaGetErrorString(e));
-  }
   *out = g;
   return DG_OK;
 }
@@ -997,6 +992,11 @@ int dg_graph_append(dg_graph* g, const dg_node* nodes, int32_t n, const int32_t*
 static int launch_plan(dg_graph* g, Plan& plan) {
   const size_t blob_bytes = (plan.blob.host.size() + 255) & ~size_t(255);
   if (blob_bytes > g->work_bytes / 2) return fail(DG_CONFIG, "plan tables exceed the workspace");
+  if (!g->counters_ready) {
+    // split-K tile counters start (and are always left) at zero
+    DG_CUDA_TRY(cudaMemsetAsync(g->work_base + g->work_bytes - (1u << 20), 0, 1u << 20, g->stream));
+    g->counters_ready = true;
+  }
   int rc = upload(g, plan.blob, g->work_base);
   if (rc) return rc;
   plan.meta.resize(plan.ops.size());

@@ -45,9 +45,11 @@ struct TileLoad {
   static constexpr int kPer = (ROWS * COLS) / THREADS;
   float v[kPer];
 
+  // cache: optional shared-memory copy of the tile's ROWS row pointers
   __device__ __forceinline__ void load(const Operand& op, bool vec, int64_t row0, int64_t row_lim, int64_t col0,
-                                       int64_t col_lim) {
+                                       int64_t col_lim, const float* const* cache = nullptr) {
     const int tid = threadIdx.x;
+    auto row = [&](int r, int64_t gr) { return cache ? cache[r] : op_row(op, gr); };
     if (vec) {
 #pragma unroll
       for (int i = 0; i < kPer / 4; ++i) {
@@ -55,7 +57,7 @@ struct TileLoad {
         const int r = idx / COLS, c = idx % COLS;
         const int64_t gr = row0 + r, gc = col0 + c;
         float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (gr < row_lim && gc < col_lim) x = __ldg(reinterpret_cast<const float4*>(op_row(op, gr) + gc));
+        if (gr < row_lim && gc < col_lim) x = __ldg(reinterpret_cast<const float4*>(row(r, gr) + gc));
         v[i * 4 + 0] = x.x;
         v[i * 4 + 1] = x.y;
         v[i * 4 + 2] = x.z;
@@ -67,7 +69,7 @@ struct TileLoad {
         const int idx = (tid + i * THREADS) * 4;
         const int r = idx / COLS, c = idx % COLS;
         const int64_t gr = row0 + r;
-        const float* rp = gr < row_lim ? op_row(op, gr) : nullptr;
+        const float* rp = gr < row_lim ? row(r, gr) : nullptr;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int64_t gc = col0 + c + q;
@@ -104,6 +106,10 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, TM, TN>::kThreads)
   __shared__ __align__(16) float Bs[2][BK * C::kBpad];
   __shared__ GemmProblem P;
   __shared__ int s_last;
+  // per-segment row pointers of the tile's fixed rows (A rows when A is
+  // m-major, B rows when B is n-major): one global load per element later
+  __shared__ const float* rowA[4][kAK ? 1 : BM];
+  __shared__ const float* rowB[4][kBN ? BN : 1];
 
   // locate this CTA's problem (problems are few; linear scan of cta0)
   int p = 0;
@@ -118,6 +124,19 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, TM, TN>::kThreads)
   const int z = local / P.tiles;
   const int tile = local - z * P.tiles;
   const int m0 = (tile / P.tiles_n) * BM, n0 = (tile % P.tiles_n) * BN;
+  if (!kAK) {
+    for (int i = threadIdx.x; i < P.n_seg * BM; i += blockDim.x) {
+      const int s = i / BM, r = i % BM;
+      rowA[s][r] = m0 + r < P.M ? op_row(P.seg[s].A, m0 + r) : nullptr;
+    }
+  }
+  if (kBN) {
+    for (int i = threadIdx.x; i < P.n_seg * BN; i += blockDim.x) {
+      const int s = i / BN, r = i % BN;
+      rowB[s][r] = n0 + r < P.N ? op_row(P.seg[s].B, n0 + r) : nullptr;
+    }
+  }
+  __syncthreads();
 
   int total_kt = 0;
   for (int s = 0; s < P.n_seg; ++s) total_kt += (P.seg[s].K + BK - 1) / BK;
@@ -146,8 +165,8 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, TM, TN>::kThreads)
     const GemmSeg& sg = P.seg[s];
     const int k0 = t * BK;
     if (kAK) la.load(sg.A, P.vec_a, k0, sg.K, m0, P.M);
-    else la.load(sg.A, P.vec_a, m0, P.M, k0, sg.K);
-    if (kBN) lb.load(sg.B, P.vec_b, n0, P.N, k0, sg.K);
+    else la.load(sg.A, P.vec_a, m0, P.M, k0, sg.K, rowA[s]);
+    if (kBN) lb.load(sg.B, P.vec_b, n0, P.N, k0, sg.K, rowB[s]);
     else lb.load(sg.B, P.vec_b, k0, sg.K, n0, P.N);
   };
 
@@ -162,6 +181,14 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, TM, TN>::kThreads)
     if (t + 1 < t1) fetch(t + 1);
     const float* Ab = As[buf];
     const float* Bb = Bs[buf];
+    // blocked summation: each k-tile accumulates into a fresh partial that is
+    // then added to the running sum (error grows with K/BK + BK instead of K;
+    // K reaches 10^4 for the output-layer dX)
+    float tacc[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) tacc[i][j] = 0.f;
 #pragma unroll
     for (int k = 0; k < BK; ++k) {
       float ra[TM], rb[TN];
@@ -178,8 +205,12 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, TM, TN>::kThreads)
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(ra[i], rb[j], acc[i][j]);
+        for (int j = 0; j < TN; ++j) tacc[i][j] = fmaf(ra[i], rb[j], tacc[i][j]);
     }
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) acc[i][j] += tacc[i][j];
     if (t + 1 < t1) {
       la.template store<!kAK, C::kApad>(As[buf ^ 1]);
       lb.template store<kBN, C::kBpad>(Bs[buf ^ 1]);
@@ -195,10 +226,11 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, TM, TN>::kThreads)
 #pragma unroll
     for (int i = 0; i < TM; ++i)
 #pragma unroll
-      for (int j = 0; j < TN; ++j) {
+      for (int g = 0; g < TN / 4; ++g) {
         const int lm = (i / 4) * (BM / (TM / 4)) + ty * 4 + (i % 4);
-        const int ln = (j / 4) * (BN / (TN / 4)) + tx * 4 + (j % 4);
-        part[lm * BN + ln] = acc[i][j];
+        const int ln = g * (BN / (TN / 4)) + tx * 4;
+        __stcg(reinterpret_cast<float4*>(part + lm * BN + ln),
+               make_float4(acc[i][g * 4], acc[i][g * 4 + 1], acc[i][g * 4 + 2], acc[i][g * 4 + 3]));
       }
     __threadfence();
     __syncthreads();
@@ -210,18 +242,32 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, TM, TN>::kThreads)
     __syncthreads();
     if (!s_last) return;
     __threadfence();
+    // splits outer, every element of the micro-tile in flight (float4 rows)
 #pragma unroll
     for (int i = 0; i < TM; ++i)
 #pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const int lm = (i / 4) * (BM / (TM / 4)) + ty * 4 + (i % 4);
-        const int ln = (j / 4) * (BN / (TN / 4)) + tx * 4 + (j % 4);
-        float s = 0.f;
-        for (int q = 0; q < P.splits; ++q)
-          s += __ldcg(work + P.work_off + (int64_t)q * ((int64_t)P.tiles * BM * BN) + (int64_t)tile * BM * BN +
-                      lm * BN + ln);
-        acc[i][j] = s;
-      }
+      for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+    for (int q = 0; q < P.splits; ++q) {
+      const float* pq = work + P.work_off + (int64_t)q * ((int64_t)P.tiles * BM * BN) + (int64_t)tile * BM * BN;
+      float4 v[TM][TN / 4];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int g = 0; g < TN / 4; ++g) {
+          const int lm = (i / 4) * (BM / (TM / 4)) + ty * 4 + (i % 4);
+          const int ln = g * (BN / (TN / 4)) + tx * 4;
+          v[i][g] = __ldcg(reinterpret_cast<const float4*>(pq + lm * BN + ln));
+        }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int g = 0; g < TN / 4; ++g) {
+          acc[i][g * 4 + 0] += v[i][g].x;
+          acc[i][g * 4 + 1] += v[i][g].y;
+          acc[i][g * 4 + 2] += v[i][g].z;
+          acc[i][g * 4 + 3] += v[i][g].w;
+        }
+    }
   }
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
@@ -305,7 +351,7 @@ GemmLaunch gemm_plan(std::vector<GemmProblem>& probs, bool a_kmajor, bool b_nmaj
     int splits = 1;
     if (tiles_all < target && kt >= 4) {
       splits = (int)std::min<int64_t>((target + tiles_all - 1) / tiles_all, kt / 2);
-      splits = std::max(1, std::min(splits, 16));
+      splits = std::max(1, std::min(splits, 8));
     }
     const int64_t part = (int64_t)splits * p.tiles * c.bm * c.bn;
     if (splits > 1 && (woff + part > work_cap_floats || counter + p.tiles > counter_cap)) splits = 1;

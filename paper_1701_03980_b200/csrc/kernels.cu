@@ -165,16 +165,21 @@ struct CellSlots {
   __device__ __forceinline__ int gg() const { return 2 + m; }
 };
 
+// One cell per block: the cell's slot pointers are staged in shared memory once.
 template <int M>
-__global__ void cell_fwd_kernel(CellArgs a) {
+__global__ void __launch_bounds__(256) cell_fwd_kernel(CellArgs a) {
   const CellSlots S(M);
+  __shared__ const float* sv[20];
   const int64_t per = (int64_t)a.batch * a.H;
-  const int64_t total = per * a.n;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int j = static_cast<int>(t / per);
-    const int64_t r = t - (int64_t)j * per;
+  const int bpc = (int)((per + 255) / 256);
+  const int j = blockIdx.x / bpc;
+  if ((int)threadIdx.x < a.nslot) sv[threadIdx.x] = a.val[(int64_t)threadIdx.x * a.n + j];
+  __syncthreads();
+  {
+    const int64_t r = (int64_t)(blockIdx.x % bpc) * 256 + threadIdx.x;
+    if (r >= per) return;
     const int b = static_cast<int>(r / a.H), u = static_cast<int>(r - (int64_t)b * a.H);
-    auto V = [&](int slot) { return a.val[(int64_t)slot * a.n + j]; };
+    auto V = [&](int slot) { return sv[slot]; };
     const float* G = V(0) + (int64_t)b * a.gw;
     const float xi = G[a.off_i + u], xo = G[a.off_o + u], xg = G[a.off_g + u];
     float xf[M > 0 ? M : 1];
@@ -214,14 +219,21 @@ template <int M, bool kLoopBatch>
 __global__ void __launch_bounds__(256) cell_bwd_kernel(CellArgs a) {
   const CellSlots S(M);
   __shared__ float red[M > 0 ? M : 1][8][32];
+  __shared__ const float* sv[20];
+  __shared__ float* sd[20];
   const int64_t per = kLoopBatch ? (int64_t)((a.H + 31) / 32) * 256 : (int64_t)a.batch * a.H;
-  const int64_t total = per * a.n;
-  const int64_t stride = kLoopBatch ? total : (int64_t)gridDim.x * blockDim.x;  // kLoopBatch: one pass
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += stride) {
-    const int j = static_cast<int>(t / per);
-    const int64_t q = t - (int64_t)j * per;
-    auto V = [&](int slot) { return a.val[(int64_t)slot * a.n + j]; };
-    auto D = [&](int slot) { return a.grad[(int64_t)slot * a.n + j]; };
+  const int bpc = (int)((per + 255) / 256);
+  const int j = blockIdx.x / bpc;
+  if ((int)threadIdx.x < a.nslot) {
+    sv[threadIdx.x] = a.val[(int64_t)threadIdx.x * a.n + j];
+    sd[threadIdx.x] = a.grad[(int64_t)threadIdx.x * a.n + j];
+  }
+  __syncthreads();
+  {
+    const int64_t q = (int64_t)(blockIdx.x % bpc) * 256 + threadIdx.x;
+    if (!kLoopBatch && q >= per) return;
+    auto V = [&](int slot) { return sv[slot]; };
+    auto D = [&](int slot) { return sd[slot]; };
     int b_lo, b_hi, b_step, u;
     if (kLoopBatch) {
       const int slice = threadIdx.x >> 5;
@@ -831,7 +843,7 @@ int launch_chain_bwd(const ChainArgs& a, cudaStream_t s) {
 }
 
 int launch_cell_fwd(const CellArgs& a, cudaStream_t s) {
-  const int g = grid_for((int64_t)a.n * a.batch * a.H);
+  const int g = a.n * (int)(((int64_t)a.batch * a.H + 255) / 256);
   switch (a.m) {
     case 0: cell_fwd_kernel<0><<<g, kThreads, 0, s>>>(a); break;
     case 1: cell_fwd_kernel<1><<<g, kThreads, 0, s>>>(a); break;
@@ -844,7 +856,7 @@ int launch_cell_bwd(const CellArgs& a, cudaStream_t s) {
   bool bcast = false;
   for (int k = 0; k < a.m; ++k) bcast = bcast || (a.cext_b1[k] && a.batch > 1);
   // broadcast variant: exactly one block per (cell, 32-unit chunk), single pass
-  const int g = bcast ? a.n * ((a.H + 31) / 32) : grid_for((int64_t)a.n * a.batch * a.H);
+  const int g = bcast ? a.n * ((a.H + 31) / 32) : a.n * (int)(((int64_t)a.batch * a.H + 255) / 256);
   switch (a.m * 2 + (bcast ? 1 : 0)) {
     case 0: cell_bwd_kernel<0, false><<<g, kThreads, 0, s>>>(a); break;
     case 1: cell_bwd_kernel<0, true><<<g, kThreads, 0, s>>>(a); break;

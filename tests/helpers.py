@@ -23,7 +23,7 @@ def parity(got, ref, rtol=RTOL, atol_frac=ATOL_FRAC, band=0.0, what=""):
     ref = np.asarray(ref, dtype=np.float64)
     assert got.shape == ref.shape, f"{what}: shape {got.shape} vs {ref.shape}"
     scale = float(np.abs(ref).max(initial=0.0))
-    tol = rtol * np.abs(ref) + max(atol_frac * scale, band)
+    tol = rtol * np.abs(ref) + np.maximum(atol_frac * scale, band)
     err = np.abs(got - ref)
     bad = err > tol
     assert not bad.any(), (
@@ -39,10 +39,10 @@ def gpu_ctx(seed=1, mb=256.0):
     return dy, dy.ComputationGraph(pools), dy.Model(pools, seed=seed)
 
 
-def oracle_ctx(seed=1):
+def oracle_ctx(seed=1, dtype=np.float32):
     from oracle import engine as orc
 
-    pools = orc.new_poolset()
+    pools = orc.new_poolset(dtype=dtype)
     return orc, orc.ComputationGraph(pools), orc.Model(pools, seed=seed)
 
 

@@ -97,12 +97,27 @@ def _run_steps(dy, cg, model, task, batches, rule, n_steps, record):
 
 
 def _compare_full(make_task, batches, rule="adam", n_steps=2):
+    """GPU vs the fp32 oracle on identical inputs and seeds.
+
+    Tolerance per element: rtol 1e-4 * |ref| + max(1e-6 * max|ref|,
+    2 * |ref32 - ref64|), where ref64 is the same oracle run in float64 from
+    the same (fp32-rounded) initial parameters: long fp32 reductions (bias and
+    weight gradients summed over hundreds of rows) carry the reference's own
+    rounding error, and the GPU's summation order may legitimately land on
+    the other side of it (SURVEY 7 calibrated-band recommendation)."""
     dyg, cgg, mg = gpu_ctx(seed=3, mb=1024)
     got, mg = _run_steps(dyg, cgg, mg, make_task(dyg, mg), batches, rule, n_steps, True)
     dyo, cgo, mo = oracle_ctx(seed=3)
-    ref, mo = _run_steps(dyo, cgo, mo, make_task(dyo, mo), batches, rule, n_steps, True)
+    task32 = make_task(dyo, mo)
+    init = [np.array(x.values, copy=True) for x in list(mo.parameters) + list(mo.lookups)]
+    ref, mo = _run_steps(dyo, cgo, mo, task32, batches, rule, n_steps, True)
+    _, cg64, m64 = oracle_ctx(seed=3, dtype=np.float64)
+    task64 = make_task(dyo, m64)
+    for x, v in zip(list(m64.parameters) + list(m64.lookups), init):
+        x.values[...] = v
+    ref64, m64 = _run_steps(dyo, cg64, m64, task64, batches, rule, n_steps, True)
     for s in range(n_steps):
-        parity(got[s]["loss"], ref[s]["loss"], what=f"loss{s}")
+        parity(got[s]["loss"], ref[s]["loss"], band=2 * abs(ref[s]["loss"] - ref64[s]["loss"]), what=f"loss{s}")
         for name, t in ref[s]["touched"].items():
             assert got[s]["touched"][name] == t  # bit-exact at every step
         # gradients: strict at every step under SGD; under Adam only before the
@@ -111,11 +126,15 @@ def _compare_full(make_task, batches, rule="adam", n_steps=2):
         if rule != "sgd" and s > 0:
             continue
         for name, g in ref[s]["grads"].items():
-            parity(got[s]["grads"][name], g, what=f"step{s} {name}")
+            band = 2 * np.abs(g - ref64[s]["grads"][name])
+            parity(got[s]["grads"][name], g, band=band, what=f"step{s} {name}")
         for name in ref[s]["touched"]:
-            parity(got[s]["lgrads"][name], ref[s]["lgrads"][name], what=f"step{s} {name} rows")
-    band = 0.0 if rule == "sgd" else 2 * 1e-3 * n_steps
-    for p, q in zip(mg.parameters, mo.parameters):
+            band = 2 * np.abs(ref[s]["lgrads"][name] - ref64[s]["lgrads"][name])
+            parity(got[s]["lgrads"][name], ref[s]["lgrads"][name], band=band, what=f"step{s} {name} rows")
+    for p, q, r in zip(mg.parameters, mo.parameters, m64.parameters):
+        band = 2 * np.abs(pvals(q) - pvals(r))
+        if rule != "sgd":
+            band = np.maximum(band, 2 * 1e-3 * n_steps)
         parity(pvals(p), pvals(q), band=band, what=f"final {p.name}")
 
 

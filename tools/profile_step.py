@@ -52,3 +52,36 @@ for k, v in acc.items():
     v = v[args.warmup:]
     print(f"{k:14s} {1e3 * np.mean(v):8.3f} ms")
 print("launches", cg._counters()[5], "plan", cg.plan_stats())
+
+# ---- live device-only per-class timing: stall the GPU with a spin kernel so
+# the host enqueues the whole step first, then read the CUDA-event windows
+classes = ("gemm_fwd", "gemm_dx", "gemm_dw", "pnls_fwd", "pnls_bwd", "elementwise", "gather", "scatter_add",
+           "bias_colsum", "other")
+cg.profile_enable(classes)
+tot = {c: 0.0 for c in classes}
+cnt = {c: 0 for c in classes}
+n_meas = 3
+for i in range(n_meas):
+    torch.cuda.synchronize()
+    cg.profile_reset()
+    cg.renew()
+    loss = bench.call_loss(task, cg, data[i])
+    cg._prepare()
+    torch.cuda._sleep(int(40e6))  # ~20 ms spin
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    cg.backward(loss)
+    tr.update()
+    e1.record()
+    torch.cuda.synchronize()
+    step_ms = e0.elapsed_time(e1)
+    for c in classes:
+        r = cg.profile_read(c)
+        tot[c] += r["ms"]
+        cnt[c] += r["launches"]
+    print(f"device-only step {step_ms:.3f} ms")
+for c in classes:
+    if cnt[c]:
+        print(f"  {c:12s} {tot[c] / n_meas:8.3f} ms/step  {cnt[c] / n_meas:6.1f} launches  "
+              f"{1e3 * tot[c] / max(1, cnt[c]):7.1f} us/launch")
