@@ -784,14 +784,18 @@ static void flush_gemm(dg_graph* g, Plan& plan, GemmBatch& gb) {
   const int64_t temp = (gb.temp_floats + 63) & ~int64_t(63);
   float* work = reinterpret_cast<float*>(scratch_base(g)) + temp;
   const int64_t cap = (int64_t)(scratch_bytes(g) / 4) - temp;
-  GemmLaunch L = gemm_plan(gb.probs, gb.a_kmajor, gb.b_nmajor, cap, kCounterCap);
+  // wide problems run on the tensor cores (tcgen05 3xTF32), the rest on the
+  // grouped SIMT kernel
+  const bool tc = tc_gemm_eligible(gb.probs);
+  GemmLaunch L = tc ? tc_gemm_plan(gb.probs, gb.a_kmajor, gb.b_nmajor)
+                    : gemm_plan(gb.probs, gb.a_kmajor, gb.b_nmajor, cap, kCounterCap);
   const size_t off = plan.blob.push(gb.probs);
   const GemmProblem* pdev = dev_at<GemmProblem>(g, off);
   int* counters = counter_base(g);
   cudaStream_t st = g->stream;
   auto post = std::move(gb.post);
-  plan.ops.push_back([L, pdev, work, counters, st, post](char*) {
-    int n = launch_gemm_group(L, pdev, work, counters, st);
+  plan.ops.push_back([L, pdev, work, counters, st, post, tc](char*) {
+    int n = tc ? launch_tc_gemm(L, pdev, st) : launch_gemm_group(L, pdev, work, counters, st);
     for (auto& f : post) n += f();
     return n;
   });

@@ -15,6 +15,7 @@
 // partial tile to the workspace, bumps a per-tile counter, and the CTA that
 // arrives last reduces the partials in split order and runs the epilogue.
 // fp32 throughout for the rtol 1e-4 parity bar.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -22,6 +23,8 @@
 #include <vector>
 
 #include "kernels.cuh"
+
+namespace cgrp = cooperative_groups;
 
 namespace dg {
 namespace {
@@ -97,13 +100,18 @@ struct TileLoad {
   }
 };
 
-template <int BM, int BN, int BK, int TM, int TN, bool kAK, bool kBN>
+// kCl: split-K across the CTAs of a thread-block cluster (cluster size =
+// splits, one cluster per output tile); partial tiles are reduced through
+// distributed shared memory in fixed split order.  Otherwise split-K goes
+// through global partials + a per-tile arrival counter (last CTA reduces).
+template <int BM, int BN, int BK, int TM, int TN, bool kAK, bool kBN, bool kCl>
 __global__ void __launch_bounds__(Cfg<BM, BN, BK, TM, TN>::kThreads)
     gemm_group_kernel(const GemmProblem* __restrict__ probs, int n_probs, float* __restrict__ work,
                       int* __restrict__ counters) {
   using C = Cfg<BM, BN, BK, TM, TN>;
   __shared__ __align__(16) float As[2][BK * C::kApad];
   __shared__ __align__(16) float Bs[2][BK * C::kBpad];
+  __shared__ __align__(16) float red[kCl ? BM * BN : 4];
   __shared__ GemmProblem P;
   __shared__ int s_last;
   // per-segment row pointers of the tile's fixed rows (A rows when A is
@@ -121,8 +129,9 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, TM, TN>::kThreads)
   }
   __syncthreads();
   const int local = blockIdx.x - P.cta0;
-  const int z = local / P.tiles;
-  const int tile = local - z * P.tiles;
+  // cluster mode: the splits of one tile are consecutive CTAs (one cluster)
+  const int z = kCl ? local % P.splits : local / P.tiles;
+  const int tile = kCl ? local / P.splits : local - z * P.tiles;
   const int m0 = (tile / P.tiles_n) * BM, n0 = (tile % P.tiles_n) * BN;
   if (!kAK) {
     for (int i = threadIdx.x; i < P.n_seg * BM; i += blockDim.x) {
@@ -220,6 +229,39 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, TM, TN>::kThreads)
   }
 
   const bool has_bias = P.bias.rows != nullptr || P.bias.base != nullptr;
+  if (kCl) {
+    // partial tile -> own shared memory; after the cluster barrier CTA z
+    // reduces rows [z*BM/S, (z+1)*BM/S) of the tile over the S partials read
+    // through DSMEM (fixed split order: deterministic) and writes them out
+    cgrp::cluster_group cl = cgrp::this_cluster();
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int g = 0; g < TN / 4; ++g) {
+        const int lm = (i / 4) * (BM / (TM / 4)) + ty * 4 + (i % 4);
+        const int ln = g * (BN / (TN / 4)) + tx * 4;
+        *reinterpret_cast<float4*>(red + lm * BN + ln) =
+            make_float4(acc[i][g * 4], acc[i][g * 4 + 1], acc[i][g * 4 + 2], acc[i][g * 4 + 3]);
+      }
+    cl.sync();
+    const int S = P.splits;
+    const int rows = (BM + S - 1) / S;
+    const int r0 = z * rows, r1 = min(BM, r0 + rows);
+    for (int e = threadIdx.x; e < (r1 - r0) * BN; e += blockDim.x) {
+      const int lm = r0 + e / BN, ln = e % BN;
+      float s = 0.f;
+      for (int q = 0; q < S; ++q) s += cl.map_shared_rank(red, q)[lm * BN + ln];
+      const int m = m0 + lm, n = n0 + ln;
+      if (m < P.M && n < P.N) {
+        float* crow = const_cast<float*>(op_row(P.C, m));
+        if (has_bias) s += op_row(P.bias, m)[n];
+        if (P.accumulate) s += crow[n];
+        crow[n] = s;
+      }
+    }
+    cl.sync();  // keep every CTA's partial alive until all reads are done
+    return;
+  }
   if (P.splits > 1) {
     // partial tile -> workspace; the last split to arrive reduces in order
     float* part = work + P.work_off + (int64_t)z * ((int64_t)P.tiles * BM * BN) + (int64_t)tile * BM * BN;
@@ -292,17 +334,37 @@ struct CfgInfo {
 };
 constexpr CfgInfo kCfg[4] = {{128, 128, 8}, {64, 64, 16}, {64, 32, 32}, {32, 32, 32}};
 
+template <int BM, int BN, int BK, int TM, int TN, bool kAK, bool kBN>
+void launch_one(const GemmLaunch& L, const GemmProblem* probs, float* work, int* counters, cudaStream_t s) {
+  using C = Cfg<BM, BN, BK, TM, TN>;
+  if (L.cluster > 0) {
+    if constexpr (BM * BN <= 64 * 64) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(L.ctas);
+      cfg.blockDim = dim3(C::kThreads);
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = L.cluster;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, gemm_group_kernel<BM, BN, BK, TM, TN, kAK, kBN, true>, probs, L.n_probs, work,
+                         counters);
+    }
+    return;
+  }
+  gemm_group_kernel<BM, BN, BK, TM, TN, kAK, kBN, false><<<L.ctas, C::kThreads, 0, s>>>(probs, L.n_probs, work,
+                                                                                        counters);
+}
+
 template <int BM, int BN, int BK, int TM, int TN>
 void launch_major(const GemmLaunch& L, const GemmProblem* probs, float* work, int* counters, cudaStream_t s) {
-  using C = Cfg<BM, BN, BK, TM, TN>;
-  if (L.a_kmajor && L.b_nmajor)
-    gemm_group_kernel<BM, BN, BK, TM, TN, true, true><<<L.ctas, C::kThreads, 0, s>>>(probs, L.n_probs, work, counters);
-  else if (L.a_kmajor)
-    gemm_group_kernel<BM, BN, BK, TM, TN, true, false><<<L.ctas, C::kThreads, 0, s>>>(probs, L.n_probs, work, counters);
-  else if (L.b_nmajor)
-    gemm_group_kernel<BM, BN, BK, TM, TN, false, true><<<L.ctas, C::kThreads, 0, s>>>(probs, L.n_probs, work, counters);
-  else
-    gemm_group_kernel<BM, BN, BK, TM, TN, false, false><<<L.ctas, C::kThreads, 0, s>>>(probs, L.n_probs, work, counters);
+  if (L.a_kmajor && L.b_nmajor) launch_one<BM, BN, BK, TM, TN, true, true>(L, probs, work, counters, s);
+  else if (L.a_kmajor) launch_one<BM, BN, BK, TM, TN, true, false>(L, probs, work, counters, s);
+  else if (L.b_nmajor) launch_one<BM, BN, BK, TM, TN, false, true>(L, probs, work, counters, s);
+  else launch_one<BM, BN, BK, TM, TN, false, false>(L, probs, work, counters, s);
 }
 
 bool base_vec_ok(const Operand& o) {
@@ -344,22 +406,38 @@ GemmLaunch gemm_plan(std::vector<GemmProblem>& probs, bool a_kmajor, bool b_nmaj
   }
   // split-K so that roughly two waves of 256-thread-equivalents are in flight
   const int64_t target = (int64_t)148 * 2 * 256 / threads;
+  // smaller tiles: one uniform split count per launch, the splits of a tile
+  // forming a thread-block cluster (DSMEM reduction, no global partials)
+  L.cluster = 0;
+  if (L.cfg != 0) {
+    int min_kt = 1 << 30;
+    for (auto& p : probs) {
+      int kt = 0;
+      for (int s = 0; s < p.n_seg; ++s) kt += (p.seg[s].K + c.bk - 1) / c.bk;
+      min_kt = std::min(min_kt, kt);
+    }
+    int S = (int)std::min<int64_t>((target + tiles_all - 1) / tiles_all, 8);
+    S = std::max(1, std::min(S, std::max(1, min_kt)));
+    if (S > 1) L.cluster = S;
+  }
   int64_t cta = 0, counter = 0, woff = 0;
   for (auto& p : probs) {
     int kt = 0;
     for (int s = 0; s < p.n_seg; ++s) kt += (p.seg[s].K + c.bk - 1) / c.bk;
     int splits = 1;
-    if (tiles_all < target && kt >= 4) {
+    if (L.cluster > 0) {
+      splits = L.cluster;
+    } else if (tiles_all < target && kt >= 4) {
       splits = (int)std::min<int64_t>((target + tiles_all - 1) / tiles_all, kt / 2);
       splits = std::max(1, std::min(splits, 8));
     }
     const int64_t part = (int64_t)splits * p.tiles * c.bm * c.bn;
-    if (splits > 1 && (woff + part > work_cap_floats || counter + p.tiles > counter_cap)) splits = 1;
+    if (L.cluster == 0 && splits > 1 && (woff + part > work_cap_floats || counter + p.tiles > counter_cap)) splits = 1;
     p.splits = splits;
     p.cta0 = (int)cta;
     p.counter0 = (int)counter;
     p.work_off = woff;
-    if (splits > 1) {
+    if (splits > 1 && L.cluster == 0) {
       woff += part;
       counter += p.tiles;
     }

@@ -189,6 +189,7 @@ struct GemmProblem {
 };
 struct GemmLaunch {
   int cfg, n_probs, ctas;
+  int cluster;  // > 0: split-K across a thread-block cluster of this size
   bool a_kmajor, b_nmajor;
   int64_t work_floats;
   double flops;
@@ -199,6 +200,12 @@ GemmLaunch gemm_plan(std::vector<GemmProblem>& probs, bool a_kmajor, bool b_nmaj
 // counters: zero-initialised ints (>= sum of split problems' tiles); left zero
 int launch_gemm_group(const GemmLaunch& L, const GemmProblem* probs_dev, float* work, int* counters,
                       cudaStream_t s);
+// tcgen05 3xTF32 path (tcgemm.cu) for wide single-segment problems
+bool tc_gemm_eligible(const std::vector<GemmProblem>& probs);
+GemmLaunch tc_gemm_plan(std::vector<GemmProblem>& probs, bool a_kmajor, bool b_nmajor);
+int launch_tc_gemm(const GemmLaunch& L, const GemmProblem* probs_dev, cudaStream_t s);
+// DG_TC=0 in the environment disables the tensor-core path (A/B checks)
+bool tc_gemm_enabled();
 
 // ------------------------------------------------------------- trainers
 struct TensorSeg { float* w; float* g; float* s0; float* s1; int64_t n; };
