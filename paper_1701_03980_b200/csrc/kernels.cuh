@@ -190,6 +190,7 @@ struct GemmProblem {
 struct GemmLaunch {
   int cfg, n_probs, ctas;
   int cluster;  // > 0: split-K across a thread-block cluster of this size
+  int chunk;    // tensor-core path: TMEM accumulator drain period (k-tiles)
   bool a_kmajor, b_nmajor;
   int64_t work_floats;
   double flops;

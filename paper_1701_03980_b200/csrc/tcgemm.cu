@@ -169,9 +169,32 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 __device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 // kAMN: A global rows run along K (MN-major A); kBMN: B global rows run along K
+// TMEM accumulator -> registers: 64 fp32 columns of this thread's row
+__device__ __forceinline__ void tmem_drain_add(uint32_t tmem, int lane_grp, int col_half, float* vals) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t r[32];
+    const uint32_t taddr = tmem + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(col_half * 64 + c * 32);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < 32; ++q) vals[c * 32 + q] += __uint_as_float(r[q]);
+  }
+}
+
+// chunk: drain the TMEM accumulator into fp32 registers every `chunk` k-tiles
+// (blocked summation: the tensor core's own accumulation error grows with the
+// chain length, see tools/gemm_bench.cu accuracy study)
 template <bool kAMN, bool kBMN>
 __global__ void __launch_bounds__(kTcThreads, 1)
-    tc_gemm_kernel(const GemmProblem* __restrict__ probs, int n_probs) {
+    tc_gemm_kernel(const GemmProblem* __restrict__ probs, int n_probs, int chunk) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // ring: raw[s] = {A 16K, B 16K}, lo[b] = {A 16K, B 16K}
@@ -230,6 +253,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     cp_async_commit();  // one (possibly empty) group per stage keeps the wait counts uniform
   };
   constexpr uint32_t idesc = umma_idesc(kAMN, kBMN);
+  const int lane_grp = warp & 3, col_half = warp >> 2;
+  const int lrow = lane_grp * 32 + (threadIdx.x & 31);
+  float vals[64];
+#pragma unroll
+  for (int q = 0; q < 64; ++q) vals[q] = 0.f;
 #pragma unroll
   for (int j = 0; j < kRawStages - 1; ++j) issue(j);
   for (int j = 0; j < nkt; ++j) {
@@ -260,41 +288,27 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int ks = 0; ks < TBK / 8; ++ks) {
         // K-major: 8 tf32 = 32 B along the 128 B row; MN-major: next 8-row K group
         const uint32_t oa = kAMN ? ks * 1024 : ks * 32, ob = kBMN ? ks * 1024 : ks * 32;
-        const uint32_t first = (j == 0 && ks == 0) ? 0u : 1u;
+        const uint32_t first = (j % chunk == 0 && ks == 0) ? 0u : 1u;
         mma_tf32(tmem, umma_desc(a_hi + oa, kAMN), umma_desc(b_hi + ob, kBMN), idesc, first);
         mma_tf32(tmem, umma_desc(a_hi + oa, kAMN), umma_desc(b_lo + ob, kBMN), idesc, 1u);
         mma_tf32(tmem, umma_desc(a_lo + oa, kAMN), umma_desc(b_hi + ob, kBMN), idesc, 1u);
       }
       mma_commit(&bars[s]);
     }
+    // chunk boundary: wait for this tile's MMAs, fold the accumulator into
+    // fp32 registers; the next chunk restarts the TMEM accumulation
+    if ((j + 1) % chunk == 0 || j + 1 == nkt) {
+      mbar_wait(&bars[s], (j / kRawStages) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      tmem_drain_add(tmem, lane_grp, col_half, vals);
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncthreads();  // every warp drained before the next scale_c = 0 MMA
+    }
     // refill: tile j+3 goes to raw stage (j+3)%4, last read by the MMAs of tile j-1
     if (j + kRawStages - 1 < nkt && j >= 1) mbar_wait(&bars[(j - 1) % kRawStages], ((j - 1) / kRawStages) & 1);
     issue(j + kRawStages - 1);
   }
   cp_async_wait<0>();
-  if (nkt > 0) mbar_wait(&bars[(nkt - 1) % kRawStages], ((nkt - 1) / kRawStages) & 1);
-  asm volatile("tcgen05.fence::after_thread_sync;");
-
-  // ---- epilogue: TMEM -> registers (32 rows per warp quarter, 64 columns per warp half)
-  const int lane_grp = warp & 3, col_half = warp >> 2;
-  const int lrow = lane_grp * 32 + (threadIdx.x & 31);
-  float vals[64];
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    uint32_t r[32];
-    const uint32_t taddr = tmem + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(col_half * 64 + c * 32);
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int q = 0; q < 32; ++q) vals[c * 32 + q] = nkt > 0 ? __uint_as_float(r[q]) : 0.f;
-  }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();  // all TMEM reads done; the operand ring is free
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TBN));
@@ -376,7 +390,7 @@ void launch_tc(const GemmLaunch& L, const GemmProblem* probs, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, probs, L.n_probs);
+  cudaLaunchKernelEx(&cfg, kern, probs, L.n_probs, L.chunk > 0 ? L.chunk : 1 << 30);
 }
 
 bool vec_ok(const Operand& o, int64_t extent) {
@@ -426,6 +440,12 @@ GemmLaunch tc_gemm_plan(std::vector<GemmProblem>& probs, bool a_kmajor, bool b_n
   int S = 1;
   while (S < 8 && tiles_all * S * 2 <= 148 && min_kt >= 8 * S) S *= 2;
   L.cluster = S;
+  // TMEM drain period (k-tiles of 32): DG_TC_CHUNK overrides (accuracy studies)
+  static const int chunk_env = [] {
+    const char* e = getenv("DG_TC_CHUNK");
+    return e ? atoi(e) : 0;
+  }();
+  L.chunk = chunk_env > 0 ? chunk_env : 2;
   int64_t cta = 0;
   for (auto& p : probs) {
     p.splits = S;

@@ -99,12 +99,19 @@ def _run_steps(dy, cg, model, task, batches, rule, n_steps, record):
 def _compare_full(make_task, batches, rule="adam", n_steps=2):
     """GPU vs the fp32 oracle on identical inputs and seeds.
 
-    Tolerance per element: rtol 1e-4 * |ref| + max(1e-6 * max|ref|,
+    Tolerance per element: rtol 1e-4 * |ref| + max(1e-5 * max|ref|,
     2 * |ref32 - ref64|), where ref64 is the same oracle run in float64 from
     the same (fp32-rounded) initial parameters: long fp32 reductions (bias and
     weight gradients summed over hundreds of rows) carry the reference's own
     rounding error, and the GPU's summation order may legitimately land on
-    the other side of it (SURVEY 7 calibrated-band recommendation)."""
+    the other side of it (SURVEY 7 calibrated-band recommendation).  The
+    1e-5 floor (vs 1e-6 for the small golden cases) covers the wide affines
+    that run on the tensor cores in 3xTF32: each product carries ~2^-22
+    relative error (truncated TF32 residual), measured at 1-2e-6 of the
+    output scale for K = 2176..10000 (tools/gemm_bench.cu accuracy study);
+    only elements that cancel to ~1e-5 of their tensor's scale reach the
+    floor, everything else is held to rtol 1e-4."""
+    floor = 1e-5
     dyg, cgg, mg = gpu_ctx(seed=3, mb=1024)
     got, mg = _run_steps(dyg, cgg, mg, make_task(dyg, mg), batches, rule, n_steps, True)
     dyo, cgo, mo = oracle_ctx(seed=3)
@@ -117,7 +124,8 @@ def _compare_full(make_task, batches, rule="adam", n_steps=2):
         x.values[...] = v
     ref64, m64 = _run_steps(dyo, cg64, m64, task64, batches, rule, n_steps, True)
     for s in range(n_steps):
-        parity(got[s]["loss"], ref[s]["loss"], band=2 * abs(ref[s]["loss"] - ref64[s]["loss"]), what=f"loss{s}")
+        parity(got[s]["loss"], ref[s]["loss"], band=2 * abs(ref[s]["loss"] - ref64[s]["loss"]), atol_frac=floor,
+               what=f"loss{s}")
         for name, t in ref[s]["touched"].items():
             assert got[s]["touched"][name] == t  # bit-exact at every step
         # gradients: strict at every step under SGD; under Adam only before the
@@ -127,15 +135,16 @@ def _compare_full(make_task, batches, rule="adam", n_steps=2):
             continue
         for name, g in ref[s]["grads"].items():
             band = 2 * np.abs(g - ref64[s]["grads"][name])
-            parity(got[s]["grads"][name], g, band=band, what=f"step{s} {name}")
+            parity(got[s]["grads"][name], g, band=band, atol_frac=floor, what=f"step{s} {name}")
         for name in ref[s]["touched"]:
             band = 2 * np.abs(ref[s]["lgrads"][name] - ref64[s]["lgrads"][name])
-            parity(got[s]["lgrads"][name], ref[s]["lgrads"][name], band=band, what=f"step{s} {name} rows")
+            parity(got[s]["lgrads"][name], ref[s]["lgrads"][name], band=band, atol_frac=floor,
+                   what=f"step{s} {name} rows")
     for p, q, r in zip(mg.parameters, mo.parameters, m64.parameters):
         band = 2 * np.abs(pvals(q) - pvals(r))
         if rule != "sgd":
             band = np.maximum(band, 2 * 1e-3 * n_steps)
-        parity(pvals(p), pvals(q), band=band, what=f"final {p.name}")
+        parity(pvals(p), pvals(q), band=band, atol_frac=floor, what=f"final {p.name}")
 
 
 def test_ptb_mb16_full_size_vs_oracle():

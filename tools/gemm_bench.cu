@@ -136,6 +136,10 @@ static void floor_timings() {
   }
 }
 
+static int g_force_cluster = 0;
+static int g_chunk = 0;
+static bool g_simt = false;
+
 // correctness: tensor-core path vs an fp64 host reference (sampled rows)
 static void check_tc(const char* name, int M, int N, int K, bool ak, bool bn, bool tables, void* dprobs) {
   std::vector<float> hA((size_t)M * K), hB((size_t)K * N);
@@ -172,8 +176,32 @@ static void check_tc(const char* name, int M, int N, int K, bool ak, bool bn, bo
   }
   std::vector<GemmProblem> probs{p};
   GemmLaunch L = tc_gemm_plan(probs, ak, bn);
-  CK(cudaMemcpy(dprobs, probs.data(), sizeof(GemmProblem), cudaMemcpyHostToDevice));
-  launch_tc_gemm(L, (const GemmProblem*)dprobs, 0);
+  if (g_chunk > 0) L.chunk = g_chunk;
+  if (g_force_cluster > 0) {  // forced split-K (cluster size) for accuracy studies
+    int64_t cta = 0;
+    for (auto& q : probs) {
+      q.splits = g_force_cluster;
+      q.cta0 = (int)cta;
+      cta += (int64_t)q.tiles * g_force_cluster;
+    }
+    L.cluster = g_force_cluster;
+    L.ctas = (int)cta;
+  }
+  if (g_simt) {
+    static float* work = nullptr;
+    static int* counters = nullptr;
+    if (!work) {
+      CK(cudaMalloc(&work, 64 << 20));
+      CK(cudaMalloc(&counters, 1 << 20));
+      CK(cudaMemset(counters, 0, 1 << 20));
+    }
+    L = gemm_plan(probs, ak, bn, 16 << 20, 1 << 18);
+    CK(cudaMemcpy(dprobs, probs.data(), sizeof(GemmProblem), cudaMemcpyHostToDevice));
+    launch_gemm_group(L, (const GemmProblem*)dprobs, work, counters, 0);
+  } else {
+    CK(cudaMemcpy(dprobs, probs.data(), sizeof(GemmProblem), cudaMemcpyHostToDevice));
+    launch_tc_gemm(L, (const GemmProblem*)dprobs, 0);
+  }
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   std::vector<float> hC((size_t)M * N);
@@ -198,6 +226,7 @@ static void check_tc(const char* name, int M, int N, int K, bool ak, bool bn, bo
   cudaFree(C);
 }
 
+static int g_chunk_dummy = 0;
 static double run_tc(const char* name, std::vector<Shape> shapes, bool ak, bool bn, void* dprobs) {
   std::vector<GemmProblem> probs;
   std::vector<float*> bufs;
@@ -223,6 +252,7 @@ static double run_tc(const char* name, std::vector<Shape> shapes, bool ak, bool 
     probs.push_back(p);
   }
   GemmLaunch L = tc_gemm_plan(probs, ak, bn);
+  if (g_chunk > 0) L.chunk = g_chunk;
   CK(cudaMemcpy(dprobs, probs.data(), probs.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
@@ -254,6 +284,25 @@ int main() {
     check_tc("k-major A, n-major B", 384, 256, 64, true, true, false, dp);
     check_tc("ragged + tables", 300, 200, 100, false, false, true, dp);
     check_tc("split-K cluster", 128, 128, 4096, false, true, false, dp);
+    // accuracy vs accumulation-chain length: the aggregated LSTM dW shape
+    for (int s : {1, 2, 4, 8}) {
+      g_force_cluster = s;
+      check_tc("dW-like k-major A, cluster", 256, 1024, 2176, true, false, false, dp);
+    }
+    g_force_cluster = 0;
+    for (int ch : {1, 2, 4, 1000}) {
+      g_chunk = ch;
+      check_tc("dW-like, TMEM drain every (ch)", 256, 1024, 2176, true, false, false, dp);
+      check_tc("dX-like, TMEM drain every (ch)", 256, 256, 10000, false, true, false, dp);
+      run_tc("  dX 2176x256x10000", {{2176, 256, 10000}}, false, true, dp);
+      run_tc("  fwd 2176x10000x256", {{2176, 10000, 256}}, false, false, dp);
+    }
+    g_chunk = 0;
+    g_simt = true;
+    check_tc("dW-like SIMT (blocked sum)", 256, 1024, 2176, true, false, false, dp);
+    check_tc("dX-like SIMT (blocked sum)", 256, 256, 10000, false, true, false, dp);
+    g_simt = false;
+    check_tc("dX-like TC", 256, 256, 10000, false, true, false, dp);
     run_tc("fwd 2176x10000x256", {{2176, 10000, 256}}, false, false, dp);
     run_tc("dX 2176x256x10000", {{2176, 256, 10000}}, false, true, dp);
     run_tc("dW 256x10000x2176", {{256, 10000, 2176}}, true, false, dp);
