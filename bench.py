@@ -293,7 +293,7 @@ def run_b200(args, cfg):
     # one untimed pass over fresh graphs of the same shapes warms allocations
     barrier()
     prof_classes = ("gemm_fwd", "gemm_dx", "gemm_dw", "pnls_fwd", "pnls_bwd", "elementwise", "gather",
-                    "scatter_add", "bias_colsum")
+                    "scatter_add", "bias_colsum", "rnn_fwd", "rnn_bwd", "other")
     for g, _ in graphs:
         g.profile_enable(prof_classes)
         g.profile_reset()

@@ -1,8 +1,8 @@
 #!/bin/bash
-# one GPU session: smoke, gpu tests, micro-bench, bench
+# one GPU session: smoke, gpu tests, bench (+ A/B without the persistent recurrence)
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 900 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-./tools/gemm_bench > gpurun_out/gemm_bench.txt 2>&1
-timeout 600 python bench.py --steps 10 --warmup 3 --cpu-budget 10 > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 900 python -m pytest tests -m gpu -q -x --timeout 600 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --steps 10 --warmup 3 --cpu-budget 5 > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+DG_RNN=0 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu > gpurun_out/bench_nornn.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_nornn.log

@@ -139,13 +139,17 @@ int dg_graph_plan_stats(dg_graph* g, int64_t* out8);
 /* live profiling: CUDA events around every launch of the enabled op classes
  * (bit c of class_mask; classes: 0 affine GEMM fwd, 1 dX GEMM, 2 aggregated dW
  * GEMM, 3 pnls fwd, 4 pnls bwd, 5 elementwise, 6 gather, 7 sorted scatter-add,
- * 8 bias column sums, 9 other).  dg_profile_read syncs and returns
+ * 8 bias column sums, 9 other, 10 persistent LSTM forward, 11 persistent LSTM
+ * backward).  dg_profile_read syncs and returns
  * out4 = {total ms, launches, algorithmic flops, algorithmic bytes}. */
 int dg_profile_enable(dg_graph* g, uint32_t class_mask);
 /* host-only planner introspection for nodes [lo, hi]: out8 = {units, groups,
  * fused cells, add chains, nodes inside cells, largest group, lookup leaves,
  * input leaves}.  Touches no device memory. */
 int dg_schedule_stats(dg_graph* g, int32_t lo, int32_t hi, int64_t* out8);
+/* host-only: persistent LSTM stacks the planner forms over nodes [lo, hi]
+ * (out4 = stacks, chains, steps, CTAs of one launch per stack) */
+int dg_schedule_rnn_stats(dg_graph* g, int32_t lo, int32_t hi, int64_t* out4);
 int dg_profile_read(dg_graph* g, int32_t cls, double* out4);
 int dg_profile_reset(dg_graph* g);
 

@@ -100,6 +100,7 @@ def _declare(lib):
         "dg_profile_read": (ctypes.c_int, [c_vp, c_i32, c_vp]),
         "dg_profile_reset": (ctypes.c_int, [c_vp]),
         "dg_schedule_stats": (ctypes.c_int, [c_vp, c_i32, c_i32, c_vp]),
+        "dg_schedule_rnn_stats": (ctypes.c_int, [c_vp, c_i32, c_i32, c_vp]),
         "dg_trainer_create": (ctypes.c_int, [ctypes.c_int, c_f32, c_f32, c_f32, c_f32, c_f32, c_f32, ctypes.c_int,
                                               ctypes.POINTER(c_vp)]),
         "dg_trainer_destroy": (ctypes.c_int, [c_vp]),
@@ -119,7 +120,7 @@ def _declare(lib):
 
 
 PROFILE_CLASSES = ("gemm_fwd", "gemm_dx", "gemm_dw", "pnls_fwd", "pnls_bwd", "elementwise", "gather",
-                   "scatter_add", "bias_colsum", "other")
+                   "scatter_add", "bias_colsum", "other", "rnn_fwd", "rnn_bwd")
 
 
 def lib():

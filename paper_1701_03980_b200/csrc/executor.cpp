@@ -128,7 +128,7 @@ struct Node {
 
 static inline size_t round64(size_t n) { return (n + 63) & ~size_t(63); }
 
-enum UnitKind { U_NODE = 0, U_CHAIN = 1, U_CELL = 2 };
+enum UnitKind { U_NODE = 0, U_CHAIN = 1, U_CELL = 2, U_RNN = 3 };
 
 struct Unit {
   int type;                 // U_NODE / U_CHAIN / U_CELL
@@ -140,12 +140,30 @@ struct Unit {
   int m = 0;
   int off[5] = {0, 0, 0, 0, 0};
   int gw = 0, H = 0;
+  int rnn = -1;  // U_RNN: index into Schedule::rnns
   int first() const { return nodes.front(); }
   int last() const { return nodes.back(); }
 };
 
+// A chain of LSTM steps sharing (Wx, Wh, b) whose h_t / c_t feed step t+1
+// (builders.py:92-101), run by the persistent recurrence kernels (rnn.cu).
+struct RnnChainPlan {
+  std::vector<Unit> cells;  // per step: the U_CELL (m = 1) unit
+  std::vector<int> G;       // per step: the gate affine node
+  int64_t hb = -1, hWx = -1, hWh = -1;
+  int H = 0, K_in = 0, B = 0, gw = 0;
+  int off[4] = {0, 0, 0, 0};  // i, f, o, g gate offsets into G
+  int src = -1;               // stacked producer chain (index in the stack)
+  int cons = -1;              // consumer chain
+  int n_s = 0, n_u = 0;
+};
+struct RnnStack {
+  std::vector<RnnChainPlan> chains;
+  int bs = 1, ctas = 0;
+};
+
 struct Group {
-  int kind;                 // node kind, -1 add chain, -2 gated cell
+  int kind;                 // node kind, -1 add chain, -2 gated cell, -3 LSTM stack
   std::vector<int> units;   // unit ids, ascending
   int level = 0;            // scheduling level (groups of one level are independent)
 };
@@ -157,6 +175,7 @@ struct Schedule {
   std::vector<int> input_nodes;    // `input` leaves
   std::vector<int> lookup_nodes;   // lookup / lookup_batch leaves
   std::vector<int> param_nodes;
+  std::vector<RnnStack> rnns;
 };
 
 struct AffineUse {  // weight-gradient aggregation (one GEMM per parameter)
@@ -281,6 +300,11 @@ static int64_t param_handle_of(const dg_graph* g, int node) {
 // Signature of a unit: everything that must agree for one batched launch.
 static uint64_t unit_signature(const dg_graph* g, const Unit& u) {
   SigHash s;
+  if (u.type == U_RNN) {
+    // stacks that become ready together share one persistent launch
+    s.add(U_RNN);
+    return s.h;
+  }
   if (u.type == U_CELL) {
     const Node& G = g->nodes[u.ins[0]];
     s.add(U_CELL);
@@ -468,6 +492,216 @@ static bool match_cell(const dg_graph* g, int h, const std::vector<int>& consume
   return true;
 }
 
+// ------------------------------------------------------------- LSTM chains
+// Device limits the planner sizes persistent launches against (sm_100a B200:
+// 148 SMs, 227 KB opt-in shared memory per CTA).  Fixed constants so the plan
+// is the same with or without a device (host-only planner tests).
+static constexpr int kSmCount = 148;
+static constexpr size_t kSmemMax = 227 * 1024 - 1024;  // dynamic (static step tables aside)
+static constexpr int kFlagInts = 65536;  // arrival counters (rnn.cu), end of the counter region
+
+// CJ (dG columns staged per chunk) for a backward launch: the largest multiple
+// of 32 (<= max gw) that fits next to the resident W^T slices.
+static int rnn_pick_cj(int gw, int gw_c, int bs) {
+  int cj = std::max(gw, gw_c);
+  cj = (cj + 31) & ~31;
+  while (cj > 32 && rnn_bwd_smem(gw, gw_c, bs, cj) > kSmemMax) cj -= 32;
+  return cj;
+}
+
+// Groups matched LSTM cells (m = 1) into chains and stacks:
+//   step t+1 of a chain: gates = affine(b, Wx, x, Wh, h_t) with the same three
+//   parameters, c_prev = c_t, and G consumed only by the cell's 4 picks;
+//   chain b is stacked on chain a when x^b_t = h^a_t for every t.
+// A stack becomes one U_RNN unit when its external inputs do not depend on it
+// and its persistent launches fit the device (CTAs <= SMs, shared memory).
+// Returns per cell index the stack id (or -1).
+static std::vector<int> find_rnn_stacks(const dg_graph* g, const std::vector<Unit>& cells,
+                                        const std::vector<int>& consumers, const std::vector<char>& in_set,
+                                        const std::vector<int>& active, std::vector<RnnStack>& stacks) {
+  const int nc = (int)cells.size();
+  std::vector<int> stack_of(nc, -1);
+  if (nc < 2 || !rnn_enabled()) return stack_of;
+  auto Nd = [&](int i) -> const Node& { return g->nodes[i]; };
+  auto in = [&](int i, int k) { return g->inputs[Nd(i).in_off + k]; };
+  const int N = (int)g->nodes.size();
+  // eligibility + per-cell descriptors
+  struct CellInfo {
+    bool ok = false;
+    int G = -1, x = -1, hp = -1, cp = -1, h = -1, c = -1, B = 0, H = 0, K = 0;
+    int64_t hb = -1, hWx = -1, hWh = -1;
+  };
+  std::vector<CellInfo> ci(nc);
+  std::unordered_map<int, int> cell_by_h;
+  for (int k = 0; k < nc; ++k) {
+    const Unit& u = cells[k];
+    CellInfo& c = ci[k];
+    if (u.m != 1 || u.nodes.size() != 13) continue;
+    const int G = u.ins[0];
+    const Node& Gn = Nd(G);
+    if (Gn.kind != DG_OP_AFFINE || Gn.n_in != 5 || !in_set[G] || consumers[G] != 4) continue;
+    const int pb = in(G, 0), pwx = in(G, 1), pwh = in(G, 3);
+    bool params = true;
+    for (int p : {pb, pwx, pwh})
+      params = params && Nd(p).kind == DG_OP_PARAMETER && Nd(p).batch == 1;
+    if (!params) continue;
+    c.G = G;
+    c.x = in(G, 2);
+    c.hp = in(G, 4);
+    c.cp = u.ins[1];
+    c.h = u.nodes[12];
+    c.c = u.nodes[10];
+    c.B = Gn.batch;
+    c.H = u.H;
+    c.K = (int)Nd(c.x).elem;
+    if ((int)Gn.elem != u.gw || Nd(c.hp).elem != c.H || Nd(c.x).rank != 1 || Nd(c.hp).rank != 1) continue;
+    auto bok = [&](int i) { return Nd(i).batch == 1 || Nd(i).batch == c.B; };
+    if (!bok(c.x) || !bok(c.hp) || !bok(c.cp)) continue;
+    c.hb = param_handle_of(g, pb);
+    c.hWx = param_handle_of(g, pwx);
+    c.hWh = param_handle_of(g, pwh);
+    c.ok = true;
+    cell_by_h[c.h] = k;
+  }
+  auto same_sig = [&](int a, int b) {
+    const Unit &ua = cells[a], &ub = cells[b];
+    const CellInfo &x = ci[a], &y = ci[b];
+    return x.hb == y.hb && x.hWx == y.hWx && x.hWh == y.hWh && x.B == y.B && x.H == y.H && x.K == y.K &&
+           ua.gw == ub.gw && std::equal(ua.off, ua.off + 4, ub.off);
+  };
+  // recurrent links p -> k (unique successor)
+  std::vector<int> pred(nc, -1), succ(nc, -1), nsucc(nc, 0);
+  for (int k = 0; k < nc; ++k) {
+    if (!ci[k].ok) continue;
+    auto it = cell_by_h.find(ci[k].hp);
+    if (it == cell_by_h.end()) continue;
+    const int p = it->second;
+    if (p == k || !ci[p].ok || ci[p].c != ci[k].cp || !same_sig(p, k)) continue;
+    pred[k] = p;
+    nsucc[p]++;
+  }
+  for (int k = 0; k < nc; ++k) {
+    if (pred[k] < 0) continue;
+    if (nsucc[pred[k]] != 1) {
+      pred[k] = -1;
+      continue;
+    }
+    succ[pred[k]] = k;
+  }
+  // chains (T >= 2), in order of their first cell
+  std::vector<std::vector<int>> chains;
+  std::vector<int> chain_of(nc, -1), step_of(nc, -1);
+  for (int k = 0; k < nc; ++k) {
+    if (!ci[k].ok || pred[k] >= 0 || succ[k] < 0) continue;
+    std::vector<int> ch;
+    for (int x = k; x >= 0; x = succ[x]) ch.push_back(x);
+    for (size_t t = 0; t < ch.size(); ++t) {
+      chain_of[ch[t]] = (int)chains.size();
+      step_of[ch[t]] = (int)t;
+    }
+    chains.push_back(std::move(ch));
+  }
+  if (chains.empty()) return stack_of;
+  // stacking: x^b_t == h^a_t for all t
+  const int nch = (int)chains.size();
+  std::vector<int> src(nch, -1), cons(nch, -1);
+  for (int b = 0; b < nch; ++b) {
+    const auto& cb = chains[b];
+    auto it = cell_by_h.find(ci[cb[0]].x);
+    if (it == cell_by_h.end()) continue;
+    const int a = chain_of[it->second];
+    if (a < 0 || a == b || step_of[it->second] != 0 || chains[a].size() != cb.size() || cons[a] >= 0) continue;
+    if (ci[chains[a][0]].B != ci[cb[0]].B) continue;
+    bool all = true;
+    for (size_t t = 0; t < cb.size() && all; ++t) all = ci[cb[t]].x == ci[chains[a][t]].h;
+    if (!all) continue;
+    src[b] = a;
+    cons[a] = b;
+  }
+  // stacks: walk from each bottom chain (no src) up through consumers
+  std::vector<char> mark(N, 0);
+  for (int bot = 0; bot < nch; ++bot) {
+    if (src[bot] >= 0) continue;
+    std::vector<int> order;
+    for (int x = bot; x >= 0; x = cons[x]) order.push_back(x);
+    // the stack's nodes and external inputs
+    std::fill(mark.begin(), mark.end(), 0);
+    std::vector<int> ext;
+    for (size_t li = 0; li < order.size(); ++li) {
+      for (int k : chains[order[li]]) {
+        mark[ci[k].G] = 1;
+        for (int x : cells[k].nodes) mark[x] = 1;
+      }
+      const auto& ch = chains[order[li]];
+      ext.push_back(ci[ch[0]].hp);
+      ext.push_back(ci[ch[0]].cp);
+      if (li == 0)
+        for (int k : ch) ext.push_back(ci[k].x);
+    }
+    // acyclic: no external input may depend on a node of the stack
+    std::vector<char> desc(N, 0);
+    for (int i : active) {
+      if (mark[i]) continue;
+      const Node& n = Nd(i);
+      for (int q = 0; q < n.n_in && !desc[i]; ++q) {
+        const int s2 = g->inputs[n.in_off + q];
+        desc[i] = mark[s2] || desc[s2];
+      }
+    }
+    bool cyclic = false;
+    for (int x : ext) cyclic = cyclic || desc[x] || mark[x];
+    if (cyclic) continue;
+    // geometry and device fit
+    RnnStack st;
+    const CellInfo& c0 = ci[chains[order[0]][0]];
+    st.bs = rnn_rows_per_cta(c0.B);
+    int ctas = 0;
+    bool fits = true;
+    for (size_t li = 0; li < order.size(); ++li) {
+      const auto& ch = chains[order[li]];
+      const CellInfo& cc = ci[ch[0]];
+      RnnChainPlan cp;
+      for (size_t t = 0; t < ch.size(); ++t) {
+        cp.cells.push_back(cells[ch[t]]);
+        cp.G.push_back(ci[ch[t]].G);
+      }
+      cp.hb = cc.hb;
+      cp.hWx = cc.hWx;
+      cp.hWh = cc.hWh;
+      cp.H = cc.H;
+      cp.K_in = cc.K;
+      cp.B = cc.B;
+      cp.gw = cells[ch[0]].gw;
+      const Unit& u0 = cells[ch[0]];
+      cp.off[0] = u0.off[0];  // i
+      cp.off[1] = u0.off[3];  // f
+      cp.off[2] = u0.off[1];  // o
+      cp.off[3] = u0.off[2];  // g
+      cp.src = li > 0 ? (int)li - 1 : -1;
+      cp.cons = li + 1 < order.size() ? (int)li + 1 : -1;
+      cp.n_s = (cp.B + st.bs - 1) / st.bs;
+      cp.n_u = (cp.H + kRnnUnits - 1) / kRnnUnits;
+      ctas += cp.n_s * cp.n_u;
+      if (rnn_fwd_smem(cp.K_in + cp.H, st.bs) > kSmemMax) fits = false;
+      st.chains.push_back(std::move(cp));
+    }
+    for (auto& cp : st.chains) {
+      const int gwc = cp.cons >= 0 ? st.chains[cp.cons].gw : 0;
+      if (rnn_bwd_smem(cp.gw, gwc, st.bs, rnn_pick_cj(cp.gw, gwc, st.bs)) > kSmemMax) fits = false;
+    }
+    st.ctas = ctas;
+    if (!fits || ctas > kSmCount || (int)st.chains.size() > kRnnMaxChains) continue;
+    int flags = 0;
+    for (auto& cp : st.chains) flags += cp.n_s * (int)cp.cells.size();
+    if (flags > kFlagInts) continue;
+    const int sid = (int)stacks.size();
+    for (int li : order)
+      for (int k : chains[li]) stack_of[k] = sid;
+    stacks.push_back(std::move(st));
+  }
+  return stack_of;
+}
+
 // ------------------------------------------------------------- scheduling
 // Builds units (with cell fusion and add-chain rewrite) and the group order
 // for the node set `active` (ascending).  scope_hi bounds the consumer-count
@@ -509,9 +743,20 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
       cells.push_back(std::move(cu));
     }
   }
+  // LSTM chains / stacks over the matched cells (persistent recurrence path)
+  std::vector<int> rnn_of(N, -1);
+  {
+    std::vector<int> stack_of = find_rnn_stacks(g, cells, consumers, in_set, active, S.rnns);
+    for (size_t k = 0; k < cells.size(); ++k) {
+      if (stack_of[k] < 0) continue;
+      for (int x : cells[k].nodes) rnn_of[x] = stack_of[k];
+      rnn_of[cells[k].ins[0]] = stack_of[k];
+    }
+  }
+  std::vector<char> rnn_made(S.rnns.size(), 0);
   auto chainable_add = [&](int i) {
     const Node& n = g->nodes[i];
-    if (n.kind != DG_OP_ADD || absorbed[i]) return false;
+    if (n.kind != DG_OP_ADD || absorbed[i] || rnn_of[i] >= 0) return false;
     const int a = g->inputs[n.in_off], b = g->inputs[n.in_off + 1];
     return same_shape(i, a) && same_shape(i, b);
   };
@@ -534,7 +779,22 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
     if (n.kind == DG_OP_PARAMETER) { S.param_nodes.push_back(i); continue; }
     if (n.kind == DG_OP_LOOKUP || n.kind == DG_OP_LOOKUP_BATCH) { S.lookup_nodes.push_back(i); continue; }
     Unit u;
-    if (cell_of[i] >= 0) {
+    if (rnn_of[i] >= 0) {
+      const int sid = rnn_of[i];
+      if (rnn_made[sid]) continue;
+      rnn_made[sid] = 1;
+      u.type = U_RNN;
+      u.rnn = sid;
+      for (const RnnChainPlan& cp : S.rnns[sid].chains) {
+        for (size_t t = 0; t < cp.G.size(); ++t) {
+          const Node& G = g->nodes[cp.G[t]];
+          u.nodes.push_back(cp.G[t]);
+          for (int k = 0; k < G.n_in; ++k) u.ins.push_back(g->inputs[G.in_off + k]);
+          for (int x : cp.cells[t].nodes) u.nodes.push_back(x);
+          u.ins.push_back(cp.cells[t].ins[1]);
+        }
+      }
+    } else if (cell_of[i] >= 0) {
       u = std::move(cells[cell_of[i]]);
     } else if (chainable_add(i) && !has_prev[i] && chain_next[i] >= 0) {
       u.type = U_CHAIN;
@@ -640,7 +900,7 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
       std::sort(members.begin(), members.end());
       Group gr;
       const Unit& u0 = S.units[members[0]];
-      gr.kind = u0.type == U_CHAIN ? -1 : (u0.type == U_CELL ? -2 : g->nodes[u0.last()].kind);
+      gr.kind = u0.type == U_CHAIN ? -1 : u0.type == U_CELL ? -2 : u0.type == U_RNN ? -3 : g->nodes[u0.last()].kind;
       gr.units = members;
       for (int u : members) {
         ++done;
@@ -660,7 +920,8 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
 // blob's device base.
 enum OpClass {
   C_GEMM_FWD = 0, C_GEMM_DX = 1, C_GEMM_DW = 2, C_PNLS_FWD = 3, C_PNLS_BWD = 4,
-  C_ELEMWISE = 5, C_GATHER = 6, C_SCATTER = 7, C_COLSUM = 8, C_OTHER = 9, C_NCLASS = 10
+  C_ELEMWISE = 5, C_GATHER = 6, C_SCATTER = 7, C_COLSUM = 8, C_OTHER = 9, C_RNN_FWD = 10,
+  C_RNN_BWD = 11, C_NCLASS = 12
 };
 
 struct OpMeta {
@@ -757,7 +1018,9 @@ static inline float* dummy_base(dg_graph* g) {
 static inline int* counter_base(dg_graph* g) {
   return reinterpret_cast<int*>(g->work_base + g->work_bytes - kCounterBytes);
 }
-static constexpr int kCounterCap = (int)(kCounterBytes / 4);
+static constexpr int kCounterCap = (int)(kCounterBytes / 4) - kFlagInts;
+// persistent-recurrence arrival counters (zeroed by each rnn launch)
+static inline int* flag_base(dg_graph* g) { return counter_base(g) + kCounterCap; }
 
 // Same-level affine problems accumulate into one grouped GEMM launch.
 struct GemmBatch {
@@ -1037,6 +1300,265 @@ static int launch_plan(dg_graph* g, Plan& plan) {
 
 // scratch region of the workspace (after the table blob half)
 
+
+// dX += G W for one row set: rows of G (device table), W column-major m x K.
+// Rows landing on one target (broadcast x, shared x) go through a dense temp
+// and a deterministic segmented row reduce (same scheme as the affine path).
+static void push_dx_problem(dg_graph* g, Plan& plan, GemmBatch& batch, const float* const* g_rows_dev, bool g_al,
+                            const float* W, int m, int K, const std::vector<uintptr_t>& dxrows) {
+  Blob& B = plan.blob;
+  const cudaStream_t st = g->stream;
+  std::vector<uintptr_t> uniq = dxrows;
+  std::sort(uniq.begin(), uniq.end());
+  const bool dup = std::adjacent_find(uniq.begin(), uniq.end()) != uniq.end();
+  GemmProblem pr{};
+  pr.M = (int)dxrows.size();
+  pr.N = K;
+  pr.n_seg = 1;
+  pr.seg[0].K = m;
+  pr.seg[0].A.rows = g_rows_dev;
+  pr.seg[0].A.rows_aligned = g_al;
+  pr.seg[0].B.base = W;
+  pr.seg[0].B.ld = m;
+  batch.bytes += 4.0 * ((double)pr.M * m + (double)m * pr.N + 2.0 * pr.M * pr.N);
+  if (!dup) {
+    pr.accumulate = 1;
+    pr.C.rows = dev_at<const float*>(g, B.push(dxrows));
+  } else {
+    const int64_t R = (int64_t)dxrows.size();
+    std::vector<int> order(R);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return dxrows[x] < dxrows[y]; });
+    std::vector<uintptr_t> tgt;
+    std::vector<int32_t> seg;
+    for (int64_t q = 0; q < R; ++q) {
+      if (q == 0 || dxrows[order[q]] != dxrows[order[q - 1]]) {
+        tgt.push_back(dxrows[order[q]]);
+        seg.push_back((int32_t)q);
+      }
+    }
+    seg.push_back((int32_t)R);
+    std::vector<int64_t> pos(R);
+    for (int64_t q = 0; q < R; ++q) pos[order[q]] = q;
+    float* temp = reinterpret_cast<float*>(scratch_base(g)) + batch.temp_floats;
+    batch.temp_floats += (R * K + 63) & ~int64_t(63);
+    std::vector<uintptr_t> crow(R);
+    for (int64_t r = 0; r < R; ++r) crow[r] = P(temp + pos[r] * K);
+    pr.accumulate = 0;
+    pr.C.rows = dev_at<const float*>(g, B.push(crow));
+    float* const* tg =
+        const_cast<float* const*>(reinterpret_cast<const float* const*>(dev_at<float*>(g, B.push(tgt))));
+    const int* sg = dev_at<int>(g, B.push(seg));
+    const int n_t = (int)tgt.size();
+    batch.post.push_back([tg, sg, temp, n_t, K, st]() { return launch_row_reduce_scatter(tg, sg, temp, n_t, K, st); });
+  }
+  batch.probs.push_back(pr);
+}
+
+// Persistent LSTM recurrence (rnn.cu) for a group of U_RNN units: stacks are
+// packed into launches (same rows-per-CTA, CTAs <= SMs).  Backward also plans
+// the batched gradients of the stacks' external inputs (x_t of the bottom
+// chain, h_{-1}; c_{-1} broadcast sums) and registers the weight / bias
+// gradient rows for the aggregated dW GEMMs and column sums.
+static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan& plan, bool bwd,
+                           std::unordered_map<int64_t, AffineUse>* wuse,
+                           std::unordered_map<int64_t, std::vector<uintptr_t>>* buse, GemmBatch* gb) {
+  Blob& B = plan.blob;
+  const cudaStream_t st = g->stream;
+  // pack
+  std::vector<std::vector<int>> launches;
+  {
+    std::vector<int> cur;
+    int cur_bs = -1, cur_ctas = 0, cur_chains = 0, cur_flags = 0;
+    for (int u : gr.units) {
+      const RnnStack& sk = S.rnns[S.units[u].rnn];
+      int fl = 0;
+      for (auto& cp : sk.chains) fl += cp.n_s * (int)cp.cells.size();
+      if (!cur.empty() && (sk.bs != cur_bs || cur_ctas + sk.ctas > kSmCount ||
+                           cur_chains + (int)sk.chains.size() > kRnnMaxChains || cur_flags + fl > kFlagInts)) {
+        launches.push_back(cur);
+        cur.clear();
+        cur_ctas = cur_chains = cur_flags = 0;
+      }
+      cur.push_back(S.units[u].rnn);
+      cur_bs = sk.bs;
+      cur_ctas += sk.ctas;
+      cur_chains += (int)sk.chains.size();
+      cur_flags += fl;
+    }
+    if (!cur.empty()) launches.push_back(cur);
+  }
+  for (const auto& L : launches) {
+    RnnArgs a{};
+    a.flags = flag_base(g);
+    a.bs = S.rnns[L[0]].bs;
+    int cta = 0, flag = 0;
+    double flops = 0, bytes = 0;
+    a.cj = 1 << 30;
+    bool vec_ok = true;
+    for (int sid : L) {
+      const RnnStack& sk = S.rnns[sid];
+      const int base = a.n_chains;
+      for (const RnnChainPlan& cp : sk.chains) {
+        RnnChain& c = a.ch[a.n_chains++];
+        const int T = (int)cp.G.size();
+        c.T = T;
+        c.B = cp.B;
+        c.H = cp.H;
+        c.K_in = cp.K_in;
+        c.gw = cp.gw;
+        c.off_i = cp.off[0];
+        c.off_f = cp.off[1];
+        c.off_o = cp.off[2];
+        c.off_g = cp.off[3];
+        c.n_s = cp.n_s;
+        c.n_u = cp.n_u;
+        c.cta0 = cta;
+        cta += cp.n_s * cp.n_u;
+        c.src = cp.src >= 0 ? base + cp.src : -1;
+        c.cons = cp.cons >= 0 ? base + cp.cons : -1;
+        c.flag0 = flag;
+        flag += cp.n_s * T;
+        c.Wx = param_at(cp.hWx)->val;
+        c.Wh = param_at(cp.hWh)->val;
+        c.bias = param_at(cp.hb)->val;
+        std::vector<uintptr_t> vals((size_t)T * kRnnSlots), grads;
+        std::vector<int32_t> b1(T);
+        if (bwd) grads.resize((size_t)T * kRnnSlots);
+        for (int t = 0; t < T; ++t) {
+          const Node& Gn = g->nodes[cp.G[t]];
+          const int x = g->inputs[Gn.in_off + 2], hp = g->inputs[Gn.in_off + 4];
+          const Unit& cu = cp.cells[t];
+          const int cprev = cu.ins[1];
+          int slot[kRnnSlots];
+          slot[0] = cp.G[t];
+          slot[1] = cprev;
+          for (int k = 0; k < 13; ++k) slot[2 + k] = cu.nodes[k];
+          slot[15] = x;
+          slot[16] = hp;
+          for (int k : {0, 15, 16}) vec_ok = vec_ok && (P(g->nodes[slot[k]].val) & 15) == 0;
+          if (bwd) vec_ok = vec_ok && (P(g->nodes[slot[0]].grad) & 15) == 0;
+          for (int k = 0; k < kRnnSlots; ++k) {
+            vals[(size_t)t * kRnnSlots + k] = P(g->nodes[slot[k]].val);
+            if (bwd) grads[(size_t)t * kRnnSlots + k] = P(g->nodes[slot[k]].grad);
+          }
+          const bool bb = cp.B > 1;
+          b1[t] = (bb && g->nodes[x].batch == 1 ? 1 : 0) | (bb && g->nodes[hp].batch == 1 ? 2 : 0) |
+                  (bb && g->nodes[cprev].batch == 1 ? 4 : 0);
+        }
+        vec_ok = vec_ok && cp.K_in % 4 == 0 && cp.H % 4 == 0 && cp.gw % 4 == 0 && cp.off[0] % 4 == 0 &&
+                 cp.off[1] % 4 == 0 && cp.off[2] % 4 == 0 && cp.off[3] % 4 == 0;
+        c.val = dev_at<const float*>(g, B.push(vals));
+        if (bwd) c.grad = dev_at<float*>(g, B.push(grads));
+        c.b1 = dev_at<int>(g, B.push(b1));
+        const double gwd = cp.gw, bd = cp.B;
+        flops += bwd ? 2.0 * bd * gwd * cp.H * (T - 1) : 2.0 * bd * gwd * (cp.K_in + cp.H) * T;
+        bytes += 4.0 * bd * cp.H * T * (bwd ? 30 : 17);
+      }
+      for (int k = base; k < a.n_chains; ++k) {
+        const RnnChain& c = a.ch[k];
+        if (c.cons >= 0 && bwd) flops += 2.0 * c.B * a.ch[c.cons].gw * c.H * c.T;
+      }
+    }
+    a.ctas = cta;
+    a.n_flags = flag;
+    a.vec = vec_ok ? 1 : 0;
+    size_t smem = 0;
+    if (bwd) {
+      for (int k = 0; k < a.n_chains; ++k) {
+        const int gwc = a.ch[k].cons >= 0 ? a.ch[a.ch[k].cons].gw : 0;
+        a.cj = std::min(a.cj, rnn_pick_cj(a.ch[k].gw, gwc, a.bs));
+      }
+      for (int k = 0; k < a.n_chains; ++k) {
+        const int gwc = a.ch[k].cons >= 0 ? a.ch[a.ch[k].cons].gw : 0;
+        smem = std::max(smem, rnn_bwd_smem(a.ch[k].gw, gwc, a.bs, a.cj));
+      }
+    } else {
+      a.cj = 0;
+      for (int k = 0; k < a.n_chains; ++k) smem = std::max(smem, rnn_fwd_smem(a.ch[k].K_in + a.ch[k].H, a.bs));
+    }
+    plan.ops.push_back([a, smem, bwd, st](char*) { return launch_rnn(a, bwd, smem, st); });
+    plan.tag(bwd ? C_RNN_BWD : C_RNN_FWD, flops, bytes);
+  }
+  if (!bwd) return;
+
+  // ---- backward: gradients leaving the stacks, weight / bias aggregation
+  RnnC0 c0{};
+  for (int u : gr.units) {
+    const RnnStack& sk = S.rnns[S.units[u].rnn];
+    for (const RnnChainPlan& cp : sk.chains) {
+      const int T = (int)cp.G.size();
+      const int Bt = cp.B;
+      std::vector<uintptr_t> grows((size_t)T * Bt), xrows((size_t)T * Bt), hrows((size_t)T * Bt);
+      std::vector<uintptr_t> dxrows, g0rows;
+      for (int t = 0; t < T; ++t) {
+        const Node& Gn = g->nodes[cp.G[t]];
+        const Node& xn = g->nodes[g->inputs[Gn.in_off + 2]];
+        const Node& hn = g->nodes[g->inputs[Gn.in_off + 4]];
+        for (int b = 0; b < Bt; ++b) {
+          const size_t q = (size_t)t * Bt + b;
+          grows[q] = P(Gn.grad + (int64_t)b * cp.gw);
+          xrows[q] = P(xn.val + (xn.batch == 1 ? 0 : (int64_t)b * cp.K_in));
+          hrows[q] = P(hn.val + (hn.batch == 1 ? 0 : (int64_t)b * cp.H));
+          if (cp.src < 0) dxrows.push_back(P(xn.grad + (xn.batch == 1 ? 0 : (int64_t)b * cp.K_in)));
+        }
+      }
+      // weight / bias gradients: one aggregated GEMM per parameter later
+      {
+        AffineUse& ux = (*wuse)[cp.hWx];
+        ux.n_in = cp.K_in;
+        ux.m = cp.gw;
+        ux.x_rows.insert(ux.x_rows.end(), xrows.begin(), xrows.end());
+        ux.g_rows.insert(ux.g_rows.end(), grows.begin(), grows.end());
+        AffineUse& uh = (*wuse)[cp.hWh];
+        uh.n_in = cp.H;
+        uh.m = cp.gw;
+        uh.x_rows.insert(uh.x_rows.end(), hrows.begin(), hrows.end());
+        uh.g_rows.insert(uh.g_rows.end(), grows.begin(), grows.end());
+        auto& bv = (*buse)[cp.hb];
+        bv.insert(bv.end(), grows.begin(), grows.end());
+      }
+      const bool g_al = all_aligned16(grows);
+      const float* const* g_dev = dev_at<const float*>(g, B.push(grows));
+      // x_t of the bottom chain: dX = dG Wx over every step
+      if (cp.src < 0) {
+        GemmBatch& bt = gemm_batch_for(g, plan, *gb, gr.level, C_GEMM_DX, false, true);
+        push_dx_problem(g, plan, bt, g_dev, g_al, param_at(cp.hWx)->val, cp.gw, cp.K_in, dxrows);
+        flush_gemm(g, plan, *gb);
+      }
+      // h_{-1}: dX = dG_0 Wh
+      {
+        const Node& G0 = g->nodes[cp.G[0]];
+        const Node& hn = g->nodes[g->inputs[G0.in_off + 4]];
+        std::vector<uintptr_t> hd(Bt);
+        for (int b = 0; b < Bt; ++b) hd[b] = P(hn.grad + (hn.batch == 1 ? 0 : (int64_t)b * cp.H));
+        GemmBatch& bt = gemm_batch_for(g, plan, *gb, gr.level, C_GEMM_DX, false, true);
+        push_dx_problem(g, plan, bt, g_dev, g_al, param_at(cp.hWh)->val, cp.gw, cp.H, hd);
+        flush_gemm(g, plan, *gb);
+      }
+      // c_{-1} broadcast over the batch: batch sum of dc_0 * f_0
+      const Node& cpn = g->nodes[cp.cells[0].ins[1]];
+      if (cpn.batch == 1 && Bt > 1) {
+        if (c0.n == kRnnMaxChains) {
+          plan.ops.push_back([c0, st](char*) { return launch_rnn_c0(c0, st); });
+          plan.tag(C_ELEMWISE, 0.0, 0.0);
+          c0 = RnnC0{};
+        }
+        c0.H[c0.n] = cp.H;
+        c0.B[c0.n] = Bt;
+        c0.dst[c0.n] = cpn.grad;
+        c0.dc[c0.n] = g->nodes[cp.cells[0].nodes[10]].grad;
+        c0.af[c0.n] = g->nodes[cp.cells[0].nodes[5]].val;
+        c0.n++;
+      }
+    }
+  }
+  if (c0.n) {
+    plan.ops.push_back([c0, st](char*) { return launch_rnn_c0(c0, st); });
+    plan.tag(C_ELEMWISE, 0.0, 0.0);
+  }
+}
+
 static int ew_kind_of(int kind) {
   switch (kind) {
     case DG_OP_TANH: return EW_TANH;
@@ -1070,6 +1592,10 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
   const cudaStream_t st = g->stream;
   if (!(gr.kind == DG_OP_AFFINE && affine_gemm_ok(g, n0))) flush_gemm(g, plan, gb);
 
+  if (gr.kind == -3) {  // persistent LSTM stacks
+    plan_rnn_group(g, S, gr, plan, false, nullptr, nullptr, nullptr);
+    return;
+  }
   if (gr.kind == -2) {  // fused gated cells
     const Unit& u0 = S.units[gr.units[0]];
     CellArgs a{};
@@ -1473,6 +1999,10 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
                                 std::unordered_map<int64_t, std::vector<uintptr_t>>& buse, GemmBatch& gb) {
   Blob& B = plan.blob;
   if (!(gr.kind == DG_OP_AFFINE && affine_gemm_ok(g, g->nodes[S.units[gr.units[0]].last()]))) flush_gemm(g, plan, gb);
+  if (gr.kind == -3) {
+    plan_rnn_group(g, S, gr, plan, true, &wuse, &buse, &gb);
+    return;
+  }
   const cudaStream_t st = g->stream;
   std::vector<int> all_nodes;
   for (int u : gr.units) all_nodes.push_back(S.units[u].last());
@@ -2140,6 +2670,11 @@ int dg_schedule_stats(dg_graph* g, int32_t lo, int32_t hi, int64_t* out8) {
       cell_nodes += (int64_t)u.nodes.size();
     }
     if (u.type == U_CHAIN) ++chains;
+    if (u.type == U_RNN)
+      for (const RnnChainPlan& cp : S.rnns[u.rnn].chains) {
+        cells += (int64_t)cp.cells.size();
+        cell_nodes += 13 * (int64_t)cp.cells.size();
+      }
   }
   int64_t max_group = 0;
   for (const Group& gr : S.groups) max_group = std::max<int64_t>(max_group, (int64_t)gr.units.size());
@@ -2151,6 +2686,26 @@ int dg_schedule_stats(dg_graph* g, int32_t lo, int32_t hi, int64_t* out8) {
   out8[5] = max_group;
   out8[6] = (int64_t)S.lookup_nodes.size();
   out8[7] = (int64_t)S.input_nodes.size();
+  return DG_OK;
+}
+
+int dg_schedule_rnn_stats(dg_graph* g, int32_t lo, int32_t hi, int64_t* out4) {
+  // host-only: persistent LSTM stacks of the schedule of nodes [lo, hi]
+  if (lo < 0 || hi >= (int)g->nodes.size() || lo > hi) return fail(DG_STALE, "node range out of bounds");
+  std::vector<int> active;
+  for (int i = lo; i <= hi; ++i) active.push_back(i);
+  Schedule S;
+  build_schedule(g, active, hi, S);
+  int64_t chains = 0, steps = 0, ctas = 0;
+  for (const RnnStack& sk : S.rnns) {
+    chains += (int64_t)sk.chains.size();
+    ctas += sk.ctas;
+    for (const RnnChainPlan& cp : sk.chains) steps += (int64_t)cp.cells.size();
+  }
+  out4[0] = (int64_t)S.rnns.size();
+  out4[1] = chains;
+  out4[2] = steps;
+  out4[3] = ctas;
   return DG_OK;
 }
 

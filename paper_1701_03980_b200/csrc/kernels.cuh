@@ -72,6 +72,50 @@ struct CellArgs {
 int launch_cell_fwd(const CellArgs& a, cudaStream_t s);
 int launch_cell_bwd(const CellArgs& a, cudaStream_t s);
 
+// ------------------------------------------- persistent LSTM recurrence (rnn.cu)
+// One launch runs every step of a stack of LSTM chains (builders.py:92-101
+// steps sharing Wx, Wh, b; x^l_t = h^{l-1}_t for stacked layers).  Per step t
+// a chain has kRnnSlots node pointers: the 15 CellArgs slots for m = 1
+// (G, c_prev, picks i,f,o,g, acts i,f,o,g, prod ig, prod fc, c, tanh c, h)
+// followed by x_t and h_{t-1}.
+constexpr int kRnnSlots = 17;
+constexpr int kRnnMaxChains = 16;
+constexpr int kRnnUnits = 16;  // hidden units per CTA
+struct RnnChain {
+  int T, B, H, K_in, gw;
+  int off_i, off_f, off_o, off_g;
+  int n_s, n_u;     // batch slices (of bs rows) x unit blocks (of kRnnUnits)
+  int cta0;         // first CTA of the chain
+  int src, cons;    // stacked producer (fwd) / consumer (bwd) chain, -1 none
+  int flag0;        // this chain's arrival counters: [n_s][T]
+  const float* Wx;  // column-major gw x K_in (W[row + k * gw])
+  const float* Wh;  // column-major gw x H
+  const float* bias;
+  const float* const* val;  // [T][kRnnSlots] (device)
+  float* const* grad;       // [T][kRnnSlots] (device, backward)
+  const int* b1;            // [T] bit0 x_t, bit1 h_{t-1}, bit2 c_{t-1} is batch-1
+};
+struct RnnArgs {
+  int n_chains, ctas, bs, cj, n_flags;
+  int vec;     // every staged row is 16B aligned with a multiple-of-4 width (cp.async path)
+  int* flags;  // zeroed by the launcher
+  RnnChain ch[kRnnMaxChains];
+};
+// batch-1 c_{-1} gradients: dst[k][u] += sum_b dc[k][b][u] * af[k][b][u]
+struct RnnC0 {
+  int n;
+  int H[kRnnMaxChains], B[kRnnMaxChains];
+  float* dst[kRnnMaxChains];
+  const float* dc[kRnnMaxChains];
+  const float* af[kRnnMaxChains];
+};
+int rnn_rows_per_cta(int B);
+size_t rnn_fwd_smem(int K, int bs);
+size_t rnn_bwd_smem(int gw, int gw_c, int bs, int cj);
+bool rnn_enabled();  // DG_RNN=0 disables the persistent path (A/B checks)
+int launch_rnn(const RnnArgs& a, bool backward, size_t smem, cudaStream_t s);
+int launch_rnn_c0(const RnnC0& a, cudaStream_t s);
+
 // --------------------------------------------------------------- structural
 struct PickArgs {
   int n, batch, in_elem, lo, width;

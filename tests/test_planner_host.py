@@ -78,3 +78,46 @@ def test_tagger_char_cells():
     rare = [w for w, _ in sent if w not in tg.vocab]
     expect = 2 * len(sent) + sum(2 * len(w) for w in rare)
     assert s["cells"] == expect
+
+
+def _rnn_stats(cg, model):
+    lib = _native.lib()
+    _stats(cg, model)  # registers placeholder parameters
+    h = ctypes.c_void_p()
+    _native.check(lib.dg_graph_create(0, 0x1000, 1 << 30, 0x2000, 1 << 30, 0x3000, 1 << 28, ctypes.byref(h)))
+    cg._sent = 0
+    cg._flush(h)
+    out = np.zeros(4, np.int64)
+    _native.check(lib.dg_schedule_rnn_stats(h, 0, len(cg.nodes) - 1, out.ctypes.data))
+    lib.dg_graph_destroy(h)
+    return dict(zip(["stacks", "chains", "steps", "ctas"], out.tolist()))
+
+
+def test_rnnlm_recurrence_is_one_persistent_stack():
+    cg, m = _ctx()
+    task = W.RNNLM(dy, m, 10_000, 128, 256, 2)
+    batch = W.ptb_corpus(1, 64)
+    task.loss(cg, batch)
+    steps = max(len(s) for s in batch) - 1
+    r = _rnn_stats(cg, m)
+    # both layers' chains stacked (x^1_t = h^0_t): one launch per direction,
+    # 64 rows / 16 per CTA x 256 units / 16 per CTA = 64 CTAs per layer
+    assert r == {"stacks": 1, "chains": 2, "steps": 2 * steps, "ctas": 128}
+
+
+def test_tiny_lm_single_chain():
+    cg, m = _ctx()
+    task = W.RNNLM(dy, m, 1000, 64, 64, 1)
+    sent = W.tiny_lm_corpus(5, 1)[0]
+    task.loss(cg, [sent])
+    r = _rnn_stats(cg, m)
+    assert r["stacks"] == 1 and r["chains"] == 1 and r["steps"] == len(sent) - 1
+    assert r["ctas"] == 4
+
+
+def test_tree_has_no_chains():
+    cg, m = _ctx()
+    td = W.tree_corpus(1, 1)
+    task = W.TreeClassifier(dy, m, td.vocab_size)
+    task.loss(cg, td.trees[0], td.labels[0])
+    assert _rnn_stats(cg, m)["stacks"] == 0

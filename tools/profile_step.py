@@ -56,7 +56,7 @@ print("launches", cg._counters()[5], "plan", cg.plan_stats())
 # ---- live device-only per-class timing: stall the GPU with a spin kernel so
 # the host enqueues the whole step first, then read the CUDA-event windows
 classes = ("gemm_fwd", "gemm_dx", "gemm_dw", "pnls_fwd", "pnls_bwd", "elementwise", "gather", "scatter_add",
-           "bias_colsum", "other")
+           "bias_colsum", "other", "rnn_fwd", "rnn_bwd")
 cg.profile_enable(classes)
 tot = {c: 0.0 for c in classes}
 cnt = {c: 0 for c in classes}
