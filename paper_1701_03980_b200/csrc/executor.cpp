@@ -220,6 +220,13 @@ struct dg_graph {
   std::vector<cudaEvent_t> event_pool;
   dg::Pinned pinned[2];
   int pin_idx = 0;
+  // small-value cache: the last forward's target node (e.g. the loss) is
+  // copied to pinned memory right after its forward launches, before any
+  // backward kernels, so value(loss) waits for the forward only
+  float* vcache = nullptr;
+  cudaEvent_t vcache_ev = nullptr;
+  int vcache_node = -1;
+  int64_t vcache_n = 0;
   bool has_grads = false;  // any backward in this generation
   bool counters_ready = false;  // split-K tile counters zeroed (first launch)
 };
@@ -1180,6 +1187,10 @@ int dg_graph_create(int device, void* fwd_base, size_t fwd_bytes, void* bwd_base
 
 int dg_graph_destroy(dg_graph* g) {
   if (!g) return DG_OK;
+  if (g->vcache_ev) {
+    cudaEventSynchronize(g->vcache_ev);
+    cudaEventDestroy(g->vcache_ev);
+  }
   for (auto& p : g->pinned) {
     if (p.pending) cudaEventSynchronize(p.ev);
     if (p.ptr) cudaFreeHost(p.ptr);
@@ -1200,6 +1211,7 @@ int dg_graph_renew(dg_graph* g) {
   g->aux_i.clear();
   g->aux_f.clear();
   g->watermark = -1;
+  g->vcache_node = -1;
   // the reference zeroes the used backward prefix here (arena.py:85-92); the
   // device backward slots are zeroed when a backward pass allocates them
   g->fwd_cursor = 0;
@@ -1975,6 +1987,28 @@ static int do_forward(dg_graph* g, int upto) {
 
   int rc = launch_plan(g, plan);
   if (rc) return rc;
+  {
+    const Node& tn = g->nodes[upto];
+    g->vcache_node = -1;
+    if (tn.kind != DG_OP_PARAMETER && tn.size() <= 64) {
+      if (!g->vcache) {
+        // slots of one process-wide pinned block (cudaHostAlloc synchronises
+        // the device, so it must not run per graph)
+        static std::mutex mu;
+        static float* block = nullptr;
+        static int next = 0;
+        std::lock_guard<std::mutex> lk(mu);
+        if (!block) DG_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&block), 4096 * 64 * sizeof(float), 0));
+        g->vcache = block + 64 * (next++ % 4096);
+        DG_CUDA_TRY(cudaEventCreateWithFlags(&g->vcache_ev, cudaEventDisableTiming));
+      }
+      DG_CUDA_TRY(cudaMemcpyAsync(g->vcache, tn.val, (size_t)tn.size() * 4, cudaMemcpyDeviceToHost, g->stream));
+      DG_CUDA_TRY(cudaEventRecord(g->vcache_ev, g->stream));
+      g->vcache_node = upto;
+      g->vcache_n = tn.size();
+      g->d2h_bytes += tn.size() * 4;
+    }
+  }
   g->fwd_cursor = cur;
   g->fwd_alloc_count += (int64_t)(S.input_nodes.size() + S.lookup_nodes.size());
   for (const Group& gr : S.groups)
@@ -2622,6 +2656,11 @@ int dg_value(dg_graph* g, int32_t node, float* host_dst, int64_t n) {
   if (rc) return rc;
   const Node& x = g->nodes[node];
   if (n != x.size()) return fail(DG_SHAPE, "value buffer size mismatch");
+  if (node == g->vcache_node && n == g->vcache_n) {
+    DG_CUDA_TRY(cudaEventSynchronize(g->vcache_ev));
+    std::memcpy(host_dst, g->vcache, (size_t)n * 4);
+    return DG_OK;
+  }
   DG_CUDA_TRY(cudaMemcpyAsync(host_dst, x.val, (size_t)n * 4, cudaMemcpyDeviceToHost, g->stream));
   g->d2h_bytes += n * 4;
   DG_CUDA_TRY(cudaStreamSynchronize(g->stream));
