@@ -7,7 +7,7 @@ PKG := paper_1701_03980_b200
 SRC := $(PKG)/csrc
 OBJ := build/obj
 LIB := $(PKG)/libdyngpu.so
-OBJS := $(OBJ)/executor.o $(OBJ)/kernels.o $(OBJ)/gemm.o $(OBJ)/tcgemm.o $(OBJ)/rnn.o
+OBJS := $(OBJ)/executor.o $(OBJ)/kernels.o $(OBJ)/gemm.o $(OBJ)/tcgemm.o $(OBJ)/rnn.o $(OBJ)/tmagemm.o
 
 all: $(LIB)
 
@@ -24,6 +24,9 @@ $(OBJ)/gemm.o: $(SRC)/gemm.cu $(SRC)/kernels.cuh | $(OBJ)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(OBJ)/tcgemm.o: $(SRC)/tcgemm.cu $(SRC)/kernels.cuh | $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(OBJ)/tmagemm.o: $(SRC)/tmagemm.cu $(SRC)/kernels.cuh | $(OBJ)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(OBJ)/rnn.o: $(SRC)/rnn.cu $(SRC)/kernels.cuh | $(OBJ)

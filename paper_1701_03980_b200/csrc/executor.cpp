@@ -792,14 +792,19 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
       rnn_made[sid] = 1;
       u.type = U_RNN;
       u.rnn = sid;
+      // slot-major node order: each slot's nodes of all steps are placed
+      // contiguously (h_0..h_{T-1} form one dense [T*B x H] block, which the
+      // layers above read as a regular GEMM operand)
       for (const RnnChainPlan& cp : S.rnns[sid].chains) {
-        for (size_t t = 0; t < cp.G.size(); ++t) {
+        const size_t T = cp.G.size();
+        for (size_t t = 0; t < T; ++t) {
           const Node& G = g->nodes[cp.G[t]];
           u.nodes.push_back(cp.G[t]);
           for (int k = 0; k < G.n_in; ++k) u.ins.push_back(g->inputs[G.in_off + k]);
-          for (int x : cp.cells[t].nodes) u.nodes.push_back(x);
           u.ins.push_back(cp.cells[t].ins[1]);
         }
+        for (int k = 0; k < 13; ++k)
+          for (size_t t = 0; t < T; ++t) u.nodes.push_back(cp.cells[t].nodes[k]);
       }
     } else if (cell_of[i] >= 0) {
       u = std::move(cells[cell_of[i]]);
@@ -1012,13 +1017,14 @@ static std::vector<std::vector<char>> conflict_rounds(const std::vector<std::vec
   return rounds;
 }
 
-// workspace layout: [0, W/2) table blob | [W/2, W-17MiB) scratch (split-K
+// workspace layout: [0, W/8) table blob | [W/8, W-17MiB) scratch (split-K
 // partials, dX temporaries, column-sum partials) | 16 MiB dummy gradient
 // target | 1 MiB zeroed split-K tile counters
 static constexpr size_t kDummyBytes = 16u << 20;
 static constexpr size_t kCounterBytes = 1u << 20;
-static inline char* scratch_base(dg_graph* g) { return g->work_base + g->work_bytes / 2; }
-static inline size_t scratch_bytes(dg_graph* g) { return g->work_bytes / 2 - kDummyBytes - kCounterBytes; }
+static inline size_t blob_cap(const dg_graph* g) { return (g->work_bytes / 8) & ~size_t(255); }
+static inline char* scratch_base(dg_graph* g) { return g->work_base + blob_cap(g); }
+static inline size_t scratch_bytes(dg_graph* g) { return g->work_bytes - blob_cap(g) - kDummyBytes - kCounterBytes; }
 static inline float* dummy_base(dg_graph* g) {
   return reinterpret_cast<float*>(g->work_base + g->work_bytes - kDummyBytes - kCounterBytes);
 }
@@ -1046,6 +1052,60 @@ static inline const T* dev_at(dg_graph* g, size_t off) {
   return reinterpret_cast<const T*>(g->work_base + off);
 }
 
+// Row table (device address inside the plan blob) -> dense block: when the
+// rows are equally spaced (row i at base + i*ld) the operand is rewritten as
+// base/ld, which the TMA path (and vectorised epilogues) need.
+static bool regularize(dg_graph* g, const Plan& plan, Operand& op, int64_t n_rows, int64_t row_len) {
+  if (!op.rows) return op.base && (reinterpret_cast<uintptr_t>(op.base) & 15) == 0 && op.ld % 4 == 0 &&
+                       op.ld >= row_len;
+  const char* dev = reinterpret_cast<const char*>(op.rows);
+  if (dev < g->work_base || dev >= g->work_base + plan.blob.host.size()) return false;
+  const uintptr_t* r = reinterpret_cast<const uintptr_t*>(plan.blob.host.data() + (dev - g->work_base));
+  if (n_rows < 1 || (r[0] & 15)) return false;
+  const int64_t step = n_rows > 1 ? (int64_t)(r[1] - r[0]) : (int64_t)row_len * 4;
+  if (step <= 0 || step % 16 || step / 4 < row_len) return false;
+  for (int64_t i = 2; i < n_rows; ++i)
+    if ((int64_t)(r[i] - r[i - 1]) != step) return false;
+  op.base = reinterpret_cast<const float*>(r[0]);
+  op.ld = step / 4;
+  op.rows = nullptr;
+  return true;
+}
+
+// TMA tensor-core path for one problem (tmagemm.cu): regular operands, wide
+// enough for 128 x 128 tiles, residual copies in the scratch at lo_base.
+static bool tma_try(dg_graph* g, const Plan& plan, const GemmProblem& p0, bool a_kmajor, bool b_nmajor,
+                    float* lo_base, int64_t lo_cap, TmaGemmPlan* out) {
+  if (!tma_gemm_enabled() || p0.n_seg != 1) return false;
+  const int64_t K = p0.seg[0].K;
+  if (p0.M < 128 || p0.N < 128 || K < 128 || K > (int64_t)1 << 30) return false;
+  GemmProblem p = p0;
+  const bool a_mn = a_kmajor, b_mn = !b_nmajor;
+  if (!regularize(g, plan, p.seg[0].A, a_mn ? K : p.M, a_mn ? p.M : K)) return false;
+  if (!regularize(g, plan, p.seg[0].B, b_mn ? K : p.N, b_mn ? p.N : K)) return false;
+  regularize(g, plan, p.C, p.M, p.N);  // optional: vectorised epilogue
+  const int64_t la = tma_lo_floats(a_mn ? K : p.M, a_mn ? p.M : K);
+  const int64_t lb = tma_lo_floats(b_mn ? K : p.N, b_mn ? p.N : K);
+  const int64_t la_p = (la + 63) & ~int64_t(63);
+  if (la_p + lb > lo_cap) return false;
+  TmaOperands o{};
+  o.M = p.M;
+  o.N = p.N;
+  o.K = (int)K;
+  o.a_mn = a_mn;
+  o.b_mn = b_mn;
+  o.A = p.seg[0].A.base;
+  o.lda = p.seg[0].A.ld;
+  o.B = p.seg[0].B.base;
+  o.ldb = p.seg[0].B.ld;
+  o.A_lo = lo_base;
+  o.B_lo = lo_base + la_p;
+  o.C = p.C;
+  o.bias = p.bias;
+  o.accumulate = p.accumulate;
+  return tma_gemm_make(o, out);
+}
+
 static void flush_gemm(dg_graph* g, Plan& plan, GemmBatch& gb) {
   if (gb.probs.empty()) {
     gb = GemmBatch();
@@ -1054,22 +1114,47 @@ static void flush_gemm(dg_graph* g, Plan& plan, GemmBatch& gb) {
   const int64_t temp = (gb.temp_floats + 63) & ~int64_t(63);
   float* work = reinterpret_cast<float*>(scratch_base(g)) + temp;
   const int64_t cap = (int64_t)(scratch_bytes(g) / 4) - temp;
-  // wide problems run on the tensor cores (tcgen05 3xTF32), the rest on the
-  // grouped SIMT kernel
-  const bool tc = tc_gemm_eligible(gb.probs);
-  GemmLaunch L = tc ? tc_gemm_plan(gb.probs, gb.a_kmajor, gb.b_nmajor)
-                    : gemm_plan(gb.probs, gb.a_kmajor, gb.b_nmajor, cap, kCounterCap);
-  const size_t off = plan.blob.push(gb.probs);
+  cudaStream_t st = g->stream;
+  // dense wide problems: TMA + warp-specialised tcgen05 (one launch each)
+  std::vector<GemmProblem> rest;
+  for (const GemmProblem& p : gb.probs) {
+    TmaGemmPlan tp;
+    if (tma_try(g, plan, p, gb.a_kmajor, gb.b_nmajor, work, cap, &tp)) {
+      plan.ops.push_back([tp, st](char*) { return launch_tma_gemm(tp, true, true, st); });
+      plan.tag(gb.cls, tp.flops, 4.0 * ((double)p.M * p.seg[0].K + (double)p.seg[0].K * p.N + 2.0 * p.M * p.N));
+    } else {
+      rest.push_back(p);
+    }
+  }
+  auto post = std::move(gb.post);
+  if (rest.empty()) {
+    if (!post.empty()) {
+      plan.ops.push_back([post](char*) {
+        int n = 0;
+        for (auto& f : post) n += f();
+        return n;
+      });
+      plan.tag(gb.cls, 0.0, 0.0);
+    }
+    gb = GemmBatch();
+    return;
+  }
+  // other wide problems run on the cp.async tensor-core kernel (tcgen05
+  // 3xTF32), the rest on the grouped SIMT kernel
+  const bool tc = tc_gemm_eligible(rest);
+  GemmLaunch L = tc ? tc_gemm_plan(rest, gb.a_kmajor, gb.b_nmajor)
+                    : gemm_plan(rest, gb.a_kmajor, gb.b_nmajor, cap, kCounterCap);
+  const size_t off = plan.blob.push(rest);
   const GemmProblem* pdev = dev_at<GemmProblem>(g, off);
   int* counters = counter_base(g);
-  cudaStream_t st = g->stream;
-  auto post = std::move(gb.post);
   plan.ops.push_back([L, pdev, work, counters, st, post, tc](char*) {
     int n = tc ? launch_tc_gemm(L, pdev, st) : launch_gemm_group(L, pdev, work, counters, st);
     for (auto& f : post) n += f();
     return n;
   });
-  plan.tag(gb.cls, L.flops, gb.bytes);
+  double bytes = 0;
+  for (const GemmProblem& p : rest) bytes += 4.0 * ((double)p.M * p.seg[0].K + (double)p.seg[0].K * p.N + 2.0 * p.M * p.N);
+  plan.tag(gb.cls, L.flops, bytes);
   gb = GemmBatch();
 }
 
@@ -1270,7 +1355,7 @@ int dg_graph_append(dg_graph* g, const dg_node* nodes, int32_t n, const int32_t*
 
 static int launch_plan(dg_graph* g, Plan& plan) {
   const size_t blob_bytes = (plan.blob.host.size() + 255) & ~size_t(255);
-  if (blob_bytes > g->work_bytes / 2) return fail(DG_CONFIG, "plan tables exceed the workspace");
+  if (blob_bytes > blob_cap(g)) return fail(DG_CONFIG, "plan tables exceed the workspace");
   if (!g->counters_ready) {
     // split-K tile counters start (and are always left) at zero
     DG_CUDA_TRY(cudaMemsetAsync(g->work_base + g->work_bytes - (1u << 20), 0, 1u << 20, g->stream));
@@ -2050,7 +2135,12 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
   if (gr.kind == DG_OP_AFFINE) {
     // dX is conflict-free by construction (temp + segmented reduce); only the
     // per-node (non-parameter) bias needs rounds
-    for (size_t j = 0; j < targets.size(); ++j) targets[j] = {targets[j][0]};
+    // (a parameter bias is aggregated into one column sum, no conflict)
+    for (size_t j = 0; j < targets.size(); ++j) {
+      const int b = targets[j][0];
+      if (g->nodes[b].kind == DG_OP_PARAMETER) targets[j].clear();
+      else targets[j] = {b};
+    }
   }
   auto rounds = conflict_rounds(targets, ew);
   // intra-node duplicate slots in non-elementwise kinds (e.g. concatenate([x,x]))

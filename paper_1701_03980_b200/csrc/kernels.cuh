@@ -8,6 +8,7 @@
 #pragma once
 #include <cstdint>
 #include <vector>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace dg {
@@ -251,6 +252,44 @@ GemmLaunch tc_gemm_plan(std::vector<GemmProblem>& probs, bool a_kmajor, bool b_n
 int launch_tc_gemm(const GemmLaunch& L, const GemmProblem* probs_dev, cudaStream_t s);
 // DG_TC=0 in the environment disables the tensor-core path (A/B checks)
 bool tc_gemm_enabled();
+
+// TMA + warp-specialised tcgen05 3xTF32 path (tmagemm.cu) for single problems
+// whose operands are dense blocks (row stride ld, 16B aligned).  The residual
+// (lo) copies of A and B live in the workspace.
+struct TmaGemmArgs {
+  int M, N, K;
+  int tiles_n, splits, accumulate, c_vec, pad_;
+  Operand C, bias;
+};
+struct TmaOperands {
+  int M, N, K;
+  bool a_mn, b_mn;      // A(m,k) = A[k*lda + m] (MN-major) else A[m*lda + k]; B(k,n) = B[k*ldb + n] else B[n*ldb + k]
+  const float* A;
+  int64_t lda;
+  const float* B;
+  int64_t ldb;
+  float* A_lo;          // tma_lo_floats(rows, cols) floats each
+  float* B_lo;
+  Operand C, bias;
+  int accumulate;
+};
+struct TmaGemmPlan {
+  CUtensorMap mAh, mAl, mBh, mBl;
+  TmaGemmArgs args;
+  bool a_mn, b_mn;
+  const float* a_src;
+  const float* b_src;
+  float* a_lo;
+  float* b_lo;
+  int64_t a_ld, a_rows, a_cols, a_colsp, b_ld, b_rows, b_cols, b_colsp;
+  int ctas;
+  double flops;
+};
+bool tma_gemm_enabled();  // DG_TMA=0 disables (A/B checks)
+int64_t tma_lo_floats(int64_t rows, int64_t cols);
+bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out);
+// split_a / split_b: (re)compute the residual copies before the GEMM
+int launch_tma_gemm(const TmaGemmPlan& p, bool split_a, bool split_b, cudaStream_t s);
 
 // ------------------------------------------------------------- trainers
 struct TensorSeg { float* w; float* g; float* s0; float* s1; int64_t n; };

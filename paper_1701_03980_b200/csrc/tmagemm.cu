@@ -1,0 +1,483 @@
+// Warp-specialised tcgen05 3xTF32 GEMM with TMA operand loads (sm_100a) for
+// the wide affine contractions whose operands are dense row-major blocks in
+// the arena (the output layer of a batched RNNLM: logits = H W^T + b,
+// dH = dLogits W, dW^T += H^T dLogits):
+//
+//   C[M x N] (= | +=) A(m,k) B(k,n) (+ bias(n))         fp32 in, fp32 out
+//
+// fp32 parity is kept with 3xTF32: the tensor core reads fp32 storage as TF32
+// (x_hi = x with the low 13 mantissa bits dropped); a residual copy
+// x_lo = x - x_hi of each operand is produced once per launch by
+// split_lo_kernel into the workspace, and every k-step issues
+// A_hi*B_hi + A_hi*B_lo + A_lo*B_hi into an fp32 TMEM accumulator.
+// Every CHUNK k-tiles the accumulator is handed to the epilogue warps, which
+// add it into fp32 registers (blocked summation: the tensor core's own
+// accumulation is not a full-precision fp32 chain over K = 10^4), while the
+// MMA warp continues in the second TMEM accumulator.
+//
+// Roles (192 threads, one CTA per SM, 128 x 128 output tile):
+//   warp 0  TMA producer: per k-tile 4 tensor loads (A_hi, A_lo, B_hi, B_lo)
+//           into a 3-stage ring (64 KiB per stage) signalling an mbarrier
+//           with the transaction byte count;
+//   warp 1  TMEM allocation + single-thread tcgen05.mma issue (12 MMAs of
+//           128x128x8 per k-tile), tcgen05.commit releases the stage and,
+//           at chunk ends, publishes the accumulator;
+//   warps 2-5  epilogue: tcgen05.ld drains (each warp its 32-lane TMEM
+//           quadrant), bias / accumulate, stores; split-K tiles reduce their
+//           partials through distributed shared memory of the cluster.
+#include <cooperative_groups.h>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+#include <mutex>
+
+#include "kernels.cuh"
+
+namespace cgrp = cooperative_groups;
+
+namespace dg {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 32;
+constexpr int kStages = 3;
+constexpr int kOpBytes = 128 * BK * 4;         // 16 KiB per operand tile
+constexpr int kStageBytes = 4 * kOpBytes;      // A_hi, A_lo, B_hi, B_lo
+constexpr int kThreads = 192;
+constexpr int kSmem = kStages * kStageBytes + 1024;
+constexpr int kChunk = 2;  // k-tiles per TMEM accumulation (K = 64)
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra W_%=;\n\t}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
+      : "memory");
+}
+
+// UMMA smem descriptors (same layouts as tcgemm.cu): K-major SWIZZLE_128B
+// (SBO 1024 B) / MN-major SWIZZLE_128B_BASE32B (LBO 4096 B, SBO 512 B)
+__device__ __forceinline__ uint64_t udesc(uint32_t saddr, bool mn) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((mn ? (4096 >> 4) : 1) & 0x3FFF) << 16;
+  d |= (uint64_t)(((mn ? 512 : 1024) >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(mn ? 1 : 2) << 61;
+  return d;
+}
+__host__ __device__ constexpr uint32_t uidesc(bool a_mn, bool b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((BN >> 3) << 17) | ((BM >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ const float* orow(const Operand& o, int64_t i) {
+  return o.rows ? o.rows[i] : o.base + i * o.ld;
+}
+
+template <bool kAMN, bool kBMN>
+__global__ void __launch_bounds__(kThreads, 1)
+    tma_gemm_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
+                    const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
+                    const __grid_constant__ TmaGemmArgs P) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[kStages], empty[kStages], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tmem_sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = P.splits;
+  const int local = blockIdx.x;
+  const int z = local % S, tile = local / S;
+  const int m0 = (tile / P.tiles_n) * BM, n0 = (tile % P.tiles_n) * BN;
+  const int kt_total = (P.K + BK - 1) / BK;
+  const int t0 = (int)((int64_t)kt_total * z / S), t1 = (int)((int64_t)kt_total * (z + 1) / S);
+  const int nkt = t1 - t0;
+  const int nchunks = (nkt + kChunk - 1) / kChunk;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAh)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAl)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBh)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBl)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_sh)),
+                 "r"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_sh;
+  const uint32_t sbase = su32(smem);
+
+  float vals[BN];  // epilogue: this thread's output row (blocked fp32 sums)
+#pragma unroll
+  for (int q = 0; q < BN; ++q) vals[q] = 0.f;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int j = 0; j < nkt; ++j) {
+        const int s = j % kStages, use = j / kStages;
+        if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+        mbar_expect_tx(&full[s], kStageBytes);
+        const uint32_t st = sbase + s * kStageBytes;
+        const int k0 = (t0 + j) * BK;
+        // A: K-major box {32 k, 128 m} at (k0, m0); MN-major 4 boxes {32 m, 32 k} at (m0 + 32g, k0)
+        if (!kAMN) {
+          tma_2d(st, &mAh, k0, m0, &full[s]);
+          tma_2d(st + kOpBytes, &mAl, k0, m0, &full[s]);
+        } else {
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            tma_2d(st + g * 4096, &mAh, m0 + 32 * g, k0, &full[s]);
+            tma_2d(st + kOpBytes + g * 4096, &mAl, m0 + 32 * g, k0, &full[s]);
+          }
+        }
+        if (!kBMN) {
+          tma_2d(st + 2 * kOpBytes, &mBh, k0, n0, &full[s]);
+          tma_2d(st + 3 * kOpBytes, &mBl, k0, n0, &full[s]);
+        } else {
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            tma_2d(st + 2 * kOpBytes + g * 4096, &mBh, n0 + 32 * g, k0, &full[s]);
+            tma_2d(st + 3 * kOpBytes + g * 4096, &mBl, n0 + 32 * g, k0, &full[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = uidesc(kAMN, kBMN);
+      for (int j = 0; j < nkt; ++j) {
+        const int s = j % kStages, use = j / kStages;
+        const int c = j / kChunk, a = c & 1;
+        if (j % kChunk == 0 && c >= 2) mbar_wait(&acc_empty[a], ((c >> 1) - 1) & 1);
+        mbar_wait(&full[s], use & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t ah = sbase + s * kStageBytes, al = ah + kOpBytes, bh = ah + 2 * kOpBytes,
+                       bl = ah + 3 * kOpBytes;
+        const uint32_t acc = tmem + (uint32_t)(a * BN);
+#pragma unroll
+        for (int ks = 0; ks < BK / 8; ++ks) {
+          const uint32_t oa = kAMN ? ks * 1024 : ks * 32, ob = kBMN ? ks * 1024 : ks * 32;
+          const uint32_t first = (j % kChunk == 0 && ks == 0) ? 0u : 1u;
+          mma_tf32(acc, udesc(ah + oa, kAMN), udesc(bh + ob, kBMN), idesc, first);
+          mma_tf32(acc, udesc(ah + oa, kAMN), udesc(bl + ob, kBMN), idesc, 1u);
+          mma_tf32(acc, udesc(al + oa, kAMN), udesc(bh + ob, kBMN), idesc, 1u);
+        }
+        mma_commit(&empty[s]);
+        if (j % kChunk == kChunk - 1 || j == nkt - 1) mma_commit(&acc_full[a]);
+      }
+    }
+  } else {
+    // epilogue warps 2..5 -> TMEM lane quadrant warp % 4
+    const int quad = warp & 3;
+    for (int c = 0; c < nchunks; ++c) {
+      const int a = c & 1;
+      mbar_wait(&acc_full[a], (c >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int h = 0; h < BN / 32; ++h) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(a * BN + h * 32);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+              "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+              "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+              "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < 32; ++q) vals[h * 32 + q] += __uint_as_float(r[q]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[a]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();  // every MMA drained and every stage consumed
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+
+  const bool has_bias = P.bias.rows != nullptr || P.bias.base != nullptr;
+  // stage the tile's fp32 sums through shared memory (the operand ring is
+  // free), rows rotated by 4*row floats against bank conflicts, then write
+  // whole rows with all warps (coalesced 512 B per row)
+  float* part = reinterpret_cast<float*>(smem);  // 128 x 128 fp32 = 64 KiB
+  if (warp >= 2) {
+    const int lrow = (warp & 3) * 32 + lane;
+#pragma unroll
+    for (int q = 0; q < BN; q += 4)
+      *reinterpret_cast<float4*>(part + lrow * BN + ((q + 4 * lrow) & (BN - 1))) =
+          make_float4(vals[q], vals[q + 1], vals[q + 2], vals[q + 3]);
+  }
+  cgrp::cluster_group cl = cgrp::this_cluster();
+  if (S > 1) cl.sync();
+  else __syncthreads();
+  const int rows = BM / S;  // S is a power of two <= 8: split z reduces rows [z*rows, (z+1)*rows)
+  const bool vec = P.c_vec && n0 + BN <= P.N;
+  const int total = rows * (BN / 4);
+  constexpr int U = 4;  // loads of U slots are issued before any store (no dependent DRAM round trips)
+  for (int e0 = threadIdx.x; e0 < total; e0 += U * kThreads) {
+    float4 acc4[U], old4[U], b4[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * kThreads;
+      acc4[u] = old4[u] = b4[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e >= total) continue;
+      const int lm = z * rows + e / (BN / 4), ln = (e % (BN / 4)) * 4;
+      const int64_t m = m0 + lm;
+      if (m >= P.M || !vec) continue;
+      if (P.accumulate) old4[u] = *reinterpret_cast<const float4*>(orow(P.C, m) + n0 + ln);
+      if (has_bias) b4[u] = *reinterpret_cast<const float4*>(orow(P.bias, m) + n0 + ln);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * kThreads;
+      if (e >= total) continue;
+      const int lm = z * rows + e / (BN / 4), ln = (e % (BN / 4)) * 4;
+      const int sw = (ln + 4 * lm) & (BN - 1);
+      for (int q = 0; q < S; ++q) {
+        const float4 x = *reinterpret_cast<const float4*>((S > 1 ? cl.map_shared_rank(part, q) : part) + lm * BN + sw);
+        acc4[u].x += x.x;
+        acc4[u].y += x.y;
+        acc4[u].z += x.z;
+        acc4[u].w += x.w;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * kThreads;
+      if (e >= total) continue;
+      const int lm = z * rows + e / (BN / 4), ln = (e % (BN / 4)) * 4;
+      const int64_t m = m0 + lm;
+      if (m >= P.M) continue;
+      float* crow = const_cast<float*>(orow(P.C, m));
+      if (vec) {
+        float4 v = acc4[u];
+        v.x += b4[u].x; v.y += b4[u].y; v.z += b4[u].z; v.w += b4[u].w;
+        v.x += old4[u].x; v.y += old4[u].y; v.z += old4[u].z; v.w += old4[u].w;
+        *reinterpret_cast<float4*>(crow + n0 + ln) = v;
+      } else {
+        const float* brow = has_bias ? orow(P.bias, m) : nullptr;
+        const float sv[4] = {acc4[u].x, acc4[u].y, acc4[u].z, acc4[u].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t n = n0 + ln + q;
+          if (n < P.N) {
+            float v = sv[q];
+            if (brow) v += brow[n];
+            if (P.accumulate) v += crow[n];
+            crow[n] = v;
+          }
+        }
+      }
+    }
+  }
+  if (S > 1) cl.sync();
+}
+
+// lo[r][c] = x - tf32(x) for a rows x cols block with row stride ld (dst dense, stride cols_p)
+__global__ void split_lo_kernel(const float* __restrict__ src, int64_t ld, int64_t rows, int64_t cols,
+                                int64_t cols_p, float* __restrict__ dst) {
+  const int64_t c4 = cols_p >> 2;
+  const int64_t total = rows * c4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / c4, c = (i - r * c4) * 4;
+    const float* s = src + r * ld + c;
+    float4 o;
+    float* op = reinterpret_cast<float*>(&o);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float x = c + q < cols ? s[q] : 0.f;
+      op[q] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    }
+    *reinterpret_cast<float4*>(dst + r * cols_p + c) = o;
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encoder() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// rows x cols fp32 block, row stride ld floats; box {32, box_rows} (K-major:
+// 32 k x 128 rows, SWIZZLE_128B) or {32, 32} (MN-major, SWIZZLE_128B_ATOM_32B)
+bool make_map(CUtensorMap* m, const float* base, int64_t ld, int64_t rows, int64_t cols, bool mn) {
+  EncodeFn enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {32, mn ? 32u : 128u};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool tma_gemm_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DG_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on && tc_gemm_enabled();
+}
+
+int64_t tma_lo_floats(int64_t rows, int64_t cols) { return rows * ((cols + 3) & ~int64_t(3)); }
+
+bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
+  TmaGemmPlan p{};
+  p.a_mn = o.a_mn;
+  p.b_mn = o.b_mn;
+  TmaGemmArgs& a = p.args;
+  a.M = o.M;
+  a.N = o.N;
+  a.K = o.K;
+  a.C = o.C;
+  a.bias = o.bias;
+  a.accumulate = o.accumulate;
+  a.c_vec = !o.C.rows && (reinterpret_cast<uintptr_t>(o.C.base) % 16 == 0) && o.C.ld % 4 == 0 &&
+            (!o.bias.base || o.bias.rows || (reinterpret_cast<uintptr_t>(o.bias.base) % 16 == 0 && o.bias.ld % 4 == 0));
+  // operand blocks: A is (M rows x K) or (K rows x M); B is (N x K) or (K x N)
+  const int64_t ar = o.a_mn ? o.K : o.M, ac = o.a_mn ? o.M : o.K;
+  const int64_t br = o.b_mn ? o.K : o.N, bc = o.b_mn ? o.N : o.K;
+  const int64_t acp = (ac + 3) & ~int64_t(3), bcp = (bc + 3) & ~int64_t(3);
+  p.a_src = o.A;
+  p.a_ld = o.lda;
+  p.a_rows = ar;
+  p.a_cols = ac;
+  p.a_colsp = acp;
+  p.a_lo = o.A_lo;
+  p.b_src = o.B;
+  p.b_ld = o.ldb;
+  p.b_rows = br;
+  p.b_cols = bc;
+  p.b_colsp = bcp;
+  p.b_lo = o.B_lo;
+  if (!make_map(&p.mAh, o.A, o.lda, ar, ac, o.a_mn) || !make_map(&p.mAl, o.A_lo, acp, ar, ac, o.a_mn) ||
+      !make_map(&p.mBh, o.B, o.ldb, br, bc, o.b_mn) || !make_map(&p.mBl, o.B_lo, bcp, br, bc, o.b_mn))
+    return false;
+  a.tiles_n = (o.N + BN - 1) / BN;
+  const int tiles = ((o.M + BM - 1) / BM) * a.tiles_n;
+  const int kt = (o.K + BK - 1) / BK;
+  // split-K (a cluster of S CTAs per tile) for the best wave efficiency on
+  // 148 SMs (one CTA per SM); each split keeps >= 4 k-tiles
+  // cost model: waves x (fixed per-CTA cost ~ 4 k-tiles + k-tiles per split)
+  int S = 1;
+  double best = 1e30;
+  for (int s2 = 1; s2 <= 8; s2 *= 2) {
+    if (s2 > 1 && kt < 4 * s2) break;
+    const int units = tiles * s2;
+    const double cost = (double)((units + 147) / 148) * (4.0 + (double)kt / s2);
+    if (cost < best * 0.97) {
+      best = cost;
+      S = s2;
+    }
+  }
+  a.splits = S;
+  p.ctas = tiles * S;
+  p.flops = 2.0 * o.M * (double)o.N * o.K;
+  *out = p;
+  return true;
+}
+
+int launch_tma_gemm(const TmaGemmPlan& p, bool split_a, bool split_b, cudaStream_t s) {
+  int n = 0;
+  if (split_a) {
+    const int64_t tot = p.a_rows * (p.a_colsp / 4);
+    split_lo_kernel<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, s>>>(p.a_src, p.a_ld, p.a_rows,
+                                                                                      p.a_cols, p.a_colsp, p.a_lo);
+    ++n;
+  }
+  if (split_b) {
+    const int64_t tot = p.b_rows * (p.b_colsp / 4);
+    split_lo_kernel<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, s>>>(p.b_src, p.b_ld, p.b_rows,
+                                                                                      p.b_cols, p.b_colsp, p.b_lo);
+    ++n;
+  }
+  void (*k)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const TmaGemmArgs) =
+      p.a_mn ? (p.b_mn ? tma_gemm_kernel<true, true> : tma_gemm_kernel<true, false>)
+             : (p.b_mn ? tma_gemm_kernel<false, true> : tma_gemm_kernel<false, false>);
+  static bool attr[4] = {false, false, false, false};
+  const int ki = (p.a_mn ? 2 : 0) + (p.b_mn ? 1 : 0);
+  if (!attr[ki]) {
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) != cudaSuccess) return -1;
+    attr[ki] = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.ctas);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = p.args.splits;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, k, p.mAh, p.mAl, p.mBh, p.mBl, p.args) != cudaSuccess) return -1;
+  return n + 1;
+}
+
+}  // namespace dg
