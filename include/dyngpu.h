@@ -150,6 +150,9 @@ int dg_schedule_stats(dg_graph* g, int32_t lo, int32_t hi, int64_t* out8);
 /* host-only: persistent LSTM stacks the planner forms over nodes [lo, hi]
  * (out4 = stacks, chains, steps, CTAs of one launch per stack) */
 int dg_schedule_rnn_stats(dg_graph* g, int32_t lo, int32_t hi, int64_t* out4);
+/* diagnostics: per-CTA globaltimer stamps of the last persistent LSTM launches
+ * recorded with DG_RNN_TRACE=1 (out: 2 x 148 x 256 uint64) */
+int dg_rnn_trace(uint64_t* out, int64_t n);
 int dg_profile_read(dg_graph* g, int32_t cls, double* out4);
 int dg_profile_reset(dg_graph* g);
 

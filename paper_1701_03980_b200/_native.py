@@ -101,6 +101,7 @@ def _declare(lib):
         "dg_profile_reset": (ctypes.c_int, [c_vp]),
         "dg_schedule_stats": (ctypes.c_int, [c_vp, c_i32, c_i32, c_vp]),
         "dg_schedule_rnn_stats": (ctypes.c_int, [c_vp, c_i32, c_i32, c_vp]),
+        "dg_rnn_trace": (ctypes.c_int, [c_vp, c_i64]),
         "dg_trainer_create": (ctypes.c_int, [ctypes.c_int, c_f32, c_f32, c_f32, c_f32, c_f32, c_f32, ctypes.c_int,
                                               ctypes.POINTER(c_vp)]),
         "dg_trainer_destroy": (ctypes.c_int, [c_vp]),

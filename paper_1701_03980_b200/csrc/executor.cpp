@@ -506,6 +506,7 @@ static bool match_cell(const dg_graph* g, int h, const std::vector<int>& consume
 static constexpr int kSmCount = 148;
 static constexpr size_t kSmemMax = 227 * 1024 - 1024;  // dynamic (static step tables aside)
 static constexpr int kFlagInts = 65536;  // arrival counters (rnn.cu), end of the counter region
+static constexpr bool kStackChains = false;
 
 // CJ (dG columns staged per chunk) for a backward launch: the largest multiple
 // of 32 (<= max gw) that fits next to the resident W^T slices.
@@ -609,10 +610,13 @@ static std::vector<int> find_rnn_stacks(const dg_graph* g, const std::vector<Uni
     chains.push_back(std::move(ch));
   }
   if (chains.empty()) return stack_of;
-  // stacking: x^b_t == h^a_t for all t
+  // stacking (x^b_t == h^a_t for all t, one wavefront launch) is off: each
+  // chain's input projection b + Wx x_t is one batched tensor-core GEMM over
+  // all steps before its recurrence, so the layers run one after the other
+  // and the recurrent kernels keep only Wh resident
   const int nch = (int)chains.size();
   std::vector<int> src(nch, -1), cons(nch, -1);
-  for (int b = 0; b < nch; ++b) {
+  for (int b = 0; b < nch && kStackChains; ++b) {
     const auto& cb = chains[b];
     auto it = cell_by_h.find(ci[cb[0]].x);
     if (it == cell_by_h.end()) continue;
@@ -689,7 +693,7 @@ static std::vector<int> find_rnn_stacks(const dg_graph* g, const std::vector<Uni
       cp.n_s = (cp.B + st.bs - 1) / st.bs;
       cp.n_u = (cp.H + kRnnUnits - 1) / kRnnUnits;
       ctas += cp.n_s * cp.n_u;
-      if (rnn_fwd_smem(cp.K_in + cp.H, st.bs) > kSmemMax) fits = false;
+      if (rnn_fwd_smem(cp.H, st.bs) > kSmemMax) fits = false;
       st.chains.push_back(std::move(cp));
     }
     for (auto& cp : st.chains) {
@@ -1485,9 +1489,46 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
     }
     if (!cur.empty()) launches.push_back(cur);
   }
+  if (!bwd) {
+    // input projections of every step, batched: G_t = b + Wx x_t (the
+    // recurrent kernels add Wh h_{t-1})
+    for (int u : gr.units) {
+      for (const RnnChainPlan& cp : S.rnns[S.units[u].rnn].chains) {
+        const int T = (int)cp.G.size(), Bt = cp.B;
+        std::vector<uintptr_t> xrows((size_t)T * Bt), crow((size_t)T * Bt);
+        for (int t = 0; t < T; ++t) {
+          const Node& Gn = g->nodes[cp.G[t]];
+          const Node& xn = g->nodes[g->inputs[Gn.in_off + 2]];
+          for (int b = 0; b < Bt; ++b) {
+            xrows[(size_t)t * Bt + b] = P(xn.val + (xn.batch == 1 ? 0 : (int64_t)b * cp.K_in));
+            crow[(size_t)t * Bt + b] = P(Gn.val + (int64_t)b * cp.gw);
+          }
+        }
+        GemmBatch& bt = gemm_batch_for(g, plan, *gb, gr.level, C_GEMM_FWD, false, false);
+        GemmProblem pr{};
+        pr.M = T * Bt;
+        pr.N = cp.gw;
+        pr.n_seg = 1;
+        pr.accumulate = 0;
+        pr.seg[0].K = cp.K_in;
+        pr.seg[0].A.rows = dev_at<const float*>(g, B.push(xrows));
+        pr.seg[0].A.rows_aligned = all_aligned16(xrows);
+        pr.seg[0].B.base = param_at(cp.hWx)->val;
+        pr.seg[0].B.ld = cp.gw;
+        pr.C.rows = dev_at<const float*>(g, B.push(crow));
+        pr.C.rows_aligned = all_aligned16(crow);
+        pr.bias.base = param_at(cp.hb)->val;
+        pr.bias.ld = 0;
+        bt.probs.push_back(pr);
+        bt.bytes += 4.0 * ((double)pr.M * cp.K_in + (double)cp.K_in * pr.N + (double)pr.M * pr.N);
+      }
+    }
+    flush_gemm(g, plan, *gb);
+  }
   for (const auto& L : launches) {
     RnnArgs a{};
     a.flags = flag_base(g);
+    a.gx = bwd ? 0 : 1;
     a.bs = S.rnns[L[0]].bs;
     int cta = 0, flag = 0;
     double flops = 0, bytes = 0;
@@ -1502,7 +1543,7 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
         c.T = T;
         c.B = cp.B;
         c.H = cp.H;
-        c.K_in = cp.K_in;
+        c.K_in = bwd ? cp.K_in : 0;  // forward: recurrent part only (gx mode)
         c.gw = cp.gw;
         c.off_i = cp.off[0];
         c.off_f = cp.off[1];
@@ -1549,7 +1590,7 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
         if (bwd) c.grad = dev_at<float*>(g, B.push(grads));
         c.b1 = dev_at<int>(g, B.push(b1));
         const double gwd = cp.gw, bd = cp.B;
-        flops += bwd ? 2.0 * bd * gwd * cp.H * (T - 1) : 2.0 * bd * gwd * (cp.K_in + cp.H) * T;
+        flops += bwd ? 2.0 * bd * gwd * cp.H * (T - 1) : 2.0 * bd * gwd * cp.H * T;
         bytes += 4.0 * bd * cp.H * T * (bwd ? 30 : 17);
       }
       for (int k = base; k < a.n_chains; ++k) {
@@ -1560,21 +1601,43 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
     a.ctas = cta;
     a.n_flags = flag;
     a.vec = vec_ok ? 1 : 0;
-    size_t smem = 0;
+    a.trace = rnn_trace_enabled() ? 1 : 0;
+    // cluster mode: one cluster per (chain, batch slice) exchanging through
+    // distributed shared memory; needs equal unit-block counts (<= 16)
+    int cl = a.ch[0].n_u;
+    bool use_cl = rnn_cluster_enabled() && a.vec && cl <= 16;
+    for (int k = 0; k < a.n_chains; ++k) use_cl = use_cl && a.ch[k].n_u == cl;
+    size_t smem = 0, smem_cl = 0;
     if (bwd) {
       for (int k = 0; k < a.n_chains; ++k) {
         const int gwc = a.ch[k].cons >= 0 ? a.ch[a.ch[k].cons].gw : 0;
         a.cj = std::min(a.cj, rnn_pick_cj(a.ch[k].gw, gwc, a.bs));
+        if (use_cl) {
+          int cj = a.cj;
+          while (cj > 32 && rnn_bwd_cl_smem(a.ch[k].H, gwc, a.bs, cj) > kSmemMax) cj -= 32;
+          a.cj = cj;
+        }
       }
       for (int k = 0; k < a.n_chains; ++k) {
         const int gwc = a.ch[k].cons >= 0 ? a.ch[a.ch[k].cons].gw : 0;
         smem = std::max(smem, rnn_bwd_smem(a.ch[k].gw, gwc, a.bs, a.cj));
+        smem_cl = std::max(smem_cl, rnn_bwd_cl_smem(a.ch[k].H, gwc, a.bs, a.cj));
       }
     } else {
       a.cj = 0;
-      for (int k = 0; k < a.n_chains; ++k) smem = std::max(smem, rnn_fwd_smem(a.ch[k].K_in + a.ch[k].H, a.bs));
+      for (int k = 0; k < a.n_chains; ++k) {
+        smem = std::max(smem, rnn_fwd_smem(a.ch[k].K_in + a.ch[k].H, a.bs));  // K_in = 0 (gx mode)
+        smem_cl = std::max(smem_cl, rnn_fwd_cl_smem(a.ch[k].K_in, a.ch[k].H, a.bs));
+      }
     }
-    plan.ops.push_back([a, smem, bwd, st](char*) { return launch_rnn(a, bwd, smem, st); });
+    use_cl = use_cl && smem_cl <= kSmemMax;
+    plan.ops.push_back([a, smem, smem_cl, use_cl, cl, bwd, st](char*) {
+      if (use_cl) {
+        const int n = launch_rnn_cluster(a, bwd, smem_cl, cl, st);
+        if (n != -2) return n;  // -2: the clusters cannot all be resident
+      }
+      return launch_rnn(a, bwd, smem, st);
+    });
     plan.tag(bwd ? C_RNN_BWD : C_RNN_FWD, flops, bytes);
   }
   if (!bwd) return;
@@ -1690,7 +1753,7 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
   if (!(gr.kind == DG_OP_AFFINE && affine_gemm_ok(g, n0))) flush_gemm(g, plan, gb);
 
   if (gr.kind == -3) {  // persistent LSTM stacks
-    plan_rnn_group(g, S, gr, plan, false, nullptr, nullptr, nullptr);
+    plan_rnn_group(g, S, gr, plan, false, nullptr, nullptr, &gb);
     return;
   }
   if (gr.kind == -2) {  // fused gated cells
@@ -2835,6 +2898,12 @@ int dg_schedule_rnn_stats(dg_graph* g, int32_t lo, int32_t hi, int64_t* out4) {
   out4[1] = chains;
   out4[2] = steps;
   out4[3] = ctas;
+  return DG_OK;
+}
+
+int dg_rnn_trace(uint64_t* out, int64_t n) {
+  if (rnn_trace_read(reinterpret_cast<unsigned long long*>(out), (size_t)n) != 0)
+    return fail(DG_CUDA, "rnn trace read failed");
   return DG_OK;
 }
 

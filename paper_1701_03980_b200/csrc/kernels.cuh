@@ -99,6 +99,8 @@ struct RnnChain {
 struct RnnArgs {
   int n_chains, ctas, bs, cj, n_flags;
   int vec;     // every staged row is 16B aligned with a multiple-of-4 width (cp.async path)
+  int trace;   // record the per-step timeline (rnn_trace_read)
+  int gx;      // G slots hold b + Wx x_t already (chains run with K_in = 0: recurrent part only)
   int* flags;  // zeroed by the launcher
   RnnChain ch[kRnnMaxChains];
 };
@@ -114,8 +116,17 @@ int rnn_rows_per_cta(int B);
 size_t rnn_fwd_smem(int K, int bs);
 size_t rnn_bwd_smem(int gw, int gw_c, int bs, int cj);
 bool rnn_enabled();  // DG_RNN=0 disables the persistent path (A/B checks)
+bool rnn_cluster_enabled();  // DG_RNN_CLUSTER=0 keeps the global-counter kernels
 int launch_rnn(const RnnArgs& a, bool backward, size_t smem, cudaStream_t s);
+// cluster variants (one cluster of n_u CTAs per chain slice, DSMEM exchange):
+// returns -2 when the clusters cannot all be resident (caller falls back)
+size_t rnn_fwd_cl_smem(int K_in, int H, int bs);
+size_t rnn_bwd_cl_smem(int H, int gw_c, int bs, int cj);
+int launch_rnn_cluster(const RnnArgs& a, bool backward, size_t smem, int cluster, cudaStream_t s);
 int launch_rnn_c0(const RnnC0& a, cudaStream_t s);
+bool rnn_trace_enabled();  // DG_RNN_TRACE=1
+// [2][148][256] globaltimer stamps of the last launches (fwd, bwd)
+int rnn_trace_read(unsigned long long* host, size_t n);
 
 // --------------------------------------------------------------- structural
 struct PickArgs {

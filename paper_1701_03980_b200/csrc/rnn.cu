@@ -39,17 +39,21 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "kernels.cuh"
 
 namespace dg {
 
+bool rnn_trace_enabled();
+
 namespace {
 
 constexpr int kRT = 256;  // threads per CTA
 constexpr int kU = kRnnUnits;
 constexpr int kCU = 4 * kU;  // gate columns per CTA
+constexpr int kSmCountTrace = 148;
 
 __device__ __forceinline__ float sigmoid_ref(float x) {
   x = fminf(fmaxf(x, -60.f), 60.f);  // ops.py:78-83
@@ -86,10 +90,36 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// optional timeline (DG_RNN_TRACE=1): per CTA [0] start, [1] weights resident,
+// [2 + t] arrival of step t (forward order for both kernels), globaltimer ns
+constexpr int kTraceSlots = 256;
+__device__ unsigned long long g_rnn_trace[2][kSmCountTrace][kTraceSlots];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace(int kind, int slot) {
+  if (slot < kTraceSlots && blockIdx.x < kSmCountTrace) g_rnn_trace[kind][blockIdx.x][slot] = gtimer();
+}
+
+// barrier among the 256 compute threads (named barrier 1); the cluster
+// kernels add a signalling warp that must not join these
+__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
 __device__ __forceinline__ int chain_of(const RnnArgs& a, int cta) {
   int ci = 0;
   while (ci + 1 < a.n_chains && cta >= a.ch[ci + 1].cta0) ++ci;
   return ci;
+}
+
+// gate column of a lane's c-th accumulator (lane column group lc of LC):
+// 4-wide chunks interleaved across lanes so a quarter-warp's float4 accesses
+// cover 128 contiguous bytes (no bank conflicts on the partial-sum stores)
+template <int LC, int TC>
+__device__ __forceinline__ int lane_col(int lc, int c) {
+  if constexpr (TC >= 4) return (c >> 2) * (LC * 4) + lc * 4 + (c & 3);
+  else return lc * TC + c;
 }
 
 // slots per step (CellSlots with m = 1, kernels.cu) + x_t + h_{t-1}
@@ -113,7 +143,7 @@ __global__ void __launch_bounds__(kRT, 1) rnn_fwd_kernel(const __grid_constant__
   float* sm = reinterpret_cast<float*>(smem4);
   __shared__ StepPtrs sp[2];
   const int ci = chain_of(a, blockIdx.x);
-  const RnnChain& C = a.ch[ci];
+  const RnnChain C = a.ch[ci];  // register copy (dynamic-index constant loads are slow)
   const int local = blockIdx.x - C.cta0;
   const int s = local / C.n_u, ub = local - (local / C.n_u) * C.n_u;
   const int b0 = s * BS, j0 = ub * kU;
@@ -125,6 +155,7 @@ __global__ void __launch_bounds__(kRT, 1) rnn_fwd_kernel(const __grid_constant__
   float* bias = part + 8 * BS * kCU;       // [kCU]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int goff[4] = {C.off_i, C.off_f, C.off_o, C.off_g};
+  if (a.trace && tid == 0) trace(0, 0);
 
   // resident weight slice: column c = gate * 16 + jj  <->  G row goff[gate] + j0 + jj
   if (a.vec) {
@@ -159,6 +190,7 @@ __global__ void __launch_bounds__(kRT, 1) rnn_fwd_kernel(const __grid_constant__
   if (tid == kRnnSlots) sp[0].b1 = C.b1[0];
   cp_async_wait_all();
   __syncthreads();
+  if (a.trace && tid == 0) trace(0, 1);
 
   int* my_flags = a.flags + C.flag0 + s * C.T;
   const int* src_flags = nullptr;
@@ -174,12 +206,59 @@ __global__ void __launch_bounds__(kRT, 1) rnn_fwd_kernel(const __grid_constant__
   constexpr int LC = 32 / LB;
   constexpr int TC = kCU / LC;
   const int lb = lane / LC, lc = lane - (lane / LC) * LC;
-  const int kper = (K + 7) / 8;
-  const int kbeg = warp * kper, kend = min(K, kbeg + kper);
   const int cb = tid / kU, cj = tid - (tid / kU) * kU;  // cell thread: (row, unit)
   const int crow = b0 + cb, cjj = j0 + cj;
   const bool cell_mine = cb < BS && crow < C.B && cjj < C.H;
   float c_carry = 0.f;  // c_{t-1} of this thread's (row, unit), produced by itself
+
+  // stage columns [k_lo, k_hi) of this slice's [x_t | h_{t-1}] rows (L2 -> smem, bypassing L1)
+  auto stage = [&](const float* src, int64_t ld, bool b1, int k_lo, int k_hi) {
+    if (a.vec) {
+      const int w4 = (k_hi - k_lo) >> 2;
+      for (int idx = tid; idx < BS * w4; idx += kRT) {
+        const int b = idx / w4, q = idx - (idx / w4) * w4;
+        const int row = b0 + b;
+        float* dst = inS + (size_t)b * KP + k_lo + 4 * q;
+        if (row < C.B) cp_async16(dst, src + (b1 ? 0 : (int64_t)row * ld) + 4 * q);
+        else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      cp_async_wait_all();
+    } else {
+      const int w = k_hi - k_lo;
+      for (int idx0 = tid; idx0 < BS * w; idx0 += 4 * kRT) {
+        float v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int idx = idx0 + q * kRT;
+          const int b = idx / w, k = idx - (idx / w) * w;
+          v[q] = (idx < BS * w && b0 + b < C.B) ? __ldcg(src + (b1 ? 0 : (int64_t)(b0 + b) * ld) + k) : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int idx = idx0 + q * kRT;
+          if (idx < BS * w) inS[(size_t)(idx / w) * KP + k_lo + (idx - (idx / w) * w)] = v[q];
+        }
+      }
+    }
+  };
+  float acc[TB][TC];
+  // acc += rows[:, k_lo:k_hi] W[k_lo:k_hi, :] over this warp's share of the range
+  auto fma_range = [&](int k_lo, int k_hi) {
+    const int per = (k_hi - k_lo + 7) / 8;
+    const int kb = k_lo + warp * per, ke = min(k_hi, kb + per);
+#pragma unroll 4
+    for (int k = kb; k < ke; ++k) {
+      float xa[TB], wv[TC];
+#pragma unroll
+      for (int i = 0; i < TB; ++i) xa[i] = inS[(size_t)(i * LB + lb) * KP + k];
+#pragma unroll
+      for (int c = 0; c < TC; ++c) wv[c] = Ws[(size_t)k * kCU + lane_col<LC, TC>(lc, c)];
+#pragma unroll
+      for (int i = 0; i < TB; ++i)
+#pragma unroll
+        for (int c = 0; c < TC; ++c) acc[i][c] = fmaf(xa[i], wv[c], acc[i][c]);
+    }
+  };
 
   for (int t = 0; t < C.T; ++t) {
     const StepPtrs& P = sp[t & 1];
@@ -192,120 +271,92 @@ __global__ void __launch_bounds__(kRT, 1) rnn_fwd_kernel(const __grid_constant__
     }
     const int fl = P.b1;
     if (t == 0 && cell_mine) c_carry = __ldcg(P.p[S_CP] + ((fl & 4) ? cjj : (int64_t)crow * C.H + cjj));
-    if (tid == 0) {
-      if (src_flags) wait_count(src_flags + t, src_need);
-      if (t > 0) wait_count(my_flags + t - 1, C.n_u);
+    // gx mode: the G slot already holds b + Wx x_t (batched tensor-core GEMM
+    // before this launch); read it ahead of the waits
+    float gx[4] = {0.f, 0.f, 0.f, 0.f};
+    if (a.gx && cell_mine) {
+      const float* Gr = P.p[S_G] + (int64_t)crow * C.gw;
+      gx[0] = Gr[C.off_i + cjj];
+      gx[1] = Gr[C.off_f + cjj];
+      gx[2] = Gr[C.off_o + cjj];
+      gx[3] = Gr[C.off_g + cjj];
     }
-    __syncthreads();
-    {
-      // stage [x_t | h_{t-1}] rows of this slice (L2 -> smem, bypassing L1)
-      const float* X = P.p[S_X];
-      const float* Hp = P.p[S_HP];
-      if (a.vec) {
-        const int K4 = K >> 2, Kin4 = C.K_in >> 2;
-        for (int idx = tid; idx < BS * K4; idx += kRT) {
-          const int b = idx / K4, k4 = idx - (idx / K4) * K4;
-          const int row = b0 + b;
-          float* dst = inS + (size_t)b * KP + 4 * k4;
-          if (row < C.B) {
-            const float* src = k4 < Kin4 ? X + ((fl & 1) ? 0 : (int64_t)row * C.K_in) + 4 * k4
-                                         : Hp + ((fl & 2) ? 0 : (int64_t)row * C.H) + 4 * (k4 - Kin4);
-            cp_async16(dst, src);
-          } else {
-            *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-        }
-        cp_async_wait_all();
-      } else {
-        for (int idx0 = tid; idx0 < BS * K; idx0 += 4 * kRT) {
-          float v[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int idx = idx0 + q * kRT;
-            const int b = idx / K, k = idx - (idx / K) * K;
-            const int row = b0 + b;
-            v[q] = 0.f;
-            if (idx < BS * K && row < C.B)
-              v[q] = k < C.K_in ? __ldcg(X + ((fl & 1) ? 0 : (int64_t)row * C.K_in) + k)
-                                : __ldcg(Hp + ((fl & 2) ? 0 : (int64_t)row * C.H) + (k - C.K_in));
-          }
+    for (int i = 0; i < TB; ++i)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int idx = idx0 + q * kRT;
-            if (idx < BS * K) inS[(size_t)(idx / K) * KP + (idx - (idx / K) * K)] = v[q];
-          }
-        }
-      }
+      for (int c = 0; c < TC; ++c) acc[i][c] = 0.f;
+    // input part: needs only x_t (external, or the producer chain's step t),
+    // so it overlaps the arrival of this chain's step t-1
+    if (C.K_in > 0) {
+      if (tid == 0 && src_flags) wait_count(src_flags + t, src_need);
+      __syncthreads();
+      stage(P.p[S_X], C.K_in, (fl & 1) != 0, 0, C.K_in);
+      __syncthreads();
+      fma_range(0, C.K_in);
     }
+    // recurrent part: h_{t-1} of every unit block of this batch slice
+    if (tid == 0 && t > 0) wait_count(my_flags + t - 1, C.n_u);
     __syncthreads();
-    {
-      float acc[TB][TC];
-#pragma unroll
-      for (int i = 0; i < TB; ++i)
-#pragma unroll
-        for (int c = 0; c < TC; ++c) acc[i][c] = 0.f;
-#pragma unroll 4
-      for (int k = kbeg; k < kend; ++k) {
-        float xa[TB], wv[TC];
-#pragma unroll
-        for (int i = 0; i < TB; ++i) xa[i] = inS[(size_t)(i * LB + lb) * KP + k];
-#pragma unroll
-        for (int c = 0; c < TC; ++c) wv[c] = Ws[(size_t)k * kCU + lc * TC + c];
-#pragma unroll
-        for (int i = 0; i < TB; ++i)
-#pragma unroll
-          for (int c = 0; c < TC; ++c) acc[i][c] = fmaf(xa[i], wv[c], acc[i][c]);
-      }
-#pragma unroll
-      for (int i = 0; i < TB; ++i)
-#pragma unroll
-        for (int c = 0; c < TC; ++c) part[(warp * BS + i * LB + lb) * kCU + lc * TC + c] = acc[i][c];
-    }
+    stage(P.p[S_HP], C.H, (fl & 2) != 0, C.K_in, K);
     __syncthreads();
+    fma_range(C.K_in, K);
+#pragma unroll
+    for (int i = 0; i < TB; ++i)
+#pragma unroll
+      for (int c = 0; c < TC; ++c) part[(warp * BS + i * LB + lb) * kCU + lane_col<LC, TC>(lc, c)] = acc[i][c];
+    __syncthreads();
+    float x4[4] = {0.f, 0.f, 0.f, 0.f}, ai = 0.f, af = 0.f, ao = 0.f, ag = 0.f, ig = 0.f, p = 0.f, c = 0.f, tc = 0.f;
+    const int64_t r = (int64_t)crow * C.H + cjj;
     if (cell_mine) {
-      float x4[4];
 #pragma unroll
       for (int gate = 0; gate < 4; ++gate) {
         float sum = 0.f;
 #pragma unroll
         for (int w = 0; w < 8; ++w) sum += part[(w * BS + cb) * kCU + gate * kU + cj];
-        x4[gate] = bias[gate * kU + cj] + sum;
+        x4[gate] = (a.gx ? gx[gate] : bias[gate * kU + cj]) + sum;
       }
-      const int row = crow, j = cjj;
-      float* G = const_cast<float*>(P.p[S_G]) + (int64_t)row * C.gw;
-      G[C.off_i + j] = x4[0];
-      G[C.off_f + j] = x4[1];
-      G[C.off_o + j] = x4[2];
-      G[C.off_g + j] = x4[3];
-      const int64_t r = (int64_t)row * C.H + j;
-      auto W = [&](int slot, float v) { const_cast<float*>(P.p[slot])[r] = v; };
-      W(S_PI, x4[0]);
-      W(S_PF, x4[1]);
-      W(S_PO, x4[2]);
-      W(S_PG, x4[3]);
-      const float ai = sigmoid_ref(x4[0]), af = sigmoid_ref(x4[1]), ao = sigmoid_ref(x4[2]);
-      const float ag = tanhf(x4[3]);
-      W(S_AI, ai);
-      W(S_AF, af);
-      W(S_AO, ao);
-      W(S_AG, ag);
-      float c = ai * ag;
-      W(S_IG, c);
-      const float p = af * c_carry;
-      W(S_FC, p);
-      c = c + p;
-      W(S_C, c);
+      ai = sigmoid_ref(x4[0]);
+      af = sigmoid_ref(x4[1]);
+      ao = sigmoid_ref(x4[2]);
+      ag = tanhf(x4[3]);
+      ig = ai * ag;
+      p = af * c_carry;
+      c = ig + p;
       c_carry = c;
-      const float tc = tanhf(c);
-      W(S_TC, tc);
-      W(S_H, ao * tc);
+      tc = tanhf(c);
+      // the critical output (read by the other CTAs of the slice) first
+      const_cast<float*>(P.p[S_H])[r] = ao * tc;
     }
     if (warp == 1 && t + 1 < C.T) {
       if (lane < kRnnSlots) sp[(t + 1) & 1].p[lane] = nxt;
       if (lane == kRnnSlots) sp[(t + 1) & 1].b1 = nxt_b1;
     }
     __syncthreads();
-    if (tid == 0) arrive(my_flags + t);
+    if (tid == 0) {
+      arrive(my_flags + t);
+      if (a.trace) trace(0, 2 + t);
+    }
+    if (cell_mine) {
+      // every other node of the step keeps its value slot (off the critical path)
+      float* G = const_cast<float*>(P.p[S_G]) + (int64_t)crow * C.gw;
+      G[C.off_i + cjj] = x4[0];
+      G[C.off_f + cjj] = x4[1];
+      G[C.off_o + cjj] = x4[2];
+      G[C.off_g + cjj] = x4[3];
+      auto W = [&](int slot, float v) { const_cast<float*>(P.p[slot])[r] = v; };
+      W(S_PI, x4[0]);
+      W(S_PF, x4[1]);
+      W(S_PO, x4[2]);
+      W(S_PG, x4[3]);
+      W(S_AI, ai);
+      W(S_AF, af);
+      W(S_AO, ao);
+      W(S_AG, ag);
+      W(S_IG, ig);
+      W(S_FC, p);
+      W(S_C, c);
+      W(S_TC, tc);
+    }
   }
 }
 
@@ -357,7 +408,7 @@ __device__ __forceinline__ float rows_times_wt(const float* dG, int gw, int B, i
         }
       }
     }
-    __syncthreads();
+    csync();
     const int per = (cj + 7) / 8;
     const int jb = warp * per, je = min(cj, jb + per);
     if (active) {
@@ -374,7 +425,7 @@ __device__ __forceinline__ float rows_times_wt(const float* dG, int gw, int B, i
           for (int c = 0; c < TC; ++c) acc[i][c] = fmaf(xa[i], wv[c], acc[i][c]);
       }
     }
-    __syncthreads();
+    csync();
   }
   if (active) {
 #pragma unroll
@@ -382,14 +433,14 @@ __device__ __forceinline__ float rows_times_wt(const float* dG, int gw, int B, i
 #pragma unroll
       for (int c = 0; c < TC; ++c) part[(warp * BS + i * LB + lb) * kU + lc * TC + c] = acc[i][c];
   }
-  __syncthreads();
+  csync();
   const int cb = tid / kU, cu = tid - (tid / kU) * kU;
   float sum = 0.f;
   if (cb < BS) {
 #pragma unroll
     for (int w = 0; w < 8; ++w) sum += part[(w * BS + cb) * kU + cu];
   }
-  __syncthreads();
+  csync();
   return sum;
 }
 
@@ -405,13 +456,14 @@ __global__ void __launch_bounds__(kRT, 1) rnn_bwd_kernel(const __grid_constant__
   float* sm = reinterpret_cast<float*>(smem4);
   __shared__ StepPtrs2 sp[2];
   const int ci = chain_of(a, blockIdx.x);
-  const RnnChain& C = a.ch[ci];
+  const RnnChain C = a.ch[ci];  // register copy (dynamic-index constant loads are slow)
   const int local = blockIdx.x - C.cta0;
   const int s = local / C.n_u, ub = local - (local / C.n_u) * C.n_u;
   const int b0 = s * BS, j0 = ub * kU;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const RnnChain* Cc = C.cons >= 0 ? &a.ch[C.cons] : nullptr;
   const int gw_c = Cc ? Cc->gw : 0;
+  if (a.trace && tid == 0) trace(1, 0);
   float* WhT = sm;                              // [gw][16]
   float* WcT = WhT + (size_t)C.gw * kU;         // [gw_c][16]
   float* dGs = WcT + (size_t)gw_c * kU;         // [BS][CJ+4]
@@ -440,6 +492,7 @@ __global__ void __launch_bounds__(kRT, 1) rnn_bwd_kernel(const __grid_constant__
   }
   cp_async_wait_all();
   __syncthreads();
+  if (a.trace && tid == 0) trace(1, 1);
 
   int* my_flags = a.flags + C.flag0 + s * C.T;
   const int* cons_flags = Cc ? a.flags + Cc->flag0 + s * Cc->T : nullptr;
@@ -447,8 +500,31 @@ __global__ void __launch_bounds__(kRT, 1) rnn_bwd_kernel(const __grid_constant__
   const int row = b0 + cb, j = j0 + cj;
   const bool mine = cb < BS && row < C.B && j < C.H;
   const int64_t r = (int64_t)row * C.H + j;
-  float rec = 0.f;      // dh_t from step t+1 of this chain
+  float rec = 0.f;       // dh_t from step t+1 of this chain
+  float cons = 0.f;      // dh_t from the consumer chain's step t
   float dc_carry = 0.f;  // dc_t contribution of step t+1 (f_{t+1} * dc_{t+1})
+  // forward values and external gradient contributions of step t's cell: all
+  // independent of other CTAs, loaded ahead of the waits
+  float ao = 0.f, ai = 0.f, ag = 0.f, tc = 0.f, af = 0.f, ck = 0.f, gh_ext = 0.f, gc_ext = 0.f;
+  auto load_cell = [&](const StepPtrs2& P) {
+    if (!mine) return;
+    const bool cb1 = (P.b1 & 4) != 0;
+    ao = P.v[S_AO][r];
+    ai = P.v[S_AI][r];
+    ag = P.v[S_AG][r];
+    tc = P.v[S_TC][r];
+    af = P.v[S_AF][r];
+    ck = P.v[S_CP][cb1 ? j : r];
+    gh_ext = P.d[S_H][r];
+    gc_ext = P.d[S_C][r];
+  };
+  load_cell(sp[(C.T - 1) & 1]);
+  if (Cc) {
+    if (tid == 0) wait_count(cons_flags + C.T - 1, Cc->n_u);
+    __syncthreads();
+    cons = rows_times_wt<BS>(Cc->grad[(size_t)(C.T - 1) * kRnnSlots + S_G], gw_c, C.B, b0, WcT, dGs, a.cj, part,
+                             a.vec);
+  }
 
   for (int t = C.T - 1; t >= 0; --t) {
     const StepPtrs2& P = sp[t & 1];
@@ -463,63 +539,30 @@ __global__ void __launch_bounds__(kRT, 1) rnn_bwd_kernel(const __grid_constant__
       }
       if (lane == kRnnSlots) nb1 = C.b1[t - 1];
     }
-    const int fl = P.b1;
-    const bool cb1 = (fl & 4) != 0;
-    // forward values and external gradient contributions of this cell: all
-    // independent of other CTAs, loaded before any wait
-    float ao = 0.f, ai = 0.f, ag = 0.f, tc = 0.f, af = 0.f, ck = 0.f, gh_ext = 0.f, gc_ext = 0.f;
+    const bool cb1 = (P.b1 & 4) != 0;
+    float gh = 0.f, d_tc = 0.f, d_o = 0.f, dc = 0.f, d_i = 0.f, d_g = 0.f, dpi = 0.f, dpo = 0.f, dpg = 0.f;
+    float d_f = 0.f, dpf = 0.f;
     if (mine) {
-      ao = P.v[S_AO][r];
-      ai = P.v[S_AI][r];
-      ag = P.v[S_AG][r];
-      tc = P.v[S_TC][r];
-      af = P.v[S_AF][r];
-      ck = P.v[S_CP][cb1 ? j : r];
-      gh_ext = P.d[S_H][r];
-      gc_ext = P.d[S_C][r];
-    }
-    float cons = 0.f;
-    if (Cc) {
-      if (tid == 0) wait_count(cons_flags + t, Cc->n_u);
-      __syncthreads();
-      cons = rows_times_wt<BS>(Cc->grad[(size_t)t * kRnnSlots + S_G], gw_c, C.B, b0, WcT, dGs, a.cj, part,
-                               a.vec);
-    }
-    if (mine) {
-      // internal slots have this cell as their only consumer: written, not
-      // accumulated; h and c slots add the contributions gathered above
-      float* const* D = P.d;
-      const float gh = gh_ext + rec + cons;
-      D[S_H][r] = gh;
-      const float d_tc = gh * ao;
-      const float d_o = gh * tc;
-      D[S_TC][r] = d_tc;
-      D[S_AO][r] = d_o;
-      const float dc = (gc_ext + dc_carry) + (1.f - tc * tc) * d_tc;
-      D[S_C][r] = dc;
-      D[S_IG][r] = dc;
-      const float d_i = dc * ag, d_g = dc * ai;
-      D[S_AI][r] = d_i;
-      D[S_AG][r] = d_g;
-      const float dpi = ai * (1.f - ai) * d_i;
-      const float dpo = ao * (1.f - ao) * d_o;
-      const float dpg = (1.f - ag * ag) * d_g;
-      D[S_PI][r] = dpi;
-      D[S_PO][r] = dpo;
-      D[S_PG][r] = dpg;
-      float* dG = D[S_G] + (int64_t)row * C.gw;
+      // cell backward; the gate gradients (read by the other CTAs of the
+      // slice) are stored first.  Internal slots have this cell as their
+      // only consumer: written, not accumulated.
+      gh = gh_ext + rec + cons;
+      d_tc = gh * ao;
+      d_o = gh * tc;
+      dc = (gc_ext + dc_carry) + (1.f - tc * tc) * d_tc;
+      d_i = dc * ag;
+      d_g = dc * ai;
+      dpi = ai * (1.f - ai) * d_i;
+      dpo = ao * (1.f - ao) * d_o;
+      dpg = (1.f - ag * ag) * d_g;
+      d_f = dc * ck;
+      dpf = af * (1.f - af) * d_f;
+      float* dG = P.d[S_G] + (int64_t)row * C.gw;
       dG[C.off_i + j] = dpi;
       dG[C.off_o + j] = dpo;
       dG[C.off_g + j] = dpg;
-      D[S_FC][r] = dc;
-      const float d_f = dc * ck;
-      D[S_AF][r] = d_f;
-      const float dpf = af * (1.f - af) * d_f;
-      D[S_PF][r] = dpf;
       dG[C.off_f + j] = dpf;
       dc_carry = dc * af;
-      // c_{-1}: external state (batch-1 broadcast: rnn_c0_kernel sums it)
-      if (t == 0 && !cb1) D[S_CP][r] += dc_carry;
     }
     if (warp == 1 && t > 0) {
       if (lane < kRnnSlots) {
@@ -529,11 +572,573 @@ __global__ void __launch_bounds__(kRT, 1) rnn_bwd_kernel(const __grid_constant__
       if (lane == kRnnSlots) sp[(t - 1) & 1].b1 = nb1;
     }
     __syncthreads();
-    if (tid == 0) arrive(my_flags + t);
+    if (tid == 0) {
+      arrive(my_flags + t);
+      if (a.trace) trace(1, 2 + t);
+    }
+    if (mine) {
+      float* const* D = P.d;
+      D[S_H][r] = gh;
+      D[S_TC][r] = d_tc;
+      D[S_AO][r] = d_o;
+      D[S_C][r] = dc;
+      D[S_IG][r] = dc;
+      D[S_AI][r] = d_i;
+      D[S_AG][r] = d_g;
+      D[S_PI][r] = dpi;
+      D[S_PO][r] = dpo;
+      D[S_PG][r] = dpg;
+      D[S_FC][r] = dc;
+      D[S_AF][r] = d_f;
+      D[S_PF][r] = dpf;
+      // c_{-1}: external state (batch-1 broadcast: rnn_c0_kernel sums it)
+      if (t == 0 && !cb1) D[S_CP][r] += dc_carry;
+    }
     if (t > 0) {
+      load_cell(sp[(t - 1) & 1]);
+      // consumer chain's step t-1 (runs ahead of this chain): off the critical path
+      if (Cc) {
+        if (tid == 0) wait_count(cons_flags + t - 1, Cc->n_u);
+        __syncthreads();
+        cons = rows_times_wt<BS>(Cc->grad[(size_t)(t - 1) * kRnnSlots + S_G], gw_c, C.B, b0, WcT, dGs, a.cj, part,
+                                 a.vec);
+      }
       if (tid == 0) wait_count(my_flags + t, C.n_u);
       __syncthreads();
       rec = rows_times_wt<BS>(P.d[S_G], C.gw, C.B, b0, WhT, dGs, a.cj, part, a.vec);
+    }
+  }
+}
+
+// ====================================================================
+// Cluster variants: one thread-block cluster per (chain, batch slice) -- the
+// n_u CTAs that exchange h_t (forward) / dG_t (backward) every step.  The
+// exchange goes through distributed shared memory instead of L2:
+//   forward : each CTA pushes its (rows x 16 units) slice of h_t into every
+//             peer's double-buffered h operand block (st.shared::cluster) and
+//             arrives on the peers' mbarrier (release.cluster); a CTA waits on
+//             its own mbarrier (acquire.cluster) before the recurrent GEMM;
+//   backward: reduce-scatter -- each CTA multiplies its own 64 gate columns of
+//             dG_t by the matching rows of Wh (all units) and pushes the
+//             partial dh_{t-1} of every peer's 16 units into that peer's slot;
+//             the owner sums the n_u slots in rank order (deterministic).
+// Cross-chain dependencies (stacked layers) stay on global arrival counters,
+// published by a dedicated signalling warp (warp 8) so the fence never sits
+// on the compute warps' critical path.
+constexpr int kClThreads = kRT + 32;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void st_cluster(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster4(uint32_t addr, float4 v) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init_cl(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* b, uint32_t parity) {
+  const uint32_t a = smem_addr(b);
+  unsigned spins = 0;
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (!done && ++spins > (1u << 24)) __trap();
+  }
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// compute warps hand completed steps to the signalling warp through a
+// shared-memory step counter (release / acquire at CTA scope)
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void signal_loop(int* done, int* flags, int T, bool reverse) {
+  // publish step counters in order as the compute warps complete steps
+  for (int i = 0; i < T; ++i) {
+    unsigned spins = 0;
+    while (ld_acquire_cta(done) < i + 1) {
+      __nanosleep(64);
+      if (++spins > (1u << 24)) __trap();
+    }
+    arrive(flags + (reverse ? T - 1 - i : i));
+  }
+}
+
+template <int BS>
+__global__ void __launch_bounds__(kClThreads, 1) rnn_fwd_cl_kernel(const __grid_constant__ RnnArgs a) {
+  extern __shared__ float4 smem4[];
+  float* sm = reinterpret_cast<float*>(smem4);
+  __shared__ StepPtrs sp[2];
+  __shared__ __align__(8) uint64_t h_ready[2];
+  __shared__ int done_steps;
+  const int ci = chain_of(a, blockIdx.x);
+  const RnnChain C = a.ch[ci];  // register copy (dynamic-index constant loads are slow)
+  const int local = blockIdx.x - C.cta0;
+  const int s = local / C.n_u, ub = local - (local / C.n_u) * C.n_u;
+  const int b0 = s * BS, j0 = ub * kU;
+  const int K = C.K_in + C.H;
+  const int XP = C.K_in + 4, HP = C.H + 4;  // padded row strides
+  float* Ws = sm;                               // [K][64]
+  float* xS = Ws + (size_t)K * kCU;             // [BS][K_in+4]
+  float* hS = xS + (size_t)BS * XP;             // [2][BS][H+4]
+  float* part = hS + 2 * (size_t)BS * HP;       // [8][BS][64]
+  float* bias = part + 8 * BS * kCU;            // [64]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int goff[4] = {C.off_i, C.off_f, C.off_o, C.off_g};
+  const bool signals = C.cons >= 0;  // a stacked chain reads h_t from global memory
+  if (a.trace && tid == 0) trace(0, 0);
+
+  if (warp < 8) {
+    for (int idx = tid; idx < K * (kCU / 4); idx += kRT) {
+      const int k = idx / (kCU / 4), q = idx - k * (kCU / 4);
+      const int gate = q / (kU / 4), j = j0 + 4 * (q - gate * (kU / 4));
+      float* dst = Ws + (size_t)k * kCU + 4 * q;
+      if (j < C.H) {
+        const int64_t row = goff[gate] + j;
+        cp_async16(dst, k < C.K_in ? C.Wx + row + (int64_t)k * C.gw : C.Wh + row + (int64_t)(k - C.K_in) * C.gw);
+      } else {
+        *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    if (tid < kCU) {
+      const int gate = tid / kU, j = j0 + (tid - gate * kU);
+      bias[tid] = j < C.H ? C.bias[goff[gate] + j] : 0.f;
+    }
+    if (tid < kRnnSlots) sp[0].p[tid] = C.val[tid];
+    if (tid == kRnnSlots) sp[0].b1 = C.b1[0];
+    // h_{-1} (external state) into h buffer 1
+    {
+      const int fl = C.b1[0];
+      const float* Hp = C.val[S_HP];
+      const int w4 = C.H >> 2;
+      for (int idx = tid; idx < BS * w4; idx += kRT) {
+        const int b = idx / w4, q = idx - (idx / w4) * w4;
+        const int row = b0 + b;
+        float* dst = hS + (size_t)BS * HP + (size_t)b * HP + 4 * q;
+        if (row < C.B) cp_async16(dst, Hp + ((fl & 2) ? 0 : (int64_t)row * C.H) + 4 * q);
+        else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    if (tid == 0) {
+      done_steps = 0;
+      mbar_init_cl(&h_ready[0], C.n_u);
+      mbar_init_cl(&h_ready[1], C.n_u);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cp_async_wait_all();
+  }
+  __syncthreads();
+  cluster_sync_all();  // every peer's barriers exist before any remote arrive
+  if (a.trace && tid == 0) trace(0, 1);
+
+  int* my_flags = a.flags + C.flag0 + s * C.T;
+  if (warp == 8) {
+    // signalling warp: publish h_t to the stacked consumer chain
+    if (signals && lane == 0) signal_loop(&done_steps, my_flags, C.T, false);
+    return;
+  }
+  const int* src_flags = nullptr;
+  int src_need = 0;
+  if (C.src >= 0) {
+    const RnnChain& Pc = a.ch[C.src];
+    src_flags = a.flags + Pc.flag0 + s * Pc.T;
+    src_need = Pc.n_u;
+  }
+  constexpr int LB = BS < 4 ? BS : 4;
+  constexpr int TB = BS / LB;
+  constexpr int LC = 32 / LB;
+  constexpr int TC = kCU / LC;
+  const int lb = lane / LC, lc = lane - (lane / LC) * LC;
+  const int cb = tid / kU, cj = tid - (tid / kU) * kU;
+  const int crow = b0 + cb, cjj = j0 + cj;
+  const bool cell_mine = cb < BS && crow < C.B && cjj < C.H;
+  const bool cell_row = cb < BS;  // pushes zeros for padded rows / units too
+  float c_carry = 0.f;
+  // remote addresses of this thread's h element in every peer's two h buffers
+  const uint32_t h_local0 = smem_addr(hS + (size_t)(cb < BS ? cb : 0) * HP + cjj);
+  const uint32_t hr_local = smem_addr(&h_ready[0]);
+  float acc[TB][TC];
+  auto fma_block = [&](const float* rows, int ld, int wk0, int k_lo, int k_hi) {
+    // acc += rows[:, k_lo:k_hi] (row stride ld, column offset k - k_lo) * Ws[wk0 + k]
+    const int per = (k_hi - k_lo + 7) / 8;
+    const int kb = k_lo + warp * per, ke = min(k_hi, kb + per);
+#pragma unroll 4
+    for (int k = kb; k < ke; ++k) {
+      float xa[TB], wv[TC];
+#pragma unroll
+      for (int i = 0; i < TB; ++i) xa[i] = rows[(size_t)(i * LB + lb) * ld + k];
+#pragma unroll
+      for (int c = 0; c < TC; ++c) wv[c] = Ws[(size_t)(wk0 + k) * kCU + lane_col<LC, TC>(lc, c)];
+#pragma unroll
+      for (int i = 0; i < TB; ++i)
+#pragma unroll
+        for (int c = 0; c < TC; ++c) acc[i][c] = fmaf(xa[i], wv[c], acc[i][c]);
+    }
+  };
+
+  for (int t = 0; t < C.T; ++t) {
+    const StepPtrs& P = sp[t & 1];
+    const float* nxt = nullptr;
+    int nxt_b1 = 0;
+    if (warp == 1 && t + 1 < C.T) {
+      if (lane < kRnnSlots) nxt = C.val[(size_t)(t + 1) * kRnnSlots + lane];
+      if (lane == kRnnSlots) nxt_b1 = C.b1[t + 1];
+    }
+    const int fl = P.b1;
+    if (t == 0 && cell_mine) c_carry = __ldcg(P.p[S_CP] + ((fl & 4) ? cjj : (int64_t)crow * C.H + cjj));
+    // gx mode: the G slot already holds b + Wx x_t (batched tensor-core GEMM
+    // before this launch); read it ahead of the waits
+    float gx[4] = {0.f, 0.f, 0.f, 0.f};
+    if (a.gx && cell_mine) {
+      const float* Gr = P.p[S_G] + (int64_t)crow * C.gw;
+      gx[0] = Gr[C.off_i + cjj];
+      gx[1] = Gr[C.off_f + cjj];
+      gx[2] = Gr[C.off_o + cjj];
+      gx[3] = Gr[C.off_g + cjj];
+    }
+#pragma unroll
+    for (int i = 0; i < TB; ++i)
+#pragma unroll
+      for (int c = 0; c < TC; ++c) acc[i][c] = 0.f;
+    // input part (x_t): external or the producer chain's step t (gx mode: none)
+    if (C.K_in > 0) {
+    if (tid == 0 && src_flags) wait_count(src_flags + t, src_need);
+    csync();
+    {
+      const float* X = P.p[S_X];
+      const int w4 = C.K_in >> 2;
+      for (int idx = tid; idx < BS * w4; idx += kRT) {
+        const int b = idx / w4, q = idx - (idx / w4) * w4;
+        const int row = b0 + b;
+        float* dst = xS + (size_t)b * XP + 4 * q;
+        if (row < C.B) cp_async16(dst, X + ((fl & 1) ? 0 : (int64_t)row * C.K_in) + 4 * q);
+        else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      cp_async_wait_all();
+    }
+    csync();
+    fma_block(xS, XP, 0, 0, C.K_in);
+    }
+    // recurrent part: h_{t-1} pushed by every CTA of the cluster
+    if (t > 0) mbar_wait_cl(&h_ready[(t - 1) & 1], ((t - 1) >> 1) & 1);
+    fma_block(hS + (size_t)((t - 1) & 1) * BS * HP, HP, C.K_in, 0, C.H);
+#pragma unroll
+    for (int i = 0; i < TB; ++i)
+#pragma unroll
+      for (int c = 0; c < TC; ++c) part[(warp * BS + i * LB + lb) * kCU + lane_col<LC, TC>(lc, c)] = acc[i][c];
+    csync();
+    float x4[4] = {0.f, 0.f, 0.f, 0.f}, ai = 0.f, af = 0.f, ao = 0.f, ag = 0.f, ig = 0.f, p = 0.f, c = 0.f, tc = 0.f;
+    float h = 0.f;
+    const int64_t r = (int64_t)crow * C.H + cjj;
+    if (cell_mine) {
+#pragma unroll
+      for (int gate = 0; gate < 4; ++gate) {
+        float sum = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) sum += part[(w * BS + cb) * kCU + gate * kU + cj];
+        x4[gate] = (a.gx ? gx[gate] : bias[gate * kU + cj]) + sum;
+      }
+      ai = sigmoid_ref(x4[0]);
+      af = sigmoid_ref(x4[1]);
+      ao = sigmoid_ref(x4[2]);
+      ag = tanhf(x4[3]);
+      ig = ai * ag;
+      p = af * c_carry;
+      c = ig + p;
+      c_carry = c;
+      tc = tanhf(c);
+      h = ao * tc;
+    }
+    if (t + 1 < C.T) {
+      // push h_t into buffer t&1 of every CTA of the cluster (padded lanes push zeros)
+      if (cell_row && cjj < C.H) {
+        const uint32_t la = h_local0 + (uint32_t)((t & 1) * BS * HP * 4);
+        for (int q = 0; q < C.n_u; ++q) st_cluster(mapa(la, q), h);
+      }
+      if (warp == 1) {
+        if (lane < kRnnSlots) sp[(t + 1) & 1].p[lane] = nxt;
+        if (lane == kRnnSlots) sp[(t + 1) & 1].b1 = nxt_b1;
+      }
+      csync();
+      if (tid < C.n_u) mbar_arrive_remote(mapa(hr_local + 8 * (t & 1), tid));
+    }
+    if (a.trace && tid == 0) trace(0, 2 + t);
+    if (cell_mine) {
+      const_cast<float*>(P.p[S_H])[r] = h;
+      float* G = const_cast<float*>(P.p[S_G]) + (int64_t)crow * C.gw;
+      G[C.off_i + cjj] = x4[0];
+      G[C.off_f + cjj] = x4[1];
+      G[C.off_o + cjj] = x4[2];
+      G[C.off_g + cjj] = x4[3];
+      auto W = [&](int slot, float v) { const_cast<float*>(P.p[slot])[r] = v; };
+      W(S_PI, x4[0]);
+      W(S_PF, x4[1]);
+      W(S_PO, x4[2]);
+      W(S_PG, x4[3]);
+      W(S_AI, ai);
+      W(S_AF, af);
+      W(S_AO, ao);
+      W(S_AG, ag);
+      W(S_IG, ig);
+      W(S_FC, p);
+      W(S_C, c);
+      W(S_TC, tc);
+    }
+    if (signals) {
+      csync();
+      if (tid == 0) st_release_cta(&done_steps, t + 1);
+    }
+  }
+}
+
+template <int BS>
+__global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_constant__ RnnArgs a) {
+  extern __shared__ float4 smem4[];
+  float* sm = reinterpret_cast<float*>(smem4);
+  __shared__ StepPtrs2 sp[2];
+  __shared__ __align__(8) uint64_t rec_ready[2];
+  __shared__ int done_steps;
+  const int ci = chain_of(a, blockIdx.x);
+  const RnnChain C = a.ch[ci];  // register copy (dynamic-index constant loads are slow)
+  const int local = blockIdx.x - C.cta0;
+  const int s = local / C.n_u, ub = local - (local / C.n_u) * C.n_u;
+  const int b0 = s * BS, j0 = ub * kU;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const RnnChain* Cc = C.cons >= 0 ? &a.ch[C.cons] : nullptr;
+  const int gw_c = Cc ? Cc->gw : 0;
+  const int HU = C.n_u * kU;                    // units covered by the cluster (>= H)
+  const int goff[4] = {C.off_i, C.off_f, C.off_o, C.off_g};
+  float* WhS = sm;                              // [64 own gate rows][HU units]
+  float* WcT = WhS + (size_t)kCU * HU;          // [gw_c][16]
+  float* dGs = WcT + (size_t)gw_c * kU;         // [BS][CJ+4] (consumer dG staging)
+  float* part = dGs + (size_t)(a.cj + 4) * BS;  // [8][BS][16]
+  float* dGl = part + 8 * BS * kU;              // [BS][64+4] own gate gradients
+  float* recv = dGl + (size_t)BS * (kCU + 4);   // [2][n_u][BS][16] reduce-scatter slots
+  const bool signals = C.src >= 0;              // the producer chain reads dG_t from global memory
+  if (a.trace && tid == 0) trace(1, 0);
+
+  if (warp < 8) {
+    // WhS[r][u] = Wh[goff[gate] + j0 + jj, u] = Wh[row + u * gw]  (r = gate * 16 + jj)
+    for (int idx = tid; idx < kCU * HU; idx += kRT) {
+      const int u = idx / kCU, rr = idx - u * kCU;
+      const int gate = rr / kU, j = j0 + (rr - gate * kU);
+      float* dst = WhS + (size_t)rr * HU + u;
+      if (j < C.H && u < C.H) cp_async4(dst, C.Wh + goff[gate] + j + (int64_t)u * C.gw);
+      else *dst = 0.f;
+    }
+    if (Cc) {
+      for (int idx = tid; idx < gw_c * kU; idx += kRT) {
+        const int u = idx / gw_c, j = idx - (idx / gw_c) * gw_c;
+        float* dst = WcT + (size_t)j * kU + u;
+        if (j0 + u < C.H) cp_async4(dst, Cc->Wx + j + (int64_t)(j0 + u) * gw_c);
+        else *dst = 0.f;
+      }
+    }
+    {
+      const int t = C.T - 1;
+      if (tid < kRnnSlots) sp[t & 1].v[tid] = C.val[(size_t)t * kRnnSlots + tid];
+      if (tid >= 32 && tid < 32 + kRnnSlots) sp[t & 1].d[tid - 32] = C.grad[(size_t)t * kRnnSlots + tid - 32];
+      if (tid == 64) sp[t & 1].b1 = C.b1[t];
+    }
+    if (tid == 0) {
+      done_steps = 0;
+      mbar_init_cl(&rec_ready[0], C.n_u);
+      mbar_init_cl(&rec_ready[1], C.n_u);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cp_async_wait_all();
+  }
+  __syncthreads();
+  cluster_sync_all();
+  if (a.trace && tid == 0) trace(1, 1);
+
+  int* my_flags = a.flags + C.flag0 + s * C.T;
+  if (warp == 8) {
+    if (signals && lane == 0) signal_loop(&done_steps, my_flags, C.T, true);
+    return;
+  }
+  const int* cons_flags = Cc ? a.flags + Cc->flag0 + s * Cc->T : nullptr;
+  const int cb = tid / kU, cj = tid - (tid / kU) * kU;
+  const int row = b0 + cb, j = j0 + cj;
+  const bool mine = cb < BS && row < C.B && j < C.H;
+  const int64_t r = (int64_t)row * C.H + j;
+  const uint32_t my_rank = cluster_rank();
+  const uint32_t recv_local = smem_addr(recv);
+  const uint32_t rr_local = smem_addr(&rec_ready[0]);
+  float rec = 0.f, cons = 0.f, dc_carry = 0.f;
+  float ao = 0.f, ai = 0.f, ag = 0.f, tc = 0.f, af = 0.f, ck = 0.f, gh_ext = 0.f, gc_ext = 0.f;
+  auto load_cell = [&](const StepPtrs2& P) {
+    if (!mine) return;
+    const bool cb1 = (P.b1 & 4) != 0;
+    ao = P.v[S_AO][r];
+    ai = P.v[S_AI][r];
+    ag = P.v[S_AG][r];
+    tc = P.v[S_TC][r];
+    af = P.v[S_AF][r];
+    ck = P.v[S_CP][cb1 ? j : r];
+    gh_ext = P.d[S_H][r];
+    gc_ext = P.d[S_C][r];
+  };
+  load_cell(sp[(C.T - 1) & 1]);
+  if (Cc) {
+    if (tid == 0) wait_count(cons_flags + C.T - 1, Cc->n_u);
+    csync();
+    cons = rows_times_wt<BS>(Cc->grad[(size_t)(C.T - 1) * kRnnSlots + S_G], gw_c, C.B, b0, WcT, dGs, a.cj, part,
+                             a.vec);
+  }
+  // reduce-scatter tiling: thread (rg, ug) -> rows 4rg..4rg+3 (of BS), units 4ug..4ug+3 (of HU)
+  constexpr int RG = BS < 4 ? 1 : BS / 4;       // row groups
+  constexpr int RPT = BS < 4 ? BS : 4;           // rows per thread
+  const int UG = HU / 4;                          // unit groups (<= 64)
+  const int rg = tid / UG, ug = tid - (tid / UG) * UG;
+  const bool rs_active = rg < RG;
+
+  for (int t = C.T - 1, it = 0; t >= 0; --t, ++it) {
+    const StepPtrs2& P = sp[t & 1];
+    const float* nv = nullptr;
+    float* nd = nullptr;
+    int nb1 = 0;
+    if (warp == 1 && t > 0) {
+      if (lane < kRnnSlots) {
+        nv = C.val[(size_t)(t - 1) * kRnnSlots + lane];
+        nd = C.grad[(size_t)(t - 1) * kRnnSlots + lane];
+      }
+      if (lane == kRnnSlots) nb1 = C.b1[t - 1];
+    }
+    const bool cb1 = (P.b1 & 4) != 0;
+    float gh = 0.f, d_tc = 0.f, d_o = 0.f, dc = 0.f, d_i = 0.f, d_g = 0.f, dpi = 0.f, dpo = 0.f, dpg = 0.f;
+    float d_f = 0.f, dpf = 0.f;
+    if (mine) {
+      gh = gh_ext + rec + cons;
+      d_tc = gh * ao;
+      d_o = gh * tc;
+      dc = (gc_ext + dc_carry) + (1.f - tc * tc) * d_tc;
+      d_i = dc * ag;
+      d_g = dc * ai;
+      dpi = ai * (1.f - ai) * d_i;
+      dpo = ao * (1.f - ao) * d_o;
+      dpg = (1.f - ag * ag) * d_g;
+      d_f = dc * ck;
+      dpf = af * (1.f - af) * d_f;
+      dc_carry = dc * af;
+    }
+    if (t > 0) {
+      // own gate gradients (zero for padded rows / units) as the local operand
+      if (cb < BS) {
+        float* dl = dGl + (size_t)cb * (kCU + 4);
+        dl[0 * kU + cj] = dpi;
+        dl[1 * kU + cj] = dpf;
+        dl[2 * kU + cj] = dpo;
+        dl[3 * kU + cj] = dpg;
+      }
+      csync();
+      // partial dh_{t-1}[rows, all units] from this CTA's 64 gate columns
+      if (rs_active) {
+        float acc4[RPT][4];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) acc4[i][0] = acc4[i][1] = acc4[i][2] = acc4[i][3] = 0.f;
+#pragma unroll 4
+        for (int k = 0; k < kCU; ++k) {
+          const float4 w = *reinterpret_cast<const float4*>(WhS + (size_t)k * HU + 4 * ug);
+#pragma unroll
+          for (int i = 0; i < RPT; ++i) {
+            const float g = dGl[(size_t)(rg * RPT + i) * (kCU + 4) + k];
+            acc4[i][0] = fmaf(g, w.x, acc4[i][0]);
+            acc4[i][1] = fmaf(g, w.y, acc4[i][1]);
+            acc4[i][2] = fmaf(g, w.z, acc4[i][2]);
+            acc4[i][3] = fmaf(g, w.w, acc4[i][3]);
+          }
+        }
+        // push into slot [my_rank] of the unit owner's buffer it&1
+        const int owner = (4 * ug) / kU, uo = (4 * ug) % kU;
+        const uint32_t base = recv_local + 4u * (uint32_t)(((it & 1) * C.n_u + (int)my_rank) * BS * kU);
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          const uint32_t la = base + 4u * (uint32_t)((rg * RPT + i) * kU + uo);
+          st_cluster4(mapa(la, owner), make_float4(acc4[i][0], acc4[i][1], acc4[i][2], acc4[i][3]));
+        }
+      }
+      if (warp == 1) {
+        if (lane < kRnnSlots) {
+          sp[(t - 1) & 1].v[lane] = nv;
+          sp[(t - 1) & 1].d[lane] = nd;
+        }
+        if (lane == kRnnSlots) sp[(t - 1) & 1].b1 = nb1;
+      }
+      csync();
+      if (tid < C.n_u) mbar_arrive_remote(mapa(rr_local + 8 * (it & 1), tid));
+    }
+    if (a.trace && tid == 0) trace(1, 2 + t);
+    if (mine) {
+      float* const* D = P.d;
+      float* dG = D[S_G] + (int64_t)row * C.gw;
+      dG[C.off_i + j] = dpi;
+      dG[C.off_o + j] = dpo;
+      dG[C.off_g + j] = dpg;
+      dG[C.off_f + j] = dpf;
+      D[S_H][r] = gh;
+      D[S_TC][r] = d_tc;
+      D[S_AO][r] = d_o;
+      D[S_C][r] = dc;
+      D[S_IG][r] = dc;
+      D[S_AI][r] = d_i;
+      D[S_AG][r] = d_g;
+      D[S_PI][r] = dpi;
+      D[S_PO][r] = dpo;
+      D[S_PG][r] = dpg;
+      D[S_FC][r] = dc;
+      D[S_AF][r] = d_f;
+      D[S_PF][r] = dpf;
+      if (t == 0 && !cb1) D[S_CP][r] += dc_carry;
+    }
+    if (signals) {
+      csync();
+      if (tid == 0) st_release_cta(&done_steps, it + 1);
+    }
+    if (t > 0) {
+      load_cell(sp[(t - 1) & 1]);
+      if (Cc) {
+        if (tid == 0) wait_count(cons_flags + t - 1, Cc->n_u);
+        csync();
+        cons = rows_times_wt<BS>(Cc->grad[(size_t)(t - 1) * kRnnSlots + S_G], gw_c, C.B, b0, WcT, dGs, a.cj, part,
+                                 a.vec);
+      }
+      mbar_wait_cl(&rec_ready[it & 1], (it >> 1) & 1);
+      rec = 0.f;
+      if (cb < BS) {
+        const float* slot = recv + (size_t)(it & 1) * C.n_u * BS * kU + (size_t)cb * kU + cj;
+        for (int q = 0; q < C.n_u; ++q) rec += slot[(size_t)q * BS * kU];
+      }
     }
   }
 }
@@ -568,7 +1173,51 @@ int launch_bwd_bs(const RnnArgs& a, size_t smem, cudaStream_t s) {
   return 1;
 }
 
+template <int BS>
+int launch_cl_bs(const RnnArgs& a, bool bwd, size_t smem, int cluster, cudaStream_t s) {
+  void (*k)(const RnnArgs) = bwd ? rnn_bwd_cl_kernel<BS> : rnn_fwd_cl_kernel<BS>;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
+  if (cluster > 8 && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+    return -1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.ctas);
+  cfg.blockDim = dim3(kClThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  // every cluster must be resident at once (stacked chains wait on each other)
+  int active = 0;
+  const cudaError_t oe = cudaOccupancyMaxActiveClusters(&active, k, &cfg);
+  if (rnn_trace_enabled())
+    fprintf(stderr, "[rnn] %s cluster %d smem %zu ctas %d: max active clusters %d (%s)\n", bwd ? "bwd" : "fwd",
+            cluster, smem, a.ctas, active, cudaGetErrorString(oe));
+  if (oe != cudaSuccess || active * cluster < a.ctas) {
+    cudaGetLastError();
+    return -2;
+  }
+  if (cudaLaunchKernelEx(&cfg, k, a) != cudaSuccess) return -1;
+  return 1;
+}
+
 }  // namespace
+
+size_t rnn_fwd_cl_smem(int K_in, int H, int bs) {
+  const int K = K_in + H;
+  return 4 * ((size_t)K * kCU + (size_t)bs * (K_in + 4) + 2 * (size_t)bs * (H + 4) + 8 * (size_t)bs * kCU + kCU);
+}
+
+size_t rnn_bwd_cl_smem(int H, int gw_c, int bs, int cj) {
+  const int HU = (H + kU - 1) / kU * kU;
+  const int nu = HU / kU;
+  return 4 * ((size_t)kCU * HU + (size_t)gw_c * kU + (size_t)(cj + 4) * bs + 8 * (size_t)bs * kU +
+              (size_t)bs * (kCU + 4) + 2 * (size_t)nu * bs * kU);
+}
 
 int rnn_rows_per_cta(int B) { return B >= 16 ? 16 : B >= 8 ? 8 : B >= 4 ? 4 : B >= 2 ? 2 : 1; }
 
@@ -580,9 +1229,25 @@ size_t rnn_bwd_smem(int gw, int gw_c, int bs, int cj) {
   return 4 * ((size_t)gw * kU + (size_t)gw_c * kU + (size_t)(cj + 4) * bs + 8 * (size_t)bs * kU);
 }
 
+bool rnn_cluster_enabled() {
+  const char* e = std::getenv("DG_RNN_CLUSTER");
+  return !(e && e[0] == '0');
+}
+
 bool rnn_enabled() {
   const char* e = std::getenv("DG_RNN");
   return !(e && e[0] == '0');
+}
+
+int launch_rnn_cluster(const RnnArgs& a, bool backward, size_t smem, int cluster, cudaStream_t s) {
+  if (cudaMemsetAsync(a.flags, 0, (size_t)a.n_flags * sizeof(int), s) != cudaSuccess) return -1;
+  switch (a.bs) {
+    case 16: return launch_cl_bs<16>(a, backward, smem, cluster, s);
+    case 8: return launch_cl_bs<8>(a, backward, smem, cluster, s);
+    case 4: return launch_cl_bs<4>(a, backward, smem, cluster, s);
+    case 2: return launch_cl_bs<2>(a, backward, smem, cluster, s);
+    default: return launch_cl_bs<1>(a, backward, smem, cluster, s);
+  }
 }
 
 int launch_rnn(const RnnArgs& a, bool backward, size_t smem, cudaStream_t s) {
@@ -596,6 +1261,17 @@ int launch_rnn(const RnnArgs& a, bool backward, size_t smem, cudaStream_t s) {
     default: n = backward ? launch_bwd_bs<1>(a, smem, s) : launch_fwd_bs<1>(a, smem, s); break;
   }
   return n;
+}
+
+int rnn_trace_read(unsigned long long* host, size_t n) {
+  const size_t bytes = sizeof(unsigned long long) * 2 * kSmCountTrace * kTraceSlots;
+  if (n * sizeof(unsigned long long) < bytes) return -1;
+  return cudaMemcpyFromSymbol(host, g_rnn_trace, bytes) == cudaSuccess ? 0 : -1;
+}
+
+bool rnn_trace_enabled() {
+  const char* e = std::getenv("DG_RNN_TRACE");
+  return e && e[0] == '1';
 }
 
 int launch_rnn_c0(const RnnC0& a, cudaStream_t s) {

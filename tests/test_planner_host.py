@@ -93,16 +93,16 @@ def _rnn_stats(cg, model):
     return dict(zip(["stacks", "chains", "steps", "ctas"], out.tolist()))
 
 
-def test_rnnlm_recurrence_is_one_persistent_stack():
+def test_rnnlm_recurrence_is_one_persistent_chain_per_layer():
     cg, m = _ctx()
     task = W.RNNLM(dy, m, 10_000, 128, 256, 2)
     batch = W.ptb_corpus(1, 64)
     task.loss(cg, batch)
     steps = max(len(s) for s in batch) - 1
     r = _rnn_stats(cg, m)
-    # both layers' chains stacked (x^1_t = h^0_t): one launch per direction,
-    # 64 rows / 16 per CTA x 256 units / 16 per CTA = 64 CTAs per layer
-    assert r == {"stacks": 1, "chains": 2, "steps": 2 * steps, "ctas": 128}
+    # one persistent chain per layer (input projections are batched GEMMs
+    # between them): 64 rows / 16 per CTA x 256 units / 16 per CTA = 64 CTAs each
+    assert r == {"stacks": 2, "chains": 2, "steps": 2 * steps, "ctas": 128}
 
 
 def test_tiny_lm_single_chain():

@@ -1,0 +1,41 @@
+"""Timeline of the persistent LSTM kernels (DG_RNN_TRACE=1): per-step arrival
+stamps of every CTA for one PTB MB=64 training step.  Diagnostic only."""
+import os
+import sys
+
+os.environ["DG_RNN_TRACE"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1701_03980_b200 as dy  # noqa: E402
+from paper_1701_03980_b200 import _native  # noqa: E402
+
+cfg = bench.CONFIGS["ptb64"]
+data, units, _ = bench.make_data(cfg, 4, 0, 1)
+pools = dy.new_poolset(1024, 1024, 64)
+cg, model = dy.ComputationGraph(pools), dy.Model(pools, seed=1)
+task = bench.make_task(dy, model, cfg)
+tr = dy.Trainer(model, "adam")
+for d in data:
+    cg.renew()
+    loss = task.loss(cg, d)
+    cg.backward(loss)
+    tr.update()
+torch.cuda.synchronize()
+T = max(len(s) for s in data[-1]) - 1
+buf = np.zeros(2 * 148 * 256, np.uint64)
+_native.check(_native.lib().dg_rnn_trace(buf.ctypes.data, buf.size))
+buf = buf.reshape(2, 148, 256).astype(np.int64)
+for kind, name in ((0, "fwd"), (1, "bwd")):
+    b = buf[kind]
+    live = b[:, 0] > 0
+    b = b[live]
+    t0 = b[:, 0].min()
+    arr = b[:, 2:2 + T] - t0
+    order = arr[:, -1] if kind == 0 else arr[:, 0]
+    steps = np.abs(np.diff(arr.max(axis=0)))
+    print(f"== {name} (last launch, {live.sum()} CTAs): weights resident {(b[:, 1] - b[:, 0]).mean() / 1e3:.1f} us, "
+          f"per-step {np.median(steps) / 1e3:.2f} us (min {steps.min() / 1e3:.2f}, max {steps.max() / 1e3:.2f}), "
+          f"total {order.max() / 1e3:.1f} us, arrival skew {np.median(arr.max(axis=0) - arr.min(axis=0)) / 1e3:.2f} us")
