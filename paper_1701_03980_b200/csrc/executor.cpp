@@ -22,10 +22,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -284,13 +286,10 @@ static int upload(dg_graph* g, const Blob& blob, void* dst) {
 // ----------------------------------------------------------- signatures
 struct SigHash {
   uint64_t h = 1469598103934665603ull;
-  void add(int64_t v) {
-    uint64_t x = static_cast<uint64_t>(v);
-    for (int i = 0; i < 8; ++i) {
-      h ^= (x & 0xff);
-      h *= 1099511628211ull;
-      x >>= 8;
-    }
+  void add(int64_t v) {  // one multiply-xorshift round per value
+    h ^= static_cast<uint64_t>(v) + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    h *= 0xff51afd7ed558ccdull;
+    h ^= h >> 33;
   }
 };
 
@@ -930,6 +929,92 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
     ++level;
   }
 }
+
+// Schedules depend only on the graph's structure (kinds, wiring, shapes,
+// parameter identities, structural aux such as pick offsets) -- not on lookup
+// ids, labels or input payloads -- so they are cached by a structural hash:
+// minibatches of equal padded length reuse one schedule.
+static uint64_t structure_hash(const dg_graph* g, const std::vector<int>& active, int scope_hi) {
+  SigHash h;
+  h.add(scope_hi);
+  h.add((int64_t)active.size());
+  for (int i : active) h.add(i);
+  for (int i = 0; i <= scope_hi; ++i) {
+    const Node& n = g->nodes[i];
+    h.add(n.kind);
+    h.add(n.batch);
+    h.add(n.rank);
+    for (int d = 0; d < n.rank; ++d) h.add(n.dims[d]);
+    h.add(n.n_in);
+    for (int k = 0; k < n.n_in; ++k) h.add(i - g->inputs[n.in_off + k]);
+    switch (n.kind) {
+      case DG_OP_PARAMETER:
+      case DG_OP_LOOKUP:
+      case DG_OP_LOOKUP_BATCH:
+        h.add(g->aux_i[n.ai_off]);  // table / parameter identity (not the ids)
+        break;
+      case DG_OP_PICK_RANGE:
+        for (int64_t q = 0; q < n.ai_len; ++q) h.add(g->aux_i[n.ai_off + q]);
+        break;
+      case DG_OP_SCALAR_MUL: {
+        int32_t bits;
+        std::memcpy(&bits, &g->aux_f[n.af_off], 4);
+        h.add(bits);
+        break;
+      }
+      default:
+        break;
+    }
+  }
+  return h.h;
+}
+
+static std::shared_ptr<const Schedule> get_schedule(const dg_graph* g, const std::vector<int>& active, int scope_hi) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, std::shared_ptr<const Schedule>> cache;
+  static const bool on = [] {
+    const char* e = std::getenv("DG_SCHED_CACHE");
+    return !(e && e[0] == '0');
+  }();
+  const uint64_t key = on ? structure_hash(g, active, scope_hi) : 0;
+  if (on) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  auto S = std::make_shared<Schedule>();
+  build_schedule(g, active, scope_hi, *S);
+  if (on) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache.size() >= 256) cache.clear();
+    cache.emplace(key, S);
+  }
+  return S;
+}
+
+// host-side planning timers (DG_PLAN_TIMING=1 prints per call to stderr)
+struct PlanTimer {
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  const char* what;
+  std::string acc;
+  explicit PlanTimer(const char* w) : what(w) {
+    const char* e = std::getenv("DG_PLAN_TIMING");
+    on = e && e[0] == '1';
+    t0 = std::chrono::steady_clock::now();
+  }
+  void lap(const char* name) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    char buf[64];
+    std::snprintf(buf, sizeof buf, " %s %.0fus", name, std::chrono::duration<double, std::micro>(t - t0).count());
+    acc += buf;
+    t0 = t;
+  }
+  ~PlanTimer() {
+    if (on) std::fprintf(stderr, "[plan] %s:%s\n", what, acc.c_str());
+  }
+};
 
 // ----------------------------------------------------------------- planning
 // A plan = host-built table blob + deferred launch closures that read the
@@ -2053,11 +2138,13 @@ static int do_forward(dg_graph* g, int upto) {
     need += round64(nb);
   }
 
+  PlanTimer tm("forward");
   std::vector<int> active;
   active.reserve(upto - lo + 1);
   for (int i = lo; i <= upto; ++i) active.push_back(i);
-  Schedule S;
-  build_schedule(g, active, upto, S);
+  const std::shared_ptr<const Schedule> Sp = get_schedule(g, active, upto);
+  const Schedule& S = *Sp;
+  tm.lap("schedule");
 
   // placement: inputs first (one contiguous block filled by a single copy),
   // then lookups, then groups in execution order
@@ -2127,14 +2214,16 @@ static int do_forward(dg_graph* g, int upto) {
       plan.tag(C_GATHER, 0.0, 8.0 * rows * dim + 8.0 * rows);
     }
   }
+  tm.lap("place+inputs");
   {
     GemmBatch gb;
     for (const Group& gr : S.groups) plan_forward_group(g, S, gr, plan, gb);
     flush_gemm(g, plan, gb);
   }
-
+  tm.lap("groups");
   int rc = launch_plan(g, plan);
   if (rc) return rc;
+  tm.lap("launch");
   {
     const Node& tn = g->nodes[upto];
     g->vcache_node = -1;
@@ -2651,11 +2740,13 @@ int dg_backward(dg_graph* g, int32_t loss) {
     const Node& x = g->nodes[i];
     for (int k = 0; k < x.n_in; ++k) anc[g->inputs[x.in_off + k]] = 1;
   }
+  PlanTimer tm("backward");
   std::vector<int> active;
   for (int i = 0; i <= loss; ++i)
     if (anc[i]) active.push_back(i);
-  Schedule S;
-  build_schedule(g, active, loss, S);
+  const std::shared_ptr<const Schedule> Sp = get_schedule(g, active, loss);
+  const Schedule& S = *Sp;
+  tm.lap("schedule");
 
   // placement of grad slots: group order for scheduled units, then the rest
   const size_t begin = g->bwd_cursor;
@@ -2694,12 +2785,14 @@ int dg_backward(dg_graph* g, int32_t loss) {
   float* dummy = dummy_base(g);
   std::unordered_map<int64_t, AffineUse> wuse;
   std::unordered_map<int64_t, std::vector<uintptr_t>> buse;
+  tm.lap("place");
   {
     GemmBatch gb;
     for (int q = (int)S.groups.size() - 1; q >= 0; --q)
       plan_backward_group(g, S, S.groups[q], plan, dummy, wuse, buse, gb);
     flush_gemm(g, plan, gb);
   }
+  tm.lap("groups");
 
   // aggregated weight gradients: dW^T (K x m) += X^T G over every use
   std::vector<int64_t> wkeys;
@@ -2793,8 +2886,10 @@ int dg_backward(dg_graph* g, int32_t loss) {
       plan.tag(C_SCATTER, 0.0, 4.0 * dim * ((double)src.size() + 2.0 * nu));
     }
   }
+  tm.lap("dW+colsum+scatter");
   rc = launch_plan(g, plan);
   if (rc) return rc;
+  tm.lap("launch");
   g->bwd_cursor = cur;
   g->bwd_alloc_count += loss + 1;
   g->has_grads = true;

@@ -41,6 +41,10 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
+#include <tuple>
+#include <utility>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -1155,10 +1159,35 @@ __global__ void rnn_c0_kernel(RnnC0 a) {
   a.dst[k][u] += s;
 }
 
+// per-kernel one-time attribute setup: the dynamic shared memory limit is
+// raised to the opt-in maximum once (cudaFuncSetAttribute is not free)
+constexpr int kSmemOptin = 227 * 1024;
+template <class K>
+bool smem_attr_once(K k, bool nonportable_cluster) {
+  static std::mutex mu;
+  static std::vector<const void*> done;
+  std::lock_guard<std::mutex> lk(mu);
+  const void* key = reinterpret_cast<const void*>(k);
+  for (const void* d : done)
+    if (d == key) return true;
+  int dev = 0, optin = kSmemOptin;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) return false;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes) !=
+      cudaSuccess)
+    return false;
+  if (nonportable_cluster && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+    return false;
+  done.push_back(key);
+  return true;
+}
+
 template <int BS>
 int launch_fwd_bs(const RnnArgs& a, size_t smem, cudaStream_t s) {
   auto k = rnn_fwd_kernel<BS>;
-  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
+  if (!smem_attr_once(k, false)) return -1;
   void* args[] = {const_cast<RnnArgs*>(&a)};
   if (cudaLaunchCooperativeKernel((const void*)k, dim3(a.ctas), dim3(kRT), args, smem, s) != cudaSuccess) return -1;
   return 1;
@@ -1167,7 +1196,7 @@ int launch_fwd_bs(const RnnArgs& a, size_t smem, cudaStream_t s) {
 template <int BS>
 int launch_bwd_bs(const RnnArgs& a, size_t smem, cudaStream_t s) {
   auto k = rnn_bwd_kernel<BS>;
-  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
+  if (!smem_attr_once(k, false)) return -1;
   void* args[] = {const_cast<RnnArgs*>(&a)};
   if (cudaLaunchCooperativeKernel((const void*)k, dim3(a.ctas), dim3(kRT), args, smem, s) != cudaSuccess) return -1;
   return 1;
@@ -1176,9 +1205,7 @@ int launch_bwd_bs(const RnnArgs& a, size_t smem, cudaStream_t s) {
 template <int BS>
 int launch_cl_bs(const RnnArgs& a, bool bwd, size_t smem, int cluster, cudaStream_t s) {
   void (*k)(const RnnArgs) = bwd ? rnn_bwd_cl_kernel<BS> : rnn_fwd_cl_kernel<BS>;
-  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
-  if (cluster > 8 && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
-    return -1;
+  if (!smem_attr_once(k, true)) return -1;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(a.ctas);
   cfg.blockDim = dim3(kClThreads);
@@ -1191,9 +1218,28 @@ int launch_cl_bs(const RnnArgs& a, bool bwd, size_t smem, int cluster, cudaStrea
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  // every cluster must be resident at once (stacked chains wait on each other)
+  // every cluster must be resident at once (stacked chains wait on each other);
+  // the occupancy answer is cached per (kernel, cluster size, smem bucket)
   int active = 0;
-  const cudaError_t oe = cudaOccupancyMaxActiveClusters(&active, k, &cfg);
+  cudaError_t oe = cudaSuccess;
+  {
+    static std::mutex mu;
+    static std::vector<std::pair<std::tuple<const void*, int, size_t>, int>> memo;
+    const auto key = std::make_tuple(reinterpret_cast<const void*>(k), cluster, (smem + 4095) / 4096);
+    std::lock_guard<std::mutex> lk(mu);
+    bool hit = false;
+    for (auto& m : memo)
+      if (m.first == key) {
+        active = m.second;
+        hit = true;
+      }
+    if (!hit) {
+      cudaLaunchConfig_t q = cfg;
+      q.dynamicSmemBytes = ((smem + 4095) / 4096) * 4096;
+      oe = cudaOccupancyMaxActiveClusters(&active, k, &q);
+      if (oe == cudaSuccess) memo.push_back({key, active});
+    }
+  }
   if (rnn_trace_enabled())
     fprintf(stderr, "[rnn] %s cluster %d smem %zu ctas %d: max active clusters %d (%s)\n", bwd ? "bwd" : "fwd",
             cluster, smem, a.ctas, active, cudaGetErrorString(oe));
