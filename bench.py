@@ -204,23 +204,50 @@ def run_reference(args, cfg):
 # ---------------------------------------------------------------------------
 
 
-def run_b200(args, cfg):
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+def _roofline(name, d, peaks):
+    """achieved = algorithmic FLOPs (or bytes) per launch / mean launch time."""
+    avg_ms = d["ms"] / max(1, d["launches"])
+    if avg_ms <= 0:
+        return None
+    if d["flops"] > 0:
+        achieved = d["flops"] / max(1, d["launches"]) / (avg_ms * 1e-3) / 1e12
+        peak = peaks.get("bf16_tflops", 1590.0)
+        r = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+             "traffic": None, "kernel": name,
+             "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if "bf16_tflops" in peaks
+             else "fallback 1.59 PFLOP/s bf16 (B200_PROFILING.md)",
+             # fp32 parity: tensor-core classes issue 3 TF32 MMAs per product
+             # (dense TF32 = 1/2 of bf16); the recurrence runs on the FP32 pipe
+             "tf32x3_issued_frac": 3 * achieved / (peak / 2),
+             "fp32_simt_frac": achieved / (148 * 128 * 2 * 1.965e-3)}
+    else:
+        achieved = d["bytes"] / max(1, d["launches"]) / (avg_ms * 1e-3) / 1e9
+        peak = peaks.get("hbm_gbs", 6650.0)
+        r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+             "traffic": None, "kernel": name,
+             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks
+             else "fallback 6.65 TB/s (B200_PROFILING.md)"}
+    r["ms_per_launch"] = avg_ms
+    return r
+
+
+def measure(dy, cfg, K, Wm, world, rank, local, profile, seed=1):
+    """One configuration: e2e through the public API, device-timed value over
+    pre-built graphs, optional per-class profile pass."""
     import torch
     import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    import paper_1701_03980_b200 as dy
-    from paper_1701_03980_b200 import _native
     from paper_1701_03980_b200.parallel import DataParallel
 
-    K, Wm = args.steps, args.warmup
-    data, units, tg = make_data(cfg, K + Wm + K, rank, world)
+    data, units, tg = make_data(cfg, K + Wm + K, rank, world, seed)
     mb_pool = 1024 if cfg["kind"] == "rnnlm" and cfg["mb"] >= 16 else 128
     pools = dy.new_poolset(mb_pool, mb_pool, 64)
     cg = dy.ComputationGraph(pools)
@@ -313,6 +340,14 @@ def run_b200(args, cfg):
     launches = sum(int(g._counters()[5]) for g, _ in graphs) - launches0
     launches += K * (1 + len(model.lookups))  # trainer: dense multi-tensor + one per touched table
     value_units = sumr(sum(units[Wm + K : Wm + 2 * K]))
+    res = {
+        "value": value_units / (dev_ms * 1e-3), "unit": unit_of(cfg), "ms_per_step": dev_ms / K,
+        "e2e": {"value": e2e_units / (e2e_ms * 1e-3), "unit": unit_of(cfg), "h2d_bytes_per_step": h2d_per_step,
+                "d2h_bytes_per_step": d2h_per_step, "ms_per_step": e2e_ms / K, "wall_s": wall},
+        "gpu_launches": launches, "clocks": clk.summary(),
+    }
+    if not profile:
+        return res
 
     # ---- per-class device time (a separate pass: CUDA events around every
     # launch cost host time that must not be inside the value region) ------
@@ -330,8 +365,6 @@ def run_b200(args, cfg):
         dp.sync()
         trainer.update()
     barrier()
-
-    # per-class device time of the timed region
     kinds = {}
     for c in prof_classes:
         tot = {"ms": 0.0, "launches": 0, "flops": 0.0, "bytes": 0.0}
@@ -340,29 +373,47 @@ def run_b200(args, cfg):
             for k2 in tot:
                 tot[k2] += r[k2]
         kinds[c] = tot
+    peaks = _peaks()
     dom = max(kinds, key=lambda c: kinds[c]["ms"])
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            peaks = json.load(fh)
-    except OSError:
-        pass
-    d = kinds[dom]
-    avg_ms = d["ms"] / max(1, d["launches"])
-    if d["flops"] > 0:
-        achieved = d["flops"] / max(1, d["launches"]) / (avg_ms * 1e-3) / 1e12
-        peak = peaks.get("bf16_tflops", 1590.0)
-        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": None, "kernel": dom, "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"
-                if "bf16_tflops" in peaks else "fallback 1.59 PFLOP/s (B200_PROFILING.md)",
-                "fp32_simt_frac": achieved / (148 * 128 * 2 * 1.965e-3)}
-    else:
-        achieved = d["bytes"] / max(1, d["launches"]) / (avg_ms * 1e-3) / 1e9
-        peak = peaks.get("hbm_gbs", 6650.0)
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": dom, "peak_source": "MEASURED_PEAKS.json hbm_gbs"
-                if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"}
-    share = {c: round(kinds[c]["ms"] / max(1e-9, sum(v["ms"] for v in kinds.values())), 4) for c in kinds}
+    res["roofline"] = _roofline(dom, kinds[dom], peaks)
+    res["rooflines"] = {c: _roofline(c, kinds[c], peaks) for c in kinds if kinds[c]["ms"] > 0}
+    res["kernel_share"] = {c: round(kinds[c]["ms"] / max(1e-9, sum(v["ms"] for v in kinds.values())), 4)
+                           for c in kinds}
+    res["kernels"] = kinds
+    return res
+
+
+def run_b200(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1701_03980_b200 as dy
+
+    K, Wm = args.steps, args.warmup
+    res = measure(dy, cfg, K, Wm, world, rank, local, profile=True)
+    # the other BASELINE configs (same contract, shorter runs) beside the headline
+    others = {}
+    if world == 1 and not args.only:
+        for name in ("ptb16", "tree", "tagger", "tiny"):
+            if name == args.config:
+                continue
+            c2 = CONFIGS[name]
+            k2 = max(K, 20) if c2["kind"] != "rnnlm" or c2["mb"] == 1 else K
+            r2 = measure(dy, c2, k2, max(Wm, 3), world, rank, local, profile=False)
+            if not args.no_cpu:
+                v, s2, u, dt = cpu_throughput(c2, args.other_cpu_budget)
+                r2["cpu_baseline"] = {"value": v, "unit": unit_of(c2), "cores": os.cpu_count(), "kind": "port",
+                                      "sample": f"{s2} graphs ({u} units) through the numpy oracle in {dt:.1f} s"}
+            r2["config"] = {"workload": name, **c2}
+            r2["steps"], r2["warmup"] = k2, max(Wm, 3)
+            others[name] = r2
 
     if rank == 0:
         cpu = None
@@ -372,12 +423,12 @@ def run_b200(args, cfg):
                    "sample": f"{s} minibatches ({u} units) of {args.config} through the numpy oracle in {dt:.1f} s"}
         line = {
             "metric": METRIC,
-            "value": value_units / (dev_ms * 1e-3),
+            "value": res["value"],
             "unit": unit_of(cfg),
             "n_gpus": world,
             "steps": K,
             "warmup": Wm,
-            "ms_per_step": dev_ms / K,
+            "ms_per_step": res["ms_per_step"],
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
@@ -385,14 +436,15 @@ def run_b200(args, cfg):
             "data": "synthetic",
             "config": {"workload": args.config, **cfg, "global_batch": cfg["mb"] * world,
                        "parallelism": f"dp{world}", "l2": "flushed between timed steps (256 MiB write)"},
-            "e2e": {"value": e2e_units / (e2e_ms * 1e-3), "unit": unit_of(cfg), "h2d_bytes_per_step": h2d_per_step,
-                    "d2h_bytes_per_step": d2h_per_step, "ms_per_step": e2e_ms / K, "wall_s": wall},
-            "gpu_launches": launches,
-            "roofline": roof,
-            "kernel_share": share,
-            "kernels": kinds,
-            "clocks": clk.summary(),
+            "e2e": res["e2e"],
+            "gpu_launches": res["gpu_launches"],
+            "roofline": res["roofline"],
+            "rooflines": res["rooflines"],
+            "kernel_share": res["kernel_share"],
+            "kernels": res["kernels"],
+            "clocks": res["clocks"],
             "cpu_baseline": cpu,
+            "other_configs": others,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -410,6 +462,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-budget", type=float, default=30.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--only", action="store_true", help="headline config only (skip the other BASELINE configs)")
+    ap.add_argument("--other-cpu-budget", type=float, default=3.0)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

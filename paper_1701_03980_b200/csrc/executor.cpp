@@ -269,10 +269,22 @@ static int pinned_acquire(Pinned& p, size_t n) {
   return DG_OK;
 }
 
+// Process-wide ring of pinned staging buffers shared by every graph: a fresh
+// graph must not pay cudaHostAlloc (slow, and it synchronises the device) on
+// its first plan; a slot is reused once its previous upload has executed.
+static Pinned& staging_slot() {
+  static std::mutex mu;
+  static Pinned ring[8];
+  static int next = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  Pinned& p = ring[next];
+  next = (next + 1) % 8;
+  return p;
+}
+
 static int upload(dg_graph* g, const Blob& blob, void* dst) {
   if (blob.host.empty()) return DG_OK;
-  Pinned& p = g->pinned[g->pin_idx];
-  g->pin_idx ^= 1;
+  Pinned& p = staging_slot();
   int rc = pinned_acquire(p, blob.host.size());
   if (rc) return rc;
   std::memcpy(p.ptr, blob.host.data(), blob.host.size());

@@ -1,0 +1,38 @@
+"""Every kernel path the executor can take produces the same results: the
+full-size PTB parity test (tests/test_gpu_parity.py) re-run in a subprocess
+with each fast path switched off, so the fallbacks stay parity-green too.
+
+  DG_RNN_CLUSTER=0  persistent LSTM kernels exchanging through L2 + global
+                    arrival counters instead of cluster distributed smem
+  DG_RNN=0          no persistent recurrence: level-batched GEMM + fused cells
+  DG_TMA=0          cp.async tcgen05 GEMM instead of the TMA warp-specialised one
+  DG_TC=0           SIMT GEMMs only
+  DG_SCHED_CACHE=0  schedules rebuilt for every graph
+"""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+VARIANTS = {
+    "rnn_no_cluster": {"DG_RNN_CLUSTER": "0"},
+    "rnn_off": {"DG_RNN": "0"},
+    "tma_off": {"DG_TMA": "0"},
+    "tensor_cores_off": {"DG_TC": "0"},
+    "schedule_cache_off": {"DG_SCHED_CACHE": "0"},
+}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+def test_ptb_parity_on_every_kernel_path(variant):
+    env = dict(os.environ, **VARIANTS[variant])
+    tests = ["tests/test_gpu_parity.py::test_ptb_mb16_full_size_vs_oracle",
+             "tests/test_gpu_parity.py::test_char_tagger_full_size_vs_oracle"]
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", *tests],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
