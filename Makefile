@@ -9,7 +9,16 @@ OBJ := build/obj
 LIB := $(PKG)/libdyngpu.so
 OBJS := $(OBJ)/executor.o $(OBJ)/kernels.o $(OBJ)/gemm.o $(OBJ)/tcgemm.o $(OBJ)/rnn.o $(OBJ)/tmagemm.o
 
-all: $(LIB)
+PYTHON ?= python3
+PYINC := $(shell $(PYTHON) -c "import sysconfig; print(sysconfig.get_paths()['include'])")
+PYEXT := $(shell $(PYTHON) -c "import sysconfig; print(sysconfig.get_config_var('EXT_SUFFIX'))")
+CORE := $(PKG)/_dgcore$(PYEXT)
+
+all: $(LIB) $(CORE)
+
+# host-side native graph construction (CPython extension, plain C)
+$(CORE): $(SRC)/dgcore.c
+	gcc -O2 -Wall -shared -fPIC -I$(PYINC) $< -o $@
 
 $(OBJ):
 	mkdir -p $(OBJ)
@@ -36,6 +45,6 @@ $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart_static -lrt -ldl -lpthread
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(CORE)
 
 .PHONY: all clean

@@ -1,0 +1,725 @@
+/* _dgcore: native host-side graph construction for the drop-in API.
+ *
+ * The reference builds its graph in Python (graph.py:97-106: staleness check,
+ * OpDef.shape rule, Node append, Expression handle).  Per training step the
+ * PTB RNNLM builds ~1200 nodes, so construction and packing the node table for
+ * the executor dominated the host side of a step.  This module implements
+ *   - the Shape / Node / Expression storage as C base types (the Python
+ *     classes in tensor.py / graph.py subclass them and keep every method),
+ *   - GraphCore.add(kind, inputs, aux): the add_node fast path -- staleness
+ *     checks, the shape rules of the built-in op kinds (happy path; anything
+ *     irregular defers to the Python rule so errors are raised by the same
+ *     code with the same messages), and the dg_node record encoding
+ *     (include/dyngpu.h) into C buffers handed to dg_graph_append without a
+ *     Python-level packing pass.
+ * Kinds without a native rule (or re-registered by the user) go through the
+ * Python OpDef.shape / OpDef.encode hooks and still land in the C records.
+ */
+#define PY_SSIZE_T_CLEAN
+#include <Python.h>
+#include <structmember.h>
+#include <stdint.h>
+#include <string.h>
+
+/* op codes (dyngpu.h dg_op) */
+enum {
+  OP_INPUT = 0, OP_PARAMETER = 1, OP_LOOKUP = 2, OP_LOOKUP_BATCH = 3, OP_ADD = 4, OP_CMULT = 5,
+  OP_SCALAR_MUL = 6, OP_TANH = 7, OP_LOGISTIC = 8, OP_MATMUL = 9, OP_AFFINE = 10, OP_CONCATENATE = 11,
+  OP_PICK_RANGE = 12, OP_SOFTMAX = 13, OP_PNLS = 14, OP_PNLS_BATCH = 15, OP_SUM_BATCHES = 16
+};
+#define HDR 13
+
+/* ------------------------------------------------------------ base types */
+typedef struct {
+  PyObject_HEAD
+  PyObject* dims; /* tuple of int */
+  long batch;
+  PyObject* enc;  /* unused slot kept for subclasses */
+} ShapeObj;
+
+typedef struct {
+  PyObject_HEAD
+  PyObject* kind;
+  PyObject* inputs;
+  PyObject* shape;
+  PyObject* aux;
+  long code;
+} NodeObj;
+
+typedef struct {
+  PyObject_HEAD
+  PyObject* graph;
+  Py_ssize_t index;
+  long generation;
+} ExprObj;
+
+static void shape_dealloc(ShapeObj* s) {
+  Py_XDECREF(s->dims);
+  Py_XDECREF(s->enc);
+  Py_TYPE(s)->tp_free((PyObject*)s);
+}
+static void node_dealloc(NodeObj* n) {
+  Py_XDECREF(n->kind);
+  Py_XDECREF(n->inputs);
+  Py_XDECREF(n->shape);
+  Py_XDECREF(n->aux);
+  Py_TYPE(n)->tp_free((PyObject*)n);
+}
+static void expr_dealloc(ExprObj* e) {
+  Py_XDECREF(e->graph);
+  Py_TYPE(e)->tp_free((PyObject*)e);
+}
+
+static PyMemberDef shape_members[] = {
+    {"dims", T_OBJECT_EX, offsetof(ShapeObj, dims), 0, "dims tuple"},
+    {"batch", T_LONG, offsetof(ShapeObj, batch), 0, "batch count"},
+    {"_enc", T_OBJECT, offsetof(ShapeObj, enc), 0, "cache slot"},
+    {NULL}};
+static PyMemberDef node_members[] = {
+    {"kind", T_OBJECT_EX, offsetof(NodeObj, kind), 0, NULL},
+    {"inputs", T_OBJECT_EX, offsetof(NodeObj, inputs), 0, NULL},
+    {"shape", T_OBJECT_EX, offsetof(NodeObj, shape), 0, NULL},
+    {"aux", T_OBJECT, offsetof(NodeObj, aux), 0, NULL},
+    {"code", T_LONG, offsetof(NodeObj, code), 0, NULL},
+    {NULL}};
+static PyMemberDef expr_members[] = {
+    {"graph", T_OBJECT_EX, offsetof(ExprObj, graph), 0, NULL},
+    {"index", T_PYSSIZET, offsetof(ExprObj, index), 0, NULL},
+    {"generation", T_LONG, offsetof(ExprObj, generation), 0, NULL},
+    {NULL}};
+
+static PyTypeObject ShapeBaseType = {PyVarObject_HEAD_INIT(NULL, 0).tp_name = "_dgcore.ShapeBase",
+                                     .tp_basicsize = sizeof(ShapeObj),
+                                     .tp_dealloc = (destructor)shape_dealloc,
+                                     .tp_flags = Py_TPFLAGS_DEFAULT | Py_TPFLAGS_BASETYPE,
+                                     .tp_members = shape_members,
+                                     .tp_new = PyType_GenericNew};
+static PyTypeObject NodeBaseType = {PyVarObject_HEAD_INIT(NULL, 0).tp_name = "_dgcore.NodeBase",
+                                    .tp_basicsize = sizeof(NodeObj),
+                                    .tp_dealloc = (destructor)node_dealloc,
+                                    .tp_flags = Py_TPFLAGS_DEFAULT | Py_TPFLAGS_BASETYPE,
+                                    .tp_members = node_members,
+                                    .tp_new = PyType_GenericNew};
+static PyTypeObject ExprBaseType = {PyVarObject_HEAD_INIT(NULL, 0).tp_name = "_dgcore.ExprBase",
+                                    .tp_basicsize = sizeof(ExprObj),
+                                    .tp_dealloc = (destructor)expr_dealloc,
+                                    .tp_flags = Py_TPFLAGS_DEFAULT | Py_TPFLAGS_BASETYPE,
+                                    .tp_members = expr_members,
+                                    .tp_new = PyType_GenericNew};
+
+/* Python subclasses registered by setup(): instances are allocated directly */
+static PyTypeObject* ShapeT = NULL;
+static PyTypeObject* NodeT = NULL;
+static PyTypeObject* ExprT = NULL;
+static PyObject* Registry = NULL;  /* ops.REGISTRY */
+static PyObject* FastKinds = NULL; /* kind str -> code for kinds with the built-in rule */
+static PyObject* s_shape = NULL, *s_encode = NULL, *s_handle = NULL, *s_rows = NULL, *s_dim = NULL,
+                *s_data = NULL, *s_check_current = NULL, *s_code = NULL;
+
+static PyObject* new_shape(PyObject* dims, long batch) {
+  ShapeObj* s = (ShapeObj*)ShapeT->tp_alloc(ShapeT, 0);
+  if (!s) return NULL;
+  Py_INCREF(dims);
+  s->dims = dims;
+  s->batch = batch;
+  s->enc = NULL;
+  return (PyObject*)s;
+}
+
+/* --------------------------------------------------------------- records */
+typedef struct {
+  char* p;
+  Py_ssize_t n, cap, esz;
+} Buf;
+
+static int buf_reserve(Buf* b, Py_ssize_t extra) {
+  if (b->n + extra <= b->cap) return 0;
+  Py_ssize_t cap = b->cap ? b->cap : 1024;
+  while (cap < b->n + extra) cap *= 2;
+  char* p = (char*)PyMem_Realloc(b->p, (size_t)(cap * b->esz));
+  if (!p) {
+    PyErr_NoMemory();
+    return -1;
+  }
+  b->p = p;
+  b->cap = cap;
+  return 0;
+}
+
+typedef struct {
+  PyObject_HEAD
+  PyObject* cg;    /* borrowed: the core is owned by its graph */
+  PyObject* nodes; /* the graph's node list */
+  long gen;
+  Buf hdr, ins, ai, af, rebased;
+  PyObject* fix; /* list of (ai position, parameter-like with .handle) */
+} CoreObj;
+
+static void core_dealloc(CoreObj* c) {
+  Py_XDECREF(c->nodes);
+  Py_XDECREF(c->fix);
+  PyMem_Free(c->hdr.p);
+  PyMem_Free(c->ins.p);
+  PyMem_Free(c->ai.p);
+  PyMem_Free(c->af.p);
+  PyMem_Free(c->rebased.p);
+  Py_TYPE(c)->tp_free((PyObject*)c);
+}
+
+static int core_init(CoreObj* c, PyObject* args, PyObject* kw) {
+  PyObject *cg, *nodes;
+  if (!PyArg_ParseTuple(args, "OO!", &cg, &PyList_Type, &nodes)) return -1;
+  c->cg = cg;
+  Py_XSETREF(c->nodes, Py_NewRef(nodes));
+  c->gen = 0;
+  c->hdr.esz = 4;
+  c->ins.esz = 4;
+  c->ai.esz = 8;
+  c->af.esz = 4;
+  c->rebased.esz = 4;
+  Py_XSETREF(c->fix, PyList_New(0));
+  return c->fix ? 0 : -1;
+}
+
+static PyObject* core_renew(CoreObj* c, PyObject* arg) {
+  c->gen = PyLong_AsLong(arg);
+  if (c->gen == -1 && PyErr_Occurred()) return NULL;
+  c->hdr.n = c->ins.n = c->ai.n = c->af.n = 0;
+  if (PyList_SetSlice(c->fix, 0, PyList_GET_SIZE(c->fix), NULL) < 0) return NULL;
+  Py_RETURN_NONE;
+}
+
+/* append a node record; ai (n_ai int64) and af (n_af float) payloads */
+static int put_record(CoreObj* c, long code, const int32_t* idx, int n_in, ShapeObj* sh, const int64_t* ai,
+                      Py_ssize_t n_ai, const float* af, Py_ssize_t n_af) {
+  if (buf_reserve(&c->hdr, HDR) || buf_reserve(&c->ins, n_in) || buf_reserve(&c->ai, n_ai) ||
+      buf_reserve(&c->af, n_af))
+    return -1;
+  int32_t* h = (int32_t*)c->hdr.p + c->hdr.n;
+  const Py_ssize_t r = PyTuple_GET_SIZE(sh->dims);
+  h[0] = (int32_t)code;
+  h[1] = n_in;
+  h[2] = (int32_t)c->ins.n;
+  h[3] = (int32_t)r;
+  for (int d = 0; d < 4; ++d) h[4 + d] = d < r ? (int32_t)PyLong_AsLong(PyTuple_GET_ITEM(sh->dims, d)) : 1;
+  h[8] = (int32_t)sh->batch;
+  h[9] = (int32_t)c->ai.n;
+  h[10] = (int32_t)n_ai;
+  h[11] = (int32_t)c->af.n;
+  h[12] = (int32_t)n_af;
+  c->hdr.n += HDR;
+  memcpy((int32_t*)c->ins.p + c->ins.n, idx, sizeof(int32_t) * (size_t)n_in);
+  c->ins.n += n_in;
+  if (n_ai) memcpy((int64_t*)c->ai.p + c->ai.n, ai, sizeof(int64_t) * (size_t)n_ai);
+  c->ai.n += n_ai;
+  if (n_af) memcpy((float*)c->af.p + c->af.n, af, sizeof(float) * (size_t)n_af);
+  c->af.n += n_af;
+  return 0;
+}
+
+static int add_fix(CoreObj* c, Py_ssize_t pos, PyObject* param) {
+  PyObject* t = Py_BuildValue("(nO)", pos, param);
+  if (!t) return -1;
+  int rc = PyList_Append(c->fix, t);
+  Py_DECREF(t);
+  return rc;
+}
+
+/* Python fallback: od.shape(aux, in_shapes) and od.encode(aux) */
+static PyObject* slow_shape(PyObject* od, PyObject* aux, PyObject* in_shapes) {
+  PyObject* rule = PyObject_GetAttr(od, s_shape);
+  if (!rule) return NULL;
+  PyObject* r = PyObject_CallFunctionObjArgs(rule, aux, in_shapes, NULL);
+  Py_DECREF(rule);
+  return r;
+}
+
+static int slow_encode(CoreObj* c, PyObject* od, long code, PyObject* aux, const int32_t* idx, int n_in,
+                       ShapeObj* sh) {
+  PyObject* enc = PyObject_GetAttr(od, s_encode);
+  if (!enc) return -1;
+  PyObject* r = PyObject_CallOneArg(enc, aux);
+  Py_DECREF(enc);
+  if (!r) return -1;
+  int rc = -1;
+  PyObject *ai = NULL, *af = NULL, *aiseq = NULL;
+  int64_t* aiv = NULL;
+  Py_buffer view = {0};
+  int have_view = 0;
+  if (!PyTuple_Check(r) || PyTuple_GET_SIZE(r) != 2) {
+    PyErr_SetString(PyExc_TypeError, "encode must return (aux_i, aux_f)");
+    goto done;
+  }
+  ai = PyTuple_GET_ITEM(r, 0);
+  af = PyTuple_GET_ITEM(r, 1);
+  aiseq = PySequence_Fast(ai, "aux_i must be a sequence");
+  if (!aiseq) goto done;
+  Py_ssize_t n_ai = PySequence_Fast_GET_SIZE(aiseq);
+  aiv = (int64_t*)PyMem_Malloc(sizeof(int64_t) * (size_t)(n_ai ? n_ai : 1));
+  if (!aiv) {
+    PyErr_NoMemory();
+    goto done;
+  }
+  for (Py_ssize_t q = 0; q < n_ai; ++q) {
+    aiv[q] = PyLong_AsLongLong(PySequence_Fast_GET_ITEM(aiseq, q));
+    if (aiv[q] == -1 && PyErr_Occurred()) goto done;
+  }
+  const float* afp = NULL;
+  Py_ssize_t n_af = 0;
+  if (af != Py_None) {
+    if (PyObject_GetBuffer(af, &view, PyBUF_C_CONTIGUOUS | PyBUF_FORMAT) < 0) goto done;
+    have_view = 1;
+    if (view.itemsize != 4 || !view.format || strcmp(view.format, "f") != 0) {
+      PyErr_SetString(PyExc_TypeError, "aux_f must be a contiguous float32 array");
+      goto done;
+    }
+    afp = (const float*)view.buf;
+    n_af = view.len / 4;
+  }
+  if ((code == OP_PARAMETER || code == OP_LOOKUP || code == OP_LOOKUP_BATCH) && n_ai > 0) {
+    /* the handle slot is resolved at flush (parameters materialise lazily) */
+    PyObject* owner = code == OP_PARAMETER ? aux : PyTuple_GetItem(aux, 0);
+    if (!owner || add_fix(c, c->ai.n, owner) < 0) goto done;
+  }
+  rc = put_record(c, code, idx, n_in, sh, aiv, n_ai, afp, n_af);
+done:
+  if (have_view) PyBuffer_Release(&view);
+  PyMem_Free(aiv);
+  Py_XDECREF(aiseq);
+  Py_DECREF(r);
+  return rc;
+}
+
+static long get_long_attr(PyObject* o, PyObject* name, int* err) {
+  PyObject* v = PyObject_GetAttr(o, name);
+  if (!v) {
+    *err = 1;
+    return 0;
+  }
+  long x = PyLong_AsLong(v);
+  Py_DECREF(v);
+  if (x == -1 && PyErr_Occurred()) *err = 1;
+  return x;
+}
+
+#define MAX_IN 64
+
+/* GraphCore.add(kind, inputs, aux) -> Expression */
+static PyObject* core_add(CoreObj* c, PyObject* const* args, Py_ssize_t nargs) {
+  if (nargs < 1 || nargs > 3) {
+    PyErr_SetString(PyExc_TypeError, "add(kind, inputs=(), aux=None)");
+    return NULL;
+  }
+  PyObject* kind = args[0];
+  PyObject* inputs = nargs > 1 ? args[1] : NULL;
+  PyObject* aux = nargs > 2 ? args[2] : Py_None;
+  PyObject* seq = NULL;
+  Py_ssize_t n_in = 0;
+  if (inputs) {
+    seq = PySequence_Fast(inputs, "inputs must be a sequence of expressions");
+    if (!seq) return NULL;
+    n_in = PySequence_Fast_GET_SIZE(seq);
+  }
+  int32_t idx_stack[MAX_IN];
+  int32_t* idx = idx_stack;
+  ShapeObj* shp_stack[MAX_IN];
+  ShapeObj** shp = shp_stack;
+  if (n_in > MAX_IN) {
+    idx = (int32_t*)PyMem_Malloc(sizeof(int32_t) * (size_t)n_in);
+    shp = (ShapeObj**)PyMem_Malloc(sizeof(ShapeObj*) * (size_t)n_in);
+    if (!idx || !shp) {
+      PyErr_NoMemory();
+      goto fail0;
+    }
+  }
+  const Py_ssize_t n_nodes = PyList_GET_SIZE(c->nodes);
+  for (Py_ssize_t k = 0; k < n_in; ++k) {
+    PyObject* e = PySequence_Fast_GET_ITEM(seq, k);
+    if (!PyObject_TypeCheck(e, &ExprBaseType) || ((ExprObj*)e)->graph != c->cg || ((ExprObj*)e)->generation != c->gen ||
+        ((ExprObj*)e)->index < 0 || ((ExprObj*)e)->index >= n_nodes) {
+      /* the Python check raises StaleExpression with the reference message */
+      PyObject* r = PyObject_CallMethodOneArg(c->cg, s_check_current, e);
+      if (!r) goto fail0;
+      Py_DECREF(r);
+      PyErr_SetString(PyExc_TypeError, "graph inputs must be expressions of this graph");
+      goto fail0;
+    }
+    const Py_ssize_t i = ((ExprObj*)e)->index;
+    idx[k] = (int32_t)i;
+    shp[k] = (ShapeObj*)((NodeObj*)PyList_GET_ITEM(c->nodes, i))->shape;
+  }
+  PyObject* codeobj = PyDict_GetItemWithError(FastKinds, kind);
+  if (!codeobj && PyErr_Occurred()) goto fail0;
+  long code = codeobj ? PyLong_AsLong(codeobj) : -1;
+  PyObject* shape = NULL; /* new reference */
+  /* ---- fast paths of the built-in rules (ops.py); irregular inputs defer to
+     the Python rule, which raises the reference error */
+  int64_t ai_small[4];
+  Py_ssize_t n_ai = 0;
+  float af_small[1];
+  Py_ssize_t n_af = 0;
+  PyObject* fixobj = NULL; /* borrowed */
+  int done = 0;
+  switch (code) {
+    case OP_TANH:
+    case OP_LOGISTIC:
+      if (n_in == 1) {
+        shape = Py_NewRef((PyObject*)shp[0]);
+        done = 1;
+      }
+      break;
+    case OP_SCALAR_MUL:
+      if (n_in == 1 && PyFloat_CheckExact(aux)) {
+        shape = Py_NewRef((PyObject*)shp[0]);
+        af_small[0] = (float)PyFloat_AS_DOUBLE(aux);
+        n_af = 1;
+        done = 1;
+      }
+      break;
+    case OP_ADD:
+    case OP_CMULT:
+      if (n_in == 2) {
+        PyObject* da = shp[0]->dims;
+        PyObject* db = shp[1]->dims;
+        int same = da == db;
+        if (!same) {
+          same = PyObject_RichCompareBool(da, db, Py_EQ);
+          if (same < 0) goto fail0;
+        }
+        const long ba = shp[0]->batch, bb = shp[1]->batch;
+        if (same && (ba == bb || ba == 1 || bb == 1)) {
+          shape = new_shape(da, ba > bb ? ba : bb);
+          if (!shape) goto fail0;
+          done = 1;
+        }
+      }
+      break;
+    case OP_PICK_RANGE:
+      if (n_in == 1 && PyTuple_CheckExact(aux) && PyTuple_GET_SIZE(aux) == 2 && PyTuple_GET_SIZE(shp[0]->dims) == 1) {
+        const long lo = PyLong_AsLong(PyTuple_GET_ITEM(aux, 0)), hi = PyLong_AsLong(PyTuple_GET_ITEM(aux, 1));
+        if (PyErr_Occurred()) goto fail0;
+        const long n = PyLong_AsLong(PyTuple_GET_ITEM(shp[0]->dims, 0));
+        if (0 <= lo && lo < hi && hi <= n) {
+          PyObject* d = Py_BuildValue("(l)", hi - lo);
+          if (!d) goto fail0;
+          shape = new_shape(d, shp[0]->batch);
+          Py_DECREF(d);
+          if (!shape) goto fail0;
+          ai_small[0] = lo;
+          ai_small[1] = hi;
+          n_ai = 2;
+          done = 1;
+        }
+      }
+      break;
+    case OP_AFFINE:
+      if (n_in >= 3 && n_in % 2 == 1 && PyTuple_GET_SIZE(shp[0]->dims) == 1) {
+        const long m = PyLong_AsLong(PyTuple_GET_ITEM(shp[0]->dims, 0));
+        long batch = shp[0]->batch;
+        int ok = 1;
+        for (Py_ssize_t k = 1; k + 1 < n_in && ok; k += 2) {
+          PyObject *wd = shp[k]->dims, *xd = shp[k + 1]->dims;
+          if (PyTuple_GET_SIZE(wd) != 2 || PyTuple_GET_SIZE(xd) != 1) {
+            ok = 0;
+            break;
+          }
+          if (PyLong_AsLong(PyTuple_GET_ITEM(wd, 0)) != m ||
+              PyLong_AsLong(PyTuple_GET_ITEM(wd, 1)) != PyLong_AsLong(PyTuple_GET_ITEM(xd, 0))) {
+            ok = 0;
+            break;
+          }
+          for (int q = 0; q < 2; ++q) {
+            const long sb = shp[k + q]->batch;
+            if (sb != 1) {
+              if (batch != 1 && sb != batch) ok = 0;
+              batch = sb;
+            }
+          }
+        }
+        if (PyErr_Occurred()) goto fail0;
+        if (ok) {
+          shape = new_shape(shp[0]->dims, batch);
+          if (!shape) goto fail0;
+          done = 1;
+        }
+      }
+      break;
+    case OP_PARAMETER:
+      if (n_in == 0) {
+        shape = PyObject_GetAttr(aux, s_shape);
+        if (!shape) goto fail0;
+        if (!PyObject_TypeCheck(shape, &ShapeBaseType)) {
+          Py_CLEAR(shape);
+          break;
+        }
+        int err = 0;
+        ai_small[0] = get_long_attr(aux, s_handle, &err);
+        if (err) goto fail_shape;
+        n_ai = 1;
+        fixobj = aux;
+        done = 1;
+      }
+      break;
+    case OP_LOOKUP_BATCH:
+      if (n_in == 0 && PyTuple_CheckExact(aux) && PyTuple_GET_SIZE(aux) == 2 && PyTuple_CheckExact(PyTuple_GET_ITEM(aux, 1))) {
+        PyObject* lp = PyTuple_GET_ITEM(aux, 0);
+        PyObject* ids = PyTuple_GET_ITEM(aux, 1);
+        const Py_ssize_t nid = PyTuple_GET_SIZE(ids);
+        int err = 0;
+        const long rows = get_long_attr(lp, s_rows, &err);
+        const long dim = err ? 0 : get_long_attr(lp, s_dim, &err);
+        const long handle = err ? 0 : get_long_attr(lp, s_handle, &err);
+        if (err) goto fail0;
+        if (nid == 0) break;
+        int64_t* v = (int64_t*)PyMem_Malloc(sizeof(int64_t) * (size_t)(nid + 1));
+        if (!v) {
+          PyErr_NoMemory();
+          goto fail0;
+        }
+        int ok = 1;
+        v[0] = handle;
+        for (Py_ssize_t q = 0; q < nid && ok; ++q) {
+          const long x = PyLong_AsLong(PyTuple_GET_ITEM(ids, q));
+          if (x == -1 && PyErr_Occurred()) {
+            PyMem_Free(v);
+            goto fail0;
+          }
+          if (x < 0 || x >= rows) ok = 0;
+          v[q + 1] = x;
+        }
+        if (!ok) {
+          PyMem_Free(v);
+          break;
+        }
+        PyObject* d = Py_BuildValue("(l)", dim);
+        if (!d) {
+          PyMem_Free(v);
+          goto fail0;
+        }
+        shape = new_shape(d, (long)nid);
+        Py_DECREF(d);
+        if (!shape) {
+          PyMem_Free(v);
+          goto fail0;
+        }
+        if (add_fix(c, c->ai.n, lp) < 0 || put_record(c, code, idx, (int)n_in, (ShapeObj*)shape, v, nid + 1, NULL, 0) < 0) {
+          PyMem_Free(v);
+          goto fail_shape;
+        }
+        PyMem_Free(v);
+        done = 2; /* record written */
+      }
+      break;
+    case OP_PNLS_BATCH:
+      if (n_in == 1 && PyTuple_CheckExact(aux) && PyTuple_GET_SIZE(shp[0]->dims) == 1 &&
+          PyTuple_GET_SIZE(aux) == shp[0]->batch) {
+        const long n = PyLong_AsLong(PyTuple_GET_ITEM(shp[0]->dims, 0));
+        const Py_ssize_t nl = PyTuple_GET_SIZE(aux);
+        int64_t* v = (int64_t*)PyMem_Malloc(sizeof(int64_t) * (size_t)(nl ? nl : 1));
+        if (!v) {
+          PyErr_NoMemory();
+          goto fail0;
+        }
+        int ok = 1;
+        for (Py_ssize_t q = 0; q < nl && ok; ++q) {
+          const long x = PyLong_AsLong(PyTuple_GET_ITEM(aux, q));
+          if (x == -1 && PyErr_Occurred()) {
+            PyMem_Free(v);
+            goto fail0;
+          }
+          if (x < 0 || x >= n) ok = 0;
+          v[q] = x;
+        }
+        if (!ok) {
+          PyMem_Free(v);
+          break;
+        }
+        static PyObject* one = NULL;
+        if (!one) one = Py_BuildValue("(i)", 1);
+        shape = new_shape(one, shp[0]->batch);
+        if (!shape || put_record(c, code, idx, (int)n_in, (ShapeObj*)shape, v, nl, NULL, 0) < 0) {
+          PyMem_Free(v);
+          goto fail_shape;
+        }
+        PyMem_Free(v);
+        done = 2;
+      }
+      break;
+    default:
+      break;
+  }
+  PyObject* od = NULL;
+  if (!done) {
+    /* Python rule + encode hooks (custom kinds, irregular inputs, errors) */
+    od = PyDict_GetItemWithError(Registry, kind);
+    if (!od) {
+      if (!PyErr_Occurred()) PyErr_SetObject(PyExc_KeyError, kind);
+      goto fail0;
+    }
+    int err = 0;
+    code = get_long_attr(od, s_code, &err);
+    if (err) goto fail0;
+    PyObject* in_shapes = PyList_New(n_in);
+    if (!in_shapes) goto fail0;
+    for (Py_ssize_t k = 0; k < n_in; ++k) PyList_SET_ITEM(in_shapes, k, Py_NewRef((PyObject*)shp[k]));
+    shape = slow_shape(od, aux, in_shapes);
+    Py_DECREF(in_shapes);
+    if (!shape) goto fail0;
+    if (!PyObject_TypeCheck(shape, &ShapeBaseType)) {
+      PyErr_SetString(PyExc_TypeError, "shape rule must return a Shape");
+      goto fail_shape;
+    }
+    if (slow_encode(c, od, code, aux, idx, (int)n_in, (ShapeObj*)shape) < 0) goto fail_shape;
+  } else if (done == 1) {
+    if (fixobj && add_fix(c, c->ai.n, fixobj) < 0) goto fail_shape;
+    if (put_record(c, code, idx, (int)n_in, (ShapeObj*)shape, ai_small, n_ai, af_small, n_af) < 0) goto fail_shape;
+  }
+  /* Node + Expression */
+  {
+    PyObject* tin = PyTuple_New(n_in);
+    if (!tin) goto fail_shape;
+    for (Py_ssize_t k = 0; k < n_in; ++k) {
+      PyObject* v = PyLong_FromLong(idx[k]);
+      if (!v) {
+        Py_DECREF(tin);
+        goto fail_shape;
+      }
+      PyTuple_SET_ITEM(tin, k, v);
+    }
+    NodeObj* nd = (NodeObj*)NodeT->tp_alloc(NodeT, 0);
+    if (!nd) {
+      Py_DECREF(tin);
+      goto fail_shape;
+    }
+    nd->kind = Py_NewRef(kind);
+    nd->inputs = tin;
+    nd->shape = shape; /* steals */
+    nd->aux = Py_NewRef(aux);
+    nd->code = code;
+    int rc = PyList_Append(c->nodes, (PyObject*)nd);
+    Py_DECREF(nd);
+    if (rc < 0) goto fail0;
+  }
+  if (idx != idx_stack) PyMem_Free(idx);
+  if (shp != shp_stack) PyMem_Free(shp);
+  Py_XDECREF(seq);
+  ExprObj* ex = (ExprObj*)ExprT->tp_alloc(ExprT, 0);
+  if (!ex) return NULL;
+  ex->graph = Py_NewRef(c->cg);
+  ex->index = PyList_GET_SIZE(c->nodes) - 1;
+  ex->generation = c->gen;
+  return (PyObject*)ex;
+fail_shape:
+  Py_XDECREF(shape);
+fail0:
+  if (idx != idx_stack) PyMem_Free(idx);
+  if (shp != shp_stack) PyMem_Free(shp);
+  Py_XDECREF(seq);
+  return NULL;
+}
+
+/* GraphCore.pack(start) -> (hdr, n, ins, n_ins, ai, n_ai, af, n_af) raw pointers of the
+ * records of nodes [start, end) with offsets rebased on the batch; parameter handles
+ * are resolved first.  The pointers stay valid until the next add/renew. */
+static PyObject* core_pack(CoreObj* c, PyObject* arg) {
+  const Py_ssize_t start = PyLong_AsSsize_t(arg);
+  if (start == -1 && PyErr_Occurred()) return NULL;
+  const Py_ssize_t end = c->hdr.n / HDR;
+  if (start < 0 || start > end) {
+    PyErr_SetString(PyExc_IndexError, "pack start out of range");
+    return NULL;
+  }
+  const Py_ssize_t nfix = PyList_GET_SIZE(c->fix);
+  for (Py_ssize_t q = 0; q < nfix; ++q) {
+    PyObject* t = PyList_GET_ITEM(c->fix, q);
+    const Py_ssize_t pos = PyLong_AsSsize_t(PyTuple_GET_ITEM(t, 0));
+    int err = 0;
+    const long h = get_long_attr(PyTuple_GET_ITEM(t, 1), s_handle, &err);
+    if (err) return NULL;
+    ((int64_t*)c->ai.p)[pos] = h;
+  }
+  const Py_ssize_t n = end - start;
+  c->rebased.n = 0;
+  if (buf_reserve(&c->rebased, n * HDR + 1)) return NULL;
+  int32_t* dst = (int32_t*)c->rebased.p;
+  const int32_t* src = (const int32_t*)c->hdr.p + start * HDR;
+  int32_t in0 = 0, ai0 = 0, af0 = 0;
+  if (n > 0) {
+    in0 = src[2];
+    ai0 = src[9];
+    af0 = src[11];
+  }
+  for (Py_ssize_t i = 0; i < n; ++i) {
+    memcpy(dst + i * HDR, src + i * HDR, sizeof(int32_t) * HDR);
+    dst[i * HDR + 2] -= in0;
+    dst[i * HDR + 9] -= ai0;
+    dst[i * HDR + 11] -= af0;
+  }
+  return Py_BuildValue("(KnKnKnKn)", (unsigned long long)(uintptr_t)dst, n,
+                       (unsigned long long)(uintptr_t)((int32_t*)c->ins.p + in0), c->ins.n - in0,
+                       (unsigned long long)(uintptr_t)((int64_t*)c->ai.p + ai0), c->ai.n - ai0,
+                       (unsigned long long)(uintptr_t)((float*)c->af.p + af0), c->af.n - af0);
+}
+
+static PyMethodDef core_methods[] = {
+    {"add", (PyCFunction)(void (*)(void))core_add, METH_FASTCALL, "add(kind, inputs=(), aux=None) -> Expression"},
+    {"renew", (PyCFunction)core_renew, METH_O, "renew(generation)"},
+    {"pack", (PyCFunction)core_pack, METH_O, "pack(start) -> raw record pointers"},
+    {NULL}};
+
+static PyTypeObject CoreType = {PyVarObject_HEAD_INIT(NULL, 0).tp_name = "_dgcore.GraphCore",
+                                .tp_basicsize = sizeof(CoreObj),
+                                .tp_dealloc = (destructor)core_dealloc,
+                                .tp_flags = Py_TPFLAGS_DEFAULT,
+                                .tp_methods = core_methods,
+                                .tp_init = (initproc)core_init,
+                                .tp_new = PyType_GenericNew};
+
+/* setup(ShapeCls, NodeCls, ExprCls, registry, fast_kinds) */
+static PyObject* mod_setup(PyObject* self, PyObject* args) {
+  PyObject *st, *nt, *et, *reg, *fk;
+  if (!PyArg_ParseTuple(args, "O!O!O!O!O!", &PyType_Type, &st, &PyType_Type, &nt, &PyType_Type, &et, &PyDict_Type,
+                        &reg, &PyDict_Type, &fk))
+    return NULL;
+  if (!PyType_IsSubtype((PyTypeObject*)st, &ShapeBaseType) || !PyType_IsSubtype((PyTypeObject*)nt, &NodeBaseType) ||
+      !PyType_IsSubtype((PyTypeObject*)et, &ExprBaseType)) {
+    PyErr_SetString(PyExc_TypeError, "setup needs subclasses of ShapeBase / NodeBase / ExprBase");
+    return NULL;
+  }
+  Py_XSETREF(ShapeT, (PyTypeObject*)Py_NewRef(st));
+  Py_XSETREF(NodeT, (PyTypeObject*)Py_NewRef(nt));
+  Py_XSETREF(ExprT, (PyTypeObject*)Py_NewRef(et));
+  Py_XSETREF(Registry, Py_NewRef(reg));
+  Py_XSETREF(FastKinds, Py_NewRef(fk));
+  Py_RETURN_NONE;
+}
+
+static PyMethodDef mod_methods[] = {{"setup", mod_setup, METH_VARARGS, "register the Python subclasses"}, {NULL}};
+
+static struct PyModuleDef moddef = {PyModuleDef_HEAD_INIT, "_dgcore", "native graph construction", -1, mod_methods};
+
+PyMODINIT_FUNC PyInit__dgcore(void) {
+  if (PyType_Ready(&ShapeBaseType) < 0 || PyType_Ready(&NodeBaseType) < 0 || PyType_Ready(&ExprBaseType) < 0 ||
+      PyType_Ready(&CoreType) < 0)
+    return NULL;
+  PyObject* m = PyModule_Create(&moddef);
+  if (!m) return NULL;
+  s_shape = PyUnicode_InternFromString("shape");
+  s_encode = PyUnicode_InternFromString("encode");
+  s_handle = PyUnicode_InternFromString("handle");
+  s_rows = PyUnicode_InternFromString("rows");
+  s_dim = PyUnicode_InternFromString("dim");
+  s_data = PyUnicode_InternFromString("data");
+  s_check_current = PyUnicode_InternFromString("check_current");
+  s_code = PyUnicode_InternFromString("code");
+  Py_INCREF(&ShapeBaseType);
+  Py_INCREF(&NodeBaseType);
+  Py_INCREF(&ExprBaseType);
+  Py_INCREF(&CoreType);
+  if (PyModule_AddObject(m, "ShapeBase", (PyObject*)&ShapeBaseType) < 0 ||
+      PyModule_AddObject(m, "NodeBase", (PyObject*)&NodeBaseType) < 0 ||
+      PyModule_AddObject(m, "ExprBase", (PyObject*)&ExprBaseType) < 0 ||
+      PyModule_AddObject(m, "GraphCore", (PyObject*)&CoreType) < 0)
+    return NULL;
+  return m;
+}

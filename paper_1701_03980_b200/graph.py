@@ -20,18 +20,19 @@ import ctypes
 
 import numpy as np
 
-from . import _native
+from . import _dgcore, _native
 from . import device as _dev
 from .errors import ConfigError, NonScalarLoss, ShapeError, StaleExpression
-from .ops import REGISTRY
+from .ops import FAST_KINDS, REGISTRY
 from .params import materialize_pending
 from .tensor import Shape, Tensor
 
 
-class Expression:
-    """Handle to a graph node; valid for one graph generation."""
+class Expression(_dgcore.ExprBase):
+    """Handle to a graph node; valid for one graph generation (storage in the
+    _dgcore base type; instances are created by the native add_node)."""
 
-    __slots__ = ("graph", "index", "generation")
+    __slots__ = ()
 
     def __init__(self, graph: "ComputationGraph", index: int, generation: int):
         self.graph = graph
@@ -47,8 +48,8 @@ class Expression:
         return f"Expression(node={self.index}, gen={self.generation})"
 
 
-class Node:
-    __slots__ = ("kind", "inputs", "shape", "aux", "code")
+class Node(_dgcore.NodeBase):
+    __slots__ = ()
 
     def __init__(self, kind: str, inputs: tuple, shape: Shape, aux, code: int):
         self.kind = kind
@@ -80,6 +81,10 @@ class ComputationGraph:
         self.sink = DIRECT_SINK
         self._h = None  # native dg_graph*
         self._sent = 0  # nodes already appended to the native table
+        # native construction (csrc/dgcore.c): node records are encoded as the
+        # graph is built; add_node is the C fast path bound per instance
+        self._core = _dgcore.GraphCore(self, self.nodes)
+        self.add_node = self._core.add
         self._stream = None
         pools.bind(self)
 
@@ -142,40 +147,13 @@ class ComputationGraph:
             pass
 
     def _flush(self, h) -> None:
-        """Pack pending nodes into one dg_node table (dg_graph_append)."""
-        nodes = self.nodes
-        start, end = self._sent, len(nodes)
+        """Hand the pending node records (encoded at construction by the
+        native add_node) to the executor as one dg_node table."""
+        start, end = self._sent, len(self.nodes)
         if start == end:
             return
-        hdr = []
-        ins = []
-        aux_i = []
-        aux_f = []
-        n_f = 0
-        for i in range(start, end):
-            nd = nodes[i]
-            inputs = nd.inputs
-            dims = nd.shape.dims
-            r = len(dims)
-            ai, af = REGISTRY[nd.kind].encode(nd.aux)
-            nai = len(ai)
-            naf = 0 if af is None else af.shape[0]
-            d = dims + (1,) * (4 - r)
-            hdr.extend((nd.code, len(inputs), len(ins), r, d[0], d[1], d[2], d[3], nd.shape.batch,
-                        len(aux_i), nai, n_f, naf))
-            ins.extend(inputs)
-            if nai:
-                aux_i.extend(ai)
-            if naf:
-                aux_f.append(af)
-                n_f += naf
-        hdr_a = np.array(hdr, dtype=np.int32)
-        ins_a = np.array(ins, dtype=np.int32) if ins else np.zeros(1, np.int32)
-        ai_a = np.array(aux_i, dtype=np.int64) if aux_i else np.zeros(1, np.int64)
-        af_a = np.concatenate(aux_f).astype(np.float32, copy=False) if aux_f else np.zeros(1, np.float32)
-        _native.check(_native.lib().dg_graph_append(
-            h, hdr_a.ctypes.data, end - start, ins_a.ctypes.data, len(ins), ai_a.ctypes.data, len(aux_i),
-            af_a.ctypes.data, n_f))
+        hdr, n, ins, n_ins, ai, n_ai, af, n_af = self._core.pack(start)
+        _native.check(_native.lib().dg_graph_append(h, hdr, n, ins, n_ins, ai, n_ai, af, n_af))
         self._sent = end
 
     def _prepare(self):
@@ -191,6 +169,7 @@ class ComputationGraph:
         self.generation += 1
         self.watermark = -1
         self._sent = 0
+        self._core.renew(self.generation)
         self.pools.reset_transient()
 
     def check_current(self, e: Expression) -> None:
@@ -201,7 +180,13 @@ class ComputationGraph:
 
     # -- construction ------------------------------------------------------
 
-    def add_node(self, kind: str, inputs=(), aux=None) -> Expression:
+    def add_node(self, kind: str, inputs=(), aux=None) -> Expression:  # noqa: F811 - per-instance native override
+        """Reference-semantics add_node (graph.py:97-106); instances use the
+        native GraphCore.add bound in __init__, which runs the same checks and
+        shape rules (deferring to the Python rules for anything irregular)."""
+        return self._core.add(kind, tuple(inputs), aux)
+
+    def _add_node_py(self, kind: str, inputs=(), aux=None) -> Expression:
         gen = self.generation
         nodes = self.nodes
         in_shapes = []
@@ -266,3 +251,6 @@ class ComputationGraph:
         out = np.empty(shape.size(), dtype=np.float32)
         _native.check(_native.lib().dg_gradient(self._h, e.index, out.ctypes.data, out.shape[0]))
         return Tensor(shape, out)
+
+
+_dgcore.setup(Shape, Node, Expression, REGISTRY, FAST_KINDS)
