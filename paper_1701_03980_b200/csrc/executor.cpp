@@ -1698,7 +1698,7 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
     a.ctas = cta;
     a.n_flags = flag;
     a.vec = vec_ok ? 1 : 0;
-    a.trace = rnn_trace_enabled() ? 1 : 0;
+    a.trace = rnn_trace_enabled() ? (std::getenv("DG_RNN_TRACE")[0] == '2' ? 2 : 1) : 0;
     // cluster mode: one cluster per (chain, batch slice) exchanging through
     // distributed shared memory; needs equal unit-block counts (<= 16)
     int cl = a.ch[0].n_u;
@@ -2811,28 +2811,78 @@ int dg_backward(dg_graph* g, int32_t loss) {
   for (auto& kv : wuse) wkeys.push_back(kv.first);
   std::sort(wkeys.begin(), wkeys.end());
   {
-    GemmBatch gb;
-    gemm_batch_for(g, plan, gb, -1, C_GEMM_DW, true, false);
-    for (int64_t h : wkeys) {
-      AffineUse& use = wuse[h];
-      Param* p = param_at(h);
+    // rows of one parameter's uses -> the longest run where both the x rows
+    // and the gradient rows are equally spaced (a dense block: TMA path) plus
+    // the rest; the two parts accumulate into dW in two launches
+    auto regular_run = [](const std::vector<uintptr_t>& a, const std::vector<uintptr_t>& b, int64_t la,
+                          int64_t lb, size_t& best_lo, size_t& best_hi) {
+      const size_t n = a.size();
+      best_lo = best_hi = 0;
+      size_t lo = 0;
+      for (size_t i = 1; i <= n; ++i) {
+        bool cont = i < n;
+        if (cont && i - lo >= 2) {
+          cont = a[i] - a[i - 1] == a[lo + 1] - a[lo] && b[i] - b[i - 1] == b[lo + 1] - b[lo];
+        } else if (cont) {
+          const int64_t sa = (int64_t)(a[i] - a[i - 1]), sb = (int64_t)(b[i] - b[i - 1]);
+          cont = sa >= la * 4 && sb >= lb * 4 && sa % 16 == 0 && sb % 16 == 0 && (a[lo] & 15) == 0 &&
+                 (b[lo] & 15) == 0;
+        }
+        if (!cont) {
+          if (i - lo > best_hi - best_lo) {
+            best_lo = lo;
+            best_hi = i;
+          }
+          lo = i;
+        }
+      }
+    };
+    GemmBatch gb, gb_rest;
+    std::vector<std::pair<std::vector<uintptr_t>, std::vector<uintptr_t>>> rest_rows;
+    auto dw_problem = [&](const std::vector<uintptr_t>& xr, const std::vector<uintptr_t>& gr, const AffineUse& use,
+                          Param* p, GemmBatch& bt) {
       GemmProblem pr{};
       pr.M = (int)use.n_in;
       pr.N = (int)use.m;
       pr.n_seg = 1;
       pr.accumulate = 1;
-      pr.seg[0].K = (int64_t)use.x_rows.size();
-      pr.seg[0].A.rows = dev_at<const float*>(g, B.push(use.x_rows));
-      pr.seg[0].A.rows_aligned = all_aligned16(use.x_rows);
-      pr.seg[0].B.rows = dev_at<const float*>(g, B.push(use.g_rows));
-      pr.seg[0].B.rows_aligned = all_aligned16(use.g_rows);
+      pr.seg[0].K = (int64_t)xr.size();
+      pr.seg[0].A.rows = dev_at<const float*>(g, B.push(xr));
+      pr.seg[0].A.rows_aligned = all_aligned16(xr);
+      pr.seg[0].B.rows = dev_at<const float*>(g, B.push(gr));
+      pr.seg[0].B.rows_aligned = all_aligned16(gr);
       pr.C.base = p->grad;  // dW^T (n_in x m) row-major == dW column-major
       pr.C.ld = use.m;
-      gb.probs.push_back(pr);
-      gb.bytes += 4.0 * ((double)pr.seg[0].K * (pr.M + pr.N) + 2.0 * pr.M * pr.N);
+      bt.probs.push_back(pr);
+      bt.bytes += 4.0 * ((double)pr.seg[0].K * (pr.M + pr.N) + 2.0 * pr.M * pr.N);
+    };
+    gemm_batch_for(g, plan, gb, -1, C_GEMM_DW, true, false);
+    std::vector<std::pair<int64_t, std::pair<std::vector<uintptr_t>, std::vector<uintptr_t>>>> rests;
+    for (int64_t h : wkeys) {
+      AffineUse& use = wuse[h];
+      Param* p = param_at(h);
+      size_t lo = 0, hi = 0;
+      regular_run(use.x_rows, use.g_rows, use.n_in, use.m, lo, hi);
+      if (hi - lo >= 128 && hi - lo < use.x_rows.size()) {
+        std::vector<uintptr_t> xr(use.x_rows.begin() + lo, use.x_rows.begin() + hi);
+        std::vector<uintptr_t> grr(use.g_rows.begin() + lo, use.g_rows.begin() + hi);
+        dw_problem(xr, grr, use, p, gb);
+        std::vector<uintptr_t> xo(use.x_rows.begin(), use.x_rows.begin() + lo), go(use.g_rows.begin(), use.g_rows.begin() + lo);
+        xo.insert(xo.end(), use.x_rows.begin() + hi, use.x_rows.end());
+        go.insert(go.end(), use.g_rows.begin() + hi, use.g_rows.end());
+        rests.push_back({h, {std::move(xo), std::move(go)}});
+      } else {
+        dw_problem(use.x_rows, use.g_rows, use, p, gb);
+      }
     }
     flush_gemm(g, plan, gb);
+    if (!rests.empty()) {
+      gemm_batch_for(g, plan, gb_rest, -1, C_GEMM_DW, true, false);
+      for (auto& r : rests) dw_problem(r.second.first, r.second.second, wuse[r.first], param_at(r.first), gb_rest);
+      flush_gemm(g, plan, gb_rest);
+    }
   }
+  tm.lap("dW");
   std::vector<int64_t> bkeys;
   for (auto& kv : buse) bkeys.push_back(kv.first);
   std::sort(bkeys.begin(), bkeys.end());
@@ -2849,6 +2899,7 @@ int dg_backward(dg_graph* g, int32_t loss) {
     });
     plan.tag(C_COLSUM, 0.0, 4.0 * nr * width + 8.0 * width);
   }
+  tm.lap("colsum");
   // lookup flush: sorted segmented scatter-add per table (graph.py:57-63)
   {
     struct Rows {
@@ -2898,7 +2949,7 @@ int dg_backward(dg_graph* g, int32_t loss) {
       plan.tag(C_SCATTER, 0.0, 4.0 * dim * ((double)src.size() + 2.0 * nu));
     }
   }
-  tm.lap("dW+colsum+scatter");
+  tm.lap("scatter");
   rc = launch_plan(g, plan);
   if (rc) return rc;
   tm.lap("launch");

@@ -673,6 +673,31 @@ __device__ __forceinline__ void mbar_wait_cl(uint64_t* b, uint32_t parity) {
     if (!done && ++spins > (1u << 24)) __trap();
   }
 }
+// remote store that completes `bytes` of a transaction on the destination
+// CTA's mbarrier: no fence / barrier needed on the producer side
+__device__ __forceinline__ void st_async_f32(uint32_t remote_addr, float v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(remote_addr), "f"(v),
+               "r"(remote_bar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_v4(uint32_t remote_addr, float4 v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   remote_addr),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(remote_bar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t remote_addr, float2 v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(remote_addr),
+               "f"(v.x), "f"(v.y), "r"(remote_bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -698,117 +723,122 @@ __device__ __forceinline__ void signal_loop(int* done, int* flags, int T, bool r
   }
 }
 
+// 3xTF32 legacy-MMA tile op: acc(16 x 8) += A(16 x 8) B(8 x 8); a/b hold fp32
+// bit patterns, the residuals lo = x - tf32(x) make A_hi B_hi + A_hi B_lo +
+// A_lo B_hi (fp32-accurate products, as the tcgen05 GEMMs)
+__device__ __forceinline__ uint32_t tf32_hi(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
+__device__ __forceinline__ uint32_t tf32_lo(float x) {
+  return __float_as_uint(x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u));
+}
+__device__ __forceinline__ void mma_1688(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma3(float* c, const float* a, float4 b) {
+  // b = {b0_hi, b1_hi, b0_lo, b1_lo} (pre-split weights)
+  uint32_t ah[4], al[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    ah[q] = tf32_hi(a[q]);
+    al[q] = tf32_lo(a[q]);
+  }
+  const uint32_t bh0 = __float_as_uint(b.x), bh1 = __float_as_uint(b.y);
+  mma_1688(c, al, bh0, bh1);
+  mma_1688(c, ah, __float_as_uint(b.z), __float_as_uint(b.w));
+  mma_1688(c, ah, bh0, bh1);
+}
+
+// Forward recurrence (gx mode: G slots hold b + Wx x_t): per step the CTA
+// computes G_rec[16 rows x 64 gate columns] = h_{t-1}[rows, :] Wh^T[:, cols]
+// on the tensor cores (warp w owns columns 8w..8w+7, 3xTF32 mma.sync over K =
+// H), adds Gx, runs the cell and pushes its 16-unit slice of h_t to the
+// cluster through distributed shared memory.
 template <int BS>
 __global__ void __launch_bounds__(kClThreads, 1) rnn_fwd_cl_kernel(const __grid_constant__ RnnArgs a) {
   extern __shared__ float4 smem4[];
   float* sm = reinterpret_cast<float*>(smem4);
   __shared__ StepPtrs sp[2];
-  __shared__ __align__(8) uint64_t h_ready[2];
-  __shared__ int done_steps;
+  __shared__ __align__(8) uint64_t h_full[2];  // h_u lands in buffer u&1 (st.async transactions)
   const int ci = chain_of(a, blockIdx.x);
   const RnnChain C = a.ch[ci];  // register copy (dynamic-index constant loads are slow)
   const int local = blockIdx.x - C.cta0;
   const int s = local / C.n_u, ub = local - (local / C.n_u) * C.n_u;
   const int b0 = s * BS, j0 = ub * kU;
-  const int K = C.K_in + C.H;
-  const int XP = C.K_in + 4, HP = C.H + 4;  // padded row strides
-  float* Ws = sm;                               // [K][64]
-  float* xS = Ws + (size_t)K * kCU;             // [BS][K_in+4]
-  float* hS = xS + (size_t)BS * XP;             // [2][BS][H+4]
-  float* part = hS + 2 * (size_t)BS * HP;       // [8][BS][64]
-  float* bias = part + 8 * BS * kCU;            // [64]
+  const int KS = (C.H + 7) / 8;                 // k-steps of 8 over the recurrent input
+  const int HP = 8 * KS + 4;                    // padded row stride: k-steps never leave the row
+  float4* Bf = reinterpret_cast<float4*>(sm);   // [KS][8 warps][32 lanes] weight fragments (hi, lo)
+  float* hS = sm + (size_t)KS * 8 * 32 * 4;     // [2][BS][HP]
+  float* gS = hS + 2 * (size_t)BS * HP;         // [BS][64 + 4] recurrent gate sums
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int goff[4] = {C.off_i, C.off_f, C.off_o, C.off_g};
-  const bool signals = C.cons >= 0;  // a stacked chain reads h_t from global memory
+  const int g8 = lane >> 2, t4 = lane & 3;      // mma fragment coordinates
   if (a.trace && tid == 0) trace(0, 0);
 
   if (warp < 8) {
-    for (int idx = tid; idx < K * (kCU / 4); idx += kRT) {
-      const int k = idx / (kCU / 4), q = idx - k * (kCU / 4);
-      const int gate = q / (kU / 4), j = j0 + 4 * (q - gate * (kU / 4));
-      float* dst = Ws + (size_t)k * kCU + 4 * q;
-      if (j < C.H) {
-        const int64_t row = goff[gate] + j;
-        cp_async16(dst, k < C.K_in ? C.Wx + row + (int64_t)k * C.gw : C.Wh + row + (int64_t)(k - C.K_in) * C.gw);
-      } else {
-        *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+    // weight fragments: warp w, k-step q, lane (g, t): b0 = B(8q + t, 8w + g),
+    // b1 = B(8q + t + 4, 8w + g), B(k, n) = Wh[row(n) + k * gw] (n = gate * 16 + jj);
+    // loaded coalesced along n and scattered into the fragment layout
+    float* Bff = reinterpret_cast<float*>(Bf);
+    constexpr int kBatch = 8;  // loads in flight per thread
+    for (int idx0 = tid; idx0 < 8 * KS * kCU; idx0 += kBatch * kRT) {
+      float v[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int idx = idx0 + u * kRT;
+        const int k = idx / kCU, n = idx - (idx / kCU) * kCU;
+        const int gate = n / kU, j = j0 + (n - gate * kU);
+        v[u] = (idx < 8 * KS * kCU && j < C.H && k < C.H) ? __ldg(C.Wh + goff[gate] + j + (int64_t)k * C.gw) : 0.f;
       }
-    }
-    if (tid < kCU) {
-      const int gate = tid / kU, j = j0 + (tid - gate * kU);
-      bias[tid] = j < C.H ? C.bias[goff[gate] + j] : 0.f;
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int idx = idx0 + u * kRT;
+        if (idx >= 8 * KS * kCU) break;
+        const int k = idx / kCU, n = idx - (idx / kCU) * kCU;
+        const int q = k >> 3, kk = k & 7, w = n >> 3, l = ((n & 7) << 2) | (kk & 3), half = kk >> 2;
+        float* f = Bff + ((size_t)(q * 8 + w) * 32 + l) * 4;
+        f[half] = __uint_as_float(tf32_hi(v[u]));
+        f[2 + half] = __uint_as_float(tf32_lo(v[u]));
+      }
     }
     if (tid < kRnnSlots) sp[0].p[tid] = C.val[tid];
     if (tid == kRnnSlots) sp[0].b1 = C.b1[0];
-    // h_{-1} (external state) into h buffer 1
-    {
-      const int fl = C.b1[0];
-      const float* Hp = C.val[S_HP];
-      const int w4 = C.H >> 2;
-      for (int idx = tid; idx < BS * w4; idx += kRT) {
-        const int b = idx / w4, q = idx - (idx / w4) * w4;
-        const int row = b0 + b;
-        float* dst = hS + (size_t)BS * HP + (size_t)b * HP + 4 * q;
-        if (row < C.B) cp_async16(dst, Hp + ((fl & 2) ? 0 : (int64_t)row * C.H) + 4 * q);
-        else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    }
+    // h buffers: zero (padding columns stay zero), then h_{-1} into buffer 1
+    for (int idx = tid; idx < 2 * BS * HP; idx += kRT) hS[idx] = 0.f;
     if (tid == 0) {
-      done_steps = 0;
-      mbar_init_cl(&h_ready[0], C.n_u);
-      mbar_init_cl(&h_ready[1], C.n_u);
+      // every (row, unit) of a slice is pushed by its owner once per step
+      const uint32_t bytes = (uint32_t)(BS * C.H * 4);
+      mbar_init_cl(&h_full[0], 1);
+      mbar_init_cl(&h_full[1], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      if (C.T > 1) mbar_arm(&h_full[0], bytes);  // h_0
+      if (C.T > 2) mbar_arm(&h_full[1], bytes);  // h_1
+    }
+  }
+  __syncthreads();
+  if (warp < 8) {
+    const int fl = C.b1[0];
+    const float* Hp = C.val[S_HP];
+    const int w4 = C.H >> 2;
+    for (int idx = tid; idx < BS * w4; idx += kRT) {
+      const int b = idx / w4, q = idx - (idx / w4) * w4;
+      const int row = b0 + b;
+      if (row < C.B) cp_async16(hS + (size_t)BS * HP + (size_t)b * HP + 4 * q, Hp + ((fl & 2) ? 0 : (int64_t)row * C.H) + 4 * q);
     }
     cp_async_wait_all();
   }
   __syncthreads();
-  cluster_sync_all();  // every peer's barriers exist before any remote arrive
+  cluster_sync_all();  // every peer is resident and initialised before any DSMEM push
   if (a.trace && tid == 0) trace(0, 1);
+  if (warp == 8) return;  // no cross-chain signalling in gx mode
 
-  int* my_flags = a.flags + C.flag0 + s * C.T;
-  if (warp == 8) {
-    // signalling warp: publish h_t to the stacked consumer chain
-    if (signals && lane == 0) signal_loop(&done_steps, my_flags, C.T, false);
-    return;
-  }
-  const int* src_flags = nullptr;
-  int src_need = 0;
-  if (C.src >= 0) {
-    const RnnChain& Pc = a.ch[C.src];
-    src_flags = a.flags + Pc.flag0 + s * Pc.T;
-    src_need = Pc.n_u;
-  }
-  constexpr int LB = BS < 4 ? BS : 4;
-  constexpr int TB = BS / LB;
-  constexpr int LC = 32 / LB;
-  constexpr int TC = kCU / LC;
-  const int lb = lane / LC, lc = lane - (lane / LC) * LC;
   const int cb = tid / kU, cj = tid - (tid / kU) * kU;
   const int crow = b0 + cb, cjj = j0 + cj;
   const bool cell_mine = cb < BS && crow < C.B && cjj < C.H;
-  const bool cell_row = cb < BS;  // pushes zeros for padded rows / units too
+  const bool cell_row = cb < BS;
   float c_carry = 0.f;
-  // remote addresses of this thread's h element in every peer's two h buffers
   const uint32_t h_local0 = smem_addr(hS + (size_t)(cb < BS ? cb : 0) * HP + cjj);
-  const uint32_t hr_local = smem_addr(&h_ready[0]);
-  float acc[TB][TC];
-  auto fma_block = [&](const float* rows, int ld, int wk0, int k_lo, int k_hi) {
-    // acc += rows[:, k_lo:k_hi] (row stride ld, column offset k - k_lo) * Ws[wk0 + k]
-    const int per = (k_hi - k_lo + 7) / 8;
-    const int kb = k_lo + warp * per, ke = min(k_hi, kb + per);
-#pragma unroll 4
-    for (int k = kb; k < ke; ++k) {
-      float xa[TB], wv[TC];
-#pragma unroll
-      for (int i = 0; i < TB; ++i) xa[i] = rows[(size_t)(i * LB + lb) * ld + k];
-#pragma unroll
-      for (int c = 0; c < TC; ++c) wv[c] = Ws[(size_t)(wk0 + k) * kCU + lane_col<LC, TC>(lc, c)];
-#pragma unroll
-      for (int i = 0; i < TB; ++i)
-#pragma unroll
-        for (int c = 0; c < TC; ++c) acc[i][c] = fmaf(xa[i], wv[c], acc[i][c]);
-    }
-  };
 
   for (int t = 0; t < C.T; ++t) {
     const StepPtrs& P = sp[t & 1];
@@ -820,58 +850,69 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_fwd_cl_kernel(const __grid_
     }
     const int fl = P.b1;
     if (t == 0 && cell_mine) c_carry = __ldcg(P.p[S_CP] + ((fl & 4) ? cjj : (int64_t)crow * C.H + cjj));
-    // gx mode: the G slot already holds b + Wx x_t (batched tensor-core GEMM
-    // before this launch); read it ahead of the waits
     float gx[4] = {0.f, 0.f, 0.f, 0.f};
-    if (a.gx && cell_mine) {
+    if (cell_mine) {
       const float* Gr = P.p[S_G] + (int64_t)crow * C.gw;
       gx[0] = Gr[C.off_i + cjj];
       gx[1] = Gr[C.off_f + cjj];
       gx[2] = Gr[C.off_o + cjj];
       gx[3] = Gr[C.off_g + cjj];
     }
-#pragma unroll
-    for (int i = 0; i < TB; ++i)
-#pragma unroll
-      for (int c = 0; c < TC; ++c) acc[i][c] = 0.f;
-    // input part (x_t): external or the producer chain's step t (gx mode: none)
-    if (C.K_in > 0) {
-    if (tid == 0 && src_flags) wait_count(src_flags + t, src_need);
-    csync();
+    if (a.trace == 2 && tid == 0) trace(0, 64 + 4 * t);
+    if (t > 0) {
+      // h_{t-1}: buffer (t-1)&1, phase (t-1)>>1; then re-arm it for h_{t+1}
+      mbar_wait_cl(&h_full[(t - 1) & 1], ((t - 1) >> 1) & 1);
+      if (tid == 0 && t + 2 < C.T) mbar_arm(&h_full[(t - 1) & 1], (uint32_t)(BS * C.H * 4));
+    }
+    if (a.trace == 2 && tid == 0) trace(0, 64 + 4 * t + 1);
     {
-      const float* X = P.p[S_X];
-      const int w4 = C.K_in >> 2;
-      for (int idx = tid; idx < BS * w4; idx += kRT) {
-        const int b = idx / w4, q = idx - (idx / w4) * w4;
-        const int row = b0 + b;
-        float* dst = xS + (size_t)b * XP + 4 * q;
-        if (row < C.B) cp_async16(dst, X + ((fl & 1) ? 0 : (int64_t)row * C.K_in) + 4 * q);
-        else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      const float* hb = hS + (size_t)((t - 1) & 1) * BS * HP;
+      const float* r0 = hb + (size_t)g8 * HP;
+      const float* r1 = hb + (size_t)(g8 + 8) * HP;
+      const bool v0 = g8 < BS, v1 = g8 + 8 < BS;
+      // six independent accumulator chains (3 products x even/odd k-steps)
+      float ac[6][4];
+#pragma unroll
+      for (int z = 0; z < 6; ++z) ac[z][0] = ac[z][1] = ac[z][2] = ac[z][3] = 0.f;
+      const float4* bw = Bf + warp * 32 + lane;
+#pragma unroll 2
+      for (int q = 0; q < KS; ++q) {
+        const int k = 8 * q + t4;
+        float av[4];
+        av[0] = v0 ? r0[k] : 0.f;
+        av[1] = v1 ? r1[k] : 0.f;
+        av[2] = v0 ? r0[k + 4] : 0.f;
+        av[3] = v1 ? r1[k + 4] : 0.f;
+        const float4 b = bw[(size_t)q * 256];
+        uint32_t ah[4], al[4];
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+          ah[z] = tf32_hi(av[z]);
+          al[z] = tf32_lo(av[z]);
+        }
+        float* c3 = ac[(q & 1) * 3];
+        mma_1688(c3, al, __float_as_uint(b.x), __float_as_uint(b.y));
+        mma_1688(c3 + 4, ah, __float_as_uint(b.z), __float_as_uint(b.w));
+        mma_1688(c3 + 8, ah, __float_as_uint(b.x), __float_as_uint(b.y));
       }
-      cp_async_wait_all();
+      float acc[4];
+#pragma unroll
+      for (int z = 0; z < 4; ++z)
+        acc[z] = ((ac[0][z] + ac[3][z]) + (ac[1][z] + ac[4][z])) + (ac[2][z] + ac[5][z]);
+      // C fragment: rows g8 / g8+8, columns 8w + 2 t4 (+1)
+      float* o0 = gS + (size_t)g8 * (kCU + 4) + 8 * warp + 2 * t4;
+      if (v0) *reinterpret_cast<float2*>(o0) = make_float2(acc[0], acc[1]);
+      if (v1) *reinterpret_cast<float2*>(o0 + 8 * (kCU + 4)) = make_float2(acc[2], acc[3]);
     }
     csync();
-    fma_block(xS, XP, 0, 0, C.K_in);
-    }
-    // recurrent part: h_{t-1} pushed by every CTA of the cluster
-    if (t > 0) mbar_wait_cl(&h_ready[(t - 1) & 1], ((t - 1) >> 1) & 1);
-    fma_block(hS + (size_t)((t - 1) & 1) * BS * HP, HP, C.K_in, 0, C.H);
-#pragma unroll
-    for (int i = 0; i < TB; ++i)
-#pragma unroll
-      for (int c = 0; c < TC; ++c) part[(warp * BS + i * LB + lb) * kCU + lane_col<LC, TC>(lc, c)] = acc[i][c];
-    csync();
+    if (a.trace == 2 && tid == 0) trace(0, 64 + 4 * t + 2);
     float x4[4] = {0.f, 0.f, 0.f, 0.f}, ai = 0.f, af = 0.f, ao = 0.f, ag = 0.f, ig = 0.f, p = 0.f, c = 0.f, tc = 0.f;
     float h = 0.f;
     const int64_t r = (int64_t)crow * C.H + cjj;
     if (cell_mine) {
+      const float* gr = gS + (size_t)cb * (kCU + 4) + cj;
 #pragma unroll
-      for (int gate = 0; gate < 4; ++gate) {
-        float sum = 0.f;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) sum += part[(w * BS + cb) * kCU + gate * kU + cj];
-        x4[gate] = (a.gx ? gx[gate] : bias[gate * kU + cj]) + sum;
-      }
+      for (int gate = 0; gate < 4; ++gate) x4[gate] = gx[gate] + gr[gate * kU];
       ai = sigmoid_ref(x4[0]);
       af = sigmoid_ref(x4[1]);
       ao = sigmoid_ref(x4[2]);
@@ -883,19 +924,20 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_fwd_cl_kernel(const __grid_
       tc = tanhf(c);
       h = ao * tc;
     }
+    if (a.trace == 2 && tid == 0) trace(0, 64 + 4 * t + 3);
     if (t + 1 < C.T) {
-      // push h_t into buffer t&1 of every CTA of the cluster (padded lanes push zeros)
+      // push h_t into buffer t&1 of every CTA of the cluster
       if (cell_row && cjj < C.H) {
         const uint32_t la = h_local0 + (uint32_t)((t & 1) * BS * HP * 4);
-        for (int q = 0; q < C.n_u; ++q) st_cluster(mapa(la, q), h);
+        const uint32_t lb = smem_addr(&h_full[t & 1]);
+        for (int q = 0; q < C.n_u; ++q) st_async_f32(mapa(la, q), h, mapa(lb, q));
       }
-      if (warp == 1) {
-        if (lane < kRnnSlots) sp[(t + 1) & 1].p[lane] = nxt;
-        if (lane == kRnnSlots) sp[(t + 1) & 1].b1 = nxt_b1;
-      }
-      csync();
-      if (tid < C.n_u) mbar_arrive_remote(mapa(hr_local + 8 * (t & 1), tid));
     }
+    if (warp == 1 && t + 1 < C.T) {
+      if (lane < kRnnSlots) sp[(t + 1) & 1].p[lane] = nxt;
+      if (lane == kRnnSlots) sp[(t + 1) & 1].b1 = nxt_b1;
+    }
+    csync();  // sp of step t+1 published; gS free for reuse
     if (a.trace && tid == 0) trace(0, 2 + t);
     if (cell_mine) {
       const_cast<float*>(P.p[S_H])[r] = h;
@@ -918,54 +960,60 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_fwd_cl_kernel(const __grid_
       W(S_C, c);
       W(S_TC, tc);
     }
-    if (signals) {
-      csync();
-      if (tid == 0) st_release_cta(&done_steps, t + 1);
-    }
   }
 }
 
+// Backward recurrence (no stacked consumer: the layer above's dX is a batched
+// GEMM): per step the cell backward of this CTA's (16 rows x 16 units), then
+// the reduce-scatter dh_{t-1}[rows, all units] = dG_t[rows, own 64 gate cols]
+// Wh[own cols, :] on the tensor cores (warp w owns unit tiles 4w..4w+3 of 8,
+// 3xTF32 mma.sync, K = 64), each partial pushed to the unit owner's slot with
+// st.async (transaction bytes on the owner's mbarrier); the owner sums the n_u
+// slots in rank order (deterministic).
 template <int BS>
 __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_constant__ RnnArgs a) {
   extern __shared__ float4 smem4[];
   float* sm = reinterpret_cast<float*>(smem4);
   __shared__ StepPtrs2 sp[2];
-  __shared__ __align__(8) uint64_t rec_ready[2];
-  __shared__ int done_steps;
+  __shared__ __align__(8) uint64_t rec_full[2];
   const int ci = chain_of(a, blockIdx.x);
   const RnnChain C = a.ch[ci];  // register copy (dynamic-index constant loads are slow)
   const int local = blockIdx.x - C.cta0;
   const int s = local / C.n_u, ub = local - (local / C.n_u) * C.n_u;
   const int b0 = s * BS, j0 = ub * kU;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const RnnChain* Cc = C.cons >= 0 ? &a.ch[C.cons] : nullptr;
-  const int gw_c = Cc ? Cc->gw : 0;
   const int HU = C.n_u * kU;                    // units covered by the cluster (>= H)
+  const int NT = HU / 8;                        // unit tiles of 8
   const int goff[4] = {C.off_i, C.off_f, C.off_o, C.off_g};
-  float* WhS = sm;                              // [64 own gate rows][HU units]
-  float* WcT = WhS + (size_t)kCU * HU;          // [gw_c][16]
-  float* dGs = WcT + (size_t)gw_c * kU;         // [BS][CJ+4] (consumer dG staging)
-  float* part = dGs + (size_t)(a.cj + 4) * BS;  // [8][BS][16]
-  float* dGl = part + 8 * BS * kU;              // [BS][64+4] own gate gradients
+  float4* Bf = reinterpret_cast<float4*>(sm);   // [NT][8 k-steps][32 lanes] Wh fragments (hi, lo)
+  float* dGl = sm + (size_t)NT * 8 * 32 * 4;    // [BS][64 + 4] own gate gradients (A operand)
   float* recv = dGl + (size_t)BS * (kCU + 4);   // [2][n_u][BS][16] reduce-scatter slots
-  const bool signals = C.src >= 0;              // the producer chain reads dG_t from global memory
+  const uint32_t slot_bytes = (uint32_t)(C.n_u * BS * kU * 4);
   if (a.trace && tid == 0) trace(1, 0);
 
   if (warp < 8) {
-    // WhS[r][u] = Wh[goff[gate] + j0 + jj, u] = Wh[row + u * gw]  (r = gate * 16 + jj)
-    for (int idx = tid; idx < kCU * HU; idx += kRT) {
-      const int u = idx / kCU, rr = idx - u * kCU;
-      const int gate = rr / kU, j = j0 + (rr - gate * kU);
-      float* dst = WhS + (size_t)rr * HU + u;
-      if (j < C.H && u < C.H) cp_async4(dst, C.Wh + goff[gate] + j + (int64_t)u * C.gw);
-      else *dst = 0.f;
-    }
-    if (Cc) {
-      for (int idx = tid; idx < gw_c * kU; idx += kRT) {
-        const int u = idx / gw_c, j = idx - (idx / gw_c) * gw_c;
-        float* dst = WcT + (size_t)j * kU + u;
-        if (j0 + u < C.H) cp_async4(dst, Cc->Wx + j + (int64_t)(j0 + u) * gw_c);
-        else *dst = 0.f;
+    // B(k, n) = Wh[row(k) + n * gw], k = own gate column (gate * 16 + jj), n = unit;
+    // fragment (nt, q, lane = g*4 + t): b0 = B(8q + t, 8nt + g), b1 = B(8q + t + 4, 8nt + g)
+    float* Bff = reinterpret_cast<float*>(Bf);
+    constexpr int kBatch = 16;
+    for (int idx0 = tid; idx0 < kCU * HU; idx0 += kBatch * kRT) {
+      float v[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int idx = idx0 + u * kRT;
+        const int n = idx / kCU, k = idx - (idx / kCU) * kCU;  // consecutive threads: consecutive k
+        const int gate = k / kU, jj = j0 + (k - gate * kU);
+        v[u] = (idx < kCU * HU && jj < C.H && n < C.H) ? __ldg(C.Wh + goff[gate] + jj + (int64_t)n * C.gw) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int idx = idx0 + u * kRT;
+        if (idx >= kCU * HU) break;
+        const int n = idx / kCU, k = idx - (idx / kCU) * kCU;
+        const int nt = n >> 3, q = k >> 3, kk = k & 7, l = ((n & 7) << 2) | (kk & 3), half = kk >> 2;
+        float* f = Bff + ((size_t)(nt * 8 + q) * 32 + l) * 4;
+        f[half] = __uint_as_float(tf32_hi(v[u]));
+        f[2 + half] = __uint_as_float(tf32_lo(v[u]));
       }
     }
     {
@@ -974,32 +1022,29 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
       if (tid >= 32 && tid < 32 + kRnnSlots) sp[t & 1].d[tid - 32] = C.grad[(size_t)t * kRnnSlots + tid - 32];
       if (tid == 64) sp[t & 1].b1 = C.b1[t];
     }
+    for (int idx = tid; idx < BS * (kCU + 4); idx += kRT) dGl[idx] = 0.f;
     if (tid == 0) {
-      done_steps = 0;
-      mbar_init_cl(&rec_ready[0], C.n_u);
-      mbar_init_cl(&rec_ready[1], C.n_u);
+      mbar_init_cl(&rec_full[0], 1);
+      mbar_init_cl(&rec_full[1], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      if (C.T > 1) mbar_arm(&rec_full[0], slot_bytes);  // iteration 0
+      if (C.T > 2) mbar_arm(&rec_full[1], slot_bytes);  // iteration 1
     }
-    cp_async_wait_all();
   }
   __syncthreads();
   cluster_sync_all();
   if (a.trace && tid == 0) trace(1, 1);
+  if (warp == 8) return;
 
-  int* my_flags = a.flags + C.flag0 + s * C.T;
-  if (warp == 8) {
-    if (signals && lane == 0) signal_loop(&done_steps, my_flags, C.T, true);
-    return;
-  }
-  const int* cons_flags = Cc ? a.flags + Cc->flag0 + s * Cc->T : nullptr;
   const int cb = tid / kU, cj = tid - (tid / kU) * kU;
   const int row = b0 + cb, j = j0 + cj;
   const bool mine = cb < BS && row < C.B && j < C.H;
   const int64_t r = (int64_t)row * C.H + j;
   const uint32_t my_rank = cluster_rank();
   const uint32_t recv_local = smem_addr(recv);
-  const uint32_t rr_local = smem_addr(&rec_ready[0]);
-  float rec = 0.f, cons = 0.f, dc_carry = 0.f;
+  const uint32_t bar_local = smem_addr(&rec_full[0]);
+  const int g8 = lane >> 2, t4 = lane & 3;
+  float rec = 0.f, dc_carry = 0.f;
   float ao = 0.f, ai = 0.f, ag = 0.f, tc = 0.f, af = 0.f, ck = 0.f, gh_ext = 0.f, gc_ext = 0.f;
   auto load_cell = [&](const StepPtrs2& P) {
     if (!mine) return;
@@ -1014,18 +1059,6 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
     gc_ext = P.d[S_C][r];
   };
   load_cell(sp[(C.T - 1) & 1]);
-  if (Cc) {
-    if (tid == 0) wait_count(cons_flags + C.T - 1, Cc->n_u);
-    csync();
-    cons = rows_times_wt<BS>(Cc->grad[(size_t)(C.T - 1) * kRnnSlots + S_G], gw_c, C.B, b0, WcT, dGs, a.cj, part,
-                             a.vec);
-  }
-  // reduce-scatter tiling: thread (rg, ug) -> rows 4rg..4rg+3 (of BS), units 4ug..4ug+3 (of HU)
-  constexpr int RG = BS < 4 ? 1 : BS / 4;       // row groups
-  constexpr int RPT = BS < 4 ? BS : 4;           // rows per thread
-  const int UG = HU / 4;                          // unit groups (<= 64)
-  const int rg = tid / UG, ug = tid - (tid / UG) * UG;
-  const bool rs_active = rg < RG;
 
   for (int t = C.T - 1, it = 0; t >= 0; --t, ++it) {
     const StepPtrs2& P = sp[t & 1];
@@ -1043,7 +1076,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
     float gh = 0.f, d_tc = 0.f, d_o = 0.f, dc = 0.f, d_i = 0.f, d_g = 0.f, dpi = 0.f, dpo = 0.f, dpg = 0.f;
     float d_f = 0.f, dpf = 0.f;
     if (mine) {
-      gh = gh_ext + rec + cons;
+      gh = gh_ext + rec;
       d_tc = gh * ao;
       d_o = gh * tc;
       dc = (gc_ext + dc_carry) + (1.f - tc * tc) * d_tc;
@@ -1057,7 +1090,6 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
       dc_carry = dc * af;
     }
     if (t > 0) {
-      // own gate gradients (zero for padded rows / units) as the local operand
       if (cb < BS) {
         float* dl = dGl + (size_t)cb * (kCU + 4);
         dl[0 * kU + cj] = dpi;
@@ -1066,30 +1098,44 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
         dl[3 * kU + cj] = dpg;
       }
       csync();
-      // partial dh_{t-1}[rows, all units] from this CTA's 64 gate columns
-      if (rs_active) {
-        float acc4[RPT][4];
+      {
+        const float* r0 = dGl + (size_t)g8 * (kCU + 4);
+        const float* r1 = dGl + (size_t)(g8 + 8) * (kCU + 4);
+        const bool v0 = g8 < BS, v1 = g8 + 8 < BS;
+        uint32_t ah[8][4], al[8][4];
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) acc4[i][0] = acc4[i][1] = acc4[i][2] = acc4[i][3] = 0.f;
-#pragma unroll 4
-        for (int k = 0; k < kCU; ++k) {
-          const float4 w = *reinterpret_cast<const float4*>(WhS + (size_t)k * HU + 4 * ug);
+        for (int q = 0; q < 8; ++q) {
+          const int k = 8 * q + t4;
+          const float av[4] = {v0 ? r0[k] : 0.f, v1 ? r1[k] : 0.f, v0 ? r0[k + 4] : 0.f, v1 ? r1[k + 4] : 0.f};
 #pragma unroll
-          for (int i = 0; i < RPT; ++i) {
-            const float g = dGl[(size_t)(rg * RPT + i) * (kCU + 4) + k];
-            acc4[i][0] = fmaf(g, w.x, acc4[i][0]);
-            acc4[i][1] = fmaf(g, w.y, acc4[i][1]);
-            acc4[i][2] = fmaf(g, w.z, acc4[i][2]);
-            acc4[i][3] = fmaf(g, w.w, acc4[i][3]);
+          for (int z = 0; z < 4; ++z) {
+            ah[q][z] = tf32_hi(av[z]);
+            al[q][z] = tf32_lo(av[z]);
           }
         }
-        // push into slot [my_rank] of the unit owner's buffer it&1
-        const int owner = (4 * ug) / kU, uo = (4 * ug) % kU;
-        const uint32_t base = recv_local + 4u * (uint32_t)(((it & 1) * C.n_u + (int)my_rank) * BS * kU);
+        const uint32_t rbase = recv_local + 4u * (uint32_t)(((it & 1) * C.n_u + (int)my_rank) * BS * kU);
+        for (int nt = warp; nt < NT; nt += 8) {
+          float ac[3][4];
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-          const uint32_t la = base + 4u * (uint32_t)((rg * RPT + i) * kU + uo);
-          st_cluster4(mapa(la, owner), make_float4(acc4[i][0], acc4[i][1], acc4[i][2], acc4[i][3]));
+          for (int z = 0; z < 3; ++z) ac[z][0] = ac[z][1] = ac[z][2] = ac[z][3] = 0.f;
+          const float4* bw = Bf + (size_t)nt * 256 + lane;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 b = bw[q * 32];
+            mma_1688(ac[0], al[q], __float_as_uint(b.x), __float_as_uint(b.y));
+            mma_1688(ac[1], ah[q], __float_as_uint(b.z), __float_as_uint(b.w));
+            mma_1688(ac[2], ah[q], __float_as_uint(b.x), __float_as_uint(b.y));
+          }
+          // C fragment rows g8 / g8+8, units 8nt + 2t4 (+1) -> owner slot [my_rank]
+          const int u0 = 8 * nt + 2 * t4;
+          const int owner = u0 / kU, uo = u0 - owner * kU;
+          const uint32_t rb = mapa(bar_local + 8 * (it & 1), owner);
+          if (v0)
+            st_async_v2(mapa(rbase + 4u * (uint32_t)(g8 * kU + uo), owner),
+                        make_float2(ac[0][0] + ac[1][0] + ac[2][0], ac[0][1] + ac[1][1] + ac[2][1]), rb);
+          if (v1)
+            st_async_v2(mapa(rbase + 4u * (uint32_t)((g8 + 8) * kU + uo), owner),
+                        make_float2(ac[0][2] + ac[1][2] + ac[2][2], ac[0][3] + ac[1][3] + ac[2][3]), rb);
         }
       }
       if (warp == 1) {
@@ -1099,8 +1145,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
         }
         if (lane == kRnnSlots) sp[(t - 1) & 1].b1 = nb1;
       }
-      csync();
-      if (tid < C.n_u) mbar_arrive_remote(mapa(rr_local + 8 * (it & 1), tid));
+      csync();  // sp of step t-1 published; dGl free for reuse
     }
     if (a.trace && tid == 0) trace(1, 2 + t);
     if (mine) {
@@ -1125,19 +1170,10 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
       D[S_PF][r] = dpf;
       if (t == 0 && !cb1) D[S_CP][r] += dc_carry;
     }
-    if (signals) {
-      csync();
-      if (tid == 0) st_release_cta(&done_steps, it + 1);
-    }
     if (t > 0) {
       load_cell(sp[(t - 1) & 1]);
-      if (Cc) {
-        if (tid == 0) wait_count(cons_flags + t - 1, Cc->n_u);
-        csync();
-        cons = rows_times_wt<BS>(Cc->grad[(size_t)(t - 1) * kRnnSlots + S_G], gw_c, C.B, b0, WcT, dGs, a.cj, part,
-                                 a.vec);
-      }
-      mbar_wait_cl(&rec_ready[it & 1], (it >> 1) & 1);
+      mbar_wait_cl(&rec_full[it & 1], (it >> 1) & 1);
+      if (tid == 0 && it + 2 <= C.T - 2) mbar_arm(&rec_full[it & 1], slot_bytes);
       rec = 0.f;
       if (cb < BS) {
         const float* slot = recv + (size_t)(it & 1) * C.n_u * BS * kU + (size_t)cb * kU + cj;
@@ -1149,14 +1185,25 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
 
 // dst[u] += sum_b dc0[b][u] * af0[b][u]  (batch-1 c_{-1} of each listed chain)
 __global__ void rnn_c0_kernel(RnnC0 a) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  // block = (chain k, 32 units); 8 warps split the batch, fixed-order reduce
+  __shared__ float red[8][32];
   int k = 0, base = 0;
-  while (k < a.n && q >= base + a.H[k]) base += a.H[k++];
+  const int blk = blockIdx.x;
+  while (k < a.n && blk >= base + (a.H[k] + 31) / 32) base += (a.H[k++] + 31) / 32;
   if (k >= a.n) return;
-  const int u = q - base;
+  const int u = (blk - base) * 32 + (threadIdx.x & 31), w = threadIdx.x >> 5;
+  const int H = a.H[k], B = a.B[k];
   float s = 0.f;
-  for (int b = 0; b < a.B[k]; ++b) s += a.dc[k][(int64_t)b * a.H[k] + u] * a.af[k][(int64_t)b * a.H[k] + u];
-  a.dst[k][u] += s;
+  if (u < H)
+    for (int b = w; b < B; b += 8) s += a.dc[k][(int64_t)b * H + u] * a.af[k][(int64_t)b * H + u];
+  red[w][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (w == 0 && u < H) {
+    float t = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += red[q][threadIdx.x];
+    a.dst[k][u] += t;
+  }
 }
 
 // per-kernel one-time attribute setup: the dynamic shared memory limit is
@@ -1254,15 +1301,17 @@ int launch_cl_bs(const RnnArgs& a, bool bwd, size_t smem, int cluster, cudaStrea
 }  // namespace
 
 size_t rnn_fwd_cl_smem(int K_in, int H, int bs) {
-  const int K = K_in + H;
-  return 4 * ((size_t)K * kCU + (size_t)bs * (K_in + 4) + 2 * (size_t)bs * (H + 4) + 8 * (size_t)bs * kCU + kCU);
+  (void)K_in;  // gx mode: recurrent input only
+  const int KS = (H + 7) / 8;
+  return 4 * ((size_t)KS * 8 * 32 * 4 + 2 * (size_t)bs * (8 * KS + 4) + (size_t)bs * (kCU + 4));
 }
 
 size_t rnn_bwd_cl_smem(int H, int gw_c, int bs, int cj) {
+  (void)gw_c;  // no stacked consumer in the cluster kernel
+  (void)cj;
   const int HU = (H + kU - 1) / kU * kU;
   const int nu = HU / kU;
-  return 4 * ((size_t)kCU * HU + (size_t)gw_c * kU + (size_t)(cj + 4) * bs + 8 * (size_t)bs * kU +
-              (size_t)bs * (kCU + 4) + 2 * (size_t)nu * bs * kU);
+  return 4 * ((size_t)(HU / 8) * 8 * 32 * 4 + (size_t)bs * (kCU + 4) + 2 * (size_t)nu * bs * kU);
 }
 
 int rnn_rows_per_cta(int B) { return B >= 16 ? 16 : B >= 8 ? 8 : B >= 4 ? 4 : B >= 2 ? 2 : 1; }
@@ -1286,7 +1335,10 @@ bool rnn_enabled() {
 }
 
 int launch_rnn_cluster(const RnnArgs& a, bool backward, size_t smem, int cluster, cudaStream_t s) {
-  if (cudaMemsetAsync(a.flags, 0, (size_t)a.n_flags * sizeof(int), s) != cudaSuccess) return -1;
+  // global arrival counters only carry cross-chain (stacked) dependencies here
+  bool cross = false;
+  for (int k = 0; k < a.n_chains; ++k) cross = cross || a.ch[k].src >= 0 || a.ch[k].cons >= 0;
+  if (cross && cudaMemsetAsync(a.flags, 0, (size_t)a.n_flags * sizeof(int), s) != cudaSuccess) return -1;
   switch (a.bs) {
     case 16: return launch_cl_bs<16>(a, backward, smem, cluster, s);
     case 8: return launch_cl_bs<8>(a, backward, smem, cluster, s);
@@ -1317,14 +1369,14 @@ int rnn_trace_read(unsigned long long* host, size_t n) {
 
 bool rnn_trace_enabled() {
   const char* e = std::getenv("DG_RNN_TRACE");
-  return e && e[0] == '1';
+  return e && (e[0] == '1' || e[0] == '2');
 }
 
 int launch_rnn_c0(const RnnC0& a, cudaStream_t s) {
-  int total = 0;
-  for (int k = 0; k < a.n; ++k) total += a.H[k];
-  if (total == 0) return 0;
-  rnn_c0_kernel<<<(total + 255) / 256, 256, 0, s>>>(a);
+  int blocks = 0;
+  for (int k = 0; k < a.n; ++k) blocks += (a.H[k] + 31) / 32;
+  if (blocks == 0) return 0;
+  rnn_c0_kernel<<<blocks, 256, 0, s>>>(a);
   return 1;
 }
 

@@ -415,7 +415,7 @@ bool tc_gemm_eligible(const std::vector<GemmProblem>& probs) {
   if (!tc_gemm_enabled()) return false;
   for (const auto& p : probs) {
     if (p.n_seg != 1) return false;
-    if (p.M < 128 || p.N < 128 || p.seg[0].K < 64) return false;
+    if (p.M < 128 || p.N < 128 || p.seg[0].K < 256) return false;  // short K: the SIMT kernel wins
   }
   return !probs.empty();
 }

@@ -121,7 +121,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int S = P.splits;
   const int local = blockIdx.x;
   const int z = local % S, tile = local / S;
-  const int m0 = (tile / P.tiles_n) * BM, n0 = (tile % P.tiles_n) * BN;
+  // m-tiles fastest: CTAs that run together share the same B columns, so a
+  // streamed B operand (dlogits in dW) is read from DRAM once
+  const int tiles_m = (P.M + BM - 1) / BM;
+  const int m0 = (tile % tiles_m) * BM, n0 = (tile / tiles_m) * BN;
   const int kt_total = (P.K + BK - 1) / BK;
   const int t0 = (int)((int64_t)kt_total * z / S), t1 = (int)((int64_t)kt_total * (z + 1) / S);
   const int nkt = t1 - t0;
@@ -323,22 +326,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (S > 1) cl.sync();
 }
 
-// lo[r][c] = x - tf32(x) for a rows x cols block with row stride ld (dst dense, stride cols_p)
-__global__ void split_lo_kernel(const float* __restrict__ src, int64_t ld, int64_t rows, int64_t cols,
-                                int64_t cols_p, float* __restrict__ dst) {
-  const int64_t c4 = cols_p >> 2;
-  const int64_t total = rows * c4;
+// lo[r][c] = x - tf32(x) for up to two rows x cols blocks (A and B of one
+// GEMM in a single launch), row stride ld; dst dense with stride cols_p
+struct SplitJob {
+  const float* src;
+  float* dst;
+  int64_t ld, rows, cols, cols_p;
+};
+__global__ void split_lo_kernel(SplitJob j0, SplitJob j1, int n_jobs) {
+  const int64_t t0 = j0.rows * (j0.cols_p >> 2);
+  const int64_t total = t0 + (n_jobs > 1 ? j1.rows * (j1.cols_p >> 2) : 0);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / c4, c = (i - r * c4) * 4;
-    const float* s = src + r * ld + c;
+    const bool second = i >= t0;
+    const SplitJob& j = second ? j1 : j0;
+    const int64_t q = second ? i - t0 : i;
+    const int64_t c4 = j.cols_p >> 2;
+    const int64_t r = q / c4, c = (q - r * c4) * 4;
+    const float* s = j.src + r * j.ld + c;
     float4 o;
     float* op = reinterpret_cast<float*>(&o);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float x = c + q < cols ? s[q] : 0.f;
-      op[q] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    for (int k = 0; k < 4; ++k) {
+      const float x = c + k < j.cols ? s[k] : 0.f;
+      op[k] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
     }
-    *reinterpret_cast<float4*>(dst + r * cols_p + c) = o;
+    *reinterpret_cast<float4*>(j.dst + r * j.cols_p + c) = o;
   }
 }
 
@@ -443,17 +455,17 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
 
 int launch_tma_gemm(const TmaGemmPlan& p, bool split_a, bool split_b, cudaStream_t s) {
   int n = 0;
-  if (split_a) {
-    const int64_t tot = p.a_rows * (p.a_colsp / 4);
-    split_lo_kernel<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, s>>>(p.a_src, p.a_ld, p.a_rows,
-                                                                                      p.a_cols, p.a_colsp, p.a_lo);
-    ++n;
-  }
-  if (split_b) {
-    const int64_t tot = p.b_rows * (p.b_colsp / 4);
-    split_lo_kernel<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, s>>>(p.b_src, p.b_ld, p.b_rows,
-                                                                                      p.b_cols, p.b_colsp, p.b_lo);
-    ++n;
+  {
+    SplitJob jobs[2];
+    int nj = 0;
+    if (split_a) jobs[nj++] = SplitJob{p.a_src, p.a_lo, p.a_ld, p.a_rows, p.a_cols, p.a_colsp};
+    if (split_b) jobs[nj++] = SplitJob{p.b_src, p.b_lo, p.b_ld, p.b_rows, p.b_cols, p.b_colsp};
+    if (nj) {
+      int64_t tot = 0;
+      for (int q = 0; q < nj; ++q) tot += jobs[q].rows * (jobs[q].cols_p / 4);
+      split_lo_kernel<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, s>>>(jobs[0], jobs[nj - 1], nj);
+      ++n;
+    }
   }
   void (*k)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const TmaGemmArgs) =
       p.a_mn ? (p.b_mn ? tma_gemm_kernel<true, true> : tma_gemm_kernel<true, false>)

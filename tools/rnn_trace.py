@@ -3,7 +3,7 @@ stamps of every CTA for one PTB MB=64 training step.  Diagnostic only."""
 import os
 import sys
 
-os.environ["DG_RNN_TRACE"] = "1"
+os.environ.setdefault("DG_RNN_TRACE", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -39,3 +39,10 @@ for kind, name in ((0, "fwd"), (1, "bwd")):
     print(f"== {name} (last launch, {live.sum()} CTAs): weights resident {(b[:, 1] - b[:, 0]).mean() / 1e3:.1f} us, "
           f"per-step {np.median(steps) / 1e3:.2f} us (min {steps.min() / 1e3:.2f}, max {steps.max() / 1e3:.2f}), "
           f"total {order.max() / 1e3:.1f} us, arrival skew {np.median(arr.max(axis=0) - arr.min(axis=0)) / 1e3:.2f} us")
+
+if os.environ.get("DG_RNN_TRACE") == "2":
+    # per-step phases of CTA 0 of the last forward launch (slots 64 + 4t + k)
+    b = buf[0, 0]
+    ph = b[64:64 + 4 * min(T, 47)].reshape(-1, 4).astype(np.int64)
+    d = np.diff(np.concatenate([ph, np.roll(ph[:, :1], -1, axis=0)], axis=1), axis=1)[:-1]
+    print("fwd CTA0 per-step phases (us): wait, fma, reduce+cell, push+rest ->", np.round(np.median(d, axis=0) / 1e3, 2))

@@ -25,7 +25,7 @@ for k, v in items:
     tot[key] += v
     cnt[key] += 1
 T = sum(tot.values())
-lines = [f"# ncu --metrics gpu__time_duration.sum launch list of `python bench.py --steps 2 --warmup 1`",
+lines = [f"# ncu --metrics gpu__time_duration.sum launch list of `python bench.py --steps 2 --warmup 1 --only`",
          f"# (cold-cache, serialised by ncu: compare SHARES, not absolutes). launches={len(items)} total={T/1e6:.3f} ms", ""]
 share = {}
 for k, v in sorted(tot.items(), key=lambda x: -x[1]):
@@ -41,7 +41,7 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__inst_executed_pipe_tensor.avg.pct_of_peak_sustained_active",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "lts__t_bytes.sum",
         "smsp__cycles_active.avg", "sm__cycles_elapsed.avg"]
-for name in ("full_tc", "full_simt", "full_cell"):
+for name in ("full_tma", "full_rnn", "full_row", "full_tc", "full_simt", "full_cell"):
     path = os.path.join(OUT, name + ".ncu-rep")
     if not os.path.exists(path):
         continue
