@@ -545,6 +545,50 @@ static PyObject* core_add(CoreObj* c, PyObject* const* args, Py_ssize_t nargs) {
         done = 2;
       }
       break;
+    case OP_SUM_BATCHES:
+      if (n_in == 1) {
+        shape = new_shape(shp[0]->dims, 1);
+        if (!shape) goto fail0;
+        done = 1;
+      }
+      break;
+    case OP_INPUT:
+      if (n_in == 0) {
+        /* aux is a Tensor: its Shape, and its payload if already contiguous float32 */
+        PyObject* sh = PyObject_GetAttr(aux, s_shape);
+        if (!sh) goto fail0;
+        if (!PyObject_TypeCheck(sh, &ShapeBaseType)) {
+          Py_DECREF(sh);
+          break;
+        }
+        PyObject* data = PyObject_GetAttr(aux, s_data);
+        if (!data) {
+          Py_DECREF(sh);
+          goto fail0;
+        }
+        Py_buffer view;
+        if (PyObject_GetBuffer(data, &view, PyBUF_C_CONTIGUOUS | PyBUF_FORMAT) < 0) {
+          PyErr_Clear();
+          Py_DECREF(data);
+          Py_DECREF(sh);
+          break;
+        }
+        const int ok = view.itemsize == 4 && view.format && strcmp(view.format, "f") == 0;
+        if (ok) {
+          shape = sh;
+          if (put_record(c, code, idx, 0, (ShapeObj*)shape, NULL, 0, (const float*)view.buf, view.len / 4) < 0) {
+            PyBuffer_Release(&view);
+            Py_DECREF(data);
+            goto fail_shape;
+          }
+          done = 2;
+        } else {
+          Py_DECREF(sh);
+        }
+        PyBuffer_Release(&view);
+        Py_DECREF(data);
+      }
+      break;
     default:
       break;
   }

@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <numeric>
@@ -63,6 +64,7 @@ struct Param {
   std::vector<uint8_t> touched_bits;
   std::vector<int64_t> touched_list;  // insertion order; sorted on read
   int64_t size() const { return rows * cols; }
+  std::vector<int32_t> sort_cnt;  // scatter planning scratch (all zero at rest)
 };
 
 static std::mutex g_param_mu;
@@ -229,6 +231,7 @@ struct dg_graph {
   cudaEvent_t vcache_ev = nullptr;
   int vcache_node = -1;
   int64_t vcache_n = 0;
+  size_t blob_hint[2] = {1 << 20, 4 << 20};  // forward / backward table blob sizes seen
   bool has_grads = false;  // any backward in this generation
   bool counters_ready = false;  // split-K tile counters zeroed (first launch)
 };
@@ -305,9 +308,6 @@ struct SigHash {
   }
 };
 
-static bool is_leaf(int kind) {
-  return kind == DG_OP_INPUT || kind == DG_OP_PARAMETER || kind == DG_OP_LOOKUP || kind == DG_OP_LOOKUP_BATCH;
-}
 
 static int64_t param_handle_of(const dg_graph* g, int node) {
   const Node& n = g->nodes[node];
@@ -1153,6 +1153,17 @@ static inline const T* dev_at(dg_graph* g, size_t off) {
   return reinterpret_cast<const T*>(g->work_base + off);
 }
 
+// true when two entries of a row-pointer table coincide (strictly increasing
+// tables -- the common, contiguous case -- are answered without sorting)
+static bool has_duplicate_rows(const std::vector<uintptr_t>& rows) {
+  bool increasing = true;
+  for (size_t i = 1; i < rows.size() && increasing; ++i) increasing = rows[i] > rows[i - 1];
+  if (increasing) return false;
+  std::vector<uintptr_t> u = rows;
+  std::sort(u.begin(), u.end());
+  return std::adjacent_find(u.begin(), u.end()) != u.end();
+}
+
 // Row table (device address inside the plan blob) -> dense block: when the
 // rows are equally spaced (row i at base + i*ld) the operand is rewritten as
 // base/ld, which the TMA path (and vectorised epilogues) need.
@@ -1454,9 +1465,20 @@ int dg_graph_append(dg_graph* g, const dg_node* nodes, int32_t n, const int32_t*
 
 // ---------------------------------------------------------------- forward
 
+// DG_DRYRUN=1: plan everything, launch nothing (host-side planner profiling
+// without a device; results are meaningless)
+static bool dry_run() {
+  static const bool on = [] {
+    const char* e = std::getenv("DG_DRYRUN");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 static int launch_plan(dg_graph* g, Plan& plan) {
   const size_t blob_bytes = (plan.blob.host.size() + 255) & ~size_t(255);
   if (blob_bytes > blob_cap(g)) return fail(DG_CONFIG, "plan tables exceed the workspace");
+  if (dry_run()) return DG_OK;
   if (!g->counters_ready) {
     // split-K tile counters start (and are always left) at zero
     DG_CUDA_TRY(cudaMemsetAsync(g->work_base + g->work_bytes - (1u << 20), 0, 1u << 20, g->stream));
@@ -1480,7 +1502,15 @@ static int launch_plan(dg_graph* g, Plan& plan) {
       }
       DG_CUDA_TRY(cudaEventRecord(e0, g->stream));
     }
+    static const bool op_timing = [] {
+      const char* e = std::getenv("DG_PLAN_TIMING");
+      return e && e[0] == '2';
+    }();
+    const auto t_op = std::chrono::steady_clock::now();
     int n = plan.ops[q](g->work_base);
+    if (op_timing)
+      std::fprintf(stderr, "[op] class %d launches %d host %.1f us\n", mt.cls, n,
+                   std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_op).count());
     if (n < 0) return fail(DG_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(cudaGetLastError()));
     g->launches += n;
     if (prof) {
@@ -1506,9 +1536,7 @@ static void push_dx_problem(dg_graph* g, Plan& plan, GemmBatch& batch, const flo
                             const float* W, int m, int K, const std::vector<uintptr_t>& dxrows) {
   Blob& B = plan.blob;
   const cudaStream_t st = g->stream;
-  std::vector<uintptr_t> uniq = dxrows;
-  std::sort(uniq.begin(), uniq.end());
-  const bool dup = std::adjacent_find(uniq.begin(), uniq.end()) != uniq.end();
+  const bool dup = has_duplicate_rows(dxrows);
   GemmProblem pr{};
   pr.M = (int)dxrows.size();
   pr.N = K;
@@ -2176,6 +2204,7 @@ static int do_forward(dg_graph* g, int upto) {
       for (int i : S.units[u].nodes) place(i);
 
   Plan plan;
+  plan.blob.host.reserve(g->blob_hint[0]);  // no regrowth copies while planning
   Blob& B = plan.blob;
   // input payloads: laid out in the blob exactly like the arena block
   size_t in_blob = 0;
@@ -2233,13 +2262,14 @@ static int do_forward(dg_graph* g, int upto) {
     flush_gemm(g, plan, gb);
   }
   tm.lap("groups");
+  g->blob_hint[0] = std::max(g->blob_hint[0], plan.blob.host.size() + plan.blob.host.size() / 4);
   int rc = launch_plan(g, plan);
   if (rc) return rc;
   tm.lap("launch");
   {
     const Node& tn = g->nodes[upto];
     g->vcache_node = -1;
-    if (tn.kind != DG_OP_PARAMETER && tn.size() <= 64) {
+    if (tn.kind != DG_OP_PARAMETER && tn.size() <= 64 && !dry_run()) {
       if (!g->vcache) {
         // slots of one process-wide pinned block (cudaHostAlloc synchronises
         // the device, so it must not run per graph)
@@ -2651,9 +2681,7 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
             use.x_rows.insert(use.x_rows.end(), xrows.begin(), xrows.end());
             use.g_rows.insert(use.g_rows.end(), grows.begin(), grows.end());
             // dX = G W   (B(k=i, n=t) = W[i + t*m]: n-major rows of W^T)
-            std::vector<uintptr_t> uniq = dxrows;
-            std::sort(uniq.begin(), uniq.end());
-            const bool dup = std::adjacent_find(uniq.begin(), uniq.end()) != uniq.end();
+            const bool dup = has_duplicate_rows(dxrows);
             GemmProblem pr{};
             pr.M = n * Bt;
             pr.N = K;
@@ -2781,6 +2809,7 @@ int dg_backward(dg_graph* g, int32_t loss) {
     if (g->nodes[i].kind == DG_OP_PARAMETER) g->nodes[i].grad = param_at(g->aux_i[g->nodes[i].ai_off])->grad;
 
   Plan plan;
+  plan.blob.host.reserve(g->blob_hint[1]);  // no regrowth copies while planning
   Blob& B = plan.blob;
   cudaStream_t st = g->stream;
   // zero the fresh slots (arena contract, graph.py:146-148) and seed dloss = 1
@@ -2800,9 +2829,23 @@ int dg_backward(dg_graph* g, int32_t loss) {
   tm.lap("place");
   {
     GemmBatch gb;
-    for (int q = (int)S.groups.size() - 1; q >= 0; --q)
+    static const bool per_kind = [] {
+      const char* e = std::getenv("DG_PLAN_TIMING");
+      return e && e[0] == '2';
+    }();
+    std::map<int, double> kt;
+    for (int q = (int)S.groups.size() - 1; q >= 0; --q) {
+      const auto t0 = std::chrono::steady_clock::now();
       plan_backward_group(g, S, S.groups[q], plan, dummy, wuse, buse, gb);
+      if (per_kind)
+        kt[S.groups[q].kind] += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    }
     flush_gemm(g, plan, gb);
+    if (per_kind) {
+      std::string o;
+      for (auto& kv : kt) o += " k" + std::to_string(kv.first) + "=" + std::to_string((int)kv.second);
+      std::fprintf(stderr, "[plan] backward groups by kind:%s\n", o.c_str());
+    }
   }
   tm.lap("groups");
 
@@ -2923,19 +2966,30 @@ int dg_backward(dg_graph* g, int32_t loss) {
       for (int64_t q = 1; q < x.ai_len; ++q)
         it->second.v.push_back({g->aux_i[x.ai_off + q], P(x.grad + (q - 1) * x.elem)});
     }
+    tm.lap("scatter-collect");
     for (int64_t h : order) {
       auto& v = by_table[h].v;
-      std::stable_sort(v.begin(), v.end(), [](auto& a, auto& b) { return a.first < b.first; });
+      // stable counting sort by row id (ids < rows): unique ids sorted, then
+      // each id's sources in graph order (deterministic segment sums)
+      Param* pt = param_at(h);
+      if ((int64_t)pt->sort_cnt.size() < pt->rows) pt->sort_cnt.assign(pt->rows, 0);
+      std::vector<int32_t>& cnt = pt->sort_cnt;
       std::vector<int64_t> uids;
+      for (auto& e : v)
+        if (cnt[e.first]++ == 0) uids.push_back(e.first);
+      std::sort(uids.begin(), uids.end());
       std::vector<int32_t> seg;
-      std::vector<uintptr_t> src;
-      for (size_t q = 0; q < v.size(); ++q) {
-        if (q == 0 || v[q].first != v[q - 1].first) {
-          uids.push_back(v[q].first);
-          seg.push_back((int32_t)q);
-        }
-        src.push_back(v[q].second);
+      seg.reserve(uids.size() + 1);
+      int32_t pos = 0;
+      for (int64_t u : uids) {
+        seg.push_back(pos);
+        const int32_t c = cnt[u];
+        cnt[u] = pos;
+        pos += c;
       }
+      std::vector<uintptr_t> src(v.size());
+      for (auto& e : v) src[cnt[e.first]++] = e.second;
+      for (int64_t u : uids) cnt[u] = 0;
       seg.push_back((int32_t)v.size());
       Param* p = param_at(h);
       const size_t ou = B.push(uids), os = B.push(seg), osrc = B.push(src);
@@ -2950,6 +3004,7 @@ int dg_backward(dg_graph* g, int32_t loss) {
     }
   }
   tm.lap("scatter");
+  g->blob_hint[1] = std::max(g->blob_hint[1], plan.blob.host.size() + plan.blob.host.size() / 4);
   rc = launch_plan(g, plan);
   if (rc) return rc;
   tm.lap("launch");

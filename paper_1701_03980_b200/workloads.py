@@ -186,15 +186,22 @@ class RNNLM:
         we, be = ops.parameter(cg, self.W), ops.parameter(cg, self.b)
         t_max = max(len(ids) for ids in batch_ids)
         nb = len(batch_ids)
+        # the padded id matrix once per batch (the per-step columns are exactly
+        # the reference's per-step list comprehensions, bench/tasks.py:432-438)
+        lens = np.array([len(ids) for ids in batch_ids])
+        padded = np.full((nb, t_max), pad_id, dtype=np.int64)
+        for r, ids in enumerate(batch_ids):
+            padded[r, : len(ids)] = ids
+        cols = padded.T.tolist()
+        masks = (np.arange(1, t_max)[:, None] < lens[None, :]).astype(cg.dtype)
+        mask_shape = dy.Shape((1,), nb)
         state = self.rnn.initial_state(cg)
         loss = None
         for t in range(t_max - 1):
-            xs = [ids[t] if t < len(ids) else pad_id for ids in batch_ids]
-            labels = [ids[t + 1] if t + 1 < len(ids) else pad_id for ids in batch_ids]
-            mask = np.array([1.0 if t + 1 < len(ids) else 0.0 for ids in batch_ids], dtype=cg.dtype)
+            xs, labels = cols[t], cols[t + 1]
             state = state.add_input(ops.lookup_batch(cg, self.E, xs))
             nll = ops.pickneglogsoftmax_batch(ops.affine(be, we, state.output()), labels)
-            masked = ops.cmult(nll, ops.input(cg, dy.Tensor(dy.Shape((1,), nb), mask)))
+            masked = ops.cmult(nll, ops.input(cg, dy.Tensor(mask_shape, masks[t])))
             step = ops.sum_batches(masked)
             loss = step if loss is None else ops.add(loss, step)
         return loss
