@@ -263,9 +263,11 @@ static int pinned_acquire(Pinned& p, size_t n) {
   }
   if (!p.ev) DG_CUDA_TRY(cudaEventCreateWithFlags(&p.ev, cudaEventDisableTiming));
   if (n > p.cap) {
+    // growth (cudaHostAlloc synchronises the device): start at 4 MiB and
+    // double, so a stream of slightly larger plans does not regrow every time
     if (p.ptr) DG_CUDA_TRY(cudaFreeHost(p.ptr));
-    size_t cap = std::max<size_t>(n, 1 << 16);
-    cap = cap + cap / 2;
+    size_t cap = std::max<size_t>(p.cap ? 2 * p.cap : (4u << 20), 1 << 16);
+    while (cap < n) cap *= 2;
     DG_CUDA_TRY(cudaHostAlloc(&p.ptr, cap, cudaHostAllocDefault));
     p.cap = cap;
   }
@@ -279,7 +281,12 @@ static Pinned& staging_slot() {
   static std::mutex mu;
   static Pinned ring[8];
   static int next = 0;
+  static bool primed = false;
   std::lock_guard<std::mutex> lk(mu);
+  if (!primed) {  // size every slot now: no allocation (device sync) on a later step
+    primed = true;
+    for (Pinned& q : ring) pinned_acquire(q, 4u << 20);
+  }
   Pinned& p = ring[next];
   next = (next + 1) % 8;
   return p;
@@ -1199,7 +1206,7 @@ static bool tma_try(dg_graph* g, const Plan& plan, const GemmProblem& p0, bool a
   const int64_t la = tma_lo_floats(a_mn ? K : p.M, a_mn ? p.M : K);
   const int64_t lb = tma_lo_floats(b_mn ? K : p.N, b_mn ? p.N : K);
   const int64_t la_p = (la + 63) & ~int64_t(63);
-  if (la_p + lb > lo_cap) return false;
+  if (!tma_conv_enabled() && la_p + lb > lo_cap) return false;  // residual copies need scratch
   TmaOperands o{};
   o.M = p.M;
   o.N = p.N;

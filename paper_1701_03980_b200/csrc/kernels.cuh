@@ -288,6 +288,7 @@ struct TmaGemmPlan {
   CUtensorMap mAh, mAl, mBh, mBl;
   TmaGemmArgs args;
   bool a_mn, b_mn;
+  bool conv;  // residuals formed in shared memory by converter warps (no lo copies)
   const float* a_src;
   const float* b_src;
   float* a_lo;
@@ -297,6 +298,7 @@ struct TmaGemmPlan {
   double flops;
 };
 bool tma_gemm_enabled();  // DG_TMA=0 disables (A/B checks)
+bool tma_conv_enabled();  // DG_TMA_CONV=0: pre-split residual copies instead of in-smem conversion
 int64_t tma_lo_floats(int64_t rows, int64_t cols);
 bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out);
 // split_a / split_b: (re)compute the residual copies before the GEMM

@@ -44,8 +44,12 @@ constexpr int BM = 128, BN = 128, BK = 32;
 constexpr int kStages = 3;
 constexpr int kOpBytes = 128 * BK * 4;         // 16 KiB per operand tile
 constexpr int kStageBytes = 4 * kOpBytes;      // A_hi, A_lo, B_hi, B_lo
-constexpr int kThreads = 192;
+constexpr int kThreads = 192;      // producer, MMA, 4 epilogue warps
+constexpr int kThreadsConv = 320;  // + 4 converter warps forming the residuals in shared memory
 constexpr int kSmem = kStages * kStageBytes + 1024;
+// conversion variant: 5 raw stages (A_hi, B_hi) + 2 residual buffers (A_lo, B_lo)
+constexpr int kRawStagesC = 3;
+constexpr int kSmemConv = kRawStagesC * 4 * kOpBytes + 1024;
 constexpr int kChunk = 2;  // k-tiles per TMEM accumulation (K = 64)
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -108,14 +112,16 @@ __device__ __forceinline__ const float* orow(const Operand& o, int64_t i) {
   return o.rows ? o.rows[i] : o.base + i * o.ld;
 }
 
-template <bool kAMN, bool kBMN>
-__global__ void __launch_bounds__(kThreads, 1)
+template <bool kAMN, bool kBMN, bool kConv>
+__global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
     tma_gemm_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                     const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
                     const __grid_constant__ TmaGemmArgs P) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[kStages], empty[kStages], acc_full[2], acc_empty[2];
+  constexpr int NS = kConv ? kRawStagesC : kStages;  // raw operand stages
+  constexpr int SB = kStageBytes;  // stage stride: A_hi, B_hi, A_lo, B_lo (conv) / A_hi, A_lo, B_hi, B_lo
+  __shared__ uint64_t full[NS], empty[NS], conv[NS], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = P.splits;
@@ -131,19 +137,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nchunks = (nkt + kChunk - 1) / kChunk;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
+    for (int b = 0; b < NS; ++b) mbar_init(&conv[b], 4);
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAh)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAl)) : "memory");
+    if (!kConv) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAl)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBh)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBl)) : "memory");
+    if (!kConv) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBl)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_sh)),
@@ -163,30 +170,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       for (int j = 0; j < nkt; ++j) {
-        const int s = j % kStages, use = j / kStages;
+        const int s = j % NS, use = j / NS;
         if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
-        mbar_expect_tx(&full[s], kStageBytes);
-        const uint32_t st = sbase + s * kStageBytes;
+        mbar_expect_tx(&full[s], kConv ? 2 * kOpBytes : kStageBytes);
+        const uint32_t st = sbase + s * SB;
         const int k0 = (t0 + j) * BK;
         // A: K-major box {32 k, 128 m} at (k0, m0); MN-major 4 boxes {32 m, 32 k} at (m0 + 32g, k0)
         if (!kAMN) {
           tma_2d(st, &mAh, k0, m0, &full[s]);
-          tma_2d(st + kOpBytes, &mAl, k0, m0, &full[s]);
+          if (!kConv) tma_2d(st + kOpBytes, &mAl, k0, m0, &full[s]);
         } else {
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
             tma_2d(st + g * 4096, &mAh, m0 + 32 * g, k0, &full[s]);
-            tma_2d(st + kOpBytes + g * 4096, &mAl, m0 + 32 * g, k0, &full[s]);
+            if (!kConv) tma_2d(st + kOpBytes + g * 4096, &mAl, m0 + 32 * g, k0, &full[s]);
           }
         }
+        const uint32_t sbh = st + (kConv ? kOpBytes : 2 * kOpBytes);
         if (!kBMN) {
-          tma_2d(st + 2 * kOpBytes, &mBh, k0, n0, &full[s]);
-          tma_2d(st + 3 * kOpBytes, &mBl, k0, n0, &full[s]);
+          tma_2d(sbh, &mBh, k0, n0, &full[s]);
+          if (!kConv) tma_2d(st + 3 * kOpBytes, &mBl, k0, n0, &full[s]);
         } else {
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
-            tma_2d(st + 2 * kOpBytes + g * 4096, &mBh, n0 + 32 * g, k0, &full[s]);
-            tma_2d(st + 3 * kOpBytes + g * 4096, &mBl, n0 + 32 * g, k0, &full[s]);
+            tma_2d(sbh + g * 4096, &mBh, n0 + 32 * g, k0, &full[s]);
+            if (!kConv) tma_2d(st + 3 * kOpBytes + g * 4096, &mBl, n0 + 32 * g, k0, &full[s]);
           }
         }
       }
@@ -195,13 +203,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = uidesc(kAMN, kBMN);
       for (int j = 0; j < nkt; ++j) {
-        const int s = j % kStages, use = j / kStages;
+        const int s = j % NS, use = j / NS;
         const int c = j / kChunk, a = c & 1;
         if (j % kChunk == 0 && c >= 2) mbar_wait(&acc_empty[a], ((c >> 1) - 1) & 1);
-        mbar_wait(&full[s], use & 1);
+        if (kConv) mbar_wait(&conv[s], use & 1);
+        else mbar_wait(&full[s], use & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t ah = sbase + s * kStageBytes, al = ah + kOpBytes, bh = ah + 2 * kOpBytes,
-                       bl = ah + 3 * kOpBytes;
+        uint32_t ah, al, bh, bl;
+        if (kConv) {
+          ah = sbase + s * SB;
+          bh = ah + kOpBytes;
+          al = ah + 2 * kOpBytes;
+          bl = ah + 3 * kOpBytes;
+        } else {
+          ah = sbase + s * SB;
+          al = ah + kOpBytes;
+          bh = ah + 2 * kOpBytes;
+          bl = ah + 3 * kOpBytes;
+        }
         const uint32_t acc = tmem + (uint32_t)(a * BN);
 #pragma unroll
         for (int ks = 0; ks < BK / 8; ++ks) {
@@ -214,6 +233,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(&empty[s]);
         if (j % kChunk == kChunk - 1 || j == nkt - 1) mma_commit(&acc_full[a]);
       }
+    }
+  } else if (kConv && warp >= 6) {
+    // converter warps 6..9: residual lo = x - tf32(x) of the landed hi tiles
+    // (same swizzled layout, elementwise), then publish to the async proxy
+    const int ct = threadIdx.x - 6 * 32;  // 0..127
+    for (int j = 0; j < nkt; ++j) {
+      const int s = j % NS, use = j / NS;
+      mbar_wait(&full[s], use & 1);
+      char* st = smem + s * SB;
+      char* lo = st + 2 * kOpBytes;
+#pragma unroll
+      for (int op = 0; op < 2; ++op) {
+        const float4* src = reinterpret_cast<const float4*>(st + op * kOpBytes);
+        float4* dst = reinterpret_cast<float4*>(lo + op * kOpBytes);
+#pragma unroll
+        for (int i = 0; i < kOpBytes / 16 / 128; ++i) {
+          const float4 x = src[ct + i * 128];
+          float4 y;
+          y.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+          y.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+          y.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+          y.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+          dst[ct + i * 128] = y;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv[s]);
     }
   } else {
     // epilogue warps 2..5 -> TMEM lane quadrant warp % 4
@@ -253,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // free), rows rotated by 4*row floats against bank conflicts, then write
   // whole rows with all warps (coalesced 512 B per row)
   float* part = reinterpret_cast<float*>(smem);  // 128 x 128 fp32 = 64 KiB
-  if (warp >= 2) {
+  if (warp >= 2 && warp < 6) {
     const int lrow = (warp & 3) * 32 + lane;
 #pragma unroll
     for (int q = 0; q < BN; q += 4)
@@ -267,11 +314,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool vec = P.c_vec && n0 + BN <= P.N;
   const int total = rows * (BN / 4);
   constexpr int U = 4;  // loads of U slots are issued before any store (no dependent DRAM round trips)
-  for (int e0 = threadIdx.x; e0 < total; e0 += U * kThreads) {
+  constexpr int NT = kConv ? kThreadsConv : kThreads;
+  for (int e0 = threadIdx.x; e0 < total; e0 += U * NT) {
     float4 acc4[U], old4[U], b4[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * kThreads;
+      const int e = e0 + u * NT;
       acc4[u] = old4[u] = b4[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (e >= total) continue;
       const int lm = z * rows + e / (BN / 4), ln = (e % (BN / 4)) * 4;
@@ -282,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * kThreads;
+      const int e = e0 + u * NT;
       if (e >= total) continue;
       const int lm = z * rows + e / (BN / 4), ln = (e % (BN / 4)) * 4;
       const int sw = (ln + 4 * lm) & (BN - 1);
@@ -296,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * kThreads;
+      const int e = e0 + u * NT;
       if (e >= total) continue;
       const int lm = z * rows + e / (BN / 4), ln = (e % (BN / 4)) * 4;
       const int64_t m = m0 + lm;
@@ -387,6 +435,14 @@ bool make_map(CUtensorMap* m, const float* base, int64_t ld, int64_t rows, int64
 
 }  // namespace
 
+bool tma_conv_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DG_TMA_CONV");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool tma_gemm_enabled() {
   static const bool on = [] {
     const char* e = getenv("DG_TMA");
@@ -426,9 +482,14 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
   p.b_cols = bc;
   p.b_colsp = bcp;
   p.b_lo = o.B_lo;
-  if (!make_map(&p.mAh, o.A, o.lda, ar, ac, o.a_mn) || !make_map(&p.mAl, o.A_lo, acp, ar, ac, o.a_mn) ||
-      !make_map(&p.mBh, o.B, o.ldb, br, bc, o.b_mn) || !make_map(&p.mBl, o.B_lo, bcp, br, bc, o.b_mn))
+  p.conv = tma_conv_enabled();
+  if (!make_map(&p.mAh, o.A, o.lda, ar, ac, o.a_mn) || !make_map(&p.mBh, o.B, o.ldb, br, bc, o.b_mn)) return false;
+  if (p.conv) {  // residuals formed in shared memory: no lo copies, no lo maps
+    p.mAl = p.mAh;
+    p.mBl = p.mBh;
+  } else if (!make_map(&p.mAl, o.A_lo, acp, ar, ac, o.a_mn) || !make_map(&p.mBl, o.B_lo, bcp, br, bc, o.b_mn)) {
     return false;
+  }
   a.tiles_n = (o.N + BN - 1) / BN;
   const int tiles = ((o.M + BM - 1) / BM) * a.tiles_n;
   const int kt = (o.K + BK - 1) / BK;
@@ -455,6 +516,7 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
 
 int launch_tma_gemm(const TmaGemmPlan& p, bool split_a, bool split_b, cudaStream_t s) {
   int n = 0;
+  if (p.conv) split_a = split_b = false;
   {
     SplitJob jobs[2];
     int nj = 0;
@@ -467,19 +529,23 @@ int launch_tma_gemm(const TmaGemmPlan& p, bool split_a, bool split_b, cudaStream
       ++n;
     }
   }
-  void (*k)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const TmaGemmArgs) =
-      p.a_mn ? (p.b_mn ? tma_gemm_kernel<true, true> : tma_gemm_kernel<true, false>)
-             : (p.b_mn ? tma_gemm_kernel<false, true> : tma_gemm_kernel<false, false>);
-  static bool attr[4] = {false, false, false, false};
-  const int ki = (p.a_mn ? 2 : 0) + (p.b_mn ? 1 : 0);
+  using K = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const TmaGemmArgs);
+  static const K table[8] = {tma_gemm_kernel<false, false, false>, tma_gemm_kernel<false, true, false>,
+                             tma_gemm_kernel<true, false, false>,  tma_gemm_kernel<true, true, false>,
+                             tma_gemm_kernel<false, false, true>,  tma_gemm_kernel<false, true, true>,
+                             tma_gemm_kernel<true, false, true>,   tma_gemm_kernel<true, true, true>};
+  const int ki = (p.conv ? 4 : 0) + (p.a_mn ? 2 : 0) + (p.b_mn ? 1 : 0);
+  const K k = table[ki];
+  static bool attr[8] = {false, false, false, false, false, false, false, false};
+  const int smem = p.conv ? kSmemConv : kSmem;
   if (!attr[ki]) {
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) != cudaSuccess) return -1;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
     attr[ki] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.ctas);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kSmem;
+  cfg.blockDim = dim3(p.conv ? kThreadsConv : kThreads);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;

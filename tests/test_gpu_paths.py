@@ -6,6 +6,8 @@ with each fast path switched off, so the fallbacks stay parity-green too.
                     arrival counters instead of cluster distributed smem
   DG_RNN=0          no persistent recurrence: level-batched GEMM + fused cells
   DG_TMA=0          cp.async tcgen05 GEMM instead of the TMA warp-specialised one
+  DG_TMA_CONV=0     TMA GEMM reading pre-split residual copies instead of forming
+                    them in shared memory
   DG_TC=0           SIMT GEMMs only
   DG_SCHED_CACHE=0  schedules rebuilt for every graph
 """
@@ -22,6 +24,7 @@ VARIANTS = {
     "rnn_no_cluster": {"DG_RNN_CLUSTER": "0"},
     "rnn_off": {"DG_RNN": "0"},
     "tma_off": {"DG_TMA": "0"},
+    "tma_presplit": {"DG_TMA_CONV": "0"},
     "tensor_cores_off": {"DG_TC": "0"},
     "schedule_cache_off": {"DG_SCHED_CACHE": "0"},
 }
