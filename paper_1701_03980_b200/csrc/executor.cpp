@@ -1812,21 +1812,33 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
       }
       const bool g_al = all_aligned16(grows);
       const float* const* g_dev = dev_at<const float*>(g, B.push(grows));
+      // gradients leaving the chain, batched across the group's chains: one
+      // grouped launch unless two problems write the same node (then flush)
+      auto add_dx = [&](const std::vector<int>& target_nodes, const float* W, int K,
+                        const std::vector<uintptr_t>& rows) {
+        GemmBatch& bt = gemm_batch_for(g, plan, *gb, gr.level, C_GEMM_DX, false, true);
+        bool clash = false;
+        for (int tnode : target_nodes)
+          clash = clash || std::find(bt.targets.begin(), bt.targets.end(), tnode) != bt.targets.end();
+        if (clash) flush_gemm(g, plan, *gb);
+        GemmBatch& b2 = gemm_batch_for(g, plan, *gb, gr.level, C_GEMM_DX, false, true);
+        push_dx_problem(g, plan, b2, g_dev, g_al, W, cp.gw, K, rows);
+        b2.targets.insert(b2.targets.end(), target_nodes.begin(), target_nodes.end());
+      };
       // x_t of the bottom chain: dX = dG Wx over every step
       if (cp.src < 0) {
-        GemmBatch& bt = gemm_batch_for(g, plan, *gb, gr.level, C_GEMM_DX, false, true);
-        push_dx_problem(g, plan, bt, g_dev, g_al, param_at(cp.hWx)->val, cp.gw, cp.K_in, dxrows);
-        flush_gemm(g, plan, *gb);
+        std::vector<int> xs;
+        for (int t = 0; t < T; ++t) xs.push_back(g->inputs[g->nodes[cp.G[t]].in_off + 2]);
+        add_dx(xs, param_at(cp.hWx)->val, cp.K_in, dxrows);
       }
       // h_{-1}: dX = dG_0 Wh
       {
         const Node& G0 = g->nodes[cp.G[0]];
-        const Node& hn = g->nodes[g->inputs[G0.in_off + 4]];
+        const int hnode = g->inputs[G0.in_off + 4];
+        const Node& hn = g->nodes[hnode];
         std::vector<uintptr_t> hd(Bt);
         for (int b = 0; b < Bt; ++b) hd[b] = P(hn.grad + (hn.batch == 1 ? 0 : (int64_t)b * cp.H));
-        GemmBatch& bt = gemm_batch_for(g, plan, *gb, gr.level, C_GEMM_DX, false, true);
-        push_dx_problem(g, plan, bt, g_dev, g_al, param_at(cp.hWh)->val, cp.gw, cp.H, hd);
-        flush_gemm(g, plan, *gb);
+        add_dx({hnode}, param_at(cp.hWh)->val, cp.H, hd);
       }
       // c_{-1} broadcast over the batch: batch sum of dc_0 * f_0
       const Node& cpn = g->nodes[cp.cells[0].ins[1]];
@@ -1845,6 +1857,7 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
       }
     }
   }
+  flush_gemm(g, plan, *gb);
   if (c0.n) {
     plan.ops.push_back([c0, st](char*) { return launch_rnn_c0(c0, st); });
     plan.tag(C_ELEMWISE, 0.0, 0.0);
