@@ -113,11 +113,30 @@ static PyTypeObject* NodeT = NULL;
 static PyTypeObject* ExprT = NULL;
 static PyObject* Registry = NULL;  /* ops.REGISTRY */
 static PyObject* FastKinds = NULL; /* kind str -> code for kinds with the built-in rule */
+/* The heap subclasses are GC types, but the cycle collector cannot see the
+   C fields (no tp_traverse on the bases), so tracking them buys nothing and
+   makes every young-generation collection walk thousands of graph objects. */
+static inline void untrack(PyObject* o) {
+  if (o && PyObject_GC_IsTracked(o)) PyObject_GC_UnTrack(o);
+}
+
+/* tuples of ints/floats (index tuples, dims, pick ranges) cannot be in a cycle */
+static void untrack_atomic_tuple(PyObject* t) {
+  if (!t || !PyTuple_CheckExact(t) || !PyObject_GC_IsTracked(t)) return;
+  for (Py_ssize_t k = 0, n = PyTuple_GET_SIZE(t); k < n; ++k) {
+    PyObject* v = PyTuple_GET_ITEM(t, k);
+    if (!PyLong_CheckExact(v) && !PyFloat_CheckExact(v)) return;
+  }
+  PyObject_GC_UnTrack(t);
+}
+
 static PyObject* s_shape = NULL, *s_encode = NULL, *s_handle = NULL, *s_rows = NULL, *s_dim = NULL,
                 *s_data = NULL, *s_check_current = NULL, *s_code = NULL;
 
 static PyObject* new_shape(PyObject* dims, long batch) {
   ShapeObj* s = (ShapeObj*)ShapeT->tp_alloc(ShapeT, 0);
+  untrack((PyObject*)s);
+  untrack_atomic_tuple(dims);
   if (!s) return NULL;
   Py_INCREF(dims);
   s->dims = dims;
@@ -631,14 +650,17 @@ static PyObject* core_add(CoreObj* c, PyObject* const* args, Py_ssize_t nargs) {
       PyTuple_SET_ITEM(tin, k, v);
     }
     NodeObj* nd = (NodeObj*)NodeT->tp_alloc(NodeT, 0);
+    untrack((PyObject*)nd);
     if (!nd) {
       Py_DECREF(tin);
       goto fail_shape;
     }
     nd->kind = Py_NewRef(kind);
+    untrack((PyObject*)tin);
     nd->inputs = tin;
     nd->shape = shape; /* steals */
     nd->aux = Py_NewRef(aux);
+    untrack_atomic_tuple(aux);
     nd->code = code;
     int rc = PyList_Append(c->nodes, (PyObject*)nd);
     Py_DECREF(nd);
@@ -648,6 +670,7 @@ static PyObject* core_add(CoreObj* c, PyObject* const* args, Py_ssize_t nargs) {
   if (shp != shp_stack) PyMem_Free(shp);
   Py_XDECREF(seq);
   ExprObj* ex = (ExprObj*)ExprT->tp_alloc(ExprT, 0);
+  untrack((PyObject*)ex);
   if (!ex) return NULL;
   ex->graph = Py_NewRef(c->cg);
   ex->index = PyList_GET_SIZE(c->nodes) - 1;
@@ -705,10 +728,235 @@ static PyObject* core_pack(CoreObj* c, PyObject* arg) {
                        (unsigned long long)(uintptr_t)((float*)c->af.p + af0), c->af.n - af0);
 }
 
+/* ---- composite builders: the node sequence of builders.py emitted without
+   per-node Python frames (same kinds, same order, same shapes) */
+static PyObject *k_affine = NULL, *k_pick = NULL, *k_logistic = NULL, *k_tanh = NULL, *k_cmult = NULL, *k_add = NULL;
+
+static PyObject* add1(CoreObj* c, PyObject* kind, PyObject* a, PyObject* aux) {
+  PyObject* t = PyTuple_Pack(1, a);
+  if (!t) return NULL;
+  PyObject* args[3] = {kind, t, aux};
+  PyObject* r = core_add(c, args, 3);
+  Py_DECREF(t);
+  return r;
+}
+
+static PyObject* add2(CoreObj* c, PyObject* kind, PyObject* a, PyObject* b) {
+  PyObject* t = PyTuple_Pack(2, a, b);
+  if (!t) return NULL;
+  PyObject* args[3] = {kind, t, Py_None};
+  PyObject* r = core_add(c, args, 3);
+  Py_DECREF(t);
+  return r;
+}
+
+static PyObject* gate(CoreObj* c, PyObject* gates, long lo, long hi, PyObject* act) {
+  PyObject* rng = Py_BuildValue("(ll)", lo, hi);
+  if (!rng) return NULL;
+  PyObject* p = add1(c, k_pick, gates, rng);
+  Py_DECREF(rng);
+  if (!p) return NULL;
+  PyObject* r = add1(c, act, p, Py_None);
+  Py_DECREF(p);
+  return r;
+}
+
+/* GraphCore.lstm(b, wx, x, wh, h, c, H) -> (h', c'): builders.py
+   RNNBuilder._lstm (i, f, o, g gate blocks of the affine output) */
+static PyObject* lstm_generic(CoreObj* c, PyObject* const* args, long H) {
+  PyObject *gates = NULL, *ig = NULL, *fg = NULL, *og = NULL, *gg = NULL, *fc = NULL, *igg = NULL, *nc = NULL,
+           *tc = NULL, *nh = NULL, *ret = NULL;
+  PyObject* ins = PyTuple_Pack(5, args[0], args[1], args[2], args[3], args[4]);
+  if (!ins) return NULL;
+  PyObject* aargs[3] = {k_affine, ins, Py_None};
+  gates = core_add(c, aargs, 3);
+  Py_DECREF(ins);
+  if (!gates) return NULL;
+  if (!(ig = gate(c, gates, 0, H, k_logistic))) goto done;
+  if (!(fg = gate(c, gates, H, 2 * H, k_logistic))) goto done;
+  if (!(og = gate(c, gates, 2 * H, 3 * H, k_logistic))) goto done;
+  if (!(gg = gate(c, gates, 3 * H, 4 * H, k_tanh))) goto done;
+  if (!(fc = add2(c, k_cmult, fg, args[5]))) goto done;
+  if (!(igg = add2(c, k_cmult, ig, gg))) goto done;
+  if (!(nc = add2(c, k_add, fc, igg))) goto done;
+  if (!(tc = add1(c, k_tanh, nc, Py_None))) goto done;
+  if (!(nh = add2(c, k_cmult, og, tc))) goto done;
+  ret = PyTuple_Pack(2, nh, nc);
+done:
+  Py_XDECREF(gates);
+  Py_XDECREF(ig);
+  Py_XDECREF(fg);
+  Py_XDECREF(og);
+  Py_XDECREF(gg);
+  Py_XDECREF(fc);
+  Py_XDECREF(igg);
+  Py_XDECREF(nc);
+  Py_XDECREF(tc);
+  Py_XDECREF(nh);
+  return ret;
+}
+
+
+/* one record + Node for the fast composite path; returns the node index */
+static Py_ssize_t emit(CoreObj* c, PyObject* kind, long code, const int32_t* idx, int n_in, PyObject* shape,
+                       const int64_t* ai, Py_ssize_t n_ai, PyObject* aux) {
+  if (put_record(c, code, idx, n_in, (ShapeObj*)shape, ai, n_ai, NULL, 0) < 0) return -1;
+  PyObject* tin = PyTuple_New(n_in);
+  if (!tin) return -1;
+  for (int k = 0; k < n_in; ++k) {
+    PyObject* v = PyLong_FromLong(idx[k]);
+    if (!v) {
+      Py_DECREF(tin);
+      return -1;
+    }
+    PyTuple_SET_ITEM(tin, k, v);
+  }
+  untrack(tin);
+  NodeObj* nd = (NodeObj*)NodeT->tp_alloc(NodeT, 0);
+  if (!nd) {
+    Py_DECREF(tin);
+    return -1;
+  }
+  untrack((PyObject*)nd);
+  nd->kind = Py_NewRef(kind);
+  nd->inputs = tin;
+  nd->shape = Py_NewRef(shape);
+  nd->aux = Py_NewRef(aux);
+  nd->code = code;
+  const int rc = PyList_Append(c->nodes, (PyObject*)nd);
+  Py_DECREF(nd);
+  return rc < 0 ? -1 : PyList_GET_SIZE(c->nodes) - 1;
+}
+
+static PyObject* new_expr(CoreObj* c, Py_ssize_t index) {
+  ExprObj* ex = (ExprObj*)ExprT->tp_alloc(ExprT, 0);
+  if (!ex) return NULL;
+  untrack((PyObject*)ex);
+  ex->graph = Py_NewRef(c->cg);
+  ex->index = index;
+  ex->generation = c->gen;
+  return (PyObject*)ex;
+}
+
+static long kind_code(PyObject* kind) {
+  PyObject* v = PyDict_GetItemWithError(FastKinds, kind);
+  return v ? PyLong_AsLong(v) : -1;
+}
+
+static long dim_at(ShapeObj* s, Py_ssize_t d) {
+  return d < PyTuple_GET_SIZE(s->dims) ? PyLong_AsLong(PyTuple_GET_ITEM(s->dims, d)) : -1;
+}
+
+/* GraphCore.lstm(b, wx, x, wh, h, c, H) -> (h', c'): the 14 nodes of
+   builders.py RNNBuilder._lstm (affine; i, f, o, g gate blocks; c' = f*c + i*g;
+   h' = o*tanh(c')), written straight into the record buffers with only the
+   two returned expressions materialised.  Anything irregular (re-registered
+   kinds, shape or batch mismatches, foreign expressions) takes the generic
+   node-by-node path, which raises the reference errors. */
+static PyObject* core_lstm(CoreObj* c, PyObject* const* args, Py_ssize_t nargs) {
+  if (nargs != 7) {
+    PyErr_SetString(PyExc_TypeError, "lstm(b, wx, x, wh, h, c, H)");
+    return NULL;
+  }
+  const long H = PyLong_AsLong(args[6]);
+  if (H == -1 && PyErr_Occurred()) return NULL;
+  const long c_aff = kind_code(k_affine), c_pick = kind_code(k_pick), c_log = kind_code(k_logistic),
+             c_tanh = kind_code(k_tanh), c_cm = kind_code(k_cmult), c_add = kind_code(k_add);
+  if (PyErr_Occurred()) return NULL;
+  const Py_ssize_t n_nodes = PyList_GET_SIZE(c->nodes);
+  int32_t in[6];
+  ShapeObj* sh[6];
+  int ok = c_aff >= 0 && c_pick >= 0 && c_log >= 0 && c_tanh >= 0 && c_cm >= 0 && c_add >= 0 && H > 0;
+  for (int k = 0; k < 6 && ok; ++k) {
+    PyObject* e = args[k];
+    if (!PyObject_TypeCheck(e, &ExprBaseType) || ((ExprObj*)e)->graph != c->cg || ((ExprObj*)e)->generation != c->gen ||
+        ((ExprObj*)e)->index < 0 || ((ExprObj*)e)->index >= n_nodes) {
+      ok = 0;
+      break;
+    }
+    in[k] = (int32_t)((ExprObj*)e)->index;
+    sh[k] = (ShapeObj*)((NodeObj*)PyList_GET_ITEM(c->nodes, in[k]))->shape;
+  }
+  /* b (4H) | wx (4H, X) | x (X) | wh (4H, H) | h (H) | c (H) */
+  if (ok) {
+    const long X = dim_at(sh[2], 0);
+    ok = PyTuple_GET_SIZE(sh[0]->dims) == 1 && dim_at(sh[0], 0) == 4 * H && PyTuple_GET_SIZE(sh[1]->dims) == 2 &&
+         dim_at(sh[1], 0) == 4 * H && dim_at(sh[1], 1) == X && PyTuple_GET_SIZE(sh[2]->dims) == 1 &&
+         PyTuple_GET_SIZE(sh[3]->dims) == 2 && dim_at(sh[3], 0) == 4 * H && dim_at(sh[3], 1) == H &&
+         PyTuple_GET_SIZE(sh[4]->dims) == 1 && dim_at(sh[4], 0) == H && PyTuple_GET_SIZE(sh[5]->dims) == 1 &&
+         dim_at(sh[5], 0) == H;
+    if (PyErr_Occurred()) return NULL;
+  }
+  long ba = 1, bn = 1;
+  if (ok) {
+    ba = sh[0]->batch;
+    for (int k = 1; k < 5; ++k) {
+      const long sb = sh[k]->batch;
+      if (sb != 1) {
+        if (ba != 1 && sb != ba) ok = 0;
+        ba = sb;
+      }
+    }
+    const long bc = sh[5]->batch;
+    if (!(bc == ba || bc == 1 || ba == 1)) ok = 0;
+    bn = ba > bc ? ba : bc;
+  }
+  if (!ok) return lstm_generic(c, args, H);
+
+  PyObject *shA = NULL, *shG = NULL, *shN = NULL, *rng[4] = {NULL, NULL, NULL, NULL}, *ret = NULL, *eh = NULL,
+           *ec = NULL;
+  Py_ssize_t base = n_nodes, r = 0;
+  if (!(shA = new_shape(sh[0]->dims, ba))) goto out;
+  if (!(shG = new_shape(sh[4]->dims, ba))) goto out;
+  if (bn == ba) {
+    shN = Py_NewRef(shG);
+  } else if (!(shN = new_shape(sh[4]->dims, bn))) {
+    goto out;
+  }
+  for (int q = 0; q < 4; ++q) {
+    if (!(rng[q] = Py_BuildValue("(ll)", q * H, (q + 1) * H))) goto out;
+    untrack(rng[q]);
+  }
+  {
+    const int32_t A = (int32_t)base;
+    const int32_t iA[5] = {in[0], in[1], in[2], in[3], in[4]};
+    r = emit(c, k_affine, c_aff, iA, 5, shA, NULL, 0, Py_None); /* base+0 */
+    for (int q = 0; q < 4 && r >= 0; ++q) {                      /* pick, act: base+1+2q, base+2+2q */
+      const int64_t lohi[2] = {(int64_t)q * H, (int64_t)(q + 1) * H};
+      r = emit(c, k_pick, c_pick, &A, 1, shG, lohi, 2, rng[q]);
+      if (r < 0) break;
+      const int32_t p = (int32_t)r;
+      r = q == 3 ? emit(c, k_tanh, c_tanh, &p, 1, shG, NULL, 0, Py_None)
+                 : emit(c, k_logistic, c_log, &p, 1, shG, NULL, 0, Py_None);
+    }
+    if (r < 0) goto out;
+    const int32_t ig = A + 2, fg = A + 4, og = A + 6, gg = A + 8;
+    const int32_t fc_in[2] = {fg, in[5]}, igg_in[2] = {ig, gg}, nc_in[2] = {A + 9, A + 10};
+    if ((r = emit(c, k_cmult, c_cm, fc_in, 2, shN, NULL, 0, Py_None)) < 0) goto out; /* base+9 */
+    if ((r = emit(c, k_cmult, c_cm, igg_in, 2, shG, NULL, 0, Py_None)) < 0) goto out; /* base+10 */
+    if ((r = emit(c, k_add, c_add, nc_in, 2, shN, NULL, 0, Py_None)) < 0) goto out; /* base+11 */
+    const int32_t nc = A + 11;
+    if ((r = emit(c, k_tanh, c_tanh, &nc, 1, shN, NULL, 0, Py_None)) < 0) goto out; /* base+12 */
+    const int32_t nh_in[2] = {og, A + 12};
+    if ((r = emit(c, k_cmult, c_cm, nh_in, 2, shN, NULL, 0, Py_None)) < 0) goto out; /* base+13 */
+    if (!(eh = new_expr(c, base + 13)) || !(ec = new_expr(c, base + 11))) goto out;
+    ret = PyTuple_Pack(2, eh, ec);
+  }
+out:
+  Py_XDECREF(shA);
+  Py_XDECREF(shG);
+  Py_XDECREF(shN);
+  for (int q = 0; q < 4; ++q) Py_XDECREF(rng[q]);
+  Py_XDECREF(eh);
+  Py_XDECREF(ec);
+  return ret;
+}
+
 static PyMethodDef core_methods[] = {
     {"add", (PyCFunction)(void (*)(void))core_add, METH_FASTCALL, "add(kind, inputs=(), aux=None) -> Expression"},
     {"renew", (PyCFunction)core_renew, METH_O, "renew(generation)"},
     {"pack", (PyCFunction)core_pack, METH_O, "pack(start) -> raw record pointers"},
+    {"lstm", (PyCFunction)(void (*)(void))core_lstm, METH_FASTCALL, "lstm(b, wx, x, wh, h, c, H) -> (h, c)"},
     {NULL}};
 
 static PyTypeObject CoreType = {PyVarObject_HEAD_INIT(NULL, 0).tp_name = "_dgcore.GraphCore",
@@ -738,7 +986,41 @@ static PyObject* mod_setup(PyObject* self, PyObject* args) {
   Py_RETURN_NONE;
 }
 
-static PyMethodDef mod_methods[] = {{"setup", mod_setup, METH_VARARGS, "register the Python subclasses"}, {NULL}};
+/* int_tuple(seq) == tuple(map(int, seq)), without a call per exact int */
+static PyObject* mod_int_tuple(PyObject* self, PyObject* seq) {
+  PyObject* t = PySequence_Tuple(seq);
+  if (!t) return NULL;
+  const Py_ssize_t n = PyTuple_GET_SIZE(t);
+  for (Py_ssize_t k = 0; k < n; ++k) {
+    PyObject* v = PyTuple_GET_ITEM(t, k);
+    if (PyLong_CheckExact(v)) continue;
+    PyObject* iv = PyNumber_Long(v);
+    if (!iv) {
+      Py_DECREF(t);
+      return NULL;
+    }
+    if (Py_REFCNT(t) == 1 && t != seq) {
+      PyTuple_SET_ITEM(t, k, iv);
+      Py_DECREF(v);
+    } else { /* PySequence_Tuple returned the caller's tuple: copy first */
+      PyObject* c = PyTuple_GetSlice(t, 0, n);
+      Py_DECREF(t);
+      if (!c) {
+        Py_DECREF(iv);
+        return NULL;
+      }
+      t = c;
+      Py_DECREF(PyTuple_GET_ITEM(t, k));
+      PyTuple_SET_ITEM(t, k, iv);
+    }
+  }
+  untrack(t);
+  return t;
+}
+
+static PyMethodDef mod_methods[] = {{"setup", mod_setup, METH_VARARGS, "register the Python subclasses"},
+                                    {"int_tuple", mod_int_tuple, METH_O, "tuple(map(int, seq))"},
+                                    {NULL}};
 
 static struct PyModuleDef moddef = {PyModuleDef_HEAD_INIT, "_dgcore", "native graph construction", -1, mod_methods};
 
@@ -749,6 +1031,12 @@ PyMODINIT_FUNC PyInit__dgcore(void) {
   PyObject* m = PyModule_Create(&moddef);
   if (!m) return NULL;
   s_shape = PyUnicode_InternFromString("shape");
+  k_affine = PyUnicode_InternFromString("affine");
+  k_pick = PyUnicode_InternFromString("pick_range");
+  k_logistic = PyUnicode_InternFromString("logistic");
+  k_tanh = PyUnicode_InternFromString("tanh");
+  k_cmult = PyUnicode_InternFromString("cmult");
+  k_add = PyUnicode_InternFromString("add");
   s_encode = PyUnicode_InternFromString("encode");
   s_handle = PyUnicode_InternFromString("handle");
   s_rows = PyUnicode_InternFromString("rows");

@@ -1,0 +1,110 @@
+"""Host-only checks of the native graph core (csrc/dgcore.c): the composite
+LSTM-cell builder must write exactly the nodes and records the node-by-node
+path writes (builders.py RNNBuilder._lstm), irregular inputs must take the
+node-by-node path and raise its errors, and the construction helpers keep the
+reference semantics (tuple(map(int, ids)) for batched lookups)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_1701_03980_b200 as dy
+from paper_1701_03980_b200 import ops
+from paper_1701_03980_b200._dgcore import int_tuple
+
+HDR = 13
+
+
+def _records(cg):
+    hdr, n, ins, n_ins, ai, n_ai, af, n_af = cg._core.pack(0)
+
+    def arr(ptr, count, ctype, dtype):
+        if count == 0:
+            return np.zeros(0, dtype)
+        return np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctype)), (count,)).copy()
+
+    return (arr(hdr, n * HDR, ctypes.c_int32, np.int32), arr(ins, n_ins, ctypes.c_int32, np.int32),
+            arr(ai, n_ai, ctypes.c_int64, np.int64), arr(af, n_af, ctypes.c_float, np.float32))
+
+
+def _aux(a):
+    if isinstance(a, dy.Tensor):
+        return ("tensor", tuple(a.shape.dims), a.shape.batch, np.asarray(a.data).tobytes())
+    if isinstance(a, tuple):
+        return tuple(_aux(v) for v in a)
+    if hasattr(a, "handle"):  # parameters of the two (separately built) models
+        return ("param", tuple(a.shape.dims) if hasattr(a, "shape") else (a.rows, a.dim))
+    return a
+
+
+def _nodes(cg):
+    return [(n.kind, tuple(n.inputs), tuple(n.shape.dims), n.shape.batch, _aux(n.aux)) for n in cg.nodes]
+
+
+def _build(native, H=8, X=6, batch_x=4, batch_state=1, steps=3):
+    pools = dy.new_poolset(64, 64, 64)
+    cg, model = dy.ComputationGraph(pools), dy.Model(pools, seed=1)
+    rnn = dy.RNNBuilder(model, 2, X, H, "lstm")
+    E = model.add_lookup_parameters(20, X)
+    saved = cg._core
+    if not native:
+        cg._core = None  # builders fall back to one ops call per node
+    try:
+        state = rnn.initial_state(cg)
+        if batch_state > 1:
+            zero = dy.Tensor(dy.Shape((H,), batch_state), np.zeros(H * batch_state, np.float32))
+            state.hs = [ops.input(cg, zero) for _ in state.hs]
+            state.cs = [ops.input(cg, zero) for _ in state.cs]
+        for t in range(steps):
+            x = ops.lookup_batch(cg, E, [(t + r) % 20 for r in range(batch_x)]) if batch_x > 1 else ops.lookup(cg, E, t)
+            state = state.add_input(x)
+        out = state.output()
+    finally:
+        cg._core = saved
+    return cg, out
+
+
+@pytest.mark.parametrize("batch_x,batch_state", [(1, 1), (4, 1), (4, 4), (1, 4)])
+def test_native_lstm_cell_matches_node_by_node_path(batch_x, batch_state):
+    cg_n, out_n = _build(True, batch_x=batch_x, batch_state=batch_state)
+    cg_p, out_p = _build(False, batch_x=batch_x, batch_state=batch_state)
+    assert _nodes(cg_n) == _nodes(cg_p)
+    assert out_n.index == out_p.index
+    for a, b in zip(_records(cg_n), _records(cg_p)):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_native_lstm_irregular_inputs_raise_like_ops():
+    pools = dy.new_poolset(64, 64, 64)
+    cg, model = dy.ComputationGraph(pools), dy.Model(pools, seed=1)
+    b = ops.parameter(cg, model.add_parameters((32,), "b"))
+    wx = ops.parameter(cg, model.add_parameters((32, 5), "wx"))
+    wh = ops.parameter(cg, model.add_parameters((32, 8), "wh"))
+    x = ops.input(cg, dy.Tensor(dy.Shape((6,)), np.zeros(6, np.float32)))  # wrong width
+    h = ops.input(cg, dy.Tensor(dy.Shape((8,)), np.zeros(8, np.float32)))
+    with pytest.raises(Exception) as native_err:
+        cg._core.lstm(b, wx, x, wh, h, h, 8)
+    with pytest.raises(Exception) as ops_err:
+        ops.affine(b, wx, x, wh, h)
+    assert type(native_err.value) is type(ops_err.value)
+
+
+def test_native_lstm_rejects_stale_expressions():
+    pools = dy.new_poolset(64, 64, 64)
+    cg, model = dy.ComputationGraph(pools), dy.Model(pools, seed=1)
+    b = ops.parameter(cg, model.add_parameters((32,), "b"))
+    cg.renew()
+    with pytest.raises(dy.errors.StaleExpression):
+        cg._core.lstm(b, b, b, b, b, b, 8)
+
+
+def test_int_tuple_is_tuple_map_int():
+    assert int_tuple([1, 2, 3]) == (1, 2, 3)
+    assert int_tuple((1, 2.0, np.int64(3))) == (1, 2, 3)
+    assert all(type(v) is int for v in int_tuple(np.arange(5)))
+    t = (4, 5)
+    assert int_tuple(t) is t
+    assert int_tuple(()) == ()
+    with pytest.raises(ValueError):
+        int_tuple(["x"])
