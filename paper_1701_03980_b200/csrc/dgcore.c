@@ -952,11 +952,106 @@ out:
   return ret;
 }
 
+/* one step through a stack of LSTM layers: pexprs[l] = (wx, wh, b); returns
+   (hs', cs') as new lists (builders.py RNNBuilder._step, cell = "lstm") */
+static int lstm_stack_step(CoreObj* c, PyObject* pexprs, PyObject* hs, PyObject* cs, PyObject* x, PyObject* Hobj,
+                           PyObject** nhs_out, PyObject** ncs_out) {
+  const Py_ssize_t L = PyList_GET_SIZE(pexprs);
+  PyObject* nhs = PyList_New(L);
+  PyObject* ncs = PyList_New(L);
+  if (!nhs || !ncs) goto fail;
+  PyObject* inp = x;
+  for (Py_ssize_t l = 0; l < L; ++l) {
+    PyObject* pe = PyList_GET_ITEM(pexprs, l);
+    if (!PyTuple_CheckExact(pe) || PyTuple_GET_SIZE(pe) != 3) {
+      PyErr_SetString(PyExc_TypeError, "layer parameters must be (wx, wh, b)");
+      goto fail;
+    }
+    PyObject* a[7] = {PyTuple_GET_ITEM(pe, 2), PyTuple_GET_ITEM(pe, 0), inp,   PyTuple_GET_ITEM(pe, 1),
+                      PyList_GET_ITEM(hs, l), PyList_GET_ITEM(cs, l), Hobj};
+    PyObject* r = core_lstm(c, a, 7);
+    if (!r) goto fail;
+    PyList_SET_ITEM(nhs, l, Py_NewRef(PyTuple_GET_ITEM(r, 0)));
+    PyList_SET_ITEM(ncs, l, Py_NewRef(PyTuple_GET_ITEM(r, 1)));
+    Py_DECREF(r);
+    inp = PyList_GET_ITEM(nhs, l);
+  }
+  *nhs_out = nhs;
+  *ncs_out = ncs;
+  return 0;
+fail:
+  Py_XDECREF(nhs);
+  Py_XDECREF(ncs);
+  return -1;
+}
+
+static int check_stack_args(PyObject* pexprs, PyObject* hs, PyObject* cs) {
+  if (!PyList_CheckExact(pexprs) || !PyList_CheckExact(hs) || !PyList_CheckExact(cs) ||
+      PyList_GET_SIZE(hs) != PyList_GET_SIZE(pexprs) || PyList_GET_SIZE(cs) != PyList_GET_SIZE(pexprs)) {
+    PyErr_SetString(PyExc_TypeError, "layer lists (params, hs, cs) must be lists of equal length");
+    return -1;
+  }
+  return 0;
+}
+
+/* GraphCore.lstm_step(pexprs, hs, cs, x, H) -> (hs', cs') */
+static PyObject* core_lstm_step(CoreObj* c, PyObject* const* args, Py_ssize_t nargs) {
+  if (nargs != 5) {
+    PyErr_SetString(PyExc_TypeError, "lstm_step(pexprs, hs, cs, x, H)");
+    return NULL;
+  }
+  if (check_stack_args(args[0], args[1], args[2]) < 0) return NULL;
+  PyObject *nhs, *ncs;
+  if (lstm_stack_step(c, args[0], args[1], args[2], args[3], args[4], &nhs, &ncs) < 0) return NULL;
+  PyObject* r = PyTuple_Pack(2, nhs, ncs);
+  Py_DECREF(nhs);
+  Py_DECREF(ncs);
+  return r;
+}
+
+/* GraphCore.lstm_transduce(pexprs, hs, cs, xs, H) -> [top h per step]
+   (builders.py RNNState.transduce over lstm_step) */
+static PyObject* core_lstm_transduce(CoreObj* c, PyObject* const* args, Py_ssize_t nargs) {
+  if (nargs != 5) {
+    PyErr_SetString(PyExc_TypeError, "lstm_transduce(pexprs, hs, cs, xs, H)");
+    return NULL;
+  }
+  if (check_stack_args(args[0], args[1], args[2]) < 0) return NULL;
+  PyObject* xs = PySequence_Fast(args[3], "xs must be a sequence");
+  if (!xs) return NULL;
+  const Py_ssize_t T = PySequence_Fast_GET_SIZE(xs);
+  PyObject* outs = PyList_New(T);
+  PyObject* hs = Py_NewRef(args[1]);
+  PyObject* cs = Py_NewRef(args[2]);
+  if (!outs) goto fail;
+  for (Py_ssize_t t = 0; t < T; ++t) {
+    PyObject *nhs, *ncs;
+    if (lstm_stack_step(c, args[0], hs, cs, PySequence_Fast_GET_ITEM(xs, t), args[4], &nhs, &ncs) < 0) goto fail;
+    Py_SETREF(hs, nhs);
+    Py_SETREF(cs, ncs);
+    PyList_SET_ITEM(outs, t, Py_NewRef(PyList_GET_ITEM(hs, PyList_GET_SIZE(hs) - 1)));
+  }
+  Py_DECREF(hs);
+  Py_DECREF(cs);
+  Py_DECREF(xs);
+  return outs;
+fail:
+  Py_XDECREF(outs);
+  Py_XDECREF(hs);
+  Py_XDECREF(cs);
+  Py_DECREF(xs);
+  return NULL;
+}
+
 static PyMethodDef core_methods[] = {
     {"add", (PyCFunction)(void (*)(void))core_add, METH_FASTCALL, "add(kind, inputs=(), aux=None) -> Expression"},
     {"renew", (PyCFunction)core_renew, METH_O, "renew(generation)"},
     {"pack", (PyCFunction)core_pack, METH_O, "pack(start) -> raw record pointers"},
     {"lstm", (PyCFunction)(void (*)(void))core_lstm, METH_FASTCALL, "lstm(b, wx, x, wh, h, c, H) -> (h, c)"},
+    {"lstm_step", (PyCFunction)(void (*)(void))core_lstm_step, METH_FASTCALL,
+     "lstm_step(pexprs, hs, cs, x, H) -> (hs, cs)"},
+    {"lstm_transduce", (PyCFunction)(void (*)(void))core_lstm_transduce, METH_FASTCALL,
+     "lstm_transduce(pexprs, hs, cs, xs, H) -> outputs"},
     {NULL}};
 
 static PyTypeObject CoreType = {PyVarObject_HEAD_INIT(NULL, 0).tp_name = "_dgcore.GraphCore",

@@ -424,63 +424,69 @@ static bool match_cell(const dg_graph* g, int h, const std::vector<int>& consume
   if (!inner(tcn) || Nd(tcn).kind != DG_OP_TANH) return false;
   const int c = in(tcn, 0);
   if (!in_set[c] || absorbed[c] || !is_vec(c, B)) return false;
-  // left-deep sum c = ((t0 + t1) + t2) or a single product
-  std::vector<int> adds_top_down, terms_rev;
+  // left-deep sum c = ((t0 + t1) + t2) or a single product (at most 3 terms;
+  // fixed arrays: this runs for every cmult of the graph)
+  int adds_top_down[2], terms[3];
+  int n_adds = 0, n_terms = 0;
   if (Nd(c).kind == DG_OP_CMULT) {
-    terms_rev.push_back(c);
+    terms[n_terms++] = c;
   } else if (Nd(c).kind == DG_OP_ADD) {
-    int x = c;
+    int x = c, rev[3], n_rev = 0;
     for (;;) {
-      adds_top_down.push_back(x);
+      if (n_adds == 2) return false;
+      adds_top_down[n_adds++] = x;
       const int l = in(x, 0), r = in(x, 1);
+      rev[n_rev++] = r;
       if (Nd(l).kind == DG_OP_ADD && inner(l)) {
-        terms_rev.push_back(r);
         x = l;
         continue;
       }
-      terms_rev.push_back(r);
-      terms_rev.push_back(l);
+      rev[n_rev++] = l;
       break;
     }
+    for (int k = 0; k < n_rev; ++k) terms[k] = rev[n_rev - 1 - k];
+    n_terms = n_rev;
   } else {
     return false;
   }
-  std::vector<int> terms(terms_rev.rbegin(), terms_rev.rend());
-  const int m = (int)terms.size() - 1;
+  const int m = n_terms - 1;
   if (m > 2) return false;
   int ig = -1, p_i = -1, p_g = -1, off_i = 0, off_g = 0;
-  std::vector<int> fterm, fact, fpick, fext, foff;
-  for (size_t t = 0; t < terms.size(); ++t) {
+  int fterm[2], fact[2], fpick[2], fext[2], foff[2], nf = 0;
+  for (int t = 0; t < n_terms; ++t) {
     const int x = terms[t];
     if (Nd(x).kind != DG_OP_CMULT) return false;
     if (m == 0 ? (x != c) : !inner(x)) return false;
     const int a = in(x, 0), b = in(x, 1);
     int pa, Ga, oa, pb, Gb, ob;
     if (ig < 0 && gate(a, DG_OP_LOGISTIC, pa, Ga, oa) && gate(b, DG_OP_TANH, pb, Gb, ob) && Ga == G && Gb == G) {
-      ig = (int)t; p_i = pa; off_i = oa; p_g = pb; off_g = ob;
+      ig = t; p_i = pa; off_i = oa; p_g = pb; off_g = ob;
       continue;
     }
     if (ig < 0 && gate(b, DG_OP_LOGISTIC, pa, Ga, oa) && gate(a, DG_OP_TANH, pb, Gb, ob) && Ga == G && Gb == G) {
-      ig = (int)t; p_i = pa; off_i = oa; p_g = pb; off_g = ob;
+      ig = t; p_i = pa; off_i = oa; p_g = pb; off_g = ob;
       continue;
     }
     int fa = -1, ext = -1;
     if (gate(a, DG_OP_LOGISTIC, pa, Ga, oa) && Ga == G) { fa = a; ext = b; }
     else if (gate(b, DG_OP_LOGISTIC, pa, Ga, oa) && Ga == G) { fa = b; ext = a; }
-    if (fa < 0) return false;
+    if (fa < 0 || nf == 2) return false;
     const Node& en = Nd(ext);
     if (en.rank != 1 || en.dims[0] != H || (en.batch != B && en.batch != 1)) return false;
-    fterm.push_back(x);
-    fact.push_back(fa);
-    fpick.push_back(pa);
-    fext.push_back(ext);
-    foff.push_back(oa);
+    fterm[nf] = x;
+    fact[nf] = fa;
+    fpick[nf] = pa;
+    fext[nf] = ext;
+    foff[nf] = oa;
+    ++nf;
   }
   if (ig < 0) return false;
   // the fused kernel sums i*g first: exact for two terms (commutative), and
   // for more terms only when the reference order already starts with i*g
   if (m >= 2 && ig != 0) return false;
   u = Unit();
+  u.nodes.reserve(9 + 4 * m);
+  u.ins.reserve(1 + m);
   u.type = U_CELL;
   u.m = m;
   u.H = H;
@@ -504,15 +510,18 @@ static bool match_cell(const dg_graph* g, int h, const std::vector<int>& consume
   u.nodes.push_back(g_act);
   u.nodes.push_back(terms[ig]);
   for (int k = 0; k < m; ++k) u.nodes.push_back(fterm[k]);
-  for (int k = (int)adds_top_down.size() - 1; k >= 0; --k) u.nodes.push_back(adds_top_down[k]);
+  for (int k = n_adds - 1; k >= 0; --k) u.nodes.push_back(adds_top_down[k]);
   u.nodes.push_back(tcn);
   u.nodes.push_back(h);
   // distinct internal nodes, none of them an external input
-  std::vector<int> all = u.nodes;
-  std::sort(all.begin(), all.end());
-  if (std::adjacent_find(all.begin(), all.end()) != all.end()) return false;
+  int all[32];
+  const int na = (int)u.nodes.size();
+  if (na > 32) return false;
+  std::copy(u.nodes.begin(), u.nodes.end(), all);
+  std::sort(all, all + na);
+  if (std::adjacent_find(all, all + na) != all + na) return false;
   for (int x : u.ins)
-    if (std::binary_search(all.begin(), all.end(), x)) return false;
+    if (std::binary_search(all, all + na, x)) return false;
   if ((int)u.nodes.size() != 9 + 4 * m) return false;  // + G and m external states = nslot
   return true;
 }
@@ -647,19 +656,24 @@ static std::vector<int> find_rnn_stacks(const dg_graph* g, const std::vector<Uni
     src[b] = a;
     cons[a] = b;
   }
-  // stacks: walk from each bottom chain (no src) up through consumers
-  std::vector<char> mark(N, 0);
+  // stacks: walk from each bottom chain (no src) up through consumers.
+  // mark / seen are stamped per stack (no O(N) clears per chain)
+  std::vector<int> mark(N, -1), seen(N, -1), dfs;
   for (int bot = 0; bot < nch; ++bot) {
     if (src[bot] >= 0) continue;
     std::vector<int> order;
     for (int x = bot; x >= 0; x = cons[x]) order.push_back(x);
     // the stack's nodes and external inputs
-    std::fill(mark.begin(), mark.end(), 0);
+    int lo = N;
     std::vector<int> ext;
     for (size_t li = 0; li < order.size(); ++li) {
       for (int k : chains[order[li]]) {
-        mark[ci[k].G] = 1;
-        for (int x : cells[k].nodes) mark[x] = 1;
+        mark[ci[k].G] = bot;
+        lo = std::min(lo, ci[k].G);
+        for (int x : cells[k].nodes) {
+          mark[x] = bot;
+          lo = std::min(lo, x);
+        }
       }
       const auto& ch = chains[order[li]];
       ext.push_back(ci[ch[0]].hp);
@@ -667,18 +681,31 @@ static std::vector<int> find_rnn_stacks(const dg_graph* g, const std::vector<Uni
       if (li == 0)
         for (int k : ch) ext.push_back(ci[k].x);
     }
-    // acyclic: no external input may depend on a node of the stack
-    std::vector<char> desc(N, 0);
-    for (int i : active) {
-      if (mark[i]) continue;
-      const Node& n = Nd(i);
-      for (int q = 0; q < n.n_in && !desc[i]; ++q) {
-        const int s2 = g->inputs[n.in_off + q];
-        desc[i] = mark[s2] || desc[s2];
+    // acyclic: no external input may depend on a node of the stack.  Inputs
+    // precede their consumers, so only ancestors with index > lo can be
+    // stack nodes: a backward walk bounded below by lo.
+    bool cyclic = false;
+    for (int x : ext) {
+      if (cyclic) break;
+      if (x < lo) continue;
+      dfs.clear();
+      dfs.push_back(x);
+      while (!dfs.empty() && !cyclic) {
+        const int i = dfs.back();
+        dfs.pop_back();
+        if (seen[i] == bot) continue;
+        seen[i] = bot;
+        if (mark[i] == bot) {
+          cyclic = true;
+          break;
+        }
+        const Node& n = Nd(i);
+        for (int q = 0; q < n.n_in; ++q) {
+          const int s2 = g->inputs[n.in_off + q];
+          if (s2 >= lo && seen[s2] != bot) dfs.push_back(s2);
+        }
       }
     }
-    bool cyclic = false;
-    for (int x : ext) cyclic = cyclic || desc[x] || mark[x];
     if (cyclic) continue;
     // geometry and device fit
     RnnStack st;
@@ -735,7 +762,32 @@ static std::vector<int> find_rnn_stacks(const dg_graph* g, const std::vector<Uni
 // Builds units (with cell fusion and add-chain rewrite) and the group order
 // for the node set `active` (ascending).  scope_hi bounds the consumer-count
 // scope.
+// host-side planning timers (DG_PLAN_TIMING=1 prints per call to stderr)
+struct PlanTimer {
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  const char* what;
+  std::string acc;
+  explicit PlanTimer(const char* w) : what(w) {
+    const char* e = std::getenv("DG_PLAN_TIMING");
+    on = e && e[0] == '1';
+    t0 = std::chrono::steady_clock::now();
+  }
+  void lap(const char* name) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    char buf[64];
+    std::snprintf(buf, sizeof buf, " %s %.0fus", name, std::chrono::duration<double, std::micro>(t - t0).count());
+    acc += buf;
+    t0 = t;
+  }
+  ~PlanTimer() {
+    if (on) std::fprintf(stderr, "[plan] %s:%s\n", what, acc.c_str());
+  }
+};
+
 static void build_schedule(const dg_graph* g, const std::vector<int>& active, int scope_hi, Schedule& S) {
+  PlanTimer tm("build_schedule");
   const int N = (int)g->nodes.size();
   S = Schedule();
   S.unit_of.assign(N, -1);
@@ -757,6 +809,7 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
       if (x.dims[d] != y.dims[d]) return false;
     return true;
   };
+  tm.lap("consumers");
   // gated cells first (they own their internal add chains)
   std::vector<char> absorbed(N, 0);
   std::vector<Unit> cells;
@@ -772,6 +825,7 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
       cells.push_back(std::move(cu));
     }
   }
+  tm.lap("cells");
   // LSTM chains / stacks over the matched cells (persistent recurrence path)
   std::vector<int> rnn_of(N, -1);
   {
@@ -782,6 +836,7 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
       rnn_of[cells[k].ins[0]] = stack_of[k];
     }
   }
+  tm.lap("rnn");
   std::vector<char> rnn_made(S.rnns.size(), 0);
   auto chainable_add = [&](int i) {
     const Node& n = g->nodes[i];
@@ -851,6 +906,7 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
     S.units.push_back(std::move(u));
   }
 
+  tm.lap("units");
   const int U = (int)S.units.size();
   if (U == 0) return;
   // unit dependency graph
@@ -891,6 +947,7 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
   std::vector<uint64_t> sig(U);
   for (int u = 0; u < U; ++u) sig[u] = unit_signature(g, S.units[u]);
 
+  tm.lap("deps+sig");
   // list scheduling
   std::unordered_map<uint64_t, std::vector<int>> ready;
   std::vector<uint64_t> ready_keys;  // insertion-ordered keys for determinism
@@ -947,6 +1004,7 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
     for (int c : newly) add_ready(c);
     ++level;
   }
+  tm.lap("list");
 }
 
 // Schedules depend only on the graph's structure (kinds, wiring, shapes,
@@ -1010,30 +1068,6 @@ static std::shared_ptr<const Schedule> get_schedule(const dg_graph* g, const std
   }
   return S;
 }
-
-// host-side planning timers (DG_PLAN_TIMING=1 prints per call to stderr)
-struct PlanTimer {
-  bool on;
-  std::chrono::steady_clock::time_point t0;
-  const char* what;
-  std::string acc;
-  explicit PlanTimer(const char* w) : what(w) {
-    const char* e = std::getenv("DG_PLAN_TIMING");
-    on = e && e[0] == '1';
-    t0 = std::chrono::steady_clock::now();
-  }
-  void lap(const char* name) {
-    if (!on) return;
-    const auto t = std::chrono::steady_clock::now();
-    char buf[64];
-    std::snprintf(buf, sizeof buf, " %s %.0fus", name, std::chrono::duration<double, std::micro>(t - t0).count());
-    acc += buf;
-    t0 = t;
-  }
-  ~PlanTimer() {
-    if (on) std::fprintf(stderr, "[plan] %s:%s\n", what, acc.c_str());
-  }
-};
 
 // ----------------------------------------------------------------- planning
 // A plan = host-built table blob + deferred launch closures that read the

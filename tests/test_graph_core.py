@@ -42,7 +42,7 @@ def _nodes(cg):
     return [(n.kind, tuple(n.inputs), tuple(n.shape.dims), n.shape.batch, _aux(n.aux)) for n in cg.nodes]
 
 
-def _build(native, H=8, X=6, batch_x=4, batch_state=1, steps=3):
+def _build(native, H=8, X=6, batch_x=4, batch_state=1, steps=3, transduce=False):
     pools = dy.new_poolset(64, 64, 64)
     cg, model = dy.ComputationGraph(pools), dy.Model(pools, seed=1)
     rnn = dy.RNNBuilder(model, 2, X, H, "lstm")
@@ -56,21 +56,29 @@ def _build(native, H=8, X=6, batch_x=4, batch_state=1, steps=3):
             zero = dy.Tensor(dy.Shape((H,), batch_state), np.zeros(H * batch_state, np.float32))
             state.hs = [ops.input(cg, zero) for _ in state.hs]
             state.cs = [ops.input(cg, zero) for _ in state.cs]
+        xs = []
         for t in range(steps):
             x = ops.lookup_batch(cg, E, [(t + r) % 20 for r in range(batch_x)]) if batch_x > 1 else ops.lookup(cg, E, t)
-            state = state.add_input(x)
-        out = state.output()
+            if transduce:
+                xs.append(x)
+            else:
+                state = state.add_input(x)
+        out = state.transduce(xs) if transduce else state.output()
     finally:
         cg._core = saved
     return cg, out
 
 
+@pytest.mark.parametrize("transduce", [False, True])
 @pytest.mark.parametrize("batch_x,batch_state", [(1, 1), (4, 1), (4, 4), (1, 4)])
-def test_native_lstm_cell_matches_node_by_node_path(batch_x, batch_state):
-    cg_n, out_n = _build(True, batch_x=batch_x, batch_state=batch_state)
-    cg_p, out_p = _build(False, batch_x=batch_x, batch_state=batch_state)
+def test_native_lstm_cell_matches_node_by_node_path(batch_x, batch_state, transduce):
+    cg_n, out_n = _build(True, batch_x=batch_x, batch_state=batch_state, transduce=transduce)
+    cg_p, out_p = _build(False, batch_x=batch_x, batch_state=batch_state, transduce=transduce)
     assert _nodes(cg_n) == _nodes(cg_p)
-    assert out_n.index == out_p.index
+    if transduce:
+        assert [e.index for e in out_n] == [e.index for e in out_p]
+    else:
+        assert out_n.index == out_p.index
     for a, b in zip(_records(cg_n), _records(cg_p)):
         np.testing.assert_array_equal(a, b)
 
