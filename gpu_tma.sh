@@ -1,5 +1,8 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 200 ./tools/tma_bench > gpurun_out/tma_bench.txt 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:tma_gemm_kernel -s 8 -c 1 -o gpurun_out/tma_fwd ./tools/tma_bench > /dev/null 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:tma_gemm_kernel -s 54 -c 1 -o gpurun_out/tma_dx ./tools/tma_bench > /dev/null 2>&1
+out=gpurun_out/tma_ep3.txt; : > $out
+timeout 120 ./tools/tma_bench 2>&1 | grep -v "with lo" >> $out; echo "rc=$?" >> $out
+for d in 1024 7168; do
+echo "== $d" >> $out
+TMA_PROF=1 DG_TMA_DBG=$d timeout 120 ./tools/tma_bench t 2>&1 | grep -E "phases|time" >> $out
+done

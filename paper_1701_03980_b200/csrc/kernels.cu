@@ -474,10 +474,102 @@ __global__ void row_kernel(RowArgs a) {
   }
 }
 
+// Wide rows (softmax / pnls over a vocabulary): one 256-thread block per row
+// with the row held in registers (kV float4 per thread), so x is read from
+// memory once: max, sum of exp and the output pass all run from registers.
+// Rows that are not 16 B aligned take the strided path above.
+template <int kOp, int kV>
+__global__ void __launch_bounds__(256) row_reg_kernel(RowArgs a) {
+  __shared__ float sh[32];
+  const int row = blockIdx.x;
+  const int j = row / a.batch, b = row - j * a.batch;
+  const int64_t off = (int64_t)b * a.width;
+  const float* x = a.in[j] + off;
+  float* gi = kOp == 3 ? a.gin[j] + off : nullptr;
+  float* o = kOp == 0 ? a.out[j] + off : nullptr;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(gi) |
+                         reinterpret_cast<uintptr_t>(o)) & 15) == 0;
+  if (!aligned) {  // block-uniform
+    const int tid = threadIdx.x;
+    float m = -INFINITY;
+    for (int c = tid; c < a.width; c += 256) m = fmaxf(m, x[c]);
+    m = row_reduce_max<true>(m, sh);
+    float s = 0.f;
+    for (int c = tid; c < a.width; c += 256) s += expf(x[c] - m);
+    s = row_reduce_sum<true>(s, sh);
+    if (kOp == 0) {
+      for (int c = tid; c < a.width; c += 256) o[c] = expf(x[c] - m) / s;
+    } else if (kOp == 2) {
+      if (tid == 0) a.out[j][b] = m + logf(s) - x[a.labels[row]];
+    } else {
+      const float g = a.gout[j][b];
+      const int lab = a.labels[row];
+      for (int c = tid; c < a.width; c += 256) {
+        float p = expf(x[c] - m) / s;
+        if (c == lab) p -= 1.f;
+        gi[c] += g * p;
+      }
+    }
+    return;
+  }
+  const int n4 = a.width >> 2;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  float4 v[kV];
+  float m = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < kV; ++i) {
+    const int q = threadIdx.x + 256 * i;
+    v[i] = q < n4 ? x4[q] : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    m = fmaxf(m, fmaxf(fmaxf(v[i].x, v[i].y), fmaxf(v[i].z, v[i].w)));
+  }
+  m = row_reduce_max<true>(m, sh);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < kV; ++i)
+    if (threadIdx.x + 256 * i < n4) s += expf(v[i].x - m) + expf(v[i].y - m) + expf(v[i].z - m) + expf(v[i].w - m);
+  s = row_reduce_sum<true>(s, sh);
+  if (kOp == 2) {
+    if (threadIdx.x == 0) a.out[j][b] = m + logf(s) - x[a.labels[row]];
+    return;
+  }
+  const float g = kOp == 3 ? a.gout[j][b] : 1.f;
+  const int lab = kOp == 3 ? a.labels[row] : -1;
+  float4* d4 = reinterpret_cast<float4*>(kOp == 3 ? gi : o);
+#pragma unroll
+  for (int i = 0; i < kV; ++i) {
+    const int q = threadIdx.x + 256 * i;
+    if (q >= n4) continue;
+    float4 p = make_float4(expf(v[i].x - m) / s, expf(v[i].y - m) / s, expf(v[i].z - m) / s, expf(v[i].w - m) / s);
+    if (kOp == 3) {
+      if ((lab >> 2) == q) {
+        const int e = lab & 3;
+        if (e == 0) p.x -= 1.f;
+        else if (e == 1) p.y -= 1.f;
+        else if (e == 2) p.z -= 1.f;
+        else p.w -= 1.f;
+      }
+      float4 d = d4[q];
+      d.x += g * p.x;
+      d.y += g * p.y;
+      d.z += g * p.z;
+      d.w += g * p.w;
+      d4[q] = d;
+    } else {
+      d4[q] = p;
+    }
+  }
+}
+
 template <int kOp>
 int launch_rows(const RowArgs& a, cudaStream_t s) {
   if (a.rows <= 0) return 0;
-  if (a.width > 512) {
+  if (a.width > 512 && (a.width & 3) == 0 && a.width <= 256 * 4 * 16 && kOp != 1) {
+    const int need = (a.width / 4 + 255) / 256;
+    if (need <= 4) row_reg_kernel<kOp, 4><<<a.rows, 256, 0, s>>>(a);
+    else if (need <= 8) row_reg_kernel<kOp, 8><<<a.rows, 256, 0, s>>>(a);
+    else if (need <= 12) row_reg_kernel<kOp, 12><<<a.rows, 256, 0, s>>>(a);
+    else row_reg_kernel<kOp, 16><<<a.rows, 256, 0, s>>>(a);
+  } else if (a.width > 512) {
     row_kernel<kOp, true><<<a.rows, 256, 0, s>>>(a);
   } else {
     const int rows_per_block = 8;
@@ -520,13 +612,26 @@ __global__ void segment_scatter_add_kernel(float* __restrict__ table_grad, int d
   const int k0 = seg[u], k1 = seg[u + 1];
   for (int c0 = 0; c0 < dim; c0 += 128) {
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int k = k0 + w; k < k1; k += 8) {
-      const float* r = src_rows[k];
+    // R rows in flight per warp (row pointers, then values, then the adds in
+    // row order): a long segment is latency-bound otherwise
+    constexpr int R = 8;
+    for (int k = k0 + w; k < k1; k += 8 * R) {
+      const float* rp[R];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = c0 + lane + 32 * q;
-        if (c < dim) acc[q] += r[c];
-      }
+      for (int r = 0; r < R; ++r) rp[r] = k + 8 * r < k1 ? src_rows[k + 8 * r] : nullptr;
+      float v[R][4];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = c0 + lane + 32 * q;
+          v[r][q] = rp[r] && c < dim ? rp[r][c] : 0.f;
+        }
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (rp[r]) acc[q] += v[r][q];
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) part[w][lane + 32 * q] = acc[q];

@@ -289,6 +289,7 @@ struct TmaGemmPlan {
   TmaGemmArgs args;
   bool a_mn, b_mn;
   bool conv;  // residuals formed in shared memory by converter warps (no lo copies)
+  bool a_tmem;  // conv with A's hi/lo split stored in TMEM (MMAs read only B from shared memory)
   const float* a_src;
   const float* b_src;
   float* a_lo;
@@ -299,10 +300,12 @@ struct TmaGemmPlan {
 };
 bool tma_gemm_enabled();  // DG_TMA=0 disables (A/B checks)
 bool tma_conv_enabled();  // DG_TMA_CONV=0: pre-split residual copies instead of in-smem conversion
+bool tma_at_enabled();    // DG_TMA_AT=0: A's split in shared memory instead of TMEM
 int64_t tma_lo_floats(int64_t rows, int64_t cols);
 bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out);
 // split_a / split_b: (re)compute the residual copies before the GEMM
 int launch_tma_gemm(const TmaGemmPlan& p, bool split_a, bool split_b, cudaStream_t s);
+int tma_prof_read(long long* out);  // diagnostics: DG_TMA_DBG bit 10 wait timestamps [5][256][2]
 
 // ------------------------------------------------------------- trainers
 struct TensorSeg { float* w; float* g; float* s0; float* s1; int64_t n; };

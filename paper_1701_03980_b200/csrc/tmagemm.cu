@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -51,6 +52,15 @@ constexpr int kSmem = kStages * kStageBytes + 1024;
 constexpr int kRawStagesC = 3;
 constexpr int kSmemConv = kRawStagesC * 4 * kOpBytes + 1024;
 constexpr int kChunk = 2;  // k-tiles per TMEM accumulation (K = 64)
+// A-in-TMEM variant: stages of A_raw | B_raw | B_lo (48 KiB) in shared memory;
+// the converter warps write A's hi/lo split straight into TMEM (columns
+// 256 + 64 s .. +63), so the MMAs read only B from shared memory
+constexpr int kStagesAT = 4;
+constexpr int kSmemAT = kStagesAT * 3 * kOpBytes + 1024;
+
+// DG_TMA_DBG bit 10: CTA 0 records (before, after) clock64 of each role's
+// per-k-tile wait (diagnostics; tools/tma_bench)
+__device__ long long g_tprof[6][256][2];
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -103,6 +113,37 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
+__device__ __forceinline__ void mma_tf32_ta(uint32_t tmem, uint32_t ta, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+      "r"(ta), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float lds32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+__device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
                : "memory");
@@ -112,19 +153,57 @@ __device__ __forceinline__ const float* orow(const Operand& o, int64_t i) {
   return o.rows ? o.rows[i] : o.base + i * o.ld;
 }
 
-template <bool kAMN, bool kBMN, bool kConv>
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+
+// ragged-N / unaligned tiles: element-wise stores (rare; kept out of line)
+__device__ __noinline__ void epilogue_scalar(const TmaGemmArgs& P, float* part, cgrp::cluster_group& cl, int S, int z,
+                                             int rows, int m0, int n0, bool has_bias) {
+  for (int e = threadIdx.x; e < rows * BN; e += blockDim.x) {
+    const int lr = e / BN, c = e % BN;
+    const int lm = z * rows + lr;
+    const int64_t m = m0 + lm, n = n0 + c;
+    if (m >= P.M || n >= P.N) continue;
+    const int sw = (c & ~3) + 4 * lm;
+    float v = 0.f;
+    for (int q = 0; q < S; ++q) v += (S > 1 ? cl.map_shared_rank(part, q) : part)[lm * BN + (sw & (BN - 1)) + (c & 3)];
+    float* crow = const_cast<float*>(orow(P.C, m));
+    if (has_bias) v += orow(P.bias, m)[n];
+    if (P.accumulate) v += crow[n];
+    crow[n] = v;
+  }
+}
+
+template <bool kAMN, bool kBMN, bool kConv, bool kAT = false>
 __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
     tma_gemm_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                     const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
                     const __grid_constant__ TmaGemmArgs P) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int NS = kConv ? kRawStagesC : kStages;  // raw operand stages
-  constexpr int SB = kStageBytes;  // stage stride: A_hi, B_hi, A_lo, B_lo (conv) / A_hi, A_lo, B_hi, B_lo
+  static_assert(!kAT || kConv, "A in TMEM needs the converter warps");
+  constexpr int NS = kAT ? kStagesAT : kConv ? kRawStagesC : kStages;  // raw operand stages
+  // stage stride: A_hi, B_hi, A_lo, B_lo (conv) / A_hi, A_lo, B_hi, B_lo / A, B, B_lo (A in TMEM)
+  constexpr int SB = kAT ? 3 * kOpBytes : kStageBytes;
+  constexpr uint32_t kTmemCols = kAT ? 512 : 2 * BN;
   __shared__ uint64_t full[NS], empty[NS], conv[NS], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#define WAITB0(b, ph) mbar_wait(b, ph)
+  const bool prof = (P.pad_ & 1024) && blockIdx.x == 0;
+#define WAITP(role, jj, b, ph)                                             \
+  do {                                                                     \
+    const long long tb_ = prof ? clock64() : 0;                            \
+    WAITB0(b, ph);                                                         \
+    if (prof && (jj) < 256) {                                              \
+      g_tprof[role][jj][0] = tb_;                                          \
+      g_tprof[role][jj][1] = clock64();                                    \
+    }                                                                      \
+  } while (0)
   const int S = P.splits;
+  const bool prof_e = prof && threadIdx.x == 64;
+  if (prof_e) g_tprof[5][0][0] = clock64();
   const int local = blockIdx.x;
   const int z = local % S, tile = local / S;
   // m-tiles fastest: CTAs that run together share the same B columns, so a
@@ -154,7 +233,7 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_sh)),
-                 "r"(2 * BN));
+                 "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -163,15 +242,15 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
   const uint32_t tmem = tmem_sh;
   const uint32_t sbase = su32(smem);
 
-  float vals[BN];  // epilogue: this thread's output row (blocked fp32 sums)
-#pragma unroll
-  for (int q = 0; q < BN; ++q) vals[q] = 0.f;
-
   if (warp == 0) {
     if (lane == 0) {
       for (int j = 0; j < nkt; ++j) {
         const int s = j % NS, use = j / NS;
-        if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+        if (use > 0) WAITP(0, j, &empty[s], (use - 1) & 1);
+        if (P.pad_ & 16) {  // DG_TMA_DBG bit 4: no loads
+          mbar_arrive(&full[s]);
+          continue;
+        }
         mbar_expect_tx(&full[s], kConv ? 2 * kOpBytes : kStageBytes);
         const uint32_t st = sbase + s * SB;
         const int k0 = (t0 + j) * BK;
@@ -201,16 +280,21 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = uidesc(kAMN, kBMN);
+      constexpr uint32_t idesc = uidesc(kAMN && !kAT, kBMN);
       for (int j = 0; j < nkt; ++j) {
         const int s = j % NS, use = j / NS;
         const int c = j / kChunk, a = c & 1;
-        if (j % kChunk == 0 && c >= 2) mbar_wait(&acc_empty[a], ((c >> 1) - 1) & 1);
-        if (kConv) mbar_wait(&conv[s], use & 1);
-        else mbar_wait(&full[s], use & 1);
+        if (j % kChunk == 0 && c >= 2) WAITP(1, j, &acc_empty[a], ((c >> 1) - 1) & 1);
+        if (kConv) WAITP(2, j, &conv[s], use & 1);
+        else WAITP(2, j, &full[s], use & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         uint32_t ah, al, bh, bl;
-        if (kConv) {
+        if (kAT) {
+          ah = tmem + 256u + 64u * (uint32_t)s;  // TMEM columns: hi, then lo at +32
+          al = ah + 32u;
+          bh = sbase + s * SB + kOpBytes;
+          bl = bh + kOpBytes;
+        } else if (kConv) {
           ah = sbase + s * SB;
           bh = ah + kOpBytes;
           al = ah + 2 * kOpBytes;
@@ -226,13 +310,75 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
         for (int ks = 0; ks < BK / 8; ++ks) {
           const uint32_t oa = kAMN ? ks * 1024 : ks * 32, ob = kBMN ? ks * 1024 : ks * 32;
           const uint32_t first = (j % kChunk == 0 && ks == 0) ? 0u : 1u;
+          if (P.pad_ & 1) continue;  // DG_TMA_DBG bit 0: no MMAs (pipeline timing only)
+          if (kAT) {
+            mma_tf32_ta(acc, ah + 8u * ks, udesc(bh + ob, kBMN), idesc, first);
+            mma_tf32_ta(acc, ah + 8u * ks, udesc(bl + ob, kBMN), idesc, 1u);
+            mma_tf32_ta(acc, al + 8u * ks, udesc(bh + ob, kBMN), idesc, 1u);
+            continue;
+          }
           mma_tf32(acc, udesc(ah + oa, kAMN), udesc(bh + ob, kBMN), idesc, first);
           mma_tf32(acc, udesc(ah + oa, kAMN), udesc(bl + ob, kBMN), idesc, 1u);
           mma_tf32(acc, udesc(al + oa, kAMN), udesc(bh + ob, kBMN), idesc, 1u);
         }
+        if (P.pad_ & 64) {  // DG_TMA_DBG bit 6 (with bit 0): plain arrives instead of commits
+          mbar_arrive(&empty[s]);
+          if (j % kChunk == kChunk - 1 || j == nkt - 1) mbar_arrive(&acc_full[a]);
+          continue;
+        }
         mma_commit(&empty[s]);
         if (j % kChunk == kChunk - 1 || j == nkt - 1) mma_commit(&acc_full[a]);
       }
+    }
+  } else if (kAT && warp >= 6) {
+    // converter warps 6..9 (TMEM lane quadrant q = warp % 4): B's residual
+    // into shared memory (elementwise, same swizzled layout) and A row
+    // m = 32 q + lane split into hi / lo and stored into TMEM (lane m,
+    // 32 columns each), then published to the tensor pipe
+    const int ct = threadIdx.x - 6 * 32;  // 0..127
+    const int q = warp & 3, m = 32 * q + lane;
+    for (int j = 0; j < nkt; ++j) {
+      const int s = j % NS, use = j / NS;
+      if (ct == 0) WAITP(3, j, &full[s], use & 1);
+      else WAITB0(&full[s], use & 1);
+      const uint32_t st = sbase + s * SB;
+      if (!(P.pad_ & 2)) {
+#pragma unroll
+        for (int i = 0; i < kOpBytes / 16 / 128; ++i) {
+          const uint32_t off = (uint32_t)(ct + i * 128) * 16u;
+          const float4 x = lds128(st + kOpBytes + off);
+          sts128(st + 2 * kOpBytes + off, make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w)));
+        }
+        uint32_t hi[32], lo[32];
+        if (!kAMN) {  // K-major SW128: row m is one 128 B line, 16 B chunk c at (c ^ (m & 7))
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 x = lds128(st + (uint32_t)m * 128u + ((uint32_t)(c ^ (m & 7)) << 4));
+            const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              hi[4 * c + e] = __float_as_uint(xv[e]) & 0xFFFFE000u;
+              lo[4 * c + e] = __float_as_uint(xv[e] - __uint_as_float(hi[4 * c + e]));
+            }
+          }
+        } else {  // MN-major box q {32 m, 32 k}, SW128 with 32 B atoms: chunk (lane / 8) ^ (k & 3)
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const float x = lds32(st + (uint32_t)q * 4096u + (uint32_t)k * 128u +
+                                  ((uint32_t)(((lane >> 3) ^ (k & 3))) << 5) + ((uint32_t)(lane & 7) << 2));
+            hi[k] = __float_as_uint(x) & 0xFFFFE000u;
+            lo[k] = __float_as_uint(x - __uint_as_float(hi[k]));
+          }
+        }
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 256u + 64u * (uint32_t)s;
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32u, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv[s]);
     }
   } else if (kConv && warp >= 6) {
     // converter warps 6..9: residual lo = x - tf32(x) of the landed hi tiles
@@ -240,11 +386,12 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
     const int ct = threadIdx.x - 6 * 32;  // 0..127
     for (int j = 0; j < nkt; ++j) {
       const int s = j % NS, use = j / NS;
-      mbar_wait(&full[s], use & 1);
+      if (ct == 0) WAITP(3, j, &full[s], use & 1);
+      else WAITB0(&full[s], use & 1);
       char* st = smem + s * SB;
       char* lo = st + 2 * kOpBytes;
 #pragma unroll
-      for (int op = 0; op < 2; ++op) {
+      for (int op = 0; op < 2 && !(P.pad_ & 2); ++op) {  // DG_TMA_DBG bit 1: no conversion
         const float4* src = reinterpret_cast<const float4*>(st + op * kOpBytes);
         float4* dst = reinterpret_cast<float4*>(lo + op * kOpBytes);
 #pragma unroll
@@ -258,19 +405,23 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
           dst[ct + i * 128] = y;
         }
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (!(P.pad_ & 128)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // bit 7: no fence
       __syncwarp();
       if (lane == 0) mbar_arrive(&conv[s]);
     }
   } else {
     // epilogue warps 2..5 -> TMEM lane quadrant warp % 4
     const int quad = warp & 3;
+    float vals[BN];  // this thread's output row (blocked fp32 sums)
+#pragma unroll
+    for (int q = 0; q < BN; ++q) vals[q] = 0.f;
     for (int c = 0; c < nchunks; ++c) {
       const int a = c & 1;
-      mbar_wait(&acc_full[a], (c >> 1) & 1);
+      if (threadIdx.x == 64) WAITP(4, c, &acc_full[a], (c >> 1) & 1);
+      else WAITB0(&acc_full[a], (c >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-      for (int h = 0; h < BN / 32; ++h) {
+      for (int h = 0; h < BN / 32 && !(P.pad_ & 4); ++h) {  // DG_TMA_DBG bit 2: no drains
         uint32_t r[32];
         const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(a * BN + h * 32);
         asm volatile(
@@ -290,88 +441,88 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[a]);
     }
+    // stage the tile's fp32 sums through shared memory: the last acc_full
+    // covers every MMA, so every operand stage has been consumed.  Rows are
+    // rotated by 4*row floats against bank conflicts; all warps then write
+    // whole rows (coalesced 512 B per row) below
+    if (prof_e) g_tprof[5][1][0] = clock64();
+    if (!(P.pad_ & 8)) {
+      float* part = reinterpret_cast<float*>(smem);  // 128 x 128 fp32 = 64 KiB
+      const int lrow = quad * 32 + lane;
+#pragma unroll
+      for (int q = 0; q < BN; q += 4)
+        *reinterpret_cast<float4*>(part + lrow * BN + ((q + 4 * lrow) & (BN - 1))) =
+            make_float4(vals[q], vals[q + 1], vals[q + 2], vals[q + 3]);
+    }
   }
+  if (prof_e) g_tprof[5][2][0] = clock64();
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();  // every MMA drained and every stage consumed
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+  if (prof_e) g_tprof[5][3][0] = clock64();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 
+  if (P.pad_ & 8) return;  // DG_TMA_DBG bit 3: no epilogue
   const bool has_bias = P.bias.rows != nullptr || P.bias.base != nullptr;
-  // stage the tile's fp32 sums through shared memory (the operand ring is
-  // free), rows rotated by 4*row floats against bank conflicts, then write
-  // whole rows with all warps (coalesced 512 B per row)
-  float* part = reinterpret_cast<float*>(smem);  // 128 x 128 fp32 = 64 KiB
-  if (warp >= 2 && warp < 6) {
-    const int lrow = (warp & 3) * 32 + lane;
-#pragma unroll
-    for (int q = 0; q < BN; q += 4)
-      *reinterpret_cast<float4*>(part + lrow * BN + ((q + 4 * lrow) & (BN - 1))) =
-          make_float4(vals[q], vals[q + 1], vals[q + 2], vals[q + 3]);
-  }
+  float* part = reinterpret_cast<float*>(smem);
   cgrp::cluster_group cl = cgrp::this_cluster();
   if (S > 1) cl.sync();
   else __syncthreads();
+  if (prof_e) g_tprof[5][4][0] = clock64();
   const int rows = BM / S;  // S is a power of two <= 8: split z reduces rows [z*rows, (z+1)*rows)
   const bool vec = P.c_vec && n0 + BN <= P.N;
-  const int total = rows * (BN / 4);
-  constexpr int U = 4;  // loads of U slots are issued before any store (no dependent DRAM round trips)
+  // thread -> fixed 4-column slot ln (NT is a multiple of 32) and rows
+  // r0, r0 + RS, ...: a warp writes one whole 512 B row segment per store;
+  // U rows per batch with every load issued before the first store.  Kept
+  // compact: the kernel's instruction footprint is what the epilogue pays
   constexpr int NT = kConv ? kThreadsConv : kThreads;
-  for (int e0 = threadIdx.x; e0 < total; e0 += U * NT) {
-    float4 acc4[U], old4[U], b4[U];
+  constexpr int RS = NT / 32;
+  constexpr int U = 4;
+  const int ln = (threadIdx.x & 31) * 4;
+  if (!vec) {
+    epilogue_scalar(P, part, cl, S, z, rows, m0, n0, has_bias);
+  } else {
+    const bool bias_bcast = has_bias && !P.bias.rows && P.bias.ld == 0;
+    const float4 bconst =
+        bias_bcast ? *reinterpret_cast<const float4*>(P.bias.base + n0 + ln) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float* src[8];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * NT;
-      acc4[u] = old4[u] = b4[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (e >= total) continue;
-      const int lm = z * rows + e / (BN / 4), ln = (e % (BN / 4)) * 4;
-      const int64_t m = m0 + lm;
-      if (m >= P.M || !vec) continue;
-      if (P.accumulate) old4[u] = *reinterpret_cast<const float4*>(orow(P.C, m) + n0 + ln);
-      if (has_bias) b4[u] = *reinterpret_cast<const float4*>(orow(P.bias, m) + n0 + ln);
-    }
+    for (int q = 0; q < 8; ++q) src[q] = q < S ? (S > 1 ? cl.map_shared_rank(part, q) : part) : part;
+#pragma unroll 1
+    for (int rb = (int)(threadIdx.x >> 5); rb < rows; rb += U * RS) {
+      float4 acc4[U];
+      const float* brow[U];
+      float* crow[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * NT;
-      if (e >= total) continue;
-      const int lm = z * rows + e / (BN / 4), ln = (e % (BN / 4)) * 4;
-      const int sw = (ln + 4 * lm) & (BN - 1);
-      for (int q = 0; q < S; ++q) {
-        const float4 x = *reinterpret_cast<const float4*>((S > 1 ? cl.map_shared_rank(part, q) : part) + lm * BN + sw);
-        acc4[u].x += x.x;
-        acc4[u].y += x.y;
-        acc4[u].z += x.z;
-        acc4[u].w += x.w;
+      for (int u = 0; u < U; ++u) {
+        const int lr = rb + u * RS;
+        const int64_t m = m0 + z * rows + lr;
+        const bool ok = lr < rows && m < P.M;
+        crow[u] = ok ? const_cast<float*>(orow(P.C, m)) + n0 + ln : nullptr;
+        brow[u] = ok && has_bias && !bias_bcast ? orow(P.bias, m) + n0 + ln : nullptr;
+        acc4[u] = bconst;
       }
-    }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * NT;
-      if (e >= total) continue;
-      const int lm = z * rows + e / (BN / 4), ln = (e % (BN / 4)) * 4;
-      const int64_t m = m0 + lm;
-      if (m >= P.M) continue;
-      float* crow = const_cast<float*>(orow(P.C, m));
-      if (vec) {
-        float4 v = acc4[u];
-        v.x += b4[u].x; v.y += b4[u].y; v.z += b4[u].z; v.w += b4[u].w;
-        v.x += old4[u].x; v.y += old4[u].y; v.z += old4[u].z; v.w += old4[u].w;
-        *reinterpret_cast<float4*>(crow + n0 + ln) = v;
-      } else {
-        const float* brow = has_bias ? orow(P.bias, m) : nullptr;
-        const float sv[4] = {acc4[u].x, acc4[u].y, acc4[u].z, acc4[u].w};
+      for (int u = 0; u < U; ++u) {
+        if (!crow[u]) continue;
+        if (P.accumulate) acc4[u] = f4add(acc4[u], *reinterpret_cast<const float4*>(crow[u]));
+        if (brow[u]) acc4[u] = f4add(acc4[u], *reinterpret_cast<const float4*>(brow[u]));
+      }
+#pragma unroll 1
+      for (int q = 0; q < S; ++q) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int64_t n = n0 + ln + q;
-          if (n < P.N) {
-            float v = sv[q];
-            if (brow) v += brow[n];
-            if (P.accumulate) v += crow[n];
-            crow[n] = v;
-          }
+        for (int u = 0; u < U; ++u) {
+          const int lm = z * rows + rb + u * RS;
+          if (rb + u * RS < rows)
+            acc4[u] = f4add(acc4[u], *reinterpret_cast<const float4*>(src[q] + lm * BN + ((ln + 4 * lm) & (BN - 1))));
         }
       }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (crow[u] && !(P.pad_ & 2048)) *reinterpret_cast<float4*>(crow[u]) = acc4[u];
     }
   }
   if (S > 1) cl.sync();
+  if (prof_e) g_tprof[5][5][0] = clock64();
 }
 
 // lo[r][c] = x - tf32(x) for up to two rows x cols blocks (A and B of one
@@ -435,6 +586,18 @@ bool make_map(CUtensorMap* m, const float* base, int64_t ld, int64_t rows, int64
 
 }  // namespace
 
+int tma_prof_read(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_tprof, sizeof(g_tprof)) == cudaSuccess ? 0 : -1;  // [6][256][2]
+}
+
+bool tma_at_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DG_TMA_AT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool tma_conv_enabled() {
   static const bool on = [] {
     const char* e = getenv("DG_TMA_CONV");
@@ -483,6 +646,7 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
   p.b_colsp = bcp;
   p.b_lo = o.B_lo;
   p.conv = tma_conv_enabled();
+  p.a_tmem = p.conv && tma_at_enabled();
   if (!make_map(&p.mAh, o.A, o.lda, ar, ac, o.a_mn) || !make_map(&p.mBh, o.B, o.ldb, br, bc, o.b_mn)) return false;
   if (p.conv) {  // residuals formed in shared memory: no lo copies, no lo maps
     p.mAl = p.mAh;
@@ -507,8 +671,22 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
       S = s2;
     }
   }
+  // DG_TMA_DBG (diagnostics, tools/tma_bench): bits 0-4 skip MMAs /
+  // conversion / drains / epilogue / loads, bit 6 plain arrives for commits,
+  // bit 7 no proxy fence, bit 10 CTA-0 wait timeline, bits 11-12 skip
+  // epilogue stores / reductions, bits 16-19 force the split factor
+  static const int dbg = [] {
+    const char* e = getenv("DG_TMA_DBG");
+    return e ? (int)strtol(e, nullptr, 0) : 0;
+  }();
+  a.pad_ = dbg & 0xFFFF;
+  if ((dbg >> 16) & 0xF) S = (dbg >> 16) & 0xF;
   a.splits = S;
   p.ctas = tiles * S;
+  if (dbg & 0x100000)  // DG_TMA_DBG bit 20: log each planned GEMM
+    fprintf(stderr, "[tma] M %d N %d K %d a_mn %d b_mn %d acc %d bias %d rows %d split %d ctas %d\n", o.M, o.N, o.K,
+            (int)o.a_mn, (int)o.b_mn, o.accumulate, (int)(o.bias.base || o.bias.rows), (int)(o.C.rows != nullptr), S,
+            p.ctas);
   p.flops = 2.0 * o.M * (double)o.N * o.K;
   *out = p;
   return true;
@@ -530,14 +708,17 @@ int launch_tma_gemm(const TmaGemmPlan& p, bool split_a, bool split_b, cudaStream
     }
   }
   using K = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const TmaGemmArgs);
-  static const K table[8] = {tma_gemm_kernel<false, false, false>, tma_gemm_kernel<false, true, false>,
-                             tma_gemm_kernel<true, false, false>,  tma_gemm_kernel<true, true, false>,
-                             tma_gemm_kernel<false, false, true>,  tma_gemm_kernel<false, true, true>,
-                             tma_gemm_kernel<true, false, true>,   tma_gemm_kernel<true, true, true>};
-  const int ki = (p.conv ? 4 : 0) + (p.a_mn ? 2 : 0) + (p.b_mn ? 1 : 0);
+  static const K table[12] = {
+      tma_gemm_kernel<false, false, false>,      tma_gemm_kernel<false, true, false>,
+      tma_gemm_kernel<true, false, false>,       tma_gemm_kernel<true, true, false>,
+      tma_gemm_kernel<false, false, true>,       tma_gemm_kernel<false, true, true>,
+      tma_gemm_kernel<true, false, true>,        tma_gemm_kernel<true, true, true>,
+      tma_gemm_kernel<false, false, true, true>, tma_gemm_kernel<false, true, true, true>,
+      tma_gemm_kernel<true, false, true, true>,  tma_gemm_kernel<true, true, true, true>};
+  const int ki = (p.a_tmem ? 8 : p.conv ? 4 : 0) + (p.a_mn ? 2 : 0) + (p.b_mn ? 1 : 0);
   const K k = table[ki];
-  static bool attr[8] = {false, false, false, false, false, false, false, false};
-  const int smem = p.conv ? kSmemConv : kSmem;
+  static bool attr[12] = {};
+  const int smem = p.a_tmem ? kSmemAT : p.conv ? kSmemConv : kSmem;
   if (!attr[ki]) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
     attr[ki] = true;

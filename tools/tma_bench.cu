@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "../paper_1701_03980_b200/csrc/kernels.cuh"
@@ -93,6 +94,30 @@ static void run(const char* name, int M, int N, int K, bool a_mn, bool b_mn, boo
     printf("check %-26s M%5d N%5d K%5d a_mn %d b_mn %d split %d  max|err| %.3e (scale %.3e, rel %.2e) %s\n", name, M,
            N, K, a_mn, b_mn, p.args.splits, worst, scale, worst / scale, worst / scale < 5e-6 ? "OK" : "FAIL");
   }
+  if (getenv("TMA_PROF")) {  // DG_TMA_DBG bit 10: CTA 0 wait timeline of one launch
+    CK(cudaDeviceSynchronize());
+    launch_tma_gemm(p, false, false, 0);
+    CK(cudaDeviceSynchronize());
+    static long long t[6][256][2];
+    tma_prof_read(&t[0][0][0]);
+    long long base = t[2][0][0];
+    const char* role[5] = {"prod empty", "mma acc_empty", "mma conv", "conv full", "epi acc_full"};
+    printf("prof %s (cycles rel. to first MMA wait; wait duration)\n", name);
+    for (int r = 0; r < 5; ++r) {
+      printf("  %-14s", role[r]);
+      int shown = 0;
+      for (int j = 0; j < 256 && shown < 24; ++j) {
+        if (t[r][j][0] == 0 && t[r][j][1] == 0) continue;
+        printf(" [%d]%lld+%lld", j, t[r][j][0] - base, t[r][j][1] - t[r][j][0]);
+        ++shown;
+      }
+      printf("\n");
+    }
+    printf("  phases (clk from kernel start): mainloop end %lld, part stored %lld, sync %lld, cluster sync %lld, end %lld\n",
+           t[5][1][0] - t[5][0][0], t[5][2][0] - t[5][0][0], t[5][3][0] - t[5][0][0], t[5][4][0] - t[5][0][0],
+           t[5][5][0] - t[5][0][0]);
+    memset(t, 0, sizeof t);
+  }
   if (reps > 0) {
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
@@ -122,7 +147,14 @@ static void run(const char* name, int M, int N, int K, bool a_mn, bool b_mn, boo
   if (bias) cudaFree(bias);
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) {  // timing only (diagnostic variants via DG_TMA_DBG / DG_TMA_CONV)
+    run("fwd 2176x10000x256", 2176, 10000, 256, false, true, false, 20);
+    run("dX 2176x256x10000", 2176, 256, 10000, false, false, false, 20);
+    run("dW 256x10000x2176", 256, 10000, 2176, true, true, false, 20);
+    run("dW LSTM 512x1024x2240", 512, 1024, 2240, true, true, false, 20);
+    return 0;
+  }
   run("kmajor/kmajor", 256, 256, 96, false, false, true, 0);
   run("kmajor A / mn B", 256, 384, 128, false, true, true, 0);
   run("mn A / kmajor B", 256, 256, 160, true, false, true, 0);
