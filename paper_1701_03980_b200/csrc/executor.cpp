@@ -193,6 +193,7 @@ struct dg_graph_impl;
 }  // namespace dg
 
 struct dg_graph {
+  std::vector<char> bwd_overwrite;  // per node: grad slot overwritten by its only contributor (backward plan)
   int device = 0;
   cudaStream_t stream = nullptr;
   char* fwd_base = nullptr;
@@ -2585,6 +2586,8 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
           a.rows = n * in0.batch;
           a.width = (int)in0.elem;
           const bool pnls = gr.kind != DG_OP_SOFTMAX;
+          const int x0 = g->inputs[n0.in_off];
+          a.overwrite = pnls && x0 < (int)g->bwd_overwrite.size() && g->bwd_overwrite[x0] ? 1 : 0;
           size_t ol = 0;
           if (pnls) {
             std::vector<int32_t> labels;
@@ -2842,6 +2845,34 @@ int dg_backward(dg_graph* g, int32_t loss) {
   const Schedule& S = *Sp;
   tm.lap("schedule");
 
+  // slots written whole by their only contributor (the logits under a
+  // pickneglogsoftmax group): placed after the zeroed range and overwritten
+  // instead of accumulated, so the arena memset and the kernel's read of the
+  // slot both skip them (a vocabulary-wide slot is the largest in the graph)
+  std::vector<char>& overwrite = g->bwd_overwrite;
+  overwrite.assign(loss + 1, 0);
+  {
+    std::vector<int> cons(loss + 1, 0);
+    for (int i : active) {
+      const Node& x = g->nodes[i];
+      for (int k = 0; k < x.n_in; ++k) cons[g->inputs[x.in_off + k]]++;
+    }
+    for (const Group& gr : S.groups) {
+      if (gr.kind != DG_OP_PNLS && gr.kind != DG_OP_PNLS_BATCH) continue;
+      bool ok = true;
+      std::vector<int> xs;
+      for (int u : gr.units) {
+        const int pn = S.units[u].last();
+        const int x = g->inputs[g->nodes[pn].in_off];
+        const int kx = g->nodes[x].kind;
+        ok = ok && x != loss && cons[x] == 1 && kx != DG_OP_PARAMETER && kx != DG_OP_LOOKUP &&
+             kx != DG_OP_LOOKUP_BATCH && kx != DG_OP_INPUT;
+        xs.push_back(x);
+      }
+      if (ok)
+        for (int x : xs) overwrite[x] = 1;
+    }
+  }
   // placement of grad slots: group order for scheduled units, then the rest
   const size_t begin = g->bwd_cursor;
   size_t cur = begin;
@@ -2855,7 +2886,11 @@ int dg_backward(dg_graph* g, int32_t loss) {
   };
   for (const Group& gr : S.groups)
     for (int u : gr.units)
-      for (int i : S.units[u].nodes) place(i);
+      for (int i : S.units[u].nodes)
+        if (!overwrite[i]) place(i);
+  for (int i = 0; i <= loss; ++i)
+    if (!overwrite[i]) place(i);
+  const size_t zero_end = cur;
   for (int i = 0; i <= loss; ++i) place(i);
   // parameter nodes accumulate straight into the parameter's gradient (the
   // default sink adds the slot to p.gradient, graph.py:54-55)
@@ -2869,7 +2904,7 @@ int dg_backward(dg_graph* g, int32_t loss) {
   // zero the fresh slots (arena contract, graph.py:146-148) and seed dloss = 1
   {
     char* z0 = g->bwd_base + begin;
-    const size_t zn = cur - begin;
+    const size_t zn = zero_end - begin;
     float* seed = g->nodes[loss].grad;
     plan.ops.push_back([z0, zn, seed, st](char*) {
       if (cudaMemsetAsync(z0, 0, zn, st) != cudaSuccess) return -1;

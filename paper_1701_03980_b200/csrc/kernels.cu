@@ -469,7 +469,7 @@ __global__ void row_kernel(RowArgs a) {
     for (int c = tid; c < a.width; c += stride) {
       float p = expf(x[c] - m) / s;
       if (c == lab) p -= 1.f;
-      gi[c] += g * p;
+      gi[c] = (a.overwrite ? 0.f : gi[c]) + g * p;
     }
   }
 }
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(256) row_reg_kernel(RowArgs a) {
       for (int c = tid; c < a.width; c += 256) {
         float p = expf(x[c] - m) / s;
         if (c == lab) p -= 1.f;
-        gi[c] += g * p;
+        gi[c] = (a.overwrite ? 0.f : gi[c]) + g * p;
       }
     }
     return;
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(256) row_reg_kernel(RowArgs a) {
         else if (e == 2) p.z -= 1.f;
         else p.w -= 1.f;
       }
-      float4 d = d4[q];
+      float4 d = a.overwrite ? make_float4(0.f, 0.f, 0.f, 0.f) : d4[q];
       d.x += g * p.x;
       d.y += g * p.y;
       d.z += g * p.z;
@@ -598,13 +598,16 @@ __global__ void gather_rows_kernel(const float* __restrict__ table, int dim, con
   }
 }
 
+constexpr int kScatterWarps = 32;
+
 __global__ void segment_scatter_add_kernel(float* __restrict__ table_grad, int dim, const int64_t* __restrict__ ids,
                                            const int* __restrict__ seg, const float* const* src_rows, int n_unique,
                                            float scale) {
-  // one block per unique id; warp w sums rows k0+w, k0+w+8, ... (a long
-  // segment, e.g. the EOS padding id, is spread over 8 warps), then the 8
-  // partials are reduced in fixed warp order: deterministic, no atomics.
-  __shared__ float part[8][128];
+  // one block per unique id; warp w sums rows k0+w, k0+w+W, ... (a long
+  // segment, e.g. the EOS padding id, is spread over W = 32 warps), then the
+  // W partials are reduced in fixed warp order: deterministic, no atomics.
+  constexpr int W = kScatterWarps;
+  __shared__ float part[W][128];
   const int u = blockIdx.x;
   if (u >= n_unique) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -615,10 +618,10 @@ __global__ void segment_scatter_add_kernel(float* __restrict__ table_grad, int d
     // R rows in flight per warp (row pointers, then values, then the adds in
     // row order): a long segment is latency-bound otherwise
     constexpr int R = 8;
-    for (int k = k0 + w; k < k1; k += 8 * R) {
+    for (int k = k0 + w; k < k1; k += W * R) {
       const float* rp[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) rp[r] = k + 8 * r < k1 ? src_rows[k + 8 * r] : nullptr;
+      for (int r = 0; r < R; ++r) rp[r] = k + W * r < k1 ? src_rows[k + W * r] : nullptr;
       float v[R][4];
 #pragma unroll
       for (int r = 0; r < R; ++r)
@@ -641,7 +644,7 @@ __global__ void segment_scatter_add_kernel(float* __restrict__ table_grad, int d
       if (c < dim) {
         float s = 0.f;
 #pragma unroll
-        for (int ww = 0; ww < 8; ++ww) s += part[ww][threadIdx.x];
+        for (int ww = 0; ww < W; ++ww) s += part[ww][threadIdx.x];
         dst[c] += scale * s;
       }
     }
@@ -1013,7 +1016,8 @@ int launch_gather_rows(const float* table, int dim, const int64_t* ids, float* c
 int launch_segment_scatter_add(float* table_grad, int dim, const int64_t* uniq_ids, const int* seg,
                                const float* const* src_rows, int n_unique, float scale, cudaStream_t s) {
   if (n_unique <= 0) return 0;
-  segment_scatter_add_kernel<<<n_unique, 256, 0, s>>>(table_grad, dim, uniq_ids, seg, src_rows, n_unique, scale);
+  segment_scatter_add_kernel<<<n_unique, 32 * kScatterWarps, 0, s>>>(table_grad, dim, uniq_ids, seg, src_rows,
+                                                                      n_unique, scale);
   return 1;
 }
 

@@ -167,6 +167,7 @@ struct RowArgs {
   const float* const* gout;  // [n]
   const float* const* oval;  // [n] (softmax backward)
   float* const* gin;         // [n]
+  int overwrite;             // pnls backward: gin = (no accumulate; the slot's only contributor)
 };
 int launch_softmax_fwd(const RowArgs& a, cudaStream_t s);
 int launch_softmax_bwd(const RowArgs& a, cudaStream_t s);
