@@ -3026,8 +3026,9 @@ int dg_backward(dg_graph* g, int32_t loss) {
     const int width = (int)p->size();
     const int nr = (int)rows.size();
     float* work = reinterpret_cast<float*>(scratch_base(g));
-    plan.ops.push_back([dst, orow, nr, width, work, st](char* d) {
-      return launch_colsum_rows(dst, at<const float* const>(d, orow), nr, width, work, st);
+    const int64_t wcap = (int64_t)(scratch_bytes(g) / 4);
+    plan.ops.push_back([dst, orow, nr, width, work, wcap, st](char* d) {
+      return launch_colsum_rows(dst, at<const float* const>(d, orow), nr, width, work, wcap, st);
     });
     plan.tag(C_COLSUM, 0.0, 4.0 * nr * width + 8.0 * width);
   }

@@ -6,6 +6,7 @@
 // accumulates into zero-initialised slots) and trainers.py:63-83.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "kernels.cuh"
@@ -784,17 +785,49 @@ __global__ void colsum_partial_kernel(const float* const* rows, int n_rows, int 
   const int ch = blockIdx.y;
   if (c >= width) return;
   const int r0 = (int)((int64_t)n_rows * ch / chunks), r1 = (int)((int64_t)n_rows * (ch + 1) / chunks);
+  // 8 rows in flight (pointers, then values), summed in row order
   float s = 0.f;
-  for (int r = r0; r < r1; ++r) s += rows[r][c];
+  int r = r0;
+  for (; r + 8 <= r1; r += 8) {
+    const float* p[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) p[k] = rows[r + k];
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = p[k][c];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += v[k];
+  }
+  for (; r < r1; ++r) s += rows[r][c];
   work[(int64_t)ch * width + c] = s;
 }
 
 __global__ void colsum_final_kernel(float* dst, const float* work, int width, int chunks) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= width) return;
+  // block = 32 columns x 8 chunk groups; group y sums chunks y, y+8, ...
+  // (4 in flight), then the 8 group sums are added in fixed order
+  __shared__ float part[8][33];
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31), y = threadIdx.x >> 5;
   float s = 0.f;
-  for (int ch = 0; ch < chunks; ++ch) s += work[(int64_t)ch * width + c];
-  dst[c] += s;
+  if (c < width) {
+    int ch = y;
+    for (; ch + 24 < chunks; ch += 32) {
+      const float a0 = work[(int64_t)ch * width + c], a1 = work[(int64_t)(ch + 8) * width + c];
+      const float a2 = work[(int64_t)(ch + 16) * width + c], a3 = work[(int64_t)(ch + 24) * width + c];
+      s += a0;
+      s += a1;
+      s += a2;
+      s += a3;
+    }
+    for (; ch < chunks; ch += 8) s += work[(int64_t)ch * width + c];
+  }
+  part[y][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (y == 0 && c < width) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += part[k][threadIdx.x];
+    dst[c] += t;
+  }
 }
 
 __global__ void row_reduce_scatter_kernel(float* const* dst_rows, const int* seg, const float* src, int n_targets,
@@ -1053,14 +1086,19 @@ int launch_affine_generic_bwd(const AffineGenericArgs& a, cudaStream_t s) {
   return launches;
 }
 
-int launch_colsum_rows(float* dst, const float* const* rows, int n_rows, int width, float* work, cudaStream_t s) {
+int launch_colsum_rows(float* dst, const float* const* rows, int n_rows, int width, float* work, int64_t work_floats,
+                       cudaStream_t s) {
   if (n_rows <= 0) return 0;
-  int chunks = n_rows / 16;
-  if (chunks < 1) chunks = 1;
-  if (chunks > 64) chunks = 64;
+  // enough (column block, row chunk) blocks to fill the device twice over,
+  // chunks of >= 8 rows, partials bounded by the scratch
+  const int xb = (width + 255) / 256;
+  int chunks = (2 * 148 * 8 + xb - 1) / xb;
+  chunks = std::min(chunks, std::max(1, n_rows / 8));
+  chunks = (int)std::min<int64_t>(chunks, std::max<int64_t>(1, work_floats / std::max(1, width)));
+  chunks = std::min(chunks, 1024);
   dim3 g1((width + 255) / 256, chunks);
   colsum_partial_kernel<<<g1, 256, 0, s>>>(rows, n_rows, width, chunks, work);
-  colsum_final_kernel<<<(width + 255) / 256, 256, 0, s>>>(dst, work, width, chunks);
+  colsum_final_kernel<<<(width + 31) / 32, 256, 0, s>>>(dst, work, width, chunks);
   return 2;
 }
 

@@ -214,7 +214,7 @@ int launch_affine_generic_bwd(const AffineGenericArgs& a, cudaStream_t s);
 
 // column sums over gathered rows: dst[c] += sum_r rows[r][c]  (deterministic)
 int launch_colsum_rows(float* dst, const float* const* rows, int n_rows, int width, float* work,
-                       cudaStream_t s);
+                       int64_t work_floats, cudaStream_t s);
 // row reduce-scatter: for t in targets: dst[t] += sum_{k in seg} src[k]  (src dense, width)
 int launch_row_reduce_scatter(float* const* dst_rows, const int* seg, const float* src, int n_targets,
                               int width, cudaStream_t s);
