@@ -18,13 +18,13 @@ __device__ __forceinline__ uint64_t kdesc(uint32_t saddr) {  // K-major SWIZZLE_
   return d;
 }
 
-template <int N, bool kF16, bool kTA>
+template <int N, bool kF16, bool kTA, int kNoise = 0>
 __global__ void probe(long long* out, int iters) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint32_t tmem_sh;
   __shared__ uint64_t bar;
-  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = 0.f;
+  for (int i = threadIdx.x; i < 128 * 1024 / 4; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = 0.f;
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_sh)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -38,6 +38,23 @@ __global__ void probe(long long* out, int iters) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_sh;
+  if (kNoise && threadIdx.x >= 32) {
+    // background shared-memory traffic (kNoise = 1: reads, 2: reads + writes)
+    // over a separate 32 KiB region while warp 0 issues MMAs
+    volatile int* flag = reinterpret_cast<volatile int*>(out + 1);
+    const uint32_t base = su32(smem + 65536);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int it = 0; it < 20000 && *flag == 0; ++it) {
+      const uint32_t a = base + (uint32_t)(((threadIdx.x - 32) * 16 + it * 1536) & 32767);
+      float4 v;
+      asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+      acc.x += v.x;
+      if (kNoise == 2)
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a ^ 16384u), "f"(acc.x), "f"(v.y), "f"(v.z),
+                     "f"(v.w));
+    }
+    if (acc.x == 12345.f) out[2] = 1;
+  }
   if (threadIdx.x == 0) {
     // idesc: D f32 (bit 4), A/B kind (tf32: 2 at bits 7 and 10; f16 family bf16: 1), K-major, N>>3 at 17, M>>4 at 24
     const uint32_t ab = kF16 ? 1u : 2u;
@@ -68,21 +85,24 @@ __global__ void probe(long long* out, int iters) {
             su32(&bar))
         : "memory");
     out[0] = clock64() - t0;
+    *reinterpret_cast<volatile int*>(out + 1) = 1;
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
-template <int N, bool kF16, bool kTA>
+template <int N, bool kF16, bool kTA, int kNoise = 0>
 void run(const char* name) {
   long long* d;
-  cudaMalloc(&d, 8);
-  const int smem = 97 * 1024;
-  cudaFuncSetAttribute(probe<N, kF16, kTA>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaMalloc(&d, 32);
+  cudaMemset(d, 0, 32);
+  const int smem = 97 * 1024 + 32768;
+  cudaFuncSetAttribute(probe<N, kF16, kTA, kNoise>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 4096;
-  probe<N, kF16, kTA><<<1, 128, smem>>>(d, iters);
-  probe<N, kF16, kTA><<<1, 128, smem>>>(d, iters);
+  probe<N, kF16, kTA, kNoise><<<1, kNoise ? 512 : 128, smem>>>(d, iters);
+  cudaMemset(d + 1, 0, 8);
+  probe<N, kF16, kTA, kNoise><<<1, kNoise ? 512 : 128, smem>>>(d, iters);
   long long c = 0;
   cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
   const double per = (double)c / iters;
@@ -102,5 +122,9 @@ int main() {
   run<128, true, false>("bf16 A smem");
   run<256, true, false>("bf16 A smem");
   run<256, true, true>("bf16 A tmem");
+  run<128, false, false, 1>("tf32 A smem + 15 warps lds");
+  run<128, false, false, 2>("tf32 A smem + lds/sts");
+  run<128, false, true, 1>("tf32 A tmem + 15 warps lds");
+  run<128, false, true, 2>("tf32 A tmem + lds/sts");
   return 0;
 }
