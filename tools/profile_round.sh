@@ -11,5 +11,5 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:tma_
     -o gpurun_out/full_tma $P > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:rnn_ -s 2 -c 4 \
     -o gpurun_out/full_rnn $P > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:row_kernel -s 2 -c 2 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"row_reg_kernel|row_kernel" -s 2 -c 2 \
     -o gpurun_out/full_row $P > /dev/null 2>&1
