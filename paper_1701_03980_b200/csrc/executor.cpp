@@ -2484,6 +2484,11 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
           a.n = n;
           a.len = len;
           a.size = (int)n0.size();
+          {
+            std::vector<uintptr_t> all(gins);
+            all.insert(all.end(), gouts.begin(), gouts.end());
+            a.distinct = has_duplicate_rows(all) ? 0 : 1;
+          }
           const size_t og = B.push(gout), ogi = B.push(gins), ogo = B.push(gouts);
           plan.ops.push_back([a, og, ogi, ogo, st](char* d) mutable {
             a.gfinal = at<const float* const>(d, og);

@@ -146,6 +146,47 @@ __global__ void chain_bwd_kernel(ChainArgs a) {
   }
 }
 
+// Few long chains (the scalar loss chain): one block per (chain, element)
+// prefetches the terms into shared memory, one thread adds them in the same
+// left-to-right order, and the block writes the prefixes back in parallel.
+__global__ void chain_fwd_seq_kernel(ChainArgs a) {
+  __shared__ float t[1024];
+  const int j = blockIdx.x / a.size;
+  const int64_t e = blockIdx.x - (int64_t)j * a.size;
+  float s = 0.f;
+  for (int base = 0; base <= a.len; base += 1024) {
+    const int cnt = min(1024, a.len + 1 - base);
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) t[i] = a.ins[(int64_t)(base + i) * a.n + j][e];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < cnt; ++i) {
+        s = base + i == 0 ? t[i] : s + t[i];
+        t[i] = s;
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+      if (base + i >= 1) a.outs[(int64_t)(base + i - 1) * a.n + j][e] = t[i];
+    __syncthreads();
+  }
+}
+
+// every (slot, element) of a chain whose gradient slots are all distinct
+// (checked on the host): g of the last add is added to each independently
+__global__ void chain_bwd_par_kernel(ChainArgs a) {
+  const int64_t per = (int64_t)a.n * a.size;
+  const int64_t total = (int64_t)(2 * a.len + 1) * per;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int slot = static_cast<int>(t / per);
+    const int64_t r = t - (int64_t)slot * per;
+    const int j = static_cast<int>(r / a.size);
+    const int64_t e = r - (int64_t)j * a.size;
+    const float g = a.gfinal[j][e];
+    if (slot < a.len) a.gouts[(int64_t)slot * a.n + j][e] += g;
+    else a.gins[(int64_t)(slot - a.len) * a.n + j][e] += g;
+  }
+}
+
 // ------------------------------------------------------------ gated cells
 
 struct CellSlots {
@@ -975,10 +1016,18 @@ int launch_ew_bwd(const EwArgs& a, cudaStream_t s) {
 }
 
 int launch_chain_fwd(const ChainArgs& a, cudaStream_t s) {
+  if ((int64_t)a.size * a.n < 2048 && a.len >= 8) {
+    chain_fwd_seq_kernel<<<a.size * a.n, 256, 0, s>>>(a);
+    return 1;
+  }
   chain_fwd_kernel<<<grid_for((int64_t)a.size * a.n), kThreads, 0, s>>>(a);
   return 1;
 }
 int launch_chain_bwd(const ChainArgs& a, cudaStream_t s) {
+  if (a.distinct) {
+    chain_bwd_par_kernel<<<grid_for((int64_t)(2 * a.len + 1) * a.n * a.size), kThreads, 0, s>>>(a);
+    return 1;
+  }
   chain_bwd_kernel<<<grid_for((int64_t)a.size * a.n), kThreads, 0, s>>>(a);
   return 1;
 }

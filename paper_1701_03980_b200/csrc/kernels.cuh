@@ -47,6 +47,7 @@ struct ChainArgs {
   const float* const* gfinal;  // [n] grad of the last add
   float* const* gins;        // [(len+1) * n]
   float* const* gouts;       // [len * n] grads of the intermediate adds (get gfinal)
+  int distinct;              // backward: every gins / gouts slot distinct (element-parallel adds)
 };
 int launch_chain_fwd(const ChainArgs& a, cudaStream_t s);
 int launch_chain_bwd(const ChainArgs& a, cudaStream_t s);
