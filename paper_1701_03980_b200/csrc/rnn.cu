@@ -926,11 +926,23 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_fwd_cl_kernel(const __grid_
     }
     if (a.trace == 2 && tid == 0) trace(0, 64 + 4 * t + 3);
     if (t + 1 < C.T) {
-      // push h_t into buffer t&1 of every CTA of the cluster
-      if (cell_row && cjj < C.H) {
+      // push h_t into buffer t&1 of every CTA of the cluster: the 4 units of
+      // a quad (consecutive lanes of one row) are gathered into the quad's
+      // first lane, one 16 B st.async per peer (a quarter of the DSMEM
+      // transactions); a ragged last quad pushes per element
+      const float h1 = __shfl_down_sync(0xffffffffu, h, 1);
+      const float h2 = __shfl_down_sync(0xffffffffu, h, 2);
+      const float h3 = __shfl_down_sync(0xffffffffu, h, 3);
+      const bool full_quad = (cjj | 3) < C.H;
+      if (cell_row && cjj < C.H && (!full_quad || (cj & 3) == 0)) {
         const uint32_t la = h_local0 + (uint32_t)((t & 1) * BS * HP * 4);
         const uint32_t lb = smem_addr(&h_full[t & 1]);
-        for (int q = 0; q < C.n_u; ++q) st_async_f32(mapa(la, q), h, mapa(lb, q));
+        if (full_quad) {
+          const float4 v = make_float4(h, h1, h2, h3);
+          for (int q = 0; q < C.n_u; ++q) st_async_v4(mapa(la, q), v, mapa(lb, q));
+        } else {
+          for (int q = 0; q < C.n_u; ++q) st_async_f32(mapa(la, q), h, mapa(lb, q));
+        }
       }
     }
     if (warp == 1 && t + 1 < C.T) {

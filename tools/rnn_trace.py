@@ -46,3 +46,9 @@ if os.environ.get("DG_RNN_TRACE") == "2":
     ph = b[64:64 + 4 * min(T, 47)].reshape(-1, 4).astype(np.int64)
     d = np.diff(np.concatenate([ph, np.roll(ph[:, :1], -1, axis=0)], axis=1), axis=1)[:-1]
     print("fwd CTA0 per-step phases (us): wait, fma, reduce+cell, push+rest ->", np.round(np.median(d, axis=0) / 1e3, 2))
+    n = min(T, 47) - 1
+    cell_end = ph[:n, 3]
+    arrive = b[2:2 + n].astype(np.int64)  # after the push and the step barrier
+    nxt = ph[1:n + 1, 0]
+    print("  push+rest split (us): push+barrier", np.round(np.median(arrive - cell_end) / 1e3, 2),
+          "stores+next step top", np.round(np.median(nxt - arrive) / 1e3, 2))
