@@ -1269,16 +1269,58 @@ static void flush_gemm(dg_graph* g, Plan& plan, GemmBatch& gb) {
   float* work = reinterpret_cast<float*>(scratch_base(g)) + temp;
   const int64_t cap = (int64_t)(scratch_bytes(g) / 4) - temp;
   cudaStream_t st = g->stream;
-  // dense wide problems: TMA + warp-specialised tcgen05 (one launch each)
+  // dense wide problems: TMA + warp-specialised tcgen05; problems of the batch
+  // that share a kernel and write disjoint outputs go up to kTmaGroup per
+  // launch with one split factor (small weight-gradient GEMMs fill a wave
+  // together instead of each splitting K eight ways)
   std::vector<GemmProblem> rest;
+  std::vector<std::pair<TmaGemmPlan, double>> tmas;
   for (const GemmProblem& p : gb.probs) {
     TmaGemmPlan tp;
-    if (tma_try(g, plan, p, gb.a_kmajor, gb.b_nmajor, work, cap, &tp)) {
-      plan.ops.push_back([tp, st](char*) { return launch_tma_gemm(tp, true, true, st); });
-      plan.tag(gb.cls, tp.flops, 4.0 * ((double)p.M * p.seg[0].K + (double)p.seg[0].K * p.N + 2.0 * p.M * p.N));
-    } else {
+    if (tma_try(g, plan, p, gb.a_kmajor, gb.b_nmajor, work, cap, &tp))
+      tmas.push_back({tp, 4.0 * ((double)p.M * p.seg[0].K + (double)p.seg[0].K * p.N + 2.0 * p.M * p.N)});
+    else
       rest.push_back(p);
+  }
+  static const bool group_on = [] {
+    const char* e = std::getenv("DG_TMA_GROUP");
+    return !(e && e[0] == '0');
+  }();
+  std::vector<char> used(tmas.size(), 0);
+  for (size_t i = 0; i < tmas.size(); ++i) {
+    if (used[i]) continue;
+    std::vector<size_t> grp{i};
+    used[i] = 1;
+    for (size_t j = i + 1; j < tmas.size() && group_on && (int)grp.size() < kTmaGroup; ++j) {
+      if (used[j]) continue;
+      bool ok = true;
+      for (size_t q : grp) ok = ok && tma_gemm_groupable(tmas[q].first, tmas[j].first);
+      if (!ok) continue;
+      grp.push_back(j);
+      used[j] = 1;
     }
+    if (grp.size() == 1) {
+      const TmaGemmPlan tp = tmas[i].first;
+      plan.ops.push_back([tp, st](char*) { return launch_tma_gemm(tp, true, true, st); });
+      plan.tag(gb.cls, tp.flops, tmas[i].second);
+      continue;
+    }
+    std::vector<TmaGemmPlan> ps;
+    double flops = 0, bytes = 0;
+    for (size_t q : grp) {
+      ps.push_back(tmas[q].first);
+      flops += tmas[q].first.flops;
+      bytes += tmas[q].second;
+    }
+    std::vector<TmaGemmPlan*> pp;
+    for (auto& x : ps) pp.push_back(&x);
+    tma_gemm_regroup(pp.data(), (int)pp.size());
+    plan.ops.push_back([ps, st](char*) {
+      const TmaGemmPlan* arr[kTmaGroup];
+      for (size_t q = 0; q < ps.size(); ++q) arr[q] = &ps[q];
+      return launch_tma_gemm_group(arr, (int)ps.size(), st);
+    });
+    plan.tag(gb.cls, flops, bytes);
   }
   auto post = std::move(gb.post);
   if (rest.empty()) {

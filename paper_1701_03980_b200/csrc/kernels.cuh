@@ -286,6 +286,16 @@ struct TmaOperands {
   Operand C, bias;
   int accumulate;
 };
+constexpr int kTmaGroup = 4;  // problems per grouped TMA GEMM launch
+struct TmaProb {
+  CUtensorMap mAh, mAl, mBh, mBl;
+  TmaGemmArgs args;
+  int cta0;
+};
+struct TmaGroup {
+  TmaProb p[kTmaGroup];
+  int n;
+};
 struct TmaGemmPlan {
   CUtensorMap mAh, mAl, mBh, mBl;
   TmaGemmArgs args;
@@ -307,6 +317,10 @@ int64_t tma_lo_floats(int64_t rows, int64_t cols);
 bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out);
 // split_a / split_b: (re)compute the residual copies before the GEMM
 int launch_tma_gemm(const TmaGemmPlan& p, bool split_a, bool split_b, cudaStream_t s);
+// grouped launches (in-smem conversion only): same kernel, disjoint outputs
+bool tma_gemm_groupable(const TmaGemmPlan& a, const TmaGemmPlan& b);
+void tma_gemm_regroup(TmaGemmPlan* const* ps, int n);  // one split factor for the group
+int launch_tma_gemm_group(const TmaGemmPlan* const* ps, int n, cudaStream_t s);
 int tma_prof_read(long long* out);  // diagnostics: DG_TMA_DBG bit 10 wait timestamps [5][256][2]
 
 // ------------------------------------------------------------- trainers

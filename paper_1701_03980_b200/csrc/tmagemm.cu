@@ -175,11 +175,21 @@ __device__ __noinline__ void epilogue_scalar(const TmaGemmArgs& P, float* part, 
   }
 }
 
+// One launch runs up to kTmaGroup independent problems of the same operand
+// majors and split factor (problem i owns CTAs [cta0_i, cta0_{i+1})): the
+// small LSTM weight-gradient GEMMs of one backward share a wave instead of
+// each under-filling the device.
 template <bool kAMN, bool kBMN, bool kConv, bool kAT = false>
 __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
-    tma_gemm_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
-                    const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
-                    const __grid_constant__ TmaGemmArgs P) {
+    tma_gemm_kernel(const __grid_constant__ TmaGroup G) {
+  int pi = 0;
+  while (pi + 1 < G.n && (int)blockIdx.x >= G.p[pi + 1].cta0) ++pi;
+  const TmaProb& PR = G.p[pi];
+  const CUtensorMap& mAh = PR.mAh;
+  const CUtensorMap& mAl = PR.mAl;
+  const CUtensorMap& mBh = PR.mBh;
+  const CUtensorMap& mBl = PR.mBl;
+  const TmaGemmArgs& P = PR.args;
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   static_assert(!kAT || kConv, "A in TMEM needs the converter warps");
@@ -204,7 +214,7 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
   const int S = P.splits;
   const bool prof_e = prof && threadIdx.x == 64;
   if (prof_e) g_tprof[5][0][0] = clock64();
-  const int local = blockIdx.x;
+  const int local = (int)blockIdx.x - PR.cta0;
   const int z = local % S, tile = local / S;
   // m-tiles fastest: CTAs that run together share the same B columns, so a
   // streamed B operand (dlogits in dW) is read from DRAM once
@@ -692,6 +702,60 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
   return true;
 }
 
+static int tma_kernel_index(const TmaGemmPlan& p) {
+  return (p.a_tmem ? 8 : p.conv ? 4 : 0) + (p.a_mn ? 2 : 0) + (p.b_mn ? 1 : 0);
+}
+
+using TmaKernel = void (*)(const TmaGroup);
+
+static TmaKernel tma_kernel(int ki) {
+  static const TmaKernel table[12] = {
+      tma_gemm_kernel<false, false, false>,      tma_gemm_kernel<false, true, false>,
+      tma_gemm_kernel<true, false, false>,       tma_gemm_kernel<true, true, false>,
+      tma_gemm_kernel<false, false, true>,       tma_gemm_kernel<false, true, true>,
+      tma_gemm_kernel<true, false, true>,        tma_gemm_kernel<true, true, true>,
+      tma_gemm_kernel<false, false, true, true>, tma_gemm_kernel<false, true, true, true>,
+      tma_gemm_kernel<true, false, true, true>,  tma_gemm_kernel<true, true, true, true>};
+  return table[ki];
+}
+
+static int tma_launch(const TmaGemmPlan* const* ps, int n, cudaStream_t s) {
+  const TmaGemmPlan& p = *ps[0];
+  const int ki = tma_kernel_index(p);
+  const TmaKernel k = tma_kernel(ki);
+  static bool attr[12] = {};
+  const int smem = p.a_tmem ? kSmemAT : p.conv ? kSmemConv : kSmem;
+  if (!attr[ki]) {
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
+    attr[ki] = true;
+  }
+  static TmaGroup G;  // launch arguments are copied at launch
+  G.n = n;
+  int ctas = 0;
+  for (int i = 0; i < n; ++i) {
+    G.p[i].mAh = ps[i]->mAh;
+    G.p[i].mAl = ps[i]->mAl;
+    G.p[i].mBh = ps[i]->mBh;
+    G.p[i].mBl = ps[i]->mBl;
+    G.p[i].args = ps[i]->args;
+    G.p[i].cta0 = ctas;
+    ctas += ps[i]->ctas;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(p.conv ? kThreadsConv : kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = p.args.splits;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, G) == cudaSuccess ? 1 : -1;
+}
+
 int launch_tma_gemm(const TmaGemmPlan& p, bool split_a, bool split_b, cudaStream_t s) {
   int n = 0;
   if (p.conv) split_a = split_b = false;
@@ -707,36 +771,51 @@ int launch_tma_gemm(const TmaGemmPlan& p, bool split_a, bool split_b, cudaStream
       ++n;
     }
   }
-  using K = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const TmaGemmArgs);
-  static const K table[12] = {
-      tma_gemm_kernel<false, false, false>,      tma_gemm_kernel<false, true, false>,
-      tma_gemm_kernel<true, false, false>,       tma_gemm_kernel<true, true, false>,
-      tma_gemm_kernel<false, false, true>,       tma_gemm_kernel<false, true, true>,
-      tma_gemm_kernel<true, false, true>,        tma_gemm_kernel<true, true, true>,
-      tma_gemm_kernel<false, false, true, true>, tma_gemm_kernel<false, true, true, true>,
-      tma_gemm_kernel<true, false, true, true>,  tma_gemm_kernel<true, true, true, true>};
-  const int ki = (p.a_tmem ? 8 : p.conv ? 4 : 0) + (p.a_mn ? 2 : 0) + (p.b_mn ? 1 : 0);
-  const K k = table[ki];
-  static bool attr[12] = {};
-  const int smem = p.a_tmem ? kSmemAT : p.conv ? kSmemConv : kSmem;
-  if (!attr[ki]) {
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
-    attr[ki] = true;
+  const TmaGemmPlan* one = &p;
+  const int r = tma_launch(&one, 1, s);
+  return r < 0 ? -1 : n + r;
+}
+
+bool tma_gemm_groupable(const TmaGemmPlan& a, const TmaGemmPlan& b) {
+  if (!a.conv || !b.conv || tma_kernel_index(a) != tma_kernel_index(b)) return false;
+  if (a.args.C.rows || b.args.C.rows) return false;
+  // output blocks must not overlap (problems of a group run concurrently)
+  auto lo = [](const TmaGemmPlan& p) { return p.args.C.base; };
+  auto hi = [](const TmaGemmPlan& p) { return p.args.C.base + (int64_t)(p.args.M - 1) * p.args.C.ld + p.args.N; };
+  return hi(a) <= lo(b) || hi(b) <= lo(a);
+}
+
+void tma_gemm_regroup(TmaGemmPlan* const* ps, int n) {
+  // one split factor for the group: waves x (fixed ~4 k-tiles + longest split)
+  int tiles = 0, kt_max = 0, kt_min = 1 << 30;
+  for (int i = 0; i < n; ++i) {
+    const TmaGemmArgs& a = ps[i]->args;
+    tiles += ((a.M + BM - 1) / BM) * a.tiles_n;
+    const int kt = (a.K + BK - 1) / BK;
+    kt_max = std::max(kt_max, kt);
+    kt_min = std::min(kt_min, kt);
   }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(p.ctas);
-  cfg.blockDim = dim3(p.conv ? kThreadsConv : kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = p.args.splits;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, k, p.mAh, p.mAl, p.mBh, p.mBl, p.args) != cudaSuccess) return -1;
-  return n + 1;
+  int S = 1;
+  double best = 1e30;
+  for (int s2 = 1; s2 <= 8; s2 *= 2) {
+    if (s2 > 1 && kt_min < 4 * s2) break;
+    const double cost = (double)((tiles * s2 + 147) / 148) * (4.0 + (double)kt_max / s2);
+    if (cost < best * 0.97) {
+      best = cost;
+      S = s2;
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    TmaGemmArgs& a = ps[i]->args;
+    a.splits = S;
+    ps[i]->ctas = ((a.M + BM - 1) / BM) * a.tiles_n * S;
+  }
+}
+
+int launch_tma_gemm_group(const TmaGemmPlan* const* ps, int n, cudaStream_t s) {
+  if (n <= 0) return 0;
+  if (n > kTmaGroup) return -1;
+  return tma_launch(ps, n, s);
 }
 
 }  // namespace dg
