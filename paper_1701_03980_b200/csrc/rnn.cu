@@ -775,33 +775,42 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_fwd_cl_kernel(const __grid_
   const int goff[4] = {C.off_i, C.off_f, C.off_o, C.off_g};
   const int g8 = lane >> 2, t4 = lane & 3;      // mma fragment coordinates
   if (a.trace && tid == 0) trace(0, 0);
+  // h_{-1} source (flags, pointer): loaded first so its latency overlaps the
+  // weight staging below
+  const int fl_hp = C.b1[0];
+  const float* Hp0 = C.val[S_HP];
 
   if (warp < 8) {
     // weight fragments: warp w, k-step q, lane (g, t): b0 = B(8q + t, 8w + g),
     // b1 = B(8q + t + 4, 8w + g), B(k, n) = Wh[row(n) + k * gw] (n = gate * 16 + jj);
     // loaded coalesced along n and scattered into the fragment layout
-    float* Bff = reinterpret_cast<float*>(Bf);
-    constexpr int kBatch = 8;  // loads in flight per thread
-    for (int idx0 = tid; idx0 < 8 * KS * kCU; idx0 += kBatch * kRT) {
-      float v[kBatch];
+    // one float4 fragment {b0_hi, b1_hi, b0_lo, b1_lo} per (k-step, warp,
+    // lane): b0 = B(8q + t, 8w + g), b1 = B(8q + t + 4, 8w + g); kBatch
+    // fragments (2 loads each) in flight per thread, conflict-free 16 B stores
+    constexpr int kBatch = 8;
+    const int nfrag = KS * 8 * 32;
+    for (int f0 = tid; f0 < nfrag; f0 += kBatch * kRT) {
+      float b0[kBatch], b1[kBatch];
 #pragma unroll
       for (int u = 0; u < kBatch; ++u) {
-        const int idx = idx0 + u * kRT;
-        const int k = idx / kCU, n = idx - (idx / kCU) * kCU;
+        const int fi = f0 + u * kRT;
+        const int q = fi >> 8, w = (fi >> 5) & 7, l = fi & 31;
+        const int n = 8 * w + (l >> 2), k = 8 * q + (l & 3);
         const int gate = n / kU, j = j0 + (n - gate * kU);
-        v[u] = (idx < 8 * KS * kCU && j < C.H && k < C.H) ? __ldg(C.Wh + goff[gate] + j + (int64_t)k * C.gw) : 0.f;
+        const float* src = C.Wh + goff[gate] + j + (int64_t)k * C.gw;
+        const bool ok = fi < nfrag && j < C.H;
+        b0[u] = ok && k < C.H ? __ldg(src) : 0.f;
+        b1[u] = ok && k + 4 < C.H ? __ldg(src + (int64_t)4 * C.gw) : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < kBatch; ++u) {
-        const int idx = idx0 + u * kRT;
-        if (idx >= 8 * KS * kCU) break;
-        const int k = idx / kCU, n = idx - (idx / kCU) * kCU;
-        const int q = k >> 3, kk = k & 7, w = n >> 3, l = ((n & 7) << 2) | (kk & 3), half = kk >> 2;
-        float* f = Bff + ((size_t)(q * 8 + w) * 32 + l) * 4;
-        f[half] = __uint_as_float(tf32_hi(v[u]));
-        f[2 + half] = __uint_as_float(tf32_lo(v[u]));
+        const int fi = f0 + u * kRT;
+        if (fi >= nfrag) break;
+        Bf[fi] = make_float4(__uint_as_float(tf32_hi(b0[u])), __uint_as_float(tf32_hi(b1[u])),
+                             __uint_as_float(tf32_lo(b0[u])), __uint_as_float(tf32_lo(b1[u])));
       }
     }
+    if (a.trace == 2 && tid == 0) trace(0, 252);
     if (tid < kRnnSlots) sp[0].p[tid] = C.val[tid];
     if (tid == kRnnSlots) sp[0].b1 = C.b1[0];
     // h buffers: zero (padding columns stay zero), then h_{-1} into buffer 1
@@ -817,9 +826,10 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_fwd_cl_kernel(const __grid_
     }
   }
   __syncthreads();
+  if (a.trace == 2 && tid == 0) trace(0, 253);
   if (warp < 8) {
-    const int fl = C.b1[0];
-    const float* Hp = C.val[S_HP];
+    const int fl = fl_hp;
+    const float* Hp = Hp0;
     const int w4 = C.H >> 2;
     for (int idx = tid; idx < BS * w4; idx += kRT) {
       const int b = idx / w4, q = idx - (idx / w4) * w4;
@@ -829,6 +839,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_fwd_cl_kernel(const __grid_
     cp_async_wait_all();
   }
   __syncthreads();
+  if (a.trace == 2 && tid == 0) trace(0, 254);
   cluster_sync_all();  // every peer is resident and initialised before any DSMEM push
   if (a.trace && tid == 0) trace(0, 1);
   if (warp == 8) return;  // no cross-chain signalling in gx mode
@@ -1006,26 +1017,29 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
   if (warp < 8) {
     // B(k, n) = Wh[row(k) + n * gw], k = own gate column (gate * 16 + jj), n = unit;
     // fragment (nt, q, lane = g*4 + t): b0 = B(8q + t, 8nt + g), b1 = B(8q + t + 4, 8nt + g)
-    float* Bff = reinterpret_cast<float*>(Bf);
-    constexpr int kBatch = 16;
-    for (int idx0 = tid; idx0 < kCU * HU; idx0 += kBatch * kRT) {
-      float v[kBatch];
+    // one float4 fragment per (unit tile, k-step, lane), 2 loads each,
+    // kBatch in flight per thread, conflict-free 16 B stores
+    constexpr int kBatch = 8;
+    const int nfrag = NT * 8 * 32;
+    for (int f0 = tid; f0 < nfrag; f0 += kBatch * kRT) {
+      float b0[kBatch], b1[kBatch];
 #pragma unroll
       for (int u = 0; u < kBatch; ++u) {
-        const int idx = idx0 + u * kRT;
-        const int n = idx / kCU, k = idx - (idx / kCU) * kCU;  // consecutive threads: consecutive k
+        const int fi = f0 + u * kRT;
+        const int nt = fi >> 8, q = (fi >> 5) & 7, l = fi & 31;
+        const int n = 8 * nt + (l >> 2), k = 8 * q + (l & 3);
         const int gate = k / kU, jj = j0 + (k - gate * kU);
-        v[u] = (idx < kCU * HU && jj < C.H && n < C.H) ? __ldg(C.Wh + goff[gate] + jj + (int64_t)n * C.gw) : 0.f;
+        const float* src = C.Wh + goff[gate] + jj + (int64_t)n * C.gw;
+        const bool ok = fi < nfrag && n < C.H;
+        b0[u] = ok && jj < C.H ? __ldg(src) : 0.f;
+        b1[u] = ok && jj + 4 < C.H ? __ldg(src + 4) : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < kBatch; ++u) {
-        const int idx = idx0 + u * kRT;
-        if (idx >= kCU * HU) break;
-        const int n = idx / kCU, k = idx - (idx / kCU) * kCU;
-        const int nt = n >> 3, q = k >> 3, kk = k & 7, l = ((n & 7) << 2) | (kk & 3), half = kk >> 2;
-        float* f = Bff + ((size_t)(nt * 8 + q) * 32 + l) * 4;
-        f[half] = __uint_as_float(tf32_hi(v[u]));
-        f[2 + half] = __uint_as_float(tf32_lo(v[u]));
+        const int fi = f0 + u * kRT;
+        if (fi >= nfrag) break;
+        Bf[fi] = make_float4(__uint_as_float(tf32_hi(b0[u])), __uint_as_float(tf32_hi(b1[u])),
+                             __uint_as_float(tf32_lo(b0[u])), __uint_as_float(tf32_lo(b1[u])));
       }
     }
     {

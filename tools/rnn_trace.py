@@ -52,3 +52,14 @@ if os.environ.get("DG_RNN_TRACE") == "2":
     nxt = ph[1:n + 1, 0]
     print("  push+rest split (us): push+barrier", np.round(np.median(arrive - cell_end) / 1e3, 2),
           "stores+next step top", np.round(np.median(nxt - arrive) / 1e3, 2))
+
+if os.environ.get("DG_RNN_TRACE") == "2":
+    b = buf[0]
+    live = b[:, 0] > 0
+    b = b[live].astype(np.int64)
+    t0 = b[:, 0]
+    ph = np.stack([b[:, 252] - t0, b[:, 253] - t0, b[:, 254] - t0, b[:, 1] - t0, t0 - t0.min()], axis=1)
+    print("fwd prologue (us, median over CTAs): weights", np.round(np.median(ph[:, 0]) / 1e3, 2), "| +init sync",
+          np.round(np.median(ph[:, 1]) / 1e3, 2), "| +h_-1", np.round(np.median(ph[:, 2]) / 1e3, 2),
+          "| +cluster sync", np.round(np.median(ph[:, 3]) / 1e3, 2), "| CTA start skew max",
+          np.round(ph[:, 4].max() / 1e3, 2))
