@@ -529,6 +529,64 @@ static PyObject* core_add(CoreObj* c, PyObject* const* args, Py_ssize_t nargs) {
         done = 2; /* record written */
       }
       break;
+    case OP_LOOKUP:
+      if (n_in == 0 && PyTuple_CheckExact(aux) && PyTuple_GET_SIZE(aux) == 2 && PyLong_CheckExact(PyTuple_GET_ITEM(aux, 1))) {
+        PyObject* lp = PyTuple_GET_ITEM(aux, 0);
+        int err = 0;
+        const long rows = get_long_attr(lp, s_rows, &err);
+        const long dim = err ? 0 : get_long_attr(lp, s_dim, &err);
+        const long handle = err ? 0 : get_long_attr(lp, s_handle, &err);
+        if (err) goto fail0;
+        const long x = PyLong_AsLong(PyTuple_GET_ITEM(aux, 1));
+        if (x == -1 && PyErr_Occurred()) goto fail0;
+        if (x < 0 || x >= rows) break; /* the Python rule raises IndexOutOfBounds */
+        PyObject* d = Py_BuildValue("(l)", dim);
+        if (!d) goto fail0;
+        shape = new_shape(d, 1);
+        Py_DECREF(d);
+        if (!shape) goto fail0;
+        const int64_t v[2] = {handle, x};
+        if (add_fix(c, c->ai.n, lp) < 0 || put_record(c, code, idx, 0, (ShapeObj*)shape, v, 2, NULL, 0) < 0)
+          goto fail_shape;
+        done = 2;
+      }
+      break;
+    case OP_CONCATENATE:
+      if (n_in >= 1) {
+        const long batch = shp[0]->batch;
+        long total = 0;
+        int ok = 1;
+        for (Py_ssize_t k = 0; k < n_in && ok; ++k) {
+          if (PyTuple_GET_SIZE(shp[k]->dims) != 1 || shp[k]->batch != batch) ok = 0;
+          else total += PyLong_AsLong(PyTuple_GET_ITEM(shp[k]->dims, 0));
+        }
+        if (PyErr_Occurred()) goto fail0;
+        if (ok) {
+          PyObject* d = Py_BuildValue("(l)", total);
+          if (!d) goto fail0;
+          shape = new_shape(d, batch);
+          Py_DECREF(d);
+          if (!shape) goto fail0;
+          done = 1;
+        }
+      }
+      break;
+    case OP_PNLS:
+      if (n_in == 1 && PyLong_CheckExact(aux) && PyTuple_GET_SIZE(shp[0]->dims) == 1 && shp[0]->batch == 1) {
+        const long lab = PyLong_AsLong(aux);
+        if (lab == -1 && PyErr_Occurred()) goto fail0;
+        const long n = PyLong_AsLong(PyTuple_GET_ITEM(shp[0]->dims, 0));
+        if (0 <= lab && lab < n) {
+          static PyObject* one1 = NULL;
+          if (!one1) one1 = Py_BuildValue("(i)", 1);
+          shape = new_shape(one1, 1);
+          if (!shape) goto fail0;
+          ai_small[0] = lab;
+          n_ai = 1;
+          done = 1;
+        }
+      }
+      break;
     case OP_PNLS_BATCH:
       if (n_in == 1 && PyTuple_CheckExact(aux) && PyTuple_GET_SIZE(shp[0]->dims) == 1 &&
           PyTuple_GET_SIZE(aux) == shp[0]->batch) {
@@ -952,6 +1010,80 @@ out:
   return ret;
 }
 
+/* Tree-LSTM (builders.py TreeLSTM._compose / encode): the node sequence of
+   one leaf or one binary internal cell, node for node, without per-node
+   Python frames; returns (h, c). */
+static PyObject* tree_compose(CoreObj* c, PyObject* gates, PyObject* t1, PyObject* t2, long H) {
+  PyObject *ig = NULL, *og = NULL, *gg = NULL, *cc = NULL, *tc = NULL, *h = NULL, *ret = NULL;
+  if (!(ig = gate(c, gates, 0, H, k_logistic))) goto out;
+  if (!(og = gate(c, gates, 3 * H, 4 * H, k_logistic))) goto out;
+  if (!(gg = gate(c, gates, 4 * H, 5 * H, k_tanh))) goto out;
+  if (!(cc = add2(c, k_cmult, ig, gg))) goto out;
+  if (t1) Py_SETREF(cc, add2(c, k_add, cc, t1));
+  if (!cc) goto out;
+  if (t2) Py_SETREF(cc, add2(c, k_add, cc, t2));
+  if (!cc) goto out;
+  if (!(tc = add1(c, k_tanh, cc, Py_None))) goto out;
+  if (!(h = add2(c, k_cmult, og, tc))) goto out;
+  ret = PyTuple_Pack(2, h, cc);
+out:
+  Py_XDECREF(ig);
+  Py_XDECREF(og);
+  Py_XDECREF(gg);
+  Py_XDECREF(cc);
+  Py_XDECREF(tc);
+  Py_XDECREF(h);
+  return ret;
+}
+
+/* GraphCore.tree_leaf(b, wx, x, H) -> (h, c) */
+static PyObject* core_tree_leaf(CoreObj* c, PyObject* const* args, Py_ssize_t nargs) {
+  if (nargs != 4) {
+    PyErr_SetString(PyExc_TypeError, "tree_leaf(b, wx, x, H)");
+    return NULL;
+  }
+  const long H = PyLong_AsLong(args[3]);
+  if (H == -1 && PyErr_Occurred()) return NULL;
+  PyObject* ins = PyTuple_Pack(3, args[0], args[1], args[2]);
+  if (!ins) return NULL;
+  PyObject* aargs[3] = {k_affine, ins, Py_None};
+  PyObject* gates = core_add(c, aargs, 3);
+  Py_DECREF(ins);
+  if (!gates) return NULL;
+  PyObject* r = tree_compose(c, gates, NULL, NULL, H);
+  Py_DECREF(gates);
+  return r;
+}
+
+/* GraphCore.tree_node(b, u1, h1, u2, h2, c1, c2, H) -> (h, c) */
+static PyObject* core_tree_node(CoreObj* c, PyObject* const* args, Py_ssize_t nargs) {
+  if (nargs != 8) {
+    PyErr_SetString(PyExc_TypeError, "tree_node(b, u1, h1, u2, h2, c1, c2, H)");
+    return NULL;
+  }
+  const long H = PyLong_AsLong(args[7]);
+  if (H == -1 && PyErr_Occurred()) return NULL;
+  PyObject *gates = NULL, *f1 = NULL, *f2 = NULL, *t1 = NULL, *t2 = NULL, *ret = NULL;
+  PyObject* ins = PyTuple_Pack(5, args[0], args[1], args[2], args[3], args[4]);
+  if (!ins) return NULL;
+  PyObject* aargs[3] = {k_affine, ins, Py_None};
+  gates = core_add(c, aargs, 3);
+  Py_DECREF(ins);
+  if (!gates) return NULL;
+  if (!(f1 = gate(c, gates, H, 2 * H, k_logistic))) goto out;
+  if (!(f2 = gate(c, gates, 2 * H, 3 * H, k_logistic))) goto out;
+  if (!(t1 = add2(c, k_cmult, f1, args[5]))) goto out;
+  if (!(t2 = add2(c, k_cmult, f2, args[6]))) goto out;
+  ret = tree_compose(c, gates, t1, t2, H);
+out:
+  Py_XDECREF(gates);
+  Py_XDECREF(f1);
+  Py_XDECREF(f2);
+  Py_XDECREF(t1);
+  Py_XDECREF(t2);
+  return ret;
+}
+
 /* one step through a stack of LSTM layers: pexprs[l] = (wx, wh, b); returns
    (hs', cs') as new lists (builders.py RNNBuilder._step, cell = "lstm") */
 static int lstm_stack_step(CoreObj* c, PyObject* pexprs, PyObject* hs, PyObject* cs, PyObject* x, PyObject* Hobj,
@@ -1048,6 +1180,9 @@ static PyMethodDef core_methods[] = {
     {"renew", (PyCFunction)core_renew, METH_O, "renew(generation)"},
     {"pack", (PyCFunction)core_pack, METH_O, "pack(start) -> raw record pointers"},
     {"lstm", (PyCFunction)(void (*)(void))core_lstm, METH_FASTCALL, "lstm(b, wx, x, wh, h, c, H) -> (h, c)"},
+    {"tree_leaf", (PyCFunction)(void (*)(void))core_tree_leaf, METH_FASTCALL, "tree_leaf(b, wx, x, H) -> (h, c)"},
+    {"tree_node", (PyCFunction)(void (*)(void))core_tree_node, METH_FASTCALL,
+     "tree_node(b, u1, h1, u2, h2, c1, c2, H) -> (h, c)"},
     {"lstm_step", (PyCFunction)(void (*)(void))core_lstm_step, METH_FASTCALL,
      "lstm_step(pexprs, hs, cs, x, H) -> (hs, cs)"},
     {"lstm_transduce", (PyCFunction)(void (*)(void))core_lstm_transduce, METH_FASTCALL,

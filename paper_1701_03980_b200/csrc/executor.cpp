@@ -192,7 +192,16 @@ struct dg_graph_impl;
 
 }  // namespace dg
 
+namespace dg {
+struct Schedule;
+}
+
 struct dg_graph {
+  // last schedule of this graph generation (forward then backward of the same
+  // node set reuse it without rehashing the node table)
+  mutable std::shared_ptr<const dg::Schedule> memo_sched;
+  mutable std::vector<int> memo_active;
+  mutable int memo_scope = -1;
   std::vector<char> bwd_overwrite;  // per node: grad slot overwritten by its only contributor (backward plan)
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -1054,11 +1063,17 @@ static std::shared_ptr<const Schedule> get_schedule(const dg_graph* g, const std
     const char* e = std::getenv("DG_SCHED_CACHE");
     return !(e && e[0] == '0');
   }();
+  if (g->memo_sched && g->memo_scope == scope_hi && g->memo_active == active) return g->memo_sched;
   const uint64_t key = on ? structure_hash(g, active, scope_hi) : 0;
   if (on) {
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
+    if (it != cache.end()) {
+      g->memo_sched = it->second;
+      g->memo_active = active;
+      g->memo_scope = scope_hi;
+      return it->second;
+    }
   }
   auto S = std::make_shared<Schedule>();
   build_schedule(g, active, scope_hi, *S);
@@ -1067,6 +1082,9 @@ static std::shared_ptr<const Schedule> get_schedule(const dg_graph* g, const std
     if (cache.size() >= 256) cache.clear();
     cache.emplace(key, S);
   }
+  g->memo_sched = S;
+  g->memo_active = active;
+  g->memo_scope = scope_hi;
   return S;
 }
 
@@ -1487,6 +1505,8 @@ int dg_graph_set_stream(dg_graph* g, void* stream) {
 }
 
 int dg_graph_renew(dg_graph* g) {
+  g->memo_sched.reset();
+  g->memo_scope = -1;
   g->nodes.clear();
   g->inputs.clear();
   g->aux_i.clear();

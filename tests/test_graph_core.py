@@ -116,3 +116,70 @@ def test_int_tuple_is_tuple_map_int():
     assert int_tuple(()) == ()
     with pytest.raises(ValueError):
         int_tuple(["x"])
+
+
+def _small_graph():
+    pools = dy.new_poolset(64, 64, 64)
+    cg, model = dy.ComputationGraph(pools), dy.Model(pools, seed=1)
+    E = model.add_lookup_parameters(12, 5)
+    W = model.add_parameters((7, 10), "W")
+    a, b = ops.lookup(cg, E, 3), ops.lookup(cg, E, 11)
+    z = ops.matmul(ops.parameter(cg, W), ops.concatenate([a, b]))
+    loss = ops.pickneglogsoftmax(z, 4)
+    bz = ops.concatenate([ops.lookup_batch(cg, E, [1, 2]), ops.lookup_batch(cg, E, [3, 4])])
+    return cg, loss, bz
+
+
+@pytest.mark.parametrize("kinds", [("lookup",), ("concatenate",), ("pickneglogsoftmax",)])
+def test_native_fast_kinds_match_python_rules(kinds):
+    from paper_1701_03980_b200 import ops as ops_mod
+
+    cg_n, _, _ = _small_graph()
+    saved = {k: ops_mod.FAST_KINDS.pop(k) for k in kinds}
+    try:
+        cg_p, _, _ = _small_graph()
+    finally:
+        ops_mod.FAST_KINDS.update(saved)
+    assert _nodes(cg_n) == _nodes(cg_p)
+    for a, b in zip(_records(cg_n), _records(cg_p)):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_native_fast_kinds_raise_reference_errors():
+    pools = dy.new_poolset(64, 64, 64)
+    cg, model = dy.ComputationGraph(pools), dy.Model(pools, seed=1)
+    E = model.add_lookup_parameters(4, 3)
+    with pytest.raises(dy.errors.IndexOutOfBounds):
+        ops.lookup(cg, E, 4)
+    x = ops.lookup(cg, E, 1)
+    with pytest.raises(dy.errors.IndexOutOfBounds):
+        ops.pickneglogsoftmax(x, 3)
+    xb = ops.lookup_batch(cg, E, [0, 1])
+    with pytest.raises(dy.errors.ShapeError):
+        ops.concatenate([x, xb])
+
+
+def _tree_graph(native):
+    from paper_1701_03980_b200 import workloads as W
+
+    pools = dy.new_poolset(64, 64, 64)
+    cg, model = dy.ComputationGraph(pools), dy.Model(pools, seed=1)
+    td = W.tree_corpus(3, 2, vocab=50)
+    enc = dy.TreeLSTM(model, {f"w{i}": i for i in range(50)}, 6, 5, "enc")
+    saved = cg._core
+    if not native:
+        cg._core = None
+    try:
+        outs = [enc.encode(cg, W.to_treenode(dy, t)) for t in td.trees]
+    finally:
+        cg._core = saved
+    return cg, outs
+
+
+def test_native_tree_lstm_matches_node_by_node_path():
+    cg_n, out_n = _tree_graph(True)
+    cg_p, out_p = _tree_graph(False)
+    assert _nodes(cg_n) == _nodes(cg_p)
+    assert [(h.index, c.index) for h, c in out_n] == [(h.index, c.index) for h, c in out_p]
+    for a, b in zip(_records(cg_n), _records(cg_p)):
+        np.testing.assert_array_equal(a, b)
