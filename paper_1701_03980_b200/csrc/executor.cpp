@@ -2676,7 +2676,8 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
             }
             return launch_softmax_bwd(a, st);
           });
-          plan.tag(pnls ? C_PNLS_BWD : C_ELEMWISE, 0.0, (double)a.rows * a.width * 4 * 3);
+          // logits read + dlogits written (and read, when accumulated)
+          plan.tag(pnls ? C_PNLS_BWD : C_ELEMWISE, 0.0, (double)a.rows * a.width * 4 * (a.overwrite ? 2 : 3));
           break;
         }
         case DG_OP_MATMUL: {
