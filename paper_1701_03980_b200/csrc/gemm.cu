@@ -108,6 +108,7 @@ template <int BM, int BN, int BK, int TM, int TN, bool kAK, bool kBN, bool kCl>
 __global__ void __launch_bounds__(Cfg<BM, BN, BK, TM, TN>::kThreads)
     gemm_group_kernel(const GemmProblem* __restrict__ probs, int n_probs, float* __restrict__ work,
                       int* __restrict__ counters) {
+  pdl_prologue();
   using C = Cfg<BM, BN, BK, TM, TN>;
   __shared__ __align__(16) float As[2][BK * C::kApad];
   __shared__ __align__(16) float Bs[2][BK * C::kBpad];
@@ -343,19 +344,21 @@ void launch_one(const GemmLaunch& L, const GemmProblem* probs, float* work, int*
       cfg.gridDim = dim3(L.ctas);
       cfg.blockDim = dim3(C::kThreads);
       cfg.stream = s;
-      cudaLaunchAttribute attr[1];
+      cudaLaunchAttribute attr[2];
       attr[0].id = cudaLaunchAttributeClusterDimension;
       attr[0].val.clusterDim.x = L.cluster;
       attr[0].val.clusterDim.y = 1;
       attr[0].val.clusterDim.z = 1;
+      attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
       cfg.attrs = attr;
-      cfg.numAttrs = 1;
+      cfg.numAttrs = 2;
       cudaLaunchKernelEx(&cfg, gemm_group_kernel<BM, BN, BK, TM, TN, kAK, kBN, true>, probs, L.n_probs, work,
                          counters);
     }
     return;
   }
-  gemm_group_kernel<BM, BN, BK, TM, TN, kAK, kBN, false><<<L.ctas, C::kThreads, 0, s>>>(probs, L.n_probs, work,
+  launch_k(gemm_group_kernel<BM, BN, BK, TM, TN, kAK, kBN, false>, L.ctas, C::kThreads, 0, s, probs, L.n_probs, work,
                                                                                         counters);
 }
 

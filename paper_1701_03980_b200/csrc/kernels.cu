@@ -13,6 +13,15 @@
 
 namespace dg {
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DG_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+
 namespace {
 
 constexpr int kThreads = 256;
@@ -37,6 +46,7 @@ __device__ __forceinline__ float warp_max(float v) {
 // ------------------------------------------------------------------ elementwise
 
 __global__ void ew_fwd_kernel(EwArgs a) {
+  pdl_prologue();
   const int64_t size = static_cast<int64_t>(a.elem) * a.batch;
   const int64_t total = size * a.n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -58,6 +68,7 @@ __global__ void ew_fwd_kernel(EwArgs a) {
 
 // no-broadcast backward: one thread per output element
 __global__ void ew_bwd_flat_kernel(EwArgs a) {
+  pdl_prologue();
   const int64_t size = static_cast<int64_t>(a.elem) * a.batch;
   const int64_t total = size * a.n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -93,6 +104,7 @@ __global__ void ew_bwd_flat_kernel(EwArgs a) {
 // broadcast backward (binary ops): one thread per (node, element) loops over
 // the batch so batch-1 operands receive the batch sum (ops.py:69-75)
 __global__ void ew_bwd_bcast_kernel(EwArgs a) {
+  pdl_prologue();
   const int64_t total = static_cast<int64_t>(a.elem) * a.n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int j = static_cast<int>(t / a.elem);
@@ -122,6 +134,7 @@ __global__ void ew_bwd_bcast_kernel(EwArgs a) {
 }
 
 __global__ void chain_fwd_kernel(ChainArgs a) {
+  pdl_prologue();
   const int64_t total = (int64_t)a.size * a.n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int j = static_cast<int>(t / a.size);
@@ -136,6 +149,7 @@ __global__ void chain_fwd_kernel(ChainArgs a) {
 }
 
 __global__ void chain_bwd_kernel(ChainArgs a) {
+  pdl_prologue();
   const int64_t total = (int64_t)a.size * a.n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int j = static_cast<int>(t / a.size);
@@ -150,6 +164,7 @@ __global__ void chain_bwd_kernel(ChainArgs a) {
 // prefetches the terms into shared memory, one thread adds them in the same
 // left-to-right order, and the block writes the prefixes back in parallel.
 __global__ void chain_fwd_seq_kernel(ChainArgs a) {
+  pdl_prologue();
   __shared__ float t[1024];
   const int j = blockIdx.x / a.size;
   const int64_t e = blockIdx.x - (int64_t)j * a.size;
@@ -174,6 +189,7 @@ __global__ void chain_fwd_seq_kernel(ChainArgs a) {
 // every (slot, element) of a chain whose gradient slots are all distinct
 // (checked on the host): g of the last add is added to each independently
 __global__ void chain_bwd_par_kernel(ChainArgs a) {
+  pdl_prologue();
   const int64_t per = (int64_t)a.n * a.size;
   const int64_t total = (int64_t)(2 * a.len + 1) * per;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -210,6 +226,7 @@ struct CellSlots {
 // One cell per block: the cell's slot pointers are staged in shared memory once.
 template <int M>
 __global__ void __launch_bounds__(256) cell_fwd_kernel(CellArgs a) {
+  pdl_prologue();
   const CellSlots S(M);
   __shared__ const float* sv[20];
   const int64_t per = (int64_t)a.batch * a.H;
@@ -259,6 +276,7 @@ __global__ void __launch_bounds__(256) cell_fwd_kernel(CellArgs a) {
 // (deterministic, no atomics).  Otherwise one thread per (cell, row, unit).
 template <int M, bool kLoopBatch>
 __global__ void __launch_bounds__(256) cell_bwd_kernel(CellArgs a) {
+  pdl_prologue();
   const CellSlots S(M);
   __shared__ float red[M > 0 ? M : 1][8][32];
   __shared__ const float* sv[20];
@@ -361,6 +379,7 @@ __global__ void __launch_bounds__(256) cell_bwd_kernel(CellArgs a) {
 // ------------------------------------------------------------------ structural
 
 __global__ void pick_fwd_kernel(PickArgs a) {
+  pdl_prologue();
   const int64_t per = (int64_t)a.batch * a.width;
   const int64_t total = per * a.n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -372,6 +391,7 @@ __global__ void pick_fwd_kernel(PickArgs a) {
 }
 
 __global__ void pick_bwd_kernel(PickArgs a) {
+  pdl_prologue();
   const int64_t per = (int64_t)a.batch * a.width;
   const int64_t total = per * a.n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -389,6 +409,7 @@ __device__ __forceinline__ int find_part(const int* offs, int parts, int col) {
 }
 
 __global__ void concat_fwd_kernel(ConcatArgs a) {
+  pdl_prologue();
   const int64_t per = (int64_t)a.batch * a.total;
   const int64_t all = per * a.n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < all; t += (int64_t)gridDim.x * blockDim.x) {
@@ -402,6 +423,7 @@ __global__ void concat_fwd_kernel(ConcatArgs a) {
 }
 
 __global__ void concat_bwd_kernel(ConcatArgs a) {
+  pdl_prologue();
   const int64_t per = (int64_t)a.batch * a.total;
   const int64_t all = per * a.n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < all; t += (int64_t)gridDim.x * blockDim.x) {
@@ -415,6 +437,7 @@ __global__ void concat_bwd_kernel(ConcatArgs a) {
 }
 
 __global__ void sum_batches_fwd_kernel(SumBatchesArgs a) {
+  pdl_prologue();
   const int64_t total = (int64_t)a.elem * a.n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int j = static_cast<int>(t / a.elem);
@@ -426,6 +449,7 @@ __global__ void sum_batches_fwd_kernel(SumBatchesArgs a) {
 }
 
 __global__ void sum_batches_bwd_kernel(SumBatchesArgs a) {
+  pdl_prologue();
   const int64_t per = (int64_t)a.batch * a.elem;
   const int64_t total = per * a.n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -475,6 +499,7 @@ __device__ __forceinline__ float row_reduce_sum(float v, float* sh) {
 // op: 0 softmax fwd, 1 softmax bwd, 2 pnls fwd, 3 pnls bwd
 template <int kOp, bool kBlock>
 __global__ void row_kernel(RowArgs a) {
+  pdl_prologue();
   __shared__ float sh[32];
   const int row = kBlock ? blockIdx.x : (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
   if (row >= a.rows) return;
@@ -522,6 +547,7 @@ __global__ void row_kernel(RowArgs a) {
 // Rows that are not 16 B aligned take the strided path above.
 template <int kOp, int kV>
 __global__ void __launch_bounds__(256) row_reg_kernel(RowArgs a) {
+  pdl_prologue();
   __shared__ float sh[32];
   const int row = blockIdx.x;
   const int j = row / a.batch, b = row - j * a.batch;
@@ -607,15 +633,15 @@ int launch_rows(const RowArgs& a, cudaStream_t s) {
   if (a.rows <= 0) return 0;
   if (a.width > 512 && (a.width & 3) == 0 && a.width <= 256 * 4 * 16 && kOp != 1) {
     const int need = (a.width / 4 + 255) / 256;
-    if (need <= 4) row_reg_kernel<kOp, 4><<<a.rows, 256, 0, s>>>(a);
-    else if (need <= 8) row_reg_kernel<kOp, 8><<<a.rows, 256, 0, s>>>(a);
-    else if (need <= 12) row_reg_kernel<kOp, 12><<<a.rows, 256, 0, s>>>(a);
-    else row_reg_kernel<kOp, 16><<<a.rows, 256, 0, s>>>(a);
+    if (need <= 4) launch_k(row_reg_kernel<kOp, 4>, a.rows, 256, 0, s, a);
+    else if (need <= 8) launch_k(row_reg_kernel<kOp, 8>, a.rows, 256, 0, s, a);
+    else if (need <= 12) launch_k(row_reg_kernel<kOp, 12>, a.rows, 256, 0, s, a);
+    else launch_k(row_reg_kernel<kOp, 16>, a.rows, 256, 0, s, a);
   } else if (a.width > 512) {
-    row_kernel<kOp, true><<<a.rows, 256, 0, s>>>(a);
+    launch_k(row_kernel<kOp, true>, a.rows, 256, 0, s, a);
   } else {
     const int rows_per_block = 8;
-    row_kernel<kOp, false><<<(a.rows + rows_per_block - 1) / rows_per_block, 32 * rows_per_block, 0, s>>>(a);
+    launch_k(row_kernel<kOp, false>, (a.rows + rows_per_block - 1) / rows_per_block, 32 * rows_per_block, 0, s, a);
   }
   return 1;
 }
@@ -624,6 +650,7 @@ int launch_rows(const RowArgs& a, cudaStream_t s) {
 
 __global__ void gather_rows_kernel(const float* __restrict__ table, int dim, const int64_t* __restrict__ ids,
                                    float* const* out_rows, int rows) {
+  pdl_prologue();
   const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= rows) return;
   const int lane = threadIdx.x & 31;
@@ -645,6 +672,7 @@ constexpr int kScatterWarps = 32;
 __global__ void segment_scatter_add_kernel(float* __restrict__ table_grad, int dim, const int64_t* __restrict__ ids,
                                            const int* __restrict__ seg, const float* const* src_rows, int n_unique,
                                            float scale) {
+  pdl_prologue();
   // one block per unique id; warp w sums rows k0+w, k0+w+W, ... (a long
   // segment, e.g. the EOS padding id, is spread over W = 32 warps), then the
   // W partials are reduced in fixed warp order: deterministic, no atomics.
@@ -696,6 +724,7 @@ __global__ void segment_scatter_add_kernel(float* __restrict__ table_grad, int d
 
 __global__ void pack_rows_kernel(const float* __restrict__ table, int dim, const int64_t* __restrict__ ids,
                                  float* __restrict__ out, int n) {
+  pdl_prologue();
   const int64_t total = (int64_t)n * dim;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t u = t / dim, c = t - u * dim;
@@ -707,6 +736,7 @@ __global__ void pack_rows_kernel(const float* __restrict__ table, int dim, const
 
 // matmul per batch element, column-major: out(i,c) = sum_t A(i,t) X(t,c)
 __global__ void matmul_fwd_kernel(MatmulArgs a) {
+  pdl_prologue();
   const int64_t osz = (int64_t)a.m * a.p;
   const int64_t total = osz * a.batch * a.n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -724,6 +754,7 @@ __global__ void matmul_fwd_kernel(MatmulArgs a) {
 
 // gA(i,q) += sum_b sum_c g(i,c) X(q,c);  one thread per (node, A-batch, element)
 __global__ void matmul_bwd_a_kernel(MatmulArgs a) {
+  pdl_prologue();
   const int ab = a.a_b1 ? 1 : a.batch;
   const int64_t asz = (int64_t)a.m * a.k;
   const int64_t total = asz * ab * a.n;
@@ -746,6 +777,7 @@ __global__ void matmul_bwd_a_kernel(MatmulArgs a) {
 
 // gX(q,c) += sum_b sum_i A(i,q) g(i,c)
 __global__ void matmul_bwd_x_kernel(MatmulArgs a) {
+  pdl_prologue();
   const int xb = a.x_b1 ? 1 : a.batch;
   const int64_t xsz = (int64_t)a.k * a.p;
   const int64_t total = xsz * xb * a.n;
@@ -767,6 +799,7 @@ __global__ void matmul_bwd_x_kernel(MatmulArgs a) {
 }
 
 __global__ void affine_generic_fwd_kernel(AffineGenericArgs a) {
+  pdl_prologue();
   const int64_t total = (int64_t)a.m * a.batch * a.n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t jb = t / a.m;
@@ -787,6 +820,7 @@ __global__ void affine_generic_fwd_kernel(AffineGenericArgs a) {
 
 // which: 0 bias, 1 W of term k, 2 x of term k
 __global__ void affine_generic_bwd_kernel(AffineGenericArgs a, int which, int k) {
+  pdl_prologue();
   const int K = which == 0 ? 1 : a.kdim[k];
   int ob;  // operand batch
   int64_t osz;
@@ -822,6 +856,7 @@ __global__ void affine_generic_bwd_kernel(AffineGenericArgs a, int which, int k)
 
 // column sums over gathered rows, two deterministic passes
 __global__ void colsum_partial_kernel(const float* const* rows, int n_rows, int width, int chunks, float* work) {
+  pdl_prologue();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int ch = blockIdx.y;
   if (c >= width) return;
@@ -844,6 +879,7 @@ __global__ void colsum_partial_kernel(const float* const* rows, int n_rows, int 
 }
 
 __global__ void colsum_final_kernel(float* dst, const float* work, int width, int chunks) {
+  pdl_prologue();
   // block = 32 columns x 8 chunk groups; group y sums chunks y, y+8, ...
   // (4 in flight), then the 8 group sums are added in fixed order
   __shared__ float part[8][33];
@@ -873,6 +909,7 @@ __global__ void colsum_final_kernel(float* dst, const float* work, int width, in
 
 __global__ void row_reduce_scatter_kernel(float* const* dst_rows, const int* seg, const float* src, int n_targets,
                                           int width) {
+  pdl_prologue();
   // one block per target row; 8 warps split the segment, fixed-order reduce
   __shared__ float part[8][128];
   const int u = blockIdx.x;
@@ -939,6 +976,7 @@ __device__ __forceinline__ void apply_rule(const RuleArgs& r, float& w, float& g
 constexpr int kUpdChunk = 2048;
 
 __global__ void update_dense_kernel(RuleArgs r, const TensorSeg* __restrict__ segs, int nseg) {
+  pdl_prologue();
   // locate this block's segment: segments are laid out in order, each taking
   // ceil(n / kUpdChunk) blocks
   int blk = blockIdx.x, s = 0;
@@ -964,6 +1002,7 @@ __global__ void update_dense_kernel(RuleArgs r, const TensorSeg* __restrict__ se
 
 __global__ void update_rows_kernel(RuleArgs r, float* w, float* g, float* s0, float* s1, int dim,
                                    const int64_t* __restrict__ ids, int n_rows) {
+  pdl_prologue();
   const int64_t total = (int64_t)n_rows * dim;
   float dummy0 = 0.f, dummy1 = 0.f;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -977,10 +1016,12 @@ __global__ void update_rows_kernel(RuleArgs r, float* w, float* g, float* s0, fl
 }
 
 __global__ void scale_kernel(float* y, int64_t n, float alpha) {
+  pdl_prologue();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
     y[t] *= alpha;
 }
 __global__ void fill_kernel(float* y, int64_t n, float v) {
+  pdl_prologue();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
     y[t] = v;
 }
@@ -999,45 +1040,45 @@ inline int grid_for(int64_t n) {
 int launch_ew_fwd(const EwArgs& a, cudaStream_t s) {
   const int64_t total = (int64_t)a.elem * a.batch * a.n;
   if (total == 0) return 0;
-  ew_fwd_kernel<<<grid_for(total), kThreads, 0, s>>>(a);
+  launch_k(ew_fwd_kernel, grid_for(total), kThreads, 0, s, a);
   return 1;
 }
 
 int launch_ew_bwd(const EwArgs& a, cudaStream_t s) {
   const bool bcast_ok = a.kind == EW_ADD || a.kind == EW_CMULT || a.kind == EW_SCALE;
   if (bcast_ok && (a.a_b1 || a.b_b1) && a.batch > 1) {
-    ew_bwd_bcast_kernel<<<grid_for((int64_t)a.elem * a.n), kThreads, 0, s>>>(a);
+    launch_k(ew_bwd_bcast_kernel, grid_for((int64_t)a.elem * a.n), kThreads, 0, s, a);
   } else {
     EwArgs c = a;
     c.a_b1 = c.b_b1 = 0;
-    ew_bwd_flat_kernel<<<grid_for((int64_t)a.elem * a.batch * a.n), kThreads, 0, s>>>(c);
+    launch_k(ew_bwd_flat_kernel, grid_for((int64_t)a.elem * a.batch * a.n), kThreads, 0, s, c);
   }
   return 1;
 }
 
 int launch_chain_fwd(const ChainArgs& a, cudaStream_t s) {
   if ((int64_t)a.size * a.n < 2048 && a.len >= 8) {
-    chain_fwd_seq_kernel<<<a.size * a.n, 256, 0, s>>>(a);
+    launch_k(chain_fwd_seq_kernel, a.size * a.n, 256, 0, s, a);
     return 1;
   }
-  chain_fwd_kernel<<<grid_for((int64_t)a.size * a.n), kThreads, 0, s>>>(a);
+  launch_k(chain_fwd_kernel, grid_for((int64_t)a.size * a.n), kThreads, 0, s, a);
   return 1;
 }
 int launch_chain_bwd(const ChainArgs& a, cudaStream_t s) {
   if (a.distinct) {
-    chain_bwd_par_kernel<<<grid_for((int64_t)(2 * a.len + 1) * a.n * a.size), kThreads, 0, s>>>(a);
+    launch_k(chain_bwd_par_kernel, grid_for((int64_t)(2 * a.len + 1) * a.n * a.size), kThreads, 0, s, a);
     return 1;
   }
-  chain_bwd_kernel<<<grid_for((int64_t)a.size * a.n), kThreads, 0, s>>>(a);
+  launch_k(chain_bwd_kernel, grid_for((int64_t)a.size * a.n), kThreads, 0, s, a);
   return 1;
 }
 
 int launch_cell_fwd(const CellArgs& a, cudaStream_t s) {
   const int g = a.n * (int)(((int64_t)a.batch * a.H + 255) / 256);
   switch (a.m) {
-    case 0: cell_fwd_kernel<0><<<g, kThreads, 0, s>>>(a); break;
-    case 1: cell_fwd_kernel<1><<<g, kThreads, 0, s>>>(a); break;
-    default: cell_fwd_kernel<2><<<g, kThreads, 0, s>>>(a); break;
+    case 0: launch_k(cell_fwd_kernel<0>, g, kThreads, 0, s, a); break;
+    case 1: launch_k(cell_fwd_kernel<1>, g, kThreads, 0, s, a); break;
+    default: launch_k(cell_fwd_kernel<2>, g, kThreads, 0, s, a); break;
   }
   return 1;
 }
@@ -1048,38 +1089,38 @@ int launch_cell_bwd(const CellArgs& a, cudaStream_t s) {
   // broadcast variant: exactly one block per (cell, 32-unit chunk), single pass
   const int g = bcast ? a.n * ((a.H + 31) / 32) : a.n * (int)(((int64_t)a.batch * a.H + 255) / 256);
   switch (a.m * 2 + (bcast ? 1 : 0)) {
-    case 0: cell_bwd_kernel<0, false><<<g, kThreads, 0, s>>>(a); break;
-    case 1: cell_bwd_kernel<0, true><<<g, kThreads, 0, s>>>(a); break;
-    case 2: cell_bwd_kernel<1, false><<<g, kThreads, 0, s>>>(a); break;
-    case 3: cell_bwd_kernel<1, true><<<g, kThreads, 0, s>>>(a); break;
-    case 4: cell_bwd_kernel<2, false><<<g, kThreads, 0, s>>>(a); break;
-    default: cell_bwd_kernel<2, true><<<g, kThreads, 0, s>>>(a); break;
+    case 0: launch_k(cell_bwd_kernel<0, false>, g, kThreads, 0, s, a); break;
+    case 1: launch_k(cell_bwd_kernel<0, true>, g, kThreads, 0, s, a); break;
+    case 2: launch_k(cell_bwd_kernel<1, false>, g, kThreads, 0, s, a); break;
+    case 3: launch_k(cell_bwd_kernel<1, true>, g, kThreads, 0, s, a); break;
+    case 4: launch_k(cell_bwd_kernel<2, false>, g, kThreads, 0, s, a); break;
+    default: launch_k(cell_bwd_kernel<2, true>, g, kThreads, 0, s, a); break;
   }
   return 1;
 }
 
 int launch_pick_fwd(const PickArgs& a, cudaStream_t s) {
-  pick_fwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.width), kThreads, 0, s>>>(a);
+  launch_k(pick_fwd_kernel, grid_for((int64_t)a.n * a.batch * a.width), kThreads, 0, s, a);
   return 1;
 }
 int launch_pick_bwd(const PickArgs& a, cudaStream_t s) {
-  pick_bwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.width), kThreads, 0, s>>>(a);
+  launch_k(pick_bwd_kernel, grid_for((int64_t)a.n * a.batch * a.width), kThreads, 0, s, a);
   return 1;
 }
 int launch_concat_fwd(const ConcatArgs& a, cudaStream_t s) {
-  concat_fwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.total), kThreads, 0, s>>>(a);
+  launch_k(concat_fwd_kernel, grid_for((int64_t)a.n * a.batch * a.total), kThreads, 0, s, a);
   return 1;
 }
 int launch_concat_bwd(const ConcatArgs& a, cudaStream_t s) {
-  concat_bwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.total), kThreads, 0, s>>>(a);
+  launch_k(concat_bwd_kernel, grid_for((int64_t)a.n * a.batch * a.total), kThreads, 0, s, a);
   return 1;
 }
 int launch_sum_batches_fwd(const SumBatchesArgs& a, cudaStream_t s) {
-  sum_batches_fwd_kernel<<<grid_for((int64_t)a.n * a.elem), kThreads, 0, s>>>(a);
+  launch_k(sum_batches_fwd_kernel, grid_for((int64_t)a.n * a.elem), kThreads, 0, s, a);
   return 1;
 }
 int launch_sum_batches_bwd(const SumBatchesArgs& a, cudaStream_t s) {
-  sum_batches_bwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.elem), kThreads, 0, s>>>(a);
+  launch_k(sum_batches_bwd_kernel, grid_for((int64_t)a.n * a.batch * a.elem), kThreads, 0, s, a);
   return 1;
 }
 
@@ -1091,45 +1132,45 @@ int launch_pnls_bwd(const RowArgs& a, cudaStream_t s) { return launch_rows<3>(a,
 int launch_gather_rows(const float* table, int dim, const int64_t* ids, float* const* out_rows, int rows,
                        cudaStream_t s) {
   if (rows <= 0) return 0;
-  gather_rows_kernel<<<(rows + 7) / 8, 256, 0, s>>>(table, dim, ids, out_rows, rows);
+  launch_k(gather_rows_kernel, (rows + 7) / 8, 256, 0, s, table, dim, ids, out_rows, rows);
   return 1;
 }
 
 int launch_segment_scatter_add(float* table_grad, int dim, const int64_t* uniq_ids, const int* seg,
                                const float* const* src_rows, int n_unique, float scale, cudaStream_t s) {
   if (n_unique <= 0) return 0;
-  segment_scatter_add_kernel<<<n_unique, 32 * kScatterWarps, 0, s>>>(table_grad, dim, uniq_ids, seg, src_rows,
+  launch_k(segment_scatter_add_kernel, n_unique, 32 * kScatterWarps, 0, s, table_grad, dim, uniq_ids, seg, src_rows,
                                                                       n_unique, scale);
   return 1;
 }
 
 int launch_pack_rows(const float* table, int dim, const int64_t* ids, float* out, int n, cudaStream_t s) {
   if (n <= 0) return 0;
-  pack_rows_kernel<<<grid_for((int64_t)n * dim), kThreads, 0, s>>>(table, dim, ids, out, n);
+  launch_k(pack_rows_kernel, grid_for((int64_t)n * dim), kThreads, 0, s, table, dim, ids, out, n);
   return 1;
 }
 
 int launch_matmul_fwd(const MatmulArgs& a, cudaStream_t s) {
-  matmul_fwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.m * a.p), kThreads, 0, s>>>(a);
+  launch_k(matmul_fwd_kernel, grid_for((int64_t)a.n * a.batch * a.m * a.p), kThreads, 0, s, a);
   return 1;
 }
 int launch_matmul_bwd(const MatmulArgs& a, cudaStream_t s) {
-  matmul_bwd_a_kernel<<<grid_for((int64_t)a.n * a.batch * a.m * a.k), kThreads, 0, s>>>(a);
-  matmul_bwd_x_kernel<<<grid_for((int64_t)a.n * a.batch * a.k * a.p), kThreads, 0, s>>>(a);
+  launch_k(matmul_bwd_a_kernel, grid_for((int64_t)a.n * a.batch * a.m * a.k), kThreads, 0, s, a);
+  launch_k(matmul_bwd_x_kernel, grid_for((int64_t)a.n * a.batch * a.k * a.p), kThreads, 0, s, a);
   return 2;
 }
 
 int launch_affine_generic_fwd(const AffineGenericArgs& a, cudaStream_t s) {
-  affine_generic_fwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.m), kThreads, 0, s>>>(a);
+  launch_k(affine_generic_fwd_kernel, grid_for((int64_t)a.n * a.batch * a.m), kThreads, 0, s, a);
   return 1;
 }
 int launch_affine_generic_bwd(const AffineGenericArgs& a, cudaStream_t s) {
   int launches = 0;
-  affine_generic_bwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.m), kThreads, 0, s>>>(a, 0, 0);
+  launch_k(affine_generic_bwd_kernel, grid_for((int64_t)a.n * a.batch * a.m), kThreads, 0, s, a, 0, 0);
   ++launches;
   for (int k = 0; k < a.terms; ++k) {
-    affine_generic_bwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.m * a.kdim[k]), kThreads, 0, s>>>(a, 1, k);
-    affine_generic_bwd_kernel<<<grid_for((int64_t)a.n * a.batch * a.kdim[k]), kThreads, 0, s>>>(a, 2, k);
+    launch_k(affine_generic_bwd_kernel, grid_for((int64_t)a.n * a.batch * a.m * a.kdim[k]), kThreads, 0, s, a, 1, k);
+    launch_k(affine_generic_bwd_kernel, grid_for((int64_t)a.n * a.batch * a.kdim[k]), kThreads, 0, s, a, 2, k);
     launches += 2;
   }
   return launches;
@@ -1146,39 +1187,39 @@ int launch_colsum_rows(float* dst, const float* const* rows, int n_rows, int wid
   chunks = (int)std::min<int64_t>(chunks, std::max<int64_t>(1, work_floats / std::max(1, width)));
   chunks = std::min(chunks, 1024);
   dim3 g1((width + 255) / 256, chunks);
-  colsum_partial_kernel<<<g1, 256, 0, s>>>(rows, n_rows, width, chunks, work);
-  colsum_final_kernel<<<(width + 31) / 32, 256, 0, s>>>(dst, work, width, chunks);
+  launch_k(colsum_partial_kernel, g1, 256, 0, s, rows, n_rows, width, chunks, work);
+  launch_k(colsum_final_kernel, (width + 31) / 32, 256, 0, s, dst, work, width, chunks);
   return 2;
 }
 
 int launch_row_reduce_scatter(float* const* dst_rows, const int* seg, const float* src, int n_targets, int width,
                               cudaStream_t s) {
   if (n_targets <= 0) return 0;
-  row_reduce_scatter_kernel<<<n_targets, 256, 0, s>>>(dst_rows, seg, src, n_targets, width);
+  launch_k(row_reduce_scatter_kernel, n_targets, 256, 0, s, dst_rows, seg, src, n_targets, width);
   return 1;
 }
 
 int launch_update_dense(const RuleArgs& r, const TensorSeg* segs_dev, int nseg, int64_t total_blocks, cudaStream_t s) {
   if (nseg <= 0 || total_blocks <= 0) return 0;
-  update_dense_kernel<<<static_cast<unsigned>(total_blocks), 256, 0, s>>>(r, segs_dev, nseg);
+  launch_k(update_dense_kernel, static_cast<unsigned>(total_blocks), 256, 0, s, r, segs_dev, nseg);
   return 1;
 }
 
 int launch_update_rows(const RuleArgs& r, float* w, float* g, float* s0, float* s1, int dim, const int64_t* ids,
                        int n_rows, cudaStream_t s) {
   if (n_rows <= 0) return 0;
-  update_rows_kernel<<<grid_for((int64_t)n_rows * dim), kThreads, 0, s>>>(r, w, g, s0, s1, dim, ids, n_rows);
+  launch_k(update_rows_kernel, grid_for((int64_t)n_rows * dim), kThreads, 0, s, r, w, g, s0, s1, dim, ids, n_rows);
   return 1;
 }
 
 int launch_scale(float* y, int64_t n, float alpha, cudaStream_t s) {
   if (n <= 0) return 0;
-  scale_kernel<<<grid_for(n), kThreads, 0, s>>>(y, n, alpha);
+  launch_k(scale_kernel, grid_for(n), kThreads, 0, s, y, n, alpha);
   return 1;
 }
 int launch_fill(float* y, int64_t n, float v, cudaStream_t s) {
   if (n <= 0) return 0;
-  fill_kernel<<<grid_for(n), kThreads, 0, s>>>(y, n, v);
+  launch_k(fill_kernel, grid_for(n), kThreads, 0, s, y, n, v);
   return 1;
 }
 

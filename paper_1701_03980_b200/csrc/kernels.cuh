@@ -13,6 +13,36 @@
 
 namespace dg {
 
+// Programmatic dependent launch: every kernel starts with pdl_prologue()
+// (wait for the preceding grid's completion and memory, then let the next
+// grid launch), and launch_k() launches with programmatic stream
+// serialization, so a kernel's launch and CTA rasterisation overlap the tail
+// of the one before it.  DG_PDL=0 launches without the attribute (the
+// prologue is then a no-op).
+__device__ __forceinline__ void pdl_prologue() {
+#if defined(__CUDA_ARCH__)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+
 // ---------------------------------------------------------------- elementwise
 enum EwKind : int {
   EW_TANH = 0, EW_LOGISTIC = 1, EW_SCALE = 2, EW_ADD = 3, EW_CMULT = 4

@@ -143,6 +143,7 @@ struct StepPtrs {
 
 template <int BS>
 __global__ void __launch_bounds__(kRT, 1) rnn_fwd_kernel(const __grid_constant__ RnnArgs a) {
+  pdl_prologue();
   extern __shared__ float4 smem4[];
   float* sm = reinterpret_cast<float*>(smem4);
   __shared__ StepPtrs sp[2];
@@ -456,6 +457,7 @@ struct StepPtrs2 {
 
 template <int BS>
 __global__ void __launch_bounds__(kRT, 1) rnn_bwd_kernel(const __grid_constant__ RnnArgs a) {
+  pdl_prologue();
   extern __shared__ float4 smem4[];
   float* sm = reinterpret_cast<float*>(smem4);
   __shared__ StepPtrs2 sp[2];
@@ -757,6 +759,7 @@ __device__ __forceinline__ void mma3(float* c, const float* a, float4 b) {
 // cluster through distributed shared memory.
 template <int BS>
 __global__ void __launch_bounds__(kClThreads, 1) rnn_fwd_cl_kernel(const __grid_constant__ RnnArgs a) {
+  pdl_prologue();
   extern __shared__ float4 smem4[];
   float* sm = reinterpret_cast<float*>(smem4);
   __shared__ StepPtrs sp[2];
@@ -995,6 +998,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_fwd_cl_kernel(const __grid_
 // slots in rank order (deterministic).
 template <int BS>
 __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_constant__ RnnArgs a) {
+  pdl_prologue();
   extern __shared__ float4 smem4[];
   float* sm = reinterpret_cast<float*>(smem4);
   __shared__ StepPtrs2 sp[2];
@@ -1211,6 +1215,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
 
 // dst[u] += sum_b dc0[b][u] * af0[b][u]  (batch-1 c_{-1} of each listed chain)
 __global__ void rnn_c0_kernel(RnnC0 a) {
+  pdl_prologue();
   // block = (chain k, 32 units); 8 warps split the batch, fixed-order reduce
   __shared__ float red[8][32];
   int k = 0, base = 0;
@@ -1320,6 +1325,11 @@ int launch_cl_bs(const RnnArgs& a, bool bwd, size_t smem, int cluster, cudaStrea
     cudaGetLastError();
     return -2;
   }
+  cudaLaunchAttribute at2[2] = {at[0], {}};
+  at2[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at2[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at2;
+  cfg.numAttrs = 2;
   if (cudaLaunchKernelEx(&cfg, k, a) != cudaSuccess) return -1;
   return 1;
 }
@@ -1402,7 +1412,7 @@ int launch_rnn_c0(const RnnC0& a, cudaStream_t s) {
   int blocks = 0;
   for (int k = 0; k < a.n; ++k) blocks += (a.H[k] + 31) / 32;
   if (blocks == 0) return 0;
-  rnn_c0_kernel<<<blocks, 256, 0, s>>>(a);
+  launch_k(rnn_c0_kernel, blocks, 256, 0, s, a);
   return 1;
 }
 

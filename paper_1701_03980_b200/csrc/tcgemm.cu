@@ -195,6 +195,7 @@ __device__ __forceinline__ void tmem_drain_add(uint32_t tmem, int lane_grp, int 
 template <bool kAMN, bool kBMN>
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_gemm_kernel(const GemmProblem* __restrict__ probs, int n_probs, int chunk) {
+  pdl_prologue();
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // ring: raw[s] = {A 16K, B 16K}, lo[b] = {A 16K, B 16K}
@@ -383,13 +384,15 @@ void launch_tc(const GemmLaunch& L, const GemmProblem* probs, cudaStream_t s) {
   cfg.blockDim = dim3(kTcThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = L.cluster > 0 ? L.cluster : 1;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaLaunchKernelEx(&cfg, kern, probs, L.n_probs, L.chunk > 0 ? L.chunk : 1 << 30);
 }
 

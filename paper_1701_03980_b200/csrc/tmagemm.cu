@@ -182,6 +182,7 @@ __device__ __noinline__ void epilogue_scalar(const TmaGemmArgs& P, float* part, 
 template <bool kAMN, bool kBMN, bool kConv, bool kAT = false>
 __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
     tma_gemm_kernel(const __grid_constant__ TmaGroup G) {
+  pdl_prologue();
   int pi = 0;
   while (pi + 1 < G.n && (int)blockIdx.x >= G.p[pi + 1].cta0) ++pi;
   const TmaProb& PR = G.p[pi];
@@ -543,6 +544,7 @@ struct SplitJob {
   int64_t ld, rows, cols, cols_p;
 };
 __global__ void split_lo_kernel(SplitJob j0, SplitJob j1, int n_jobs) {
+  pdl_prologue();
   const int64_t t0 = j0.rows * (j0.cols_p >> 2);
   const int64_t total = t0 + (n_jobs > 1 ? j1.rows * (j1.cols_p >> 2) : 0);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -746,13 +748,15 @@ static int tma_launch(const TmaGemmPlan* const* ps, int n, cudaStream_t s) {
   cfg.blockDim = dim3(p.conv ? kThreadsConv : kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = p.args.splits;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, k, G) == cudaSuccess ? 1 : -1;
 }
 
@@ -767,7 +771,7 @@ int launch_tma_gemm(const TmaGemmPlan& p, bool split_a, bool split_b, cudaStream
     if (nj) {
       int64_t tot = 0;
       for (int q = 0; q < nj; ++q) tot += jobs[q].rows * (jobs[q].cols_p / 4);
-      split_lo_kernel<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, s>>>(jobs[0], jobs[nj - 1], nj);
+      launch_k(split_lo_kernel, (int)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, s, jobs[0], jobs[nj - 1], nj);
       ++n;
     }
   }

@@ -27,6 +27,7 @@ VARIANTS = {
     "tma_presplit": {"DG_TMA_CONV": "0"},
     "tma_a_in_smem": {"DG_TMA_AT": "0"},
     "tma_ungrouped": {"DG_TMA_GROUP": "0"},
+    "pdl_off": {"DG_PDL": "0"},
     "tensor_cores_off": {"DG_TC": "0"},
     "schedule_cache_off": {"DG_SCHED_CACHE": "0"},
 }
