@@ -759,7 +759,7 @@ __device__ __forceinline__ void mma3(float* c, const float* a, float4 b) {
 // cluster through distributed shared memory.
 template <int BS>
 __global__ void __launch_bounds__(kClThreads, 1) rnn_fwd_cl_kernel(const __grid_constant__ RnnArgs a) {
-  pdl_prologue();
+  // (pdl_prologue after the weight staging below)
   extern __shared__ float4 smem4[];
   float* sm = reinterpret_cast<float*>(smem4);
   __shared__ StepPtrs sp[2];
@@ -828,6 +828,9 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_fwd_cl_kernel(const __grid_
       if (C.T > 2) mbar_arm(&h_full[1], bytes);  // h_1
     }
   }
+  // weights and tables above do not depend on the preceding grid (PDL):
+  // wait for it only now, so this staging overlaps its tail
+  pdl_prologue();
   __syncthreads();
   if (a.trace == 2 && tid == 0) trace(0, 253);
   if (warp < 8) {
@@ -998,7 +1001,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_fwd_cl_kernel(const __grid_
 // slots in rank order (deterministic).
 template <int BS>
 __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_constant__ RnnArgs a) {
-  pdl_prologue();
+  // (pdl_prologue after the weight staging below)
   extern __shared__ float4 smem4[];
   float* sm = reinterpret_cast<float*>(smem4);
   __shared__ StepPtrs2 sp[2];
@@ -1061,6 +1064,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
       if (C.T > 2) mbar_arm(&rec_full[1], slot_bytes);  // iteration 1
     }
   }
+  pdl_prologue();  // weight staging above overlaps the preceding grid
   __syncthreads();
   cluster_sync_all();
   if (a.trace && tid == 0) trace(1, 1);

@@ -182,7 +182,7 @@ __device__ __noinline__ void epilogue_scalar(const TmaGemmArgs& P, float* part, 
 template <bool kAMN, bool kBMN, bool kConv, bool kAT = false>
 __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
     tma_gemm_kernel(const __grid_constant__ TmaGroup G) {
-  pdl_prologue();
+  // (pdl_prologue after barrier init / TMEM allocation / descriptor prefetch)
   int pi = 0;
   while (pi + 1 < G.n && (int)blockIdx.x >= G.p[pi + 1].cta0) ++pi;
   const TmaProb& PR = G.p[pi];
@@ -250,6 +250,7 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
+  pdl_prologue();  // operands / C of the preceding grid are read only from here on
   const uint32_t tmem = tmem_sh;
   const uint32_t sbase = su32(smem);
 
