@@ -33,6 +33,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <unordered_map>
 
 #include "kernels.cuh"
 
@@ -585,7 +586,49 @@ EncodeFn encoder() {
 
 // rows x cols fp32 block, row stride ld floats; box {32, box_rows} (K-major:
 // 32 k x 128 rows, SWIZZLE_128B) or {32, 32} (MN-major, SWIZZLE_128B_ATOM_32B)
+struct MapKey {
+  const float* base;
+  int64_t ld, rows, cols;
+  bool mn;
+  bool operator==(const MapKey& o) const {
+    return base == o.base && ld == o.ld && rows == o.rows && cols == o.cols && mn == o.mn;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    uint64_t h = reinterpret_cast<uintptr_t>(k.base) * 0x9E3779B97F4A7C15ull;
+    h ^= (uint64_t)k.ld + 0x632BE59BD9B4E019ull + (h << 6) + (h >> 2);
+    h ^= (uint64_t)k.rows * 0xC2B2AE3D27D4EB4Full + (h << 6) + (h >> 2);
+    h ^= (uint64_t)k.cols * 0x165667B19E3779F9ull + (h << 6) + (h >> 2);
+    return (size_t)(h ^ (k.mn ? 0x27D4EB2F165667C5ull : 0));
+  }
+};
+
+bool make_map_uncached(CUtensorMap* m, const float* base, int64_t ld, int64_t rows, int64_t cols, bool mn);
+
+// Tensor maps are pure functions of (base, ld, rows, cols, layout); the
+// arenas are reused step after step, so the same blocks recur and the
+// driver-side encode (several us each) is done once per distinct block
 bool make_map(CUtensorMap* m, const float* base, int64_t ld, int64_t rows, int64_t cols, bool mn) {
+  static std::mutex mu;
+  static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+  const MapKey key{base, ld, rows, cols, mn};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *m = it->second;
+      return true;
+    }
+  }
+  if (!make_map_uncached(m, base, ld, rows, cols, mn)) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() >= 4096) cache.clear();
+  cache.emplace(key, *m);
+  return true;
+}
+
+bool make_map_uncached(CUtensorMap* m, const float* base, int64_t ld, int64_t rows, int64_t cols, bool mn) {
   EncodeFn enc = encoder();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
