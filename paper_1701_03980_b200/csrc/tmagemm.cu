@@ -58,6 +58,13 @@ constexpr int kChunk = 2;  // k-tiles per TMEM accumulation (K = 64)
 // 256 + 64 s .. +63), so the MMAs read only B from shared memory
 constexpr int kStagesAT = 4;
 constexpr int kSmemAT = kStagesAT * 3 * kOpBytes + 1024;
+// "lite" variant (split-free GEMMs with K <= kLiteMaxK): 2 stages, one TMEM
+// accumulator over the whole K drained once, 256 TMEM columns and ~97 KiB of
+// shared memory, so two CTAs share an SM and one's epilogue overlaps the
+// other's mainloop
+constexpr int kStagesLite = 2;
+constexpr int kSmemLite = kStagesLite * 3 * kOpBytes + 1024;
+constexpr int kLiteMaxK = 1024;
 
 // DG_TMA_DBG bit 10: CTA 0 records (before, after) clock64 of each role's
 // per-k-tile wait (diagnostics; tools/tma_bench)
@@ -180,8 +187,8 @@ __device__ __noinline__ void epilogue_scalar(const TmaGemmArgs& P, float* part, 
 // majors and split factor (problem i owns CTAs [cta0_i, cta0_{i+1})): the
 // small LSTM weight-gradient GEMMs of one backward share a wave instead of
 // each under-filling the device.
-template <bool kAMN, bool kBMN, bool kConv, bool kAT = false>
-__global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
+template <bool kAMN, bool kBMN, bool kConv, bool kAT = false, bool kLite = false>
+__global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, kLite ? 2 : 1)
     tma_gemm_kernel(const __grid_constant__ TmaGroup G) {
   // (pdl_prologue after barrier init / TMEM allocation / descriptor prefetch)
   int pi = 0;
@@ -195,10 +202,12 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   static_assert(!kAT || kConv, "A in TMEM needs the converter warps");
-  constexpr int NS = kAT ? kStagesAT : kConv ? kRawStagesC : kStages;  // raw operand stages
+  static_assert(!kLite || kAT, "the lite variant keeps A in TMEM");
+  constexpr int NS = kLite ? kStagesLite : kAT ? kStagesAT : kConv ? kRawStagesC : kStages;  // raw operand stages
   // stage stride: A_hi, B_hi, A_lo, B_lo (conv) / A_hi, A_lo, B_hi, B_lo / A, B, B_lo (A in TMEM)
   constexpr int SB = kAT ? 3 * kOpBytes : kStageBytes;
-  constexpr uint32_t kTmemCols = kAT ? 512 : 2 * BN;
+  constexpr uint32_t kTmemCols = kLite ? 256 : kAT ? 512 : 2 * BN;
+  constexpr uint32_t kAcol = kLite ? BN : 2 * BN;  // first TMEM column of A's per-stage hi/lo (A in TMEM)
   __shared__ uint64_t full[NS], empty[NS], conv[NS], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -296,14 +305,14 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
       constexpr uint32_t idesc = uidesc(kAMN && !kAT, kBMN);
       for (int j = 0; j < nkt; ++j) {
         const int s = j % NS, use = j / NS;
-        const int c = j / kChunk, a = c & 1;
-        if (j % kChunk == 0 && c >= 2) WAITP(1, j, &acc_empty[a], ((c >> 1) - 1) & 1);
+        const int c = kLite ? 0 : j / kChunk, a = c & 1;
+        if (!kLite && j % kChunk == 0 && c >= 2) WAITP(1, j, &acc_empty[a], ((c >> 1) - 1) & 1);
         if (kConv) WAITP(2, j, &conv[s], use & 1);
         else WAITP(2, j, &full[s], use & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         uint32_t ah, al, bh, bl;
         if (kAT) {
-          ah = tmem + 256u + 64u * (uint32_t)s;  // TMEM columns: hi, then lo at +32
+          ah = tmem + kAcol + 64u * (uint32_t)s;  // TMEM columns: hi, then lo at +32
           al = ah + 32u;
           bh = sbase + s * SB + kOpBytes;
           bl = bh + kOpBytes;
@@ -322,7 +331,7 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
 #pragma unroll
         for (int ks = 0; ks < BK / 8; ++ks) {
           const uint32_t oa = kAMN ? ks * 1024 : ks * 32, ob = kBMN ? ks * 1024 : ks * 32;
-          const uint32_t first = (j % kChunk == 0 && ks == 0) ? 0u : 1u;
+          const uint32_t first = ((kLite ? j == 0 : j % kChunk == 0) && ks == 0) ? 0u : 1u;
           if (P.pad_ & 1) continue;  // DG_TMA_DBG bit 0: no MMAs (pipeline timing only)
           if (kAT) {
             mma_tf32_ta(acc, ah + 8u * ks, udesc(bh + ob, kBMN), idesc, first);
@@ -340,7 +349,7 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
           continue;
         }
         mma_commit(&empty[s]);
-        if (j % kChunk == kChunk - 1 || j == nkt - 1) mma_commit(&acc_full[a]);
+        if ((!kLite && j % kChunk == kChunk - 1) || j == nkt - 1) mma_commit(&acc_full[a]);
       }
     }
   } else if (kAT && warp >= 6) {
@@ -383,7 +392,7 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
             lo[k] = __float_as_uint(x - __uint_as_float(hi[k]));
           }
         }
-        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 256u + 64u * (uint32_t)s;
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + kAcol + 64u * (uint32_t)s;
         tmem_st32(ta, hi);
         tmem_st32(ta + 32u, lo);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -421,6 +430,34 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, 1)
       if (!(P.pad_ & 128)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // bit 7: no fence
       __syncwarp();
       if (lane == 0) mbar_arrive(&conv[s]);
+    }
+  } else if (kLite) {
+    // epilogue warps 2..5: one drain of the whole-K accumulator, 32 columns at
+    // a time, straight into the staging tile (no register-resident row)
+    const int quad = warp & 3;
+    mbar_wait(&acc_full[0], 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    float* part = reinterpret_cast<float*>(smem);
+    const int lrow = quad * 32 + lane;
+#pragma unroll 1
+    for (int h = 0; h < BN / 32; ++h) {
+      uint32_t r[32];
+      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(h * 32);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+            "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+            "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+            "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int q = 0; q < 32; q += 4)
+        *reinterpret_cast<float4*>(part + lrow * BN + ((h * 32 + q + 4 * lrow) & (BN - 1))) =
+            make_float4(__uint_as_float(r[q]), __uint_as_float(r[q + 1]), __uint_as_float(r[q + 2]),
+                        __uint_as_float(r[q + 3]));
     }
   } else {
     // epilogue warps 2..5 -> TMEM lane quadrant warp % 4
@@ -646,6 +683,14 @@ int tma_prof_read(long long* out) {
   return cudaMemcpyFromSymbol(out, g_tprof, sizeof(g_tprof)) == cudaSuccess ? 0 : -1;  // [6][256][2]
 }
 
+bool tma_lite_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DG_TMA_LITE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool tma_at_enabled() {
   static const bool on = [] {
     const char* e = getenv("DG_TMA_AT");
@@ -739,6 +784,7 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
   if ((dbg >> 16) & 0xF) S = (dbg >> 16) & 0xF;
   a.splits = S;
   p.ctas = tiles * S;
+  p.lite = p.a_tmem && S == 1 && o.K <= kLiteMaxK && tma_lite_enabled();
   if (dbg & 0x100000)  // DG_TMA_DBG bit 20: log each planned GEMM
     fprintf(stderr, "[tma] M %d N %d K %d a_mn %d b_mn %d acc %d bias %d rows %d split %d ctas %d\n", o.M, o.N, o.K,
             (int)o.a_mn, (int)o.b_mn, o.accumulate, (int)(o.bias.base || o.bias.rows), (int)(o.C.rows != nullptr), S,
@@ -749,19 +795,21 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
 }
 
 static int tma_kernel_index(const TmaGemmPlan& p) {
-  return (p.a_tmem ? 8 : p.conv ? 4 : 0) + (p.a_mn ? 2 : 0) + (p.b_mn ? 1 : 0);
+  return (p.lite ? 12 : p.a_tmem ? 8 : p.conv ? 4 : 0) + (p.a_mn ? 2 : 0) + (p.b_mn ? 1 : 0);
 }
 
 using TmaKernel = void (*)(const TmaGroup);
 
 static TmaKernel tma_kernel(int ki) {
-  static const TmaKernel table[12] = {
+  static const TmaKernel table[16] = {
       tma_gemm_kernel<false, false, false>,      tma_gemm_kernel<false, true, false>,
       tma_gemm_kernel<true, false, false>,       tma_gemm_kernel<true, true, false>,
       tma_gemm_kernel<false, false, true>,       tma_gemm_kernel<false, true, true>,
       tma_gemm_kernel<true, false, true>,        tma_gemm_kernel<true, true, true>,
       tma_gemm_kernel<false, false, true, true>, tma_gemm_kernel<false, true, true, true>,
-      tma_gemm_kernel<true, false, true, true>,  tma_gemm_kernel<true, true, true, true>};
+      tma_gemm_kernel<true, false, true, true>,  tma_gemm_kernel<true, true, true, true>,
+      tma_gemm_kernel<false, false, true, true, true>, tma_gemm_kernel<false, true, true, true, true>,
+      tma_gemm_kernel<true, false, true, true, true>,  tma_gemm_kernel<true, true, true, true, true>};
   return table[ki];
 }
 
@@ -769,8 +817,8 @@ static int tma_launch(const TmaGemmPlan* const* ps, int n, cudaStream_t s) {
   const TmaGemmPlan& p = *ps[0];
   const int ki = tma_kernel_index(p);
   const TmaKernel k = tma_kernel(ki);
-  static bool attr[12] = {};
-  const int smem = p.a_tmem ? kSmemAT : p.conv ? kSmemConv : kSmem;
+  static bool attr[16] = {};
+  const int smem = p.lite ? kSmemLite : p.a_tmem ? kSmemAT : p.conv ? kSmemConv : kSmem;
   if (!attr[ki]) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
     attr[ki] = true;
@@ -825,7 +873,7 @@ int launch_tma_gemm(const TmaGemmPlan& p, bool split_a, bool split_b, cudaStream
 }
 
 bool tma_gemm_groupable(const TmaGemmPlan& a, const TmaGemmPlan& b) {
-  if (!a.conv || !b.conv || tma_kernel_index(a) != tma_kernel_index(b)) return false;
+  if (!a.conv || !b.conv || a.a_tmem != b.a_tmem || a.a_mn != b.a_mn || a.b_mn != b.b_mn) return false;
   if (a.args.C.rows || b.args.C.rows) return false;
   // output blocks must not overlap (problems of a group run concurrently)
   auto lo = [](const TmaGemmPlan& p) { return p.args.C.base; };
@@ -857,6 +905,7 @@ void tma_gemm_regroup(TmaGemmPlan* const* ps, int n) {
     TmaGemmArgs& a = ps[i]->args;
     a.splits = S;
     ps[i]->ctas = ((a.M + BM - 1) / BM) * a.tiles_n * S;
+    ps[i]->lite = ps[i]->a_tmem && S == 1 && a.K <= kLiteMaxK && tma_lite_enabled();
   }
 }
 

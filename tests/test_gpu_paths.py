@@ -28,6 +28,7 @@ VARIANTS = {
     "tma_a_in_smem": {"DG_TMA_AT": "0"},
     "tma_ungrouped": {"DG_TMA_GROUP": "0"},
     "pdl_off": {"DG_PDL": "0"},
+    "tma_lite_off": {"DG_TMA_LITE": "0"},
     "tensor_cores_off": {"DG_TC": "0"},
     "schedule_cache_off": {"DG_SCHED_CACHE": "0"},
 }

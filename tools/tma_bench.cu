@@ -153,6 +153,8 @@ int main(int argc, char** argv) {
     run("dX 2176x256x10000", 2176, 256, 10000, false, false, false, 20);
     run("dW 256x10000x2176", 256, 10000, 2176, true, true, false, 20);
     run("dW LSTM 512x1024x2240", 512, 1024, 2240, true, true, false, 20);
+    run("fwd 2752x10000x256", 2752, 10000, 256, false, true, false, 20);
+    run("Gx 2752x1024x256", 2752, 1024, 256, false, true, false, 20);
     return 0;
   }
   run("kmajor/kmajor", 256, 256, 96, false, false, true, 0);
@@ -167,5 +169,6 @@ int main(int argc, char** argv) {
   run("dX 2176x256x10000", 2176, 256, 10000, false, false, true, 20);
   run("dW 256x10000x2176", 256, 10000, 2176, true, true, true, 20);
   run("dW LSTM 512x1024x2240", 512, 1024, 2240, true, true, true, 20);
+  run("Gx 2752x1024x256", 2752, 1024, 256, false, true, true, 20);
   return 0;
 }
