@@ -332,7 +332,7 @@ struct TmaGemmPlan {
   bool a_mn, b_mn;
   bool conv;  // residuals formed in shared memory by converter warps (no lo copies)
   bool a_tmem;  // conv with A's hi/lo split stored in TMEM (MMAs read only B from shared memory)
-  bool lite;    // a_tmem, no split, K <= 1024: 2 stages, one accumulator, two CTAs per SM
+  bool lite;    // a_tmem, K per split <= 1280: 2 stages, one accumulator, two CTAs per SM
   const float* a_src;
   const float* b_src;
   float* a_lo;
@@ -344,7 +344,7 @@ struct TmaGemmPlan {
 bool tma_gemm_enabled();  // DG_TMA=0 disables (A/B checks)
 bool tma_conv_enabled();  // DG_TMA_CONV=0: pre-split residual copies instead of in-smem conversion
 bool tma_at_enabled();    // DG_TMA_AT=0: A's split in shared memory instead of TMEM
-bool tma_lite_enabled();  // DG_TMA_LITE=0: no two-CTA-per-SM variant for split-free short-K GEMMs
+bool tma_lite_enabled();  // DG_TMA_LITE=0: no two-CTA-per-SM variant for short-K (per split) GEMMs
 int64_t tma_lo_floats(int64_t rows, int64_t cols);
 bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out);
 // split_a / split_b: (re)compute the residual copies before the GEMM

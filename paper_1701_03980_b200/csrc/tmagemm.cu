@@ -58,13 +58,14 @@ constexpr int kChunk = 2;  // k-tiles per TMEM accumulation (K = 64)
 // 256 + 64 s .. +63), so the MMAs read only B from shared memory
 constexpr int kStagesAT = 4;
 constexpr int kSmemAT = kStagesAT * 3 * kOpBytes + 1024;
-// "lite" variant (split-free GEMMs with K <= kLiteMaxK): 2 stages, one TMEM
+// "lite" variant (K per split <= kLiteMaxK): 2 stages, one TMEM
 // accumulator over the whole K drained once, 256 TMEM columns and ~97 KiB of
 // shared memory, so two CTAs share an SM and one's epilogue overlaps the
 // other's mainloop
 constexpr int kStagesLite = 2;
 constexpr int kSmemLite = kStagesLite * 3 * kOpBytes + 1024;
 constexpr int kLiteMaxK = 1024;
+constexpr int kLiteMaxKSplit = 768;  // per split, when a cluster reduces the splits
 
 // DG_TMA_DBG bit 10: CTA 0 records (before, after) clock64 of each role's
 // per-k-tile wait (diagnostics; tools/tma_bench)
@@ -683,6 +684,17 @@ int tma_prof_read(long long* out) {
   return cudaMemcpyFromSymbol(out, g_tprof, sizeof(g_tprof)) == cudaSuccess ? 0 : -1;  // [6][256][2]
 }
 
+bool tma_lite_enabled();
+
+// whole-split accumulation in TMEM (no blocked drains) for short splits: the
+// error stays at a few 1e-6 relative, the size of the fp32 reference's own
+// summation error (tools/tma_bench.cu; long splits keep the blocked drains)
+static bool lite_ok(bool a_tmem, int K, int S) {
+  const int kt = (K + BK - 1) / BK;
+  const int per = ((kt + S - 1) / S) * BK;
+  return a_tmem && S <= 4 && per <= (S == 1 ? kLiteMaxK : kLiteMaxKSplit) && tma_lite_enabled();
+}
+
 bool tma_lite_enabled() {
   static const bool on = [] {
     const char* e = getenv("DG_TMA_LITE");
@@ -784,7 +796,7 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
   if ((dbg >> 16) & 0xF) S = (dbg >> 16) & 0xF;
   a.splits = S;
   p.ctas = tiles * S;
-  p.lite = p.a_tmem && S == 1 && o.K <= kLiteMaxK && tma_lite_enabled();
+  p.lite = lite_ok(p.a_tmem, o.K, S);
   if (dbg & 0x100000)  // DG_TMA_DBG bit 20: log each planned GEMM
     fprintf(stderr, "[tma] M %d N %d K %d a_mn %d b_mn %d acc %d bias %d rows %d split %d ctas %d\n", o.M, o.N, o.K,
             (int)o.a_mn, (int)o.b_mn, o.accumulate, (int)(o.bias.base || o.bias.rows), (int)(o.C.rows != nullptr), S,
@@ -905,7 +917,7 @@ void tma_gemm_regroup(TmaGemmPlan* const* ps, int n) {
     TmaGemmArgs& a = ps[i]->args;
     a.splits = S;
     ps[i]->ctas = ((a.M + BM - 1) / BM) * a.tiles_n * S;
-    ps[i]->lite = ps[i]->a_tmem && S == 1 && a.K <= kLiteMaxK && tma_lite_enabled();
+    ps[i]->lite = lite_ok(ps[i]->a_tmem, a.K, S);
   }
 }
 
