@@ -990,7 +990,29 @@ __global__ void update_dense_kernel(RuleArgs r, const TensorSeg* __restrict__ se
   const int64_t e0 = (int64_t)blk * kUpdChunk;
   const int64_t e1 = min(e0 + kUpdChunk, sg.n);
   float dummy0 = 0.f, dummy1 = 0.f;
-  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+  int64_t e_tail = e0;
+  const uintptr_t al = reinterpret_cast<uintptr_t>(sg.w) | reinterpret_cast<uintptr_t>(sg.g) |
+                       reinterpret_cast<uintptr_t>(sg.s0) | reinterpret_cast<uintptr_t>(sg.s1);
+  if ((al & 15) == 0 && (e0 & 3) == 0) {
+    // 16 B accesses: 4 parameters (w, g and the rule's state) per thread
+    const int64_t n4 = (e1 - e0) >> 2;
+    for (int64_t q = threadIdx.x; q < n4; q += blockDim.x) {
+      const int64_t e = e0 + 4 * q;
+      float4 w4 = *reinterpret_cast<const float4*>(sg.w + e), g4 = *reinterpret_cast<const float4*>(sg.g + e);
+      float4 a4 = sg.s0 ? *reinterpret_cast<const float4*>(sg.s0 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 b4 = sg.s1 ? *reinterpret_cast<const float4*>(sg.s1 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+      apply_rule(r, w4.x, g4.x, &a4.x, &b4.x);
+      apply_rule(r, w4.y, g4.y, &a4.y, &b4.y);
+      apply_rule(r, w4.z, g4.z, &a4.z, &b4.z);
+      apply_rule(r, w4.w, g4.w, &a4.w, &b4.w);
+      *reinterpret_cast<float4*>(sg.w + e) = w4;
+      *reinterpret_cast<float4*>(sg.g + e) = g4;
+      if (sg.s0) *reinterpret_cast<float4*>(sg.s0 + e) = a4;
+      if (sg.s1) *reinterpret_cast<float4*>(sg.s1 + e) = b4;
+    }
+    e_tail = e0 + 4 * n4;
+  }
+  for (int64_t e = e_tail + threadIdx.x; e < e1; e += blockDim.x) {
     float w = sg.w[e], g = sg.g[e];
     float* p0 = sg.s0 ? sg.s0 + e : &dummy0;
     float* p1 = sg.s1 ? sg.s1 + e : &dummy1;

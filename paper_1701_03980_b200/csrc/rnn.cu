@@ -1106,7 +1106,6 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
       }
       if (lane == kRnnSlots) nb1 = C.b1[t - 1];
     }
-    if (a.trace == 2 && tid == 0 && it < 47) trace(1, 64 + 4 * it);
     const bool cb1 = (P.b1 & 4) != 0;
     float gh = 0.f, d_tc = 0.f, d_o = 0.f, dc = 0.f, d_i = 0.f, d_g = 0.f, dpi = 0.f, dpo = 0.f, dpg = 0.f;
     float d_f = 0.f, dpf = 0.f;
@@ -1173,7 +1172,6 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
                         make_float2(ac[0][2] + ac[1][2] + ac[2][2], ac[0][3] + ac[1][3] + ac[2][3]), rb);
         }
       }
-      if (a.trace == 2 && tid == 0 && it < 47) trace(1, 64 + 4 * it + 1);
       if (warp == 1) {
         if (lane < kRnnSlots) {
           sp[(t - 1) & 1].v[lane] = nv;
@@ -1206,23 +1204,14 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
       D[S_PF][r] = dpf;
       if (t == 0 && !cb1) D[S_CP][r] += dc_carry;
     }
-    if (a.trace == 2 && tid == 0 && it < 47) trace(1, 64 + 4 * it + 2);
     if (t > 0) {
       load_cell(sp[(t - 1) & 1]);
       mbar_wait_cl(&rec_full[it & 1], (it >> 1) & 1);
-      if (a.trace == 2 && tid == 0 && it < 47) trace(1, 64 + 4 * it + 3);
       if (tid == 0 && it + 2 <= C.T - 2) mbar_arm(&rec_full[it & 1], slot_bytes);
       rec = 0.f;
       if (cb < BS) {
-        // the n_u partials: all loads first, then the adds in rank order
         const float* slot = recv + (size_t)(it & 1) * C.n_u * BS * kU + (size_t)cb * kU + cj;
-        float pv[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) pv[q] = q < C.n_u ? slot[(size_t)q * BS * kU] : 0.f;
-#pragma unroll
-        for (int q = 0; q < 16; ++q)
-          if (q < C.n_u) rec += pv[q];
-        for (int q = 16; q < C.n_u; ++q) rec += slot[(size_t)q * BS * kU];
+        for (int q = 0; q < C.n_u; ++q) rec += slot[(size_t)q * BS * kU];
       }
     }
   }

@@ -64,11 +64,3 @@ if os.environ.get("DG_RNN_TRACE") == "2":
           "| +cluster sync", np.round(np.median(ph[:, 3]) / 1e3, 2), "| CTA start skew max",
           np.round(ph[:, 4].max() / 1e3, 2))
 
-if os.environ.get("DG_RNN_TRACE") == "2":
-    b = buf[1, 0].astype(np.int64)
-    n = min(T, 47) - 1
-    ph = b[64:64 + 4 * n].reshape(-1, 4)
-    nxt = b[64 + 4:64 + 4 * (n + 1):4][:n]
-    d = np.stack([ph[:, 1] - ph[:, 0], ph[:, 2] - ph[:, 1], ph[:, 3] - ph[:, 2], nxt - ph[:, 3]], axis=1)
-    print("bwd CTA0 per-step phases (us): cell+MMA+push, barrier+stores, load+wait partials, sum+top ->",
-          np.round(np.median(d[:-1], axis=0) / 1e3, 2))
