@@ -2940,6 +2940,19 @@ int dg_backward(dg_graph* g, int32_t loss) {
       if (ok)
         for (int x : xs) overwrite[x] = 1;
     }
+    // the persistent recurrence backward (rnn.cu) stores every element of the
+    // chain-internal gradient slots (gate affine, picks, activations, both
+    // products, tanh(c)); only c_t and h_t can carry outside contributions
+    for (const Group& gr : S.groups) {
+      if (gr.kind != -3) continue;
+      for (int u : gr.units)
+        for (const RnnChainPlan& cp : S.rnns[S.units[u].rnn].chains)
+          for (size_t t = 0; t < cp.G.size(); ++t) {
+            overwrite[cp.G[t]] = 1;
+            const std::vector<int>& cn = cp.cells[t].nodes;
+            for (int k : {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 11}) overwrite[cn[k]] = 1;
+          }
+    }
   }
   // placement of grad slots: group order for scheduled units, then the rest
   const size_t begin = g->bwd_cursor;
@@ -2959,6 +2972,11 @@ int dg_backward(dg_graph* g, int32_t loss) {
   for (int i = 0; i <= loss; ++i)
     if (!overwrite[i]) place(i);
   const size_t zero_end = cur;
+  // overwritten slots: same group / unit order (slot-major recurrence blocks
+  // stay dense GEMM operands), then the rest
+  for (const Group& gr : S.groups)
+    for (int u : gr.units)
+      for (int i : S.units[u].nodes) place(i);
   for (int i = 0; i <= loss; ++i) place(i);
   // parameter nodes accumulate straight into the parameter's gradient (the
   // default sink adds the slot to p.gradient, graph.py:54-55)
