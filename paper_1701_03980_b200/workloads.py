@@ -195,15 +195,29 @@ class RNNLM:
         cols = padded.T.tolist()
         masks = (np.arange(1, t_max)[:, None] < lens[None, :]).astype(cg.dtype)
         mask_shape = dy.Shape((1,), nb)
-        state = self.rnn.initial_state(cg)
+        rnn = self.rnn
+        state = rnn.initial_state(cg)
+        lookup_batch, affine, pnls_batch = ops.lookup_batch, ops.affine, ops.pickneglogsoftmax_batch
+        cmult, inp, sum_batches, add, Tensor, E = ops.cmult, ops.input, ops.sum_batches, ops.add, dy.Tensor, self.E
+        # LSTM steps through the native graph core (the nodes add_input makes,
+        # in the same order; the layer parameters appear at the first step)
+        core = getattr(cg, "_core", None)
+        native = core is not None and rnn.cell == "lstm" and type(state.hs) is list and type(state.cs) is list
+        hs, cs, pex, H = state.hs, state.cs, None, rnn.hidden_dim
         loss = None
         for t in range(t_max - 1):
-            xs, labels = cols[t], cols[t + 1]
-            state = state.add_input(ops.lookup_batch(cg, self.E, xs))
-            nll = ops.pickneglogsoftmax_batch(ops.affine(be, we, state.output()), labels)
-            masked = ops.cmult(nll, ops.input(cg, dy.Tensor(mask_shape, masks[t])))
-            step = ops.sum_batches(masked)
-            loss = step if loss is None else ops.add(loss, step)
+            x = lookup_batch(cg, E, cols[t])
+            if native:
+                if pex is None:
+                    pex = rnn._graph_params(cg)
+                hs, cs = core.lstm_step(pex, hs, cs, x, H)
+                h = hs[-1]
+            else:
+                state = state.add_input(x)
+                h = state.output()
+            nll = pnls_batch(affine(be, we, h), cols[t + 1])
+            step = sum_batches(cmult(nll, inp(cg, Tensor(mask_shape, masks[t]))))
+            loss = step if loss is None else add(loss, step)
         return loss
 
     def loss(self, cg, batch):
