@@ -202,8 +202,9 @@ class RNNLM:
         # LSTM steps through the native graph core (the nodes add_input makes,
         # in the same order; the layer parameters appear at the first step)
         core = getattr(cg, "_core", None)
-        native = core is not None and rnn.cell == "lstm" and type(state.hs) is list and type(state.cs) is list
-        hs, cs, pex, H = state.hs, state.cs, None, rnn.hidden_dim
+        native = (core is not None and getattr(rnn, "cell", None) == "lstm" and type(getattr(state, "hs", None)) is list
+                  and type(getattr(state, "cs", None)) is list)
+        hs, cs, pex, H = (state.hs, state.cs, None, rnn.hidden_dim) if native else (None, None, None, None)
         loss = None
         for t in range(t_max - 1):
             x = lookup_batch(cg, E, cols[t])
