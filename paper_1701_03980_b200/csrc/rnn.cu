@@ -646,19 +646,8 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
-__device__ __forceinline__ void st_cluster(uint32_t addr, float v) {
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
-}
-__device__ __forceinline__ void st_cluster4(uint32_t addr, float4 v) {
-  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z),
-               "f"(v.w)
-               : "memory");
-}
 __device__ __forceinline__ void mbar_init_cl(uint64_t* b, uint32_t n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(n));
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t remote_bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cl(uint64_t* b, uint32_t parity) {
   const uint32_t a = smem_addr(b);
@@ -696,33 +685,8 @@ __device__ __forceinline__ void st_async_v2(uint32_t remote_addr, float2 v, uint
 __device__ __forceinline__ void mbar_arm(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void cluster_arrive() {
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// compute warps hand completed steps to the signalling warp through a
-// shared-memory step counter (release / acquire at CTA scope)
-__device__ __forceinline__ void st_release_cta(int* p, int v) {
-  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ int ld_acquire_cta(const int* p) {
-  int v;
-  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
-  return v;
-}
-__device__ __forceinline__ void signal_loop(int* done, int* flags, int T, bool reverse) {
-  // publish step counters in order as the compute warps complete steps
-  for (int i = 0; i < T; ++i) {
-    unsigned spins = 0;
-    while (ld_acquire_cta(done) < i + 1) {
-      __nanosleep(64);
-      if (++spins > (1u << 24)) __trap();
-    }
-    arrive(flags + (reverse ? T - 1 - i : i));
-  }
 }
 
 // 3xTF32 legacy-MMA tile op: acc(16 x 8) += A(16 x 8) B(8 x 8); a/b hold fp32
@@ -737,19 +701,6 @@ __device__ __forceinline__ void mma_1688(float* c, const uint32_t* a, uint32_t b
       "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ void mma3(float* c, const float* a, float4 b) {
-  // b = {b0_hi, b1_hi, b0_lo, b1_lo} (pre-split weights)
-  uint32_t ah[4], al[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    ah[q] = tf32_hi(a[q]);
-    al[q] = tf32_lo(a[q]);
-  }
-  const uint32_t bh0 = __float_as_uint(b.x), bh1 = __float_as_uint(b.y);
-  mma_1688(c, al, bh0, bh1);
-  mma_1688(c, ah, __float_as_uint(b.z), __float_as_uint(b.w));
-  mma_1688(c, ah, bh0, bh1);
 }
 
 // Forward recurrence (gx mode: G slots hold b + Wx x_t): per step the CTA
