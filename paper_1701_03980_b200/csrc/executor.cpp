@@ -3104,19 +3104,39 @@ int dg_backward(dg_graph* g, int32_t loss) {
   std::vector<int64_t> bkeys;
   for (auto& kv : buse) bkeys.push_back(kv.first);
   std::sort(bkeys.begin(), bkeys.end());
-  for (int64_t h : bkeys) {
-    auto& rows = buse[h];
-    Param* p = param_at(h);
-    const size_t orow = B.push(rows);
-    float* dst = p->grad;
-    const int width = (int)p->size();
-    const int nr = (int)rows.size();
+  // bias gradients: up to kColsumGroup column sums per pair of launches
+  {
     float* work = reinterpret_cast<float*>(scratch_base(g));
     const int64_t wcap = (int64_t)(scratch_bytes(g) / 4);
-    plan.ops.push_back([dst, orow, nr, width, work, wcap, st](char* d) {
-      return launch_colsum_rows(dst, at<const float* const>(d, orow), nr, width, work, wcap, st);
-    });
-    plan.tag(C_COLSUM, 0.0, 4.0 * nr * width + 8.0 * width);
+    struct Job {
+      float* dst;
+      size_t orow;
+      int nr, width;
+    };
+    std::vector<Job> jobs;
+    double bytes = 0;
+    auto flush_jobs = [&] {
+      if (jobs.empty()) return;
+      plan.ops.push_back([jobs, work, wcap, st](char* d) {
+        ColsumGroup G{};
+        G.n = (int)jobs.size();
+        for (int q = 0; q < G.n; ++q)
+          G.j[q] = ColsumJob{jobs[q].dst, at<const float* const>(d, jobs[q].orow), jobs[q].nr, jobs[q].width, 0, 0, 0,
+                             nullptr};
+        return launch_colsum_group(G, work, wcap, st);
+      });
+      plan.tag(C_COLSUM, 0.0, bytes);
+      jobs.clear();
+      bytes = 0;
+    };
+    for (int64_t h : bkeys) {
+      auto& rows = buse[h];
+      Param* p = param_at(h);
+      jobs.push_back({p->grad, B.push(rows), (int)rows.size(), (int)p->size()});
+      bytes += 4.0 * rows.size() * p->size() + 8.0 * p->size();
+      if ((int)jobs.size() == kColsumGroup) flush_jobs();
+    }
+    flush_jobs();
   }
   tm.lap("colsum");
   // lookup flush: sorted segmented scatter-add per table (graph.py:57-63)

@@ -907,6 +907,65 @@ __global__ void colsum_final_kernel(float* dst, const float* work, int width, in
   }
 }
 
+// the bias gradients of one backward (several widths / row sets) in one pair
+// of launches: job q owns partial blocks [pb0, pb0 + xb*chunks) and final
+// blocks [fb0, fb0 + ceil(width/32)); same arithmetic as the kernels above
+__global__ void colsum_partial_group_kernel(const __grid_constant__ ColsumGroup G) {
+  pdl_prologue();
+  int q = 0;
+  while (q + 1 < G.n && (int)blockIdx.x >= G.j[q + 1].pb0) ++q;
+  const ColsumJob& J = G.j[q];
+  const int lb = (int)blockIdx.x - J.pb0;
+  const int xb = (J.width + 255) / 256;
+  const int ch = lb / xb, c = (lb - ch * xb) * 256 + threadIdx.x;
+  if (c >= J.width) return;
+  const int r0 = (int)((int64_t)J.n_rows * ch / J.chunks), r1 = (int)((int64_t)J.n_rows * (ch + 1) / J.chunks);
+  float s = 0.f;
+  int r = r0;
+  for (; r + 8 <= r1; r += 8) {
+    const float* p[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) p[k] = J.rows[r + k];
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = p[k][c];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += v[k];
+  }
+  for (; r < r1; ++r) s += J.rows[r][c];
+  J.work[(int64_t)ch * J.width + c] = s;
+}
+
+__global__ void colsum_final_group_kernel(const __grid_constant__ ColsumGroup G) {
+  pdl_prologue();
+  int q = 0;
+  while (q + 1 < G.n && (int)blockIdx.x >= G.j[q + 1].fb0) ++q;
+  const ColsumJob& J = G.j[q];
+  __shared__ float part[8][33];
+  const int c = ((int)blockIdx.x - J.fb0) * 32 + (threadIdx.x & 31), y = threadIdx.x >> 5;
+  float s = 0.f;
+  if (c < J.width) {
+    int ch = y;
+    for (; ch + 24 < J.chunks; ch += 32) {
+      const float a0 = J.work[(int64_t)ch * J.width + c], a1 = J.work[(int64_t)(ch + 8) * J.width + c];
+      const float a2 = J.work[(int64_t)(ch + 16) * J.width + c], a3 = J.work[(int64_t)(ch + 24) * J.width + c];
+      s += a0;
+      s += a1;
+      s += a2;
+      s += a3;
+    }
+    for (; ch < J.chunks; ch += 8) s += J.work[(int64_t)ch * J.width + c];
+  }
+  part[y][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (y == 0 && c < J.width) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += part[k][threadIdx.x];
+    J.dst[c] += t;
+  }
+}
+
 __global__ void row_reduce_scatter_kernel(float* const* dst_rows, const int* seg, const float* src, int n_targets,
                                           int width) {
   pdl_prologue();
@@ -1196,6 +1255,33 @@ int launch_affine_generic_bwd(const AffineGenericArgs& a, cudaStream_t s) {
     launches += 2;
   }
   return launches;
+}
+
+int launch_colsum_group(ColsumGroup G, float* work, int64_t work_floats, cudaStream_t s) {
+  if (G.n <= 0) return 0;
+  // chunking per job as launch_colsum_rows, partials packed into the scratch
+  int pb = 0, fb = 0;
+  int64_t off = 0;
+  for (int q = 0; q < G.n; ++q) {
+    ColsumJob& J = G.j[q];
+    const int xb = (J.width + 255) / 256;
+    int chunks = (2 * 148 * 8 + xb - 1) / xb;
+    chunks = std::min(chunks, std::max(1, J.n_rows / 8));
+    const int64_t left = work_floats - off;
+    chunks = (int)std::min<int64_t>(chunks, std::max<int64_t>(1, left / std::max(1, J.width)));
+    chunks = std::min(chunks, 1024);
+    if ((int64_t)chunks * J.width > left) return -1;
+    J.chunks = chunks;
+    J.work = work + off;
+    off += ((int64_t)chunks * J.width + 63) & ~int64_t(63);
+    J.pb0 = pb;
+    J.fb0 = fb;
+    pb += xb * chunks;
+    fb += (J.width + 31) / 32;
+  }
+  launch_k(colsum_partial_group_kernel, pb, 256, 0, s, G);
+  launch_k(colsum_final_group_kernel, fb, 256, 0, s, G);
+  return 2;
 }
 
 int launch_colsum_rows(float* dst, const float* const* rows, int n_rows, int width, float* work, int64_t work_floats,

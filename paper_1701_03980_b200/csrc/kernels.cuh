@@ -246,6 +246,20 @@ int launch_affine_generic_bwd(const AffineGenericArgs& a, cudaStream_t s);
 // column sums over gathered rows: dst[c] += sum_r rows[r][c]  (deterministic)
 int launch_colsum_rows(float* dst, const float* const* rows, int n_rows, int width, float* work,
                        int64_t work_floats, cudaStream_t s);
+// several column sums (the bias gradients of one backward) in one pair of launches
+struct ColsumJob {
+  float* dst;
+  const float* const* rows;
+  int n_rows, width;
+  int chunks, pb0, fb0;  // filled by launch_colsum_group
+  float* work;
+};
+constexpr int kColsumGroup = 8;
+struct ColsumGroup {
+  ColsumJob j[kColsumGroup];
+  int n;
+};
+int launch_colsum_group(ColsumGroup G, float* work, int64_t work_floats, cudaStream_t s);
 // row reduce-scatter: for t in targets: dst[t] += sum_{k in seg} src[k]  (src dense, width)
 int launch_row_reduce_scatter(float* const* dst_rows, const int* seg, const float* src, int n_targets,
                               int width, cudaStream_t s);
