@@ -1356,6 +1356,14 @@ static void flush_gemm(dg_graph* g, Plan& plan, GemmBatch& gb) {
   // other wide problems run on the cp.async tensor-core kernel (tcgen05
   // 3xTF32), the rest on the grouped SIMT kernel
   const bool tc = tc_gemm_eligible(rest);
+  static const bool log_rest = [] {
+    const char* e = std::getenv("DG_GEMM_LOG");
+    return e && e[0] == '1';
+  }();
+  if (log_rest)
+    for (const GemmProblem& p : rest)
+      std::fprintf(stderr, "[gemm-rest] cls %d M %d N %d K %lld segs %d tc %d\n", gb.cls, (int)p.M, (int)p.N,
+                   (long long)(p.n_seg ? p.seg[0].K : 0), (int)p.n_seg, (int)tc);
   GemmLaunch L = tc ? tc_gemm_plan(rest, gb.a_kmajor, gb.b_nmajor)
                     : gemm_plan(rest, gb.a_kmajor, gb.b_nmajor, cap, kCounterCap);
   const size_t off = plan.blob.push(rest);
