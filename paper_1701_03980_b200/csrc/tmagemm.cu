@@ -52,7 +52,7 @@ constexpr int kSmem = kStages * kStageBytes + 1024;
 // conversion variant: 5 raw stages (A_hi, B_hi) + 2 residual buffers (A_lo, B_lo)
 constexpr int kRawStagesC = 3;
 constexpr int kSmemConv = kRawStagesC * 4 * kOpBytes + 1024;
-constexpr int kChunk = 2;  // k-tiles per TMEM accumulation (K = 64)
+constexpr int kChunk = 4;  // k-tiles per TMEM accumulation (K = 128)
 // A-in-TMEM variant: stages of A_raw | B_raw | B_lo (48 KiB) in shared memory;
 // the converter warps write A's hi/lo split straight into TMEM (columns
 // 256 + 64 s .. +63), so the MMAs read only B from shared memory
