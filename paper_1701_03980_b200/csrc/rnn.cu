@@ -843,7 +843,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_fwd_cl_kernel(const __grid_
 #pragma unroll
       for (int z = 0; z < 6; ++z) ac[z][0] = ac[z][1] = ac[z][2] = ac[z][3] = 0.f;
       const float4* bw = Bf + warp * 32 + lane;
-#pragma unroll 2
+#pragma unroll 4
       for (int q = 0; q < KS; ++q) {
         const int k = 8 * q + t4;
         float av[4];
