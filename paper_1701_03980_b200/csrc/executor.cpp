@@ -96,26 +96,41 @@ static void touched_clear(Param& p) {
 // ------------------------------------------------------------------ staging
 // One table blob per forward/backward call: built on the host, copied with a
 // single H2D into the head of the workspace; kernels read it from there.
+struct Pinned {
+  void* ptr = nullptr;
+  size_t cap = 0;
+  cudaEvent_t ev = nullptr;
+  bool pending = false;
+};
+
+// Written straight into a pinned staging slot when one is attached (no host
+// copy before the H2D); a plan that outgrows the slot moves to a vector.
 struct Blob {
-  std::vector<uint8_t> host;
-  size_t push_bytes(const void* p, size_t n, size_t align = 16) {
-    size_t off = (host.size() + align - 1) & ~(align - 1);
-    host.resize(off + n);
-    if (n) std::memcpy(host.data() + off, p, n);
+  std::vector<uint8_t> vec;
+  uint8_t* ext = nullptr;
+  size_t ext_cap = 0;
+  Pinned* slot = nullptr;
+  size_t n = 0;
+  uint8_t* data() { return ext ? ext : vec.data(); }
+  const uint8_t* data() const { return ext ? ext : vec.data(); }
+  size_t size() const { return n; }
+  bool empty() const { return n == 0; }
+  size_t push_bytes(const void* p, size_t bytes, size_t align = 16) {
+    const size_t off = (n + align - 1) & ~(align - 1);
+    if (ext && off + bytes > ext_cap) {  // spill
+      vec.assign(ext, ext + n);
+      ext = nullptr;
+      slot = nullptr;
+    }
+    if (!ext && vec.size() < off + bytes) vec.resize(std::max(off + bytes, 2 * vec.size()));
+    if (bytes) std::memcpy(data() + off, p, bytes);
+    n = off + bytes;
     return off;
   }
   template <class T>
   size_t push(const std::vector<T>& v) {
     return push_bytes(v.data(), v.size() * sizeof(T));
   }
-  void clear() { host.clear(); }
-};
-
-struct Pinned {
-  void* ptr = nullptr;
-  size_t cap = 0;
-  cudaEvent_t ev = nullptr;
-  bool pending = false;
 };
 
 // -------------------------------------------------------------------- graph
@@ -302,16 +317,30 @@ static Pinned& staging_slot() {
   return p;
 }
 
-static int upload(dg_graph* g, const Blob& blob, void* dst) {
-  if (blob.host.empty()) return DG_OK;
+// plans build their table blob in place in the next staging slot
+static int blob_attach(Blob& b, size_t hint) {
   Pinned& p = staging_slot();
-  int rc = pinned_acquire(p, blob.host.size());
+  int rc = pinned_acquire(p, std::max<size_t>(hint, 1));
   if (rc) return rc;
-  std::memcpy(p.ptr, blob.host.data(), blob.host.size());
-  DG_CUDA_TRY(cudaMemcpyAsync(dst, p.ptr, blob.host.size(), cudaMemcpyHostToDevice, g->stream));
-  g->h2d_bytes += (int64_t)blob.host.size();
-  DG_CUDA_TRY(cudaEventRecord(p.ev, g->stream));
-  p.pending = true;
+  b.ext = static_cast<uint8_t*>(p.ptr);
+  b.ext_cap = p.cap;
+  b.slot = &p;
+  return DG_OK;
+}
+
+static int upload(dg_graph* g, const Blob& blob, void* dst) {
+  if (blob.empty()) return DG_OK;
+  Pinned* p = blob.slot;
+  if (!blob.ext) {  // spilled (or never attached): through a staging slot
+    p = &staging_slot();
+    int rc = pinned_acquire(*p, blob.size());
+    if (rc) return rc;
+    std::memcpy(p->ptr, blob.data(), blob.size());
+  }
+  DG_CUDA_TRY(cudaMemcpyAsync(dst, p->ptr, blob.size(), cudaMemcpyHostToDevice, g->stream));
+  g->h2d_bytes += (int64_t)blob.size();
+  DG_CUDA_TRY(cudaEventRecord(p->ev, g->stream));
+  p->pending = true;
   return DG_OK;
 }
 
@@ -1231,8 +1260,8 @@ static bool regularize(dg_graph* g, const Plan& plan, Operand& op, int64_t n_row
   if (!op.rows) return op.base && (reinterpret_cast<uintptr_t>(op.base) & 15) == 0 && op.ld % 4 == 0 &&
                        op.ld >= row_len;
   const char* dev = reinterpret_cast<const char*>(op.rows);
-  if (dev < g->work_base || dev >= g->work_base + plan.blob.host.size()) return false;
-  const uintptr_t* r = reinterpret_cast<const uintptr_t*>(plan.blob.host.data() + (dev - g->work_base));
+  if (dev < g->work_base || dev >= g->work_base + plan.blob.size()) return false;
+  const uintptr_t* r = reinterpret_cast<const uintptr_t*>(plan.blob.data() + (dev - g->work_base));
   if (n_rows < 1 || (r[0] & 15)) return false;
   const int64_t step = n_rows > 1 ? (int64_t)(r[1] - r[0]) : (int64_t)row_len * 4;
   if (step <= 0 || step % 16 || step / 4 < row_len) return false;
@@ -1588,7 +1617,7 @@ static bool dry_run() {
 }
 
 static int launch_plan(dg_graph* g, Plan& plan) {
-  const size_t blob_bytes = (plan.blob.host.size() + 255) & ~size_t(255);
+  const size_t blob_bytes = (plan.blob.size() + 255) & ~size_t(255);
   if (blob_bytes > blob_cap(g)) return fail(DG_CONFIG, "plan tables exceed the workspace");
   if (dry_run()) return DG_OK;
   if (!g->counters_ready) {
@@ -2329,7 +2358,10 @@ static int do_forward(dg_graph* g, int upto) {
       for (int i : S.units[u].nodes) place(i);
 
   Plan plan;
-  plan.blob.host.reserve(g->blob_hint[0]);  // no regrowth copies while planning
+  {
+    const int rc0 = blob_attach(plan.blob, g->blob_hint[0]);  // no regrowth copies while planning
+    if (rc0) return rc0;
+  }
   Blob& B = plan.blob;
   // input payloads: laid out in the blob exactly like the arena block
   size_t in_blob = 0;
@@ -2387,7 +2419,7 @@ static int do_forward(dg_graph* g, int upto) {
     flush_gemm(g, plan, gb);
   }
   tm.lap("groups");
-  g->blob_hint[0] = std::max(g->blob_hint[0], plan.blob.host.size() + plan.blob.host.size() / 4);
+  g->blob_hint[0] = std::max(g->blob_hint[0], plan.blob.size() + plan.blob.size() / 4);
   int rc = launch_plan(g, plan);
   if (rc) return rc;
   tm.lap("launch");
@@ -2992,7 +3024,10 @@ int dg_backward(dg_graph* g, int32_t loss) {
     if (g->nodes[i].kind == DG_OP_PARAMETER) g->nodes[i].grad = param_at(g->aux_i[g->nodes[i].ai_off])->grad;
 
   Plan plan;
-  plan.blob.host.reserve(g->blob_hint[1]);  // no regrowth copies while planning
+  {
+    const int rc1 = blob_attach(plan.blob, g->blob_hint[1]);  // no regrowth copies while planning
+    if (rc1) return rc1;
+  }
   Blob& B = plan.blob;
   cudaStream_t st = g->stream;
   // zero the fresh slots (arena contract, graph.py:146-148) and seed dloss = 1
@@ -3208,7 +3243,7 @@ int dg_backward(dg_graph* g, int32_t loss) {
     }
   }
   tm.lap("scatter");
-  g->blob_hint[1] = std::max(g->blob_hint[1], plan.blob.host.size() + plan.blob.host.size() / 4);
+  g->blob_hint[1] = std::max(g->blob_hint[1], plan.blob.size() + plan.blob.size() / 4);
   rc = launch_plan(g, plan);
   if (rc) return rc;
   tm.lap("launch");
