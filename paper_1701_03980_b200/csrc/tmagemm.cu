@@ -740,7 +740,11 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
   a.C = o.C;
   a.bias = o.bias;
   a.accumulate = o.accumulate;
-  a.c_vec = !o.C.rows && (reinterpret_cast<uintptr_t>(o.C.base) % 16 == 0) && o.C.ld % 4 == 0 &&
+  // 16 B epilogue accesses: a dense C aligned with ld % 4 == 0, or a row table
+  // whose rows are arena / parameter slots (64 B aligned, rows of N floats
+  // apart) with N % 4 == 0
+  a.c_vec = (o.C.rows ? o.N % 4 == 0
+                      : (reinterpret_cast<uintptr_t>(o.C.base) % 16 == 0) && o.C.ld % 4 == 0) &&
             (!o.bias.base || o.bias.rows || (reinterpret_cast<uintptr_t>(o.bias.base) % 16 == 0 && o.bias.ld % 4 == 0));
   // operand blocks: A is (M rows x K) or (K rows x M); B is (N x K) or (K x N)
   const int64_t ar = o.a_mn ? o.K : o.M, ac = o.a_mn ? o.M : o.K;
