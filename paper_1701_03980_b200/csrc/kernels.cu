@@ -442,8 +442,18 @@ __global__ void sum_batches_fwd_kernel(SumBatchesArgs a) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int j = static_cast<int>(t / a.elem);
     const int e = static_cast<int>(t - (int64_t)j * a.elem);
+    // 16 loads in flight, added in batch order
+    const float* src = a.in[j] + e;
     float s = 0.f;
-    for (int b = 0; b < a.batch; ++b) s += a.in[j][(int64_t)b * a.elem + e];
+    int b = 0;
+    for (; b + 16 <= a.batch; b += 16) {
+      float v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = src[(int64_t)(b + q) * a.elem];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) s += v[q];
+    }
+    for (; b < a.batch; ++b) s += src[(int64_t)b * a.elem];
     a.out[j][e] = s;
   }
 }
