@@ -51,8 +51,33 @@ CONFIGS = {
 METRIC = "train words/sec (RNNLM, BiLSTM tagger), sents/sec (Tree-LSTM); 1/8 B200"
 
 
+_WL = None
+
+
+def workloads():
+    """paper_1701_03980_b200/workloads.py loaded by path: pure numpy corpus
+    generators + graph builders generic over the engine namespace, so the
+    reference arm never imports the product package (or maps its .so)."""
+    global _WL
+    if _WL is None:
+        import importlib.util
+
+        spec = importlib.util.spec_from_file_location(
+            "dg_bench_workloads", os.path.join(ROOT, "paper_1701_03980_b200", "workloads.py"))
+        _WL = importlib.util.module_from_spec(spec)
+        sys.modules[spec.name] = _WL
+        spec.loader.exec_module(_WL)
+    return _WL
+
+
+def bench_config(name, cfg, world):
+    """The `config` object of the JSON line (identical for both arms)."""
+    return {"workload": name, **cfg, "global_batch": cfg["mb"] * world, "parallelism": f"dp{world}",
+            "l2": "flushed between timed steps (256 MiB write)"}
+
+
 def make_task(dy, model, cfg, tagger_data=None):
-    from paper_1701_03980_b200 import workloads as W
+    W = workloads()
 
     if cfg["kind"] == "rnnlm":
         return W.RNNLM(dy, model, cfg["vocab"], cfg["embed"], cfg["hidden"], cfg["layers"])
@@ -63,7 +88,7 @@ def make_task(dy, model, cfg, tagger_data=None):
 
 def make_data(cfg, n_steps, rank, world, seed=1):
     """Per-rank minibatches: rank r takes batches r, r+R, ... of one corpus."""
-    from paper_1701_03980_b200 import workloads as W
+    W = workloads()
 
     total = n_steps * world
     if cfg["kind"] == "rnnlm":
@@ -147,7 +172,17 @@ class Clocks:
 # ---------------------------------------------------------------------------
 
 
-def cpu_throughput(cfg, budget_s: float, seed=1):
+def cpu_threads(n):
+    """Cap the BLAS pool of the oracle (numpy/OpenBLAS) at n threads."""
+    from threadpoolctl import threadpool_limits
+
+    return threadpool_limits(limits=n)
+
+
+def cpu_throughput(cfg, budget_s: float, seed=1, threads=None):
+    if threads is not None:
+        with cpu_threads(threads):
+            return cpu_throughput(cfg, budget_s, seed)
     from oracle import engine as orc
 
     data, units, tg = make_data(cfg, 64, 0, 1, seed)
@@ -170,30 +205,44 @@ def cpu_throughput(cfg, budget_s: float, seed=1):
     return done_units / dt, steps, done_units, dt
 
 
+def cpu_baseline(cfg, name, budget_s):
+    """The oracle on this host at the box's full thread count (the reported
+    value) and at one BLAS thread (both are reported)."""
+    nproc = os.cpu_count() or 1
+    v, s, u, dt = cpu_throughput(cfg, budget_s, threads=nproc)
+    v1, s1, u1, dt1 = cpu_throughput(cfg, max(1.0, budget_s / 3), threads=1)
+    return {"value": v, "unit": unit_of(cfg), "cores": nproc, "kind": "port",
+            "sample": f"{s} graphs ({u} units) of the {name} workload through the numpy oracle in {dt:.1f} s, "
+                      f"BLAS threads={nproc}",
+            "single_thread": {"value": v1, "cores": 1,
+                              "sample": f"{s1} graphs ({u1} units) in {dt1:.1f} s, BLAS threads=1"}}
+
+
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
-    value, steps, units, dt = 0.0, 0, 0, 0.0
-    per = []
-    # warmup + K timed steps, each a bounded sample (~budget/K seconds)
-    cpu_throughput(cfg, min(5.0, 1.0 * args.warmup))
-    for _ in range(args.steps):
-        v, s, u, d = cpu_throughput(cfg, args.ref_budget / max(1, args.steps))
-        per.append(v)
-        steps += s
-        units += u
-        dt += d
+    nproc = os.cpu_count() or 1
+    steps, units, dt = 0, 0, 0.0
+    with cpu_threads(nproc):
+        # warmup + K timed steps, each a bounded sample (~budget/K seconds)
+        cpu_throughput(cfg, min(5.0, 1.0 * args.warmup))
+        for _ in range(args.steps):
+            v, s, u, d = cpu_throughput(cfg, args.ref_budget / max(1, args.steps))
+            steps += s
+            units += u
+            dt += d
     value = units / dt
-    cores = os.cpu_count()
     line = {
         "metric": METRIC, "value": value, "unit": unit_of(cfg), "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(1, steps), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": args.config, **cfg}, "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": unit_of(cfg), "cores": cores, "kind": "port",
+        "config": bench_config(args.config, cfg, world), "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": unit_of(cfg), "cores": nproc, "kind": "port",
                          "sample": f"{steps} minibatches ({units} units) of the {args.config} workload through the "
-                                   f"numpy oracle, {dt:.1f} s"},
+                                   f"numpy oracle (the reference algorithm restated), {dt:.1f} s, "
+                                   f"BLAS threads={nproc}"},
         "e2e": {"value": value, "unit": unit_of(cfg), "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -408,19 +457,15 @@ def run_b200(args, cfg):
             k2 = max(K, 20) if c2["kind"] != "rnnlm" or c2["mb"] == 1 else K
             r2 = measure(dy, c2, k2, max(Wm, 3), world, rank, local, profile=False)
             if not args.no_cpu:
-                v, s2, u, dt = cpu_throughput(c2, args.other_cpu_budget)
-                r2["cpu_baseline"] = {"value": v, "unit": unit_of(c2), "cores": os.cpu_count(), "kind": "port",
-                                      "sample": f"{s2} graphs ({u} units) through the numpy oracle in {dt:.1f} s"}
-            r2["config"] = {"workload": name, **c2}
+                r2["cpu_baseline"] = cpu_baseline(c2, name, args.other_cpu_budget)
+            r2["config"] = bench_config(name, c2, world)
             r2["steps"], r2["warmup"] = k2, max(Wm, 3)
             others[name] = r2
 
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu:
-            v, s, u, dt = cpu_throughput(cfg, args.cpu_budget)
-            cpu = {"value": v, "unit": unit_of(cfg), "cores": os.cpu_count(), "kind": "port",
-                   "sample": f"{s} minibatches ({u} units) of {args.config} through the numpy oracle in {dt:.1f} s"}
+            cpu = cpu_baseline(cfg, args.config, args.cpu_budget)
         line = {
             "metric": METRIC,
             "value": res["value"],
@@ -434,8 +479,7 @@ def run_b200(args, cfg):
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": args.config, **cfg, "global_batch": cfg["mb"] * world,
-                       "parallelism": f"dp{world}", "l2": "flushed between timed steps (256 MiB write)"},
+            "config": bench_config(args.config, cfg, world),
             "e2e": res["e2e"],
             "gpu_launches": res["gpu_launches"],
             "roofline": res["roofline"],
@@ -466,6 +510,18 @@ def main():
     ap.add_argument("--other-cpu-budget", type=float, default=3.0)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun
+        if args.impl == "b200":
+            import torch
+
+            have = torch.cuda.device_count()
+            if have < args.gpus:
+                sys.exit(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible")
+        port = 29500 + (os.getpid() % 2000)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

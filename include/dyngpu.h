@@ -173,12 +173,17 @@ int dg_trainer_step_count(dg_trainer* t, int64_t* step);
 int dg_trainer_set_step(dg_trainer* t, int64_t step);
 
 /* ---- data-parallel exchange helpers (parallel.py:55-65,105-109) --------
- * Pack the sorted touched rows of a lookup table into (ids, rows) device
- * buffers for an all-gather, and merge gathered (ids, rows) from all ranks
- * back into the table gradient (sorted segmented sum, scaled), deterministic. */
+ * dg_lookup_pack: copy the sorted touched rows of a lookup table's gradient
+ * into rows_dev (n x dim) and their ids into ids_dev, for an all-gather.
+ * dg_lookup_merge: ranks' packed rows (rank r: counts[r] rows at the device
+ * pointer rank_rows[r], ids in ids_host, concatenated in rank order) replace
+ * the table gradient on the union of ids with (sum in rank order) / div —
+ * average_slots + _load_average_into_model for the touched rows — and the
+ * union joins the touched set.  Both asynchronous on `stream` (host staging
+ * goes through pinned memory; no stream synchronisation), deterministic. */
 int dg_lookup_pack(int64_t handle, int64_t* ids_dev, float* rows_dev, int64_t cap, int64_t* n, void* stream);
-int dg_lookup_merge(int64_t handle, const int64_t* ids_host, const float* rows_dev, int64_t n, float scale,
-                    void* stream);
+int dg_lookup_merge(int64_t handle, int32_t n_ranks, const int64_t* counts, const int64_t* ids_host,
+                    const float* const* rank_rows, float div, void* stream);
 /* plain device helpers used by the sinks: y = alpha * y; zero */
 int dg_scale(float* y, int64_t n, float alpha, void* stream);
 

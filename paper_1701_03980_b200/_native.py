@@ -111,7 +111,7 @@ def _declare(lib):
         "dg_trainer_step_count": (ctypes.c_int, [c_vp, ctypes.POINTER(c_i64)]),
         "dg_trainer_set_step": (ctypes.c_int, [c_vp, c_i64]),
         "dg_lookup_pack": (ctypes.c_int, [c_i64, c_vp, c_vp, c_i64, ctypes.POINTER(c_i64), c_vp]),
-        "dg_lookup_merge": (ctypes.c_int, [c_i64, c_vp, c_vp, c_i64, c_f32, c_vp]),
+        "dg_lookup_merge": (ctypes.c_int, [c_i64, ctypes.c_int32, c_vp, c_vp, c_vp, c_f32, c_vp]),
         "dg_scale": (ctypes.c_int, [c_vp, c_i64, c_f32, c_vp]),
     }
     for name, (res, args) in sig.items():

@@ -65,6 +65,8 @@ struct Param {
   std::vector<int64_t> touched_list;  // insertion order; sorted on read
   int64_t size() const { return rows * cols; }
   std::vector<int32_t> sort_cnt;  // scatter planning scratch (all zero at rest)
+  void* dp_dev = nullptr;         // DP merge staging (dg_lookup_merge)
+  size_t dp_cap = 0;
 };
 
 static std::mutex g_param_mu;
@@ -1221,9 +1223,13 @@ static inline float* dummy_base(dg_graph* g) {
 static inline int* counter_base(dg_graph* g) {
   return reinterpret_cast<int*>(g->work_base + g->work_bytes - kCounterBytes);
 }
-static constexpr int kCounterCap = (int)(kCounterBytes / 4) - kFlagInts;
+// [0, kScatterCtrBase) split-K tile counters | kScatterCtrs lookup-scatter
+// segment counters | kFlagInts recurrence arrival flags
+static constexpr int kScatterCtrs = 8192;
+static constexpr int kCounterCap = (int)(kCounterBytes / 4) - kFlagInts - kScatterCtrs;
+static constexpr int kScatterCtrBase = kCounterCap;
 // persistent-recurrence arrival counters (zeroed by each rnn launch)
-static inline int* flag_base(dg_graph* g) { return counter_base(g) + kCounterCap; }
+static inline int* flag_base(dg_graph* g) { return counter_base(g) + kCounterCap + kScatterCtrs; }
 
 // Same-level affine problems accumulate into one grouped GEMM launch.
 struct GemmBatch {
@@ -1464,6 +1470,9 @@ int dg_param_release(int64_t h) {
   p->alive = false;
   p->touched_bits.clear();
   p->touched_list.clear();
+  if (p->dp_dev) cudaFree(p->dp_dev);  // best effort (may run at interpreter exit)
+  p->dp_dev = nullptr;
+  p->dp_cap = 0;
   return DG_OK;
 }
 
@@ -3231,15 +3240,21 @@ int dg_backward(dg_graph* g, int32_t loss) {
       for (int64_t u : uids) cnt[u] = 0;
       seg.push_back((int32_t)v.size());
       Param* p = param_at(h);
-      const size_t ou = B.push(uids), os = B.push(seg), osrc = B.push(src);
+      std::vector<ScatterItem> items;
+      int n_part = 0, n_long = 0;
+      const int n_items = plan_scatter_items(seg.data(), (int)uids.size(), items, &n_part, &n_long);
+      const size_t ou = B.push(uids), oit = B.push(items), osrc = B.push(src);
       float* tg = p->grad;
       const int dim = (int)p->cols;
-      const int nu = (int)uids.size();
-      plan.ops.push_back([tg, dim, ou, os, osrc, nu, st](char* d) {
-        return launch_segment_scatter_add(tg, dim, at<const int64_t>(d, ou), at<const int>(d, os),
-                                          at<const float* const>(d, osrc), nu, 1.f, st);
+      float* partials = reinterpret_cast<float*>(scratch_base(g));
+      int* ctr = counter_base(g) + kScatterCtrBase;
+      if ((int64_t)n_part * dim * 4 > (int64_t)scratch_bytes(g) || n_long > kScatterCtrs)
+        return fail(DG_POOL_EXHAUSTED, "workspace too small for the lookup scatter");
+      plan.ops.push_back([tg, dim, ou, oit, osrc, n_items, partials, ctr, st](char* d) {
+        return launch_scatter_rows(tg, dim, at<const int64_t>(d, ou), at<const ScatterItem>(d, oit), n_items,
+                                   at<const float* const>(d, osrc), partials, ctr, 1.f, false, st);
       });
-      plan.tag(C_SCATTER, 0.0, 4.0 * dim * ((double)src.size() + 2.0 * nu));
+      plan.tag(C_SCATTER, 0.0, 4.0 * dim * ((double)src.size() + 2.0 * (double)uids.size()));
     }
   }
   tm.lap("scatter");
@@ -3537,6 +3552,33 @@ int dg_trainer_update(dg_trainer* t, void* stream) {
 
 // --------------------------------------------------------------- DP helpers
 
+// Host staging of the DP helpers: a pinned slot of the process-wide ring
+// (reused once its previous upload has executed; no stream synchronisation)
+// and a per-table device buffer, grown geometrically, whose scatter counter
+// tail is zero at rest.
+static int stage_to_device(const std::vector<uint8_t>& host, char* dev, cudaStream_t st) {
+  if (host.empty()) return DG_OK;
+  Pinned& slot = staging_slot();
+  int rc = pinned_acquire(slot, host.size());
+  if (rc) return rc;
+  std::memcpy(slot.ptr, host.data(), host.size());
+  DG_CUDA_TRY(cudaMemcpyAsync(dev, slot.ptr, host.size(), cudaMemcpyHostToDevice, st));
+  DG_CUDA_TRY(cudaEventRecord(slot.ev, st));
+  slot.pending = true;
+  return DG_OK;
+}
+
+static int dp_buffer(Param& p, size_t need, cudaStream_t st) {
+  constexpr size_t kCtr = sizeof(int) * 4096;
+  if (p.dp_cap < need + kCtr) {
+    if (p.dp_dev) DG_CUDA_TRY(cudaFree(p.dp_dev));  // implicit device sync, growth only
+    p.dp_cap = std::max<size_t>(2 * (need + kCtr), 1 << 20);
+    DG_CUDA_TRY(cudaMalloc(&p.dp_dev, p.dp_cap));
+    DG_CUDA_TRY(cudaMemsetAsync(static_cast<char*>(p.dp_dev) + p.dp_cap - kCtr, 0, kCtr, st));
+  }
+  return DG_OK;
+}
+
 int dg_lookup_pack(int64_t handle, int64_t* ids_dev, float* rows_dev, int64_t cap, int64_t* n, void* stream) {
   Param* p = param_at(handle);
   if (!p || p->kind != 1) return fail(DG_INDEX, "not a lookup parameter");
@@ -3545,57 +3587,78 @@ int dg_lookup_pack(int64_t handle, int64_t* ids_dev, float* rows_dev, int64_t ca
   if ((int64_t)ids.size() > cap) return fail(DG_INDEX, "pack capacity too small");
   if (ids.empty()) return DG_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  DG_CUDA_TRY(cudaMemcpyAsync(ids_dev, ids.data(), ids.size() * 8, cudaMemcpyHostToDevice, st));
+  std::vector<uint8_t> host(ids.size() * 8);
+  std::memcpy(host.data(), ids.data(), host.size());
+  int rc = stage_to_device(host, reinterpret_cast<char*>(ids_dev), st);
+  if (rc) return rc;
   launch_pack_rows(p->grad, (int)p->cols, ids_dev, rows_dev, (int)ids.size(), st);
-  DG_CUDA_TRY(cudaStreamSynchronize(st));  // ids vector is pageable host memory
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(DG_CUDA, std::string("pack launch: ") + cudaGetErrorString(e));
   return DG_OK;
 }
 
-int dg_lookup_merge(int64_t handle, const int64_t* ids_host, const float* rows_dev, int64_t n, float scale,
-                    void* stream) {
-  // table_grad[ids] = scale * sum of gathered rows per id (ranks' rows arrive
-  // in rank order; the stable sort keeps that order inside a segment)
+int dg_lookup_merge(int64_t handle, int32_t n_ranks, const int64_t* counts, const int64_t* ids_host,
+                    const float* const* rank_rows, float div, void* stream) {
+  // table_grad[id] = (sum over ranks, in rank order, of that rank's row) / div
+  // for every id in the union; the union becomes the touched set
+  // (average_slots + _load_average_into_model, parallel.py:55-65,105-109).
   Param* p = param_at(handle);
   if (!p || p->kind != 1) return fail(DG_INDEX, "not a lookup parameter");
+  if (n_ranks <= 0 || !(div > 0.f)) return fail(DG_CONFIG, "merge needs n_ranks >= 1 and div > 0");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int dim = (int)p->cols;
+  std::vector<uintptr_t> rows_src;
+  std::vector<int64_t> ids_all;
+  for (int r = 0; r < n_ranks; ++r) {
+    if (counts[r] < 0) return fail(DG_CONFIG, "negative merge count");
+    for (int64_t k = 0; k < counts[r]; ++k) {
+      const int64_t id = ids_host[ids_all.size()];
+      if (id < 0 || id >= p->rows) return fail(DG_INDEX, "merge id out of range");
+      ids_all.push_back(id);
+      rows_src.push_back(P(rank_rows[r] + k * dim));
+    }
+  }
+  const int64_t n = (int64_t)ids_all.size();
+  if (n == 0) return DG_OK;
   std::vector<int64_t> order(n);
   std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return ids_host[a] < ids_host[b]; });
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return ids_all[a] < ids_all[b]; });
   std::vector<int64_t> uids;
   std::vector<int32_t> seg;
-  std::vector<uintptr_t> src;
+  std::vector<uintptr_t> src(n);
   for (int64_t q = 0; q < n; ++q) {
-    const int64_t id = ids_host[order[q]];
-    if (id < 0 || id >= p->rows) return fail(DG_INDEX, "merge id out of range");
-    if (q == 0 || id != ids_host[order[q - 1]]) {
+    const int64_t id = ids_all[order[q]];
+    if (q == 0 || id != ids_all[order[q - 1]]) {
       uids.push_back(id);
       seg.push_back((int32_t)q);
     }
-    src.push_back(P(rows_dev + order[q] * p->cols));
+    src[q] = rows_src[order[q]];
   }
   seg.push_back((int32_t)n);
-  // zero the rows that will be overwritten, then add the merged sums
-  size_t bytes = uids.size() * 8 + seg.size() * 4 + src.size() * 8 + 64;
-  void* dbuf = nullptr;
-  DG_CUDA_TRY(cudaMallocAsync(&dbuf, bytes, st));
-  char* d = static_cast<char*>(dbuf);
-  std::vector<uint8_t> host(bytes, 0);
-  size_t o_u = 0, o_s = (uids.size() * 8 + 15) & ~size_t(15);
-  size_t o_src = (o_s + seg.size() * 4 + 15) & ~size_t(15);
-  if (o_src + src.size() * 8 > bytes) return fail(DG_INTERNAL, "merge staging");
+  std::vector<ScatterItem> items;
+  int n_part = 0, n_long = 0;
+  const int n_items = plan_scatter_items(seg.data(), (int)uids.size(), items, &n_part, &n_long);
+  if (n_long > 4096) return fail(DG_INTERNAL, "merge: too many long segments");
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t o_u = 0, o_it = al(uids.size() * 8), o_src = o_it + al(items.size() * sizeof(ScatterItem));
+  const size_t o_part = o_src + al(src.size() * 8);
+  const size_t need = o_part + (size_t)n_part * dim * 4;
+  int rc = dp_buffer(*p, need, st);
+  if (rc) return rc;
+  std::vector<uint8_t> host(o_part, 0);
   std::memcpy(host.data() + o_u, uids.data(), uids.size() * 8);
-  std::memcpy(host.data() + o_s, seg.data(), seg.size() * 4);
+  std::memcpy(host.data() + o_it, items.data(), items.size() * sizeof(ScatterItem));
   std::memcpy(host.data() + o_src, src.data(), src.size() * 8);
-  DG_CUDA_TRY(cudaMemcpyAsync(d, host.data(), bytes, cudaMemcpyHostToDevice, st));
-  // rows of this table's gradient that are in the merged set are replaced:
-  // scale them to zero first (the local contribution is part of the gather)
-  launch_update_rows(RuleArgs{0, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 1.f, 1.f}, p->val, p->grad, nullptr, nullptr,
-                     (int)p->cols, reinterpret_cast<const int64_t*>(d + o_u), (int)uids.size(), st);
-  launch_segment_scatter_add(p->grad, (int)p->cols, reinterpret_cast<const int64_t*>(d + o_u),
-                             reinterpret_cast<const int*>(d + o_s), reinterpret_cast<const float* const*>(d + o_src),
-                             (int)uids.size(), scale, st);
-  DG_CUDA_TRY(cudaStreamSynchronize(st));
-  DG_CUDA_TRY(cudaFreeAsync(dbuf, st));
+  char* d = static_cast<char*>(p->dp_dev);
+  rc = stage_to_device(host, d, st);
+  if (rc) return rc;
+  int* ctr = reinterpret_cast<int*>(d + p->dp_cap - sizeof(int) * 4096);
+  launch_scatter_rows(p->grad, dim, reinterpret_cast<const int64_t*>(d + o_u),
+                      reinterpret_cast<const ScatterItem*>(d + o_it), n_items,
+                      reinterpret_cast<const float* const*>(d + o_src), reinterpret_cast<float*>(d + o_part), ctr, div,
+                      true, st);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(DG_CUDA, std::string("merge launch: ") + cudaGetErrorString(e));
   for (int64_t id : uids) touch(*p, id);
   return DG_OK;
 }

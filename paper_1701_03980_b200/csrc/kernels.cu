@@ -677,59 +677,90 @@ __global__ void gather_rows_kernel(const float* __restrict__ table, int dim, con
   }
 }
 
-constexpr int kScatterWarps = 32;
-
-__global__ void segment_scatter_add_kernel(float* __restrict__ table_grad, int dim, const int64_t* __restrict__ ids,
-                                           const int* __restrict__ seg, const float* const* src_rows, int n_unique,
-                                           float scale) {
+// Sorted segmented scatter of lookup-row gradients (graph.py:57-63
+// `np.add.at`), deterministic and atomic-free in its arithmetic: one warp per
+// work item; a segment of <= kScatterChunk rows is one item that writes its
+// row directly; a longer segment (the EOS padding id collects one row per
+// padded position) is split into chunks whose partial sums go to scratch, and
+// the warp that finishes a segment's last chunk (arrival counter) adds the
+// partials in chunk order.  Rows are summed in segment order inside a chunk,
+// 8 row loads in flight per lane.
+template <bool kSet>
+__global__ void __launch_bounds__(256) scatter_rows_kernel(float* __restrict__ table_grad, int dim,
+                                                           const int64_t* __restrict__ ids,
+                                                           const ScatterItem* __restrict__ items, int n_items,
+                                                           const float* const* __restrict__ src_rows,
+                                                           float* __restrict__ partials, int* __restrict__ counters,
+                                                           float scale) {
   pdl_prologue();
-  // one block per unique id; warp w sums rows k0+w, k0+w+W, ... (a long
-  // segment, e.g. the EOS padding id, is spread over W = 32 warps), then the
-  // W partials are reduced in fixed warp order: deterministic, no atomics.
-  constexpr int W = kScatterWarps;
-  __shared__ float part[W][128];
-  const int u = blockIdx.x;
-  if (u >= n_unique) return;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float* dst = table_grad + ids[u] * (int64_t)dim;
-  const int k0 = seg[u], k1 = seg[u + 1];
-  for (int c0 = 0; c0 < dim; c0 += 128) {
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    // R rows in flight per warp (row pointers, then values, then the adds in
-    // row order): a long segment is latency-bound otherwise
-    constexpr int R = 8;
-    for (int k = k0 + w; k < k1; k += W * R) {
-      const float* rp[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) rp[r] = k + W * r < k1 ? src_rows[k + W * r] : nullptr;
-      float v[R][4];
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int c = c0 + lane + 32 * q;
-          v[r][q] = rp[r] && c < dim ? rp[r][c] : 0.f;
-        }
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (rp[r]) acc[q] += v[r][q];
+  const int w = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (w >= n_items) return;
+  const int lane = threadIdx.x & 31;
+  const ScatterItem it = items[w];
+  float* dst = table_grad + ids[it.u] * (int64_t)dim;
+  const bool chunked = it.nchunks > 0;
+  float* part = chunked ? partials + (int64_t)(it.pbase + it.chunk) * dim : nullptr;
+  bool vec = (dim & 3) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  for (int k = it.k0; k < it.k1 && vec; ++k) vec = (reinterpret_cast<uintptr_t>(src_rows[k]) & 15) == 0;
+  auto finish = [&](int c, float s) {
+    if (chunked) {
+      part[c] = s;
+    } else if (kSet) {
+      dst[c] = s / scale;
+    } else {
+      dst[c] += scale * s;
     }
+  };
+  if (vec) {
+    for (int c4 = lane; c4 < (dim >> 2); c4 += 32) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      constexpr int R = 8;
+      for (int k = it.k0; k < it.k1; k += R) {
+        float4 v[R];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) part[w][lane + 32 * q] = acc[q];
-    __syncthreads();
-    if (threadIdx.x < 128) {
-      const int c = c0 + threadIdx.x;
-      if (c < dim) {
-        float s = 0.f;
+        for (int r = 0; r < R; ++r)
+          v[r] = k + r < it.k1 ? __ldg(reinterpret_cast<const float4*>(src_rows[k + r]) + c4)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int ww = 0; ww < W; ++ww) s += part[ww][threadIdx.x];
-        dst[c] += scale * s;
+        for (int r = 0; r < R; ++r)
+          if (k + r < it.k1) {
+            acc.x += v[r].x;
+            acc.y += v[r].y;
+            acc.z += v[r].z;
+            acc.w += v[r].w;
+          }
       }
+      finish(4 * c4 + 0, acc.x);
+      finish(4 * c4 + 1, acc.y);
+      finish(4 * c4 + 2, acc.z);
+      finish(4 * c4 + 3, acc.w);
     }
-    __syncthreads();
+  } else {
+    for (int c = lane; c < dim; c += 32) {
+      float acc = 0.f;
+      for (int k = it.k0; k < it.k1; ++k) acc += src_rows[k][c];
+      finish(c, acc);
+    }
   }
+  if (!chunked) return;
+  // last chunk of the segment to arrive combines the partials in chunk order
+  __threadfence();
+  int last = 0;
+  if (lane == 0) last = atomicAdd(counters + it.seg_slot, 1) == it.nchunks - 1;
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  __threadfence();
+  const float* pb = partials + (int64_t)it.pbase * dim;
+  for (int c = lane; c < dim; c += 32) {
+    float s = 0.f;
+    for (int q = 0; q < it.nchunks; ++q) s += __ldcg(pb + (int64_t)q * dim + c);
+    if (kSet) {
+      dst[c] = s / scale;
+    } else {
+      dst[c] += scale * s;
+    }
+  }
+  if (lane == 0) counters[it.seg_slot] = 0;  // left at zero for the next launch
 }
 
 __global__ void pack_rows_kernel(const float* __restrict__ table, int dim, const int64_t* __restrict__ ids,
@@ -1227,11 +1258,39 @@ int launch_gather_rows(const float* table, int dim, const int64_t* ids, float* c
   return 1;
 }
 
-int launch_segment_scatter_add(float* table_grad, int dim, const int64_t* uniq_ids, const int* seg,
-                               const float* const* src_rows, int n_unique, float scale, cudaStream_t s) {
-  if (n_unique <= 0) return 0;
-  launch_k(segment_scatter_add_kernel, n_unique, 32 * kScatterWarps, 0, s, table_grad, dim, uniq_ids, seg, src_rows,
-                                                                      n_unique, scale);
+int plan_scatter_items(const int* seg, int n_unique, std::vector<ScatterItem>& items, int* n_partials,
+                       int* n_long) {
+  items.clear();
+  int pb = 0, nl = 0;
+  for (int u = 0; u < n_unique; ++u) {
+    const int k0 = seg[u], k1 = seg[u + 1], len = k1 - k0;
+    if (len <= kScatterChunk) {
+      items.push_back(ScatterItem{u, k0, k1, 0, 0, 0, 0, 0});
+      continue;
+    }
+    const int nc = (len + kScatterChunk - 1) / kScatterChunk;
+    for (int c = 0; c < nc; ++c)
+      items.push_back(ScatterItem{u, k0 + c * kScatterChunk, std::min(k1, k0 + (c + 1) * kScatterChunk), c, nc, pb, nl,
+                                  0});
+    pb += nc;
+    ++nl;
+  }
+  *n_partials = pb;
+  *n_long = nl;
+  return (int)items.size();
+}
+
+int launch_scatter_rows(float* table_grad, int dim, const int64_t* uniq_ids, const ScatterItem* items, int n_items,
+                        const float* const* src_rows, float* partials, int* counters, float scale, bool set_mean,
+                        cudaStream_t s) {
+  if (n_items <= 0) return 0;
+  const int grid = (n_items + 7) / 8;
+  if (set_mean)
+    launch_k(scatter_rows_kernel<true>, grid, 256, 0, s, table_grad, dim, uniq_ids, items, n_items, src_rows, partials,
+             counters, scale);
+  else
+    launch_k(scatter_rows_kernel<false>, grid, 256, 0, s, table_grad, dim, uniq_ids, items, n_items, src_rows,
+             partials, counters, scale);
   return 1;
 }
 

@@ -209,10 +209,20 @@ int launch_pnls_bwd(const RowArgs& a, cudaStream_t s);
 // gather: out_rows[r] = table[ids[r]]  (one warp per row, 128-bit vectors)
 int launch_gather_rows(const float* table, int dim, const int64_t* ids, float* const* out_rows, int rows,
                        cudaStream_t s);
-// atomic-free sorted segmented scatter-add:
+// sorted segmented scatter of row gradients (graph.py:57-63):
 //   for u in unique: table_grad[ids[u]] += scale * sum_{k in seg[u]..seg[u+1]} src_rows[k]
-int launch_segment_scatter_add(float* table_grad, int dim, const int64_t* uniq_ids, const int* seg,
-                               const float* const* src_rows, int n_unique, float scale, cudaStream_t s);
+// (set_mean: table_grad[ids[u]] = sum / scale).  Deterministic: fixed
+// summation order, no float atomics.  Segments longer than kScatterChunk rows
+// are split into chunks (partials: n_partials x dim floats of scratch;
+// counters: n_long ints, zero at rest and left at zero).
+constexpr int kScatterChunk = 16;
+struct ScatterItem {
+  int u, k0, k1, chunk, nchunks, pbase, seg_slot, pad;
+};
+int plan_scatter_items(const int* seg, int n_unique, std::vector<ScatterItem>& items, int* n_partials, int* n_long);
+int launch_scatter_rows(float* table_grad, int dim, const int64_t* uniq_ids, const ScatterItem* items, int n_items,
+                        const float* const* src_rows, float* partials, int* counters, float scale, bool set_mean,
+                        cudaStream_t s);
 
 // ---------------------------------------------------------------- generic
 // matmul (ops.py:252-301) per batch element, column-major element layout

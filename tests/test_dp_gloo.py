@@ -1,16 +1,19 @@
-"""World-size-2 (gloo, CPU) test of the data-parallel exchange protocol.
+"""CPU tests of the data-parallel exchange: the product `DataParallel.sync`
+(paper_1701_03980_b200/parallel.py) runs unchanged over
 
-The GPU path (parallel.DataParallel) all-reduces the flat dense gradient and
-exchanges sparse lookup rows with `exchange_rows` (counts all-gather, padded
-ids/rows all-gather, rank-order concatenation) before a deterministic sorted
-segmented merge.  Here the same protocol runs over gloo on CPU tensors with
-oracle-computed per-rank gradients and a numpy merge, and must reproduce the
-oracle's deterministic DP restatement (oracle.engine.dp_step: average over R
-participants, touched = union), with bit-identical replicas on both ranks.
+  * a world-size-2 gloo process group (`ProcessGroupComm`, mp.spawn), and
+  * in-process replicas (`ThreadComm`, 3 threads: a non-power-of-two R),
+
+with an oracle-backed gradient store standing in for HBM (the device store is
+covered by tests/test_gpu_dp.py on the GPU).  Results must reproduce the
+oracle's deterministic DP restatement (oracle.engine.dp_step: average over
+the R participants, touched = union; reference parallel.py:55-65,105-109),
+with bit-identical replicas.
 """
 
 import os
 import socket
+import threading
 
 import numpy as np
 import pytest
@@ -20,14 +23,61 @@ import torch.multiprocessing as mp
 
 from oracle import engine as orc
 from paper_1701_03980_b200 import workloads as W
-from paper_1701_03980_b200.parallel import exchange_rows, merge_plan
+from paper_1701_03980_b200.parallel import DataParallel, ProcessGroupComm, ThreadComm, merge_plan
 
-R = 2
 VOCAB, E, H = 120, 8, 12
 
 
-def _shards():
-    sents = W.ptb_corpus(31, 8, vocab=VOCAB)
+class OracleGradStore:
+    """DataParallel's store interface over an oracle Model (numpy arrays)."""
+
+    def __init__(self, model):
+        self.m = model
+        self._dense = None
+
+    def begin(self):
+        self._dense = torch.from_numpy(np.concatenate([p.gradient.ravel() for p in self.m.parameters]))
+
+    def end(self):
+        off = 0
+        for p in self.m.parameters:
+            n = p.gradient.size
+            p.gradient.ravel()[:] = self._dense[off : off + n].numpy()
+            off += n
+
+    def dense(self):
+        return self._dense
+
+    def lookups(self):
+        return list(self.m.lookups)
+
+    def table_grad(self, lp):
+        return torch.from_numpy(lp.gradient)
+
+    def touched(self, lp):
+        return np.array(sorted(lp.touched), dtype=np.int64)
+
+    def alloc(self, n):
+        return torch.zeros(max(1, int(n)), dtype=torch.float32)
+
+    def pack(self, lp, ids, out):
+        out.view(-1, lp.dim)[:] = torch.from_numpy(lp.gradient[ids])
+
+    def merge(self, lp, counts, ids, rank_rows, divisor):
+        """What dg_lookup_merge computes: rows of the union = (sum in rank
+        order) / divisor; the union joins the touched set."""
+        rows = np.concatenate([rank_rows[r].numpy().reshape(-1, lp.dim)[: counts[r]] for r in range(len(counts))])
+        _, order, uniq, seg = merge_plan([ids])
+        for u, rid in enumerate(uniq):
+            acc = np.zeros(lp.dim, dtype=np.float32)
+            for k in range(seg[u], seg[u + 1]):
+                acc += rows[order[k]]
+            lp.gradient[rid] = acc / np.float32(divisor)
+        lp.touched = set(lp.touched) | set(int(i) for i in uniq)
+
+
+def _shards(n):
+    sents = W.ptb_corpus(31, 4 * n, vocab=VOCAB)
     return W.minibatches(sents, 4)  # rank r takes batch r
 
 
@@ -37,49 +87,38 @@ def _make(seed=1):
     return cg, m, W.RNNLM(orc, m, VOCAB, E, H, 2)
 
 
-def _numpy_merge(grad, ids, rows, scale):
-    """The merge dg_lookup_merge performs, restated for the CPU check."""
-    _, order, uniq, seg = merge_plan([ids])
-    grad[uniq] = 0
-    for u, rid in enumerate(uniq):
-        acc = np.zeros(grad.shape[1], dtype=np.float32)
-        for k in range(seg[u], seg[u + 1]):
-            acc += rows[order[k]]
-        grad[rid] += np.float32(scale) * acc
+def _replica_step(rank, R, comm, sparse, rule="adam"):
+    cg, m, task = _make()
+    tr = orc.Trainer(m, rule)
+    tr.sparse = sparse
+    cg.renew()
+    loss = task.loss(cg, _shards(R)[rank])
+    cg.backward(loss)
+    DataParallel(m, sparse=sparse, comm=comm, store=OracleGradStore(m)).sync()
+    tr.update()
+    return {**{p.name: p.values.copy() for p in m.parameters}, **{lp.name: lp.values.copy() for lp in m.lookups}}
 
 
-def _worker(rank, port, outdir):
+def _oracle(R, sparse, rule="adam"):
+    _, m, task = _make()
+    tr = orc.Trainer(m, rule)
+    tr.sparse = sparse
+    shards = _shards(R)
+
+    def graph_for(r):
+        g = orc.ComputationGraph(orc.new_poolset())
+        return g, task.loss(g, shards[r])
+
+    orc.dp_step(m, tr, graph_for, R)
+    return {**{p.name: p.values for p in m.parameters}, **{lp.name: lp.values for lp in m.lookups}}
+
+
+def _worker(rank, port, outdir, sparse):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=R)
-    cg, m, task = _make()
-    tr = orc.Trainer(m, "adam")
-    batch = _shards()[rank]
-    cg.renew()
-    loss = task.loss(cg, batch)
-    cg.backward(loss)
-    # dense: one flat all-reduce (average over R participants)
-    flat = torch.from_numpy(np.concatenate([p.gradient for p in m.parameters]))
-    dist.all_reduce(flat)
-    flat /= R
-    off = 0
-    for p in m.parameters:
-        p.gradient[:] = flat[off : off + p.gradient.size].numpy()
-        off += p.gradient.size
-    # sparse rows
-    for lp in m.lookups:
-        mine = np.array(sorted(lp.touched), dtype=np.int64)
-
-        def pack(ids, rows, cap, mine=mine, lp=lp):
-            ids[: len(mine)] = torch.from_numpy(mine)
-            rows[: len(mine)] = torch.from_numpy(lp.gradient[mine])
-
-        ids, rows = exchange_rows(dist, None, R, len(mine), lp.dim, pack, torch.device("cpu"))
-        _numpy_merge(lp.gradient, ids, rows.numpy(), 1.0 / R)
-        lp.touched = set(int(i) for i in ids)
-    tr.update()
-    np.savez(os.path.join(outdir, f"rank{rank}.npz"),
-             **{p.name: p.values for p in m.parameters}, **{lp.name: lp.values for lp in m.lookups})
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    out = _replica_step(rank, 2, ProcessGroupComm(), sparse)
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), **out)
     dist.destroy_process_group()
 
 
@@ -97,25 +136,63 @@ def test_merge_plan_is_sorted_stable():
     assert list(order[:2]) == [1, 3]
 
 
-def test_dp_exchange_matches_oracle_restatement(tmp_path):
-    mp.spawn(_worker, args=(_free_port(), str(tmp_path)), nprocs=R, join=True)
+@pytest.mark.parametrize("sparse", [True, False])
+def test_sync_over_gloo_matches_oracle_dp(tmp_path, sparse):
+    mp.spawn(_worker, args=(_free_port(), str(tmp_path), sparse), nprocs=2, join=True)
     r0 = np.load(tmp_path / "rank0.npz")
     r1 = np.load(tmp_path / "rank1.npz")
+    ref = _oracle(2, sparse)
     for k in r0.files:
         assert np.array_equal(r0[k], r1[k]), f"replicas diverged on {k}"
-    # serial oracle DP restatement on the same shards
-    cgs = [_make() for _ in range(R)]
-    _, m, task = _make()
-    tr = orc.Trainer(m, "adam")
-    shards = _shards()
+        # R=2: the gloo sum of two addends then /2 is the reference's sum/2
+        np.testing.assert_array_equal(r0[k], ref[k], err_msg=k)
 
-    def graph_for(r):
-        g = orc.ComputationGraph(orc.new_poolset())
-        return g, task.loss(g, shards[r])
 
-    orc.dp_step(m, tr, graph_for, R)
-    for p in m.parameters:
-        np.testing.assert_allclose(r0[p.name], p.values, rtol=1e-5, atol=1e-7)
-    for lp in m.lookups:
-        np.testing.assert_allclose(r0[lp.name], lp.values, rtol=1e-5, atol=1e-7)
-    del cgs
+@pytest.mark.parametrize("sparse", [True, False])
+def test_sync_over_threads_is_bit_exact(sparse):
+    R = 3
+    comms = ThreadComm.group(R)
+    outs = [None] * R
+    errs = []
+
+    def run(r):
+        try:
+            outs[r] = _replica_step(r, R, comms[r], sparse)
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+            comms[r].shared.barrier.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(R)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    ref = _oracle(R, sparse)
+    for k in ref:
+        for r in range(R):
+            # rank-order sums divided by R: exactly the reference's average_slots
+            np.testing.assert_array_equal(outs[r][k], ref[k], err_msg=f"{k} rank {r}")
+
+
+def test_sync_touched_is_union():
+    R = 2
+    comms = ThreadComm.group(R)
+    touched = [None] * R
+
+    def run(r):
+        cg, m, task = _make()
+        cg.renew()
+        cg.backward(task.loss(cg, _shards(R)[r]))
+        mine = set(m.lookups[0].touched)
+        DataParallel(m, sparse=True, comm=comms[r], store=OracleGradStore(m)).sync()
+        touched[r] = (mine, set(m.lookups[0].touched))
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(R)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    union = touched[0][0] | touched[1][0]
+    assert touched[0][0] != touched[1][0]
+    assert touched[0][1] == union and touched[1][1] == union
