@@ -77,6 +77,11 @@ def new_poolset(*_args, **kw):
     return np.dtype(kw.get("dtype", F32))
 
 
+def poolset_from_mem_flag(_flag, dtype=F32):
+    """bench/cli.py --mem pools (arena.py:105-107); the oracle keeps the dtype."""
+    return np.dtype(dtype)
+
+
 def col_major(flat_elem, dims):
     """Element view following the layout contract (tensor.py:1-6, :65-68)."""
     return flat_elem.reshape(dims, order="F")

@@ -22,7 +22,7 @@ import numpy as np
 
 from . import _dgcore, _native
 from . import device as _dev
-from .errors import ConfigError, NonScalarLoss, ShapeError, StaleExpression
+from .errors import NonScalarLoss, ShapeError, StaleExpression
 from .ops import FAST_KINDS, REGISTRY
 from .params import materialize_pending
 from .tensor import Shape, Tensor
@@ -60,9 +60,23 @@ class Node(_dgcore.NodeBase):
 
 
 class ModelGradientSink:
-    """Default backward target: the parameters' own gradient storage.  On the
-    device executor this is the only sink (data parallelism uses per-rank
-    model replicas plus a collective, see parallel.py)."""
+    """Default backward target: the parameters' own gradient storage
+    (graph.py:51-66).  The device executor accumulates into it directly.  Any
+    other object assigned to `cg.sink` receives the reference sink protocol
+    (`add_param_grad`, `add_lookup_rows_grad`) after the device backward, see
+    ComputationGraph._backward_to_sink."""
+
+    def add_param_grad(self, p, flat) -> None:
+        g = p.gradient.data
+        g += np.asarray(flat, dtype=g.dtype).reshape(g.shape)
+
+    def add_lookup_row_grad(self, lp, row: int, vec) -> None:
+        self.add_lookup_rows_grad(lp, [row], np.asarray(vec).reshape(1, -1))
+
+    def add_lookup_rows_grad(self, lp, ids, rows) -> None:
+        g = lp.gradient
+        np.add.at(g, list(ids), np.asarray(rows, dtype=g.dtype).reshape(len(ids), -1))
+        lp.touched = lp.touched | set(int(i) for i in ids)
 
 
 DIRECT_SINK = ModelGradientSink()
@@ -234,11 +248,65 @@ class ComputationGraph:
         if loss.shape.elem_size() != 1 or loss.shape.batch != 1:
             raise NonScalarLoss(f"backward needs a scalar, got {loss.shape}")
         if self.sink is not DIRECT_SINK:
-            raise ConfigError("the device executor accumulates into model storage only; use parallel.py for DP")
+            self._backward_to_sink(e)
+            return
         h = self._prepare()
         _native.check(_native.lib().dg_backward(h, e.index))
         self._advance(e.index)
         _dev.bump_epoch()
+
+    def _backward_to_sink(self, e: Expression) -> None:
+        """backward() with a custom sink (graph.py:139-164 flushing through
+        `self.sink`, e.g. the reference's GradientSlots, parallel.py:30-46).
+
+        The device backward runs unchanged into zeroed gradient storage of
+        every parameter / lookup table a node <= loss references (all nodes
+        <= loss flush, ancestors or not); the result is handed to the sink as
+        ONE `add_param_grad(p, flat)` per parameter and ONE
+        `add_lookup_rows_grad(lp, ids, rows)` per table with the sorted unique
+        rows this backward touched, then the model's own gradients and touched
+        sets are restored.  For an additive sink this equals the reference's
+        per-node flushes up to the order of fp32 additions."""
+        h = self._prepare()
+        params, tables, seen = [], [], set()
+        for node in self.nodes[: e.index + 1]:
+            if node.kind == "parameter":
+                x = node.aux
+            elif node.kind in ("lookup", "lookup_batch"):
+                x = node.aux[0]
+            else:
+                continue
+            if id(x) in seen:
+                continue
+            seen.add(id(x))
+            (params if node.kind == "parameter" else tables).append(x)
+        saved = []
+        for x in params + tables:
+            saved.append(x._gm.dev.clone())
+            x._gm.dev.zero_()
+        touched = [lp.touched for lp in tables]
+        for lp in tables:
+            lp.touched = ()
+        _native.check(_native.lib().dg_backward(h, e.index))
+        self._advance(e.index)
+        grads = []
+        for x, keep in zip(params + tables, saved):
+            if x in tables:
+                ids = np.array(sorted(x.touched), dtype=np.int64)
+                it = _dev.torch().from_numpy(ids).to(x._gm.dev.device)
+                rows = x._gm.dev.view(x.rows, x.dim).index_select(0, it).cpu().numpy()
+                grads.append((ids, rows))
+            else:
+                grads.append(x._gm.dev.cpu().numpy())
+            x._gm.dev.copy_(keep)
+        for lp, t in zip(tables, touched):
+            lp.touched = t
+        _dev.bump_epoch()
+        for x, g in zip(params + tables, grads):
+            if x in tables:
+                self.sink.add_lookup_rows_grad(x, [int(i) for i in g[0]], g[1])
+            else:
+                self.sink.add_param_grad(x, g)
 
     def gradient(self, e: Expression) -> Tensor:
         """Debug accessor for a node's last backward slot.  Parameter nodes

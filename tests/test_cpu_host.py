@@ -159,3 +159,41 @@ def test_tree_node_validation():
         dc.TreeNode(token="a", children=(dc.TreeNode.leaf("b"),))
     with pytest.raises(BadShape):
         dc.TreeNode()
+
+
+def test_opdef_reference_positional_order():
+    """The reference plug-in contract OpDef(name, shape, forward, backward,
+    alias, flush) (pkg/src/dyncore/ops.py:33-40) constructs positionally;
+    re-registering a built-in kind keeps its native kernel and encoding, and
+    its Python shape rule runs at construction."""
+    calls = []
+    orig = ops.get_op("tanh")
+
+    def shape(aux, in_shapes):
+        calls.append(in_shapes[0])
+        return in_shapes[0]
+
+    def fwd(out, ins, aux):
+        raise AssertionError("never called: the kernel is native")
+
+    od = ops.OpDef("tanh", shape, fwd, None, None, None)
+    assert od.forward is fwd and od.backward is None and od.encode is None
+    try:
+        reg = ops.register(od)
+        assert reg.code == orig.code and reg.encode is orig.encode and reg.forward is fwd
+        cg, _ = make_ctx()
+        y = ops.tanh(ops.input(cg, vec([0.5, -0.5])))
+        assert len(calls) == 1 and cg.nodes[y.index].shape.dims == (2,)
+    finally:
+        ops.REGISTRY["tanh"] = orig
+        ops.FAST_KINDS["tanh"] = orig.code
+
+
+def test_python_only_op_is_a_config_error():
+    """No CPU execution path: a kind with only Python forward/backward raises
+    the reference taxonomy's ConfigError at registration, not TypeError."""
+    od = ops.OpDef("my_square", lambda aux, s: s[0], lambda out, ins, aux: None,
+                   lambda i, g, iv, ov, og, aux: None)
+    with pytest.raises(ConfigError):
+        ops.register(od)
+    assert "my_square" not in ops.REGISTRY

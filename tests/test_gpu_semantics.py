@@ -305,10 +305,14 @@ def test_dyn1_roundtrip(tmp_path):
     W_ = model.add_parameters((3, 4), "W")
     E = model.add_lookup_parameters(5, 2, "E")
     tr = dy.Trainer(model, "sgd")
-    loss = ops.pickneglogsoftmax(ops.affine(ops.input(cg, vec([0.0, 0.0, 0.0])), ops.parameter(cg, W_),
-                                            ops.lookup(cg, E, 1) if False else ops.input(cg, vec([1.0, 2.0, 3.0, 4.0]))), 1)
+    x = ops.concatenate([ops.lookup(cg, E, 1), ops.lookup(cg, E, 3)])
+    loss = ops.pickneglogsoftmax(ops.affine(ops.input(cg, vec([0.0, 0.0, 0.0])), ops.parameter(cg, W_), x), 1)
+    before = E.values.copy()
     cg.backward(loss)
     tr.update()
+    after = E.values.copy()
+    assert not np.array_equal(after[[1, 3]], before[[1, 3]]), "the looked-up rows must have trained"
+    assert np.array_equal(np.delete(after, [1, 3], 0), np.delete(before, [1, 3], 0))
     path = str(tmp_path / "m.dyn")
     model.save(path)
     dy2, cg2, m2 = gpu_ctx(seed=99, mb=8)
@@ -317,3 +321,58 @@ def test_dyn1_roundtrip(tmp_path):
     m2.load(path)
     assert np.array_equal(m2.parameters[0].values.data, W_.values.data)
     assert np.array_equal(m2.lookups[0].values, E.values)
+
+
+# -- the reference sink protocol (graph.py:51-66, parallel.py:30-46) ----------
+
+
+class _SlotsSink:
+    """A GradientSlots-style sink (reference parallel.py:30-46)."""
+
+    def __init__(self, model):
+        self.params = {id(p): np.zeros(p.size, np.float64) for p in model.parameters}
+        self.lookups = {id(lp): np.zeros((lp.rows, lp.dim), np.float64) for lp in model.lookups}
+        self.rows_seen = {}
+
+    def add_param_grad(self, p, flat):
+        self.params[id(p)] += np.asarray(flat).reshape(-1)
+
+    def add_lookup_row_grad(self, lp, row, vec):
+        self.lookups[id(lp)][row] += vec
+
+    def add_lookup_rows_grad(self, lp, ids, rows):
+        self.rows_seen.setdefault(id(lp), []).extend(ids)
+        np.add.at(self.lookups[id(lp)], list(ids), rows)
+
+
+def test_custom_sink_receives_the_default_sinks_gradients():
+    """cg.sink = <sink object>: the device backward's gradients arrive through
+    add_param_grad / add_lookup_rows_grad and the model's own gradients and
+    touched sets stay as they were; the same graph under the default sink
+    accumulates exactly those gradients into the model."""
+    from paper_1701_03980_b200 import workloads as W
+    from tests.helpers import pgrad
+
+    sents = W.ptb_corpus(7, 4, vocab=500)
+    dy, cg, model = gpu_ctx(seed=5, mb=64)
+    task = W.RNNLM(dy, model, 500, 16, 32, 2)
+
+    cg.renew()
+    cg.backward(task.loss(cg, sents))
+    ref_p = {id(p): pgrad(p) for p in model.parameters}
+    ref_l = {id(lp): lp.gradient.astype(np.float64).copy() for lp in model.lookups}
+    ref_t = {id(lp): sorted(lp.touched) for lp in model.lookups}
+    model.zero_gradients()
+
+    sink = _SlotsSink(model)
+    cg.renew()
+    cg.sink = sink
+    cg.backward(task.loss(cg, sents))
+    cg.sink = dc.graph.DIRECT_SINK
+    for p in model.parameters:
+        assert not pgrad(p).any(), f"{p.name}: model gradient written under a custom sink"
+        assert np.allclose(sink.params[id(p)], ref_p[id(p)], rtol=1e-6, atol=1e-9), p.name
+    for lp in model.lookups:
+        assert not lp.touched and not lp.gradient.any()
+        assert sorted(set(sink.rows_seen[id(lp)])) == ref_t[id(lp)]
+        assert np.allclose(sink.lookups[id(lp)], ref_l[id(lp)], rtol=1e-6, atol=1e-9)
