@@ -843,3 +843,68 @@ class TreeNode:
 
     def is_leaf(self):
         return self.token is not None
+
+
+class TreeRNN:
+    """builders.py:183-210: leaf -> E row, unary -> child, binary ->
+    tanh(W [h_l; h_r]); parameters W then E; one W node per graph."""
+
+    def __init__(self, model, word_vocab, hidden_dim, name=None):
+        name = name if name is not None else f"treernn{len(model.parameters) + len(model.lookups)}"
+        self.w2i = dict(word_vocab)
+        self.W = model.add_parameters((hidden_dim, 2 * hidden_dim), f"{name}.W")
+        self.E = model.add_lookup_parameters(max(1, len(self.w2i)), hidden_dim, f"{name}.E")
+        self._cache = {}
+
+    def encode(self, g, tree):
+        if tree.token is not None:
+            return ops.lookup(g, self.E, self.w2i.get(tree.token, 0))
+        if len(tree.children) == 1:
+            return self.encode(g, tree.children[0])
+        a = self.encode(g, tree.children[0])
+        b = self.encode(g, tree.children[1])
+        c = self._cache.get(id(g))
+        if c is None or c[0] != g.generation:
+            c = (g.generation, ops.parameter(g, self.W))
+            self._cache[id(g)] = c
+        return ops.tanh(ops.matmul(c[1], ops.concatenate([a, b])))
+
+
+class ClassFactoredSoftmax:
+    """builders.py:282-378: classes renumbered densely in sorted raw-id order,
+    words slotted in map order; parameters Wc, bc, Ww[0..C), bw[0..C); the
+    class and word score affines are built once per (generation, h.index);
+    -log p(w) = pnls(class scores, c) + pnls(word scores of c, slot)."""
+
+    def __init__(self, model, hidden_dim, word_to_class, name=None):
+        name = name if name is not None else f"cfsm{len(model.parameters) + len(model.lookups)}"
+        dense = {raw: i for i, raw in enumerate(sorted(set(word_to_class.values())))}
+        self.members = [[] for _ in dense]
+        self.slot = {}
+        for w, raw in word_to_class.items():
+            c = dense[raw]
+            self.slot[w] = (c, len(self.members[c]))
+            self.members[c].append(w)
+        C = len(dense)
+        self.Wc = model.add_parameters((C, hidden_dim), f"{name}.Wc")
+        self.bc = model.add_parameters((C,), f"{name}.bc")
+        self.Ww = [model.add_parameters((len(m), hidden_dim), f"{name}.Ww{c}") for c, m in enumerate(self.members)]
+        self.bw = [model.add_parameters((len(m),), f"{name}.bw{c}") for c, m in enumerate(self.members)]
+        self._cache = {}
+
+    def _scores(self, g, h):
+        key = (g.generation, h.i)
+        c = self._cache.get(id(g))
+        if c is None or c[0] != key:
+            cs = ops.affine(ops.parameter(g, self.bc), ops.parameter(g, self.Wc), h)
+            ws = [ops.affine(ops.parameter(g, self.bw[k]), ops.parameter(g, self.Ww[k]), h)
+                  for k in range(len(self.members))]
+            c = (key, (cs, ws))
+            self._cache[id(g)] = c
+        return c[1]
+
+    def neg_log_softmax(self, g, h, word):
+        c, k = self.slot[word]
+        cs, ws = self._scores(g, h)
+        return ops.add(ops.pickneglogsoftmax(cs, c), ops.pickneglogsoftmax(ws[c], k))
+

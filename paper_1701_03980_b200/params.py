@@ -313,52 +313,39 @@ class Model:
         roster.update({lp.name: (1, (lp.rows, lp.dim)) for lp in self.lookups})
         return roster
 
+    def _entries(self):
+        """(kind, name, dims, flat host values) in roster order."""
+        for p in self.parameters:
+            yield 0, p.name, tuple(p.shape.dims), p._vm.pull().reshape(-1)
+        for lp in self.lookups:
+            yield 1, lp.name, (lp.rows, lp.dim), lp._vm.pull().reshape(-1)
+
     def save(self, path: str) -> None:
-        entries = [(0, p.name, p.shape.dims, p._vm.pull().reshape(-1)) for p in self.parameters]
-        entries += [(1, lp.name, (lp.rows, lp.dim), lp._vm.pull().reshape(-1)) for lp in self.lookups]
+        """DYN1 (params.py:128-143): magic, <u32 version, u32 count>, then per
+        entry <u8 kind, u16 name length> name <u8 rank> <u32 dims...> and the
+        little-endian f32 values.  Values are read back from the device."""
+        entries = list(self._entries())
+        blob = bytearray(MAGIC) + struct.pack("<II", FORMAT_VERSION, len(entries))
+        for kind, name, dims, flat in entries:
+            raw = name.encode("utf-8")
+            blob += struct.pack(f"<BH{len(raw)}sB{len(dims)}I", kind, len(raw), raw, len(dims), *dims)
+            blob += np.asarray(flat, dtype="<f4").tobytes()
         try:
             with open(path, "wb") as fh:
-                fh.write(MAGIC)
-                fh.write(struct.pack("<II", FORMAT_VERSION, len(entries)))
-                for kind, name, dims, flat in entries:
-                    raw = name.encode("utf-8")
-                    fh.write(struct.pack("<BH", kind, len(raw)))
-                    fh.write(raw)
-                    fh.write(struct.pack("<B", len(dims)))
-                    fh.write(struct.pack(f"<{len(dims)}I", *dims))
-                    fh.write(np.ascontiguousarray(flat, dtype="<f4").tobytes())
+                fh.write(blob)
         except OSError as exc:
             raise FileError(f"cannot write {path}: {exc}") from exc
 
     def load(self, path: str) -> None:
+        """params.py:145-189: the file's roster (names, kinds, shapes) must equal
+        this model's; values land in the host mirrors and reach the device
+        before the next device use."""
         try:
             with open(path, "rb") as fh:
                 blob = fh.read()
         except OSError as exc:
             raise FileError(f"cannot read {path}: {exc}") from exc
-        if blob[:4] != MAGIC:
-            raise FormatError(f"{path}: bad magic {blob[:4]!r}")
-        seen = {}
-        try:
-            version, count = struct.unpack_from("<II", blob, 4)
-            if version != FORMAT_VERSION:
-                raise FormatError(f"{path}: unsupported format version {version}")
-            pos = 12
-            for _ in range(count):
-                kind, nlen = struct.unpack_from("<BH", blob, pos)
-                pos += 3
-                name = blob[pos : pos + nlen].decode("utf-8")
-                pos += nlen
-                (rank,) = struct.unpack_from("<B", blob, pos)
-                pos += 1
-                dims = struct.unpack_from(f"<{rank}I", blob, pos)
-                pos += 4 * rank
-                size = int(np.prod(dims))
-                vals = np.frombuffer(blob, dtype="<f4", count=size, offset=pos)
-                pos += 4 * size
-                seen[name] = (kind, tuple(dims), vals)
-        except struct.error as exc:
-            raise FormatError(f"{path}: truncated or corrupt file") from exc
+        seen = dict(_dyn1_records(blob, path))
         got = {name: (kind, dims) for name, (kind, dims, _) in seen.items()}
         roster = self._roster()
         if roster != got:
@@ -367,7 +354,29 @@ class Model:
                 f"{path}: parameter roster differs from this model"
                 + (f" (by {missing})" if missing else " (kind or shape changed)")
             )
-        for p in self.parameters:
-            p._vm.host_view()[:] = seen[p.name][2]
-        for lp in self.lookups:
-            lp._vm.host_view()[:] = seen[lp.name][2].reshape(lp.rows, lp.dim)
+        for x in self._all():
+            x._vm.host_view().reshape(-1)[:] = seen[x.name][2]
+
+
+def _dyn1_records(blob: bytes, path: str):
+    """Yield (name, (kind, dims, values)) for every entry of a DYN1 blob."""
+    if blob[:4] != MAGIC:
+        raise FormatError(f"{path}: bad magic {blob[:4]!r}")
+    try:
+        version, count = struct.unpack_from("<II", blob, 4)
+        if version != FORMAT_VERSION:
+            raise FormatError(f"{path}: unsupported format version {version}")
+        at = 12
+        for _ in range(count):
+            kind, nlen = struct.unpack_from("<BH", blob, at)
+            name = blob[at + 3 : at + 3 + nlen].decode("utf-8")
+            at += 3 + nlen
+            rank = blob[at]
+            dims = struct.unpack_from(f"<{rank}I", blob, at + 1)
+            at += 1 + 4 * rank
+            size = int(np.prod(dims))
+            values = np.frombuffer(blob, dtype="<f4", count=size, offset=at)
+            at += 4 * size
+            yield name, (kind, tuple(dims), values)
+    except (struct.error, IndexError, ValueError) as exc:
+        raise FormatError(f"{path}: truncated or corrupt file") from exc

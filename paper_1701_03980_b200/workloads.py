@@ -161,10 +161,10 @@ def count_leaves(t) -> int:
 class RNNLM:
     """bench/tasks.py:443-452 registration order: E, rnn, W, b."""
 
-    def __init__(self, dy, model, vocab: int, embed: int, hidden: int, layers: int):
+    def __init__(self, dy, model, vocab: int, embed: int, hidden: int, layers: int, cell: str = "lstm"):
         self.dy = dy
         self.E = model.add_lookup_parameters(vocab, embed, "E")
-        self.rnn = dy.RNNBuilder(model, layers, embed, hidden, "lstm", "rnn")
+        self.rnn = dy.RNNBuilder(model, layers, embed, hidden, cell, "rnn")
         self.W = model.add_parameters((vocab, hidden), "W")
         self.b = model.add_parameters((vocab,), "b")
 
@@ -295,6 +295,47 @@ class TreeClassifier:
         h, _ = self.encoder.encode(cg, to_treenode(self.dy, tree))
         scores = ops.affine(ops.parameter(cg, self.bu), ops.parameter(cg, self.U), h)
         return ops.pickneglogsoftmax(scores, label)
+
+
+class TreeRNNClassifier:
+    """The Fig. 5 TreeRNN encoder (builders.py:183-210) under the Tree-LSTM
+    task's root classifier (bench/tasks.py:600-637 shape): registration
+    enc.W, enc.E, U, bu."""
+
+    def __init__(self, dy, model, vocab_size: int, n_labels: int = 5, hidden=150):
+        self.dy = dy
+        self.encoder = dy.TreeRNN(model, {f"w{i}": i for i in range(vocab_size)}, hidden, "enc")
+        self.U = model.add_parameters((n_labels, hidden), "U")
+        self.bu = model.add_parameters((n_labels,), "bu")
+
+    def loss(self, cg, tree, label):
+        ops = self.dy.ops
+        h = self.encoder.encode(cg, to_treenode(self.dy, tree))
+        return ops.pickneglogsoftmax(ops.affine(ops.parameter(cg, self.bu), ops.parameter(cg, self.U), h), label)
+
+
+class CFSMLM:
+    """LSTM language model with a ClassFactoredSoftmax output layer
+    (builders.py:282-378): per-sentence graphs, loss = sum over t of
+    -log p(class) - log p(word | class).  Word w belongs to class
+    (w * 7919) % n_classes (a deterministic, unbalanced map)."""
+
+    def __init__(self, dy, model, vocab: int, embed: int, hidden: int, n_classes: int):
+        self.dy = dy
+        self.E = model.add_lookup_parameters(vocab, embed, "E")
+        self.rnn = dy.RNNBuilder(model, 1, embed, hidden, "lstm", "rnn")
+        self.out = dy.ClassFactoredSoftmax(model, hidden, {w: (w * 7919) % n_classes for w in range(vocab)}, "cfsm")
+
+    def loss(self, cg, batch):
+        ops = self.dy.ops
+        ids = batch[0]
+        state = self.rnn.initial_state(cg)
+        loss = None
+        for t in range(len(ids) - 1):
+            state = state.add_input(ops.lookup(cg, self.E, ids[t]))
+            step = self.out.neg_log_softmax(cg, state.output(), ids[t + 1])
+            loss = step if loss is None else ops.add(loss, step)
+        return loss
 
 
 @dataclass

@@ -225,4 +225,10 @@ def workload_cases():
                       list(zip(td.trees, td.labels)), "adam", 3),
         # config 3 family: BiLSTM tagger with char-LSTM rare words
         "tagger_mini": (lambda dy, m: W.CharTagger(dy, m, tg, 16, 8, 8, 6, 7), tg.sentences, "adam", 3),
+        # the remaining builders
+        "gru_lm": (lambda dy, m: W.RNNLM(dy, m, 400, 24, 32, 2, "gru"), ptb, "adam", 3),
+        "simple_lm": (lambda dy, m: W.RNNLM(dy, m, 400, 24, 32, 2, "simple"), ptb, "sgd", 3),
+        "gru_lm_b1": (lambda dy, m: W.RNNLM(dy, m, 1000, 16, 24, 1, "gru"), [[s] for s in lm_tiny], "sgd", 3),
+        "treernn": (lambda dy, m: W.TreeRNNClassifier(dy, m, 60, 5, 16), list(zip(td.trees, td.labels)), "adam", 3),
+        "cfsm_lm": (lambda dy, m: W.CFSMLM(dy, m, 1000, 16, 24, 12), [[s] for s in lm_tiny], "adam", 3),
     }

@@ -44,9 +44,35 @@ def test_op_cases_match_reference(name):
     assert cg.pools.backward.alloc_count == ba
 
 
+# Named, measured exceptions to the plain rtol 1e-4 + 1e-6*max bar of the
+# golden workload traces.  simple_lm: a tanh RNN under SGD lr 0.1 whose
+# gradients grow to ~100 by step 2; the REFERENCE itself, run in fp32 vs fp64
+# from the same initial values, differs by up to 2.2e-4 (8e-6 of the scale,
+# above rtol 1e-4 on small elements) on rnn.l0.Wx at step 2 (measured with
+# the oracle, which equals the golden bit for bit).  For steps >= 1 of such a
+# case the band 2*|ref32 - ref64| is added, ref64 from the oracle in float64.
+F64_BAND_AFTER_STEP0 = {"simple_lm"}
+
+
+def _oracle_f64_grads(name):
+    make_task, data, rule, steps = cases.workload_cases()[name]
+    pools = orc.new_poolset(dtype=np.float64)
+    m = orc.Model(pools, seed=1, dtype=np.float64)
+    task, tr, out = make_task(orc, m), orc.Trainer(m, rule), []
+    for x in list(m.parameters) + list(m.lookups):  # start from the fp32 initial values
+        x.values[...] = np.asarray(x.values, dtype=np.float32)
+    for s in range(steps):
+        g = orc.ComputationGraph(pools)
+        g.backward(cases.call_loss(task, g, data[s]))
+        out.append({p.name: np.array(p.gradient, dtype=np.float64).reshape(-1) for p in m.parameters})
+        tr.update()
+    return out
+
+
 @pytest.mark.parametrize("name", sorted(cases.workload_cases()))
 def test_workload_traces_match_reference(name):
     make_task, data, rule, steps = cases.workload_cases()[name]
+    f64 = _oracle_f64_grads(name) if name in F64_BAND_AFTER_STEP0 else None
     dy, cg, model = gpu_ctx(seed=1, mb=256)
     task = make_task(dy, model)
     for p in model.parameters:
@@ -61,7 +87,8 @@ def test_workload_traces_match_reference(name):
         for p in model.parameters:
             key = f"{name}/grad{s}/{p.name}"
             if key in WL:
-                parity(pgrad(p), WL[key], what=key)
+                band = 2 * np.abs(WL[key].reshape(-1) - f64[s][p.name]) if f64 is not None and s > 0 else 0.0
+                parity(pgrad(p), WL[key], band=band, what=key)
         for lp in model.lookups:
             rows = WL[f"{name}/touched{s}/{lp.name}"]
             assert sorted(lp.touched) == list(rows), "touched set must be bit-exact"
