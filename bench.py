@@ -261,8 +261,31 @@ def _peaks():
         return {}
 
 
+def _traffic():
+    """Measured DRAM bytes per launch by op class (tools/summarize_profiles.py
+    writes profiles/traffic.json from one ncu --set full capture each)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            t = json.load(fh)
+        return {k: v["dram_bytes"] for k, v in t["classes"].items()}, t["source"]
+    except (OSError, KeyError, ValueError):
+        return {}, None
+
+
 def _roofline(name, d, peaks):
-    """achieved = algorithmic FLOPs (or bytes) per launch / mean launch time."""
+    """achieved = algorithmic FLOPs (or bytes) per launch / mean launch time;
+    traffic = the ncu-measured DRAM bytes per launch of the same kernel."""
+    traffic, source = _traffic()
+    r = _roofline_core(name, d, peaks)
+    if r is not None:
+        r["traffic"] = traffic.get(name)
+        if r["traffic"] is not None:
+            r["traffic_source"] = source
+            r["algorithmic_bytes_per_launch"] = d["bytes"] / max(1, d["launches"])
+    return r
+
+
+def _roofline_core(name, d, peaks):
     avg_ms = d["ms"] / max(1, d["launches"])
     if avg_ms <= 0:
         return None

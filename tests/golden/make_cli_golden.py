@@ -29,7 +29,11 @@ RUNS = {
     "rnnlm_mb4": ("rnnlm", 3, dict(sentences=40), ["--epochs", "2", "--trainer", "sgd", "--batch-size", "4"]),
     "tagger": ("tagger", 4, dict(sentences=30), ["--epochs", "2", "--trainer", "adam"]),
     "tagger-char": ("tagger-char", 5, dict(sentences=30), ["--epochs", "2", "--unk-threshold", "2"]),
-    "treelstm": ("treelstm", 6, dict(sentences=20), ["--epochs", "2", "--trainer", "adagrad"]),
+    # (not adagrad: with the reference's eps = 1e-20 the first AdaGrad step is
+    # lr * sign(g) even for rounding-level gradients, so a +-1e-9 gradient
+    # element that cancels differently under another summation order moves a
+    # weight by +-0.1; the AdaGrad kernel has its own known-answer test)
+    "treelstm": ("treelstm", 6, dict(sentences=20), ["--epochs", "2", "--trainer", "adam"]),
     "pairclass": ("pairclass", 7, dict(sentences=60), ["--epochs", "3", "--trainer", "sgd", "--seed", "5"]),
     "pairclass_mb8": ("pairclass", 7, dict(sentences=60), ["--epochs", "2", "--trainer", "momentum",
                                                            "--batch-size", "8"]),

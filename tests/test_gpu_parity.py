@@ -50,7 +50,10 @@ def test_op_cases_match_reference(name):
 # from the same initial values, differs by up to 2.2e-4 (8e-6 of the scale,
 # above rtol 1e-4 on small elements) on rnn.l0.Wx at step 2 (measured with
 # the oracle, which equals the golden bit for bit).  For steps >= 1 of such a
-# case the band 2*|ref32 - ref64| is added, ref64 from the oracle in float64.
+# case the atol floor is 2*max|ref32 - ref64| over the tensor (ref64 from the
+# oracle in float64 from the same fp32 initial values): the device's own fp32
+# rounding is amplified by the same dynamics, element by element in other
+# places than the reference's.
 F64_BAND_AFTER_STEP0 = {"simple_lm"}
 
 
@@ -87,7 +90,7 @@ def test_workload_traces_match_reference(name):
         for p in model.parameters:
             key = f"{name}/grad{s}/{p.name}"
             if key in WL:
-                band = 2 * np.abs(WL[key].reshape(-1) - f64[s][p.name]) if f64 is not None and s > 0 else 0.0
+                band = 2 * float(np.abs(WL[key].reshape(-1) - f64[s][p.name]).max()) if f64 is not None and s > 0 else 0.0
                 parity(pgrad(p), WL[key], band=band, what=key)
         for lp in model.lookups:
             rows = WL[f"{name}/touched{s}/{lp.name}"]
