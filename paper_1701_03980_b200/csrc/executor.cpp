@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -71,6 +72,9 @@ struct Param {
 
 static std::mutex g_param_mu;
 static std::vector<Param> g_params;
+// bumped whenever a parameter's device storage may move: cached plans embed
+// parameter pointers, so it is part of their key
+static std::atomic<uint64_t> g_param_epoch{1};
 
 static Param* param_at(int64_t h) {
   if (h < 0 || h >= (int64_t)g_params.size() || !g_params[h].alive) return nullptr;
@@ -211,6 +215,7 @@ struct dg_graph_impl;
 
 namespace dg {
 struct Schedule;
+struct CachedPlan;
 }
 
 struct dg_graph {
@@ -261,6 +266,12 @@ struct dg_graph {
   size_t blob_hint[2] = {1 << 20, 4 << 20};  // forward / backward table blob sizes seen
   bool has_grads = false;  // any backward in this generation
   bool counters_ready = false;  // split-K tile counters zeroed (first launch)
+  // launch-plan cache (per graph object: plans embed its arena addresses and
+  // stream): [0] forward plans, [1] backward plans, most recent first
+  std::vector<std::shared_ptr<dg::CachedPlan>> pcache[2];
+  mutable uint64_t memo_key = 0;   // structure hash of memo_sched
+  uint64_t fwd_hist = 0;   // forward calls of this generation (placement history)
+  cudaStream_t cap_stream = nullptr;  // CUDA-graph capture of cached plans
 };
 
 struct dg_trainer {
@@ -1095,7 +1106,8 @@ static std::shared_ptr<const Schedule> get_schedule(const dg_graph* g, const std
     return !(e && e[0] == '0');
   }();
   if (g->memo_sched && g->memo_scope == scope_hi && g->memo_active == active) return g->memo_sched;
-  const uint64_t key = on ? structure_hash(g, active, scope_hi) : 0;
+  const uint64_t key = structure_hash(g, active, scope_hi);
+  g->memo_key = key;
   if (on) {
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);
@@ -1141,6 +1153,55 @@ struct Plan {
   void tag(int cls, double flops, double bytes) {
     meta.resize(ops.size());
     meta.back() = OpMeta{cls, flops, bytes};
+  }
+};
+
+// The data-dependent part of a plan's table blob: input payloads, lookup
+// ids and pickneglogsoftmax labels.  Everything else in a plan (schedule,
+// placement, row-pointer tables, launch configurations, TMA descriptors) is
+// a function of the graph's structure hash, the arena cursors and the
+// parameter storage, so a plan built once is replayed for every later graph
+// of the same structure with only these entries rewritten.
+struct PatchRec {
+  struct Payload {
+    int node;
+    size_t off, bytes;
+  };
+  struct Ids {
+    int node, q0, width;  // aux_i[ai_off + q0 .. ai_off + ai_len) as int64 (8) or int32 (4)
+    size_t off;
+  };
+  std::vector<Payload> payload;
+  std::vector<Ids> ids;
+};
+static thread_local PatchRec* g_rec = nullptr;  // recorder of the plan being built
+// stream the launch closures issue into: the graph's stream, or the private
+// capture stream while a cached plan is recorded into a CUDA graph
+static thread_local cudaStream_t g_launch_stream = nullptr;
+
+struct RecScope {
+  explicit RecScope(PatchRec* r) { g_rec = r; }
+  ~RecScope() { g_rec = nullptr; }
+};
+
+static void rec_payload(int node, size_t off, size_t bytes) {
+  if (g_rec) g_rec->payload.push_back({node, off, bytes});
+}
+static void rec_ids(int node, int q0, int width, size_t off) {
+  if (g_rec) g_rec->ids.push_back({node, q0, width, off});
+}
+
+struct CachedPlan {
+  uint64_t key = 0;
+  std::vector<uint8_t> tmpl;  // blob bytes of the static part
+  std::vector<std::function<int(char*)>> ops;
+  std::vector<OpMeta> meta;
+  PatchRec patch;
+  int64_t kernel_launches = 0;  // launches issued by `ops` (counted at build)
+  cudaGraphExec_t exec = nullptr;
+  int replays = 0;
+  ~CachedPlan() {
+    if (exec) cudaGraphExecDestroy(exec);
   }
 };
 
@@ -1321,7 +1382,6 @@ static void flush_gemm(dg_graph* g, Plan& plan, GemmBatch& gb) {
   const int64_t temp = (gb.temp_floats + 63) & ~int64_t(63);
   float* work = reinterpret_cast<float*>(scratch_base(g)) + temp;
   const int64_t cap = (int64_t)(scratch_bytes(g) / 4) - temp;
-  cudaStream_t st = g->stream;
   // dense wide problems: TMA + warp-specialised tcgen05; problems of the batch
   // that share a kernel and write disjoint outputs go up to kTmaGroup per
   // launch with one split factor (small weight-gradient GEMMs fill a wave
@@ -1354,7 +1414,8 @@ static void flush_gemm(dg_graph* g, Plan& plan, GemmBatch& gb) {
     }
     if (grp.size() == 1) {
       const TmaGemmPlan tp = tmas[i].first;
-      plan.ops.push_back([tp, st](char*) { return launch_tma_gemm(tp, true, true, st); });
+      plan.ops.push_back([tp](char*) {
+      const cudaStream_t st = g_launch_stream; return launch_tma_gemm(tp, true, true, st); });
       plan.tag(gb.cls, tp.flops, tmas[i].second);
       continue;
     }
@@ -1368,7 +1429,8 @@ static void flush_gemm(dg_graph* g, Plan& plan, GemmBatch& gb) {
     std::vector<TmaGemmPlan*> pp;
     for (auto& x : ps) pp.push_back(&x);
     tma_gemm_regroup(pp.data(), (int)pp.size());
-    plan.ops.push_back([ps, st](char*) {
+    plan.ops.push_back([ps](char*) {
+      const cudaStream_t st = g_launch_stream;
       const TmaGemmPlan* arr[kTmaGroup];
       for (size_t q = 0; q < ps.size(); ++q) arr[q] = &ps[q];
       return launch_tma_gemm_group(arr, (int)ps.size(), st);
@@ -1404,7 +1466,8 @@ static void flush_gemm(dg_graph* g, Plan& plan, GemmBatch& gb) {
   const size_t off = plan.blob.push(rest);
   const GemmProblem* pdev = dev_at<GemmProblem>(g, off);
   int* counters = counter_base(g);
-  plan.ops.push_back([L, pdev, work, counters, st, post, tc](char*) {
+  plan.ops.push_back([L, pdev, work, counters, post, tc](char*) {
+      const cudaStream_t st = g_launch_stream;
     int n = tc ? launch_tc_gemm(L, pdev, st) : launch_gemm_group(L, pdev, work, counters, st);
     for (auto& f : post) n += f();
     return n;
@@ -1451,6 +1514,7 @@ int dg_param_register(int kind, int64_t rows, int64_t cols, float* values, float
   if (kind == 1) p.touched_bits.assign(rows, 0);
   g_params.push_back(std::move(p));
   *handle = (int64_t)g_params.size() - 1;
+  g_param_epoch++;
   return DG_OK;
 }
 
@@ -1460,6 +1524,7 @@ int dg_param_rebind(int64_t h, float* values, float* grad) {
   if (!p) return fail(DG_INDEX, "unknown parameter handle");
   p->val = values;
   p->grad = grad;
+  g_param_epoch++;
   return DG_OK;
 }
 
@@ -1468,6 +1533,7 @@ int dg_param_release(int64_t h) {
   Param* p = param_at(h);
   if (!p) return fail(DG_INDEX, "unknown parameter handle");
   p->alive = false;
+  g_param_epoch++;
   p->touched_bits.clear();
   p->touched_list.clear();
   if (p->dp_dev) cudaFree(p->dp_dev);  // best effort (may run at interpreter exit)
@@ -1532,6 +1598,9 @@ int dg_graph_create(int device, void* fwd_base, size_t fwd_bytes, void* bwd_base
 
 int dg_graph_destroy(dg_graph* g) {
   if (!g) return DG_OK;
+  g->pcache[0].clear();
+  g->pcache[1].clear();
+  if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
   if (g->vcache_ev) {
     cudaEventSynchronize(g->vcache_ev);
     cudaEventDestroy(g->vcache_ev);
@@ -1564,6 +1633,7 @@ int dg_graph_renew(dg_graph* g) {
   g->fwd_cursor = 0;
   g->bwd_cursor = 0;
   g->has_grads = false;
+  g->fwd_hist = 0;
   return DG_OK;
 }
 
@@ -1625,20 +1695,14 @@ static bool dry_run() {
   return on;
 }
 
-static int launch_plan(dg_graph* g, Plan& plan) {
-  const size_t blob_bytes = (plan.blob.size() + 255) & ~size_t(255);
-  if (blob_bytes > blob_cap(g)) return fail(DG_CONFIG, "plan tables exceed the workspace");
-  if (dry_run()) return DG_OK;
-  if (!g->counters_ready) {
-    // split-K tile counters start (and are always left) at zero
-    DG_CUDA_TRY(cudaMemsetAsync(g->work_base + g->work_bytes - (1u << 20), 0, 1u << 20, g->stream));
-    g->counters_ready = true;
-  }
-  int rc = upload(g, plan.blob, g->work_base);
-  if (rc) return rc;
-  plan.meta.resize(plan.ops.size());
-  for (size_t q = 0; q < plan.ops.size(); ++q) {
-    const OpMeta& mt = plan.meta[q];
+// run launch closures in order (with CUDA events around the profiled op
+// classes); adds the kernel launches issued to *launched
+static int run_ops(dg_graph* g, std::vector<std::function<int(char*)>>& ops, std::vector<OpMeta>& meta,
+                   int64_t* launched, cudaStream_t stream) {
+  g_launch_stream = stream;
+  meta.resize(ops.size());
+  for (size_t q = 0; q < ops.size(); ++q) {
+    const OpMeta& mt = meta[q];
     const bool prof = (g->prof_mask >> mt.cls) & 1u;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (prof) {
@@ -1657,12 +1721,12 @@ static int launch_plan(dg_graph* g, Plan& plan) {
       return e && e[0] == '2';
     }();
     const auto t_op = std::chrono::steady_clock::now();
-    int n = plan.ops[q](g->work_base);
+    int n = ops[q](g->work_base);
     if (op_timing)
       std::fprintf(stderr, "[op] class %d launches %d host %.1f us\n", mt.cls, n,
                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_op).count());
     if (n < 0) return fail(DG_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(cudaGetLastError()));
-    g->launches += n;
+    *launched += n;
     if (prof) {
       DG_CUDA_TRY(cudaEventRecord(e1, g->stream));
       g->prof_pending[mt.cls].push_back({e0, e1});
@@ -1676,6 +1740,151 @@ static int launch_plan(dg_graph* g, Plan& plan) {
   return DG_OK;
 }
 
+static int prepare_launch(dg_graph* g, const Blob& blob) {
+  const size_t blob_bytes = (blob.size() + 255) & ~size_t(255);
+  if (blob_bytes > blob_cap(g)) return fail(DG_CONFIG, "plan tables exceed the workspace");
+  if (dry_run()) return DG_OK;
+  if (!g->counters_ready) {
+    // split-K tile counters start (and are always left) at zero
+    DG_CUDA_TRY(cudaMemsetAsync(g->work_base + g->work_bytes - (1u << 20), 0, 1u << 20, g->stream));
+    g->counters_ready = true;
+  }
+  return upload(g, blob, g->work_base);
+}
+
+static int launch_plan(dg_graph* g, Plan& plan, int64_t* launched = nullptr) {
+  int rc = prepare_launch(g, plan.blob);
+  if (rc || dry_run()) return rc;
+  int64_t n = 0;
+  rc = run_ops(g, plan.ops, plan.meta, &n, g->stream);
+  g->launches += n;
+  if (launched) *launched = n;
+  return rc;
+}
+
+static bool plan_cache_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("DG_PLAN_CACHE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static bool cuda_graphs_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("DG_CUDA_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static uint64_t mix64(uint64_t h, uint64_t v) {
+  h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  return h * 0xff51afd7ed558ccdull;
+}
+
+// key of a plan: structure, the node range, the placement history of this
+// generation, arena cursors, parameter storage epoch, stream
+static uint64_t plan_key(const dg_graph* g, int which, int lo, int hi) {
+  uint64_t h = mix64(g->memo_key, (uint64_t)which);
+  h = mix64(h, (uint64_t)(uint32_t)lo);
+  h = mix64(h, (uint64_t)(uint32_t)hi);
+  h = mix64(h, g->fwd_hist);
+  h = mix64(h, (uint64_t)g->fwd_cursor);
+  h = mix64(h, (uint64_t)g->bwd_cursor);
+  h = mix64(h, g_param_epoch.load());
+  h = mix64(h, (uint64_t)reinterpret_cast<uintptr_t>(g->stream));
+  return h;
+}
+
+static CachedPlan* plan_cache_find(dg_graph* g, int which, uint64_t key) {
+  if (!plan_cache_on()) return nullptr;
+  auto& v = g->pcache[which];
+  for (size_t i = 0; i < v.size(); ++i)
+    if (v[i]->key == key) {
+      if (i) std::rotate(v.begin(), v.begin() + i, v.begin() + i + 1);
+      return v[0].get();
+    }
+  return nullptr;
+}
+
+// keep a freshly launched plan (its closures move into the cache)
+static void plan_cache_store(dg_graph* g, int which, uint64_t key, Plan& plan, size_t static_ops,
+                             size_t static_bytes, PatchRec&& rec, int64_t launched_static) {
+  if (!plan_cache_on() || dry_run()) return;
+  auto cp = std::make_shared<CachedPlan>();
+  cp->key = key;
+  cp->tmpl.assign(plan.blob.data(), plan.blob.data() + static_bytes);
+  plan.meta.resize(plan.ops.size());
+  cp->ops.assign(std::make_move_iterator(plan.ops.begin()), std::make_move_iterator(plan.ops.begin() + static_ops));
+  cp->meta.assign(plan.meta.begin(), plan.meta.begin() + static_ops);
+  cp->patch = std::move(rec);
+  cp->kernel_launches = launched_static;
+  auto& v = g->pcache[which];
+  v.insert(v.begin(), std::move(cp));
+  if (v.size() > 8) v.pop_back();
+}
+
+// blob for a cached plan: the template with this graph's data written in
+static void blob_from_template(const dg_graph* g, const CachedPlan& cp, Blob& B) {
+  B.push_bytes(cp.tmpl.data(), cp.tmpl.size(), 16);
+  uint8_t* d = B.data();
+  for (const PatchRec::Payload& p : cp.patch.payload)
+    std::memcpy(d + p.off, g->aux_f.data() + g->nodes[p.node].af_off, p.bytes);
+  for (const PatchRec::Ids& r : cp.patch.ids) {
+    const Node& x = g->nodes[r.node];
+    const int64_t* src = g->aux_i.data() + x.ai_off + r.q0;
+    const int64_t n = x.ai_len - r.q0;
+    if (r.width == 8) {
+      std::memcpy(d + r.off, src, (size_t)n * 8);
+    } else {
+      int32_t* o = reinterpret_cast<int32_t*>(d + r.off);
+      for (int64_t q = 0; q < n; ++q) o[q] = (int32_t)src[q];
+    }
+  }
+}
+
+// upload the blob, replay the cached static ops (as a CUDA graph from the
+// second use on), then the per-call tail ops of `tail`
+static int launch_cached(dg_graph* g, CachedPlan& cp, Plan& tail) {
+  int rc = prepare_launch(g, tail.blob);
+  if (rc || dry_run()) return rc;
+  bool profiling = false;
+  for (const OpMeta& m : cp.meta) profiling = profiling || ((g->prof_mask >> m.cls) & 1u);
+  int64_t n = 0;
+  if (cuda_graphs_on() && !profiling && cp.replays >= 1 && !cp.exec && cp.replays != -1000) {
+    // recorded on a private non-blocking stream (the graph's own stream may
+    // be the legacy default stream, which cannot be captured); replayed on
+    // the graph's stream
+    if (!g->cap_stream) DG_CUDA_TRY(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
+    cudaGraph_t graph = nullptr;
+    bool ok = cudaStreamBeginCapture(g->cap_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    int64_t n_cap = 0;
+    int rc_cap = ok ? run_ops(g, cp.ops, cp.meta, &n_cap, g->cap_stream) : DG_CUDA;
+    ok = cudaStreamEndCapture(g->cap_stream, &graph) == cudaSuccess && ok && rc_cap == DG_OK;
+    if (ok) ok = cudaGraphInstantiateWithFlags(&cp.exec, graph, 0) == cudaSuccess;
+    if (graph) cudaGraphDestroy(graph);
+    if (!ok) {
+      cudaGetLastError();  // capture unsupported for this plan: replay op by op
+      cp.exec = nullptr;
+      cp.replays = -1000;
+    }
+  }
+  g->stats[5]++;  // plan-cache hits (cumulative)
+  if (cp.exec && !profiling) {
+    DG_CUDA_TRY(cudaGraphLaunch(cp.exec, g->stream));
+    n += cp.kernel_launches;
+    g->stats[6]++;  // CUDA-graph replays (cumulative)
+  } else {
+    rc = run_ops(g, cp.ops, cp.meta, &n, g->stream);
+    if (rc) return rc;
+  }
+  if (cp.replays >= 0) cp.replays++;
+  rc = run_ops(g, tail.ops, tail.meta, &n, g->stream);
+  g->launches += n;
+  return rc;
+}
+
 // scratch region of the workspace (after the table blob half)
 
 
@@ -1685,7 +1894,6 @@ static int launch_plan(dg_graph* g, Plan& plan) {
 static void push_dx_problem(dg_graph* g, Plan& plan, GemmBatch& batch, const float* const* g_rows_dev, bool g_al,
                             const float* W, int m, int K, const std::vector<uintptr_t>& dxrows) {
   Blob& B = plan.blob;
-  const cudaStream_t st = g->stream;
   const bool dup = has_duplicate_rows(dxrows);
   GemmProblem pr{};
   pr.M = (int)dxrows.size();
@@ -1726,7 +1934,9 @@ static void push_dx_problem(dg_graph* g, Plan& plan, GemmBatch& batch, const flo
         const_cast<float* const*>(reinterpret_cast<const float* const*>(dev_at<float*>(g, B.push(tgt))));
     const int* sg = dev_at<int>(g, B.push(seg));
     const int n_t = (int)tgt.size();
-    batch.post.push_back([tg, sg, temp, n_t, K, st]() { return launch_row_reduce_scatter(tg, sg, temp, n_t, K, st); });
+    batch.post.push_back([tg, sg, temp, n_t, K]() {
+      return launch_row_reduce_scatter(tg, sg, temp, n_t, K, g_launch_stream);
+    });
   }
   batch.probs.push_back(pr);
 }
@@ -1740,7 +1950,6 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
                            std::unordered_map<int64_t, AffineUse>* wuse,
                            std::unordered_map<int64_t, std::vector<uintptr_t>>* buse, GemmBatch* gb) {
   Blob& B = plan.blob;
-  const cudaStream_t st = g->stream;
   // pack
   std::vector<std::vector<int>> launches;
   {
@@ -1906,7 +2115,8 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
       }
     }
     use_cl = use_cl && smem_cl <= kSmemMax;
-    plan.ops.push_back([a, smem, smem_cl, use_cl, cl, bwd, st](char*) {
+    plan.ops.push_back([a, smem, smem_cl, use_cl, cl, bwd](char*) {
+      const cudaStream_t st = g_launch_stream;
       if (use_cl) {
         const int n = launch_rnn_cluster(a, bwd, smem_cl, cl, st);
         if (n != -2) return n;  // -2: the clusters cannot all be resident
@@ -1987,7 +2197,8 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
       const Node& cpn = g->nodes[cp.cells[0].ins[1]];
       if (cpn.batch == 1 && Bt > 1) {
         if (c0.n == kRnnMaxChains) {
-          plan.ops.push_back([c0, st](char*) { return launch_rnn_c0(c0, st); });
+          plan.ops.push_back([c0](char*) {
+      const cudaStream_t st = g_launch_stream; return launch_rnn_c0(c0, st); });
           plan.tag(C_ELEMWISE, 0.0, 0.0);
           c0 = RnnC0{};
         }
@@ -2002,7 +2213,8 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
   }
   flush_gemm(g, plan, *gb);
   if (c0.n) {
-    plan.ops.push_back([c0, st](char*) { return launch_rnn_c0(c0, st); });
+    plan.ops.push_back([c0](char*) {
+      const cudaStream_t st = g_launch_stream; return launch_rnn_c0(c0, st); });
     plan.tag(C_ELEMWISE, 0.0, 0.0);
   }
 }
@@ -2037,7 +2249,6 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
   for (int u : gr.units) nodes.push_back(S.units[u].last());
   const int n = (int)nodes.size();
   const Node& n0 = g->nodes[nodes[0]];
-  const cudaStream_t st = g->stream;
   if (!(gr.kind == DG_OP_AFFINE && affine_gemm_ok(g, n0))) flush_gemm(g, plan, gb);
 
   if (gr.kind == -3) {  // persistent LSTM stacks
@@ -2068,7 +2279,8 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
       for (int x : u.nodes) vals[(size_t)(s++) * n + j] = P(g->nodes[x].val);
     }
     const size_t ov = B.push(vals);
-    plan.ops.push_back([a, ov, st](char* d) mutable {
+    plan.ops.push_back([a, ov](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
       a.val = at<const float* const>(d, ov);
       return launch_cell_fwd(a, st);
     });
@@ -2088,7 +2300,8 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
     a.n = n;
     a.len = len;
     a.size = (int)n0.size();
-    plan.ops.push_back([a, oi, oo, st](char* d) mutable {
+    plan.ops.push_back([a, oi, oo](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
       a.ins = at<const float* const>(d, oi);
       a.outs = at<float* const>(d, oo);
       return launch_chain_fwd(a, st);
@@ -2126,7 +2339,8 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
       }
       const size_t oo = B.push(outs);
       const bool binary = n0.n_in > 1;
-      plan.ops.push_back([a, oa, ob, oo, binary, st](char* d) mutable {
+      plan.ops.push_back([a, oa, ob, oo, binary](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
         a.a = at<const float* const>(d, oa);
         a.b = binary ? at<const float* const>(d, ob) : nullptr;
         a.out = at<float* const>(d, oo);
@@ -2143,7 +2357,8 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
       a.lo = (int)g->aux_i[n0.ai_off];
       a.width = (int)n0.elem;
       const size_t oi = B.push(in_vals(0)), oo = B.push(outs);
-      plan.ops.push_back([a, oi, oo, st](char* d) mutable {
+      plan.ops.push_back([a, oi, oo](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
         a.in = at<const float* const>(d, oi);
         a.out = at<float* const>(d, oo);
         return launch_pick_fwd(a, st);
@@ -2164,7 +2379,8 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
         std::copy(v.begin(), v.end(), ins.begin() + (size_t)k * n);
       }
       const size_t of = B.push(offs), oi = B.push(ins), oo = B.push(outs);
-      plan.ops.push_back([a, of, oi, oo, st](char* d) mutable {
+      plan.ops.push_back([a, of, oi, oo](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
         a.offs = at<const int>(d, of);
         a.in = at<const float* const>(d, oi);
         a.out = at<float* const>(d, oo);
@@ -2178,7 +2394,8 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
       a.batch = in0.batch;
       a.elem = (int)in0.elem;
       const size_t oi = B.push(in_vals(0)), oo = B.push(outs);
-      plan.ops.push_back([a, oi, oo, st](char* d) mutable {
+      plan.ops.push_back([a, oi, oo](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
         a.in = at<const float* const>(d, oi);
         a.out = at<float* const>(d, oo);
         return launch_sum_batches_fwd(a, st);
@@ -2203,8 +2420,10 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
           for (int64_t q = 0; q < x.ai_len; ++q) labels.push_back((int32_t)g->aux_i[x.ai_off + q]);
         }
         ol = B.push(labels);
+        for (int j = 0, k = 0; j < n; k += (int)g->nodes[nodes[j]].ai_len, ++j) rec_ids(nodes[j], 0, 4, ol + 4 * k);
       }
-      plan.ops.push_back([a, oi, oo, ol, pnls, st](char* d) mutable {
+      plan.ops.push_back([a, oi, oo, ol, pnls](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
         a.in = at<const float* const>(d, oi);
         a.out = at<float* const>(d, oo);
         if (pnls) {
@@ -2227,7 +2446,8 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
       a.a_b1 = in0.batch == 1 && n0.batch > 1;
       a.x_b1 = x.batch == 1 && n0.batch > 1;
       const size_t oa = B.push(in_vals(0)), ox = B.push(in_vals(1)), oo = B.push(outs);
-      plan.ops.push_back([a, oa, ox, oo, st](char* d) mutable {
+      plan.ops.push_back([a, oa, ox, oo](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
         a.a = at<const float* const>(d, oa);
         a.x = at<const float* const>(d, ox);
         a.out = at<float* const>(d, oo);
@@ -2308,7 +2528,8 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
           }
         }
         const size_t ob = B.push(in_vals(0)), ow = B.push(w), ox = B.push(x), oo = B.push(outs);
-        plan.ops.push_back([a, ob, ow, ox, oo, st](char* d) mutable {
+        plan.ops.push_back([a, ob, ow, ox, oo](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
           a.bias = at<const float* const>(d, ob);
           a.w = at<const float* const>(d, ow);
           a.x = at<const float* const>(d, ox);
@@ -2322,6 +2543,8 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
       return;
   }
 }
+
+static int finish_forward(dg_graph* g, const Schedule& S, int lo, int upto, size_t cur, uint64_t pkey);
 
 static int do_forward(dg_graph* g, int upto) {
   const int lo = g->watermark + 1;
@@ -2366,6 +2589,21 @@ static int do_forward(dg_graph* g, int upto) {
     for (int u : gr.units)
       for (int i : S.units[u].nodes) place(i);
 
+  const uint64_t pkey = plan_key(g, 0, lo, upto);
+  if (CachedPlan* hit = plan_cache_find(g, 0, pkey)) {
+    // same structure as an earlier graph: its plan with this graph's data
+    Plan tail;
+    int rc = blob_attach(tail.blob, hit->tmpl.size());
+    if (rc) return rc;
+    blob_from_template(g, *hit, tail.blob);
+    tm.lap("cached");
+    rc = launch_cached(g, *hit, tail);
+    if (rc) return rc;
+    tm.lap("launch");
+    return finish_forward(g, S, lo, upto, cur, pkey);
+  }
+  PatchRec rec;
+  RecScope rec_scope(&rec);
   Plan plan;
   {
     const int rc0 = blob_attach(plan.blob, g->blob_hint[0]);  // no regrowth copies while planning
@@ -2382,20 +2620,25 @@ static int do_forward(dg_graph* g, int upto) {
       std::memcpy(block.data() + off, g->aux_f.data() + x.af_off, (size_t)x.size() * 4);
     }
     in_blob = B.push_bytes(block.data(), block.size(), 64);
+    for (int i : S.input_nodes)
+      rec_payload(i, in_blob + (reinterpret_cast<char*>(g->nodes[i].val) - (g->fwd_base + in_begin)),
+                  (size_t)g->nodes[i].size() * 4);
     char* dst = g->fwd_base + in_begin;
     const size_t nbytes = in_end - in_begin;
-    cudaStream_t st = g->stream;
-    plan.ops.push_back([dst, in_blob, nbytes, st](char* d) {
+    plan.ops.push_back([dst, in_blob, nbytes](char* d) {
+      const cudaStream_t st = g_launch_stream;
       return cudaMemcpyAsync(dst, d + in_blob, nbytes, cudaMemcpyDeviceToDevice, st) == cudaSuccess ? 0 : -1;
     });
   }
   // lookups: one gather per table
   {
     std::unordered_map<int64_t, std::pair<std::vector<int64_t>, std::vector<uintptr_t>>> by_table;
+    std::unordered_map<int64_t, std::vector<int>> nodes_of;
     std::vector<int64_t> order;
     for (int i : S.lookup_nodes) {
       const Node& x = g->nodes[i];
       const int64_t h = g->aux_i[x.ai_off];
+      nodes_of[h].push_back(i);
       auto it = by_table.find(h);
       if (it == by_table.end()) {
         order.push_back(h);
@@ -2411,11 +2654,18 @@ static int do_forward(dg_graph* g, int upto) {
       Param* p = param_at(h);
       auto& pr = by_table[h];
       const size_t oid = B.push(pr.first), orow = B.push(pr.second);
+      {
+        size_t k = 0;
+        for (int i : nodes_of[h]) {
+          rec_ids(i, 1, 8, oid + 8 * k);
+          k += (size_t)g->nodes[i].ai_len - 1;
+        }
+      }
       const float* table = p->val;
       const int dim = (int)p->cols;
       const int rows = (int)pr.first.size();
-      cudaStream_t st = g->stream;
-      plan.ops.push_back([table, dim, oid, orow, rows, st](char* d) {
+      plan.ops.push_back([table, dim, oid, orow, rows](char* d) {
+      const cudaStream_t st = g_launch_stream;
         return launch_gather_rows(table, dim, at<const int64_t>(d, oid), at<float* const>(d, orow), rows, st);
       });
       plan.tag(C_GATHER, 0.0, 8.0 * rows * dim + 8.0 * rows);
@@ -2429,9 +2679,16 @@ static int do_forward(dg_graph* g, int upto) {
   }
   tm.lap("groups");
   g->blob_hint[0] = std::max(g->blob_hint[0], plan.blob.size() + plan.blob.size() / 4);
-  int rc = launch_plan(g, plan);
+  int64_t launched = 0;
+  int rc = launch_plan(g, plan, &launched);
   if (rc) return rc;
   tm.lap("launch");
+  plan_cache_store(g, 0, pkey, plan, plan.ops.size(), plan.blob.size(), std::move(rec), launched);
+  return finish_forward(g, S, lo, upto, cur, pkey);
+}
+
+// bookkeeping after a forward's launches (planned or cached)
+static int finish_forward(dg_graph* g, const Schedule& S, int lo, int upto, size_t cur, uint64_t pkey) {
   {
     const Node& tn = g->nodes[upto];
     g->vcache_node = -1;
@@ -2463,6 +2720,7 @@ static int do_forward(dg_graph* g, int upto) {
   g->stats[0] = (int64_t)S.groups.size();
   g->stats[1] = (int64_t)S.units.size();
   g->stats[2] = (int64_t)(upto - lo + 1);
+  g->fwd_hist = mix64(g->fwd_hist, pkey);
   return DG_OK;
 }
 
@@ -2482,7 +2740,6 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
     plan_rnn_group(g, S, gr, plan, true, &wuse, &buse, &gb);
     return;
   }
-  const cudaStream_t st = g->stream;
   std::vector<int> all_nodes;
   for (int u : gr.units) all_nodes.push_back(S.units[u].last());
   const Node& n0 = g->nodes[all_nodes[0]];
@@ -2550,7 +2807,8 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
         }
       }
       const size_t ov = B.push(vals), og = B.push(grads);
-      plan.ops.push_back([a, ov, og, st](char* d) mutable {
+      plan.ops.push_back([a, ov, og](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
         a.val = at<const float* const>(d, ov);
         a.grad = at<float* const>(d, og);
         return launch_cell_bwd(a, st);
@@ -2601,7 +2859,8 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
             a.distinct = has_duplicate_rows(all) ? 0 : 1;
           }
           const size_t og = B.push(gout), ogi = B.push(gins), ogo = B.push(gouts);
-          plan.ops.push_back([a, og, ogi, ogo, st](char* d) mutable {
+          plan.ops.push_back([a, og, ogi, ogo](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
             a.gfinal = at<const float* const>(d, og);
             a.gins = at<float* const>(d, ogi);
             a.gouts = at<float* const>(d, ogo);
@@ -2630,7 +2889,8 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
             ogb = B.push(gin(1));
           }
           const size_t ogo = B.push(gout), oov = B.push(oval);
-          plan.ops.push_back([a, oa, oga, ob, ogb, ogo, oov, binary, st](char* d) mutable {
+          plan.ops.push_back([a, oa, oga, ob, ogb, ogo, oov, binary](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
             a.a = at<const float* const>(d, oa);
             a.ga = at<float* const>(d, oga);
             if (binary) {
@@ -2652,7 +2912,8 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
           a.lo = (int)g->aux_i[n0.ai_off];
           a.width = (int)n0.elem;
           const size_t og = B.push(gout), oi = B.push(gin(0));
-          plan.ops.push_back([a, og, oi, st](char* d) mutable {
+          plan.ops.push_back([a, og, oi](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
             a.gout = at<const float* const>(d, og);
             a.gin = at<float* const>(d, oi);
             return launch_pick_bwd(a, st);
@@ -2673,7 +2934,8 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
             std::copy(v.begin(), v.end(), gins.begin() + (size_t)k * n);
           }
           const size_t of = B.push(offs), og = B.push(gout), oi = B.push(gins);
-          plan.ops.push_back([a, of, og, oi, st](char* d) mutable {
+          plan.ops.push_back([a, of, og, oi](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
             a.offs = at<const int>(d, of);
             a.gout = at<const float* const>(d, og);
             a.gin = at<float* const>(d, oi);
@@ -2687,7 +2949,8 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
           a.batch = in0.batch;
           a.elem = (int)in0.elem;
           const size_t og = B.push(gout), oi = B.push(gin(0));
-          plan.ops.push_back([a, og, oi, st](char* d) mutable {
+          plan.ops.push_back([a, og, oi](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
             a.gout = at<const float* const>(d, og);
             a.gin = at<float* const>(d, oi);
             return launch_sum_batches_bwd(a, st);
@@ -2712,9 +2975,11 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
               for (int64_t q = 0; q < x.ai_len; ++q) labels.push_back((int32_t)g->aux_i[x.ai_off + q]);
             }
             ol = B.push(labels);
+            for (int j = 0, k = 0; j < n; k += (int)g->nodes[nodes[j]].ai_len, ++j) rec_ids(nodes[j], 0, 4, ol + 4 * k);
           }
           const size_t oi = B.push(inval(0)), og = B.push(gout), ov = B.push(oval), ogi = B.push(gin(0));
-          plan.ops.push_back([a, oi, og, ov, ogi, ol, pnls, st](char* d) mutable {
+          plan.ops.push_back([a, oi, og, ov, ogi, ol, pnls](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
             a.in = at<const float* const>(d, oi);
             a.gout = at<const float* const>(d, og);
             a.oval = at<const float* const>(d, ov);
@@ -2741,7 +3006,8 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
           a.x_b1 = x.batch == 1 && n0.batch > 1;
           const size_t oa = B.push(inval(0)), ox = B.push(inval(1)), og = B.push(gout);
           const size_t oga = B.push(gin(0)), ogx = B.push(gin(1));
-          plan.ops.push_back([a, oa, ox, og, oga, ogx, st](char* d) mutable {
+          plan.ops.push_back([a, oa, ox, og, oga, ogx](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
             a.a = at<const float* const>(d, oa);
             a.x = at<const float* const>(d, ox);
             a.gout = at<const float* const>(d, og);
@@ -2780,7 +3046,8 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
             }
             const size_t ob = B.push(inval(0)), ow = B.push(w), ox = B.push(x), og = B.push(gout);
             const size_t ogb = B.push(gin(0)), ogw = B.push(gw), ogx = B.push(gx);
-            plan.ops.push_back([a, ob, ow, ox, og, ogb, ogw, ogx, st](char* d) mutable {
+            plan.ops.push_back([a, ob, ow, ox, og, ogb, ogw, ogx](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
               a.bias = at<const float* const>(d, ob);
               a.w = at<const float* const>(d, ow);
               a.x = at<const float* const>(d, ox);
@@ -2810,7 +3077,8 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
             a.batch = Bt;
             a.a_b1 = b0.batch == 1 && Bt > 1;
             const size_t og = B.push(gout), oga = B.push(gin(0));
-            plan.ops.push_back([a, og, oga, st](char* d) mutable {
+            plan.ops.push_back([a, og, oga](char* d) mutable {
+      const cudaStream_t st = g_launch_stream;
               a.gout = at<const float* const>(d, og);
               a.ga = at<float* const>(d, oga);
               return launch_ew_bwd(a, st);
@@ -2898,7 +3166,8 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
                   dev_at<float*>(g, B.push(tgt))));
               const int* sg = dev_at<int>(g, B.push(seg));
               const int n_t = (int)tgt.size();
-              batch.post.push_back([tg, sg, temp, n_t, K, st]() {
+              batch.post.push_back([tg, sg, temp, n_t, K]() {
+                const cudaStream_t st = g_launch_stream;
                 return launch_row_reduce_scatter(tg, sg, temp, n_t, K, st);
               });
             }
@@ -3038,159 +3307,174 @@ int dg_backward(dg_graph* g, int32_t loss) {
     if (rc1) return rc1;
   }
   Blob& B = plan.blob;
-  cudaStream_t st = g->stream;
-  // zero the fresh slots (arena contract, graph.py:146-148) and seed dloss = 1
-  {
-    char* z0 = g->bwd_base + begin;
-    const size_t zn = zero_end - begin;
-    float* seed = g->nodes[loss].grad;
-    plan.ops.push_back([z0, zn, seed, st](char*) {
-      if (cudaMemsetAsync(z0, 0, zn, st) != cudaSuccess) return -1;
-      return launch_fill(seed, 1, 1.f, st);
-    });
-  }
-  // dummy gradient target for slot-serial passes
-  float* dummy = dummy_base(g);
-  std::unordered_map<int64_t, AffineUse> wuse;
-  std::unordered_map<int64_t, std::vector<uintptr_t>> buse;
-  tm.lap("place");
-  {
-    GemmBatch gb;
-    static const bool per_kind = [] {
-      const char* e = std::getenv("DG_PLAN_TIMING");
-      return e && e[0] == '2';
-    }();
-    std::map<int, double> kt;
-    for (int q = (int)S.groups.size() - 1; q >= 0; --q) {
-      const auto t0 = std::chrono::steady_clock::now();
-      plan_backward_group(g, S, S.groups[q], plan, dummy, wuse, buse, gb);
-      if (per_kind)
-        kt[S.groups[q].kind] += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
-    }
-    flush_gemm(g, plan, gb);
-    if (per_kind) {
-      std::string o;
-      for (auto& kv : kt) o += " k" + std::to_string(kv.first) + "=" + std::to_string((int)kv.second);
-      std::fprintf(stderr, "[plan] backward groups by kind:%s\n", o.c_str());
-    }
-  }
-  tm.lap("groups");
+  // static part (cached per structure) | per-call tail (lookup flush)
+  const uint64_t pkey = plan_key(g, 1, 0, loss);
+  CachedPlan* hit = plan_cache_find(g, 1, pkey);
+  PatchRec rec;
+  size_t n_wparams = hit ? (size_t)g->stats[4] : 0;
+  if (hit) {
+    blob_from_template(g, *hit, B);
+    tm.lap("cached");
+  } else {
+    RecScope rec_scope(&rec);
 
-  // aggregated weight gradients: dW^T (K x m) += X^T G over every use
-  std::vector<int64_t> wkeys;
-  for (auto& kv : wuse) wkeys.push_back(kv.first);
-  std::sort(wkeys.begin(), wkeys.end());
-  {
-    // rows of one parameter's uses -> the longest run where both the x rows
-    // and the gradient rows are equally spaced (a dense block: TMA path) plus
-    // the rest; the two parts accumulate into dW in two launches
-    auto regular_run = [](const std::vector<uintptr_t>& a, const std::vector<uintptr_t>& b, int64_t la,
-                          int64_t lb, size_t& best_lo, size_t& best_hi) {
-      const size_t n = a.size();
-      best_lo = best_hi = 0;
-      size_t lo = 0;
-      for (size_t i = 1; i <= n; ++i) {
-        bool cont = i < n;
-        if (cont && i - lo >= 2) {
-          cont = a[i] - a[i - 1] == a[lo + 1] - a[lo] && b[i] - b[i - 1] == b[lo + 1] - b[lo];
-        } else if (cont) {
-          const int64_t sa = (int64_t)(a[i] - a[i - 1]), sb = (int64_t)(b[i] - b[i - 1]);
-          cont = sa >= la * 4 && sb >= lb * 4 && sa % 16 == 0 && sb % 16 == 0 && (a[lo] & 15) == 0 &&
-                 (b[lo] & 15) == 0;
-        }
-        if (!cont) {
-          if (i - lo > best_hi - best_lo) {
-            best_lo = lo;
-            best_hi = i;
-          }
-          lo = i;
-        }
-      }
-    };
-    GemmBatch gb, gb_rest;
-    std::vector<std::pair<std::vector<uintptr_t>, std::vector<uintptr_t>>> rest_rows;
-    auto dw_problem = [&](const std::vector<uintptr_t>& xr, const std::vector<uintptr_t>& gr, const AffineUse& use,
-                          Param* p, GemmBatch& bt) {
-      GemmProblem pr{};
-      pr.M = (int)use.n_in;
-      pr.N = (int)use.m;
-      pr.n_seg = 1;
-      pr.accumulate = 1;
-      pr.seg[0].K = (int64_t)xr.size();
-      pr.seg[0].A.rows = dev_at<const float*>(g, B.push(xr));
-      pr.seg[0].A.rows_aligned = all_aligned16(xr);
-      pr.seg[0].B.rows = dev_at<const float*>(g, B.push(gr));
-      pr.seg[0].B.rows_aligned = all_aligned16(gr);
-      pr.C.base = p->grad;  // dW^T (n_in x m) row-major == dW column-major
-      pr.C.ld = use.m;
-      bt.probs.push_back(pr);
-      bt.bytes += 4.0 * ((double)pr.seg[0].K * (pr.M + pr.N) + 2.0 * pr.M * pr.N);
-    };
-    gemm_batch_for(g, plan, gb, -1, C_GEMM_DW, true, false);
-    std::vector<std::pair<int64_t, std::pair<std::vector<uintptr_t>, std::vector<uintptr_t>>>> rests;
-    for (int64_t h : wkeys) {
-      AffineUse& use = wuse[h];
-      Param* p = param_at(h);
-      size_t lo = 0, hi = 0;
-      regular_run(use.x_rows, use.g_rows, use.n_in, use.m, lo, hi);
-      if (hi - lo >= 128 && hi - lo < use.x_rows.size()) {
-        std::vector<uintptr_t> xr(use.x_rows.begin() + lo, use.x_rows.begin() + hi);
-        std::vector<uintptr_t> grr(use.g_rows.begin() + lo, use.g_rows.begin() + hi);
-        dw_problem(xr, grr, use, p, gb);
-        std::vector<uintptr_t> xo(use.x_rows.begin(), use.x_rows.begin() + lo), go(use.g_rows.begin(), use.g_rows.begin() + lo);
-        xo.insert(xo.end(), use.x_rows.begin() + hi, use.x_rows.end());
-        go.insert(go.end(), use.g_rows.begin() + hi, use.g_rows.end());
-        rests.push_back({h, {std::move(xo), std::move(go)}});
-      } else {
-        dw_problem(use.x_rows, use.g_rows, use, p, gb);
-      }
-    }
-    flush_gemm(g, plan, gb);
-    if (!rests.empty()) {
-      gemm_batch_for(g, plan, gb_rest, -1, C_GEMM_DW, true, false);
-      for (auto& r : rests) dw_problem(r.second.first, r.second.second, wuse[r.first], param_at(r.first), gb_rest);
-      flush_gemm(g, plan, gb_rest);
-    }
-  }
-  tm.lap("dW");
-  std::vector<int64_t> bkeys;
-  for (auto& kv : buse) bkeys.push_back(kv.first);
-  std::sort(bkeys.begin(), bkeys.end());
-  // bias gradients: up to kColsumGroup column sums per pair of launches
-  {
-    float* work = reinterpret_cast<float*>(scratch_base(g));
-    const int64_t wcap = (int64_t)(scratch_bytes(g) / 4);
-    struct Job {
-      float* dst;
-      size_t orow;
-      int nr, width;
-    };
-    std::vector<Job> jobs;
-    double bytes = 0;
-    auto flush_jobs = [&] {
-      if (jobs.empty()) return;
-      plan.ops.push_back([jobs, work, wcap, st](char* d) {
-        ColsumGroup G{};
-        G.n = (int)jobs.size();
-        for (int q = 0; q < G.n; ++q)
-          G.j[q] = ColsumJob{jobs[q].dst, at<const float* const>(d, jobs[q].orow), jobs[q].nr, jobs[q].width, 0, 0, 0,
-                             nullptr};
-        return launch_colsum_group(G, work, wcap, st);
+    // zero the fresh slots (arena contract, graph.py:146-148) and seed dloss = 1
+    {
+      char* z0 = g->bwd_base + begin;
+      const size_t zn = zero_end - begin;
+      float* seed = g->nodes[loss].grad;
+      plan.ops.push_back([z0, zn, seed](char*) {
+        const cudaStream_t st = g_launch_stream;
+        if (cudaMemsetAsync(z0, 0, zn, st) != cudaSuccess) return -1;
+        return launch_fill(seed, 1, 1.f, st);
       });
-      plan.tag(C_COLSUM, 0.0, bytes);
-      jobs.clear();
-      bytes = 0;
-    };
-    for (int64_t h : bkeys) {
-      auto& rows = buse[h];
-      Param* p = param_at(h);
-      jobs.push_back({p->grad, B.push(rows), (int)rows.size(), (int)p->size()});
-      bytes += 4.0 * rows.size() * p->size() + 8.0 * p->size();
-      if ((int)jobs.size() == kColsumGroup) flush_jobs();
     }
-    flush_jobs();
+    // dummy gradient target for slot-serial passes
+    float* dummy = dummy_base(g);
+    std::unordered_map<int64_t, AffineUse> wuse;
+    std::unordered_map<int64_t, std::vector<uintptr_t>> buse;
+    tm.lap("place");
+    {
+      GemmBatch gb;
+      static const bool per_kind = [] {
+        const char* e = std::getenv("DG_PLAN_TIMING");
+        return e && e[0] == '2';
+      }();
+      std::map<int, double> kt;
+      for (int q = (int)S.groups.size() - 1; q >= 0; --q) {
+        const auto t0 = std::chrono::steady_clock::now();
+        plan_backward_group(g, S, S.groups[q], plan, dummy, wuse, buse, gb);
+        if (per_kind)
+          kt[S.groups[q].kind] += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+      }
+      flush_gemm(g, plan, gb);
+      if (per_kind) {
+        std::string o;
+        for (auto& kv : kt) o += " k" + std::to_string(kv.first) + "=" + std::to_string((int)kv.second);
+        std::fprintf(stderr, "[plan] backward groups by kind:%s\n", o.c_str());
+      }
+    }
+    tm.lap("groups");
+
+    // aggregated weight gradients: dW^T (K x m) += X^T G over every use
+    std::vector<int64_t> wkeys;
+    for (auto& kv : wuse) wkeys.push_back(kv.first);
+    std::sort(wkeys.begin(), wkeys.end());
+    {
+      // rows of one parameter's uses -> the longest run where both the x rows
+      // and the gradient rows are equally spaced (a dense block: TMA path) plus
+      // the rest; the two parts accumulate into dW in two launches
+      auto regular_run = [](const std::vector<uintptr_t>& a, const std::vector<uintptr_t>& b, int64_t la,
+                            int64_t lb, size_t& best_lo, size_t& best_hi) {
+        const size_t n = a.size();
+        best_lo = best_hi = 0;
+        size_t lo = 0;
+        for (size_t i = 1; i <= n; ++i) {
+          bool cont = i < n;
+          if (cont && i - lo >= 2) {
+            cont = a[i] - a[i - 1] == a[lo + 1] - a[lo] && b[i] - b[i - 1] == b[lo + 1] - b[lo];
+          } else if (cont) {
+            const int64_t sa = (int64_t)(a[i] - a[i - 1]), sb = (int64_t)(b[i] - b[i - 1]);
+            cont = sa >= la * 4 && sb >= lb * 4 && sa % 16 == 0 && sb % 16 == 0 && (a[lo] & 15) == 0 &&
+                   (b[lo] & 15) == 0;
+          }
+          if (!cont) {
+            if (i - lo > best_hi - best_lo) {
+              best_lo = lo;
+              best_hi = i;
+            }
+            lo = i;
+          }
+        }
+      };
+      GemmBatch gb, gb_rest;
+      std::vector<std::pair<std::vector<uintptr_t>, std::vector<uintptr_t>>> rest_rows;
+      auto dw_problem = [&](const std::vector<uintptr_t>& xr, const std::vector<uintptr_t>& gr, const AffineUse& use,
+                            Param* p, GemmBatch& bt) {
+        GemmProblem pr{};
+        pr.M = (int)use.n_in;
+        pr.N = (int)use.m;
+        pr.n_seg = 1;
+        pr.accumulate = 1;
+        pr.seg[0].K = (int64_t)xr.size();
+        pr.seg[0].A.rows = dev_at<const float*>(g, B.push(xr));
+        pr.seg[0].A.rows_aligned = all_aligned16(xr);
+        pr.seg[0].B.rows = dev_at<const float*>(g, B.push(gr));
+        pr.seg[0].B.rows_aligned = all_aligned16(gr);
+        pr.C.base = p->grad;  // dW^T (n_in x m) row-major == dW column-major
+        pr.C.ld = use.m;
+        bt.probs.push_back(pr);
+        bt.bytes += 4.0 * ((double)pr.seg[0].K * (pr.M + pr.N) + 2.0 * pr.M * pr.N);
+      };
+      gemm_batch_for(g, plan, gb, -1, C_GEMM_DW, true, false);
+      std::vector<std::pair<int64_t, std::pair<std::vector<uintptr_t>, std::vector<uintptr_t>>>> rests;
+      for (int64_t h : wkeys) {
+        AffineUse& use = wuse[h];
+        Param* p = param_at(h);
+        size_t lo = 0, hi = 0;
+        regular_run(use.x_rows, use.g_rows, use.n_in, use.m, lo, hi);
+        if (hi - lo >= 128 && hi - lo < use.x_rows.size()) {
+          std::vector<uintptr_t> xr(use.x_rows.begin() + lo, use.x_rows.begin() + hi);
+          std::vector<uintptr_t> grr(use.g_rows.begin() + lo, use.g_rows.begin() + hi);
+          dw_problem(xr, grr, use, p, gb);
+          std::vector<uintptr_t> xo(use.x_rows.begin(), use.x_rows.begin() + lo), go(use.g_rows.begin(), use.g_rows.begin() + lo);
+          xo.insert(xo.end(), use.x_rows.begin() + hi, use.x_rows.end());
+          go.insert(go.end(), use.g_rows.begin() + hi, use.g_rows.end());
+          rests.push_back({h, {std::move(xo), std::move(go)}});
+        } else {
+          dw_problem(use.x_rows, use.g_rows, use, p, gb);
+        }
+      }
+      flush_gemm(g, plan, gb);
+      if (!rests.empty()) {
+        gemm_batch_for(g, plan, gb_rest, -1, C_GEMM_DW, true, false);
+        for (auto& r : rests) dw_problem(r.second.first, r.second.second, wuse[r.first], param_at(r.first), gb_rest);
+        flush_gemm(g, plan, gb_rest);
+      }
+    }
+    tm.lap("dW");
+    std::vector<int64_t> bkeys;
+    for (auto& kv : buse) bkeys.push_back(kv.first);
+    std::sort(bkeys.begin(), bkeys.end());
+    // bias gradients: up to kColsumGroup column sums per pair of launches
+    {
+      float* work = reinterpret_cast<float*>(scratch_base(g));
+      const int64_t wcap = (int64_t)(scratch_bytes(g) / 4);
+      struct Job {
+        float* dst;
+        size_t orow;
+        int nr, width;
+      };
+      std::vector<Job> jobs;
+      double bytes = 0;
+      auto flush_jobs = [&] {
+        if (jobs.empty()) return;
+        plan.ops.push_back([jobs, work, wcap](char* d) {
+        const cudaStream_t st = g_launch_stream;
+          ColsumGroup G{};
+          G.n = (int)jobs.size();
+          for (int q = 0; q < G.n; ++q)
+            G.j[q] = ColsumJob{jobs[q].dst, at<const float* const>(d, jobs[q].orow), jobs[q].nr, jobs[q].width, 0, 0, 0,
+                               nullptr};
+          return launch_colsum_group(G, work, wcap, st);
+        });
+        plan.tag(C_COLSUM, 0.0, bytes);
+        jobs.clear();
+        bytes = 0;
+      };
+      for (int64_t h : bkeys) {
+        auto& rows = buse[h];
+        Param* p = param_at(h);
+        jobs.push_back({p->grad, B.push(rows), (int)rows.size(), (int)p->size()});
+        bytes += 4.0 * rows.size() * p->size() + 8.0 * p->size();
+        if ((int)jobs.size() == kColsumGroup) flush_jobs();
+      }
+      flush_jobs();
+    }
+    tm.lap("colsum");
+    n_wparams = wuse.size();
   }
-  tm.lap("colsum");
+  const size_t static_ops = plan.ops.size(), static_bytes = plan.blob.size();
   // lookup flush: sorted segmented scatter-add per table (graph.py:57-63)
   {
     struct Rows {
@@ -3250,7 +3534,8 @@ int dg_backward(dg_graph* g, int32_t loss) {
       int* ctr = counter_base(g) + kScatterCtrBase;
       if ((int64_t)n_part * dim * 4 > (int64_t)scratch_bytes(g) || n_long > kScatterCtrs)
         return fail(DG_POOL_EXHAUSTED, "workspace too small for the lookup scatter");
-      plan.ops.push_back([tg, dim, ou, oit, osrc, n_items, partials, ctr, st](char* d) {
+      plan.ops.push_back([tg, dim, ou, oit, osrc, n_items, partials, ctr](char* d) {
+      const cudaStream_t st = g_launch_stream;
         return launch_scatter_rows(tg, dim, at<const int64_t>(d, ou), at<const ScatterItem>(d, oit), n_items,
                                    at<const float* const>(d, osrc), partials, ctr, 1.f, false, st);
       });
@@ -3259,14 +3544,33 @@ int dg_backward(dg_graph* g, int32_t loss) {
   }
   tm.lap("scatter");
   g->blob_hint[1] = std::max(g->blob_hint[1], plan.blob.size() + plan.blob.size() / 4);
-  rc = launch_plan(g, plan);
-  if (rc) return rc;
+  if (hit) {
+    rc = launch_cached(g, *hit, plan);  // plan.ops holds the tail only
+    if (rc) return rc;
+  } else {
+    rc = prepare_launch(g, plan.blob);
+    if (rc) return rc;
+    if (!dry_run()) {
+      std::vector<std::function<int(char*)>> tail_ops(std::make_move_iterator(plan.ops.begin() + static_ops),
+                                                      std::make_move_iterator(plan.ops.end()));
+      plan.meta.resize(plan.ops.size());
+      std::vector<OpMeta> tail_meta(plan.meta.begin() + static_ops, plan.meta.end());
+      plan.ops.resize(static_ops);
+      plan.meta.resize(static_ops);
+      int64_t n_static = 0, n_tail = 0;
+      rc = run_ops(g, plan.ops, plan.meta, &n_static, g->stream);
+      if (!rc) rc = run_ops(g, tail_ops, tail_meta, &n_tail, g->stream);
+      g->launches += n_static + n_tail;
+      if (rc) return rc;
+      plan_cache_store(g, 1, pkey, plan, static_ops, static_bytes, std::move(rec), n_static);
+    }
+  }
   tm.lap("launch");
   g->bwd_cursor = cur;
   g->bwd_alloc_count += loss + 1;
   g->has_grads = true;
   g->stats[3] = (int64_t)S.groups.size();
-  g->stats[4] = (int64_t)wuse.size();
+  g->stats[4] = (int64_t)n_wparams;
   return DG_OK;
 }
 

@@ -58,6 +58,8 @@ F64_BAND_AFTER_STEP0 = {"simple_lm"}
 
 
 def _oracle_f64_grads(name):
+    """Per step {param: grad, lookup: grad rows of the touched set}, plus the
+    final values, of the oracle run in float64 from the fp32 initial values."""
     make_task, data, rule, steps = cases.workload_cases()[name]
     pools = orc.new_poolset(dtype=np.float64)
     m = orc.Model(pools, seed=1, dtype=np.float64)
@@ -67,9 +69,21 @@ def _oracle_f64_grads(name):
     for s in range(steps):
         g = orc.ComputationGraph(pools)
         g.backward(cases.call_loss(task, g, data[s]))
-        out.append({p.name: np.array(p.gradient, dtype=np.float64).reshape(-1) for p in m.parameters})
+        rec = {p.name: np.array(p.gradient, dtype=np.float64).reshape(-1) for p in m.parameters}
+        for lp in m.lookups:
+            rec[lp.name] = np.array(lp.gradient, dtype=np.float64)[sorted(lp.touched)]
+        out.append(rec)
         tr.update()
-    return out
+    final = {x.name: np.array(x.values, dtype=np.float64).reshape(-1) for x in list(m.parameters) + list(m.lookups)}
+    return out, final
+
+
+def _f64_band(f64, s, name, ref):
+    """2 * max|ref32 - ref64| of one tensor (0 when the case has no exception)."""
+    if f64 is None or s == 0:
+        return 0.0
+    other = f64[1][name] if s == "final" else f64[0][s][name]
+    return 2 * float(np.abs(np.asarray(ref, dtype=np.float64).reshape(-1) - other.reshape(-1)).max())
 
 
 @pytest.mark.parametrize("name", sorted(cases.workload_cases()))
@@ -90,18 +104,17 @@ def test_workload_traces_match_reference(name):
         for p in model.parameters:
             key = f"{name}/grad{s}/{p.name}"
             if key in WL:
-                band = 2 * float(np.abs(WL[key].reshape(-1) - f64[s][p.name]).max()) if f64 is not None and s > 0 else 0.0
-                parity(pgrad(p), WL[key], band=band, what=key)
+                parity(pgrad(p), WL[key], band=_f64_band(f64, s, p.name, WL[key]), what=key)
         for lp in model.lookups:
             rows = WL[f"{name}/touched{s}/{lp.name}"]
             assert sorted(lp.touched) == list(rows), "touched set must be bit-exact"
-            parity(np.asarray(lp.gradient)[rows], WL[f"{name}/lgrad{s}/{lp.name}"], what=f"{lp.name} rows")
+            ref = WL[f"{name}/lgrad{s}/{lp.name}"]
+            parity(np.asarray(lp.gradient)[rows], ref, band=_f64_band(f64, s, lp.name, ref), what=f"{lp.name} rows")
         tr.update()
     band = 0.0 if rule == "sgd" else 2 * lr * steps
-    for p in model.parameters:
-        parity(pvals(p), WL[f"{name}/final/{p.name}"], band=band, what=f"final {p.name}")
-    for lp in model.lookups:
-        parity(pvals(lp), WL[f"{name}/final/{lp.name}"].reshape(-1), band=band, what=f"final {lp.name}")
+    for x in list(model.parameters) + list(model.lookups):
+        ref = WL[f"{name}/final/{x.name}"].reshape(-1)
+        parity(pvals(x), ref, band=max(band, _f64_band(f64, "final", x.name, ref)), what=f"final {x.name}")
 
 
 # ---------------------------------------------------------------------------

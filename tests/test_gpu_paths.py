@@ -10,6 +10,8 @@ with each fast path switched off, so the fallbacks stay parity-green too.
                     them in shared memory
   DG_TC=0           SIMT GEMMs only
   DG_SCHED_CACHE=0  schedules rebuilt for every graph
+  DG_PLAN_CACHE=0   launch plans rebuilt for every graph (no plan cache)
+  DG_CUDA_GRAPH=0   cached plans replayed launch by launch, not as CUDA graphs
 """
 
 import os
@@ -31,6 +33,8 @@ VARIANTS = {
     "tma_lite_off": {"DG_TMA_LITE": "0"},
     "tensor_cores_off": {"DG_TC": "0"},
     "schedule_cache_off": {"DG_SCHED_CACHE": "0"},
+    "plan_cache_off": {"DG_PLAN_CACHE": "0"},
+    "cuda_graph_off": {"DG_CUDA_GRAPH": "0"},
 }
 
 
@@ -43,3 +47,53 @@ def test_ptb_parity_on_every_kernel_path(variant):
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", *tests],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+_REPLAY = r"""
+import hashlib, json, sys
+import numpy as np
+sys.path.insert(0, ROOT)
+import paper_1701_03980_b200 as dy
+from paper_1701_03980_b200 import workloads as W
+# equal padded length -> equal structure: the plan of step 0 serves steps 1..
+# (each batch: one 22-token sentence + 7 shorter ones, so masks differ)
+corpus = W.ptb_corpus(9, 4000, vocab=500)
+longs = [s for s in corpus if len(s) == 22][:6]
+shorts = [s for s in corpus if 2 <= len(s) < 22][:42]
+batches = [[longs[k]] + shorts[7 * k: 7 * k + 7] for k in range(6)]
+pools = dy.new_poolset(256, 256, 64)
+cg, m = dy.ComputationGraph(pools), dy.Model(pools, seed=2)
+task = W.RNNLM(dy, m, 500, 32, 64, 2)
+tr = dy.Trainer(m, "adam")
+losses = []
+for b in batches:
+    cg.renew()
+    loss = task.loss(cg, b)
+    cg.backward(loss)
+    losses.append(float(cg.value(loss).data[0]))
+    tr.update()
+h = hashlib.sha256()
+for x in list(m.parameters) + list(m.lookups):
+    v = x.values
+    h.update(np.ascontiguousarray(v if isinstance(v, np.ndarray) else v.data, dtype=np.float32).tobytes())
+st = cg.plan_stats()
+print(json.dumps({"losses": losses, "params": h.hexdigest(), "hits": int(st[5]), "replays": int(st[6])}))
+"""
+
+
+@pytest.mark.gpu
+def test_plan_cache_and_cuda_graph_replay_are_bitwise_identical():
+    """Six minibatches of one structure (same padded length, different ids,
+    labels and masks): the cached plans (patched data, CUDA-graph replay)
+    give bit-identical losses and parameters to planning every graph."""
+    outs = {}
+    for name, env in {"cached": {}, "uncached": {"DG_PLAN_CACHE": "0"}, "no_graph": {"DG_CUDA_GRAPH": "0"}}.items():
+        r = subprocess.run([sys.executable, "-c", f"ROOT={ROOT!r}\n" + _REPLAY], cwd=ROOT, capture_output=True,
+                           text=True, timeout=600, env=dict(os.environ, **env))
+        assert r.returncode == 0, r.stderr[-3000:]
+        outs[name] = __import__("json").loads(r.stdout.strip().splitlines()[-1])
+    assert outs["cached"]["hits"] >= 10 and outs["cached"]["replays"] >= 8, outs["cached"]
+    assert outs["uncached"]["hits"] == 0 and outs["no_graph"]["replays"] == 0
+    for name in ("uncached", "no_graph"):
+        assert outs[name]["losses"] == outs["cached"]["losses"], name
+        assert outs[name]["params"] == outs["cached"]["params"], name
