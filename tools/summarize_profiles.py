@@ -22,11 +22,11 @@ tag = sys.argv[1] if len(sys.argv) > 1 else "r02"
 os.makedirs(PROF, exist_ok=True)
 
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
-         "nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9,
+         "nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3, "ms": 1e6, "s": 1e9,
          "cycle": 1, "Kcycle": 1e3, "Mcycle": 1e6, "%": 1, "": 1,
          "byte/second": 1, "Kbyte/second": 1e3, "Mbyte/second": 1e6, "Gbyte/second": 1e9, "Tbyte/second": 1e12,
          "hz": 1, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9}
-BASE = {"byte": "byte", "nsecond": "ns", "cycle": "cycle", "%": "%", "byte/second": "byte/s", "hz": "hz"}
+BASE = {"byte": "byte", "nsecond": "ns", "ns": "ns", "cycle": "cycle", "%": "%", "byte/second": "byte/s", "hz": "hz"}
 
 
 def base_unit(u):
@@ -99,7 +99,7 @@ json.dump(summary, open(os.path.join(PROF, f"{tag}_summary.json"), "w"), indent=
 # bench op class -> kernel name fragment of its (single) kernel
 CLASS_KERNEL = {"rnn_fwd": "rnn_fwd_cl_kernel", "rnn_bwd": "rnn_bwd_cl_kernel", "pnls_fwd": "row_reg_kernel<2",
                 "pnls_bwd": "row_reg_kernel<3", "gather": "gather_rows_kernel",
-                "scatter_add": "segment_scatter_add_kernel"}
+                "scatter_add": "scatter_rows_kernel", "bias_colsum": "colsum_partial_group_kernel"}
 traffic = {"source": f"profiles/{tag}_summary.json", "unit": "bytes per launch (dram read + write)", "classes": {}}
 for cls, frag in CLASS_KERNEL.items():
     hits = [d for ls in summary["full"].values() for d in ls if frag in d["kernel"] and "dram_bytes" in d]
