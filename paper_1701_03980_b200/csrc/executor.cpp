@@ -271,7 +271,6 @@ struct dg_graph {
   std::vector<std::shared_ptr<dg::CachedPlan>> pcache[2];
   mutable uint64_t memo_key = 0;   // structure hash of memo_sched
   uint64_t fwd_hist = 0;   // forward calls of this generation (placement history)
-  cudaStream_t cap_stream = nullptr;  // CUDA-graph capture of cached plans
 };
 
 struct dg_trainer {
@@ -1498,6 +1497,10 @@ using namespace dg;
 
 extern "C" {
 
+static bool dry_run();
+static bool cuda_graphs_on();
+static void warm_graph_runtime();
+
 const char* dg_last_error(void) { return g_err.c_str(); }
 int dg_abi_version(void) { return 1; }
 
@@ -1592,6 +1595,7 @@ int dg_graph_create(int device, void* fwd_base, size_t fwd_bytes, void* bwd_base
     delete g;
     return fail(DG_CONFIG, "workspace must be at least 64 MiB");
   }
+  if (cuda_graphs_on() && !dry_run()) warm_graph_runtime();
   *out = g;
   return DG_OK;
 }
@@ -1600,7 +1604,6 @@ int dg_graph_destroy(dg_graph* g) {
   if (!g) return DG_OK;
   g->pcache[0].clear();
   g->pcache[1].clear();
-  if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
   if (g->vcache_ev) {
     cudaEventSynchronize(g->vcache_ev);
     cudaEventDestroy(g->vcache_ev);
@@ -1822,7 +1825,7 @@ static void plan_cache_store(dg_graph* g, int which, uint64_t key, Plan& plan, s
   cp->kernel_launches = launched_static;
   auto& v = g->pcache[which];
   v.insert(v.begin(), std::move(cp));
-  if (v.size() > 8) v.pop_back();
+  if (v.size() > 32) v.pop_back();
 }
 
 // blob for a cached plan: the template with this graph's data written in
@@ -1844,6 +1847,45 @@ static void blob_from_template(const dg_graph* g, const CachedPlan& cp, Blob& B)
   }
 }
 
+// per host thread: the private non-blocking stream cached plans are recorded
+// on (captures are synchronous host calls, so one per thread serves every
+// graph); the first use also pays the runtime's one-time graph set-up with a
+// throwaway capture
+static cudaStream_t capture_stream() {
+  static thread_local cudaStream_t cs = nullptr;
+  if (!cs && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    cs = nullptr;
+  }
+  return cs;
+}
+
+static void warm_graph_runtime() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaStream_t cs = capture_stream();
+    void* buf = nullptr;
+    if (!cs || cudaMalloc(&buf, 256) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      cudaMemsetAsync(buf, 0, 256, cs);
+      if (cudaStreamEndCapture(cs, &graph) == cudaSuccess && graph &&
+          cudaGraphInstantiateWithFlags(&exec, graph, 0) == cudaSuccess) {
+        cudaGraphLaunch(exec, cs);
+        cudaStreamSynchronize(cs);
+      }
+    }
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    cudaFree(buf);
+    cudaGetLastError();
+  });
+}
+
 // upload the blob, replay the cached static ops (as a CUDA graph from the
 // second use on), then the per-call tail ops of `tail`
 static int launch_cached(dg_graph* g, CachedPlan& cp, Plan& tail) {
@@ -1852,17 +1894,23 @@ static int launch_cached(dg_graph* g, CachedPlan& cp, Plan& tail) {
   bool profiling = false;
   for (const OpMeta& m : cp.meta) profiling = profiling || ((g->prof_mask >> m.cls) & 1u);
   int64_t n = 0;
-  if (cuda_graphs_on() && !profiling && cp.replays >= 1 && !cp.exec && cp.replays != -1000) {
+  // a structure seen for the third time is recorded as a CUDA graph (the
+  // capture + instantiate, ~0.1-0.2 ms, pays off only for plans that recur)
+  if (cuda_graphs_on() && !profiling && cp.replays >= 2 && !cp.exec && cp.replays != -1000) {
     // recorded on a private non-blocking stream (the graph's own stream may
     // be the legacy default stream, which cannot be captured); replayed on
     // the graph's stream
-    if (!g->cap_stream) DG_CUDA_TRY(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
+    PlanTimer ct("graph-capture");
+    cudaStream_t cs = capture_stream();
+    if (!cs) return fail(DG_CUDA, "cannot create the capture stream");
     cudaGraph_t graph = nullptr;
-    bool ok = cudaStreamBeginCapture(g->cap_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    bool ok = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
     int64_t n_cap = 0;
-    int rc_cap = ok ? run_ops(g, cp.ops, cp.meta, &n_cap, g->cap_stream) : DG_CUDA;
-    ok = cudaStreamEndCapture(g->cap_stream, &graph) == cudaSuccess && ok && rc_cap == DG_OK;
+    int rc_cap = ok ? run_ops(g, cp.ops, cp.meta, &n_cap, cs) : DG_CUDA;
+    ok = cudaStreamEndCapture(cs, &graph) == cudaSuccess && ok && rc_cap == DG_OK;
+    ct.lap("capture");
     if (ok) ok = cudaGraphInstantiateWithFlags(&cp.exec, graph, 0) == cudaSuccess;
+    ct.lap("instantiate");
     if (graph) cudaGraphDestroy(graph);
     if (!ok) {
       cudaGetLastError();  // capture unsupported for this plan: replay op by op
@@ -1872,7 +1920,9 @@ static int launch_cached(dg_graph* g, CachedPlan& cp, Plan& tail) {
   }
   g->stats[5]++;  // plan-cache hits (cumulative)
   if (cp.exec && !profiling) {
+    PlanTimer lt("graph-launch");
     DG_CUDA_TRY(cudaGraphLaunch(cp.exec, g->stream));
+    lt.lap("launch");
     n += cp.kernel_launches;
     g->stats[6]++;  // CUDA-graph replays (cumulative)
   } else {

@@ -92,7 +92,7 @@ def test_plan_cache_and_cuda_graph_replay_are_bitwise_identical():
                            text=True, timeout=600, env=dict(os.environ, **env))
         assert r.returncode == 0, r.stderr[-3000:]
         outs[name] = __import__("json").loads(r.stdout.strip().splitlines()[-1])
-    assert outs["cached"]["hits"] >= 10 and outs["cached"]["replays"] >= 8, outs["cached"]
+    assert outs["cached"]["hits"] >= 10 and outs["cached"]["replays"] >= 6, outs["cached"]
     assert outs["uncached"]["hits"] == 0 and outs["no_graph"]["replays"] == 0
     for name in ("uncached", "no_graph"):
         assert outs[name]["losses"] == outs["cached"]["losses"], name

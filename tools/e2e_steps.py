@@ -14,7 +14,10 @@ import paper_1701_03980_b200 as dy  # noqa: E402
 
 cfg = bench.CONFIGS["ptb64"]
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 30
+CYCLE = int(sys.argv[2]) if len(sys.argv) > 2 else 0  # >0: reuse this many batches cyclically (plan-cache hits)
 data, units, _ = bench.make_data(cfg, K + 3, 0, 1)
+if CYCLE:
+    data = [data[i % CYCLE] for i in range(K + 3)]
 pools = dy.new_poolset(1024, 1024, 64)
 cg, model = dy.ComputationGraph(pools), dy.Model(pools, seed=1)
 task = bench.make_task(dy, model, cfg)
