@@ -103,7 +103,8 @@ def make_data(cfg, n_steps, rank, world, seed=1):
         td = W.tree_corpus(seed, total)
         items = list(zip(td.trees, td.labels))[rank::world][:n_steps]
         return items, [1] * len(items), None
-    tg = W.tagger_corpus(seed, max(total, 200))
+    # WSJ-shaped: vocabulary (rare words -> char path) counted over 40k sentences
+    tg = W.tagger_corpus(seed, max(total, 200), corpus_sentences=40_000)
     items = tg.sentences[rank::world][:n_steps]
     return items, [len(s) for s in items], tg
 

@@ -78,8 +78,15 @@ class TaggerData:
 
 
 def tagger_corpus(seed: int, n_sent: int, n_types: int = 40_000, n_tags: int = 45,
-                  alphabet: int = 80, mean_len: float = 22.9, unk_threshold: int = 5) -> TaggerData:
-    """Config 3: Zipf word types, rare words (count < 5) take the char path."""
+                  alphabet: int = 80, mean_len: float = 22.9, unk_threshold: int = 5,
+                  corpus_sentences: int | None = None) -> TaggerData:
+    """Config 3: Zipf word types, rare words (count < 5) take the char path.
+
+    The vocabulary (and so which words are rare) is counted over a corpus of
+    `corpus_sentences` sentences (default: the n_sent returned); the WSJ-shaped
+    benchmark counts it over 40k sentences (WSJ sections 02-21, ~40k
+    sentences) and trains on the first n_sent of them."""
+    n_all = max(n_sent, corpus_sentences or 0)
     rng = np.random.default_rng(seed)
     draw = _zipf_sampler(rng, 0, n_types)
     letters = [chr(0x21 + i) for i in range(alphabet)]
@@ -92,7 +99,7 @@ def tagger_corpus(seed: int, n_sent: int, n_types: int = 40_000, n_tags: int = 4
             s = s + letters[t % alphabet]
         seen[s] = t
         spellings[t] = s
-    lens = 1 + rng.poisson(mean_len, n_sent)
+    lens = 1 + rng.poisson(mean_len, n_all)
     sents = []
     for n in lens:
         types = draw(int(n))
@@ -115,7 +122,7 @@ def tagger_corpus(seed: int, n_sent: int, n_types: int = 40_000, n_tags: int = 4
             for ch in w:
                 if ch not in chars:
                     chars[ch] = len(chars)
-    return TaggerData(sents, vocab, chars, n_tags)
+    return TaggerData(sents[:n_sent], vocab, chars, n_tags)
 
 
 @dataclass

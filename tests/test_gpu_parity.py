@@ -139,7 +139,27 @@ def _run_steps(dy, cg, model, task, batches, rule, n_steps, record):
     return out, model
 
 
-def _compare_full(make_task, batches, rule="adam", n_steps=2):
+# SURVEY 7 (ii) metric for the gradients before any update:
+#   |gpu - ref| <= 1e-4 |ref| + 1e-6 max|ref|      (no fp64 band, no 1e-5 floor)
+# Tensors measured to need more are listed here by name with the measured
+# worst ratio err / tol (they still pass the calibrated comparator below).
+STRICT_STEP0_EXCEPTIONS: dict = {}
+
+
+def _strict_step0(test, name, got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    tol = 1e-4 * np.abs(ref) + 1e-6 * float(np.abs(ref).max(initial=0.0))
+    ratio = float((np.abs(got - ref) / np.maximum(tol, 1e-30)).max(initial=0.0))
+    path = os.environ.get("DG_STRICT_REPORT")
+    if path:
+        with open(path, "a") as fh:
+            fh.write(f"{test}\t{name}\t{ratio:.4g}\n")
+    bound = STRICT_STEP0_EXCEPTIONS.get((test, name), 1.0)
+    assert ratio <= bound, f"{test} step0 {name}: err/tol {ratio:.3g} > {bound} (SURVEY 7 strict metric)"
+
+
+def _compare_full(make_task, batches, rule="adam", n_steps=2, test=None):
     """GPU vs the fp32 oracle on identical inputs and seeds.
 
     Tolerance per element: rtol 1e-4 * |ref| + max(1e-5 * max|ref|,
@@ -174,6 +194,11 @@ def _compare_full(make_task, batches, rule="adam", n_steps=2):
         # gradients: strict at every step under SGD; under Adam only before the
         # first update -- after it the two runs evaluate the graph at parameters
         # that already differ inside the Adam band ("Adam amplifies")
+        if s == 0 and test is not None:
+            for name, g in ref[0]["grads"].items():
+                _strict_step0(test, name, got[0]["grads"][name], g)
+            for name in ref[0]["touched"]:
+                _strict_step0(test, name + " rows", got[0]["lgrads"][name], ref[0]["lgrads"][name])
         if rule != "sgd" and s > 0:
             continue
         for name, g in ref[s]["grads"].items():
@@ -193,7 +218,7 @@ def _compare_full(make_task, batches, rule="adam", n_steps=2):
 def test_ptb_mb16_full_size_vs_oracle():
     sents = W.ptb_corpus(21, 32)
     batches = W.minibatches(sents, 16)
-    _compare_full(lambda dy, m: W.RNNLM(dy, m, 10_000, 128, 256, 2), batches)
+    _compare_full(lambda dy, m: W.RNNLM(dy, m, 10_000, 128, 256, 2), batches, test="ptb16")
 
 
 def test_ptb_mb16_full_size_vs_oracle_sgd_multistep():
@@ -205,23 +230,32 @@ def test_ptb_mb16_full_size_vs_oracle_sgd_multistep():
 def test_ptb_mb64_full_size_vs_oracle_sgd():
     sents = W.ptb_corpus(22, 64)
     batches = W.minibatches(sents, 64)
-    _compare_full(lambda dy, m: W.RNNLM(dy, m, 10_000, 128, 256, 2), batches, rule="sgd", n_steps=1)
+    _compare_full(lambda dy, m: W.RNNLM(dy, m, 10_000, 128, 256, 2), batches, rule="sgd", n_steps=1, test="ptb64_sgd")
+
+
+def test_ptb_mb64_bench_config_adam_3_steps_vs_oracle():
+    """The headline configuration exactly as bench.py runs it: PTB-shaped
+    RNNLM, minibatch 64, Adam, the bench's corpus seed, 3 steps."""
+    import bench
+
+    data, _, _ = bench.make_data(bench.CONFIGS["ptb64"], 3, 0, 1, 1)
+    _compare_full(lambda dy, m: W.RNNLM(dy, m, 10_000, 128, 256, 2), data, rule="adam", n_steps=3, test="ptb64_adam")
 
 
 def test_tiny_lm_full_size_vs_oracle():
     sents = W.tiny_lm_corpus(23, 3)
-    _compare_full(lambda dy, m: W.RNNLM(dy, m, 1000, 64, 64, 1), [[s] for s in sents], n_steps=3)
+    _compare_full(lambda dy, m: W.RNNLM(dy, m, 1000, 64, 64, 1), [[s] for s in sents], n_steps=3, test="tiny")
 
 
 def test_tree_lstm_full_size_vs_oracle():
     td = W.tree_corpus(24, 3)
     _compare_full(lambda dy, m: W.TreeClassifier(dy, m, td.vocab_size, 5, 128, 150),
-                  list(zip(td.trees, td.labels)), n_steps=3)
+                  list(zip(td.trees, td.labels)), n_steps=3, test="tree")
 
 
 def test_char_tagger_full_size_vs_oracle():
-    tg = W.tagger_corpus(25, 200, n_types=4000)
-    _compare_full(lambda dy, m: W.CharTagger(dy, m, tg), tg.sentences, n_steps=3)
+    tg = W.tagger_corpus(25, 200, corpus_sentences=40_000)  # the bench shape: ~5% rare tokens
+    _compare_full(lambda dy, m: W.CharTagger(dy, m, tg), tg.sentences, n_steps=3, test="tagger")
 
 
 def test_bitwise_determinism_full_size():
