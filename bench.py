@@ -371,8 +371,11 @@ def measure(dy, cfg, K, Wm, world, rank, local, profile, seed=1):
     barrier()
     e0.record(stream)
     t_wall = time.perf_counter()
+    step_wall = []
     for i in range(K):
+        t_s = time.perf_counter()
         api_step(cg, data[Wm + i])
+        step_wall.append(time.perf_counter() - t_s)
     e1.record(stream)
     barrier()
     wall = time.perf_counter() - t_wall
@@ -416,7 +419,9 @@ def measure(dy, cfg, K, Wm, world, rank, local, profile, seed=1):
     res = {
         "value": value_units / (dev_ms * 1e-3), "unit": unit_of(cfg), "ms_per_step": dev_ms / K,
         "e2e": {"value": e2e_units / (e2e_ms * 1e-3), "unit": unit_of(cfg), "h2d_bytes_per_step": h2d_per_step,
-                "d2h_bytes_per_step": d2h_per_step, "ms_per_step": e2e_ms / K, "wall_s": wall},
+                "d2h_bytes_per_step": d2h_per_step, "ms_per_step": e2e_ms / K, "wall_s": wall,
+                # host wall time of each API step (diagnostic: the loop blocks on value(loss))
+                "step_wall_ms": {"median": 1e3 * statistics.median(step_wall), "max": 1e3 * max(step_wall)}},
         "gpu_launches": launches, "clocks": clk.summary(),
     }
     if not profile:

@@ -143,7 +143,19 @@ def _run_steps(dy, cg, model, task, batches, rule, n_steps, record):
 #   |gpu - ref| <= 1e-4 |ref| + 1e-6 max|ref|      (no fp64 band, no 1e-5 floor)
 # Tensors measured to need more are listed here by name with the measured
 # worst ratio err / tol (they still pass the calibrated comparator below).
-STRICT_STEP0_EXCEPTIONS: dict = {}
+#
+# ptb64: the recurrent-weight gradients (dW over K = T*B = 2240 rows, fed by
+# the backward recurrence) reach 1.6x / 1.3x of the strict tolerance at their
+# worst element (measured on B200, r02; every other tensor of every config is
+# <= 0.94).  The reference itself, fp32 vs fp64 from the same initial values,
+# sits at 0.27 / 0.34 of it on the same tensors (tests/golden has no fp64
+# trace; measured with the oracle), so these two carry a 25% margin over the
+# measured device value, and the calibrated comparator below still holds them
+# to rtol 1e-4.
+STRICT_STEP0_EXCEPTIONS: dict = {
+    ("ptb64_adam", "rnn.l0.Wh"): 2.05,  # measured 1.61-1.65
+    ("ptb64_sgd", "rnn.l0.Wx"): 1.65,   # measured 1.27-1.31
+}
 
 
 def _strict_step0(test, name, got, ref):
