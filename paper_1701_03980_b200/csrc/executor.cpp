@@ -1773,10 +1773,13 @@ static bool plan_cache_on() {
   return on;
 }
 
+// CUDA-graph replay of cached plans is opt-in (DG_CUDA_GRAPH=1): on the PTB
+// headline the loop is device-bound once plans are cached, and a capture
+// (~0.1-0.2 ms host) only pays off for plans that recur many times
 static bool cuda_graphs_on() {
   static const bool on = [] {
     const char* e = std::getenv("DG_CUDA_GRAPH");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }

@@ -11,7 +11,7 @@ with each fast path switched off, so the fallbacks stay parity-green too.
   DG_TC=0           SIMT GEMMs only
   DG_SCHED_CACHE=0  schedules rebuilt for every graph
   DG_PLAN_CACHE=0   launch plans rebuilt for every graph (no plan cache)
-  DG_CUDA_GRAPH=0   cached plans replayed launch by launch, not as CUDA graphs
+  DG_CUDA_GRAPH=1   cached plans replayed as CUDA graphs (default: launch by launch)
 """
 
 import os
@@ -34,7 +34,7 @@ VARIANTS = {
     "tensor_cores_off": {"DG_TC": "0"},
     "schedule_cache_off": {"DG_SCHED_CACHE": "0"},
     "plan_cache_off": {"DG_PLAN_CACHE": "0"},
-    "cuda_graph_off": {"DG_CUDA_GRAPH": "0"},
+    "cuda_graph_on": {"DG_CUDA_GRAPH": "1"},
 }
 
 
@@ -87,7 +87,8 @@ def test_plan_cache_and_cuda_graph_replay_are_bitwise_identical():
     labels and masks): the cached plans (patched data, CUDA-graph replay)
     give bit-identical losses and parameters to planning every graph."""
     outs = {}
-    for name, env in {"cached": {}, "uncached": {"DG_PLAN_CACHE": "0"}, "no_graph": {"DG_CUDA_GRAPH": "0"}}.items():
+    for name, env in {"cached": {"DG_CUDA_GRAPH": "1"}, "uncached": {"DG_PLAN_CACHE": "0"},
+                      "no_graph": {}}.items():
         r = subprocess.run([sys.executable, "-c", f"ROOT={ROOT!r}\n" + _REPLAY], cwd=ROOT, capture_output=True,
                            text=True, timeout=600, env=dict(os.environ, **env))
         assert r.returncode == 0, r.stderr[-3000:]
