@@ -20,6 +20,7 @@
 //      of a parameter are aggregated into ONE GEMM (K = all rows), lookup rows
 //      are flushed by an atomic-free sorted segmented scatter-add.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -1698,6 +1699,28 @@ static bool dry_run() {
   return on;
 }
 
+// DG_NVTX=1: NVTX ranges around planning and around every launch group
+// (named by op class), for nsys / ncu --nvtx timelines
+static bool nvtx_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("DG_NVTX");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+static const char* const kClassName[C_NCLASS] = {"gemm_fwd", "gemm_dx", "gemm_dw", "pnls_fwd", "pnls_bwd",
+                                                 "elementwise", "gather", "scatter_add", "bias_colsum", "other",
+                                                 "rnn_fwd", "rnn_bwd"};
+struct NvtxRange {
+  bool on;
+  explicit NvtxRange(const char* name) : on(nvtx_on()) {
+    if (on) nvtxRangePushA(name);
+  }
+  ~NvtxRange() {
+    if (on) nvtxRangePop();
+  }
+};
+
 // run launch closures in order (with CUDA events around the profiled op
 // classes); adds the kernel launches issued to *launched
 static int run_ops(dg_graph* g, std::vector<std::function<int(char*)>>& ops, std::vector<OpMeta>& meta,
@@ -1724,6 +1747,7 @@ static int run_ops(dg_graph* g, std::vector<std::function<int(char*)>>& ops, std
       return e && e[0] == '2';
     }();
     const auto t_op = std::chrono::steady_clock::now();
+    NvtxRange nv(mt.cls >= 0 && mt.cls < C_NCLASS ? kClassName[mt.cls] : "op");
     int n = ops[q](g->work_base);
     if (op_timing)
       std::fprintf(stderr, "[op] class %d launches %d host %.1f us\n", mt.cls, n,
@@ -2618,6 +2642,7 @@ static int do_forward(dg_graph* g, int upto) {
   }
 
   PlanTimer tm("forward");
+  NvtxRange nv_fwd("dg_forward");
   std::vector<int> active;
   active.reserve(upto - lo + 1);
   for (int i = lo; i <= upto; ++i) active.push_back(i);
@@ -3277,6 +3302,7 @@ int dg_backward(dg_graph* g, int32_t loss) {
     for (int k = 0; k < x.n_in; ++k) anc[g->inputs[x.in_off + k]] = 1;
   }
   PlanTimer tm("backward");
+  NvtxRange nv_bwd("dg_backward");
   std::vector<int> active;
   for (int i = 0; i <= loss; ++i)
     if (anc[i]) active.push_back(i);
