@@ -188,18 +188,22 @@ __global__ void chain_fwd_seq_kernel(ChainArgs a) {
 
 // every (slot, element) of a chain whose gradient slots are all distinct
 // (checked on the host): g of the last add is added to each independently
+// one thread per (target slot, chain, element): the len - 1 intermediate adds
+// and the len + 1 inputs each get the final add's gradient.  The final add's
+// own slot is the source and is never written (it would race with the reads
+// and leave d(final) doubled).
 __global__ void chain_bwd_par_kernel(ChainArgs a) {
   pdl_prologue();
   const int64_t per = (int64_t)a.n * a.size;
-  const int64_t total = (int64_t)(2 * a.len + 1) * per;
+  const int64_t total = (int64_t)(2 * a.len) * per;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int slot = static_cast<int>(t / per);
     const int64_t r = t - (int64_t)slot * per;
     const int j = static_cast<int>(r / a.size);
     const int64_t e = r - (int64_t)j * a.size;
     const float g = a.gfinal[j][e];
-    if (slot < a.len) a.gouts[(int64_t)slot * a.n + j][e] += g;
-    else a.gins[(int64_t)(slot - a.len) * a.n + j][e] += g;
+    if (slot + 1 < a.len) a.gouts[(int64_t)slot * a.n + j][e] += g;
+    else a.gins[(int64_t)(slot - (a.len - 1)) * a.n + j][e] += g;
   }
 }
 
@@ -1188,7 +1192,7 @@ int launch_chain_fwd(const ChainArgs& a, cudaStream_t s) {
 }
 int launch_chain_bwd(const ChainArgs& a, cudaStream_t s) {
   if (a.distinct) {
-    launch_k(chain_bwd_par_kernel, grid_for((int64_t)(2 * a.len + 1) * a.n * a.size), kThreads, 0, s, a);
+    launch_k(chain_bwd_par_kernel, grid_for((int64_t)(2 * a.len) * a.n * a.size), kThreads, 0, s, a);
     return 1;
   }
   launch_k(chain_bwd_kernel, grid_for((int64_t)a.size * a.n), kThreads, 0, s, a);

@@ -376,3 +376,28 @@ def test_custom_sink_receives_the_default_sinks_gradients():
         assert not lp.touched and not lp.gradient.any()
         assert sorted(set(sink.rows_seen[id(lp)])) == ref_t[id(lp)]
         assert np.allclose(sink.lookups[id(lp)], ref_l[id(lp)], rtol=1e-6, atol=1e-9)
+
+
+def test_loss_chain_gradients_are_exactly_one():
+    """A left-deep chain of scalar adds (the bench loss, bench/tasks.py:419)
+    runs as one prefix-sum unit: d loss / d loss stays the seed 1.0
+    (graph.py:151) and every term and intermediate sum gets exactly 1.0.
+    Regression: the element-parallel chain backward once also added into the
+    final add's own slot (doubling it, and racing with the reads of it)."""
+    from paper_1701_03980_b200.graph import Expression
+
+    cg, model = make_ctx(mb=16)
+    W = model.add_parameters((6, 4), "W")
+    terms = []
+    for k in range(40):
+        x = ops.input(cg, vec([0.1 * k, -0.2, 0.3, 0.05 * k]))
+        terms.append(ops.pickneglogsoftmax(ops.matmul(ops.parameter(cg, W), x), k % 6))
+    loss = terms[0]
+    sums = []
+    for t in terms[1:]:
+        loss = ops.add(loss, t)
+        sums.append(loss)
+    cg.backward(loss)
+    assert cg.gradient(loss).data.tolist() == [1.0]
+    for e in terms + sums[:-1]:
+        assert cg.gradient(e).data.tolist() == [1.0], cg.nodes[e.index].kind
