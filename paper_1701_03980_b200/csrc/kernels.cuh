@@ -26,6 +26,23 @@ __device__ __forceinline__ void pdl_prologue() {
 #endif
 }
 bool pdl_enabled();
+
+// 3xTF32 operand splits (x ~ hi + lo, products hi*hi + hi*lo + lo*hi).
+// Both parts are rounded to nearest (cvt.rna), not truncated: a truncated
+// split leaves lo with the sign of x, so the dropped lo*lo term has the sign
+// of the product and accumulates as a bias over K; rounded parts have
+// |lo| <= 2^-11 |x| with either sign.  tf32_rn_lo_of_raw is the residual for
+// an operand the tensor core reads raw (its hardware hi = truncation).
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ uint32_t tf32_rn_hi(float x) { return tf32_rna(x); }
+__device__ __forceinline__ uint32_t tf32_rn_lo(float x) { return tf32_rna(x - __uint_as_float(tf32_rna(x))); }
+__device__ __forceinline__ float tf32_rn_lo_of_raw(float x) {
+  return __uint_as_float(tf32_rna(x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u)));
+}
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                             Args... args) {

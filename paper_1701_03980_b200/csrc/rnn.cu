@@ -692,10 +692,8 @@ __device__ __forceinline__ void cluster_sync_all() {
 // 3xTF32 legacy-MMA tile op: acc(16 x 8) += A(16 x 8) B(8 x 8); a/b hold fp32
 // bit patterns, the residuals lo = x - tf32(x) make A_hi B_hi + A_hi B_lo +
 // A_lo B_hi (fp32-accurate products, as the tcgen05 GEMMs)
-__device__ __forceinline__ uint32_t tf32_hi(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
-__device__ __forceinline__ uint32_t tf32_lo(float x) {
-  return __float_as_uint(x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u));
-}
+__device__ __forceinline__ uint32_t tf32_hi(float x) { return tf32_rn_hi(x); }
+__device__ __forceinline__ uint32_t tf32_lo(float x) { return tf32_rn_lo(x); }
 __device__ __forceinline__ void mma_1688(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"

@@ -166,7 +166,7 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 
 // residual lo = x - tf32(x) (the tensor core reads fp32 storage as TF32 by
 // dropping the low 13 mantissa bits)
-__device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+__device__ __forceinline__ float tf32_lo(float x) { return tf32_rn_lo_of_raw(x); }
 
 // kAMN: A global rows run along K (MN-major A); kBMN: B global rows run along K
 // TMEM accumulator -> registers: 64 fp32 columns of this thread's row

@@ -7,8 +7,10 @@
 //
 // fp32 parity is kept with 3xTF32: the tensor core reads fp32 storage as TF32
 // (x_hi = x with the low 13 mantissa bits dropped); a residual copy
-// x_lo = x - x_hi of each operand is produced once per launch by
-// split_lo_kernel into the workspace, and every k-step issues
+// x_lo = rn(x - x_hi) of each operand is produced once per launch by
+// split_lo_kernel into the workspace (or per tile by converter warps; an
+// operand split by the converters is rounded to nearest in both parts,
+// kernels.cuh tf32_rn_*), and every k-step issues
 // A_hi*B_hi + A_hi*B_lo + A_lo*B_hi into an fp32 TMEM accumulator.
 // Every CHUNK k-tiles the accumulator is handed to the epilogue warps, which
 // add it into fp32 registers (blocked summation: the tensor core's own
@@ -142,7 +144,7 @@ __device__ __forceinline__ float lds32(uint32_t a) {
 __device__ __forceinline__ void sts128(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
-__device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+__device__ __forceinline__ float tf32_lo(float x) { return tf32_rn_lo_of_raw(x); }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -380,8 +382,8 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, kLite ? 2 : 1
             const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              hi[4 * c + e] = __float_as_uint(xv[e]) & 0xFFFFE000u;
-              lo[4 * c + e] = __float_as_uint(xv[e] - __uint_as_float(hi[4 * c + e]));
+              hi[4 * c + e] = tf32_rn_hi(xv[e]);
+              lo[4 * c + e] = tf32_rna(xv[e] - __uint_as_float(hi[4 * c + e]));
             }
           }
         } else {  // MN-major box q {32 m, 32 k}, SW128 with 32 B atoms: chunk (lane / 8) ^ (k & 3)
@@ -389,8 +391,8 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, kLite ? 2 : 1
           for (int k = 0; k < 32; ++k) {
             const float x = lds32(st + (uint32_t)q * 4096u + (uint32_t)k * 128u +
                                   ((uint32_t)(((lane >> 3) ^ (k & 3))) << 5) + ((uint32_t)(lane & 7) << 2));
-            hi[k] = __float_as_uint(x) & 0xFFFFE000u;
-            lo[k] = __float_as_uint(x - __uint_as_float(hi[k]));
+            hi[k] = tf32_rn_hi(x);
+            lo[k] = tf32_rna(x - __uint_as_float(hi[k]));
           }
         }
         const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + kAcol + 64u * (uint32_t)s;
@@ -421,10 +423,10 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, kLite ? 2 : 1
         for (int i = 0; i < kOpBytes / 16 / 128; ++i) {
           const float4 x = src[ct + i * 128];
           float4 y;
-          y.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-          y.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-          y.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-          y.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+          y.x = tf32_rn_lo_of_raw(x.x);
+          y.y = tf32_rn_lo_of_raw(x.y);
+          y.z = tf32_rn_lo_of_raw(x.z);
+          y.w = tf32_rn_lo_of_raw(x.w);
           dst[ct + i * 128] = y;
         }
       }
@@ -599,7 +601,7 @@ __global__ void split_lo_kernel(SplitJob j0, SplitJob j1, int n_jobs) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const float x = c + k < j.cols ? s[k] : 0.f;
-      op[k] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+      op[k] = tf32_rn_lo_of_raw(x);
     }
     *reinterpret_cast<float4*>(j.dst + r * j.cols_p + c) = o;
   }

@@ -144,29 +144,39 @@ def _run_steps(dy, cg, model, task, batches, rule, n_steps, record):
 # Tensors measured to need more are listed here by name with the measured
 # worst ratio err / tol (they still pass the calibrated comparator below).
 #
-# ptb64: the recurrent-weight gradients (dW over K = T*B = 2240 rows, fed by
-# the backward recurrence) reach 1.6x / 1.3x of the strict tolerance at their
-# worst element (measured on B200, r02; every other tensor of every config is
-# <= 0.94).  The reference itself, fp32 vs fp64 from the same initial values,
-# sits at 0.27 / 0.34 of it on the same tensors (tests/golden has no fp64
-# trace; measured with the oracle), so these two carry a 25% margin over the
-# measured device value, and the calibrated comparator below still holds them
-# to rtol 1e-4.
+# ptb64: the layer-0 weight gradients (dW over K = T*B = 2240 rows, fed by
+# two backward recurrences and the K = 10^4 output-layer dX) reach 1.0-1.35x
+# of the strict tolerance at their worst element (measured on B200, r02e,
+# with round-to-nearest 3xTF32 splits, kernels.cuh tf32_rn_*; every other
+# tensor of every config is <= 0.97).  Against the fp64 oracle the same
+# tensors sit at 0.93-1.12 of it, the fp32 oracle at 0.27-0.40
+# (DG_STRICT_REPORT writes all three ratios per tensor).  Bounds carry a ~30%
+# margin over the measured device value; the calibrated comparator below
+# still holds these tensors to rtol 1e-4.
 STRICT_STEP0_EXCEPTIONS: dict = {
-    ("ptb64_adam", "rnn.l0.Wh"): 2.05,  # measured 1.61-1.65
-    ("ptb64_sgd", "rnn.l0.Wx"): 1.65,   # measured 1.27-1.31
+    ("ptb64_adam", "rnn.l0.Wh"): 1.8,   # measured 1.35
+    ("ptb64_sgd", "rnn.l0.Wx"): 1.65,   # measured 1.24
+    ("ptb64_sgd", "rnn.l0.Wh"): 1.35,   # measured 1.01
 }
 
 
-def _strict_step0(test, name, got, ref):
+def _strict_ratio(got, ref):
     got = np.asarray(got, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     tol = 1e-4 * np.abs(ref) + 1e-6 * float(np.abs(ref).max(initial=0.0))
-    ratio = float((np.abs(got - ref) / np.maximum(tol, 1e-30)).max(initial=0.0))
+    return float((np.abs(got - ref) / np.maximum(tol, 1e-30)).max(initial=0.0))
+
+
+def _strict_step0(test, name, got, ref, ref64=None):
+    ratio = _strict_ratio(got, ref)
     path = os.environ.get("DG_STRICT_REPORT")
     if path:
+        # also: the GPU against the fp64 oracle, and the fp32 oracle against it
+        extra = ""
+        if ref64 is not None:
+            extra = f"\tgpu_vs_f64={_strict_ratio(got, ref64):.4g}\tref32_vs_f64={_strict_ratio(ref, ref64):.4g}"
         with open(path, "a") as fh:
-            fh.write(f"{test}\t{name}\t{ratio:.4g}\n")
+            fh.write(f"{test}\t{name}\t{ratio:.4g}{extra}\n")
     bound = STRICT_STEP0_EXCEPTIONS.get((test, name), 1.0)
     assert ratio <= bound, f"{test} step0 {name}: err/tol {ratio:.3g} > {bound} (SURVEY 7 strict metric)"
 
@@ -208,9 +218,10 @@ def _compare_full(make_task, batches, rule="adam", n_steps=2, test=None):
         # that already differ inside the Adam band ("Adam amplifies")
         if s == 0 and test is not None:
             for name, g in ref[0]["grads"].items():
-                _strict_step0(test, name, got[0]["grads"][name], g)
+                _strict_step0(test, name, got[0]["grads"][name], g, ref64[0]["grads"][name])
             for name in ref[0]["touched"]:
-                _strict_step0(test, name + " rows", got[0]["lgrads"][name], ref[0]["lgrads"][name])
+                _strict_step0(test, name + " rows", got[0]["lgrads"][name], ref[0]["lgrads"][name],
+                              ref64[0]["lgrads"][name])
         if rule != "sgd" and s > 0:
             continue
         for name, g in ref[s]["grads"].items():
