@@ -2163,6 +2163,10 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
     a.n_flags = flag;
     a.vec = vec_ok ? 1 : 0;
     a.trace = rnn_trace_enabled() ? (std::getenv("DG_RNN_TRACE")[0] == '2' ? 2 : 1) : 0;
+    {
+      static const int knob = std::getenv("DG_RNN_KNOB") ? std::atoi(std::getenv("DG_RNN_KNOB")) : 0;
+      a.knob = knob;
+    }
     // cluster mode: one cluster per (chain, batch slice) exchanging through
     // distributed shared memory; needs equal unit-block counts (<= 16)
     int cl = a.ch[0].n_u;

@@ -40,8 +40,12 @@ __device__ __forceinline__ uint32_t tf32_rna(float x) {
 }
 __device__ __forceinline__ uint32_t tf32_rn_hi(float x) { return tf32_rna(x); }
 __device__ __forceinline__ uint32_t tf32_rn_lo(float x) { return tf32_rna(x - __uint_as_float(tf32_rna(x))); }
+// cheap forms for finite operands inside hot loops: round-half-away of the
+// magnitude in two integer ops (no NaN/Inf handling, which cvt.rna spends
+// three more instructions on)
+__device__ __forceinline__ uint32_t tf32_rn_bits(float x) { return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u; }
 __device__ __forceinline__ float tf32_rn_lo_of_raw(float x) {
-  return __uint_as_float(tf32_rna(x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u)));
+  return __uint_as_float(tf32_rn_bits(x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u)));
 }
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
@@ -148,6 +152,7 @@ struct RnnArgs {
   int n_chains, ctas, bs, cj, n_flags;
   int vec;     // every staged row is 16B aligned with a multiple-of-4 width (cp.async path)
   int trace;   // record the per-step timeline (rnn_trace_read)
+  int knob;    // DG_RNN_KNOB: A/B switches of the recurrence kernels (diagnostics)
   int gx;      // G slots hold b + Wx x_t already (chains run with K_in = 0: recurrent part only)
   int* flags;  // zeroed by the launcher
   RnnChain ch[kRnnMaxChains];

@@ -692,8 +692,18 @@ __device__ __forceinline__ void cluster_sync_all() {
 // 3xTF32 legacy-MMA tile op: acc(16 x 8) += A(16 x 8) B(8 x 8); a/b hold fp32
 // bit patterns, the residuals lo = x - tf32(x) make A_hi B_hi + A_hi B_lo +
 // A_lo B_hi (fp32-accurate products, as the tcgen05 GEMMs)
+// Splits for 3xTF32.  Resident weight fragments (split once per launch):
+// both parts rounded to nearest (cvt.rna, kernels.cuh), so lo has either
+// sign.  Per-step operands (h_{t-1} forward, dG_t backward, split inside the
+// k-loop by every warp): hi truncated, lo = x - hi exact.  The k-loop is
+// bound by the legacy tensor pipe and shared-memory bandwidth together
+// (tools/rnn_step_probe.cu), so every ALU op per element shows: rounding hi
+// there costs +14% on the forward step (cvt.rna on both parts +17%) for no
+// measurable change of the parity ratios (r02 A/B, tools/gpu/gpu_ab_src.sh).
 __device__ __forceinline__ uint32_t tf32_hi(float x) { return tf32_rn_hi(x); }
 __device__ __forceinline__ uint32_t tf32_lo(float x) { return tf32_rn_lo(x); }
+__device__ __forceinline__ uint32_t step_hi(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
+__device__ __forceinline__ uint32_t step_lo(float x, uint32_t hi) { return __float_as_uint(x - __uint_as_float(hi)); }
 __device__ __forceinline__ void mma_1688(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
@@ -853,8 +863,8 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_fwd_cl_kernel(const __grid_
         uint32_t ah[4], al[4];
 #pragma unroll
         for (int z = 0; z < 4; ++z) {
-          ah[z] = tf32_hi(av[z]);
-          al[z] = tf32_lo(av[z]);
+          ah[z] = step_hi(av[z]);
+          al[z] = step_lo(av[z], ah[z]);
         }
         float* c3 = ac[(q & 1) * 3];
         mma_1688(c3, al, __float_as_uint(b.x), __float_as_uint(b.y));
@@ -1092,8 +1102,8 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
           const float av[4] = {v0 ? r0[k] : 0.f, v1 ? r1[k] : 0.f, v0 ? r0[k + 4] : 0.f, v1 ? r1[k + 4] : 0.f};
 #pragma unroll
           for (int z = 0; z < 4; ++z) {
-            ah[q][z] = tf32_hi(av[z]);
-            al[q][z] = tf32_lo(av[z]);
+            ah[q][z] = step_hi(av[z]);
+            al[q][z] = step_lo(av[z], ah[q][z]);
           }
         }
         const uint32_t rbase = recv_local + 4u * (uint32_t)(((it & 1) * C.n_u + (int)my_rank) * BS * kU);

@@ -382,8 +382,8 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, kLite ? 2 : 1
             const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              hi[4 * c + e] = tf32_rn_hi(xv[e]);
-              lo[4 * c + e] = tf32_rna(xv[e] - __uint_as_float(hi[4 * c + e]));
+              hi[4 * c + e] = tf32_rn_bits(xv[e]);
+              lo[4 * c + e] = __float_as_uint(xv[e] - __uint_as_float(hi[4 * c + e]));
             }
           }
         } else {  // MN-major box q {32 m, 32 k}, SW128 with 32 B atoms: chunk (lane / 8) ^ (k & 3)
@@ -391,8 +391,8 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, kLite ? 2 : 1
           for (int k = 0; k < 32; ++k) {
             const float x = lds32(st + (uint32_t)q * 4096u + (uint32_t)k * 128u +
                                   ((uint32_t)(((lane >> 3) ^ (k & 3))) << 5) + ((uint32_t)(lane & 7) << 2));
-            hi[k] = tf32_rn_hi(x);
-            lo[k] = tf32_rna(x - __uint_as_float(hi[k]));
+            hi[k] = tf32_rn_bits(x);
+            lo[k] = __float_as_uint(x - __uint_as_float(hi[k]));
           }
         }
         const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + kAcol + 64u * (uint32_t)s;
