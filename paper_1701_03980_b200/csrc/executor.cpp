@@ -35,6 +35,7 @@
 #include <numeric>
 #include <string>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/dyngpu.h"
@@ -217,6 +218,17 @@ struct dg_graph_impl;
 namespace dg {
 struct Schedule;
 struct CachedPlan;
+// Gradient of an INPUT leaf that the backward pass leaves as per-slice
+// partial sums (the batch-1 initial states of the LSTM recurrences): the
+// reference computes it during backward, but only gradient() can observe it,
+// so the final slice sum runs when gradient() asks for that node.
+struct LazyGrad {
+  int node;
+  float* dst;
+  const float* part;
+  int n_s, H;
+};
+
 }
 
 struct dg_graph {
@@ -272,6 +284,7 @@ struct dg_graph {
   std::vector<std::shared_ptr<dg::CachedPlan>> pcache[2];
   mutable uint64_t memo_key = 0;   // structure hash of memo_sched
   uint64_t fwd_hist = 0;   // forward calls of this generation (placement history)
+  std::vector<dg::LazyGrad> lazy;  // pending input-leaf gradients of the last backward
 };
 
 struct dg_trainer {
@@ -1148,6 +1161,8 @@ struct OpMeta {
 struct Plan {
   Blob blob;
   std::vector<std::function<int(char*)>> ops;  // arg: device blob base
+  std::vector<LazyGrad> lazy;
+  size_t lazy_floats = 0;  // used part of the lazy-partials region
   std::vector<OpMeta> meta;
   size_t scratch_need = 0;
   void tag(int cls, double flops, double bytes) {
@@ -1197,6 +1212,7 @@ struct CachedPlan {
   std::vector<std::function<int(char*)>> ops;
   std::vector<OpMeta> meta;
   PatchRec patch;
+  std::vector<LazyGrad> lazy;
   int64_t kernel_launches = 0;  // launches issued by `ops` (counted at build)
   cudaGraphExec_t exec = nullptr;
   int replays = 0;
@@ -1277,7 +1293,15 @@ static constexpr size_t kDummyBytes = 16u << 20;
 static constexpr size_t kCounterBytes = 1u << 20;
 static inline size_t blob_cap(const dg_graph* g) { return (g->work_bytes / 8) & ~size_t(255); }
 static inline char* scratch_base(dg_graph* g) { return g->work_base + blob_cap(g); }
-static inline size_t scratch_bytes(dg_graph* g) { return g->work_bytes - blob_cap(g) - kDummyBytes - kCounterBytes; }
+// per-slice partial sums of lazily summed input-leaf gradients (LazyGrad):
+// written by the backward recurrence, read when gradient() asks
+static constexpr size_t kLazyBytes = 1u << 20;
+static inline size_t scratch_bytes(dg_graph* g) {
+  return g->work_bytes - blob_cap(g) - kDummyBytes - kCounterBytes - kLazyBytes;
+}
+static inline float* lazy_base(dg_graph* g) {
+  return reinterpret_cast<float*>(g->work_base + g->work_bytes - kDummyBytes - kCounterBytes - kLazyBytes);
+}
 static inline float* dummy_base(dg_graph* g) {
   return reinterpret_cast<float*>(g->work_base + g->work_bytes - kDummyBytes - kCounterBytes);
 }
@@ -1638,6 +1662,7 @@ int dg_graph_renew(dg_graph* g) {
   g->bwd_cursor = 0;
   g->has_grads = false;
   g->fwd_hist = 0;
+  g->lazy.clear();
   return DG_OK;
 }
 
@@ -1849,6 +1874,7 @@ static void plan_cache_store(dg_graph* g, int which, uint64_t key, Plan& plan, s
   cp->ops.assign(std::make_move_iterator(plan.ops.begin()), std::make_move_iterator(plan.ops.begin() + static_ops));
   cp->meta.assign(plan.meta.begin(), plan.meta.begin() + static_ops);
   cp->patch = std::move(rec);
+  cp->lazy = plan.lazy;
   cp->kernel_launches = launched_static;
   auto& v = g->pcache[which];
   v.insert(v.begin(), std::move(cp));
@@ -2086,8 +2112,10 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
     }
     flush_gemm(g, plan, *gb);
   }
+  std::unordered_set<int> init_h_done, init_c_done;  // chains (by G_0) whose initial-state grads the kernel owns
   for (const auto& L : launches) {
     RnnArgs a{};
+    std::vector<const RnnChainPlan*> cps;
     a.flags = flag_base(g);
     a.gx = bwd ? 0 : 1;
     a.bs = S.rnns[L[0]].bs;
@@ -2099,6 +2127,7 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
       const RnnStack& sk = S.rnns[sid];
       const int base = a.n_chains;
       for (const RnnChainPlan& cp : sk.chains) {
+        cps.push_back(&cp);
         RnnChain& c = a.ch[a.n_chains++];
         const int T = (int)cp.G.size();
         c.T = T;
@@ -2197,15 +2226,71 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
       }
     }
     use_cl = use_cl && smem_cl <= kSmemMax;
+    // decided here, not at launch: the initial-state gradients below exist
+    // only in the cluster backward kernel
+    use_cl = use_cl && rnn_cluster_fits(a, bwd, smem_cl, cl);
+    // initial-state gradients inside the backward cluster kernel (one more
+    // reduce-scatter round gives dh_{-1}): per-row h_{-1} is accumulated in
+    // place, batch-1 h_{-1} / c_{-1} leave per-slice row sums that one
+    // rnn_part_sum_kernel adds up -- now for computed / parameter targets,
+    // on gradient() for INPUT leaves (LazyGrad)
+    RnnPartSum eager{};
+    if (bwd && use_cl) {
+      std::vector<int> own_h;
+      const size_t cap = kLazyBytes / 4;
+      for (int k = 0; k < a.n_chains; ++k) {
+        const RnnChainPlan& cp = *cps[k];
+        RnnChain& c = a.ch[k];
+        const int hnode = g->inputs[g->nodes[cp.G[0]].in_off + 4];
+        const int cnode = cp.cells[0].ins[1];
+        const Node& hn = g->nodes[hnode];
+        const Node& cn = g->nodes[cnode];
+        const size_t need = (size_t)cp.n_s * cp.H;
+        auto add_part = [&](int node, float*& part) {
+          part = lazy_base(g) + plan.lazy_floats;
+          plan.lazy_floats += (need + 63) & ~size_t(63);
+          const Node& x = g->nodes[node];
+          if (x.kind == DG_OP_INPUT) {
+            plan.lazy.push_back(LazyGrad{node, x.grad, part, cp.n_s, cp.H});
+          } else {
+            eager.H[eager.n] = cp.H;
+            eager.n_s[eager.n] = cp.n_s;
+            eager.dst[eager.n] = x.grad;
+            eager.part[eager.n] = part;
+            eager.n++;
+          }
+        };
+        if (hn.batch == cp.B && std::find(own_h.begin(), own_h.end(), hnode) == own_h.end()) {
+          c.h0 = 1;  // per row, in place (no other chain of this launch adds into it)
+          own_h.push_back(hnode);
+          init_h_done.insert(cp.G[0]);
+        } else if (hn.batch == 1 && cp.B > 1 && plan.lazy_floats + need <= cap) {
+          c.h0 = 2;
+          add_part(hnode, c.h0_part);
+          init_h_done.insert(cp.G[0]);
+        }
+        if (cn.batch == 1 && cp.B > 1 && plan.lazy_floats + need <= cap) {
+          c.c0 = 1;
+          add_part(cnode, c.c0_part);
+          init_c_done.insert(cp.G[0]);
+        }
+      }
+    }
     plan.ops.push_back([a, smem, smem_cl, use_cl, cl, bwd](char*) {
       const cudaStream_t st = g_launch_stream;
       if (use_cl) {
+        // residency was checked while planning; the fallback kernels do not
+        // produce the initial-state gradients the plan counts on
         const int n = launch_rnn_cluster(a, bwd, smem_cl, cl, st);
-        if (n != -2) return n;  // -2: the clusters cannot all be resident
+        return n == -2 ? -1 : n;
       }
       return launch_rnn(a, bwd, smem, st);
     });
     plan.tag(bwd ? C_RNN_BWD : C_RNN_FWD, flops, bytes);
+    if (eager.n) {
+      plan.ops.push_back([eager](char*) { return launch_rnn_part_sum(eager, g_launch_stream); });
+      plan.tag(C_ELEMWISE, 0.0, 0.0);
+    }
   }
   if (!bwd) return;
 
@@ -2266,8 +2351,8 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
         for (int t = 0; t < T; ++t) xs.push_back(g->inputs[g->nodes[cp.G[t]].in_off + 2]);
         add_dx(xs, param_at(cp.hWx)->val, cp.K_in, dxrows);
       }
-      // h_{-1}: dX = dG_0 Wh
-      {
+      // h_{-1}: dX = dG_0 Wh (unless the backward kernel produced it)
+      if (!init_h_done.count(cp.G[0])) {
         const Node& G0 = g->nodes[cp.G[0]];
         const int hnode = g->inputs[G0.in_off + 4];
         const Node& hn = g->nodes[hnode];
@@ -2277,7 +2362,7 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
       }
       // c_{-1} broadcast over the batch: batch sum of dc_0 * f_0
       const Node& cpn = g->nodes[cp.cells[0].ins[1]];
-      if (cpn.batch == 1 && Bt > 1) {
+      if (cpn.batch == 1 && Bt > 1 && !init_c_done.count(cp.G[0])) {
         if (c0.n == kRnnMaxChains) {
           plan.ops.push_back([c0](char*) {
       const cudaStream_t st = g_launch_stream; return launch_rnn_c0(c0, st); });
@@ -3650,6 +3735,7 @@ int dg_backward(dg_graph* g, int32_t loss) {
     }
   }
   tm.lap("launch");
+  g->lazy = hit ? hit->lazy : plan.lazy;  // supersedes the previous backward's
   g->bwd_cursor = cur;
   g->bwd_alloc_count += loss + 1;
   g->has_grads = true;
@@ -3680,6 +3766,28 @@ int dg_gradient(dg_graph* g, int32_t node, float* host_dst, int64_t n) {
   const Node& x = g->nodes[node];
   if (!g->has_grads || !x.grad) return fail(DG_SHAPE, "no backward pass has populated this node yet");
   if (n != x.size()) return fail(DG_SHAPE, "gradient buffer size mismatch");
+  // slice sums left by the last backward for this INPUT leaf (LazyGrad)
+  for (size_t i = 0; i < g->lazy.size();) {
+    if (g->lazy[i].node != node) {
+      ++i;
+      continue;
+    }
+    RnnPartSum ps{};
+    for (size_t q = i; q < g->lazy.size() && ps.n < kRnnMaxChains;) {
+      if (g->lazy[q].node == node) {
+        const LazyGrad& L = g->lazy[q];
+        ps.H[ps.n] = L.H;
+        ps.n_s[ps.n] = L.n_s;
+        ps.dst[ps.n] = L.dst;
+        ps.part[ps.n] = L.part;
+        ps.n++;
+        g->lazy.erase(g->lazy.begin() + (ptrdiff_t)q);
+      } else {
+        ++q;
+      }
+    }
+    if (launch_rnn_part_sum(ps, g->stream) < 0) return fail(DG_CUDA, "initial-state gradient sum failed");
+  }
   DG_CUDA_TRY(cudaMemcpyAsync(host_dst, x.grad, (size_t)n * 4, cudaMemcpyDeviceToHost, g->stream));
   DG_CUDA_TRY(cudaStreamSynchronize(g->stream));
   return DG_OK;

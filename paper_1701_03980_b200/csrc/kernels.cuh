@@ -147,6 +147,13 @@ struct RnnChain {
   const float* const* val;  // [T][kRnnSlots] (device)
   float* const* grad;       // [T][kRnnSlots] (device, backward)
   const int* b1;            // [T] bit0 x_t, bit1 h_{t-1}, bit2 c_{t-1} is batch-1
+  // initial-state gradients computed by the backward cluster kernel: h0 = 1
+  // adds dh_{-1} into h_{-1}'s per-row slot, h0 = 2 writes per-slice row sums
+  // to h0_part[n_s][H] (batch-1 h_{-1}); c0 = 1 writes per-slice row sums of
+  // the batch-1 c_{-1} term to c0_part[n_s][H]
+  int h0, c0;
+  float* h0_part;
+  float* c0_part;
 };
 struct RnnArgs {
   int n_chains, ctas, bs, cj, n_flags;
@@ -165,6 +172,16 @@ struct RnnC0 {
   const float* dc[kRnnMaxChains];
   const float* af[kRnnMaxChains];
 };
+// dst[k][u] += sum_s part[k][s * H + u] for every item k (in order)
+struct RnnPartSum {
+  int n;
+  int H[kRnnMaxChains], n_s[kRnnMaxChains];
+  float* dst[kRnnMaxChains];
+  const float* part[kRnnMaxChains];
+};
+int launch_rnn_part_sum(const RnnPartSum& a, cudaStream_t s);
+// the cluster launch of these arguments can have every cluster resident
+bool rnn_cluster_fits(const RnnArgs& a, bool backward, size_t smem, int cluster);
 int rnn_rows_per_cta(int B);
 size_t rnn_fwd_smem(int K, int bs);
 size_t rnn_bwd_smem(int gw, int gw_c, int bs, int cj);

@@ -1019,8 +1019,9 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
       mbar_init_cl(&rec_full[0], 1);
       mbar_init_cl(&rec_full[1], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      if (C.T > 1) mbar_arm(&rec_full[0], slot_bytes);  // iteration 0
-      if (C.T > 2) mbar_arm(&rec_full[1], slot_bytes);  // iteration 1
+      const int R = C.T - 1 + (C.h0 ? 1 : 0);  // reduce-scatter rounds (+1: dh_{-1})
+      if (R > 0) mbar_arm(&rec_full[0], slot_bytes);  // iteration 0
+      if (R > 1) mbar_arm(&rec_full[1], slot_bytes);  // iteration 1
     }
   }
   pdl_prologue();  // weight staging above overlaps the preceding grid
@@ -1037,6 +1038,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
   const uint32_t recv_local = smem_addr(recv);
   const uint32_t bar_local = smem_addr(&rec_full[0]);
   const int g8 = lane >> 2, t4 = lane & 3;
+  const int R = C.T - 1 + (C.h0 ? 1 : 0);
   float rec = 0.f, dc_carry = 0.f;
   float ao = 0.f, ai = 0.f, ag = 0.f, tc = 0.f, af = 0.f, ck = 0.f, gh_ext = 0.f, gc_ext = 0.f;
   auto load_cell = [&](const StepPtrs2& P) {
@@ -1082,7 +1084,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
       dpf = af * (1.f - af) * d_f;
       dc_carry = dc * af;
     }
-    if (t > 0) {
+    if (t > 0 || C.h0) {  // t == 0: the round that yields dh_{-1}
       if (cb < BS) {
         float* dl = dGl + (size_t)cb * (kCU + 4);
         dl[0 * kU + cj] = dpi;
@@ -1131,7 +1133,7 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
                         make_float2(ac[0][2] + ac[1][2] + ac[2][2], ac[0][3] + ac[1][3] + ac[2][3]), rb);
         }
       }
-      if (warp == 1) {
+      if (warp == 1 && t > 0) {
         if (lane < kRnnSlots) {
           sp[(t - 1) & 1].v[lane] = nv;
           sp[(t - 1) & 1].d[lane] = nd;
@@ -1163,16 +1165,53 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_bwd_cl_kernel(const __grid_
       D[S_PF][r] = dpf;
       if (t == 0 && !cb1) D[S_CP][r] += dc_carry;
     }
-    if (t > 0) {
-      load_cell(sp[(t - 1) & 1]);
+    if (t > 0 || C.h0) {
+      if (t > 0) load_cell(sp[(t - 1) & 1]);
       mbar_wait_cl(&rec_full[it & 1], (it >> 1) & 1);
-      if (tid == 0 && it + 2 <= C.T - 2) mbar_arm(&rec_full[it & 1], slot_bytes);
+      if (tid == 0 && it + 2 <= R - 1) mbar_arm(&rec_full[it & 1], slot_bytes);
       rec = 0.f;
       if (cb < BS) {
         const float* slot = recv + (size_t)(it & 1) * C.n_u * BS * kU + (size_t)cb * kU + cj;
         for (int q = 0; q < C.n_u; ++q) rec += slot[(size_t)q * BS * kU];
       }
     }
+  }
+  // initial-state gradients (t = -1), replacing a dX GEMM + row reduce and
+  // rnn_c0_kernel launch per chain: rec now holds dh_{-1}[row, j], dc_carry
+  // the batch-1 c_{-1} term dc_0 * f_0 of (row, j)
+  if (C.h0 == 1 && mine) sp[0].d[S_HP][r] += rec;  // per-row h_{-1}
+  if (C.h0 == 2 || C.c0) {
+    // batch-1 targets: this slice's rows summed in fixed order into
+    // part[s][j] (the slices' partials are summed by rnn_part_sum_kernel)
+    __shared__ float red[2][16][kU + 1];
+    if (cb < BS) {
+      red[0][cb][cj] = mine ? rec : 0.f;
+      red[1][cb][cj] = mine ? dc_carry : 0.f;
+    }
+    csync();
+    if (tid < 2 * kU) {
+      const int which = tid / kU, u = tid - which * kU;
+      float* part = which == 0 ? (C.h0 == 2 ? C.h0_part : nullptr) : (C.c0 ? C.c0_part : nullptr);
+      if (part && j0 + u < C.H) {
+        float acc = 0.f;
+        for (int b = 0; b < BS; ++b) acc += red[which][b][u];
+        part[(size_t)s * C.H + j0 + u] = acc;
+      }
+    }
+  }
+}
+
+// dst[u] += sum_s part[s][u] over the batch slices of each item, items in
+// order, one block (initial-state gradients of batch-1 h_{-1} / c_{-1})
+__global__ void rnn_part_sum_kernel(RnnPartSum a) {
+  pdl_prologue();
+  for (int k = 0; k < a.n; ++k) {
+    for (int u = threadIdx.x; u < a.H[k]; u += blockDim.x) {
+      float acc = 0.f;
+      for (int q = 0; q < a.n_s[k]; ++q) acc += a.part[k][(size_t)q * a.H[k] + u];
+      a.dst[k][u] += acc;
+    }
+    __syncthreads();  // a later item may target the same node
   }
 }
 
@@ -1243,6 +1282,52 @@ int launch_bwd_bs(const RnnArgs& a, size_t smem, cudaStream_t s) {
   return 1;
 }
 
+// max co-resident clusters of kernel k at this cluster size and shared
+// memory (cached per (kernel, cluster size, 4 KiB smem bucket))
+cudaError_t cluster_active(void (*k)(const RnnArgs), const cudaLaunchConfig_t& cfg, int cluster, size_t smem,
+                           int* active) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::tuple<const void*, int, size_t>, int>> memo;
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(k), cluster, (smem + 4095) / 4096);
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& m : memo)
+    if (m.first == key) {
+      *active = m.second;
+      return cudaSuccess;
+    }
+  cudaLaunchConfig_t q = cfg;
+  q.dynamicSmemBytes = ((smem + 4095) / 4096) * 4096;
+  const cudaError_t oe = cudaOccupancyMaxActiveClusters(active, k, &q);
+  if (oe == cudaSuccess) memo.push_back({key, *active});
+  return oe;
+}
+
+template <int BS>
+void (*cl_kernel(bool bwd))(const RnnArgs) {
+  return bwd ? rnn_bwd_cl_kernel<BS> : rnn_fwd_cl_kernel<BS>;
+}
+
+template <int BS>
+bool cl_fits_bs(const RnnArgs& a, bool bwd, size_t smem, int cluster) {
+  void (*k)(const RnnArgs) = cl_kernel<BS>(bwd);
+  if (!smem_attr_once(k, true)) return false;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.ctas);
+  cfg.blockDim = dim3(kClThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int active = 0;
+  const cudaError_t oe = cluster_active(k, cfg, cluster, smem, &active);
+  if (oe != cudaSuccess) cudaGetLastError();
+  return oe == cudaSuccess && active * cluster >= a.ctas;
+}
+
 template <int BS>
 int launch_cl_bs(const RnnArgs& a, bool bwd, size_t smem, int cluster, cudaStream_t s) {
   void (*k)(const RnnArgs) = bwd ? rnn_bwd_cl_kernel<BS> : rnn_fwd_cl_kernel<BS>;
@@ -1259,28 +1344,9 @@ int launch_cl_bs(const RnnArgs& a, bool bwd, size_t smem, int cluster, cudaStrea
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  // every cluster must be resident at once (stacked chains wait on each other);
-  // the occupancy answer is cached per (kernel, cluster size, smem bucket)
+  // every cluster must be resident at once (stacked chains wait on each other)
   int active = 0;
-  cudaError_t oe = cudaSuccess;
-  {
-    static std::mutex mu;
-    static std::vector<std::pair<std::tuple<const void*, int, size_t>, int>> memo;
-    const auto key = std::make_tuple(reinterpret_cast<const void*>(k), cluster, (smem + 4095) / 4096);
-    std::lock_guard<std::mutex> lk(mu);
-    bool hit = false;
-    for (auto& m : memo)
-      if (m.first == key) {
-        active = m.second;
-        hit = true;
-      }
-    if (!hit) {
-      cudaLaunchConfig_t q = cfg;
-      q.dynamicSmemBytes = ((smem + 4095) / 4096) * 4096;
-      oe = cudaOccupancyMaxActiveClusters(&active, k, &q);
-      if (oe == cudaSuccess) memo.push_back({key, active});
-    }
-  }
+  const cudaError_t oe = cluster_active(k, cfg, cluster, smem, &active);
   if (rnn_trace_enabled())
     fprintf(stderr, "[rnn] %s cluster %d smem %zu ctas %d: max active clusters %d (%s)\n", bwd ? "bwd" : "fwd",
             cluster, smem, a.ctas, active, cudaGetErrorString(oe));
@@ -1333,6 +1399,16 @@ bool rnn_enabled() {
   return !(e && e[0] == '0');
 }
 
+bool rnn_cluster_fits(const RnnArgs& a, bool backward, size_t smem, int cluster) {
+  switch (a.bs) {
+    case 16: return cl_fits_bs<16>(a, backward, smem, cluster);
+    case 8: return cl_fits_bs<8>(a, backward, smem, cluster);
+    case 4: return cl_fits_bs<4>(a, backward, smem, cluster);
+    case 2: return cl_fits_bs<2>(a, backward, smem, cluster);
+    default: return cl_fits_bs<1>(a, backward, smem, cluster);
+  }
+}
+
 int launch_rnn_cluster(const RnnArgs& a, bool backward, size_t smem, int cluster, cudaStream_t s) {
   // global arrival counters only carry cross-chain (stacked) dependencies here
   bool cross = false;
@@ -1369,6 +1445,12 @@ int rnn_trace_read(unsigned long long* host, size_t n) {
 bool rnn_trace_enabled() {
   const char* e = std::getenv("DG_RNN_TRACE");
   return e && (e[0] == '1' || e[0] == '2');
+}
+
+int launch_rnn_part_sum(const RnnPartSum& a, cudaStream_t s) {
+  if (a.n == 0) return 0;
+  launch_k(rnn_part_sum_kernel, 1, 256, 0, s, a);
+  return 1;
 }
 
 int launch_rnn_c0(const RnnC0& a, cudaStream_t s) {
