@@ -87,14 +87,22 @@ __global__ void ew_bwd_flat_kernel(EwArgs a) {
         break;
       }
       case EW_SCALE: a.ga[j][r] += a.scalar * g; break;
-      case EW_ADD:
-        a.ga[j][r] += g;
-        a.gb[j][r] += g;
-        break;
       default: {
-        const float av = a.a[j][r], bv = a.b[j][r];
-        a.ga[j][r] += g * bv;
-        a.gb[j][r] += g * av;
+        // both old gradient values are read before either store (a store
+        // would otherwise order the second read behind it); x op x keeps
+        // the sequential (ga + ca) + cb
+        const bool add = a.kind == EW_ADD;
+        const float av = add ? 0.f : a.a[j][r], bv = add ? 0.f : a.b[j][r];
+        const float ca = add ? g : g * bv, cb = add ? g : g * av;
+        float* pa = a.ga[j] + r;
+        float* pb = a.gb[j] + r;
+        const float oa = *pa, ob = *pb;
+        if (pa == pb) {
+          *pa = (oa + ca) + cb;
+        } else {
+          *pa = oa + ca;
+          *pb = ob + cb;
+        }
         break;
       }
     }
@@ -245,9 +253,12 @@ __global__ void __launch_bounds__(256) cell_fwd_kernel(CellArgs a) {
     auto V = [&](int slot) { return sv[slot]; };
     const float* G = V(0) + (int64_t)b * a.gw;
     const float xi = G[a.off_i + u], xo = G[a.off_o + u], xg = G[a.off_g + u];
-    float xf[M > 0 ? M : 1];
+    float xf[M > 0 ? M : 1], ck[M > 0 ? M : 1];
 #pragma unroll
-    for (int k = 0; k < M; ++k) xf[k] = G[a.off_f[k] + u];
+    for (int k = 0; k < M; ++k) {
+      xf[k] = G[a.off_f[k] + u];
+      ck[k] = V(1 + k)[a.cext_b1[k] ? u : r];  // loaded before any store (no store-to-load waits)
+    }
     const_cast<float*>(V(S.pick0 + S.gi()))[r] = xi;
     const_cast<float*>(V(S.pick0 + S.go()))[r] = xo;
     const_cast<float*>(V(S.pick0 + S.gg()))[r] = xg;
@@ -262,8 +273,7 @@ __global__ void __launch_bounds__(256) cell_fwd_kernel(CellArgs a) {
       const_cast<float*>(V(S.pick0 + S.gf(k)))[r] = xf[k];
       const float af = sigmoidf_ref(xf[k]);
       const_cast<float*>(V(S.act0 + S.gf(k)))[r] = af;
-      const float ck = V(1 + k)[a.cext_b1[k] ? u : r];
-      const float p = af * ck;
+      const float p = af * ck[k];
       const_cast<float*>(V(S.prod0 + 1 + k))[r] = p;
       c = c + p;
       const_cast<float*>(V(S.add0 + k))[r] = c;
@@ -316,48 +326,69 @@ __global__ void __launch_bounds__(256) cell_bwd_kernel(CellArgs a) {
     for (int k = 0; k < M; ++k) acc_c[k] = 0.f;
     for (int b = b_lo; b < b_hi; b += b_step) {
       const int64_t r = (int64_t)b * a.H + u;
+      float* dG = D(0) + (int64_t)b * a.gw;
+      // every load first: the slots are distinct nodes, but the compiler
+      // cannot know, so a load after a store to another slot would wait for
+      // the store (one L2 round trip per read-modify-write otherwise)
       const float gh = D(S.h)[r];
       const float ao = V(S.act0 + S.go())[r], ai = V(S.act0 + S.gi())[r], ag = V(S.act0 + S.gg())[r];
       const float tc = V(S.tc)[r];
-      // h = o * tanh(c)
+      const float dc_ext = D(S.c)[r];
+      const float o_tc = D(S.tc)[r], o_ao = D(S.act0 + S.go())[r], o_ai = D(S.act0 + S.gi())[r];
+      const float o_ag = D(S.act0 + S.gg())[r];
+      const float o_pi = D(S.pick0 + S.gi())[r], o_po = D(S.pick0 + S.go())[r], o_pg = D(S.pick0 + S.gg())[r];
+      const float o_gi = dG[a.off_i + u], o_go = dG[a.off_o + u], o_gg = dG[a.off_g + u];
+      const float o_p0 = M > 0 ? D(S.prod0)[r] : 0.f;
+      float o_add[M > 1 ? M - 1 : 1], o_pk[M > 0 ? M : 1], o_af[M > 0 ? M : 1], o_pf[M > 0 ? M : 1];
+      float o_gf[M > 0 ? M : 1], ck[M > 0 ? M : 1], af[M > 0 ? M : 1], o_ck[M > 0 ? M : 1];
+#pragma unroll
+      for (int k = 0; k + 1 < M; ++k) o_add[k] = D(S.add0 + k)[r];
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        const int64_t rc = a.cext_b1[k] ? u : r;
+        o_pk[k] = D(S.prod0 + 1 + k)[r];
+        ck[k] = V(1 + k)[rc];
+        af[k] = V(S.act0 + S.gf(k))[r];
+        o_af[k] = D(S.act0 + S.gf(k))[r];
+        o_pf[k] = D(S.pick0 + S.gf(k))[r];
+        o_gf[k] = dG[a.off_f[k] + u];
+        o_ck[k] = (kLoopBatch && a.cext_b1[k]) ? 0.f : D(1 + k)[rc];
+      }
+      // h = o * tanh(c); c slot: external contributions + tanh path
       const float d_tc = gh * ao;
       const float d_o = gh * tc;
-      D(S.tc)[r] += d_tc;
-      D(S.act0 + S.go())[r] += d_o;
-      // c slot: external contributions + tanh path
-      const float dc = D(S.c)[r] + (1.f - tc * tc) * d_tc;
-      D(S.c)[r] = dc;
-#pragma unroll
-      for (int k = 0; k + 1 < M; ++k) D(S.add0 + k)[r] += dc;
-      if (M > 0) D(S.prod0)[r] += dc;
+      const float dc = dc_ext + (1.f - tc * tc) * d_tc;
       // i * g
       const float d_i = dc * ag, d_g = dc * ai;
-      D(S.act0 + S.gi())[r] += d_i;
-      D(S.act0 + S.gg())[r] += d_g;
       const float dpi = ai * (1.f - ai) * d_i;
       const float dpo = ao * (1.f - ao) * d_o;
       const float dpg = (1.f - ag * ag) * d_g;
-      D(S.pick0 + S.gi())[r] += dpi;
-      D(S.pick0 + S.go())[r] += dpo;
-      D(S.pick0 + S.gg())[r] += dpg;
-      float* dG = D(0) + (int64_t)b * a.gw;
-      dG[a.off_i + u] += dpi;
-      dG[a.off_o + u] += dpo;
-      dG[a.off_g + u] += dpg;
+      D(S.tc)[r] = o_tc + d_tc;
+      D(S.act0 + S.go())[r] = o_ao + d_o;
+      D(S.c)[r] = dc;
+#pragma unroll
+      for (int k = 0; k + 1 < M; ++k) D(S.add0 + k)[r] = o_add[k] + dc;
+      if (M > 0) D(S.prod0)[r] = o_p0 + dc;
+      D(S.act0 + S.gi())[r] = o_ai + d_i;
+      D(S.act0 + S.gg())[r] = o_ag + d_g;
+      D(S.pick0 + S.gi())[r] = o_pi + dpi;
+      D(S.pick0 + S.go())[r] = o_po + dpo;
+      D(S.pick0 + S.gg())[r] = o_pg + dpg;
+      dG[a.off_i + u] = o_gi + dpi;
+      dG[a.off_o + u] = o_go + dpo;
+      dG[a.off_g + u] = o_gg + dpg;
 #pragma unroll
       for (int k = 0; k < M; ++k) {
-        D(S.prod0 + 1 + k)[r] += dc;
+        D(S.prod0 + 1 + k)[r] = o_pk[k] + dc;
         const int64_t rc = a.cext_b1[k] ? u : r;
-        const float ck = V(1 + k)[rc];
-        const float af = V(S.act0 + S.gf(k))[r];
-        const float d_f = dc * ck;
-        const float d_ck = dc * af;
-        D(S.act0 + S.gf(k))[r] += d_f;
-        const float dpf = af * (1.f - af) * d_f;
-        D(S.pick0 + S.gf(k))[r] += dpf;
-        dG[a.off_f[k] + u] += dpf;
+        const float d_f = dc * ck[k];
+        const float d_ck = dc * af[k];
+        D(S.act0 + S.gf(k))[r] = o_af[k] + d_f;
+        const float dpf = af[k] * (1.f - af[k]) * d_f;
+        D(S.pick0 + S.gf(k))[r] = o_pf[k] + dpf;
+        dG[a.off_f[k] + u] = o_gf[k] + dpf;
         if (kLoopBatch && a.cext_b1[k]) acc_c[k] += d_ck;
-        else D(1 + k)[rc] += d_ck;
+        else D(1 + k)[rc] = o_ck[k] + d_ck;
       }
     }
     if (kLoopBatch) {
