@@ -2200,7 +2200,7 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
     // distributed shared memory; needs equal unit-block counts (<= 16)
     int cl = a.ch[0].n_u;
     // a one-CTA "cluster" has nothing to exchange: the global-counter kernels serve it
-    bool use_cl = rnn_cluster_enabled() && a.vec && cl >= 2 && cl <= 16;
+    bool use_cl = rnn_cluster_enabled() && cl >= 2 && cl <= 16;
     for (int k = 0; k < a.n_chains; ++k) use_cl = use_cl && a.ch[k].n_u == cl;
     size_t smem = 0, smem_cl = 0;
     if (bwd) {

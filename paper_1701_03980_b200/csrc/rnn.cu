@@ -795,13 +795,22 @@ __global__ void __launch_bounds__(kClThreads, 1) rnn_fwd_cl_kernel(const __grid_
   if (warp < 8) {
     const int fl = fl_hp;
     const float* Hp = Hp0;
-    const int w4 = C.H >> 2;
-    for (int idx = tid; idx < BS * w4; idx += kRT) {
-      const int b = idx / w4, q = idx - (idx / w4) * w4;
-      const int row = b0 + b;
-      if (row < C.B) cp_async16(hS + (size_t)BS * HP + (size_t)b * HP + 4 * q, Hp + ((fl & 2) ? 0 : (int64_t)row * C.H) + 4 * q);
+    if (a.vec) {
+      const int w4 = C.H >> 2;
+      for (int idx = tid; idx < BS * w4; idx += kRT) {
+        const int b = idx / w4, q = idx - (idx / w4) * w4;
+        const int row = b0 + b;
+        if (row < C.B)
+          cp_async16(hS + (size_t)BS * HP + (size_t)b * HP + 4 * q, Hp + ((fl & 2) ? 0 : (int64_t)row * C.H) + 4 * q);
+      }
+      cp_async_wait_all();
+    } else {  // rows not 16 B aligned (H % 4 != 0): element loads
+      for (int idx = tid; idx < BS * C.H; idx += kRT) {
+        const int b = idx / C.H, k = idx - (idx / C.H) * C.H;
+        const int row = b0 + b;
+        if (row < C.B) hS[(size_t)BS * HP + (size_t)b * HP + k] = Hp[((fl & 2) ? 0 : (int64_t)row * C.H) + k];
+      }
     }
-    cp_async_wait_all();
   }
   __syncthreads();
   if (a.trace == 2 && tid == 0) trace(0, 254);
