@@ -7,7 +7,7 @@ PKG := paper_1701_03980_b200
 SRC := $(PKG)/csrc
 OBJ := build/obj
 LIB := $(PKG)/libdyngpu.so
-OBJS := $(OBJ)/executor.o $(OBJ)/kernels.o $(OBJ)/gemm.o $(OBJ)/tcgemm.o $(OBJ)/rnn.o $(OBJ)/tmagemm.o
+OBJS := $(OBJ)/executor.o $(OBJ)/kernels.o $(OBJ)/gemm.o $(OBJ)/tcgemm.o $(OBJ)/rnn.o $(OBJ)/tmagemm.o $(OBJ)/cellgemm.o
 
 PYTHON ?= python3
 PYINC := $(shell $(PYTHON) -c "import sysconfig; print(sysconfig.get_paths()['include'])")
@@ -36,6 +36,9 @@ $(OBJ)/tcgemm.o: $(SRC)/tcgemm.cu $(SRC)/kernels.cuh | $(OBJ)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(OBJ)/tmagemm.o: $(SRC)/tmagemm.cu $(SRC)/kernels.cuh | $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(OBJ)/cellgemm.o: $(SRC)/cellgemm.cu $(SRC)/kernels.cuh | $(OBJ)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(OBJ)/rnn.o: $(SRC)/rnn.cu $(SRC)/kernels.cuh | $(OBJ)

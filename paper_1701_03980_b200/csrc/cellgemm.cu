@@ -1,0 +1,316 @@
+// Fused gate affine + gated cell for small batched levels (sm_100a, fp32).
+//
+// A Tree-LSTM level (builders.py:250-274: gates = affine(b, U1, h1, U2, h2),
+// then i, f1, f2, o, g picks and activations, c = i*g + f1*c1 + f2*c2,
+// h = o*tanh(c); leaves: gates = affine(b, Wx, x), c = i*g) is two node
+// groups in the reference interpreter and two launches in the generic
+// executor (a grouped GEMM, then cell_fwd_kernel).  Both are tiny -- a
+// handful of rows against a 5H x (2H) weight -- so the launch and the
+// dependent memory round trips dominate, and the level loop of a tree makes
+// them sequential.  Here one launch does both: CTA c owns hidden units
+// [8c, 8c+8), computes every gate row of those units (all gw / H gate blocks,
+// so the gate node's value is complete) for every row of the level from
+// shared-memory copies of the inputs and its weight slice, then runs the cell
+// for its units.  Every node of the pattern keeps its own value slot.
+//
+// Arithmetic: fp32 FMA, each term's dot product in k order, then
+// ((b + W1 x1) + W2 x2) like the reference's affine (ops.py:323-340).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace dg {
+namespace {
+
+__device__ __forceinline__ float sigmoid_ref(float x) {
+  x = fminf(fmaxf(x, -60.f), 60.f);  // ops.py:78-83
+  return 1.f / (1.f + expf(-x));
+}
+
+__global__ void __launch_bounds__(256) affine_cell_fwd_kernel(const __grid_constant__ AffCellArgs a) {
+  // (pdl_prologue after the weight staging: weights do not depend on the
+  // preceding kernel, so their loads overlap its tail)
+  extern __shared__ float4 smem4[];
+  float* sm = reinterpret_cast<float*>(smem4);
+  const CellArgs& c = a.cell;
+  const int nb = c.gw / c.H;  // gate blocks of width H
+  const int u0 = blockIdx.x * kAffCellUnits;
+  const int U = min(kAffCellUnits, c.H - u0);
+  const int NR = nb * kAffCellUnits;  // gate rows of this CTA (q = blk * 8 + uu)
+  const int KP = a.kpad;
+  const int R = a.rows;
+  float* xs = sm;                 // [R][KP] inputs, terms at koff[t] (zero padded)
+  float* ws = xs + (size_t)R * KP;  // [NR][KP] weight rows of this CTA's units
+  float* gs = ws + (size_t)NR * KP;  // [R][NR] gate values
+  // slot pointers of every cell (the blob is uploaded before the plan's
+  // first kernel): one global load each instead of one per element use
+  __shared__ float* sval[20 * 64];
+  for (int i = threadIdx.x; i < c.nslot * c.n; i += blockDim.x) sval[i] = const_cast<float*>(c.val[i]);
+  // weights and inputs into shared memory, kB independent loads in flight
+  // per thread (a load-store pair per iteration would serialise on latency)
+  constexpr int kB = 8;
+  __shared__ const float* xrow[kAffCellMaxTerms][64];
+  for (int t = 0; t < a.terms; ++t) {
+    const int K = a.K[t], ko = a.koff[t];
+    const int kend = (t + 1 < a.terms) ? a.koff[t + 1] : KP;
+    const int KT = kend - ko;  // padded width of this term
+    const float* W = a.W[t];
+    const int totw = KT * NR;  // consecutive threads: consecutive units of one gate block
+    for (int i0 = threadIdx.x; i0 < totw; i0 += kB * blockDim.x) {
+      float v[kB];
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        const int idx = i0 + i * blockDim.x;
+        const int k = idx / NR, q = idx - (idx / NR) * NR;
+        const int blk = q / kAffCellUnits, uu = q - blk * kAffCellUnits;
+        v[i] = (idx < totw && k < K && uu < U) ? __ldg(W + blk * c.H + u0 + uu + (int64_t)k * c.gw) : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        const int idx = i0 + i * blockDim.x;
+        if (idx < totw) {
+          const int k = idx / NR, q = idx - (idx / NR) * NR;
+          ws[(size_t)q * KP + ko + k] = v[i];
+        }
+      }
+    }
+  }
+  pdl_prologue();  // inputs (and the cell's external states) come from the preceding kernels
+  for (int i = threadIdx.x; i < a.terms * R; i += blockDim.x) xrow[i / R][i % R] = a.x[i / R][i % R];
+  __syncthreads();
+  for (int t = 0; t < a.terms; ++t) {
+    const int K = a.K[t], ko = a.koff[t];
+    const int kend = (t + 1 < a.terms) ? a.koff[t + 1] : KP;
+    const int KT = kend - ko;
+    const int totx = R * KT;
+    for (int i0 = threadIdx.x; i0 < totx; i0 += kB * blockDim.x) {
+      float v[kB];
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        const int idx = i0 + i * blockDim.x;
+        const int r = idx / KT, k = idx - (idx / KT) * KT;
+        v[i] = (idx < totx && k < K) ? xrow[t][r][k] : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        const int idx = i0 + i * blockDim.x;
+        if (idx < totx) xs[(size_t)(idx / KT) * KP + ko + idx % KT] = v[i];
+      }
+    }
+  }
+  __syncthreads();
+  // gate rows: every (row, gate row) dot split into L k-parts (one thread
+  // each, 4-aligned chunks in k order), the parts summed in order after
+  const int pairs = R * NR;
+  int L = 1;
+  while (L < 8 && pairs * L * 2 <= (int)blockDim.x) L *= 2;
+  float* part = gs + (size_t)R * NR;  // [L][pairs] per term (terms summed in order below)
+  for (int t = 0; t < a.terms; ++t) {
+    const int n4 = (a.K[t] + 3) >> 2;
+    const int c4 = (n4 + L - 1) / L;
+    for (int p = threadIdx.x; p < pairs * L; p += blockDim.x) {
+      const int l = p / pairs, pr = p - l * pairs;
+      const int r = pr / NR, q = pr - r * NR;
+      const float4* xr = reinterpret_cast<const float4*>(xs + (size_t)r * KP + a.koff[t]);
+      const float4* wr = reinterpret_cast<const float4*>(ws + (size_t)q * KP + a.koff[t]);
+      float acc = 0.f;
+      const int e = min(n4, (l + 1) * c4);
+      for (int k4 = l * c4; k4 < e; ++k4) {
+        const float4 x = xr[k4], w = wr[k4];
+        acc = fmaf(w.x, x.x, acc);
+        acc = fmaf(w.y, x.y, acc);
+        acc = fmaf(w.z, x.z, acc);
+        acc = fmaf(w.w, x.w, acc);
+      }
+      part[((size_t)t * L + l) * pairs + pr] = acc;
+    }
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < pairs; p += blockDim.x) {
+    const int r = p / NR, q = p - r * NR;
+    const int blk = q / kAffCellUnits, uu = q - blk * kAffCellUnits;
+    if (uu >= U) continue;
+    const int grow = blk * c.H + u0 + uu;
+    float v = a.bias[grow];
+    for (int t = 0; t < a.terms; ++t) {
+      float dot = 0.f;
+      for (int l = 0; l < L; ++l) dot += part[((size_t)t * L + l) * pairs + p];
+      v += dot;
+    }
+    gs[p] = v;
+    const int j = r / c.batch, b = r - j * c.batch;
+    sval[j][(int64_t)b * c.gw + grow] = v;  // the gate node's value
+  }
+  __syncthreads();
+  // the cell of this CTA's units (same arithmetic as cell_fwd_kernel)
+  const int m = c.m;
+  const int s_pick0 = 1 + m, s_act0 = s_pick0 + 3 + m, s_prod0 = s_act0 + 3 + m, s_add0 = s_prod0 + 1 + m;
+  const int s_tc = s_add0 + m, s_h = s_tc + 1;
+  const int bi = c.off_i / c.H, bo = c.off_o / c.H, bg = c.off_g / c.H;
+  for (int p = threadIdx.x; p < R * U; p += blockDim.x) {
+    const int r = p / U, uu = p - r * U;
+    const int j = r / c.batch, b = r - j * c.batch;
+    const int u = u0 + uu;
+    const int64_t rr = (int64_t)b * c.H + u;
+    auto V = [&](int slot) { return sval[slot * c.n + j]; };
+    const float* gr = gs + (size_t)r * NR + uu;
+    const float xi = gr[bi * kAffCellUnits], xo = gr[bo * kAffCellUnits], xg = gr[bg * kAffCellUnits];
+    float xf[2] = {0.f, 0.f}, ck[2] = {0.f, 0.f};
+    for (int k = 0; k < m; ++k) {
+      xf[k] = gr[(c.off_f[k] / c.H) * kAffCellUnits];
+      ck[k] = V(1 + k)[rr];
+    }
+    V(s_pick0)[rr] = xi;
+    V(s_pick0 + 1 + m)[rr] = xo;
+    V(s_pick0 + 2 + m)[rr] = xg;
+    const float ai = sigmoid_ref(xi), ao = sigmoid_ref(xo), ag = tanhf(xg);
+    V(s_act0)[rr] = ai;
+    V(s_act0 + 1 + m)[rr] = ao;
+    V(s_act0 + 2 + m)[rr] = ag;
+    float cv = ai * ag;
+    V(s_prod0)[rr] = cv;
+    for (int k = 0; k < m; ++k) {
+      V(s_pick0 + 1 + k)[rr] = xf[k];
+      const float af = sigmoid_ref(xf[k]);
+      V(s_act0 + 1 + k)[rr] = af;
+      const float pk = af * ck[k];
+      V(s_prod0 + 1 + k)[rr] = pk;
+      cv = cv + pk;
+      V(s_add0 + k)[rr] = cv;
+    }
+    const float tc = tanhf(cv);
+    V(s_tc)[rr] = tc;
+    V(s_h)[rr] = ao * tc;
+  }
+}
+
+// Input gradients of a small affine group, dX_t += W_t^T dG (the tree
+// levels' gate affines, the tagger's per-word layers): CTA c owns
+// kAffCellCols input columns (of the terms' concatenation); it stages the
+// rows of W_t^T for them before waiting on the preceding kernel (weights do
+// not change during backward), then reads the group's dG rows once and adds
+// its columns of dX into the input rows' gradient slots.  The generic path
+// is the grouped split-K GEMM, whose dependent loads dominate at a few rows.
+// Weight and bias gradients stay in the executor's aggregated dW GEMM /
+// column sums.
+__global__ void __launch_bounds__(256) affine_dx_small_kernel(const __grid_constant__ AffCellArgs a) {
+  extern __shared__ float4 smem4[];
+  float* sm = reinterpret_cast<float*>(smem4);
+  const int R = a.rows, GW = a.cell.gw;
+  int Ktot = 0;
+  for (int t = 0; t < a.terms; ++t) Ktot += a.K[t];
+  const int kc0 = blockIdx.x * kAffCellCols;
+  const int KC = min(kAffCellCols, Ktot - kc0);
+  float* wt = sm;                              // [kAffCellCols][GW] rows of W^T (own columns)
+  float* dg = wt + (size_t)kAffCellCols * GW;  // [R][GW] gate gradients
+  float* part = dg + (size_t)R * GW;           // [L][R * kAffCellCols]
+  __shared__ int col_t[kAffCellCols], col_k[kAffCellCols];
+  __shared__ float* sgx[kAffCellMaxTerms][64];
+  __shared__ const float* sgr[64];
+  if (threadIdx.x < kAffCellCols) {
+    int kc = kc0 + threadIdx.x, t = 0;
+    while (t + 1 < a.terms && kc >= a.K[t]) kc -= a.K[t++];
+    col_t[threadIdx.x] = t;
+    col_k[threadIdx.x] = kc;
+  }
+  for (int i = threadIdx.x; i < a.terms * R; i += blockDim.x) sgx[i / R][i % R] = a.gx[i / R][i % R];
+  for (int i = threadIdx.x; i < R; i += blockDim.x) sgr[i] = a.grow[i];
+  __syncthreads();
+  // W_t[:, k] is contiguous (column-major): coalesced, kB loads in flight per
+  // thread, before the wait
+  constexpr int kB = 8;
+  for (int i0 = threadIdx.x; i0 < KC * GW; i0 += kB * blockDim.x) {
+    float v[kB];
+#pragma unroll
+    for (int i = 0; i < kB; ++i) {
+      const int idx = i0 + i * blockDim.x;
+      const int q = idx / GW, g = idx - (idx / GW) * GW;
+      v[i] = idx < KC * GW ? __ldg(a.W[col_t[q]] + g + (int64_t)col_k[q] * GW) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < kB; ++i) {
+      const int idx = i0 + i * blockDim.x;
+      if (idx < KC * GW) wt[idx] = v[i];
+    }
+  }
+  pdl_prologue();
+  for (int i0 = threadIdx.x; i0 < R * GW; i0 += kB * blockDim.x) {
+    float v[kB];
+#pragma unroll
+    for (int i = 0; i < kB; ++i) {
+      const int idx = i0 + i * blockDim.x;
+      v[i] = idx < R * GW ? sgr[idx / GW][idx % GW] : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < kB; ++i) {
+      const int idx = i0 + i * blockDim.x;
+      if (idx < R * GW) dg[idx] = v[i];
+    }
+  }
+  __syncthreads();
+  // (row, column) dots over the gate rows in L parts, summed in order
+  const int pairs = R * KC;
+  int L = 1;
+  while (L < 16 && pairs * L * 2 <= (int)blockDim.x) L *= 2;
+  const int cg = (GW + L - 1) / L;
+  for (int p = threadIdx.x; p < pairs * L; p += blockDim.x) {
+    const int l = p / pairs, pr = p - l * pairs;
+    const int r = pr / KC, q = pr - r * KC;
+    const float* w = wt + (size_t)q * GW;
+    const float* d = dg + (size_t)r * GW;
+    float acc = 0.f;
+    const int e = min(GW, (l + 1) * cg);
+    for (int g = l * cg; g < e; ++g) acc = fmaf(w[g], d[g], acc);
+    part[(size_t)l * pairs + pr] = acc;
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < pairs; p += blockDim.x) {
+    const int r = p / KC, q = p - r * KC;
+    float v = 0.f;
+    for (int l = 0; l < L; ++l) v += part[(size_t)l * pairs + p];
+    float* gx = sgx[col_t[q]][r] + col_k[q];
+    *gx += v;
+  }
+}
+
+}  // namespace
+
+size_t affine_dx_small_smem(int rows, int gw) {
+  return 4 * ((size_t)kAffCellCols * gw + (size_t)rows * gw + 16 * (size_t)rows * kAffCellCols);
+}
+
+int launch_affine_dx_small(const AffCellArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(affine_dx_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  int Ktot = 0;
+  for (int t = 0; t < a.terms; ++t) Ktot += a.K[t];
+  const int grid = (Ktot + kAffCellCols - 1) / kAffCellCols;
+  if (launch_k(affine_dx_small_kernel, grid, 256, affine_dx_small_smem(a.rows, a.cell.gw), s, a) != cudaSuccess)
+    return -1;
+  return 1;
+}
+
+size_t affine_cell_smem(int rows, int kpad, int gw, int H) {
+  const int NR = (gw / H) * kAffCellUnits;
+  // inputs, weight rows, gate values, k-part partial sums (<= 8 parts x 3 terms)
+  return 4 * ((size_t)rows * kpad + (size_t)NR * kpad + (size_t)rows * NR + 24 * (size_t)rows * NR);
+}
+
+int launch_affine_cell_fwd(const AffCellArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(affine_cell_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  const int grid = (a.cell.H + kAffCellUnits - 1) / kAffCellUnits;
+  const size_t smem = affine_cell_smem(a.rows, a.kpad, a.cell.gw, a.cell.H);
+  if (launch_k(affine_cell_fwd_kernel, grid, 256, smem, s, a) != cudaSuccess) return -1;
+  return 1;
+}
+
+}  // namespace dg

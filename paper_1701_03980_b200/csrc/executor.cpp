@@ -2410,6 +2410,109 @@ static bool affine_gemm_ok(const dg_graph* g, const Node& n0) {
   return true;
 }
 
+// A gate-affine group immediately followed by the gated-cell group that
+// consumes it (a Tree-LSTM level, its leaves, unchained LSTM cells): one
+// fused launch (cellgemm.cu) when the level is small -- the generic path
+// is a grouped GEMM plus cell_fwd_kernel, two launches whose dependent memory
+// round trips dominate at a few rows.  Returns false (nothing planned) when
+// the pair does not qualify.
+static bool plan_affine_cell_fwd(dg_graph* g, const Schedule& S, size_t q, Plan& plan, GemmBatch& gb) {
+  static const bool on = [] {
+    const char* e = std::getenv("DG_AFFCELL");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || q + 1 >= S.groups.size()) return false;
+  const Group& ga = S.groups[q];
+  const Group& gc = S.groups[q + 1];
+  if (ga.kind != DG_OP_AFFINE || gc.kind != -2 || ga.units.size() != gc.units.size()) return false;
+  const int n = (int)gc.units.size();
+  const Unit& c0 = S.units[gc.units[0]];
+  const Node& a0 = g->nodes[S.units[ga.units[0]].last()];
+  const int terms = (a0.n_in - 1) / 2;
+  const int Bt = a0.batch;
+  const int rows = n * Bt;
+  if (terms < 1 || terms > kAffCellMaxTerms || c0.m > 2 || c0.H <= 0 || c0.gw != (int)a0.elem || c0.gw % c0.H)
+    return false;
+  if (rows > 64) return false;
+  for (int k = 0; k < 3 + c0.m; ++k)
+    if (c0.off[k] % c0.H) return false;
+  // cell j <-> affine node: the cell's gate input
+  std::unordered_map<int, int> pos;
+  for (int j = 0; j < n; ++j) pos[S.units[ga.units[j]].last()] = j;
+  std::vector<int> aff(n);
+  for (int j = 0; j < n; ++j) {
+    const Unit& cu = S.units[gc.units[j]];
+    auto it = pos.find(cu.ins[0]);
+    if (it == pos.end()) return false;
+    aff[j] = S.units[ga.units[it->second]].last();
+    if (g->nodes[cu.ins[0]].batch != Bt) return false;
+    for (int k = 0; k < cu.m; ++k)
+      if (g->nodes[cu.ins[1 + k]].batch != Bt) return false;  // no broadcast external c
+  }
+  // shared parameters: the same bias row and weights in every member
+  const Node& b0 = g->nodes[g->inputs[a0.in_off]];
+  if (b0.kind != DG_OP_PARAMETER || b0.batch != 1) return false;
+  AffCellArgs A{};
+  int kp = 0;
+  for (int t = 0; t < terms; ++t) {
+    const Node& w = g->nodes[g->inputs[a0.in_off + 1 + 2 * t]];
+    const Node& x = g->nodes[g->inputs[a0.in_off + 2 + 2 * t]];
+    if (w.kind != DG_OP_PARAMETER || w.batch != 1) return false;
+    A.W[t] = w.val;
+    A.K[t] = (int)x.elem;
+    A.koff[t] = kp;
+    kp += (A.K[t] + 3) & ~3;
+  }
+  for (int j = 0; j < n; ++j) {
+    const Node& aj = g->nodes[aff[j]];
+    if (aj.n_in != a0.n_in || aj.batch != Bt || g->nodes[g->inputs[aj.in_off]].val != b0.val) return false;
+    for (int t = 0; t < terms; ++t)
+      if (g->nodes[g->inputs[aj.in_off + 1 + 2 * t]].val != A.W[t]) return false;
+  }
+  A.kpad = kp;
+  if (affine_cell_smem(rows, kp, c0.gw, c0.H) > 200 * 1024) return false;
+  flush_gemm(g, plan, gb);
+  Blob& B = plan.blob;
+  A.rows = rows;
+  A.terms = terms;
+  A.bias = b0.val;
+  std::vector<size_t> ox(terms);
+  for (int t = 0; t < terms; ++t) {
+    std::vector<uintptr_t> xr((size_t)rows);
+    for (int j = 0; j < n; ++j) {
+      const Node& x = g->nodes[g->inputs[g->nodes[aff[j]].in_off + 2 + 2 * t]];
+      for (int b = 0; b < Bt; ++b) xr[(size_t)j * Bt + b] = P(x.val + (x.batch == 1 ? 0 : (int64_t)b * A.K[t]));
+    }
+    ox[t] = B.push(xr);
+  }
+  CellArgs& a = A.cell;
+  a.n = n;
+  a.m = c0.m;
+  a.H = c0.H;
+  a.gw = c0.gw;
+  a.batch = Bt;
+  a.off_i = c0.off[0];
+  a.off_o = c0.off[1];
+  a.off_g = c0.off[2];
+  for (int k = 0; k < c0.m; ++k) a.off_f[k] = c0.off[3 + k];
+  a.nslot = 10 + 5 * c0.m;
+  std::vector<uintptr_t> vals((size_t)a.nslot * n);
+  for (int j = 0; j < n; ++j) {
+    const Unit& u = S.units[gc.units[j]];
+    int sl = 0;
+    for (int x : u.ins) vals[(size_t)(sl++) * n + j] = P(g->nodes[x].val);
+    for (int x : u.nodes) vals[(size_t)(sl++) * n + j] = P(g->nodes[x].val);
+  }
+  const size_t ov = B.push(vals);
+  plan.ops.push_back([A, ox, ov](char* d) mutable {
+    A.cell.val = at<const float* const>(d, ov);
+    for (size_t t = 0; t < ox.size(); ++t) A.x[t] = at<const float* const>(d, ox[t]);
+    return launch_affine_cell_fwd(A, g_launch_stream);
+  });
+  plan.tag(C_GEMM_FWD, 2.0 * rows * c0.gw * kp, 4.0 * ((double)rows * kp + (double)kp * c0.gw + 14.0 * rows * c0.H));
+  return true;
+}
+
 static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, Plan& plan, GemmBatch& gb) {
   Blob& B = plan.blob;
   std::vector<int> nodes;
@@ -2842,7 +2945,13 @@ static int do_forward(dg_graph* g, int upto) {
   tm.lap("place+inputs");
   {
     GemmBatch gb;
-    for (const Group& gr : S.groups) plan_forward_group(g, S, gr, plan, gb);
+    for (size_t q = 0; q < S.groups.size(); ++q) {
+      if (plan_affine_cell_fwd(g, S, q, plan, gb)) {
+        ++q;  // the cell group went into the same launch
+        continue;
+      }
+      plan_forward_group(g, S, S.groups[q], plan, gb);
+    }
     flush_gemm(g, plan, gb);
   }
   tm.lap("groups");
@@ -2898,6 +3007,94 @@ int dg_forward(dg_graph* g, int32_t upto) {
 }
 
 // --------------------------------------------------------------- backward
+
+// Backward of a small affine group (a few rows: the tree levels' gate
+// affines, per-word layers): dX through affine_dx_small_kernel (weights staged
+// before the dependency wait, one launch) instead of the grouped split-K GEMM;
+// weight / bias gradients registered for the aggregated dW GEMM / column sums
+// exactly as the affine's generic backward does.
+static bool plan_affine_dx_small(dg_graph* g, const Schedule& S, const Group& ga, Plan& plan, GemmBatch& gb,
+                                 std::unordered_map<int64_t, AffineUse>& wuse,
+                                 std::unordered_map<int64_t, std::vector<uintptr_t>>& buse) {
+  static const bool on = [] {
+    const char* e = std::getenv("DG_AFFCELL");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || ga.kind != DG_OP_AFFINE) return false;
+  const int n = (int)ga.units.size();
+  const Node& a0 = g->nodes[S.units[ga.units[0]].last()];
+  const int terms = (a0.n_in - 1) / 2;
+  const int Bt = a0.batch;
+  const int rows = n * Bt;
+  const int gw = (int)a0.elem;
+  if (terms < 1 || terms > kAffCellMaxTerms || rows > 64 || a0.rank != 1) return false;
+  const Node& b0 = g->nodes[g->inputs[a0.in_off]];
+  if (b0.kind != DG_OP_PARAMETER || b0.batch != 1) return false;
+  AffCellArgs A{};
+  int Ktot = 0;
+  for (int t = 0; t < terms; ++t) {
+    const Node& w = g->nodes[g->inputs[a0.in_off + 1 + 2 * t]];
+    if (w.kind != DG_OP_PARAMETER || w.batch != 1) return false;
+    A.W[t] = w.val;
+    A.K[t] = (int)g->nodes[g->inputs[a0.in_off + 2 + 2 * t]].elem;
+    Ktot += A.K[t];
+  }
+  std::vector<int> targets;
+  for (int u : ga.units) {
+    const Node& aj = g->nodes[S.units[u].last()];
+    if (aj.n_in != a0.n_in || aj.batch != Bt || aj.elem != a0.elem || g->nodes[g->inputs[aj.in_off]].val != b0.val)
+      return false;
+    for (int t = 0; t < terms; ++t) {
+      const int x = g->inputs[aj.in_off + 2 + 2 * t];
+      if (g->nodes[g->inputs[aj.in_off + 1 + 2 * t]].val != A.W[t] || g->nodes[x].batch != Bt) return false;
+      targets.push_back(x);
+    }
+  }
+  std::sort(targets.begin(), targets.end());
+  if (std::adjacent_find(targets.begin(), targets.end()) != targets.end()) return false;
+  if (affine_dx_small_smem(rows, gw) > 200 * 1024 || Ktot < 1) return false;
+  flush_gemm(g, plan, gb);
+  Blob& B = plan.blob;
+  A.rows = rows;
+  A.terms = terms;
+  A.cell.gw = gw;
+  std::vector<uintptr_t> grows((size_t)rows);
+  for (int j = 0; j < n; ++j) {
+    const Node& aj = g->nodes[S.units[ga.units[j]].last()];
+    for (int b = 0; b < Bt; ++b) grows[(size_t)j * Bt + b] = P(aj.grad + (int64_t)b * gw);
+  }
+  const size_t ogr = B.push(grows);
+  std::vector<size_t> ogx(terms);
+  for (int t = 0; t < terms; ++t) {
+    const Node& wn = g->nodes[g->inputs[a0.in_off + 1 + 2 * t]];
+    std::vector<uintptr_t> xrows((size_t)rows), dxrows((size_t)rows);
+    for (int j = 0; j < n; ++j) {
+      const Node& aj = g->nodes[S.units[ga.units[j]].last()];
+      const Node& x = g->nodes[g->inputs[aj.in_off + 2 + 2 * t]];
+      for (int b = 0; b < Bt; ++b) {
+        xrows[(size_t)j * Bt + b] = P(x.val + (int64_t)b * A.K[t]);
+        dxrows[(size_t)j * Bt + b] = P(x.grad + (int64_t)b * A.K[t]);
+      }
+    }
+    ogx[t] = B.push(dxrows);
+    AffineUse& use = wuse[g->aux_i[wn.ai_off]];
+    use.n_in = A.K[t];
+    use.m = gw;
+    use.x_rows.insert(use.x_rows.end(), xrows.begin(), xrows.end());
+    use.g_rows.insert(use.g_rows.end(), grows.begin(), grows.end());
+  }
+  {
+    auto& v = buse[g->aux_i[b0.ai_off]];
+    v.insert(v.end(), grows.begin(), grows.end());
+  }
+  plan.ops.push_back([A, ogx, ogr](char* d) mutable {
+    A.grow = at<const float* const>(d, ogr);
+    for (size_t t = 0; t < ogx.size(); ++t) A.gx[t] = at<float* const>(d, ogx[t]);
+    return launch_affine_dx_small(A, g_launch_stream);
+  });
+  plan.tag(C_GEMM_DX, 2.0 * rows * gw * Ktot, 4.0 * ((double)Ktot * gw + 2.0 * rows * Ktot + (double)rows * gw));
+  return true;
+}
 
 static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr, Plan& plan, float* dummy,
                                 std::unordered_map<int64_t, AffineUse>& wuse,
@@ -3512,7 +3709,8 @@ int dg_backward(dg_graph* g, int32_t loss) {
       std::map<int, double> kt;
       for (int q = (int)S.groups.size() - 1; q >= 0; --q) {
         const auto t0 = std::chrono::steady_clock::now();
-        plan_backward_group(g, S, S.groups[q], plan, dummy, wuse, buse, gb);
+        if (!plan_affine_dx_small(g, S, S.groups[q], plan, gb, wuse, buse))
+          plan_backward_group(g, S, S.groups[q], plan, dummy, wuse, buse, gb);
         if (per_kind)
           kt[S.groups[q].kind] += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
       }

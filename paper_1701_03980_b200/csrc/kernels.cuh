@@ -125,6 +125,29 @@ struct CellArgs {
 int launch_cell_fwd(const CellArgs& a, cudaStream_t s);
 int launch_cell_bwd(const CellArgs& a, cudaStream_t s);
 
+// gate affine + gated cell of a small level in one launch (cellgemm.cu):
+// G = bias + sum_t W_t x_t (W_t column-major gw x K_t), then the cell
+constexpr int kAffCellUnits = 4;  // hidden units per CTA
+constexpr int kAffCellMaxTerms = 3;
+struct AffCellArgs {
+  CellArgs cell;  // val[0 * n + j] = the gate node (written whole)
+  int rows;       // n * batch
+  int terms;
+  int K[kAffCellMaxTerms];
+  int koff[kAffCellMaxTerms];  // 4-aligned offsets of the terms in the padded K
+  int kpad;
+  const float* W[kAffCellMaxTerms];
+  const float* const* x[kAffCellMaxTerms];  // [rows] input rows per term
+  const float* bias;                        // broadcast row (gw)
+  float* const* gx[kAffCellMaxTerms];       // [rows] input gradient rows per term (backward)
+  const float* const* grow;                 // [rows] gate gradient rows (backward)
+};
+constexpr int kAffCellCols = 8;  // backward: input columns per CTA
+size_t affine_cell_smem(int rows, int kpad, int gw, int H);
+int launch_affine_cell_fwd(const AffCellArgs& a, cudaStream_t s);
+size_t affine_dx_small_smem(int rows, int gw);
+int launch_affine_dx_small(const AffCellArgs& a, cudaStream_t s);
+
 // ------------------------------------------- persistent LSTM recurrence (rnn.cu)
 // One launch runs every step of a stack of LSTM chains (builders.py:92-101
 // steps sharing Wx, Wh, b; x^l_t = h^{l-1}_t for stacked layers).  Per step t

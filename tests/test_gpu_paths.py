@@ -12,6 +12,11 @@ with each fast path switched off, so the fallbacks stay parity-green too.
   DG_SCHED_CACHE=0  schedules rebuilt for every graph
   DG_PLAN_CACHE=0   launch plans rebuilt for every graph (no plan cache)
   DG_CUDA_GRAPH=1   cached plans replayed as CUDA graphs (default: launch by launch)
+  DG_AFFCELL=0      gate affine and gated cell of a small level as a grouped
+                    GEMM + cell kernel instead of one fused launch
+
+(the fused affine + cell path is exercised by the Tree-LSTM test added to
+the list below)
 """
 
 import os
@@ -35,6 +40,7 @@ VARIANTS = {
     "schedule_cache_off": {"DG_SCHED_CACHE": "0"},
     "plan_cache_off": {"DG_PLAN_CACHE": "0"},
     "cuda_graph_on": {"DG_CUDA_GRAPH": "1"},
+    "affine_cell_unfused": {"DG_AFFCELL": "0"},
 }
 
 
@@ -43,7 +49,8 @@ VARIANTS = {
 def test_ptb_parity_on_every_kernel_path(variant):
     env = dict(os.environ, **VARIANTS[variant])
     tests = ["tests/test_gpu_parity.py::test_ptb_mb16_full_size_vs_oracle",
-             "tests/test_gpu_parity.py::test_char_tagger_full_size_vs_oracle"]
+             "tests/test_gpu_parity.py::test_char_tagger_full_size_vs_oracle",
+             "tests/test_gpu_parity.py::test_tree_lstm_full_size_vs_oracle"]
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", *tests],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
