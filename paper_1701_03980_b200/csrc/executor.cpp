@@ -155,7 +155,7 @@ struct Node {
 
 static inline size_t round64(size_t n) { return (n + 63) & ~size_t(63); }
 
-enum UnitKind { U_NODE = 0, U_CHAIN = 1, U_CELL = 2, U_RNN = 3 };
+enum UnitKind { U_NODE = 0, U_CHAIN = 1, U_CELL = 2, U_RNN = 3, U_GRUA = 4, U_GRUB = 5, U_PNLS2 = 6 };
 
 struct Unit {
   int type;                 // U_NODE / U_CHAIN / U_CELL
@@ -395,6 +395,18 @@ static uint64_t unit_signature(const dg_graph* g, const Unit& u) {
     s.add(U_RNN);
     return s.h;
   }
+  if (u.type == U_PNLS2) {  // widths and labels are per unit: one launch for all
+    s.add(U_PNLS2);
+    return s.h;
+  }
+  if (u.type == U_GRUA || u.type == U_GRUB) {
+    s.add(u.type);
+    s.add(u.H);
+    s.add(u.gw);
+    for (int k = 0; k < 3; ++k) s.add(u.off[k]);
+    for (int x : u.ins) s.add(g->nodes[x].batch);
+    return s.h;
+  }
   if (u.type == U_CELL) {
     const Node& G = g->nodes[u.ins[0]];
     s.add(U_CELL);
@@ -588,6 +600,84 @@ static bool match_cell(const dg_graph* g, int h, const std::vector<int>& consume
   for (int x : u.ins)
     if (std::binary_search(all, all + na, x)) return false;
   if ((int)u.nodes.size() != 9 + 4 * m) return false;  // + G and m external states = nslot
+  return true;
+}
+
+// GRU step (builders.py:102-110), matched from its output nh = add(kh, zc):
+//   zr = affine(b, Wx, x, Wh, h); z = logistic(pick(zr, z)); r = logistic(pick(zr, r))
+//   cx = pick(affine(b, Wx, x), c); rh = cmult(r, h); mh = matmul(Wh, rh); ch = pick(mh, c)
+//   cand = tanh(add(cx, ch)); keep = add(input(ones), scalar_mul(z, -1))
+//   nh = add(cmult(keep, h), cmult(z, cand))
+// as two units around the matmul (kernels.cuh GruArgs slot order).  Every
+// internal node has exactly one consumer; z (two consumers, both in part B),
+// cx and rh are part A's outputs.
+static bool match_gru(const dg_graph* g, int nh, const std::vector<int>& consumers, const std::vector<char>& in_set,
+                      const std::vector<char>& absorbed, Unit& ua, Unit& ub) {
+  auto Nd = [&](int i) -> const Node& { return g->nodes[i]; };
+  auto in = [&](int i, int k) { return g->inputs[Nd(i).in_off + k]; };
+  const Node& hn = Nd(nh);
+  if (hn.kind != DG_OP_ADD || hn.rank != 1 || !in_set[nh] || absorbed[nh]) return false;
+  const int H = hn.dims[0], B = hn.batch;
+  auto vec = [&](int i, bool b1_ok) {
+    const Node& x = Nd(i);
+    return x.rank == 1 && x.dims[0] == H && (x.batch == B || (b1_ok && x.batch == 1));
+  };
+  auto inner = [&](int i, int kind) {
+    return i >= 0 && in_set[i] && !absorbed[i] && consumers[i] == 1 && Nd(i).kind == kind && vec(i, false);
+  };
+  auto pick = [&](int p, int& src, int& off) {
+    if (!inner(p, DG_OP_PICK_RANGE)) return false;
+    src = in(p, 0);
+    off = (int)g->aux_i[Nd(p).ai_off];
+    return Nd(src).rank == 1 && Nd(src).batch == B && Nd(src).dims[0] == 3 * H;
+  };
+  const int kh = in(nh, 0), zc = in(nh, 1);
+  if (!inner(kh, DG_OP_CMULT) || !inner(zc, DG_OP_CMULT)) return false;
+  const int keep = in(kh, 0), h = in(kh, 1), z = in(zc, 0), cand = in(zc, 1);
+  if (!inner(keep, DG_OP_ADD) || !vec(h, true) || !inner(cand, DG_OP_TANH)) return false;
+  if (!in_set[z] || absorbed[z] || consumers[z] != 2 || Nd(z).kind != DG_OP_LOGISTIC || !vec(z, false)) return false;
+  const int ones = in(keep, 0), nz = in(keep, 1);
+  if (Nd(ones).kind != DG_OP_INPUT || !vec(ones, true) || !inner(nz, DG_OP_SCALAR_MUL) || in(nz, 0) != z ||
+      g->aux_f[Nd(nz).af_off] != -1.f)
+    return false;
+  const int sv = in(cand, 0);
+  if (!inner(sv, DG_OP_ADD)) return false;
+  const int cx = in(sv, 0), ch = in(sv, 1);
+  int ax, off_c, mh, off_ch;
+  if (!pick(cx, ax, off_c) || !pick(ch, mh, off_ch)) return false;
+  if (Nd(mh).kind != DG_OP_MATMUL || consumers[mh] != 1 || !in_set[mh] || absorbed[mh]) return false;
+  const int rh = in(mh, 1);
+  if (!inner(rh, DG_OP_CMULT) || in(rh, 1) != h) return false;
+  const int r = in(rh, 0);
+  if (!inner(r, DG_OP_LOGISTIC)) return false;
+  int zr, off_r, zr2, off_z;
+  if (!pick(in(r, 0), zr, off_r) || !pick(in(z, 0), zr2, off_z) || zr != zr2) return false;
+  if (Nd(zr).kind != DG_OP_AFFINE || Nd(ax).kind != DG_OP_AFFINE || !in_set[zr] || !in_set[ax]) return false;
+  ua = Unit();
+  ua.type = U_GRUA;
+  ua.m = -1;
+  ua.H = H;
+  ua.gw = 3 * H;
+  ua.off[0] = off_z;
+  ua.off[1] = off_r;
+  ua.off[2] = off_c;
+  ua.ins = {zr, ax, h};
+  ua.nodes = {in(z, 0), z, in(r, 0), r, cx, rh};
+  ub = Unit();
+  ub.type = U_GRUB;
+  ub.m = -1;
+  ub.H = H;
+  ub.gw = 3 * H;
+  ub.off[0] = off_ch;
+  ub.ins = {mh, cx, z, ones, h};
+  ub.nodes = {ch, sv, cand, nz, keep, kh, zc, nh};
+  // distinct nodes, no external input inside
+  std::vector<int> all(ua.nodes);
+  all.insert(all.end(), ub.nodes.begin(), ub.nodes.end());
+  std::sort(all.begin(), all.end());
+  if (std::adjacent_find(all.begin(), all.end()) != all.end()) return false;
+  for (int x : {zr, ax, h, mh, ones})
+    if (std::binary_search(all.begin(), all.end(), x)) return false;
   return true;
 }
 
@@ -890,6 +980,53 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
       cells.push_back(std::move(cu));
     }
   }
+  // GRU steps: two units each (part A before the recurrent matmul, part B after)
+  {
+    static const bool gru_on = [] {
+      const char* e = std::getenv("DG_GRU_FUSE");
+      return !(e && e[0] == '0');
+    }();
+    for (int i : active) {
+      if (!gru_on || g->nodes[i].kind != DG_OP_ADD || absorbed[i]) continue;
+      Unit ua, ub;
+      if (!match_gru(g, i, consumers, in_set, absorbed, ua, ub)) continue;
+      for (Unit* pu : {&ua, &ub}) {
+        for (int x : pu->nodes) {
+          absorbed[x] = 1;
+          cell_of[x] = (int)cells.size();
+        }
+        cells.push_back(std::move(*pu));
+      }
+    }
+  }
+  // class-factored softmax terms: add(pnls(class scores), pnls(word scores))
+  {
+    static const bool on = [] {
+      const char* e = std::getenv("DG_PNLS2");
+      return !(e && e[0] == '0');
+    }();
+    auto Nd = [&](int i) -> const Node& { return g->nodes[i]; };
+    auto in = [&](int i, int k) { return g->inputs[Nd(i).in_off + k]; };
+    auto term = [&](int p) {
+      return p >= 0 && in_set[p] && !absorbed[p] && consumers[p] == 1 && Nd(p).kind == DG_OP_PNLS &&
+             Nd(p).batch == 1 && Nd(in(p, 0)).rank == 1 && Nd(in(p, 0)).batch == 1;
+    };
+    for (int i : active) {
+      if (!on || Nd(i).kind != DG_OP_ADD || absorbed[i] || Nd(i).batch != 1) continue;
+      const int p1 = in(i, 0), p2 = in(i, 1);
+      if (p1 == p2 || !term(p1) || !term(p2)) continue;
+      Unit u;
+      u.type = U_PNLS2;
+      u.m = -1;
+      u.ins = {in(p1, 0), in(p2, 0)};
+      u.nodes = {p1, p2, i};
+      for (int x : u.nodes) {
+        absorbed[x] = 1;
+        cell_of[x] = (int)cells.size();
+      }
+      cells.push_back(std::move(u));
+    }
+  }
   tm.lap("cells");
   // LSTM chains / stacks over the matched cells (persistent recurrence path)
   std::vector<int> rnn_of(N, -1);
@@ -1056,7 +1193,9 @@ static void build_schedule(const dg_graph* g, const std::vector<int>& active, in
       std::sort(members.begin(), members.end());
       Group gr;
       const Unit& u0 = S.units[members[0]];
-      gr.kind = u0.type == U_CHAIN ? -1 : u0.type == U_CELL ? -2 : u0.type == U_RNN ? -3 : g->nodes[u0.last()].kind;
+      gr.kind = u0.type == U_CHAIN ? -1 : u0.type == U_CELL ? -2 : u0.type == U_RNN ? -3
+              : u0.type == U_GRUA ? -4 : u0.type == U_GRUB ? -5 : u0.type == U_PNLS2 ? -6
+              : g->nodes[u0.last()].kind;
       gr.units = members;
       for (int u : members) {
         ++done;
@@ -2410,6 +2549,60 @@ static bool affine_gemm_ok(const dg_graph* g, const Node& n0) {
   return true;
 }
 
+static void plan_pnls2(dg_graph* g, const Schedule& S, const std::vector<int>& units, Plan& plan, bool bwd) {
+  Blob& B = plan.blob;
+  const int n = (int)units.size();
+  std::vector<uintptr_t> vals((size_t)5 * n), grads(bwd ? (size_t)5 * n : 0);
+  std::vector<int32_t> width((size_t)2 * n), label((size_t)2 * n);
+  double bytes = 0;
+  for (int j = 0; j < n; ++j) {
+    const Unit& u = S.units[units[j]];
+    const int slot[5] = {u.ins[0], u.ins[1], u.nodes[0], u.nodes[1], u.nodes[2]};
+    for (int k = 0; k < 5; ++k) {
+      vals[(size_t)k * n + j] = P(g->nodes[slot[k]].val);
+      if (bwd) grads[(size_t)k * n + j] = P(g->nodes[slot[k]].grad);
+    }
+    for (int k = 0; k < 2; ++k) {
+      width[2 * j + k] = (int32_t)g->nodes[u.ins[k]].elem;
+      const Node& pn = g->nodes[u.nodes[k]];
+      label[2 * j + k] = (int32_t)g->aux_i[pn.ai_off];
+      bytes += 4.0 * width[2 * j + k] * (bwd ? 3 : 1);
+    }
+  }
+  const size_t ov = B.push(vals), ow = B.push(width), ol = B.push(label);
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < 2; ++k) rec_ids(S.units[units[j]].nodes[k], 0, 4, ol + 4 * (size_t)(2 * j + k));
+  const size_t og = bwd ? B.push(grads) : 0;
+  Pnls2Args a{};
+  a.n = n;
+  plan.ops.push_back([a, ov, ow, ol, og, bwd](char* d) mutable {
+    a.val = at<const float* const>(d, ov);
+    a.width = at<const int>(d, ow);
+    a.label = at<const int>(d, ol);
+    if (!bwd) return launch_pnls2_fwd(a, g_launch_stream);
+    a.grad = at<float* const>(d, og);
+    return launch_pnls2_bwd(a, g_launch_stream);
+  });
+  plan.tag(bwd ? C_PNLS_BWD : C_PNLS_FWD, 0.0, bytes);
+}
+
+static GruArgs gru_args(const dg_graph* g, const Unit& u0, int n) {
+  GruArgs a{};
+  a.n = n;
+  a.H = u0.H;
+  a.gw = u0.gw;
+  a.off0 = u0.off[0];
+  a.off1 = u0.off[1];
+  a.off2 = u0.off[2];
+  const bool part_b = u0.type == U_GRUB;
+  a.batch = g->nodes[u0.nodes.back()].batch;
+  const int hslot = part_b ? 4 : 2;
+  a.h_b1 = g->nodes[u0.ins[hslot]].batch == 1 && a.batch > 1;
+  a.ones_b1 = part_b && g->nodes[u0.ins[3]].batch == 1 && a.batch > 1;
+  a.nslot = part_b ? 13 : 9;
+  return a;
+}
+
 // A gate-affine group immediately followed by the gated-cell group that
 // consumes it (a Tree-LSTM level, its leaves, unchained LSTM cells): one
 // fused launch (cellgemm.cu) when the level is small -- the generic path
@@ -2523,6 +2716,29 @@ static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, 
 
   if (gr.kind == -3) {  // persistent LSTM stacks
     plan_rnn_group(g, S, gr, plan, false, nullptr, nullptr, &gb);
+    return;
+  }
+  if (gr.kind == -6) {  // class-factored softmax terms
+    plan_pnls2(g, S, gr.units, plan, false);
+    return;
+  }
+  if (gr.kind == -4 || gr.kind == -5) {  // fused GRU parts
+    const Unit& u0 = S.units[gr.units[0]];
+    GruArgs a = gru_args(g, u0, n);
+    std::vector<uintptr_t> vals((size_t)a.nslot * n);
+    for (int j = 0; j < n; ++j) {
+      const Unit& u = S.units[gr.units[j]];
+      int s = 0;
+      for (int x : u.ins) vals[(size_t)(s++) * n + j] = P(g->nodes[x].val);
+      for (int x : u.nodes) vals[(size_t)(s++) * n + j] = P(g->nodes[x].val);
+    }
+    const size_t ov = B.push(vals);
+    const bool part_b = gr.kind == -5;
+    plan.ops.push_back([a, ov, part_b](char* d) mutable {
+      a.val = at<const float* const>(d, ov);
+      return launch_gru_fwd(a, part_b, g_launch_stream);
+    });
+    plan.tag(C_ELEMWISE, 0.0, 4.0 * n * (double)a.batch * a.H * (part_b ? 13 : 9));
     return;
   }
   if (gr.kind == -2) {  // fused gated cells
@@ -3113,7 +3329,8 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
   std::vector<std::vector<int>> targets(gr.units.size());
   for (size_t j = 0; j < gr.units.size(); ++j) targets[j] = S.units[gr.units[j]].ins;
   const bool ew = gr.kind == DG_OP_ADD || gr.kind == DG_OP_CMULT || gr.kind == DG_OP_TANH ||
-                  gr.kind == DG_OP_LOGISTIC || gr.kind == DG_OP_SCALAR_MUL || gr.kind == -1 || gr.kind == -2;
+                  gr.kind == DG_OP_LOGISTIC || gr.kind == DG_OP_SCALAR_MUL || gr.kind == -1 || gr.kind == -2 ||
+                  gr.kind == -4 || gr.kind == -5 || gr.kind == -6;
   if (gr.kind == DG_OP_AFFINE) {
     // dX is conflict-free by construction (temp + segmented reduce); only the
     // per-node (non-parameter) bias needs rounds
@@ -3142,6 +3359,36 @@ static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr,
       if (mask[j]) { nodes.push_back(all_nodes[j]); units.push_back(gr.units[j]); }
     const int n = (int)nodes.size();
     if (n == 0) continue;
+    if (gr.kind == -6) {  // class-factored softmax terms
+      plan_pnls2(g, S, units, plan, true);
+      continue;
+    }
+    if (gr.kind == -4 || gr.kind == -5) {  // fused GRU parts
+      const Unit& u0 = S.units[units[0]];
+      GruArgs a = gru_args(g, u0, n);
+      std::vector<uintptr_t> vals((size_t)a.nslot * n), grads((size_t)a.nslot * n);
+      for (int j = 0; j < n; ++j) {
+        const Unit& u = S.units[units[j]];
+        int s = 0;
+        for (int x : u.ins) {
+          vals[(size_t)s * n + j] = P(g->nodes[x].val);
+          grads[(size_t)(s++) * n + j] = P(g->nodes[x].grad);
+        }
+        for (int x : u.nodes) {
+          vals[(size_t)s * n + j] = P(g->nodes[x].val);
+          grads[(size_t)(s++) * n + j] = P(g->nodes[x].grad);
+        }
+      }
+      const size_t ov = B.push(vals), og = B.push(grads);
+      const bool part_b = gr.kind == -5;
+      plan.ops.push_back([a, ov, og, part_b](char* d) mutable {
+        a.val = at<const float* const>(d, ov);
+        a.grad = at<float* const>(d, og);
+        return launch_gru_bwd(a, part_b, g_launch_stream);
+      });
+      plan.tag(C_ELEMWISE, 0.0, 4.0 * n * (double)a.batch * a.H * (part_b ? 26 : 18));
+      continue;
+    }
     if (gr.kind == -2) {  // fused gated cells
       const Unit& u0 = S.units[units[0]];
       CellArgs a{};

@@ -411,6 +411,130 @@ __global__ void __launch_bounds__(256) cell_bwd_kernel(CellArgs a) {
   }
 }
 
+// ---------------------------------------------------------------- GRU parts
+// (kernels.cuh GruArgs).  Arithmetic node by node as the generic kernels:
+// logistic = sigmoidf_ref, scalar_mul x * c, add a + b, cmult a * b, tanhf;
+// backward accumulations in the reference's reverse node order.
+template <bool kB>
+__global__ void __launch_bounds__(256) gru_fwd_kernel(GruArgs a) {
+  pdl_prologue();
+  const int64_t per = (int64_t)a.batch * a.H;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < per * a.n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(t / per);
+    const int64_t r = t - (int64_t)j * per;
+    const int b = static_cast<int>(r / a.H), u = static_cast<int>(r - (int64_t)b * a.H);
+    auto V = [&](int slot) { return const_cast<float*>(a.val[(int64_t)slot * a.n + j]); };
+    const int64_t rg = (int64_t)b * a.gw;
+    const int64_t rh_ = a.h_b1 ? u : r;
+    if (!kB) {
+      const float* zr = V(0);
+      const float* ax = V(1);
+      const float pz = zr[rg + a.off0 + u], pr = zr[rg + a.off1 + u], cx = ax[rg + a.off2 + u];
+      const float h = V(2)[rh_];
+      const float z = sigmoidf_ref(pz), rr = sigmoidf_ref(pr);
+      V(3)[r] = pz;
+      V(4)[r] = z;
+      V(5)[r] = pr;
+      V(6)[r] = rr;
+      V(7)[r] = cx;
+      V(8)[r] = rr * h;
+    } else {
+      const float ch = V(0)[rg + a.off0 + u];
+      const float cx = V(1)[r], z = V(2)[r], ones = V(3)[a.ones_b1 ? u : r], h = V(4)[rh_];
+      const float sv = cx + ch;
+      const float cand = tanhf(sv);
+      const float nz = z * -1.f;
+      const float keep = ones + nz;
+      const float kh = keep * h, zc = z * cand;
+      V(5)[r] = ch;
+      V(6)[r] = sv;
+      V(7)[r] = cand;
+      V(8)[r] = nz;
+      V(9)[r] = keep;
+      V(10)[r] = kh;
+      V(11)[r] = zc;
+      V(12)[r] = kh + zc;
+    }
+  }
+}
+
+template <bool kB>
+__global__ void __launch_bounds__(256) gru_bwd_kernel(GruArgs a) {
+  pdl_prologue();
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)a.n * a.H;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(t / a.H), u = static_cast<int>(t - (int64_t)j * a.H);
+    auto V = [&](int slot) { return a.val[(int64_t)slot * a.n + j]; };
+    auto D = [&](int slot) { return a.grad[(int64_t)slot * a.n + j]; };
+    float acc_h = 0.f, acc_ones = 0.f;
+    for (int b = 0; b < a.batch; ++b) {
+      const int64_t r = (int64_t)b * a.H + u, rg = (int64_t)b * a.gw;
+      const int64_t rh_ = a.h_b1 ? u : r;
+      if (!kB) {
+        // loads first (no store-to-load waits)
+        const float h = V(2)[rh_], z = V(4)[r], rr = V(6)[r];
+        const float g_pz = D(3)[r], g_z = D(4)[r], g_pr = D(5)[r], g_r = D(6)[r], g_cx = D(7)[r], g_rh = D(8)[r];
+        const float o_zr0 = D(0)[rg + a.off0 + u], o_zr1 = D(0)[rg + a.off1 + u], o_ax = D(1)[rg + a.off2 + u];
+        const float o_h = a.h_b1 ? 0.f : D(2)[r];
+        // rh = r * h
+        const float gr_tot = g_r + g_rh * h;
+        const float dh = g_rh * rr;
+        // cx = pick(ax); r = logistic(pr); pr = pick(zr); z = logistic(pz); pz = pick(zr)
+        const float gpr_tot = g_pr + rr * (1.f - rr) * gr_tot;
+        const float gpz_tot = g_pz + z * (1.f - z) * g_z;
+        D(6)[r] = gr_tot;
+        D(5)[r] = gpr_tot;
+        D(3)[r] = gpz_tot;
+        D(1)[rg + a.off2 + u] = o_ax + g_cx;
+        D(0)[rg + a.off1 + u] = o_zr1 + gpr_tot;
+        D(0)[rg + a.off0 + u] = o_zr0 + gpz_tot;
+        if (a.h_b1) acc_h += dh;
+        else D(2)[r] = o_h + dh;
+      } else {
+        const float h = V(4)[rh_], z = V(2)[r], cand = V(7)[r], keep = V(9)[r];
+        const float g_nh = D(12)[r];
+        const float o_zc = D(11)[r], o_kh = D(10)[r], o_keep = D(9)[r], o_nz = D(8)[r], o_cand = D(7)[r];
+        const float o_s = D(6)[r], o_ch = D(5)[r], o_z = D(2)[r], o_cx = D(1)[r];
+        const float o_mh = D(0)[rg + a.off0 + u];
+        const float o_ones = a.ones_b1 ? 0.f : D(3)[r];
+        const float o_h = a.h_b1 ? 0.f : D(4)[r];
+        // nh = kh + zc
+        const float g_zc = o_zc + g_nh, g_kh = o_kh + g_nh;
+        // zc = z * cand
+        float gz = o_z + g_zc * cand;
+        const float g_cand = o_cand + g_zc * z;
+        // kh = keep * h
+        const float g_keep = o_keep + g_kh * h;
+        const float dh = g_kh * keep;
+        // keep = ones + nz
+        const float dones = g_keep;
+        const float g_nz = o_nz + g_keep;
+        // nz = z * -1
+        gz = gz + -1.f * g_nz;
+        // cand = tanh(s); s = cx + ch; ch = pick(mh)
+        const float g_s = o_s + (1.f - cand * cand) * g_cand;
+        const float g_ch = o_ch + g_s;
+        D(11)[r] = g_zc;
+        D(10)[r] = g_kh;
+        D(9)[r] = g_keep;
+        D(8)[r] = g_nz;
+        D(7)[r] = g_cand;
+        D(6)[r] = g_s;
+        D(5)[r] = g_ch;
+        D(2)[r] = gz;
+        D(1)[r] = o_cx + g_s;
+        D(0)[rg + a.off0 + u] = o_mh + g_ch;
+        if (a.ones_b1) acc_ones += dones;
+        else D(3)[r] = o_ones + dones;
+        if (a.h_b1) acc_h += dh;
+        else D(4)[r] = o_h + dh;
+      }
+    }
+    if (a.h_b1) D(kB ? 4 : 2)[u] += acc_h;
+    if (kB && a.ones_b1) D(3)[u] += acc_ones;
+  }
+}
+
 // ------------------------------------------------------------------ structural
 
 __global__ void pick_fwd_kernel(PickArgs a) {
@@ -670,6 +794,60 @@ __global__ void __launch_bounds__(256) row_reg_kernel(RowArgs a) {
     } else {
       d4[q] = p;
     }
+  }
+}
+
+// ------------------------------------------------------ two-level softmax term
+// (kernels.cuh Pnls2Args): the row_kernel arithmetic (max, sum of expf(x - m),
+// m + logf(s) - x[label]) for both rows of a unit, one block per unit.
+__device__ __forceinline__ void row_stats(const float* x, int w, float* sh, float& m, float& s) {
+  float mm = -INFINITY;
+  for (int c = threadIdx.x; c < w; c += blockDim.x) mm = fmaxf(mm, x[c]);
+  m = row_reduce_max<true>(mm, sh);
+  float ss = 0.f;
+  for (int c = threadIdx.x; c < w; c += blockDim.x) ss += expf(x[c] - m);
+  s = row_reduce_sum<true>(ss, sh);
+}
+
+__global__ void __launch_bounds__(256) pnls2_fwd_kernel(Pnls2Args a) {
+  pdl_prologue();
+  __shared__ float sh[32];
+  const int j = blockIdx.x;
+  float loss[2];
+  for (int k = 0; k < 2; ++k) {
+    const float* x = a.val[(int64_t)k * a.n + j];
+    float m, s;
+    row_stats(x, a.width[2 * j + k], sh, m, s);
+    loss[k] = m + logf(s) - x[a.label[2 * j + k]];
+  }
+  if (threadIdx.x == 0) {
+    const_cast<float*>(a.val[(int64_t)2 * a.n + j])[0] = loss[0];
+    const_cast<float*>(a.val[(int64_t)3 * a.n + j])[0] = loss[1];
+    const_cast<float*>(a.val[(int64_t)4 * a.n + j])[0] = loss[0] + loss[1];
+  }
+}
+
+__global__ void __launch_bounds__(256) pnls2_bwd_kernel(Pnls2Args a) {
+  pdl_prologue();
+  __shared__ float sh[32];
+  const int j = blockIdx.x;
+  const float gs = a.grad[(int64_t)4 * a.n + j][0];
+  for (int k = 0; k < 2; ++k) {
+    // the pnls node's gradient: its own slot (other consumers) + the add's
+    float* gp = a.grad[(int64_t)(2 + k) * a.n + j];
+    const float g = gp[0] + gs;
+    const float* x = a.val[(int64_t)k * a.n + j];
+    float* gx = a.grad[(int64_t)k * a.n + j];
+    const int w = a.width[2 * j + k], lab = a.label[2 * j + k];
+    float m, s;
+    row_stats(x, w, sh, m, s);
+    for (int c = threadIdx.x; c < w; c += blockDim.x) {
+      float p = expf(x[c] - m) / s;
+      if (c == lab) p -= 1.f;
+      gx[c] += g * p;
+    }
+    __syncthreads();  // every thread read gp[0] before it is overwritten
+    if (threadIdx.x == 0) gp[0] = g;
   }
 }
 
@@ -1253,6 +1431,32 @@ int launch_cell_bwd(const CellArgs& a, cudaStream_t s) {
     case 4: launch_k(cell_bwd_kernel<2, false>, g, kThreads, 0, s, a); break;
     default: launch_k(cell_bwd_kernel<2, true>, g, kThreads, 0, s, a); break;
   }
+  return 1;
+}
+
+int launch_pnls2_fwd(const Pnls2Args& a, cudaStream_t s) {
+  if (a.n <= 0) return 0;
+  launch_k(pnls2_fwd_kernel, a.n, kThreads, 0, s, a);
+  return 1;
+}
+
+int launch_pnls2_bwd(const Pnls2Args& a, cudaStream_t s) {
+  if (a.n <= 0) return 0;
+  launch_k(pnls2_bwd_kernel, a.n, kThreads, 0, s, a);
+  return 1;
+}
+
+int launch_gru_fwd(const GruArgs& a, bool part_b, cudaStream_t s) {
+  const int64_t total = (int64_t)a.n * a.batch * a.H;
+  if (part_b) launch_k(gru_fwd_kernel<true>, grid_for(total), kThreads, 0, s, a);
+  else launch_k(gru_fwd_kernel<false>, grid_for(total), kThreads, 0, s, a);
+  return 1;
+}
+
+int launch_gru_bwd(const GruArgs& a, bool part_b, cudaStream_t s) {
+  const int64_t total = (int64_t)a.n * a.H;
+  if (part_b) launch_k(gru_bwd_kernel<true>, grid_for(total), kThreads, 0, s, a);
+  else launch_k(gru_bwd_kernel<false>, grid_for(total), kThreads, 0, s, a);
   return 1;
 }
 

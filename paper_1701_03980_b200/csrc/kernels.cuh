@@ -125,6 +125,40 @@ struct CellArgs {
 int launch_cell_fwd(const CellArgs& a, cudaStream_t s);
 int launch_cell_bwd(const CellArgs& a, cudaStream_t s);
 
+// GRU step (builders.py:102-110) in two fused parts around the recurrent
+// matmul: part A (picks z, r of the gate affine zr, the candidate's input
+// pick cx of ax, r*h), part B (candidate pick of Wh(r*h), cx + ch, tanh,
+// 1 - z as input(ones) + (-1)*z, (1-z)*h + z*cand).  Slots: A = zr, ax, h |
+// pz, z, pr, r, cx, rh; B = mh, cx, z, ones, h | ch, s, cand, nz, keep, kh,
+// zc, nh.  One thread per (node, unit) loops over the batch (broadcast h /
+// ones gradients are summed in batch order).
+struct GruArgs {
+  int n, batch, H, gw;    // gw: width of zr / ax / mh (3H)
+  int off0, off1, off2;   // A: z, r offsets in zr, cx offset in ax; B: ch offset in mh
+  int h_b1, ones_b1;      // broadcast (batch-1) h / ones under a batched step
+  int nslot;
+  const float* const* val;  // [nslot * n]
+  float* const* grad;       // [nslot * n] (backward)
+};
+int launch_gru_fwd(const GruArgs& a, bool part_b, cudaStream_t s);
+int launch_gru_bwd(const GruArgs& a, bool part_b, cudaStream_t s);
+
+// Class-factored softmax term (builders.py:282-378 neg_log_softmax):
+// s = add(pickneglogsoftmax(class_scores, c), pickneglogsoftmax(word_scores, i))
+// as one unit: one block per unit computes both picked negative log
+// softmaxes (rows of different widths) and their sum; backward adds
+// g * (softmax - onehot) into both score rows.  Per unit slots:
+// [0] class scores, [1] word scores, [2] pnls class, [3] pnls word, [4] s.
+struct Pnls2Args {
+  int n;
+  const float* const* val;  // [5 * n]
+  float* const* grad;       // [5 * n] (backward)
+  const int* width;         // [2 * n]
+  const int* label;         // [2 * n]
+};
+int launch_pnls2_fwd(const Pnls2Args& a, cudaStream_t s);
+int launch_pnls2_bwd(const Pnls2Args& a, cudaStream_t s);
+
 // gate affine + gated cell of a small level in one launch (cellgemm.cu):
 // G = bias + sum_t W_t x_t (W_t column-major gw x K_t), then the cell
 constexpr int kAffCellUnits = 4;  // hidden units per CTA
