@@ -913,8 +913,17 @@ __global__ void __launch_bounds__(256) scatter_rows_kernel(float* __restrict__ t
   float* dst = table_grad + ids[it.u] * (int64_t)dim;
   const bool chunked = it.nchunks > 0;
   float* part = chunked ? partials + (int64_t)(it.pbase + it.chunk) * dim : nullptr;
+  // the item's <= kScatterChunk row pointers in one round of independent
+  // loads, then every row's data in flight at once (two memory round trips
+  // per item); alignment decided from the loaded pointers
+  const int nk = it.k1 - it.k0;
+  const float* rp[kScatterChunk];
   bool vec = (dim & 3) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
-  for (int k = it.k0; k < it.k1 && vec; ++k) vec = (reinterpret_cast<uintptr_t>(src_rows[k]) & 15) == 0;
+#pragma unroll
+  for (int r = 0; r < kScatterChunk; ++r) {
+    rp[r] = r < nk ? src_rows[it.k0 + r] : nullptr;
+    if (r < nk) vec = vec && (reinterpret_cast<uintptr_t>(rp[r]) & 15) == 0;
+  }
   auto finish = [&](int c, float s) {
     if (chunked) {
       part[c] = s;
@@ -926,23 +935,19 @@ __global__ void __launch_bounds__(256) scatter_rows_kernel(float* __restrict__ t
   };
   if (vec) {
     for (int c4 = lane; c4 < (dim >> 2); c4 += 32) {
+      float4 v[kScatterChunk];
+#pragma unroll
+      for (int r = 0; r < kScatterChunk; ++r)
+        v[r] = r < nk ? __ldg(reinterpret_cast<const float4*>(rp[r]) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      constexpr int R = 8;
-      for (int k = it.k0; k < it.k1; k += R) {
-        float4 v[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r)
-          v[r] = k + r < it.k1 ? __ldg(reinterpret_cast<const float4*>(src_rows[k + r]) + c4)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-          if (k + r < it.k1) {
-            acc.x += v[r].x;
-            acc.y += v[r].y;
-            acc.z += v[r].z;
-            acc.w += v[r].w;
-          }
-      }
+      for (int r = 0; r < kScatterChunk; ++r)
+        if (r < nk) {
+          acc.x += v[r].x;
+          acc.y += v[r].y;
+          acc.z += v[r].z;
+          acc.w += v[r].w;
+        }
       finish(4 * c4 + 0, acc.x);
       finish(4 * c4 + 1, acc.y);
       finish(4 * c4 + 2, acc.z);
@@ -951,7 +956,7 @@ __global__ void __launch_bounds__(256) scatter_rows_kernel(float* __restrict__ t
   } else {
     for (int c = lane; c < dim; c += 32) {
       float acc = 0.f;
-      for (int k = it.k0; k < it.k1; ++k) acc += src_rows[k][c];
+      for (int r = 0; r < nk; ++r) acc += rp[r][c];
       finish(c, acc);
     }
   }
@@ -966,7 +971,15 @@ __global__ void __launch_bounds__(256) scatter_rows_kernel(float* __restrict__ t
   const float* pb = partials + (int64_t)it.pbase * dim;
   for (int c = lane; c < dim; c += 32) {
     float s = 0.f;
-    for (int q = 0; q < it.nchunks; ++q) s += __ldcg(pb + (int64_t)q * dim + c);
+    int q = 0;
+    for (; q + 8 <= it.nchunks; q += 8) {  // 8 partial loads in flight, summed in chunk order
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = __ldcg(pb + (int64_t)(q + i) * dim + c);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s += v[i];
+    }
+    for (; q < it.nchunks; ++q) s += __ldcg(pb + (int64_t)q * dim + c);
     if (kSet) {
       dst[c] = s / scale;
     } else {
