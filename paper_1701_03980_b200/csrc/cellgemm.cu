@@ -15,11 +15,15 @@
 //
 // Arithmetic: fp32 FMA, each term's dot product in k order, then
 // ((b + W1 x1) + W2 x2) like the reference's affine (ops.py:323-340).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "kernels.cuh"
+
+namespace cgrp = cooperative_groups;
 
 namespace dg {
 namespace {
@@ -29,29 +33,14 @@ __device__ __forceinline__ float sigmoid_ref(float x) {
   return 1.f / (1.f + expf(-x));
 }
 
-__global__ void __launch_bounds__(256) affine_cell_fwd_kernel(const __grid_constant__ AffCellArgs a) {
-  // (pdl_prologue after the weight staging: weights do not depend on the
-  // preceding kernel, so their loads overlap its tail)
-  extern __shared__ float4 smem4[];
-  float* sm = reinterpret_cast<float*>(smem4);
+// weight rows of this CTA's units (gate row q = blk * kAffCellUnits + uu
+// <-> G row blk * H + u0 + uu), kB independent loads in flight per thread (a
+// load-store pair per iteration would serialise on latency)
+__device__ void stage_weights(const AffCellArgs& a, float* ws, int u0, int U) {
   const CellArgs& c = a.cell;
-  const int nb = c.gw / c.H;  // gate blocks of width H
-  const int u0 = blockIdx.x * kAffCellUnits;
-  const int U = min(kAffCellUnits, c.H - u0);
-  const int NR = nb * kAffCellUnits;  // gate rows of this CTA (q = blk * 8 + uu)
+  const int NR = (c.gw / c.H) * kAffCellUnits;
   const int KP = a.kpad;
-  const int R = a.rows;
-  float* xs = sm;                 // [R][KP] inputs, terms at koff[t] (zero padded)
-  float* ws = xs + (size_t)R * KP;  // [NR][KP] weight rows of this CTA's units
-  float* gs = ws + (size_t)NR * KP;  // [R][NR] gate values
-  // slot pointers of every cell (the blob is uploaded before the plan's
-  // first kernel): one global load each instead of one per element use
-  __shared__ float* sval[20 * 64];
-  for (int i = threadIdx.x; i < c.nslot * c.n; i += blockDim.x) sval[i] = const_cast<float*>(c.val[i]);
-  // weights and inputs into shared memory, kB independent loads in flight
-  // per thread (a load-store pair per iteration would serialise on latency)
   constexpr int kB = 8;
-  __shared__ const float* xrow[kAffCellMaxTerms][64];
   for (int t = 0; t < a.terms; ++t) {
     const int K = a.K[t], ko = a.koff[t];
     const int kend = (t + 1 < a.terms) ? a.koff[t + 1] : KP;
@@ -77,7 +66,20 @@ __global__ void __launch_bounds__(256) affine_cell_fwd_kernel(const __grid_const
       }
     }
   }
-  pdl_prologue();  // inputs (and the cell's external states) come from the preceding kernels
+}
+
+// one level once the weight rows are in shared memory: inputs, gate rows,
+// the gate node's value, the cell (same arithmetic as cell_fwd_kernel)
+__device__ void level_fwd(const AffCellArgs& a, const float* ws, float* xs, float* gs, float** sval,
+                          const float* (*xrow)[64], int u0, int U) {
+  const CellArgs& c = a.cell;
+  const int NR = (c.gw / c.H) * kAffCellUnits;
+  const int KP = a.kpad;
+  const int R = a.rows;
+  constexpr int kB = 8;
+  // slot pointers of every cell and the input row pointers: one global load
+  // each instead of one per element use
+  for (int i = threadIdx.x; i < c.nslot * c.n; i += blockDim.x) sval[i] = const_cast<float*>(c.val[i]);
   for (int i = threadIdx.x; i < a.terms * R; i += blockDim.x) xrow[i / R][i % R] = a.x[i / R][i % R];
   __syncthreads();
   for (int t = 0; t < a.terms; ++t) {
@@ -144,7 +146,6 @@ __global__ void __launch_bounds__(256) affine_cell_fwd_kernel(const __grid_const
     sval[j][(int64_t)b * c.gw + grow] = v;  // the gate node's value
   }
   __syncthreads();
-  // the cell of this CTA's units (same arithmetic as cell_fwd_kernel)
   const int m = c.m;
   const int s_pick0 = 1 + m, s_act0 = s_pick0 + 3 + m, s_prod0 = s_act0 + 3 + m, s_add0 = s_prod0 + 1 + m;
   const int s_tc = s_add0 + m, s_h = s_tc + 1;
@@ -183,6 +184,56 @@ __global__ void __launch_bounds__(256) affine_cell_fwd_kernel(const __grid_const
     const float tc = tanhf(cv);
     V(s_tc)[rr] = tc;
     V(s_h)[rr] = ao * tc;
+  }
+  __syncthreads();  // shared buffers are reused by the next level
+}
+
+__global__ void __launch_bounds__(256) affine_cell_fwd_kernel(const __grid_constant__ AffCellArgs a) {
+  extern __shared__ float4 smem4[];
+  float* sm = reinterpret_cast<float*>(smem4);
+  const CellArgs& c = a.cell;
+  const int u0 = blockIdx.x * kAffCellUnits;
+  const int U = min(kAffCellUnits, c.H - u0);
+  const int NR = (c.gw / c.H) * kAffCellUnits;
+  float* ws = sm;                                   // [NR][KP] weight rows of this CTA's units
+  float* xs = ws + (size_t)NR * a.kpad;             // [R][KP] inputs, terms at koff[t] (zero padded)
+  float* gs = xs + (size_t)a.rows * a.kpad;         // [R][NR] gate values, then k-part partials
+  __shared__ float* sval[20 * 64];
+  __shared__ const float* xrow[kAffCellMaxTerms][64];
+  stage_weights(a, ws, u0, U);
+  pdl_prologue();  // weights above do not depend on the preceding kernel: their loads overlap its tail
+  level_fwd(a, ws, xs, gs, sval, xrow, u0, U);
+}
+
+// Every level of a tree in ONE launch (Tree-LSTM leaves + compose levels,
+// builders.py:250-274): the weight rows of this CTA's units for each weight
+// set (leaf Wx, compose U1|U2) are staged once and stay in shared memory for
+// every level; a grid-wide barrier separates the levels (a level's inputs
+// are the previous levels' h).  Cooperative launch: all CTAs co-resident.
+__global__ void __launch_bounds__(256) tree_fwd_kernel(const __grid_constant__ TreeFwdArgs t) {
+  extern __shared__ float4 smem4[];
+  float* sm = reinterpret_cast<float*>(smem4);
+  __shared__ float* sval[20 * 64];
+  __shared__ const float* xrow[kAffCellMaxTerms][64];
+  __shared__ AffCellArgs lv;
+  const int H = t.H;
+  const int u0 = blockIdx.x * kAffCellUnits;
+  const int U = min(kAffCellUnits, H - u0);
+  float* ws[2] = {sm, sm + t.wfloats[0]};
+  float* xs = sm + t.wfloats[0] + t.wfloats[1];
+  for (int w = 0; w < t.n_wsets; ++w) stage_weights(t.wset[w], ws[w], u0, U);
+  pdl_prologue();
+  cgrp::grid_group grid = cgrp::this_grid();
+  for (int l = 0; l < t.n_levels; ++l) {
+    if (threadIdx.x == 0) lv = t.levels[l];
+    __syncthreads();
+    const int w = lv.wslot;
+    float* gs = xs + (size_t)lv.rows * lv.kpad;
+    level_fwd(lv, ws[w], xs, gs, sval, xrow, u0, U);
+    if (l + 1 < t.n_levels) {
+      __threadfence();
+      grid.sync();
+    }
   }
 }
 
@@ -297,8 +348,33 @@ int launch_affine_dx_small(const AffCellArgs& a, cudaStream_t s) {
 
 size_t affine_cell_smem(int rows, int kpad, int gw, int H) {
   const int NR = (gw / H) * kAffCellUnits;
-  // inputs, weight rows, gate values, k-part partial sums (<= 8 parts x 3 terms)
+  // weight rows, inputs, gate values, k-part partial sums (<= 8 parts x 3 terms)
   return 4 * ((size_t)rows * kpad + (size_t)NR * kpad + (size_t)rows * NR + 24 * (size_t)rows * NR);
+}
+
+size_t tree_fwd_smem(const TreeFwdArgs& t) {
+  // weight sets, then the largest level's inputs + gate values + partials
+  size_t lvl = 0;
+  for (int w = 0; w < t.n_wsets; ++w) {
+    const AffCellArgs& a = t.wset[w];
+    const int NR = (a.cell.gw / a.cell.H) * kAffCellUnits;
+    lvl = std::max(lvl, (size_t)t.max_rows * a.kpad + (size_t)t.max_rows * NR + 24 * (size_t)t.max_rows * NR);
+  }
+  return 4 * ((size_t)t.wfloats[0] + t.wfloats[1] + lvl);
+}
+
+int launch_tree_fwd(const TreeFwdArgs& t, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tree_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  const int grid = (t.H + kAffCellUnits - 1) / kAffCellUnits;
+  void* args[] = {const_cast<TreeFwdArgs*>(&t)};
+  if (cudaLaunchCooperativeKernel((const void*)tree_fwd_kernel, dim3(grid), dim3(256), args, tree_fwd_smem(t), s) !=
+      cudaSuccess)
+    return -1;
+  return 1;
 }
 
 int launch_affine_cell_fwd(const AffCellArgs& a, cudaStream_t s) {

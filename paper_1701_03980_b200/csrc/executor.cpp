@@ -2609,7 +2609,9 @@ static GruArgs gru_args(const dg_graph* g, const Unit& u0, int n) {
 // is a grouped GEMM plus cell_fwd_kernel, two launches whose dependent memory
 // round trips dominate at a few rows.  Returns false (nothing planned) when
 // the pair does not qualify.
-static bool plan_affine_cell_fwd(dg_graph* g, const Schedule& S, size_t q, Plan& plan, GemmBatch& gb) {
+// Checks one (affine, cell) level and fills A; with a plan, also pushes the
+// level's row / slot tables into its blob (device pointers in A).
+static bool affine_cell_level(dg_graph* g, const Schedule& S, size_t q, Plan* plan, AffCellArgs& A) {
   static const bool on = [] {
     const char* e = std::getenv("DG_AFFCELL");
     return !(e && e[0] == '0');
@@ -2645,7 +2647,7 @@ static bool plan_affine_cell_fwd(dg_graph* g, const Schedule& S, size_t q, Plan&
   // shared parameters: the same bias row and weights in every member
   const Node& b0 = g->nodes[g->inputs[a0.in_off]];
   if (b0.kind != DG_OP_PARAMETER || b0.batch != 1) return false;
-  AffCellArgs A{};
+  A = AffCellArgs{};
   int kp = 0;
   for (int t = 0; t < terms; ++t) {
     const Node& w = g->nodes[g->inputs[a0.in_off + 1 + 2 * t]];
@@ -2664,20 +2666,9 @@ static bool plan_affine_cell_fwd(dg_graph* g, const Schedule& S, size_t q, Plan&
   }
   A.kpad = kp;
   if (affine_cell_smem(rows, kp, c0.gw, c0.H) > 200 * 1024) return false;
-  flush_gemm(g, plan, gb);
-  Blob& B = plan.blob;
   A.rows = rows;
   A.terms = terms;
   A.bias = b0.val;
-  std::vector<size_t> ox(terms);
-  for (int t = 0; t < terms; ++t) {
-    std::vector<uintptr_t> xr((size_t)rows);
-    for (int j = 0; j < n; ++j) {
-      const Node& x = g->nodes[g->inputs[g->nodes[aff[j]].in_off + 2 + 2 * t]];
-      for (int b = 0; b < Bt; ++b) xr[(size_t)j * Bt + b] = P(x.val + (x.batch == 1 ? 0 : (int64_t)b * A.K[t]));
-    }
-    ox[t] = B.push(xr);
-  }
   CellArgs& a = A.cell;
   a.n = n;
   a.m = c0.m;
@@ -2689,6 +2680,16 @@ static bool plan_affine_cell_fwd(dg_graph* g, const Schedule& S, size_t q, Plan&
   a.off_g = c0.off[2];
   for (int k = 0; k < c0.m; ++k) a.off_f[k] = c0.off[3 + k];
   a.nslot = 10 + 5 * c0.m;
+  if (!plan) return true;
+  Blob& B = plan->blob;
+  for (int t = 0; t < terms; ++t) {
+    std::vector<uintptr_t> xr((size_t)rows);
+    for (int j = 0; j < n; ++j) {
+      const Node& x = g->nodes[g->inputs[g->nodes[aff[j]].in_off + 2 + 2 * t]];
+      for (int b = 0; b < Bt; ++b) xr[(size_t)j * Bt + b] = P(x.val + (x.batch == 1 ? 0 : (int64_t)b * A.K[t]));
+    }
+    A.x[t] = dev_at<const float*>(g, B.push(xr));
+  }
   std::vector<uintptr_t> vals((size_t)a.nslot * n);
   for (int j = 0; j < n; ++j) {
     const Unit& u = S.units[gc.units[j]];
@@ -2696,14 +2697,78 @@ static bool plan_affine_cell_fwd(dg_graph* g, const Schedule& S, size_t q, Plan&
     for (int x : u.ins) vals[(size_t)(sl++) * n + j] = P(g->nodes[x].val);
     for (int x : u.nodes) vals[(size_t)(sl++) * n + j] = P(g->nodes[x].val);
   }
-  const size_t ov = B.push(vals);
-  plan.ops.push_back([A, ox, ov](char* d) mutable {
-    A.cell.val = at<const float* const>(d, ov);
-    for (size_t t = 0; t < ox.size(); ++t) A.x[t] = at<const float* const>(d, ox[t]);
-    return launch_affine_cell_fwd(A, g_launch_stream);
-  });
-  plan.tag(C_GEMM_FWD, 2.0 * rows * c0.gw * kp, 4.0 * ((double)rows * kp + (double)kp * c0.gw + 14.0 * rows * c0.H));
+  a.val = dev_at<const float*>(g, B.push(vals));
   return true;
+}
+
+static double affine_cell_flops(const AffCellArgs& A) { return 2.0 * A.rows * A.cell.gw * A.kpad; }
+static double affine_cell_bytes(const AffCellArgs& A) {
+  return 4.0 * ((double)A.rows * A.kpad + (double)A.kpad * A.cell.gw + 14.0 * A.rows * A.cell.H);
+}
+
+static bool plan_affine_cell_fwd(dg_graph* g, const Schedule& S, size_t q, Plan& plan, GemmBatch& gb) {
+  AffCellArgs A;
+  if (!affine_cell_level(g, S, q, nullptr, A)) return false;
+  flush_gemm(g, plan, gb);
+  affine_cell_level(g, S, q, &plan, A);
+  plan.ops.push_back([A](char*) { return launch_affine_cell_fwd(A, g_launch_stream); });
+  plan.tag(C_GEMM_FWD, affine_cell_flops(A), affine_cell_bytes(A));
+  return true;
+}
+
+// A run of >= 2 consecutive (affine, cell) levels with at most two weight
+// sets and one hidden size (the leaves and compose levels of a Tree-LSTM):
+// one cooperative launch for all of them (cellgemm.cu tree_fwd_kernel).
+// Returns the number of groups consumed (0: not applicable).
+static size_t plan_tree_fwd(dg_graph* g, const Schedule& S, size_t q, Plan& plan, GemmBatch& gb) {
+  static const bool on = [] {
+    const char* e = std::getenv("DG_TREE_PERSIST");
+    return !(e && e[0] == '0');
+  }();
+  if (!on) return 0;
+  std::vector<AffCellArgs> lv;
+  TreeFwdArgs T{};
+  size_t qq = q;
+  for (;; qq += 2) {
+    AffCellArgs A;
+    if (!affine_cell_level(g, S, qq, nullptr, A)) break;
+    if (!lv.empty() && A.cell.H != lv[0].cell.H) break;
+    int w = -1;
+    for (int k = 0; k < T.n_wsets; ++k) {
+      const AffCellArgs& W = T.wset[k];
+      bool same = W.terms == A.terms && W.cell.gw == A.cell.gw && W.kpad == A.kpad && W.bias == A.bias;
+      for (int t = 0; t < A.terms && same; ++t) same = W.W[t] == A.W[t] && W.K[t] == A.K[t] && W.koff[t] == A.koff[t];
+      if (same) w = k;
+    }
+    if (w < 0) {
+      if (T.n_wsets == 2) break;
+      w = T.n_wsets++;
+      T.wset[w] = A;
+      T.wfloats[w] = (A.cell.gw / A.cell.H) * kAffCellUnits * A.kpad;
+    }
+    A.wslot = w;
+    T.max_rows = std::max(T.max_rows, A.rows);
+    lv.push_back(A);
+    if (tree_fwd_smem(T) > 200 * 1024) {
+      lv.pop_back();
+      break;
+    }
+  }
+  if (lv.size() < 2) return 0;
+  flush_gemm(g, plan, gb);
+  double flops = 0, bytes = 0;
+  for (size_t l = 0; l < lv.size(); ++l) {
+    affine_cell_level(g, S, q + 2 * l, &plan, lv[l]);
+    lv[l].wslot = (lv[l].cell.gw == T.wset[0].cell.gw && lv[l].W[0] == T.wset[0].W[0]) ? 0 : 1;
+    flops += affine_cell_flops(lv[l]);
+    bytes += affine_cell_bytes(lv[l]);
+  }
+  T.H = lv[0].cell.H;
+  T.n_levels = (int)lv.size();
+  T.levels = dev_at<AffCellArgs>(g, plan.blob.push(lv));
+  plan.ops.push_back([T](char*) { return launch_tree_fwd(T, g_launch_stream); });
+  plan.tag(C_GEMM_FWD, flops, bytes);
+  return 2 * lv.size();
 }
 
 static void plan_forward_group(dg_graph* g, const Schedule& S, const Group& gr, Plan& plan, GemmBatch& gb) {
@@ -3162,6 +3227,10 @@ static int do_forward(dg_graph* g, int upto) {
   {
     GemmBatch gb;
     for (size_t q = 0; q < S.groups.size(); ++q) {
+      if (const size_t used = plan_tree_fwd(g, S, q, plan, gb)) {
+        q += used - 1;  // every level of the run went into one launch
+        continue;
+      }
       if (plan_affine_cell_fwd(g, S, q, plan, gb)) {
         ++q;  // the cell group went into the same launch
         continue;

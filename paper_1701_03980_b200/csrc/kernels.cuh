@@ -175,7 +175,17 @@ struct AffCellArgs {
   const float* bias;                        // broadcast row (gw)
   float* const* gx[kAffCellMaxTerms];       // [rows] input gradient rows per term (backward)
   const float* const* grow;                 // [rows] gate gradient rows (backward)
+  int wslot;                                // tree launches: which staged weight set
 };
+// every level of a tree in one cooperative launch (cellgemm.cu tree_fwd_kernel)
+struct TreeFwdArgs {
+  int H, n_levels, n_wsets, max_rows;
+  int wfloats[2];            // shared-memory floats of each staged weight set
+  AffCellArgs wset[2];       // weight set w: terms, K, koff, kpad, W, gw, H (its rows / tables unused)
+  const AffCellArgs* levels;  // [n_levels] (device)
+};
+size_t tree_fwd_smem(const TreeFwdArgs& t);
+int launch_tree_fwd(const TreeFwdArgs& t, cudaStream_t s);
 constexpr int kAffCellCols = 8;  // backward: input columns per CTA
 size_t affine_cell_smem(int rows, int kpad, int gw, int H);
 int launch_affine_cell_fwd(const AffCellArgs& a, cudaStream_t s);

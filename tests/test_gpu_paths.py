@@ -14,6 +14,8 @@ with each fast path switched off, so the fallbacks stay parity-green too.
   DG_CUDA_GRAPH=1   cached plans replayed as CUDA graphs (default: launch by launch)
   DG_AFFCELL=0      gate affine and gated cell of a small level as a grouped
                     GEMM + cell kernel instead of one fused launch
+  DG_TREE_PERSIST=0 one fused launch per tree level instead of one
+                    cooperative launch for every level
 
 (the fused affine + cell path is exercised by the Tree-LSTM test added to
 the list below)
@@ -41,6 +43,7 @@ VARIANTS = {
     "plan_cache_off": {"DG_PLAN_CACHE": "0"},
     "cuda_graph_on": {"DG_CUDA_GRAPH": "1"},
     "affine_cell_unfused": {"DG_AFFCELL": "0"},
+    "tree_levels_per_launch": {"DG_TREE_PERSIST": "0"},
 }
 
 
