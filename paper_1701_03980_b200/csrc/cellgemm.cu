@@ -346,10 +346,15 @@ int launch_affine_dx_small(const AffCellArgs& a, cudaStream_t s) {
   return 1;
 }
 
+// k-part partial sums of level_fwd: L parts with L * pairs <= max(pairs, 256)
+static size_t part_floats(int rows, int NR) {
+  return (size_t)kAffCellMaxTerms * std::max<size_t>((size_t)rows * NR, 256);
+}
+
 size_t affine_cell_smem(int rows, int kpad, int gw, int H) {
   const int NR = (gw / H) * kAffCellUnits;
-  // weight rows, inputs, gate values, k-part partial sums (<= 8 parts x 3 terms)
-  return 4 * ((size_t)rows * kpad + (size_t)NR * kpad + (size_t)rows * NR + 24 * (size_t)rows * NR);
+  // weight rows, inputs, gate values, k-part partial sums
+  return 4 * ((size_t)rows * kpad + (size_t)NR * kpad + (size_t)rows * NR + part_floats(rows, NR));
 }
 
 size_t tree_fwd_smem(const TreeFwdArgs& t) {
@@ -358,7 +363,7 @@ size_t tree_fwd_smem(const TreeFwdArgs& t) {
   for (int w = 0; w < t.n_wsets; ++w) {
     const AffCellArgs& a = t.wset[w];
     const int NR = (a.cell.gw / a.cell.H) * kAffCellUnits;
-    lvl = std::max(lvl, (size_t)t.max_rows * a.kpad + (size_t)t.max_rows * NR + 24 * (size_t)t.max_rows * NR);
+    lvl = std::max(lvl, (size_t)t.max_rows * a.kpad + (size_t)t.max_rows * NR + part_floats(t.max_rows, NR));
   }
   return 4 * ((size_t)t.wfloats[0] + t.wfloats[1] + lvl);
 }
