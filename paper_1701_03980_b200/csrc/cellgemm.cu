@@ -135,7 +135,7 @@ __device__ void level_fwd(const AffCellArgs& a, const float* ws, float* xs, floa
     const int blk = q / kAffCellUnits, uu = q - blk * kAffCellUnits;
     if (uu >= U) continue;
     const int grow = blk * c.H + u0 + uu;
-    float v = a.bias[grow];
+    float v = a.bias ? a.bias[grow] : 0.f;
     for (int t = 0; t < a.terms; ++t) {
       float dot = 0.f;
       for (int l = 0; l < L; ++l) dot += part[((size_t)t * L + l) * pairs + p];
@@ -143,9 +143,26 @@ __device__ void level_fwd(const AffCellArgs& a, const float* ws, float* xs, floa
     }
     gs[p] = v;
     const int j = r / c.batch, b = r - j * c.batch;
-    sval[j][(int64_t)b * c.gw + grow] = v;  // the gate node's value
+    sval[j][(int64_t)b * c.gw + grow] = v;  // the gate (affine / matmul) node's value
+    if (a.act) sval[c.n + j][(int64_t)b * c.gw + grow] = a.act == 1 ? tanhf(v) : sigmoid_ref(v);
+  }
+  if (a.cat && blockIdx.x == 0) {  // the concatenate node's value: the staged inputs side by side
+    for (int idx = threadIdx.x; idx < R * a.kpad; idx += blockDim.x) {
+      const int r = idx / a.kpad, k = idx - (idx / a.kpad) * a.kpad;
+      int t = 0, base = 0;
+      while (t + 1 < a.terms && k >= a.koff[t + 1]) {
+        base += a.K[t];
+        ++t;
+      }
+      const int kk = k - a.koff[t];
+      if (kk < a.K[t]) a.cat[r][base + kk] = xs[(size_t)r * a.kpad + k];
+    }
   }
   __syncthreads();
+  if (a.act) {
+    __syncthreads();
+    return;
+  }
   const int m = c.m;
   const int s_pick0 = 1 + m, s_act0 = s_pick0 + 3 + m, s_prod0 = s_act0 + 3 + m, s_add0 = s_prod0 + 1 + m;
   const int s_tc = s_add0 + m, s_h = s_tc + 1;

@@ -2701,6 +2701,135 @@ static bool affine_cell_level(dg_graph* g, const Schedule& S, size_t q, Plan* pl
   return true;
 }
 
+// A small affine / matmul level followed by its activation group (simple
+// RNN steps: tanh(affine(b, Wx, x, Wh, h)), builders.py:90-91) or a
+// concatenate -> matmul -> tanh level (TreeRNN compose: tanh(matmul(W,
+// concatenate([e1, e2]))), builders.py:183-210): the same fused launch as a
+// gated-cell level, the activation in place of the cell.  Fills A (and, with
+// a plan, pushes its tables); returns the number of groups it covers.
+static size_t act_level(dg_graph* g, const Schedule& S, size_t q, Plan* plan, AffCellArgs& A) {
+  static const bool on = [] {
+    const char* e = std::getenv("DG_AFFCELL");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || q + 1 >= S.groups.size()) return 0;
+  const Group& g0 = S.groups[q];
+  const bool tree = g0.kind == DG_OP_CONCATENATE;
+  if (g0.kind != DG_OP_AFFINE && !tree) return 0;
+  if (tree && q + 2 >= S.groups.size()) return 0;
+  const Group& gm = tree ? S.groups[q + 1] : g0;  // the affine / matmul group
+  const Group& gt = S.groups[q + (tree ? 2 : 1)];
+  if (tree && gm.kind != DG_OP_MATMUL) return 0;
+  if (gt.kind != DG_OP_TANH && gt.kind != DG_OP_LOGISTIC) return 0;
+  const int n = (int)gt.units.size();
+  if ((int)gm.units.size() != n || (int)g0.units.size() != n) return 0;
+  std::unordered_map<int, int> mpos, cpos;
+  for (int j = 0; j < n; ++j) mpos[S.units[gm.units[j]].last()] = j;
+  if (tree)
+    for (int j = 0; j < n; ++j) cpos[S.units[g0.units[j]].last()] = j;
+  std::vector<int> mm(n), act(n), cat(n, -1);
+  for (int j = 0; j < n; ++j) {
+    act[j] = S.units[gt.units[j]].last();
+    auto it = mpos.find(g->inputs[g->nodes[act[j]].in_off]);
+    if (it == mpos.end()) return 0;
+    mm[j] = S.units[gm.units[it->second]].last();
+    if (tree) {
+      auto ic = cpos.find(g->inputs[g->nodes[mm[j]].in_off + 1]);
+      if (ic == cpos.end()) return 0;
+      cat[j] = S.units[g0.units[ic->second]].last();
+    }
+  }
+  const Node& m0 = g->nodes[mm[0]];
+  const int Bt = m0.batch, gw = (int)m0.elem, rows = n * Bt;
+  if (m0.rank != 1 || rows > 64 || gw <= 0) return 0;
+  A = AffCellArgs{};
+  int kp = 0, terms = 0;
+  if (!tree) {
+    terms = (m0.n_in - 1) / 2;
+    if (terms < 1 || terms > kAffCellMaxTerms) return 0;
+    const Node& b0 = g->nodes[g->inputs[m0.in_off]];
+    if (b0.kind != DG_OP_PARAMETER || b0.batch != 1) return 0;
+    A.bias = b0.val;
+    for (int t = 0; t < terms; ++t) {
+      const Node& w = g->nodes[g->inputs[m0.in_off + 1 + 2 * t]];
+      if (w.kind != DG_OP_PARAMETER || w.batch != 1) return 0;
+      A.W[t] = w.val;
+      A.K[t] = (int)g->nodes[g->inputs[m0.in_off + 2 + 2 * t]].elem;
+    }
+  } else {
+    const Node& w = g->nodes[g->inputs[m0.in_off]];
+    const Node& c0 = g->nodes[cat[0]];
+    if (w.kind != DG_OP_PARAMETER || w.batch != 1 || w.rank != 2 || c0.rank != 1) return 0;
+    terms = c0.n_in;
+    if (terms < 1 || terms > kAffCellMaxTerms) return 0;
+    int k0 = 0;
+    for (int t = 0; t < terms; ++t) {  // W [e1; e2] = W[:, part 1] e1 + W[:, part 2] e2
+      const Node& x = g->nodes[g->inputs[c0.in_off + t]];
+      if (x.rank != 1) return 0;
+      A.W[t] = w.val + (int64_t)k0 * gw;
+      A.K[t] = (int)x.elem;
+      k0 += A.K[t];
+    }
+    if (k0 != (int)c0.elem) return 0;
+  }
+  for (int t = 0; t < terms; ++t) {
+    A.koff[t] = kp;
+    kp += (A.K[t] + 3) & ~3;
+  }
+  for (int j = 0; j < n; ++j) {  // same parameters and shapes in every member
+    const Node& mj = g->nodes[mm[j]];
+    if (mj.n_in != m0.n_in || mj.batch != Bt || mj.elem != m0.elem || g->nodes[act[j]].batch != Bt) return 0;
+    if (!tree) {
+      if (g->nodes[g->inputs[mj.in_off]].val != A.bias) return 0;
+      for (int t = 0; t < terms; ++t)
+        if (g->nodes[g->inputs[mj.in_off + 1 + 2 * t]].val != A.W[t]) return 0;
+    } else {
+      const Node& cj = g->nodes[cat[j]];
+      if (g->nodes[g->inputs[mj.in_off]].val != A.W[0] || cj.n_in != terms || cj.batch != Bt) return 0;
+      for (int t = 0; t < terms; ++t)
+        if (g->nodes[g->inputs[cj.in_off + t]].elem != A.K[t] || g->nodes[g->inputs[cj.in_off + t]].batch != Bt)
+          return 0;
+    }
+  }
+  A.kpad = kp;
+  if (affine_cell_smem(rows, kp, gw, gw) > 200 * 1024) return 0;
+  A.rows = rows;
+  A.terms = terms;
+  A.act = gt.kind == DG_OP_TANH ? 1 : 2;
+  CellArgs& a = A.cell;
+  a.n = n;
+  a.H = gw;
+  a.gw = gw;
+  a.batch = Bt;
+  a.nslot = 2;
+  const size_t used = tree ? 3 : 2;
+  if (!plan) return used;
+  Blob& B = plan->blob;
+  for (int t = 0; t < terms; ++t) {
+    std::vector<uintptr_t> xr((size_t)rows);
+    for (int j = 0; j < n; ++j) {
+      const Node& x = tree ? g->nodes[g->inputs[g->nodes[cat[j]].in_off + t]]
+                           : g->nodes[g->inputs[g->nodes[mm[j]].in_off + 2 + 2 * t]];
+      for (int b = 0; b < Bt; ++b) xr[(size_t)j * Bt + b] = P(x.val + (x.batch == 1 ? 0 : (int64_t)b * A.K[t]));
+    }
+    A.x[t] = dev_at<const float*>(g, B.push(xr));
+  }
+  std::vector<uintptr_t> vals((size_t)2 * n);
+  for (int j = 0; j < n; ++j) {
+    vals[j] = P(g->nodes[mm[j]].val);
+    vals[(size_t)n + j] = P(g->nodes[act[j]].val);
+  }
+  a.val = dev_at<const float*>(g, B.push(vals));
+  if (tree) {
+    const int kc = (int)g->nodes[cat[0]].elem;
+    std::vector<uintptr_t> cr((size_t)rows);
+    for (int j = 0; j < n; ++j)
+      for (int b = 0; b < Bt; ++b) cr[(size_t)j * Bt + b] = P(g->nodes[cat[j]].val + (int64_t)b * kc);
+    A.cat = dev_at<float*>(g, B.push(cr));
+  }
+  return used;
+}
+
 static double affine_cell_flops(const AffCellArgs& A) { return 2.0 * A.rows * A.cell.gw * A.kpad; }
 static double affine_cell_bytes(const AffCellArgs& A) {
   return 4.0 * ((double)A.rows * A.kpad + (double)A.kpad * A.cell.gw + 14.0 * A.rows * A.cell.H);
@@ -3230,6 +3359,17 @@ static int do_forward(dg_graph* g, int upto) {
       if (const size_t used = plan_tree_fwd(g, S, q, plan, gb)) {
         q += used - 1;  // every level of the run went into one launch
         continue;
+      }
+      {
+        AffCellArgs A;
+        if (const size_t used = act_level(g, S, q, nullptr, A)) {
+          flush_gemm(g, plan, gb);
+          act_level(g, S, q, &plan, A);
+          plan.ops.push_back([A](char*) { return launch_affine_cell_fwd(A, g_launch_stream); });
+          plan.tag(C_GEMM_FWD, affine_cell_flops(A), affine_cell_bytes(A));
+          q += used - 1;
+          continue;
+        }
       }
       if (plan_affine_cell_fwd(g, S, q, plan, gb)) {
         ++q;  // the cell group went into the same launch

@@ -176,6 +176,12 @@ struct AffCellArgs {
   float* const* gx[kAffCellMaxTerms];       // [rows] input gradient rows per term (backward)
   const float* const* grow;                 // [rows] gate gradient rows (backward)
   int wslot;                                // tree launches: which staged weight set
+  // act != 0: no gated cell -- slot 0 = the affine / matmul node, slot 1 =
+  // its activation (1 tanh, 2 logistic); bias may be null (matmul); cat (if
+  // set): [rows] value rows of a concatenate node = the terms' inputs side by
+  // side (TreeRNN: tanh(matmul(W, concatenate([e1, e2]))))
+  int act;
+  float* const* cat;
 };
 // every level of a tree in one cooperative launch (cellgemm.cu tree_fwd_kernel)
 struct TreeFwdArgs {
