@@ -2883,7 +2883,8 @@ static size_t plan_tree_fwd(dg_graph* g, const Schedule& S, size_t q, Plan& plan
       break;
     }
   }
-  if (lv.size() < 2) return 0;
+  // cooperative launch: one CTA per kAffCellUnits units, all co-resident
+  if (lv.size() < 2 || (lv[0].cell.H + kAffCellUnits - 1) / kAffCellUnits > kSmCount) return 0;
   flush_gemm(g, plan, gb);
   double flops = 0, bytes = 0;
   for (size_t l = 0; l < lv.size(); ++l) {
