@@ -4267,7 +4267,7 @@ int dg_backward(dg_graph* g, int32_t loss) {
       struct Job {
         float* dst;
         size_t orow;
-        int nr, width;
+        int nr, width, vec;
       };
       std::vector<Job> jobs;
       double bytes = 0;
@@ -4279,7 +4279,7 @@ int dg_backward(dg_graph* g, int32_t loss) {
           G.n = (int)jobs.size();
           for (int q = 0; q < G.n; ++q)
             G.j[q] = ColsumJob{jobs[q].dst, at<const float* const>(d, jobs[q].orow), jobs[q].nr, jobs[q].width, 0, 0, 0,
-                               nullptr};
+                               nullptr, jobs[q].vec};
           return launch_colsum_group(G, work, wcap, st);
         });
         plan.tag(C_COLSUM, 0.0, bytes);
@@ -4289,7 +4289,7 @@ int dg_backward(dg_graph* g, int32_t loss) {
       for (int64_t h : bkeys) {
         auto& rows = buse[h];
         Param* p = param_at(h);
-        jobs.push_back({p->grad, B.push(rows), (int)rows.size(), (int)p->size()});
+        jobs.push_back({p->grad, B.push(rows), (int)rows.size(), (int)p->size(), all_aligned16(rows) ? 1 : 0});
         bytes += 4.0 * rows.size() * p->size() + 8.0 * p->size();
         if ((int)jobs.size() == kColsumGroup) flush_jobs();
       }

@@ -1212,6 +1212,49 @@ __global__ void colsum_partial_group_kernel(const __grid_constant__ ColsumGroup 
   if (c < J.width) J.work[(int64_t)ch * J.width + c] = s;
 }
 
+// Column sums over 16 B aligned rows (the logits bias: 10^4 columns over T*B
+// rows; the gate biases): a block reads kColsumWideRows whole row segments of
+// up to 2048 columns (contiguous 8 KiB, float4 per thread, 16 rows in flight)
+// instead of many rows x 1 KiB fragments -- DRAM pages stay open.  Grouped:
+// block -> (job, column slab, row chunk) through the jobs' pb0 offsets.
+// work[chunk][c], rows summed in order.
+constexpr int kColsumWideRows = 32;
+__global__ void __launch_bounds__(256) colsum_wide_partial_kernel(const __grid_constant__ ColsumGroup G) {
+  pdl_prologue();
+  int q = 0;
+  while (q + 1 < G.n && (int)blockIdx.x >= G.j[q + 1].pb0) ++q;
+  const ColsumJob& J = G.j[q];
+  const int w4 = J.width >> 2;
+  const int slabs = (w4 + 511) / 512;
+  const int lb = (int)blockIdx.x - J.pb0;
+  const int ch = lb / slabs, slab = lb - ch * slabs;
+  __shared__ const float* rp[kColsumWideRows];
+  const int r0 = ch * kColsumWideRows, nr = min(kColsumWideRows, J.n_rows - r0);
+  if ((int)threadIdx.x < nr) rp[threadIdx.x] = J.rows[r0 + threadIdx.x];
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int c4 = slab * 512 + i * 256 + threadIdx.x;
+    if (c4 >= w4) continue;
+    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int rb = 0; rb < nr; rb += 16) {
+      float4 v[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        v[r] = rb + r < nr ? __ldg(reinterpret_cast<const float4*>(rp[rb + r]) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        if (rb + r < nr) {
+          sum.x += v[r].x;
+          sum.y += v[r].y;
+          sum.z += v[r].z;
+          sum.w += v[r].w;
+        }
+    }
+    reinterpret_cast<float4*>(J.work + (int64_t)ch * J.width)[c4] = sum;
+  }
+}
+
 __global__ void colsum_final_group_kernel(const __grid_constant__ ColsumGroup G) {
   pdl_prologue();
   int q = 0;
@@ -1589,6 +1632,40 @@ int launch_affine_generic_bwd(const AffineGenericArgs& a, cudaStream_t s) {
 
 int launch_colsum_group(ColsumGroup G, float* work, int64_t work_floats, cudaStream_t s) {
   if (G.n <= 0) return 0;
+  // jobs with 16 B rows (width % 4 == 0): grouped row-segment partials, then
+  // one final pass; the others below
+  int launched = 0;
+  {
+    ColsumGroup W{}, N{};
+    int64_t off = 0;
+    int pb = 0, fb = 0;
+    for (int q = 0; q < G.n; ++q) {
+      ColsumJob J = G.j[q];
+      const int chunks = (J.n_rows + kColsumWideRows - 1) / kColsumWideRows;
+      const bool wide = J.vec && J.width % 4 == 0 && J.width >= 64 && off + (int64_t)chunks * J.width <= work_floats;
+      if (!wide) {
+        N.j[N.n++] = J;
+        continue;
+      }
+      J.chunks = chunks;
+      J.work = work + off;
+      off += ((int64_t)chunks * J.width + 63) & ~int64_t(63);
+      J.pb0 = pb;
+      J.fb0 = fb;
+      pb += chunks * ((J.width / 4 + 511) / 512);
+      fb += (J.width + 31) / 32;
+      W.j[W.n++] = J;
+    }
+    if (W.n) {
+      launch_k(colsum_wide_partial_kernel, pb, 256, 0, s, W);
+      launch_k(colsum_final_group_kernel, fb, 256, 0, s, W);
+      launched = 2;
+    }
+    if (N.n == 0) return launched;
+    G = N;
+    work += off;
+    work_floats -= off;
+  }
   // chunking per job as launch_colsum_rows, partials packed into the scratch
   int pb = 0, fb = 0;
   int64_t off = 0;
@@ -1611,7 +1688,7 @@ int launch_colsum_group(ColsumGroup G, float* work, int64_t work_floats, cudaStr
   }
   launch_k(colsum_partial_group_kernel, pb, 256, 0, s, G);
   launch_k(colsum_final_group_kernel, fb, 256, 0, s, G);
-  return 2;
+  return launched + 2;
 }
 
 int launch_colsum_rows(float* dst, const float* const* rows, int n_rows, int width, float* work, int64_t work_floats,

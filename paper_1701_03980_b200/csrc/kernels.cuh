@@ -375,6 +375,7 @@ struct ColsumJob {
   int n_rows, width;
   int chunks, pb0, fb0;  // filled by launch_colsum_group
   float* work;
+  int vec;               // every row 16 B aligned (wide row-segment path)
 };
 constexpr int kColsumGroup = 8;
 struct ColsumGroup {
