@@ -760,15 +760,20 @@ __global__ void __launch_bounds__(256) row_reg_kernel(RowArgs a) {
     m = fmaxf(m, fmaxf(fmaxf(v[i].x, v[i].y), fmaxf(v[i].z, v[i].w)));
   }
   m = row_reduce_max<true>(m, sh);
+  // exp(x - m) once: kept in the row registers for the output pass
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < kV; ++i)
-    if (threadIdx.x + 256 * i < n4) s += expf(v[i].x - m) + expf(v[i].y - m) + expf(v[i].z - m) + expf(v[i].w - m);
+    if (threadIdx.x + 256 * i < n4) {
+      v[i] = make_float4(expf(v[i].x - m), expf(v[i].y - m), expf(v[i].z - m), expf(v[i].w - m));
+      s += v[i].x + v[i].y + v[i].z + v[i].w;
+    }
   s = row_reduce_sum<true>(s, sh);
   if (kOp == 2) {
     if (threadIdx.x == 0) a.out[j][b] = m + logf(s) - x[a.labels[row]];
     return;
   }
+  const float inv_s = 1.f / s;
   const float g = kOp == 3 ? a.gout[j][b] : 1.f;
   const int lab = kOp == 3 ? a.labels[row] : -1;
   float4* d4 = reinterpret_cast<float4*>(kOp == 3 ? gi : o);
@@ -776,7 +781,7 @@ __global__ void __launch_bounds__(256) row_reg_kernel(RowArgs a) {
   for (int i = 0; i < kV; ++i) {
     const int q = threadIdx.x + 256 * i;
     if (q >= n4) continue;
-    float4 p = make_float4(expf(v[i].x - m) / s, expf(v[i].y - m) / s, expf(v[i].z - m) / s, expf(v[i].w - m) / s);
+    float4 p = make_float4(v[i].x * inv_s, v[i].y * inv_s, v[i].z * inv_s, v[i].w * inv_s);
     if (kOp == 3) {
       if ((lab >> 2) == q) {
         const int e = lab & 3;
