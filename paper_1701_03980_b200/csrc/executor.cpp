@@ -1531,6 +1531,15 @@ static bool tma_try(dg_graph* g, const Plan& plan, const GemmProblem& p0, bool a
   o.ldb = p.seg[0].B.ld;
   o.A_lo = lo_base;
   o.B_lo = lo_base + la_p;
+  // split-K partials: the scratch past the residual copies (all of it when the
+  // converter warps form the residuals); tile counters in the zeroed region
+  const int64_t lo_used = tma_conv_enabled() ? 0 : ((la_p + lb + 63) & ~int64_t(63));
+  if (lo_cap - lo_used >= (int64_t)128 * 128) {
+    o.ws = lo_base + lo_used;
+    o.ws_floats = lo_cap - lo_used;
+    o.cnt = counter_base(g);
+    o.cnt_cap = kScatterCtrBase;
+  }
   o.C = p.C;
   o.bias = p.bias;
   o.accumulate = p.accumulate;

@@ -439,7 +439,10 @@ bool tc_gemm_enabled();
 struct TmaGemmArgs {
   int M, N, K;
   int tiles_n, splits, accumulate, c_vec, pad_;
+  int gsplit;  // split-K partials reduced through `ws` by the tile's last CTA (no cluster)
   Operand C, bias;
+  float* ws;   // gsplit: one BM x BN partial per CTA of the launch
+  int* cnt;    // gsplit: zeroed per-tile arrival counters (left zero)
 };
 struct TmaOperands {
   int M, N, K;
@@ -452,6 +455,10 @@ struct TmaOperands {
   float* B_lo;
   Operand C, bias;
   int accumulate;
+  float* ws;           // optional split-K partial workspace (ws_floats floats) + zeroed tile counters
+  int64_t ws_floats;
+  int* cnt;
+  int cnt_cap;
 };
 constexpr int kTmaGroup = 4;  // problems per grouped TMA GEMM launch
 struct TmaProb {
@@ -476,11 +483,14 @@ struct TmaGemmPlan {
   float* b_lo;
   int64_t a_ld, a_rows, a_cols, a_colsp, b_ld, b_rows, b_cols, b_colsp;
   int ctas;
+  int64_t ws_floats;
+  int cnt_cap;
   double flops;
 };
 bool tma_gemm_enabled();  // DG_TMA=0 disables (A/B checks)
 bool tma_conv_enabled();  // DG_TMA_CONV=0: pre-split residual copies instead of in-smem conversion
 bool tma_at_enabled();    // DG_TMA_AT=0: A's split in shared memory instead of TMEM
+bool tma_gsplit_enabled();  // DG_TMA_GSPLIT=0: split-K through a cluster's shared memory instead of the workspace
 bool tma_lite_enabled();  // DG_TMA_LITE=0: no two-CTA-per-SM variant for short-K (per split) GEMMs
 int64_t tma_lo_floats(int64_t rows, int64_t cols);
 bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out);

@@ -169,8 +169,9 @@ __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
 }
 
 // ragged-N / unaligned tiles: element-wise stores (rare; kept out of line)
-__device__ __noinline__ void epilogue_scalar(const TmaGemmArgs& P, float* part, cgrp::cluster_group& cl, int S, int z,
-                                             int rows, int m0, int n0, bool has_bias) {
+__device__ __noinline__ void epilogue_scalar(const TmaGemmArgs& P, float* part, const float* gws,
+                                             cgrp::cluster_group& cl, int S, int z, int rows, int m0, int n0,
+                                             bool has_bias) {
   for (int e = threadIdx.x; e < rows * BN; e += blockDim.x) {
     const int lr = e / BN, c = e % BN;
     const int lm = z * rows + lr;
@@ -178,7 +179,9 @@ __device__ __noinline__ void epilogue_scalar(const TmaGemmArgs& P, float* part, 
     if (m >= P.M || n >= P.N) continue;
     const int sw = (c & ~3) + 4 * lm;
     float v = 0.f;
-    for (int q = 0; q < S; ++q) v += (S > 1 ? cl.map_shared_rank(part, q) : part)[lm * BN + (sw & (BN - 1)) + (c & 3)];
+    const int off = lm * BN + (sw & (BN - 1)) + (c & 3);
+    for (int q = 0; q < S; ++q)
+      v += gws ? __ldcg(gws + (size_t)q * (BM * BN) + off) : (S > 1 ? cl.map_shared_rank(part, q) : part)[off];
     float* crow = const_cast<float*>(orow(P.C, m));
     if (has_bias) v += orow(P.bias, m)[n];
     if (P.accumulate) v += crow[n];
@@ -518,10 +521,36 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, kLite ? 2 : 1
   const bool has_bias = P.bias.rows != nullptr || P.bias.base != nullptr;
   float* part = reinterpret_cast<float*>(smem);
   cgrp::cluster_group cl = cgrp::this_cluster();
-  if (S > 1) cl.sync();
-  else __syncthreads();
+  const bool gs = P.gsplit && S > 1;
+  // gsplit: the tile's S CTAs are not co-scheduled as a cluster; each
+  // publishes its partial (shared-memory layout verbatim) to the workspace and
+  // the last to arrive reduces all S in split order (deterministic)
+  const float* gws = gs ? P.ws + (size_t)(blockIdx.x - z) * (BM * BN) : nullptr;
+  if (gs) {
+    __shared__ int last_sh;
+    float4* dst = reinterpret_cast<float4*>(P.ws + (size_t)blockIdx.x * (BM * BN));
+    const float4* s4 = reinterpret_cast<const float4*>(part);
+    for (int i = threadIdx.x; i < BM * BN / 4; i += blockDim.x) __stcg(dst + i, s4[i]);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int t = (int)blockIdx.x / S;
+      const int last = atomicAdd(P.cnt + t, 1) == S - 1;
+      if (last) P.cnt[t] = 0;  // every split has arrived: leave the counter zero
+      last_sh = last;
+    }
+    __syncthreads();
+    if (!last_sh) return;
+    __threadfence();
+  } else if (S > 1) {
+    cl.sync();
+  } else {
+    __syncthreads();
+  }
   if (prof_e) g_tprof[5][4][0] = clock64();
-  const int rows = BM / S;  // S is a power of two <= 8: split z reduces rows [z*rows, (z+1)*rows)
+  // cluster: S is a power of two <= 8 and split z reduces rows [z*rows, (z+1)*rows)
+  const int rows = gs ? BM : BM / S;
+  const int zr = gs ? 0 : z;
   const bool vec = P.c_vec && n0 + BN <= P.N;
   // thread -> fixed 4-column slot ln (NT is a multiple of 32) and rows
   // r0, r0 + RS, ...: a warp writes one whole 512 B row segment per store;
@@ -532,14 +561,48 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, kLite ? 2 : 1
   constexpr int U = 4;
   const int ln = (threadIdx.x & 31) * 4;
   if (!vec) {
-    epilogue_scalar(P, part, cl, S, z, rows, m0, n0, has_bias);
+    epilogue_scalar(P, part, gws, cl, S, zr, rows, m0, n0, has_bias);
+  } else if (gs) {
+    // last CTA of a workspace split: whole tile, every split's loads of a row
+    // batch in flight before the in-order sum
+    constexpr int GU = 2;
+    const bool bias_bcast = has_bias && !P.bias.rows && P.bias.ld == 0;
+#pragma unroll 1
+    for (int rb = (int)(threadIdx.x >> 5); rb < BM; rb += GU * RS) {
+      float4 acc4[GU], pv[GU][8];
+      float* crow[GU];
+#pragma unroll
+      for (int u = 0; u < GU; ++u) {
+        const int lm = rb + u * RS;
+        const int64_t m = m0 + lm;
+        const bool ok = lm < BM && m < P.M;
+        crow[u] = ok ? const_cast<float*>(orow(P.C, m)) + n0 + ln : nullptr;
+        acc4[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ok && has_bias)
+          acc4[u] = *reinterpret_cast<const float4*>((bias_bcast ? P.bias.base : orow(P.bias, m)) + n0 + ln);
+        const int off = lm * BN + ((ln + 4 * lm) & (BN - 1));
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (ok && q < S) pv[u][q] = __ldcg(reinterpret_cast<const float4*>(gws + (size_t)q * (BM * BN) + off));
+      }
+#pragma unroll
+      for (int u = 0; u < GU; ++u) {
+        if (!crow[u]) continue;
+        float4 v = acc4[u];
+        if (P.accumulate) v = f4add(v, *reinterpret_cast<const float4*>(crow[u]));
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < S) v = f4add(v, pv[u][q]);
+        if (!(P.pad_ & 2048)) *reinterpret_cast<float4*>(crow[u]) = v;
+      }
+    }
   } else {
     const bool bias_bcast = has_bias && !P.bias.rows && P.bias.ld == 0;
     const float4 bconst =
         bias_bcast ? *reinterpret_cast<const float4*>(P.bias.base + n0 + ln) : make_float4(0.f, 0.f, 0.f, 0.f);
     const float* src[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) src[q] = q < S ? (S > 1 ? cl.map_shared_rank(part, q) : part) : part;
+    for (int q = 0; q < 8; ++q) src[q] = q < S && !gs ? (S > 1 ? cl.map_shared_rank(part, q) : part) : part;
 #pragma unroll 1
     for (int rb = (int)(threadIdx.x >> 5); rb < rows; rb += U * RS) {
       float4 acc4[U];
@@ -548,7 +611,7 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, kLite ? 2 : 1
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int lr = rb + u * RS;
-        const int64_t m = m0 + z * rows + lr;
+        const int64_t m = m0 + zr * rows + lr;
         const bool ok = lr < rows && m < P.M;
         crow[u] = ok ? const_cast<float*>(orow(P.C, m)) + n0 + ln : nullptr;
         brow[u] = ok && has_bias && !bias_bcast ? orow(P.bias, m) + n0 + ln : nullptr;
@@ -564,9 +627,11 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, kLite ? 2 : 1
       for (int q = 0; q < S; ++q) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int lm = z * rows + rb + u * RS;
+          const int lm = zr * rows + rb + u * RS;
+          const int off = lm * BN + ((ln + 4 * lm) & (BN - 1));
           if (rb + u * RS < rows)
-            acc4[u] = f4add(acc4[u], *reinterpret_cast<const float4*>(src[q] + lm * BN + ((ln + 4 * lm) & (BN - 1))));
+            acc4[u] = f4add(acc4[u], gs ? __ldcg(reinterpret_cast<const float4*>(gws + (size_t)q * (BM * BN) + off))
+                                        : *reinterpret_cast<const float4*>(src[q] + off));
         }
       }
 #pragma unroll
@@ -574,7 +639,7 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, kLite ? 2 : 1
         if (crow[u] && !(P.pad_ & 2048)) *reinterpret_cast<float4*>(crow[u]) = acc4[u];
     }
   }
-  if (S > 1) cl.sync();
+  if (S > 1 && !gs) cl.sync();
   if (prof_e) g_tprof[5][5][0] = clock64();
 }
 
@@ -729,6 +794,75 @@ bool tma_gemm_enabled() {
   return on && tc_gemm_enabled();
 }
 
+bool tma_gsplit_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DG_TMA_GSPLIT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static int tma_kernel_index(const TmaGemmPlan& p);
+using TmaKernel = void (*)(const TmaGroup);
+static TmaKernel tma_kernel(int ki);
+static int tma_smem(bool lite, bool a_tmem, bool conv) {
+  return lite ? kSmemLite : a_tmem ? kSmemAT : conv ? kSmemConv : kSmem;
+}
+static bool tma_attr(int ki, int smem) {
+  static bool attr[16] = {};
+  if (!attr[ki]) {
+    if (cudaFuncSetAttribute(tma_kernel(ki), cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return false;
+    attr[ki] = true;
+  }
+  return true;
+}
+
+// clusters of S CTAs of kernel variant ki that can be resident at once
+static int max_clusters(int ki, int S, int smem, int threads) {
+  static std::mutex mu;
+  static int cache[16][9] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache[ki][S]) return cache[ki][S];
+  int n = 0;
+  if (tma_attr(ki, smem)) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(S * 256);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = S;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&n, tma_kernel(ki), &cfg) != cudaSuccess) n = 0;
+    cudaGetLastError();
+  }
+  cache[ki][S] = n > 0 ? n : 1;
+  return cache[ki][S];
+}
+
+// Workspace split-K instead of clusters when the S-CTA clusters of a launch
+// would not all be co-resident (cluster placement is per GPC: on 148 SMs only
+// ~32 four-CTA clusters of a one-CTA-per-SM kernel fit, so 34 clusters run in
+// two rounds) while the same CTAs without clusters fit in one round.
+static bool use_gsplit(int tiles, int S, bool a_tmem, int K, int64_t ws_floats, int cnt_cap) {
+  if (S < 2 || !tma_gsplit_enabled() || cnt_cap < tiles || (int64_t)tiles * S * (BM * BN) > ws_floats) return false;
+  const bool lite = lite_ok(a_tmem, K, S);
+  const bool conv = tma_conv_enabled();
+  const int c = lite ? 2 : 1;
+  if (tiles * S > 148 * c) return false;
+  TmaGemmPlan q{};
+  q.lite = lite;
+  q.a_tmem = a_tmem;
+  q.conv = conv;
+  const int ki = tma_kernel_index(q);
+  const int mc = max_clusters(ki, S, tma_smem(lite, a_tmem, conv), conv ? kThreadsConv : kThreads);
+  return tiles > mc;
+}
+
 int64_t tma_lo_floats(int64_t rows, int64_t cols) { return rows * ((cols + 3) & ~int64_t(3)); }
 
 bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
@@ -776,6 +910,10 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
   a.tiles_n = (o.N + BN - 1) / BN;
   const int tiles = ((o.M + BM - 1) / BM) * a.tiles_n;
   const int kt = (o.K + BK - 1) / BK;
+  p.ws_floats = o.ws ? o.ws_floats : 0;
+  p.cnt_cap = o.cnt ? o.cnt_cap : 0;
+  a.ws = o.ws;
+  a.cnt = o.cnt;
   // split-K (a cluster of S CTAs per tile) for the best wave efficiency on
   // 148 SMs (one CTA per SM); each split keeps >= 4 k-tiles
   // cost model: waves x (fixed per-CTA cost ~ 4 k-tiles + k-tiles per split)
@@ -790,6 +928,7 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
       S = s2;
     }
   }
+  a.gsplit = use_gsplit(tiles, S, p.a_tmem, o.K, p.ws_floats, p.cnt_cap) ? 1 : 0;
   // DG_TMA_DBG (diagnostics, tools/tma_bench): bits 0-4 skip MMAs /
   // conversion / drains / epilogue / loads, bit 6 plain arrives for commits,
   // bit 7 no proxy fence, bit 10 CTA-0 wait timeline, bits 11-12 skip
@@ -800,6 +939,10 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
   }();
   a.pad_ = dbg & 0xFFFF;
   if ((dbg >> 16) & 0xF) S = (dbg >> 16) & 0xF;
+  if ((dbg >> 20) & 2) a.gsplit = p.ws_floats >= (int64_t)tiles * S * (BM * BN) && p.cnt_cap >= tiles;  // bit 21
+  if (a.gsplit && (int64_t)tiles * S * (BM * BN) > p.ws_floats) S = 1;
+  if (!a.gsplit && (S & (S - 1))) S = 1;  // cluster splits reduce BM / S rows each
+  if (S == 1) a.gsplit = 0;
   a.splits = S;
   p.ctas = tiles * S;
   p.lite = lite_ok(p.a_tmem, o.K, S);
@@ -812,11 +955,9 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
   return true;
 }
 
-static int tma_kernel_index(const TmaGemmPlan& p) {
+static int tma_kernel_index(const TmaGemmPlan& p) {  // (declared above)
   return (p.lite ? 12 : p.a_tmem ? 8 : p.conv ? 4 : 0) + (p.a_mn ? 2 : 0) + (p.b_mn ? 1 : 0);
 }
-
-using TmaKernel = void (*)(const TmaGroup);
 
 static TmaKernel tma_kernel(int ki) {
   static const TmaKernel table[16] = {
@@ -835,12 +976,8 @@ static int tma_launch(const TmaGemmPlan* const* ps, int n, cudaStream_t s) {
   const TmaGemmPlan& p = *ps[0];
   const int ki = tma_kernel_index(p);
   const TmaKernel k = tma_kernel(ki);
-  static bool attr[16] = {};
-  const int smem = p.lite ? kSmemLite : p.a_tmem ? kSmemAT : p.conv ? kSmemConv : kSmem;
-  if (!attr[ki]) {
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
-    attr[ki] = true;
-  }
+  const int smem = tma_smem(p.lite, p.a_tmem, p.conv);
+  if (!tma_attr(ki, smem)) return -1;
   static TmaGroup G;  // launch arguments are copied at launch
   G.n = n;
   int ctas = 0;
@@ -860,7 +997,7 @@ static int tma_launch(const TmaGemmPlan* const* ps, int n, cudaStream_t s) {
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = p.args.splits;
+  at[0].val.clusterDim.x = p.args.gsplit ? 1 : p.args.splits;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -919,8 +1056,17 @@ void tma_gemm_regroup(TmaGemmPlan* const* ps, int n) {
       S = s2;
     }
   }
+  // workspace split-K when every problem shares one workspace
+  bool gs = true;
+  int K_max = 0;
+  for (int i = 0; i < n; ++i) {
+    gs = gs && ps[i]->args.ws == ps[0]->args.ws && ps[i]->args.cnt == ps[0]->args.cnt;
+    K_max = std::max(K_max, ps[i]->args.K);
+  }
+  gs = gs && use_gsplit(tiles, S, ps[0]->a_tmem, K_max, ps[0]->ws_floats, ps[0]->cnt_cap);
   for (int i = 0; i < n; ++i) {
     TmaGemmArgs& a = ps[i]->args;
+    a.gsplit = gs ? 1 : 0;
     a.splits = S;
     ps[i]->ctas = ((a.M + BM - 1) / BM) * a.tiles_n * S;
     ps[i]->lite = lite_ok(ps[i]->a_tmem, a.K, S);

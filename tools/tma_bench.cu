@@ -55,6 +55,20 @@ static void run(const char* name, int M, int N, int K, bool a_mn, bool b_mn, boo
   o.B_lo = Blo;
   o.C.base = C;
   o.C.ld = N;
+  static float* ws = nullptr;
+  static int* cnt = nullptr;
+  const int64_t ws_floats = (int64_t)64 << 20;
+  if (!ws) {
+    CK(cudaMalloc(&ws, ws_floats * 4));
+    CK(cudaMalloc(&cnt, 65536 * 4));
+    CK(cudaMemset(cnt, 0, 65536 * 4));
+  }
+  if (!getenv("TMA_NO_WS")) {
+    o.ws = ws;
+    o.ws_floats = ws_floats;
+    o.cnt = cnt;
+    o.cnt_cap = 65536;
+  }
   o.accumulate = 1;
   std::vector<float> hb;
   float* bias = nullptr;
@@ -91,8 +105,8 @@ static void run(const char* name, int M, int N, int K, bool a_mn, bool b_mn, boo
         scale = std::max(scale, std::fabs(s));
       }
     }
-    printf("check %-26s M%5d N%5d K%5d a_mn %d b_mn %d split %d  max|err| %.3e (scale %.3e, rel %.2e) %s\n", name, M,
-           N, K, a_mn, b_mn, p.args.splits, worst, scale, worst / scale, worst / scale < 8e-6 ? "OK" : "FAIL");
+    printf("check %-26s M%5d N%5d K%5d a_mn %d b_mn %d split %d%s  max|err| %.3e (scale %.3e, rel %.2e) %s\n", name, M,
+           N, K, a_mn, b_mn, p.args.splits, p.args.gsplit ? "g" : "c", worst, scale, worst / scale, worst / scale < 8e-6 ? "OK" : "FAIL");
   }
   if (getenv("TMA_PROF")) {  // DG_TMA_DBG bit 10: CTA 0 wait timeline of one launch
     CK(cudaDeviceSynchronize());
@@ -130,8 +144,8 @@ static void run(const char* name, int M, int N, int K, bool a_mn, bool b_mn, boo
     float ms;
     CK(cudaEventElapsedTime(&ms, e0, e1));
     const double us = 1e3 * ms / reps;
-    printf("time  %-26s ctas %5d split %d  %8.2f us  %7.2f TFLOP/s (3xTF32 issued %.1f TF/s)\n", name, p.ctas,
-           p.args.splits, us, p.flops / (us * 1e-6) / 1e12, 3 * p.flops / (us * 1e-6) / 1e12);
+    printf("time  %-26s ctas %5d split %d%s  %8.2f us  %7.2f TFLOP/s (3xTF32 issued %.1f TF/s)\n", name, p.ctas,
+           p.args.splits, p.args.gsplit ? "g" : "c", us, p.flops / (us * 1e-6) / 1e12, 3 * p.flops / (us * 1e-6) / 1e12);
     CK(cudaEventRecord(e0));
     for (int i = 0; i < reps; ++i) launch_tma_gemm(p, true, true, 0);
     CK(cudaEventRecord(e1));
