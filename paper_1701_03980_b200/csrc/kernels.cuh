@@ -440,6 +440,7 @@ struct TmaGemmArgs {
   int M, N, K;
   int tiles_n, splits, accumulate, c_vec, pad_;
   int gsplit;  // split-K partials reduced through `ws` by the tile's last CTA (no cluster)
+  int tstore;  // persistent kernel: C written by TMA tensor stores (map in TmaProb::mAl)
   Operand C, bias;
   float* ws;   // gsplit: one BM x BN partial per CTA of the launch
   int* cnt;    // gsplit: zeroed per-tile arrival counters (left zero)
@@ -477,6 +478,8 @@ struct TmaGemmPlan {
   bool conv;  // residuals formed in shared memory by converter warps (no lo copies)
   bool a_tmem;  // conv with A's hi/lo split stored in TMEM (MMAs read only B from shared memory)
   bool lite;    // a_tmem, K per split <= 1280: 2 stages, one accumulator, two CTAs per SM
+  bool pers;    // lite-shaped single-split problem with many tiles: persistent CTAs, double-buffered
+                // TMEM accumulators, each tile's epilogue overlapping the next tile's mainloop
   const float* a_src;
   const float* b_src;
   float* a_lo;
@@ -491,6 +494,8 @@ bool tma_gemm_enabled();  // DG_TMA=0 disables (A/B checks)
 bool tma_conv_enabled();  // DG_TMA_CONV=0: pre-split residual copies instead of in-smem conversion
 bool tma_at_enabled();    // DG_TMA_AT=0: A's split in shared memory instead of TMEM
 bool tma_gsplit_enabled();  // DG_TMA_GSPLIT=0: split-K through a cluster's shared memory instead of the workspace
+bool tma_pers_enabled();  // DG_TMA_PERS=0: no persistent variant
+bool tma_tstore_enabled();  // DG_TMA_TSTORE=0: persistent epilogue with thread stores instead of TMA stores
 bool tma_lite_enabled();  // DG_TMA_LITE=0: no two-CTA-per-SM variant for short-K (per split) GEMMs
 int64_t tma_lo_floats(int64_t rows, int64_t cols);
 bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out);

@@ -67,6 +67,12 @@ constexpr int kSmemAT = kStagesAT * 3 * kOpBytes + 1024;
 constexpr int kStagesLite = 2;
 constexpr int kSmemLite = kStagesLite * 3 * kOpBytes + 1024;
 constexpr int kLiteMaxK = 1024;
+// persistent variant: 4 stages of A_raw | B_raw | B_lo, two 16 KiB output
+// staging buffers (32 columns each); TMEM: two 128-column accumulators + A's
+// hi/lo per stage
+constexpr int kStagesPers = 4;
+constexpr int kThreadsPers = 448;  // producer, MMA, 4 epilogue, 4 A-converter, 4 B-converter warps
+constexpr int kSmemPers = kStagesPers * 3 * kOpBytes + 2 * BM * 32 * 4 + 1024;
 constexpr int kLiteMaxKSplit = 768;  // per split, when a cluster reduces the splits
 
 // DG_TMA_DBG bit 10: CTA 0 records (before, after) clock64 of each role's
@@ -643,6 +649,351 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, kLite ? 2 : 1
   if (prof_e) g_tprof[5][5][0] = clock64();
 }
 
+// Persistent form of the lite kernel for single-split problems with many
+// tiles (the output-layer logits: ~1.3k tiles, K = 256).  One CTA per SM
+// walks tiles blockIdx.x, +gridDim.x, ...; the operand ring runs across tile
+// boundaries and the MMA warp alternates two TMEM accumulators, so the
+// epilogue warps drain tile i (registers -> staging tile -> coalesced rows)
+// while tile i+1 is multiplied.  Same MMA sequence and the same epilogue
+// arithmetic as the lite kernel (bit-identical results).
+template <bool kAMN, bool kBMN>
+__global__ void __launch_bounds__(kThreadsPers, 1) tma_gemm_pers_kernel(const __grid_constant__ TmaGroup G) {
+  const TmaProb& PR = G.p[0];
+  const CUtensorMap& mAh = PR.mAh;
+  const CUtensorMap& mBh = PR.mBh;
+  const CUtensorMap& mC = PR.mAl;  // tstore: C's tensor map (the A residual map is unused here)
+  const TmaGemmArgs& P = PR.args;
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int NS = kStagesPers;
+  constexpr int SB = 3 * kOpBytes;
+  constexpr uint32_t kAcol = 2 * BN;
+  __shared__ uint64_t full[NS], empty[NS], conv[NS], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tmem_sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_m = (P.M + BM - 1) / BM;
+  const int ntiles = tiles_m * P.tiles_n;
+  const int nkt = (P.K + BK - 1) / BK;
+  const bool prof = (P.pad_ & 1024) && blockIdx.x == 0;  // DG_TMA_DBG bit 10: CTA 0 wait timeline
+#define PWAIT(role, jj, b, ph)                           \
+  do {                                                   \
+    const long long tb_ = prof ? clock64() : 0;          \
+    mbar_wait(b, ph);                                    \
+    if (prof && (jj) < 256) {                            \
+      g_tprof[role][jj][0] = tb_;                        \
+      g_tprof[role][jj][1] = clock64();                  \
+    }                                                    \
+  } while (0)
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&conv[s], 8);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAh)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBh)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_sh)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  pdl_prologue();
+  const uint32_t tmem = tmem_sh;
+  const uint32_t sbase = su32(smem);
+  float* part = reinterpret_cast<float*>(smem + NS * SB);  // output staging tile
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int j = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int m0 = (tile % tiles_m) * BM, n0 = (tile / tiles_m) * BN;
+        for (int kt = 0; kt < nkt; ++kt, ++j) {
+          const int s = j % NS, use = j / NS;
+          if (use > 0) PWAIT(0, j, &empty[s], (use - 1) & 1);
+          if (P.pad_ & 16) {  // DG_TMA_DBG bit 4: no loads
+            mbar_arrive(&full[s]);
+            continue;
+          }
+          mbar_expect_tx(&full[s], 2 * kOpBytes);
+          const uint32_t st = sbase + s * SB;
+          const int k0 = kt * BK;
+          if (!kAMN) {
+            tma_2d(st, &mAh, k0, m0, &full[s]);
+          } else {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) tma_2d(st + g * 4096, &mAh, m0 + 32 * g, k0, &full[s]);
+          }
+          if (!kBMN) {
+            tma_2d(st + kOpBytes, &mBh, k0, n0, &full[s]);
+          } else {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) tma_2d(st + kOpBytes + g * 4096, &mBh, n0 + 32 * g, k0, &full[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = uidesc(false, kBMN);
+      int j = 0, i = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+        const int a = i & 1;
+        if (i >= 2) PWAIT(1, i, &acc_empty[a], ((i >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t acc = tmem + (uint32_t)(a * BN);
+        for (int kt = 0; kt < nkt; ++kt, ++j) {
+          const int s = j % NS, use = j / NS;
+          PWAIT(2, j, &conv[s], use & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t ah = tmem + kAcol + 64u * (uint32_t)s, al = ah + 32u;
+          const uint32_t bh = sbase + s * SB + kOpBytes, bl = bh + kOpBytes;
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const uint32_t ob = kBMN ? ks * 1024 : ks * 32;
+            const uint32_t first = (kt == 0 && ks == 0) ? 0u : 1u;
+            if (P.pad_ & 1) continue;  // DG_TMA_DBG bit 0: no MMAs
+            mma_tf32_ta(acc, ah + 8u * ks, udesc(bh + ob, kBMN), idesc, first);
+            mma_tf32_ta(acc, ah + 8u * ks, udesc(bl + ob, kBMN), idesc, 1u);
+            mma_tf32_ta(acc, al + 8u * ks, udesc(bh + ob, kBMN), idesc, 1u);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&acc_full[a]);
+      }
+    }
+  } else if (warp >= 10) {
+    // B-converter warps 10..13: B's residual into shared memory (elementwise,
+    // same swizzled layout)
+    const int ct = threadIdx.x - 10 * 32;
+    int j = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int kt = 0; kt < nkt; ++kt, ++j) {
+        const int s = j % NS, use = j / NS;
+        mbar_wait(&full[s], use & 1);
+        const uint32_t st = sbase + s * SB;
+        if (!(P.pad_ & 34)) {  // DG_TMA_DBG bit 1: no conversion (bit 5: no B residual)
+#pragma unroll
+          for (int i = 0; i < kOpBytes / 16 / 128; ++i) {
+            const uint32_t off = (uint32_t)(ct + i * 128) * 16u;
+            const float4 x = lds128(st + kOpBytes + off);
+            sts128(st + 2 * kOpBytes + off, make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w)));
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[s]);
+      }
+    }
+  } else if (warp >= 6) {
+    // A-converter warps 6..9 (TMEM lane quadrant warp % 4): A row m split
+    // into hi / lo in TMEM lane m
+    const int q = warp & 3, m = 32 * q + lane;
+    int j = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int kt = 0; kt < nkt; ++kt, ++j) {
+        const int s = j % NS, use = j / NS;
+        if (threadIdx.x == 6 * 32) PWAIT(3, j, &full[s], use & 1);
+        else mbar_wait(&full[s], use & 1);
+        const uint32_t st = sbase + s * SB;
+        if (!(P.pad_ & 514)) {  // bit 9: no A split
+          uint32_t hi[32], lo[32];
+          if (!kAMN) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const float4 x = lds128(st + (uint32_t)m * 128u + ((uint32_t)(c ^ (m & 7)) << 4));
+              const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                hi[4 * c + e] = tf32_rn_bits(xv[e]);
+                lo[4 * c + e] = __float_as_uint(xv[e] - __uint_as_float(hi[4 * c + e]));
+              }
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              const float x = lds32(st + (uint32_t)q * 4096u + (uint32_t)k * 128u +
+                                    ((uint32_t)(((lane >> 3) ^ (k & 3))) << 5) + ((uint32_t)(lane & 7) << 2));
+              hi[k] = tf32_rn_bits(x);
+              lo[k] = __float_as_uint(x - __uint_as_float(hi[k]));
+            }
+          }
+          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + kAcol + 64u * (uint32_t)s;
+          tmem_st32(ta, hi);
+          tmem_st32(ta + 32u, lo);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[s]);
+      }
+    }
+  } else {
+    // epilogue warps 2..5 (TMEM lane quadrant warp % 4): 32 columns at a time,
+    // registers -> staging buffer (h & 1) -> 8 threads per 128 B row segment
+    const int quad = warp & 3, et = threadIdx.x - 64;
+    const int lrow = quad * 32 + lane;
+    const int c4 = et & 7, r0 = et >> 3;  // store phase: column quad, first row
+    const bool has_bias = P.bias.rows != nullptr || P.bias.base != nullptr;
+    const bool bias_bcast = has_bias && !P.bias.rows && P.bias.ld == 0;
+    int i = 0;
+    if (P.tstore) {
+      // TMA tensor stores: row lrow's 32 columns of a chunk (+ broadcast bias)
+      // into staging buffer h & 1 in the 128 B-swizzled box layout, one
+      // thread stores the box; OOB rows / columns are clipped by the TMA unit
+      const uint32_t stg0 = su32(part);
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+        const int a = i & 1;
+        const int m0 = (tile % tiles_m) * BM, n0 = (tile / tiles_m) * BN;
+        if (threadIdx.x == 64) PWAIT(4, i, &acc_full[a], (i >> 1) & 1);
+        else mbar_wait(&acc_full[a], (i >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+        for (int h = 0; h < BN / 32; ++h) {
+          uint32_t r[32];
+          const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(a * BN + h * 32);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+              : "r"(taddr));
+          const int nc = n0 + h * 32;
+          float bv[32];
+#pragma unroll
+          for (int q = 0; q < 32; q += 4) {
+            if (has_bias && nc + q + 3 < P.N) {
+              const float4 t = *reinterpret_cast<const float4*>(P.bias.base + nc + q);
+              bv[q] = t.x, bv[q + 1] = t.y, bv[q + 2] = t.z, bv[q + 3] = t.w;
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) bv[q + e] = has_bias && nc + q + e < P.N ? P.bias.base[nc + q + e] : 0.f;
+            }
+          }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (h == BN / 32 - 1) {
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[a]);
+          }
+          // buffer h & 1 was last read by the store of chunk h - 2
+          if (threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          const uint32_t stg = stg0 + (uint32_t)((h & 1) * BM * 32 * 4);
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            sts128(stg + (uint32_t)lrow * 128u + ((uint32_t)(c ^ (lrow & 7)) << 4),
+                   make_float4(bv[4 * c] + __uint_as_float(r[4 * c]), bv[4 * c + 1] + __uint_as_float(r[4 * c + 1]),
+                               bv[4 * c + 2] + __uint_as_float(r[4 * c + 2]),
+                               bv[4 * c + 3] + __uint_as_float(r[4 * c + 3])));
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (threadIdx.x == 64 && !(P.pad_ & 8)) {
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                    reinterpret_cast<uint64_t>(&mC)),
+                "r"(nc), "r"(m0), "r"(stg)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+        if (prof && threadIdx.x == 64 && i < 256) g_tprof[5][i][0] = clock64();
+      }
+      if (threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    for (int tile = P.tstore ? ntiles : blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+      const int a = i & 1;
+      const int m0 = (tile % tiles_m) * BM, n0 = (tile / tiles_m) * BN;
+      const bool vec = P.c_vec && n0 + BN <= P.N;
+      float4 bpre[BN / 32];  // broadcast bias of this thread's column quad in each chunk, loaded ahead
+#pragma unroll
+      for (int h = 0; h < BN / 32; ++h)
+        bpre[h] = vec && bias_bcast ? *reinterpret_cast<const float4*>(P.bias.base + n0 + h * 32 + 4 * c4)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (threadIdx.x == 64) PWAIT(4, i, &acc_full[a], (i >> 1) & 1);
+      else mbar_wait(&acc_full[a], (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int h = 0; h < BN / 32; ++h) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(a * BN + h * 32);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+              "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+              "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+              "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const bool pe = prof && threadIdx.x == 64 && i >= 1 && i <= 3;
+        if (pe) g_tprof[4][64 + i * 16 + h * 4 + 0][0] = clock64();
+        if (h == BN / 32 - 1) {  // accumulator drained: the MMA warp may refill it
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[a]);
+        }
+        float* stg = part + (h & 1) * (BM * 32);
+#pragma unroll
+        for (int q = 0; q < 32; q += 4)
+          *reinterpret_cast<float4*>(stg + lrow * 32 + ((q + 4 * lrow) & 31)) =
+              make_float4(__uint_as_float(r[q]), __uint_as_float(r[q + 1]), __uint_as_float(r[q + 2]),
+                          __uint_as_float(r[q + 3]));
+        // buffer h & 1 complete; its previous contents (chunk h - 2) were
+        // stored before every thread passed the barrier of chunk h - 1
+        if (pe) g_tprof[4][64 + i * 16 + h * 4 + 1][0] = clock64();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (pe) g_tprof[4][64 + i * 16 + h * 4 + 2][0] = clock64();
+        const int nc = n0 + h * 32;
+        if (P.pad_ & 8) continue;  // DG_TMA_DBG bit 3: no global stores
+        if (vec) {
+          const float4 bconst = bpre[h];
+#pragma unroll 4
+          for (int lr = r0; lr < BM; lr += 16) {
+            const int64_t m = m0 + lr;
+            if (m >= P.M) break;
+            float* crow = const_cast<float*>(orow(P.C, m)) + nc + 4 * c4;
+            float4 v = bconst;
+            if (P.accumulate) v = f4add(v, *reinterpret_cast<const float4*>(crow));
+            if (has_bias && !bias_bcast) v = f4add(v, *reinterpret_cast<const float4*>(orow(P.bias, m) + nc + 4 * c4));
+            v = f4add(v, *reinterpret_cast<const float4*>(stg + lr * 32 + ((4 * c4 + 4 * lr) & 31)));
+            *reinterpret_cast<float4*>(crow) = v;
+          }
+          if (pe) g_tprof[4][64 + i * 16 + h * 4 + 3][0] = clock64();
+        } else {
+          for (int e = et; e < BM * 32; e += 128) {
+            const int lr = e >> 5, c = e & 31;
+            const int64_t m = m0 + lr, n = nc + c;
+            if (m >= P.M || n >= P.N) continue;
+            float v = 0.f;
+            v += stg[lr * 32 + (((c & ~3) + 4 * lr) & 31) + (c & 3)];
+            float* crow = const_cast<float*>(orow(P.C, m));
+            if (has_bias) v += orow(P.bias, m)[n];
+            if (P.accumulate) v += crow[n];
+            crow[n] = v;
+          }
+        }
+      }
+      if (prof && threadIdx.x == 64 && i < 256) g_tprof[5][i][0] = clock64();
+    }
+  }
+#undef PWAIT
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 // lo[r][c] = x - tf32(x) for up to two rows x cols blocks (A and B of one
 // GEMM in a single launch), row stride ld; dst dense with stride cols_p
 struct SplitJob {
@@ -794,6 +1145,32 @@ bool tma_gemm_enabled() {
   return on && tc_gemm_enabled();
 }
 
+bool tma_pers_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DG_TMA_PERS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static int sm_count() {
+  static const int n = [] {
+    int d = 0, v = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess)
+      v = 148;
+    return v > 0 ? v : 148;
+  }();
+  return n;
+}
+
+bool tma_tstore_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DG_TMA_TSTORE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool tma_gsplit_enabled() {
   static const bool on = [] {
     const char* e = getenv("DG_TMA_GSPLIT");
@@ -805,11 +1182,11 @@ bool tma_gsplit_enabled() {
 static int tma_kernel_index(const TmaGemmPlan& p);
 using TmaKernel = void (*)(const TmaGroup);
 static TmaKernel tma_kernel(int ki);
-static int tma_smem(bool lite, bool a_tmem, bool conv) {
-  return lite ? kSmemLite : a_tmem ? kSmemAT : conv ? kSmemConv : kSmem;
+static int tma_smem(bool lite, bool a_tmem, bool conv, bool pers = false) {
+  return pers ? kSmemPers : lite ? kSmemLite : a_tmem ? kSmemAT : conv ? kSmemConv : kSmem;
 }
 static bool tma_attr(int ki, int smem) {
-  static bool attr[16] = {};
+  static bool attr[20] = {};
   if (!attr[ki]) {
     if (cudaFuncSetAttribute(tma_kernel(ki), cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
       return false;
@@ -821,7 +1198,7 @@ static bool tma_attr(int ki, int smem) {
 // clusters of S CTAs of kernel variant ki that can be resident at once
 static int max_clusters(int ki, int S, int smem, int threads) {
   static std::mutex mu;
-  static int cache[16][9] = {};
+  static int cache[20][9] = {};
   std::lock_guard<std::mutex> lk(mu);
   if (cache[ki][S]) return cache[ki][S];
   int n = 0;
@@ -946,6 +1323,15 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
   a.splits = S;
   p.ctas = tiles * S;
   p.lite = lite_ok(p.a_tmem, o.K, S);
+  // persistent CTAs once the lite tiles fill more than ~two rounds of two CTAs per SM
+  p.pers = p.lite && S == 1 && tma_pers_enabled() && tiles > 4 * sm_count();
+  a.tstore = 0;
+  const bool bias_ok = !(o.bias.base || o.bias.rows) || (o.bias.base && !o.bias.rows && o.bias.ld == 0 &&
+                                                          reinterpret_cast<uintptr_t>(o.bias.base) % 16 == 0);
+  if (p.pers && tma_tstore_enabled() && !o.accumulate && !o.C.rows && o.C.base && bias_ok &&
+      reinterpret_cast<uintptr_t>(o.C.base) % 16 == 0 && o.C.ld % 4 == 0 &&
+      make_map(&p.mAl, o.C.base, o.C.ld, o.M, o.N, false))
+    a.tstore = 1;
   if (dbg & 0x100000)  // DG_TMA_DBG bit 20: log each planned GEMM
     fprintf(stderr, "[tma] M %d N %d K %d a_mn %d b_mn %d acc %d bias %d rows %d split %d ctas %d\n", o.M, o.N, o.K,
             (int)o.a_mn, (int)o.b_mn, o.accumulate, (int)(o.bias.base || o.bias.rows), (int)(o.C.rows != nullptr), S,
@@ -956,11 +1342,11 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
 }
 
 static int tma_kernel_index(const TmaGemmPlan& p) {  // (declared above)
-  return (p.lite ? 12 : p.a_tmem ? 8 : p.conv ? 4 : 0) + (p.a_mn ? 2 : 0) + (p.b_mn ? 1 : 0);
+  return (p.pers ? 16 : p.lite ? 12 : p.a_tmem ? 8 : p.conv ? 4 : 0) + (p.a_mn ? 2 : 0) + (p.b_mn ? 1 : 0);
 }
 
 static TmaKernel tma_kernel(int ki) {
-  static const TmaKernel table[16] = {
+  static const TmaKernel table[20] = {
       tma_gemm_kernel<false, false, false>,      tma_gemm_kernel<false, true, false>,
       tma_gemm_kernel<true, false, false>,       tma_gemm_kernel<true, true, false>,
       tma_gemm_kernel<false, false, true>,       tma_gemm_kernel<false, true, true>,
@@ -968,7 +1354,9 @@ static TmaKernel tma_kernel(int ki) {
       tma_gemm_kernel<false, false, true, true>, tma_gemm_kernel<false, true, true, true>,
       tma_gemm_kernel<true, false, true, true>,  tma_gemm_kernel<true, true, true, true>,
       tma_gemm_kernel<false, false, true, true, true>, tma_gemm_kernel<false, true, true, true, true>,
-      tma_gemm_kernel<true, false, true, true, true>,  tma_gemm_kernel<true, true, true, true, true>};
+      tma_gemm_kernel<true, false, true, true, true>,  tma_gemm_kernel<true, true, true, true, true>,
+      tma_gemm_pers_kernel<false, false>,              tma_gemm_pers_kernel<false, true>,
+      tma_gemm_pers_kernel<true, false>,               tma_gemm_pers_kernel<true, true>};
   return table[ki];
 }
 
@@ -976,7 +1364,7 @@ static int tma_launch(const TmaGemmPlan* const* ps, int n, cudaStream_t s) {
   const TmaGemmPlan& p = *ps[0];
   const int ki = tma_kernel_index(p);
   const TmaKernel k = tma_kernel(ki);
-  const int smem = tma_smem(p.lite, p.a_tmem, p.conv);
+  const int smem = tma_smem(p.lite, p.a_tmem, p.conv, p.pers);
   if (!tma_attr(ki, smem)) return -1;
   static TmaGroup G;  // launch arguments are copied at launch
   G.n = n;
@@ -991,8 +1379,8 @@ static int tma_launch(const TmaGemmPlan* const* ps, int n, cudaStream_t s) {
     ctas += ps[i]->ctas;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(ctas);
-  cfg.blockDim = dim3(p.conv ? kThreadsConv : kThreads);
+  cfg.gridDim = dim3(p.pers ? std::min(ctas, sm_count()) : ctas);
+  cfg.blockDim = dim3(p.pers ? kThreadsPers : p.conv ? kThreadsConv : kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
@@ -1028,6 +1416,7 @@ int launch_tma_gemm(const TmaGemmPlan& p, bool split_a, bool split_b, cudaStream
 }
 
 bool tma_gemm_groupable(const TmaGemmPlan& a, const TmaGemmPlan& b) {
+  if (a.pers || b.pers) return false;
   if (!a.conv || !b.conv || a.a_tmem != b.a_tmem || a.a_mn != b.a_mn || a.b_mn != b.b_mn) return false;
   if (a.args.C.rows || b.args.C.rows) return false;
   // output blocks must not overlap (problems of a group run concurrently)
@@ -1070,6 +1459,7 @@ void tma_gemm_regroup(TmaGemmPlan* const* ps, int n) {
     a.splits = S;
     ps[i]->ctas = ((a.M + BM - 1) / BM) * a.tiles_n * S;
     ps[i]->lite = lite_ok(ps[i]->a_tmem, a.K, S);
+    ps[i]->pers = false;
   }
 }
 

@@ -1,0 +1,13 @@
+#!/bin/bash
+# persistent logits GEMM: correctness + timing, parity tests, A/B bench
+mkdir -p gpurun_out
+out=gpurun_out/tma_pers.txt; : > $out
+timeout 120 ./tools/tma_bench 2>&1 | grep -E "check|time" >> $out; echo "rc=$?" >> $out
+echo "== DG_TMA_PERS=0" >> $out
+DG_TMA_PERS=0 timeout 120 ./tools/tma_bench t 2>&1 | grep -E "^time" >> $out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_paths.py -m gpu -q -x --timeout 600 -p no:cacheprovider > gpurun_out/pytest_tma.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_tma.log
+rm -f gpurun_out/ab_pers.txt
+for i in 1 2; do
+  DG_TMA_PERS=0 DG_TMA_GSPLIT=0 timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu --only >> gpurun_out/ab_pers.txt 2>&1
+  timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu --only >> gpurun_out/ab_pers.txt 2>&1
+done

@@ -115,17 +115,26 @@ static void run(const char* name, int M, int N, int K, bool a_mn, bool b_mn, boo
     static long long t[6][256][2];
     tma_prof_read(&t[0][0][0]);
     long long base = t[2][0][0];
-    const char* role[5] = {"prod empty", "mma acc_empty", "mma conv", "conv full", "epi acc_full"};
+    const char* role[6] = {"prod empty", "mma acc_empty", "mma conv", "conv full", "epi acc_full", "epi end(pers)"};
     printf("prof %s (cycles rel. to first MMA wait; wait duration)\n", name);
-    for (int r = 0; r < 5; ++r) {
+    for (int r = 0; r < 6; ++r) {
       printf("  %-14s", role[r]);
       int shown = 0;
-      for (int j = 0; j < 256 && shown < 24; ++j) {
+      for (int j = 0; j < 256 && shown < 40; ++j) {
         if (t[r][j][0] == 0 && t[r][j][1] == 0) continue;
         printf(" [%d]%lld+%lld", j, t[r][j][0] - base, t[r][j][1] - t[r][j][0]);
         ++shown;
       }
       printf("\n");
+    }
+    if (getenv("TMA_PROF_EPI")) {
+      for (int i = 1; i <= 3; ++i) {
+        printf("  epi tile %d chunks (ld, staged, bar, stored):", i);
+        for (int h = 0; h < 4; ++h)
+          printf(" [%lld %lld %lld %lld]", t[4][64 + i * 16 + h * 4][0] - base, t[4][64 + i * 16 + h * 4 + 1][0] - base,
+                 t[4][64 + i * 16 + h * 4 + 2][0] - base, t[4][64 + i * 16 + h * 4 + 3][0] - base);
+        printf("\n");
+      }
     }
     printf("  phases (clk from kernel start): mainloop end %lld, part stored %lld, sync %lld, cluster sync %lld, end %lld\n",
            t[5][1][0] - t[5][0][0], t[5][2][0] - t[5][0][0], t[5][3][0] - t[5][0][0], t[5][4][0] - t[5][0][0],
