@@ -672,8 +672,10 @@ __global__ void __launch_bounds__(kThreadsPers, 1) tma_gemm_pers_kernel(const __
   __shared__ uint32_t tmem_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_m = (P.M + BM - 1) / BM;
-  const int ntiles = tiles_m * P.tiles_n;
-  const int nkt = (P.K + BK - 1) / BK;
+  const int S = P.splits;  // work unit u = (tile u / S, K split u % S); S > 1: workspace partials
+  const int ntiles = tiles_m * P.tiles_n * S;  // work units
+  const int kt_total = (P.K + BK - 1) / BK;
+  __shared__ int last_sh;
   const bool prof = (P.pad_ & 1024) && blockIdx.x == 0;  // DG_TMA_DBG bit 10: CTA 0 wait timeline
 #define PWAIT(role, jj, b, ph)                           \
   do {                                                   \
@@ -713,8 +715,10 @@ __global__ void __launch_bounds__(kThreadsPers, 1) tma_gemm_pers_kernel(const __
   if (warp == 0) {
     if (lane == 0) {
       int j = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
+        const int tile = u / S, z = u % S;
         const int m0 = (tile % tiles_m) * BM, n0 = (tile / tiles_m) * BN;
+        const int t0 = kt_total * z / S, nkt = kt_total * (z + 1) / S - t0;
         for (int kt = 0; kt < nkt; ++kt, ++j) {
           const int s = j % NS, use = j / NS;
           if (use > 0) PWAIT(0, j, &empty[s], (use - 1) & 1);
@@ -724,7 +728,7 @@ __global__ void __launch_bounds__(kThreadsPers, 1) tma_gemm_pers_kernel(const __
           }
           mbar_expect_tx(&full[s], 2 * kOpBytes);
           const uint32_t st = sbase + s * SB;
-          const int k0 = kt * BK;
+          const int k0 = (t0 + kt) * BK;
           if (!kAMN) {
             tma_2d(st, &mAh, k0, m0, &full[s]);
           } else {
@@ -744,7 +748,9 @@ __global__ void __launch_bounds__(kThreadsPers, 1) tma_gemm_pers_kernel(const __
     if (lane == 0) {
       constexpr uint32_t idesc = uidesc(false, kBMN);
       int j = 0, i = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+      for (int u = blockIdx.x; u < ntiles; u += gridDim.x, ++i) {
+        const int z = u % S;
+        const int nkt = kt_total * (z + 1) / S - kt_total * z / S;
         const int a = i & 1;
         if (i >= 2) PWAIT(1, i, &acc_empty[a], ((i >> 1) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
@@ -774,7 +780,8 @@ __global__ void __launch_bounds__(kThreadsPers, 1) tma_gemm_pers_kernel(const __
     // same swizzled layout)
     const int ct = threadIdx.x - 10 * 32;
     int j = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
+      const int nkt = kt_total * (u % S + 1) / S - kt_total * (u % S) / S;
       for (int kt = 0; kt < nkt; ++kt, ++j) {
         const int s = j % NS, use = j / NS;
         mbar_wait(&full[s], use & 1);
@@ -797,7 +804,8 @@ __global__ void __launch_bounds__(kThreadsPers, 1) tma_gemm_pers_kernel(const __
     // into hi / lo in TMEM lane m
     const int q = warp & 3, m = 32 * q + lane;
     int j = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
+      const int nkt = kt_total * (u % S + 1) / S - kt_total * (u % S) / S;
       for (int kt = 0; kt < nkt; ++kt, ++j) {
         const int s = j % NS, use = j / NS;
         if (threadIdx.x == 6 * 32) PWAIT(3, j, &full[s], use & 1);
@@ -849,7 +857,7 @@ __global__ void __launch_bounds__(kThreadsPers, 1) tma_gemm_pers_kernel(const __
       // into staging buffer h & 1 in the 128 B-swizzled box layout, one
       // thread stores the box; OOB rows / columns are clipped by the TMA unit
       const uint32_t stg0 = su32(part);
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {  // S == 1: unit = tile
         const int a = i & 1;
         const int m0 = (tile % tiles_m) * BM, n0 = (tile / tiles_m) * BN;
         if (threadIdx.x == 64) PWAIT(4, i, &acc_full[a], (i >> 1) & 1);
@@ -911,7 +919,122 @@ __global__ void __launch_bounds__(kThreadsPers, 1) tma_gemm_pers_kernel(const __
       }
       if (threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
-    for (int tile = P.tstore ? ntiles : blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+    if (S > 1) {
+      // split units: the raw accumulator goes to workspace slot u (row-major
+      // 128 x 128); the tile's last unit to arrive adds bias, C and the S
+      // partials in split order (the cluster kernels' arithmetic and order)
+      const int ew = warp - 2;
+      for (int u = blockIdx.x; u < ntiles; u += gridDim.x, ++i) {
+        const int a = i & 1;
+        const int tile = u / S;
+        const int m0 = (tile % tiles_m) * BM, n0 = (tile / tiles_m) * BN;
+        if (threadIdx.x == 64) PWAIT(4, i, &acc_full[a], (i >> 1) & 1);
+        else mbar_wait(&acc_full[a], (i >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        float* slot = P.ws + (size_t)u * (BM * BN) + (size_t)lrow * BN;
+#pragma unroll 1
+        for (int h = 0; h < BN / 32; ++h) {
+          uint32_t r[32];
+          const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(a * BN + h * 32);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (h == BN / 32 - 1) {
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[a]);
+          }
+#pragma unroll
+          for (int q = 0; q < 32; q += 4)
+            __stcg(reinterpret_cast<float4*>(slot + h * 32 + q),
+                   make_float4(__uint_as_float(r[q]), __uint_as_float(r[q + 1]), __uint_as_float(r[q + 2]),
+                               __uint_as_float(r[q + 3])));
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 64) {
+          const int last = atomicAdd(P.cnt + tile, 1) == S - 1;
+          if (last) P.cnt[tile] = 0;  // every split has arrived: leave the counter zero
+          last_sh = last;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (last_sh) {
+          __threadfence();
+          const float* base = P.ws + (size_t)tile * S * (BM * BN);
+          const int ln = lane * 4;
+          const bool vec = P.c_vec && n0 + BN <= P.N;
+          const float4 bconst = vec && bias_bcast ? *reinterpret_cast<const float4*>(P.bias.base + n0 + ln)
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+          for (int lr0 = ew; lr0 < BM; lr0 += 8) {
+            // rows lr0 and lr0 + 4: the partials in batches of 8 (all loads of
+            // a batch in flight), summed in split order
+            float4 acc[2];
+            bool ok[2];
+            float* crow[2];
+#pragma unroll
+            for (int w = 0; w < 2; ++w) {
+              const int64_t m = m0 + lr0 + 4 * w;
+              ok[w] = m < P.M;
+              crow[w] = ok[w] ? const_cast<float*>(orow(P.C, m)) : nullptr;
+              acc[w] = bconst;
+              if (ok[w] && vec) {
+                if (P.accumulate) acc[w] = f4add(acc[w], *reinterpret_cast<const float4*>(crow[w] + n0 + ln));
+                if (has_bias && !bias_bcast)
+                  acc[w] = f4add(acc[w], *reinterpret_cast<const float4*>(orow(P.bias, m) + n0 + ln));
+              }
+            }
+            float4 ps[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};  // scalar path
+#pragma unroll 1
+            for (int qb = 0; qb < S; qb += 8) {
+              float4 pv[2][8];
+#pragma unroll
+              for (int w = 0; w < 2; ++w)
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                  if (qb + q < S)
+                    pv[w][q] = __ldcg(reinterpret_cast<const float4*>(base + (size_t)(qb + q) * (BM * BN) +
+                                                                      (lr0 + 4 * w) * BN + ln));
+#pragma unroll
+              for (int w = 0; w < 2; ++w)
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                  if (qb + q < S) {
+                    if (vec) acc[w] = f4add(acc[w], pv[w][q]);
+                    else ps[w] = f4add(ps[w], pv[w][q]);
+                  }
+            }
+#pragma unroll
+            for (int w = 0; w < 2; ++w) {
+              if (!ok[w]) continue;
+              if (vec) {
+                *reinterpret_cast<float4*>(crow[w] + n0 + ln) = acc[w];
+              } else {
+                const int64_t m = m0 + lr0 + 4 * w;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int64_t n = n0 + ln + e;
+                  if (n >= P.N) continue;
+                  float v = reinterpret_cast<const float*>(&ps[w])[e];
+                  if (has_bias) v += orow(P.bias, m)[n];
+                  if (P.accumulate) v += crow[w][n];
+                  crow[w][n] = v;
+                }
+              }
+            }
+          }
+        }
+        if (prof && threadIdx.x == 64 && i < 256) g_tprof[5][i][0] = clock64();
+      }
+    }
+    for (int tile = P.tstore || S > 1 ? ntiles : blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
       const int a = i & 1;
       const int m0 = (tile % tiles_m) * BM, n0 = (tile / tiles_m) * BN;
       const bool vec = P.c_vec && n0 + BN <= P.N;
@@ -1163,6 +1286,17 @@ static int sm_count() {
   return n;
 }
 
+constexpr int kPersMaxSplit = 16;
+// work units per SM below which the persistent kernel is not used
+// (DG_TMA_PERS_MIN, default 4)
+static int pers_min_units() {
+  static const int v = [] {
+    const char* e = getenv("DG_TMA_PERS_MIN");
+    return e ? atoi(e) : 4;
+  }();
+  return v;
+}
+
 bool tma_tstore_enabled() {
   static const bool on = [] {
     const char* e = getenv("DG_TMA_TSTORE");
@@ -1323,12 +1457,47 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
   a.splits = S;
   p.ctas = tiles * S;
   p.lite = lite_ok(p.a_tmem, o.K, S);
-  // persistent CTAs once the lite tiles fill more than ~two rounds of two CTAs per SM
-  p.pers = p.lite && S == 1 && tma_pers_enabled() && tiles > 4 * sm_count();
+  // persistent CTAs once the lite-sized work units (tile x K split) fill more
+  // than ~two rounds of two CTAs per SM: the split factor minimises rounds x
+  // (k-tiles per unit + a partial-tile cost per split)
+  p.pers = false;
+  if (tma_pers_enabled() && p.a_tmem && !(dbg & 0xF0000)) {
+    const int sm = sm_count();
+    double best_c = 1e30;
+    int best_s = 0;
+    // DG_TMA_PERS_SPLIT=1: split problems as persistent work units too (opt-in:
+    // the PTB dW 100 -> 210 us, dX 80 -> 235 us; profiles/r02i_tma_pers_split.txt)
+    static const bool split_on = [] {
+      const char* e = getenv("DG_TMA_PERS_SPLIT");
+      return e && e[0] == '1';
+    }();
+    for (int s2 = 1; s2 <= (split_on ? kPersMaxSplit : 1); ++s2) {
+      const int per = (kt + s2 - 1) / s2;
+      if (per * BK > (s2 == 1 ? kLiteMaxK : kLiteMaxKSplit) || !tma_lite_enabled()) continue;
+      if (s2 > 1 && (kt < 4 * s2 || !tma_gsplit_enabled() || p.cnt_cap < tiles ||
+                     (int64_t)tiles * s2 * (BM * BN) > p.ws_floats))
+        continue;
+      const int units = tiles * s2;
+      if (units <= pers_min_units() * sm) continue;
+      const double c = (double)((units + sm - 1) / sm) * (per + (s2 > 1 ? 0.25 * s2 : 0.0));
+      if (c < best_c) {
+        best_c = c;
+        best_s = s2;
+      }
+    }
+    if (best_s) {
+      p.pers = true;
+      p.lite = true;
+      S = best_s;
+      a.splits = S;
+      a.gsplit = S > 1;
+      p.ctas = tiles * S;
+    }
+  }
   a.tstore = 0;
   const bool bias_ok = !(o.bias.base || o.bias.rows) || (o.bias.base && !o.bias.rows && o.bias.ld == 0 &&
                                                           reinterpret_cast<uintptr_t>(o.bias.base) % 16 == 0);
-  if (p.pers && tma_tstore_enabled() && !o.accumulate && !o.C.rows && o.C.base && bias_ok &&
+  if (p.pers && S == 1 && tma_tstore_enabled() && !o.accumulate && !o.C.rows && o.C.base && bias_ok &&
       reinterpret_cast<uintptr_t>(o.C.base) % 16 == 0 && o.C.ld % 4 == 0 &&
       make_map(&p.mAl, o.C.base, o.C.ld, o.M, o.N, false))
     a.tstore = 1;

@@ -14,5 +14,6 @@ full() {  # name, kernel regex, skip, count
 full full_rnnf rnn_fwd_cl 2 2
 full full_rnnb rnn_bwd_cl 2 2
 full full_tma tma_gemm_kernel 8 6
+full full_pers tma_gemm_pers 1 1
 full full_row row_reg_kernel 2 2
 full full_bw "scatter_rows|gather_rows|colsum_partial|update_dense|update_rows" 5 10

@@ -65,7 +65,7 @@ for i in range(n_meas):
     torch.cuda.synchronize()
     cg.profile_reset()
     cg.renew()
-    loss = bench.call_loss(task, cg, data[i])
+    loss = bench.call_loss(task, cg, data[i % len(data)])
     cg._prepare()
     torch.cuda._sleep(int(40e6))  # ~20 ms spin
     e0 = torch.cuda.Event(enable_timing=True)
