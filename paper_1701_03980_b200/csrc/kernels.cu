@@ -974,6 +974,35 @@ __global__ void __launch_bounds__(256) scatter_rows_kernel(float* __restrict__ t
   if (!last) return;
   __threadfence();
   const float* pb = partials + (int64_t)it.pbase * dim;
+  if ((dim & 3) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (reinterpret_cast<uintptr_t>(pb) & 15) == 0) {
+    // one float4 column group per lane, 16 partial loads in flight (the EOS
+    // segment of a padded minibatch has ~60 chunks); same chunk-order sums
+    for (int c4 = lane; c4 < (dim >> 2); c4 += 32) {
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q0 = 0; q0 < it.nchunks; q0 += 16) {
+        float4 v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (q0 + i < it.nchunks) v[i] = __ldcg(reinterpret_cast<const float4*>(pb + (int64_t)(q0 + i) * dim) + c4);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (q0 + i < it.nchunks) {
+            s.x += v[i].x;
+            s.y += v[i].y;
+            s.z += v[i].z;
+            s.w += v[i].w;
+          }
+      }
+      float* d = dst + 4 * c4;
+      if (kSet) {
+        d[0] = s.x / scale, d[1] = s.y / scale, d[2] = s.z / scale, d[3] = s.w / scale;
+      } else {
+        d[0] += scale * s.x, d[1] += scale * s.y, d[2] += scale * s.z, d[3] += scale * s.w;
+      }
+    }
+    if (lane == 0) counters[it.seg_slot] = 0;
+    return;
+  }
   for (int c = lane; c < dim; c += 32) {
     float s = 0.f;
     int q = 0;

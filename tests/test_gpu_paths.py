@@ -16,6 +16,9 @@ with each fast path switched off, so the fallbacks stay parity-green too.
                     GEMM + cell kernel instead of one fused launch
   DG_TREE_PERSIST=0 one fused launch per tree level instead of one
                     cooperative launch for every level
+  DG_TMA_GSPLIT=0, DG_TMA_PERS=0, DG_TMA_TSTORE=0
+                    split-K only through clusters / no persistent logits GEMM /
+                    its epilogue with thread stores (run on the MB64 test)
 
 (the fused affine + cell path is exercised by the Tree-LSTM test added to
 the list below)
@@ -54,6 +57,26 @@ def test_ptb_parity_on_every_kernel_path(variant):
     tests = ["tests/test_gpu_parity.py::test_ptb_mb16_full_size_vs_oracle",
              "tests/test_gpu_parity.py::test_char_tagger_full_size_vs_oracle",
              "tests/test_gpu_parity.py::test_tree_lstm_full_size_vs_oracle"]
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", *tests],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+# output-layer GEMM paths that only the MB64 shapes reach (workspace split-K
+# for the K = 10^4 dX, the persistent logits kernel and its TMA stores)
+GEMM_VARIANTS = {
+    "tma_cluster_split_only": {"DG_TMA_GSPLIT": "0"},
+    "tma_pers_off": {"DG_TMA_PERS": "0"},
+    "tma_pers_thread_stores": {"DG_TMA_TSTORE": "0"},
+    "tma_pers_split_units": {"DG_TMA_PERS_SPLIT": "1"},
+}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", sorted(GEMM_VARIANTS))
+def test_ptb_mb64_parity_on_every_gemm_path(variant):
+    env = dict(os.environ, **GEMM_VARIANTS[variant])
+    tests = ["tests/test_gpu_parity.py::test_ptb_mb64_full_size_vs_oracle_sgd"]
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", *tests],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
