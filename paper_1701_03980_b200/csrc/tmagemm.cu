@@ -856,9 +856,13 @@ __global__ void __launch_bounds__(kThreadsPers, 1) tma_gemm_pers_kernel(const __
       // TMA tensor stores: row lrow's 32 columns of a chunk (+ broadcast bias)
       // into staging buffer h & 1 in the 128 B-swizzled box layout, one
       // thread stores the box; OOB rows / columns are clipped by the TMA unit
+      // S > 1: unit u's raw accumulator goes to rows [u*BM, u*BM + BM) of the
+      // partial workspace (mC maps it), summed afterwards by split_reduce_kernel
       const uint32_t stg0 = su32(part);
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {  // S == 1: unit = tile
+      const bool ext = S > 1;
+      for (int u = blockIdx.x; u < ntiles; u += gridDim.x, ++i) {
         const int a = i & 1;
+        const int tile = u / S;
         const int m0 = (tile % tiles_m) * BM, n0 = (tile / tiles_m) * BN;
         if (threadIdx.x == 64) PWAIT(4, i, &acc_full[a], (i >> 1) & 1);
         else mbar_wait(&acc_full[a], (i >> 1) & 1);
@@ -880,7 +884,9 @@ __global__ void __launch_bounds__(kThreadsPers, 1) tma_gemm_pers_kernel(const __
           float bv[32];
 #pragma unroll
           for (int q = 0; q < 32; q += 4) {
-            if (has_bias && nc + q + 3 < P.N) {
+            if (ext) {
+              bv[q] = bv[q + 1] = bv[q + 2] = bv[q + 3] = 0.f;
+            } else if (has_bias && nc + q + 3 < P.N) {
               const float4 t = *reinterpret_cast<const float4*>(P.bias.base + nc + q);
               bv[q] = t.x, bv[q + 1] = t.y, bv[q + 2] = t.z, bv[q + 3] = t.w;
             } else {
@@ -910,7 +916,7 @@ __global__ void __launch_bounds__(kThreadsPers, 1) tma_gemm_pers_kernel(const __
             asm volatile(
                 "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                     reinterpret_cast<uint64_t>(&mC)),
-                "r"(nc), "r"(m0), "r"(stg)
+                "r"(ext ? h * 32 : nc), "r"(ext ? u * BM : m0), "r"(stg)
                 : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
@@ -919,7 +925,7 @@ __global__ void __launch_bounds__(kThreadsPers, 1) tma_gemm_pers_kernel(const __
       }
       if (threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
-    if (S > 1) {
+    if (S > 1 && !P.tstore) {
       // split units: the raw accumulator goes to workspace slot u (row-major
       // 128 x 128); the tile's last unit to arrive adds bias, C and the S
       // partials in split order (the cluster kernels' arithmetic and order)
@@ -1115,6 +1121,40 @@ __global__ void __launch_bounds__(kThreadsPers, 1) tma_gemm_pers_kernel(const __
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// Sum of the persistent kernel's split partials (workspace rows u*BM.. of
+// unit u = tile*S + z, row-major BM x BN) into C, in split order, with the
+// cluster kernels' arithmetic: bias + C + row bias + p_0 + ... + p_{S-1}
+// (vector path) / p_0 + ... + bias + C (scalar path)
+__global__ void split_reduce_kernel(const __grid_constant__ TmaGemmArgs P) {
+  pdl_prologue();
+  const int S = P.splits, tiles_m = (P.M + BM - 1) / BM;
+  const int nq = (P.N + 3) >> 2;
+  const int64_t total = (int64_t)P.M * nq;
+  const bool has_bias = P.bias.rows != nullptr || P.bias.base != nullptr;
+  const bool bias_bcast = has_bias && !P.bias.rows && P.bias.ld == 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(t / nq), n = 4 * (int)(t - (int64_t)m * nq);
+    const int tile = m / BM + (n / BN) * tiles_m;
+    const float* p0 = P.ws + ((size_t)tile * S * BM + (m % BM)) * BN + (n % BN);
+    float* crow = const_cast<float*>(orow(P.C, m));
+    if (P.c_vec && n + 3 < P.N) {
+      float4 v = bias_bcast ? *reinterpret_cast<const float4*>(P.bias.base + n) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (P.accumulate) v = f4add(v, *reinterpret_cast<const float4*>(crow + n));
+      if (has_bias && !bias_bcast) v = f4add(v, *reinterpret_cast<const float4*>(orow(P.bias, m) + n));
+      for (int q = 0; q < S; ++q) v = f4add(v, __ldcg(reinterpret_cast<const float4*>(p0 + (size_t)q * BM * BN)));
+      *reinterpret_cast<float4*>(crow + n) = v;
+    } else {
+      for (int e = 0; e < 4 && n + e < P.N; ++e) {
+        float v = 0.f;
+        for (int q = 0; q < S; ++q) v += __ldcg(p0 + (size_t)q * BM * BN + e);
+        if (has_bias) v += orow(P.bias, m)[n + e];
+        if (P.accumulate) v += crow[n + e];
+        crow[n + e] = v;
+      }
+    }
+  }
 }
 
 // lo[r][c] = x - tf32(x) for up to two rows x cols blocks (A and B of one
@@ -1465,11 +1505,10 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
     const int sm = sm_count();
     double best_c = 1e30;
     int best_s = 0;
-    // DG_TMA_PERS_SPLIT=1: split problems as persistent work units too (opt-in:
-    // the PTB dW 100 -> 210 us, dX 80 -> 235 us; profiles/r02i_tma_pers_split.txt)
+    // DG_TMA_PERS_SPLIT=0: persistent kernel for unsplit problems only
     static const bool split_on = [] {
       const char* e = getenv("DG_TMA_PERS_SPLIT");
-      return e && e[0] == '1';
+      return !(e && e[0] == '0');
     }();
     for (int s2 = 1; s2 <= (split_on ? kPersMaxSplit : 1); ++s2) {
       const int per = (kt + s2 - 1) / s2;
@@ -1495,6 +1534,11 @@ bool tma_gemm_make(const TmaOperands& o, TmaGemmPlan* out) {
     }
   }
   a.tstore = 0;
+  // split units: partial tiles through TMA stores into the workspace (a
+  // tensor map over units*BM rows of BN floats), reduced by a second launch
+  if (p.pers && S > 1 && tma_tstore_enabled() &&
+      make_map(&p.mAl, o.ws, BN, (int64_t)p.ctas * BM, BN, false))
+    a.tstore = 1;
   const bool bias_ok = !(o.bias.base || o.bias.rows) || (o.bias.base && !o.bias.rows && o.bias.ld == 0 &&
                                                           reinterpret_cast<uintptr_t>(o.bias.base) % 16 == 0);
   if (p.pers && S == 1 && tma_tstore_enabled() && !o.accumulate && !o.C.rows && o.C.base && bias_ok &&
@@ -1581,7 +1625,13 @@ int launch_tma_gemm(const TmaGemmPlan& p, bool split_a, bool split_b, cudaStream
   }
   const TmaGemmPlan* one = &p;
   const int r = tma_launch(&one, 1, s);
-  return r < 0 ? -1 : n + r;
+  if (r < 0) return -1;
+  if (p.pers && p.args.splits > 1 && p.args.tstore) {
+    const int64_t total = (int64_t)p.args.M * ((p.args.N + 3) / 4);
+    launch_k(split_reduce_kernel, (int)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, s, p.args);
+    ++n;
+  }
+  return n + r;
 }
 
 bool tma_gemm_groupable(const TmaGemmPlan& a, const TmaGemmPlan& b) {

@@ -16,9 +16,11 @@ with each fast path switched off, so the fallbacks stay parity-green too.
                     GEMM + cell kernel instead of one fused launch
   DG_TREE_PERSIST=0 one fused launch per tree level instead of one
                     cooperative launch for every level
-  DG_TMA_GSPLIT=0, DG_TMA_PERS=0, DG_TMA_TSTORE=0
-                    split-K only through clusters / no persistent logits GEMM /
-                    its epilogue with thread stores (run on the MB64 test)
+  DG_TMA_GSPLIT=0, DG_TMA_PERS=0, DG_TMA_TSTORE=0, DG_TMA_PERS_SPLIT=0
+                    split-K only through clusters / no persistent kernel /
+                    its epilogue with thread stores and in-kernel split
+                    reduction / persistent kernel for unsplit problems only
+                    (run on the MB64 test)
 
 (the fused affine + cell path is exercised by the Tree-LSTM test added to
 the list below)
@@ -68,7 +70,7 @@ GEMM_VARIANTS = {
     "tma_cluster_split_only": {"DG_TMA_GSPLIT": "0"},
     "tma_pers_off": {"DG_TMA_PERS": "0"},
     "tma_pers_thread_stores": {"DG_TMA_TSTORE": "0"},
-    "tma_pers_split_units": {"DG_TMA_PERS_SPLIT": "1"},
+    "tma_pers_unsplit_only": {"DG_TMA_PERS_SPLIT": "0"},
 }
 
 
