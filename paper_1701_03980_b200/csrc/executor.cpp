@@ -1300,6 +1300,8 @@ struct OpMeta {
 struct Plan {
   Blob blob;
   std::vector<std::function<int(char*)>> ops;  // arg: device blob base
+  int rnn_bwd_ctas = 0;   // CTAs of the last backward cluster recurrence planned
+  size_t rnn_bwd_op = 0;  // ops.size() right after it (early dW only directly behind it)
   std::vector<LazyGrad> lazy;
   size_t lazy_floats = 0;  // used part of the lazy-partials region
   std::vector<OpMeta> meta;
@@ -2435,6 +2437,8 @@ static void plan_rnn_group(dg_graph* g, const Schedule& S, const Group& gr, Plan
       return launch_rnn(a, bwd, smem, st);
     });
     plan.tag(bwd ? C_RNN_BWD : C_RNN_FWD, flops, bytes);
+    plan.rnn_bwd_ctas = bwd && use_cl && !eager.n ? a.ctas : 0;
+    plan.rnn_bwd_op = plan.ops.size();
     if (eager.n) {
       plan.ops.push_back([eager](char*) { return launch_rnn_part_sum(eager, g_launch_stream); });
       plan.tag(C_ELEMWISE, 0.0, 0.0);
@@ -3531,6 +3535,62 @@ static bool plan_affine_dx_small(dg_graph* g, const Schedule& S, const Group& ga
   return true;
 }
 
+// The weight gradient of a large parameter whose every use is already
+// registered (the output layer's W once its affine group is planned), run
+// while the backward recurrence just planned occupies its clusters: the
+// persistent TMA GEMM is launched right behind the recurrence with
+// programmatic dependent launch, on at most the SMs the recurrence leaves
+// free, and without waiting for it (it neither reads nor writes anything the
+// recurrence touches; the recurrence started only after every earlier kernel
+// completed).  The next launch goes without PDL, so it waits for both.
+static int sm_count_host() {
+  static const int n = [] {
+    int d = 0, v = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess)
+      v = 148;
+    return v > 0 ? v : 148;
+  }();
+  return n;
+}
+
+static bool early_dw_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("DG_EARLY_DW");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static bool plan_early_dw(dg_graph* g, Plan& plan, const AffineUse& use, Param* p, int grid_cap) {
+  Blob& B = plan.blob;
+  GemmProblem pr{};
+  pr.M = (int)use.n_in;
+  pr.N = (int)use.m;
+  pr.n_seg = 1;
+  pr.accumulate = 1;
+  pr.seg[0].K = (int64_t)use.x_rows.size();
+  pr.seg[0].A.rows = dev_at<const float*>(g, B.push(use.x_rows));
+  pr.seg[0].A.rows_aligned = all_aligned16(use.x_rows);
+  pr.seg[0].B.rows = dev_at<const float*>(g, B.push(use.g_rows));
+  pr.seg[0].B.rows_aligned = all_aligned16(use.g_rows);
+  pr.C.base = p->grad;
+  pr.C.ld = use.m;
+  float* work = reinterpret_cast<float*>(scratch_base(g));
+  const int64_t cap = (int64_t)(scratch_bytes(g) / 4);
+  TmaGemmPlan tp;
+  if (!tma_try(g, plan, pr, true, false, work, cap, &tp) || !tp.pers) return false;
+  tp.args.nowait = 1;
+  tp.grid_cap = grid_cap;
+  plan.ops.push_back([tp](char*) { return launch_tma_gemm(tp, true, true, g_launch_stream); });
+  plan.tag(C_GEMM_DW, tp.flops, 4.0 * ((double)pr.seg[0].K * (pr.M + pr.N) + 2.0 * pr.M * pr.N));
+  plan.ops.push_back([](char*) {
+    pdl_skip_next();
+    return 0;
+  });
+  plan.tag(C_OTHER, 0.0, 0.0);
+  return true;
+}
+
 static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr, Plan& plan, float* dummy,
                                 std::unordered_map<int64_t, AffineUse>& wuse,
                                 std::unordered_map<int64_t, std::vector<uintptr_t>>& buse, GemmBatch& gb) {
@@ -4173,10 +4233,60 @@ int dg_backward(dg_graph* g, int32_t loss) {
         return e && e[0] == '2';
       }();
       std::map<int, double> kt;
+      // rows per weight key over all scheduled affine nodes, and over those in
+      // plain affine groups: a key whose uses are all plain affine groups has
+      // every use registered once its registered rows reach that count
+      std::unordered_map<int64_t, int64_t> rows_all, rows_plain;
+      bool early_done = !early_dw_on();
+      if (!early_done) {
+        auto count = [&](int id, std::unordered_map<int64_t, int64_t>& m) {
+          const Node& x = g->nodes[id];
+          for (int t = 0; 2 + 2 * t < x.n_in; ++t) {
+            const Node& wn = g->nodes[g->inputs[x.in_off + 1 + 2 * t]];
+            if (wn.kind == DG_OP_PARAMETER) m[g->aux_i[wn.ai_off]] += x.batch;
+          }
+        };
+        for (int id = 0; id < (int)g->nodes.size() && id < (int)S.unit_of.size(); ++id)
+          if (g->nodes[id].kind == DG_OP_AFFINE && S.unit_of[id] >= 0) count(id, rows_all);
+        for (const Group& gq : S.groups)
+          if (gq.kind == DG_OP_AFFINE)
+            for (int u : gq.units) count(S.units[u].last(), rows_plain);
+      }
       for (int q = (int)S.groups.size() - 1; q >= 0; --q) {
         const auto t0 = std::chrono::steady_clock::now();
         if (!plan_affine_dx_small(g, S, S.groups[q], plan, gb, wuse, buse))
           plan_backward_group(g, S, S.groups[q], plan, dummy, wuse, buse, gb);
+        if (!early_done && plan.rnn_bwd_ctas > 0 && plan.rnn_bwd_op > 0 && plan.rnn_bwd_op <= plan.ops.size()) {
+          early_done = true;  // behind the first backward recurrence only
+          const int free_sms = sm_count_host() - plan.rnn_bwd_ctas;
+          std::vector<int64_t> keys;
+          for (auto& kv : wuse) keys.push_back(kv.first);
+          std::sort(keys.begin(), keys.end());
+          static const bool elog = std::getenv("DG_EARLY_DW_LOG") != nullptr;
+          for (int64_t h : keys) {
+            const AffineUse& use = wuse[h];
+            const auto pa = rows_all.find(h), pp = rows_plain.find(h);
+            if (elog)
+              std::fprintf(stderr, "[early-dw] key %lld free %d all %lld plain %lld reg %zu size %lld\n", (long long)h,
+                           free_sms, pa == rows_all.end() ? -1LL : (long long)pa->second,
+                           pp == rows_plain.end() ? -1LL : (long long)pp->second, use.x_rows.size(),
+                           (long long)(use.n_in * use.m));
+            if (free_sms < 32 || pa == rows_all.end() || pp == rows_plain.end() || pa->second != pp->second ||
+                (int64_t)use.x_rows.size() != pp->second || use.n_in * use.m < ((int64_t)1 << 21))
+              continue;
+            const size_t at_op = plan.rnn_bwd_op, n_before = plan.ops.size();
+            if (plan_early_dw(g, plan, use, param_at(h), free_sms)) {
+              // move the two ops directly behind the recurrence (ops planned
+              // after it in this group follow them; the first runs without PDL)
+              plan.meta.resize(plan.ops.size());
+              std::rotate(plan.ops.begin() + at_op, plan.ops.begin() + n_before, plan.ops.end());
+              std::rotate(plan.meta.begin() + at_op, plan.meta.begin() + n_before, plan.meta.end());
+              if (elog) std::fprintf(stderr, "[early-dw] planned key %lld on %d SMs at op %zu of %zu\n", (long long)h, free_sms, at_op, n_before);
+              wuse.erase(h);
+              break;  // one overlapped GEMM
+            }
+          }
+        }
         if (per_kind)
           kt[S.groups[q].kind] += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
       }

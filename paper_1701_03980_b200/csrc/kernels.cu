@@ -13,11 +13,19 @@
 
 namespace dg {
 
+namespace {
+thread_local bool g_pdl_skip = false;
+}
+void pdl_skip_next() { g_pdl_skip = true; }
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("DG_PDL");
     return !(e && e[0] == '0');
   }();
+  if (g_pdl_skip) {
+    g_pdl_skip = false;
+    return false;
+  }
   return on;
 }
 

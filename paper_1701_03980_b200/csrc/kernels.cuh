@@ -26,6 +26,9 @@ __device__ __forceinline__ void pdl_prologue() {
 #endif
 }
 bool pdl_enabled();
+// the next launch that asks pdl_enabled() goes without programmatic
+// serialization (waits for every earlier grid of the stream)
+void pdl_skip_next();
 
 // 3xTF32 operand splits (x ~ hi + lo, products hi*hi + hi*lo + lo*hi).
 // Both parts are rounded to nearest (cvt.rna), not truncated: a truncated
@@ -440,6 +443,7 @@ struct TmaGemmArgs {
   int M, N, K;
   int tiles_n, splits, accumulate, c_vec, pad_;
   int gsplit;  // split-K partials reduced through `ws` by the tile's last CTA (no cluster)
+  int nowait;  // persistent kernel launched behind an independent grid: no griddepcontrol.wait
   int tstore;  // persistent kernel: C written by TMA tensor stores (map in TmaProb::mAl)
   Operand C, bias;
   float* ws;   // gsplit: one BM x BN partial per CTA of the launch
@@ -486,6 +490,7 @@ struct TmaGemmPlan {
   float* b_lo;
   int64_t a_ld, a_rows, a_cols, a_colsp, b_ld, b_rows, b_cols, b_colsp;
   int ctas;
+  int grid_cap;  // persistent kernel: at most this many CTAs (0: one per SM)
   int64_t ws_floats;
   int cnt_cap;
   double flops;

@@ -707,7 +707,8 @@ __global__ void __launch_bounds__(kThreadsPers, 1) tma_gemm_pers_kernel(const __
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  pdl_prologue();
+  if (P.nowait) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // inputs complete before the preceding grid began
+  else pdl_prologue();
   const uint32_t tmem = tmem_sh;
   const uint32_t sbase = su32(smem);
   float* part = reinterpret_cast<float*>(smem + NS * SB);  // output staging tile
@@ -1592,7 +1593,7 @@ static int tma_launch(const TmaGemmPlan* const* ps, int n, cudaStream_t s) {
     ctas += ps[i]->ctas;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(p.pers ? std::min(ctas, sm_count()) : ctas);
+  cfg.gridDim = dim3(p.pers ? std::min(ctas, p.grid_cap > 0 ? std::min(p.grid_cap, sm_count()) : sm_count()) : ctas);
   cfg.blockDim = dim3(p.pers ? kThreadsPers : p.conv ? kThreadsConv : kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;

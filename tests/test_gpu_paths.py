@@ -20,7 +20,8 @@ with each fast path switched off, so the fallbacks stay parity-green too.
                     split-K only through clusters / no persistent kernel /
                     its epilogue with thread stores and in-kernel split
                     reduction / persistent kernel for unsplit problems only
-                    (run on the MB64 test)
+  DG_EARLY_DW=0     the output layer's dW after the backward recurrences instead
+                    of overlapped with the first one (run on the MB64 test)
 
 (the fused affine + cell path is exercised by the Tree-LSTM test added to
 the list below)
@@ -71,6 +72,7 @@ GEMM_VARIANTS = {
     "tma_pers_off": {"DG_TMA_PERS": "0"},
     "tma_pers_thread_stores": {"DG_TMA_TSTORE": "0"},
     "tma_pers_unsplit_only": {"DG_TMA_PERS_SPLIT": "0"},
+    "dw_after_recurrences": {"DG_EARLY_DW": "0"},
 }
 
 
