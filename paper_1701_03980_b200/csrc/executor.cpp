@@ -1467,6 +1467,7 @@ struct GemmBatch {
   std::vector<std::function<int()>> post;
   double bytes = 0;
   std::vector<int> targets;  // nodes written with += (dX): must be disjoint per launch
+  bool nowait = false;       // TMA launches skip griddepcontrol.wait (overlap window)
 };
 
 template <class T>
@@ -1564,10 +1565,12 @@ static void flush_gemm(dg_graph* g, Plan& plan, GemmBatch& gb) {
   std::vector<std::pair<TmaGemmPlan, double>> tmas;
   for (const GemmProblem& p : gb.probs) {
     TmaGemmPlan tp;
-    if (tma_try(g, plan, p, gb.a_kmajor, gb.b_nmajor, work, cap, &tp))
+    if (tma_try(g, plan, p, gb.a_kmajor, gb.b_nmajor, work, cap, &tp)) {
+      if (gb.nowait) tp.args.nowait = 1;
       tmas.push_back({tp, 4.0 * ((double)p.M * p.seg[0].K + (double)p.seg[0].K * p.N + 2.0 * p.M * p.N)});
-    else
+    } else {
       rest.push_back(p);
+    }
   }
   static const bool group_on = [] {
     const char* e = std::getenv("DG_TMA_GROUP");
@@ -3591,6 +3594,119 @@ static bool plan_early_dw(dg_graph* g, Plan& plan, const AffineUse& use, Param* 
   return true;
 }
 
+// Work for the SMs the second backward recurrence leaves free: column sums
+// of biases whose uses are all plain affine nodes already planned (the
+// output bias) and weight gradients whose every use is registered (the upper
+// LSTM layer's), launched behind the recurrence without waiting for it; the
+// next launch goes without PDL.  Scratch: the column-sum partials first, the
+// GEMMs' split-K workspace after them.
+static void plan_window_work(dg_graph* g, Plan& plan, std::unordered_map<int64_t, AffineUse>& wuse,
+                             std::unordered_map<int64_t, std::vector<uintptr_t>>& buse,
+                             const std::unordered_map<int64_t, int64_t>& rows_all,
+                             const std::unordered_map<int64_t, int64_t>& brows_all,
+                             const std::unordered_map<int64_t, int64_t>& brows_plain) {
+  Blob& B = plan.blob;
+  const size_t at_op = plan.rnn_bwd_op, n_before = plan.ops.size();
+  static const bool elog = std::getenv("DG_EARLY_DW_LOG") != nullptr;
+  // DG_WINDOW: bit 0 column sums (default), bit 1 weight gradients too (the
+  // lite TMA kernels co-reside with the recurrence's CTAs and slow it:
+  // 0.950 -> 1.013 ms per PTB step)
+  static const int mode = [] {
+    const char* e = std::getenv("DG_WINDOW");
+    return e ? std::atoi(e) : 1;
+  }();
+  // bias column sums (wide rows only: the pass that can skip the wait)
+  std::vector<int64_t> bkeys;
+  for (auto& kv : buse) bkeys.push_back(kv.first);
+  std::sort(bkeys.begin(), bkeys.end());
+  struct Job {
+    float* dst;
+    size_t orow;
+    int nr, width;
+  };
+  std::vector<Job> jobs;
+  int64_t cw = 0;
+  double cbytes = 0;
+  for (int64_t h : bkeys) {
+    const auto& rows = buse[h];
+    const auto pa = brows_all.find(h), pp = brows_plain.find(h);
+    Param* p = param_at(h);
+    const int width = (int)p->size();
+    if (!(mode & 1) || pa == brows_all.end() || pp == brows_plain.end() || pa->second != pp->second ||
+        (int64_t)rows.size() != pp->second || width % 4 || width < 1024 || !all_aligned16(rows) ||
+        (int)jobs.size() == kColsumGroup)
+      continue;
+    jobs.push_back({p->grad, B.push(rows), (int)rows.size(), width});
+    cw += (((int64_t)(rows.size() + 31) / 32) * width + 63) & ~int64_t(63);
+    cbytes += 4.0 * rows.size() * width + 8.0 * width;
+  }
+  float* work = reinterpret_cast<float*>(scratch_base(g));
+  const int64_t wcap = (int64_t)(scratch_bytes(g) / 4);
+  if (!jobs.empty() && cw < wcap / 2) {
+    for (const Job& j : jobs)
+      for (int64_t h : bkeys)
+        if (param_at(h)->grad == j.dst) buse.erase(h);
+    plan.ops.push_back([jobs, work, cw](char* d) {
+      ColsumGroup G{};
+      G.n = (int)jobs.size();
+      G.nowait = 1;
+      for (int q = 0; q < G.n; ++q)
+        G.j[q] = ColsumJob{jobs[q].dst, at<const float* const>(d, jobs[q].orow), jobs[q].nr, jobs[q].width, 0, 0, 0,
+                           nullptr, 1};
+      return launch_colsum_group(G, work, cw, g_launch_stream);
+    });
+    plan.tag(C_COLSUM, 0.0, cbytes);
+    if (elog) std::fprintf(stderr, "[early-dw] window: %zu column sums\n", jobs.size());
+  } else {
+    cw = 0;
+  }
+  // weight gradients complete by now
+  std::vector<int64_t> wkeys;
+  for (auto& kv : wuse) wkeys.push_back(kv.first);
+  std::sort(wkeys.begin(), wkeys.end());
+  GemmBatch gb;
+  gemm_batch_for(g, plan, gb, -1, C_GEMM_DW, true, false);
+  gb.nowait = true;
+  gb.temp_floats = cw;
+  std::vector<int64_t> taken;
+  for (int64_t h : wkeys) {
+    const AffineUse& use = wuse[h];
+    const auto pa = rows_all.find(h);
+    if (!(mode & 2) || pa == rows_all.end() || (int64_t)use.x_rows.size() != pa->second ||
+        use.n_in * use.m < ((int64_t)1 << 18))
+      continue;
+    GemmProblem pr{};
+    pr.M = (int)use.n_in;
+    pr.N = (int)use.m;
+    pr.n_seg = 1;
+    pr.accumulate = 1;
+    pr.seg[0].K = (int64_t)use.x_rows.size();
+    pr.seg[0].A.rows = dev_at<const float*>(g, B.push(use.x_rows));
+    pr.seg[0].A.rows_aligned = all_aligned16(use.x_rows);
+    pr.seg[0].B.rows = dev_at<const float*>(g, B.push(use.g_rows));
+    pr.seg[0].B.rows_aligned = all_aligned16(use.g_rows);
+    pr.C.base = param_at(h)->grad;
+    pr.C.ld = use.m;
+    gb.probs.push_back(pr);
+    gb.bytes += 4.0 * ((double)pr.seg[0].K * (pr.M + pr.N) + 2.0 * pr.M * pr.N);
+    taken.push_back(h);
+  }
+  if (!gb.probs.empty()) {
+    flush_gemm(g, plan, gb);
+    for (int64_t h : taken) wuse.erase(h);
+    if (elog) std::fprintf(stderr, "[early-dw] window: %zu weight gradients\n", taken.size());
+  }
+  if (plan.ops.size() == n_before) return;
+  plan.ops.push_back([](char*) {
+    pdl_skip_next();
+    return 0;
+  });
+  plan.tag(C_OTHER, 0.0, 0.0);
+  plan.meta.resize(plan.ops.size());
+  std::rotate(plan.ops.begin() + at_op, plan.ops.begin() + n_before, plan.ops.end());
+  std::rotate(plan.meta.begin() + at_op, plan.meta.begin() + n_before, plan.meta.end());
+}
+
 static void plan_backward_group(dg_graph* g, const Schedule& S, const Group& gr, Plan& plan, float* dummy,
                                 std::unordered_map<int64_t, AffineUse>& wuse,
                                 std::unordered_map<int64_t, std::vector<uintptr_t>>& buse, GemmBatch& gb) {
@@ -4236,27 +4352,38 @@ int dg_backward(dg_graph* g, int32_t loss) {
       // rows per weight key over all scheduled affine nodes, and over those in
       // plain affine groups: a key whose uses are all plain affine groups has
       // every use registered once its registered rows reach that count
-      std::unordered_map<int64_t, int64_t> rows_all, rows_plain;
-      bool early_done = !early_dw_on();
+      std::unordered_map<int64_t, int64_t> rows_all, rows_plain, brows_all, brows_plain;
+      bool early_done = !early_dw_on(), early2_done = !early_dw_on();
+      size_t early_op = 0;
       if (!early_done) {
-        auto count = [&](int id, std::unordered_map<int64_t, int64_t>& m) {
+        auto count = [&](int id, std::unordered_map<int64_t, int64_t>& m, std::unordered_map<int64_t, int64_t>& mb) {
           const Node& x = g->nodes[id];
           for (int t = 0; 2 + 2 * t < x.n_in; ++t) {
             const Node& wn = g->nodes[g->inputs[x.in_off + 1 + 2 * t]];
             if (wn.kind == DG_OP_PARAMETER) m[g->aux_i[wn.ai_off]] += x.batch;
           }
+          const Node& bn = g->nodes[g->inputs[x.in_off]];
+          if (bn.kind == DG_OP_PARAMETER) mb[g->aux_i[bn.ai_off]] += x.batch;
         };
         for (int id = 0; id < (int)g->nodes.size() && id < (int)S.unit_of.size(); ++id)
-          if (g->nodes[id].kind == DG_OP_AFFINE && S.unit_of[id] >= 0) count(id, rows_all);
+          if (g->nodes[id].kind == DG_OP_AFFINE && S.unit_of[id] >= 0) count(id, rows_all, brows_all);
         for (const Group& gq : S.groups)
           if (gq.kind == DG_OP_AFFINE)
-            for (int u : gq.units) count(S.units[u].last(), rows_plain);
+            for (int u : gq.units) count(S.units[u].last(), rows_plain, brows_plain);
       }
       for (int q = (int)S.groups.size() - 1; q >= 0; --q) {
         const auto t0 = std::chrono::steady_clock::now();
         if (!plan_affine_dx_small(g, S, S.groups[q], plan, gb, wuse, buse))
           plan_backward_group(g, S, S.groups[q], plan, dummy, wuse, buse, gb);
+        if (early_done && !early2_done && plan.rnn_bwd_ctas > 0 && plan.rnn_bwd_op > early_op &&
+            plan.rnn_bwd_op <= plan.ops.size()) {
+          // behind the second backward recurrence: column sums of biases and
+          // weight gradients whose uses are all registered by now
+          early2_done = true;
+          plan_window_work(g, plan, wuse, buse, rows_all, brows_all, brows_plain);
+        }
         if (!early_done && plan.rnn_bwd_ctas > 0 && plan.rnn_bwd_op > 0 && plan.rnn_bwd_op <= plan.ops.size()) {
+          early_op = plan.rnn_bwd_op;
           early_done = true;  // behind the first backward recurrence only
           const int free_sms = sm_count_host() - plan.rnn_bwd_ctas;
           std::vector<int64_t> keys;

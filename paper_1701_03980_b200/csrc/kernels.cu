@@ -1262,7 +1262,8 @@ __global__ void colsum_partial_group_kernel(const __grid_constant__ ColsumGroup 
 // work[chunk][c], rows summed in order.
 constexpr int kColsumWideRows = 32;
 __global__ void __launch_bounds__(256) colsum_wide_partial_kernel(const __grid_constant__ ColsumGroup G) {
-  pdl_prologue();
+  if (G.nowait) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  else pdl_prologue();
   int q = 0;
   while (q + 1 < G.n && (int)blockIdx.x >= G.j[q + 1].pb0) ++q;
   const ColsumJob& J = G.j[q];
@@ -1679,6 +1680,7 @@ int launch_colsum_group(ColsumGroup G, float* work, int64_t work_floats, cudaStr
   int launched = 0;
   {
     ColsumGroup W{}, N{};
+    W.nowait = G.nowait;
     int64_t off = 0;
     int pb = 0, fb = 0;
     for (int q = 0; q < G.n; ++q) {

@@ -384,6 +384,7 @@ constexpr int kColsumGroup = 8;
 struct ColsumGroup {
   ColsumJob j[kColsumGroup];
   int n;
+  int nowait;  // wide jobs only: the partial pass skips griddepcontrol.wait (launched behind an independent grid)
 };
 int launch_colsum_group(ColsumGroup G, float* work, int64_t work_floats, cudaStream_t s);
 // row reduce-scatter: for t in targets: dst[t] += sum_{k in seg} src[k]  (src dense, width)

@@ -272,7 +272,10 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, kLite ? 2 : 1
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  pdl_prologue();  // operands / C of the preceding grid are read only from here on
+  // operands / C of the preceding grid are read only from here on (nowait:
+  // launched behind an independent grid whose own inputs were complete)
+  if (P.nowait) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  else pdl_prologue();
   const uint32_t tmem = tmem_sh;
   const uint32_t sbase = su32(smem);
 
