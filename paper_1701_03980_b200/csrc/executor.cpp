@@ -1566,7 +1566,10 @@ static void flush_gemm(dg_graph* g, Plan& plan, GemmBatch& gb) {
   for (const GemmProblem& p : gb.probs) {
     TmaGemmPlan tp;
     if (tma_try(g, plan, p, gb.a_kmajor, gb.b_nmajor, work, cap, &tp)) {
-      if (gb.nowait) tp.args.nowait = 1;
+      // only the first launch of an overlap window skips the wait: the later
+      // ones wait for their predecessor (which never waited for the window's
+      // recurrence) and so never race on the shared workspace
+      if (gb.nowait && tmas.empty()) tp.args.nowait = 1;
       tmas.push_back({tp, 4.0 * ((double)p.M * p.seg[0].K + (double)p.seg[0].K * p.N + 2.0 * p.M * p.N)});
     } else {
       rest.push_back(p);
@@ -3666,7 +3669,7 @@ static void plan_window_work(dg_graph* g, Plan& plan, std::unordered_map<int64_t
   std::sort(wkeys.begin(), wkeys.end());
   GemmBatch gb;
   gemm_batch_for(g, plan, gb, -1, C_GEMM_DW, true, false);
-  gb.nowait = true;
+  gb.nowait = cw == 0;  // behind the column sums the GEMMs simply wait for them
   gb.temp_floats = cw;
   std::vector<int64_t> taken;
   for (int64_t h : wkeys) {
