@@ -417,6 +417,11 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, kLite ? 2 : 1
       __syncwarp();
       if (lane == 0) mbar_arrive(&conv[s]);
     }
+    // the epilogue reuses the operand stages for its staging tile: order our
+    // last shared-memory reads before its writes explicitly (the mbarrier /
+    // tcgen05.commit chain already does; named barrier 2 makes it visible to
+    // compute-sanitizer racecheck too)
+    asm volatile("bar.arrive 2, 256;" ::: "memory");
   } else if (kConv && warp >= 6) {
     // converter warps 6..9: residual lo = x - tf32(x) of the landed hi tiles
     // (same swizzled layout, elementwise), then publish to the async proxy
@@ -446,12 +451,14 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, kLite ? 2 : 1
       __syncwarp();
       if (lane == 0) mbar_arrive(&conv[s]);
     }
+    asm volatile("bar.arrive 2, 256;" ::: "memory");  // see the A-in-TMEM converters
   } else if (kLite) {
     // epilogue warps 2..5: one drain of the whole-K accumulator, 32 columns at
     // a time, straight into the staging tile (no register-resident row)
     const int quad = warp & 3;
     mbar_wait(&acc_full[0], 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("bar.sync 2, 256;" ::: "memory");  // converters done with the stages (kLite implies kConv)
     float* part = reinterpret_cast<float*>(smem);
     const int lrow = quad * 32 + lane;
 #pragma unroll 1
@@ -511,6 +518,7 @@ __global__ void __launch_bounds__(kConv ? kThreadsConv : kThreads, kLite ? 2 : 1
     // rotated by 4*row floats against bank conflicts; all warps then write
     // whole rows (coalesced 512 B per row) below
     if (prof_e) g_tprof[5][1][0] = clock64();
+    if (kConv) asm volatile("bar.sync 2, 256;" ::: "memory");  // converters done with the stages
     if (!(P.pad_ & 8)) {
       float* part = reinterpret_cast<float*>(smem);  // 128 x 128 fp32 = 64 KiB
       const int lrow = quad * 32 + lane;

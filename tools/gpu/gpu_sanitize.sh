@@ -1,7 +1,11 @@
 #!/bin/bash
+# compute-sanitizer over every kernel family (tools/sanitize.py); summaries to gpurun_out/san_*.txt
 mkdir -p gpurun_out
-timeout 300 python tools/sanitize.py > gpurun_out/san_plain.txt 2>&1
-for t in memcheck racecheck synccheck initcheck; do
-  timeout 1200 compute-sanitizer --tool $t --print-limit 50 python tools/sanitize.py > gpurun_out/san_$t.txt 2>&1
-  echo "rc=$?" >> gpurun_out/san_$t.txt
+S=/usr/local/cuda/bin/compute-sanitizer
+for tool in memcheck racecheck synccheck; do
+  for w in ptb tiny tree tagger gru ptb_big; do
+    timeout 900 $S --tool $tool --print-limit 20 python tools/sanitize.py $w > gpurun_out/san_${tool}_${w}.txt 2>&1
+    echo "rc=$?" >> gpurun_out/san_${tool}_${w}.txt
+  done
 done
+grep -H -E "ERROR SUMMARY|RACECHECK SUMMARY|rc=|Error|error" gpurun_out/san_*.txt | grep -v "^.*: *$" > gpurun_out/san_summary.txt

@@ -87,4 +87,9 @@ if want("tagger"):
 gru = W.minibatches(W.ptb_corpus(7, 8, vocab=300, mean_len=6.0), 4)
 if want("gru"):
     print("gru", run(lambda m: W.RNNLM(dy, m, 300, 16, 32, 1, "gru"), gru, rule="sgd"))
+# headline-shaped output layer (V 10k, H 256, MB 64): the persistent logits
+# GEMM with TMA stores, the split dW units and both backward overlap windows
+big = W.minibatches(W.ptb_corpus(8, 64, vocab=10000, mean_len=16.0), 64)
+if want("ptb_big"):
+    print("ptb_big", run(lambda m: W.RNNLM(dy, m, 10000, 128, 256, 2), big, steps=1))
 print("sanitize workloads done")
