@@ -482,7 +482,7 @@ struct TmaGemmPlan {
   bool a_mn, b_mn;
   bool conv;  // residuals formed in shared memory by converter warps (no lo copies)
   bool a_tmem;  // conv with A's hi/lo split stored in TMEM (MMAs read only B from shared memory)
-  bool lite;    // a_tmem, K per split <= 1280: 2 stages, one accumulator, two CTAs per SM
+  bool lite;    // a_tmem, K per split <= 1024 (768 when split): 2 stages, one accumulator, two CTAs per SM
   bool pers;    // lite-shaped single-split problem with many tiles: persistent CTAs, double-buffered
                 // TMEM accumulators, each tile's epilogue overlapping the next tile's mainloop
   const float* a_src;

@@ -26,7 +26,14 @@
 //           at chunk ends, publishes the accumulator;
 //   warps 2-5  epilogue: tcgen05.ld drains (each warp its 32-lane TMEM
 //           quadrant), bias / accumulate, stores; split-K tiles reduce their
-//           partials through distributed shared memory of the cluster.
+//           partials through distributed shared memory of the cluster, or
+//           (when the clusters could not all be co-resident) through a
+//           workspace summed in split order by the tile's last CTA.
+// Default variants: converter warps (320 threads) form the residuals in
+// shared memory / A's split in TMEM; *lite* (K per split <= 1024) runs two
+// CTAs per SM with one accumulator.  tma_gemm_pers_kernel below is the
+// persistent form (one CTA per SM over tiles or K-split units, double-
+// buffered TMEM accumulators, TMA tensor stores of C or of split partials).
 #include <cooperative_groups.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
